@@ -1,0 +1,22 @@
+# Builds the CUDA C-ABI library in-tree for sm_100a (B200).
+NVCC ?= nvcc
+ARCH := -gencode arch=compute_100a,code=sm_100a
+FLAGS := -O3 -std=c++17 -lineinfo $(ARCH) -Xcompiler -fPIC,-ffp-contract=off -Iinclude \
+         -Xptxas -v --expt-relaxed-constexpr
+LIB := paper_1409_7474_b200/_lib/liblse_b200.so
+SRC := paper_1409_7474_b200/csrc/lse_api.cu
+HDR := $(wildcard paper_1409_7474_b200/csrc/*.cuh) include/lse_b200.h
+
+all: $(LIB)
+
+$(LIB): $(SRC) $(HDR)
+	@mkdir -p $(dir $@)
+	$(NVCC) $(FLAGS) -shared -o $@ $(SRC) 2> paper_1409_7474_b200/_lib/ptxas.log || (cat paper_1409_7474_b200/_lib/ptxas.log; false)
+
+oracle:
+	$(MAKE) -C oracle
+
+clean:
+	rm -f $(LIB)
+
+.PHONY: all clean oracle

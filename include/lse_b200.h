@@ -1,0 +1,175 @@
+/*
+ * lse_b200.h -- C ABI of the B200-native fast level-set-evolution (LSE) path.
+ *
+ * The reference (`lsekit` 0.1.0, pure Python) has no FFI: its drop-in
+ * boundary is the Python module API (lsekit/__init__.py:3-32).  The entry
+ * points below are the seams a maintainer would bind from that API; each
+ * names the reference function it replaces.  Plain pointers and sizes only:
+ * images/fields are row-major (H, W) host arrays unless stated otherwise.
+ * All calls are synchronous with respect to the caller (they return after
+ * the device work finished) and thread-safe per handle.
+ *
+ * Errors: every int-returning call returns LSE_OK (0) or an LSE_ERR_* code;
+ * lse_last_error() gives the message of the calling thread's last failure.
+ */
+#ifndef LSE_B200_H
+#define LSE_B200_H
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define LSE_ABI_VERSION 1
+
+#define LSE_OK 0
+#define LSE_ERR_ARG 1            /* ValueError in the reference               */
+#define LSE_ERR_CUDA 2           /* device/runtime failure                    */
+#define LSE_ERR_INSTABILITY 3    /* NumericalInstabilityError (engine.py:29)  */
+#define LSE_ERR_DEGENERATE 4     /* DegeneratePartitionError (grid.py:20)     */
+#define LSE_ERR_NODEVICE 5       /* no CUDA device visible                    */
+#define LSE_ERR_DEGENERATE_SEED 6 /* DegenerateSeedError (grid.py:16)         */
+#define LSE_ERR_UNSUPPORTED 7    /* model outside the hot path (cv / zhang)   */
+
+#define LSE_MODEL_EDGE 0         /* ModelKind.EDGE   (models.py:30)  E_Td, Eq. 14 */
+#define LSE_MODEL_REGION 1       /* ModelKind.REGION (models.py:31)  R_Td, Eq. 17 */
+
+/* EvolutionParams + ModelParams (engine.py:40-81, models.py:44-68).  The
+ * Gaussian 1-D weights are passed in exactly as
+ * gaussian_kernel(sigma, ts).axis_weights (kernels.py:50-64) computes them,
+ * so host and oracle share one weight vector bit-for-bit. */
+typedef struct lse_params {
+  int model;
+  double dt;
+  double sigma2;
+  int ts_reg;
+  int reinit_period;
+  int reg_period;
+  long long max_iters;
+  long long conv_check_every;
+  long long conv_window;
+  double sigma1;
+  int ts_pre;
+  double edge_gain;
+  const double* reg_weights; /* ts_reg values */
+  const double* pre_weights; /* ts_pre values (edge model) */
+} lse_params;
+
+#define LSE_PHI0_FIELD 0     /* float64 (H, W) level-set field                 */
+#define LSE_PHI0_SIGNS 1     /* int8 (H, W) in {-1, +1}; phi = sign * scale     */
+#define LSE_PHI0_POLYGONS 2  /* seed polygons, rasterized on the device         */
+
+/* Initial / injected state: EvolutionState (engine.py:98-103) or a SeedSpec
+ * (grid.py:34-55) rasterized by rasterize_seeds (grid.py:76-93). */
+typedef struct lse_phi0 {
+  int kind;
+  const double* field;            /* LSE_PHI0_FIELD                          */
+  const signed char* signs;       /* LSE_PHI0_SIGNS                          */
+  double scale;                   /* LSE_PHI0_SIGNS magnitude (> 0)          */
+  const double* poly_xy;          /* LSE_PHI0_POLYGONS: concatenated (x, y)  */
+  const long long* poly_counts;   /* vertices per polygon                    */
+  long long n_polys;
+  int inside_sign;                /* +1 / -1                                 */
+  long long iteration;            /* EvolutionState.iteration                */
+  int converged;                  /* EvolutionState.converged                */
+  int degenerate;                 /* EvolutionState.degenerate               */
+} lse_phi0;
+
+typedef struct lse_status {
+  long long iteration;             /* EvolutionState.iteration                */
+  int converged;                   /* EvolutionState.converged                */
+  int degenerate;                  /* EvolutionState.degenerate (sticky)      */
+  long long instability_iteration; /* NumericalInstabilityError.iteration / -1 */
+  long long exact_fallbacks;       /* fp64 re-evaluations of near-tie pixels  */
+  long long fast_iterations;       /* iterations run by the fused bit-state path */
+  long long generic_iterations;    /* iterations run by the fp64 field path   */
+} lse_status;
+
+typedef struct lse_run lse_run;
+
+/* ---- library ----------------------------------------------------------- */
+int lse_abi_version(void);
+const char* lse_last_error(void);
+int lse_device_count(void);
+
+/* ---- the resumable driver: EvolutionRun (engine.py:193-269) -------------- */
+
+/* EvolutionRun.__init__ (engine.py:202-216): uploads the image, builds the
+ * edge indicator on the device for the edge model (engine.py:210-211), and
+ * sets the initial state (init_state, engine.py:123-133).  image is float64
+ * (image_is_f32 = 0) or float32 (image_is_f32 = 1). */
+int lse_run_create(lse_run** out, const lse_params* p, long long height, long long width,
+                   const void* image, int image_is_f32, const lse_phi0* init);
+
+/* Replace the image of an existing run (same shape), keeping its buffers. */
+int lse_run_load_image(lse_run* run, const void* image, int image_is_f32);
+
+/* EvolutionRun.state = ... (engine.py:207, 239): inject a state; the
+ * checkpoint history is kept, as in the reference. */
+int lse_run_set_state(lse_run* run, const lse_phi0* st);
+
+/* EvolutionRun.advance(n_steps) (engine.py:242-254), i.e. up to n_steps
+ * calls of _advance_once (engine.py:148-174) + convergence bookkeeping
+ * (engine.py:222-240).  Returns LSE_ERR_INSTABILITY with
+ * st->instability_iteration set when the update produced NaN/Inf; the state
+ * then stays at the last good iteration (engine.py:150-153). */
+int lse_run_advance(lse_run* run, long long n_steps, lse_status* st);
+
+int lse_run_status(lse_run* run, lse_status* st);
+
+/* EvolutionRun.state.phi: float64 (H, W), bit-identical to the reference's
+ * G * b when the state is binary-regularized. */
+int lse_run_read_phi(lse_run* run, double* out);
+
+/* EvolutionRun.mask() (engine.py:256-259): (phi > 0) if inside_sign > 0
+ * else (phi <= 0).  packed = 0 -> uint8 (H, W) of 0/1; packed = 1 -> row-major
+ * bits, numpy.packbits(mask, axis=None) order (ceil(H*W/8) bytes). */
+int lse_run_read_mask(lse_run* run, unsigned char* out, int inside_sign, int packed);
+
+/* Device-event timing of the fused kernels (bench/roofline support). */
+int lse_run_set_profiling(lse_run* run, int enabled);
+int lse_run_kernel_times(lse_run* run, double* update_ms, long long* update_launches,
+                         double* partition_ms, long long* partition_launches);
+
+void lse_run_destroy(lse_run* run);
+
+/* ---- stateless kernels of the public API --------------------------------- */
+
+/* edge_function (models.py:71-81): g = 1/(1 + (gain fx)^2 + (gain fy)^2). */
+int lse_edge_function(const double* image, long long h, long long w,
+                      const double* weights, int ts, double gain, double* g_out);
+
+/* convolve_same (kernels.py:67-78), separable, zero padding. */
+int lse_convolve_same(const double* f, long long h, long long w,
+                      const double* weights, int ts, double* out);
+
+/* convolve_same with a non-separable Kernel2D (kernels.py:77-78,
+ * ndimage.correlate, zero padding); weights is ts x ts row-major. */
+int lse_correlate2d(const double* f, long long h, long long w,
+                    const double* weights, int ts, double* out);
+
+/* gradient_central / gradient_magnitude (kernels.py:81-95). */
+int lse_gradient(const double* f, long long h, long long w,
+                 double* fx, double* fy, double* magnitude);
+
+/* binarize (grid.py:96-99). */
+int lse_binarize(const double* phi, long long n, double* out);
+
+/* region_means (grid.py:102-118); LSE_ERR_DEGENERATE on an empty side. */
+int lse_region_means(const double* image, const double* phi, long long h, long long w,
+                     double* c_plus, double* c_minus);
+
+/* region_velocity (models.py:101-119) and edge_velocity (models.py:84-90). */
+int lse_region_velocity(const double* image, const double* phi, long long h, long long w,
+                        double* v_out, int* degenerate);
+int lse_edge_velocity(const double* g, const double* phi, long long h, long long w,
+                      double* v_out);
+
+/* rasterize_seeds (grid.py:76-93): +-1 as int8; LSE_ERR_DEGENERATE_SEED when
+ * the union covers no pixel centre or every pixel centre. */
+int lse_rasterize_seeds(const double* poly_xy, const long long* poly_counts, long long n_polys,
+                        int inside_sign, long long h, long long w, signed char* out);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* LSE_B200_H */

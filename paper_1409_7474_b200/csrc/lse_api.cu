@@ -1,0 +1,1117 @@
+// lse_api.cu -- C ABI (include/lse_b200.h): the run handle and its driver.
+//
+// The driver mirrors EvolutionRun (engine.py:193-269).  Per iteration it
+// picks one of two device paths:
+//   * fast  : binary state (reinit_period = reg_period = 1, 3 <= ts_reg <= 9)
+//             -> k_update + k_partition (two launches, no host sync; a
+//             device stop flag turns later launches into no-ops after
+//             convergence);
+//   * generic: exact fp64 field kernels (any other cadence, injected
+//             non-binary states, out-of-range inputs), host-synchronised so
+//             NumericalInstabilityError can name the iteration.
+#include <cuda_runtime.h>
+
+#include <algorithm>
+#include <climits>
+#include <cmath>
+#include <cstdio>
+#include <cstring>
+#include <string>
+#include <vector>
+
+#include "lse_b200.h"
+#include "lse_device.cuh"
+#include "lse_fast.cuh"
+#include "lse_generic.cuh"
+
+using namespace lse;
+
+namespace {
+
+thread_local std::string g_err;
+
+int fail(int code, const std::string& msg) {
+  g_err = msg;
+  return code;
+}
+
+#define CK(x)                                                                            \
+  do {                                                                                   \
+    cudaError_t e_ = (x);                                                                \
+    if (e_ != cudaSuccess)                                                               \
+      return fail(LSE_ERR_CUDA, std::string(#x) + ": " + cudaGetErrorString(e_));        \
+  } while (0)
+
+#define CKL()                                                                            \
+  do {                                                                                   \
+    cudaError_t e_ = cudaGetLastError();                                                 \
+    if (e_ != cudaSuccess)                                                               \
+      return fail(LSE_ERR_CUDA, std::string("launch: ") + cudaGetErrorString(e_));       \
+  } while (0)
+
+#define TRY(x)                 \
+  do {                         \
+    int rc_ = (x);             \
+    if (rc_ != LSE_OK) return rc_; \
+  } while (0)
+
+inline long long round_up(long long a, long long b) { return (a + b - 1) / b * b; }
+
+int num_sms() {
+  static int n = 0;
+  if (!n) {
+    int dev = 0;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&n, cudaDevAttrMultiProcessorCount, dev);
+    if (n <= 0) n = 148;
+  }
+  return n;
+}
+
+template <typename T>
+int dalloc(T** p, size_t n) {
+  *p = nullptr;
+  if (n == 0) n = 1;
+  CK(cudaMalloc((void**)p, n * sizeof(T)));
+  return LSE_OK;
+}
+
+int check_device() {
+  int n = 0;
+  cudaError_t e = cudaGetDeviceCount(&n);
+  if (e != cudaSuccess || n == 0)
+    return fail(LSE_ERR_NODEVICE, std::string("no CUDA device: ") + cudaGetErrorString(e));
+  return LSE_OK;
+}
+
+// exact vertical-pass value of a full-window bit pattern (host, same order as
+// the device and scipy; built with -ffp-contract=off)
+double host_t64(unsigned p, int R, const double* w) {
+  auto b = [&](int k) { return ((p >> k) & 1u) ? 1.0 : -1.0; };
+  volatile double acc = b(R) * w[0];
+  for (int d = R; d >= 1; --d) {
+    volatile double s = b(R - d) + b(R + d);
+    volatile double m = s * w[d];
+    acc = acc + m;
+  }
+  return acc;
+}
+
+const double kEpsPhi = 0x1p-16;
+
+double edge_eps_u(double dt) {
+  return 4.0 * (0x1p-18 + dt * (0x1p-16 + 1.5 * 0x1p-22 + 0x1p-21) + 0x1p-22 * (1.0 + 1.5 * dt));
+}
+
+}  // namespace
+
+struct lse_run {
+  lse_params p{};
+  std::vector<double> wreg, wpre;
+  int H = 0, W = 0, R = 0;
+  RunGeom g{};
+  long long npx = 0;
+  int nthr = kThreads;
+  cudaStream_t st = nullptr;
+  // data plane
+  float* d_data32 = nullptr;
+  double* d_data64 = nullptr;
+  bool fp32_exact = true;
+  double img_absmax = 0.0;
+  // state
+  uint32_t* d_bits[2] = {nullptr, nullptr};
+  uint32_t* d_P = nullptr;
+  uint32_t* d_M = nullptr;
+  uint32_t* d_mask = nullptr;
+  TilePartial* d_part = nullptr;
+  Scalars* d_scal = nullptr;
+  Scalars* h_scal = nullptr;
+  float* d_lut_t = nullptr;
+  float* d_lut_s = nullptr;
+  ExactCtx* d_ctx = nullptr;
+  ExactCtx h_ctx{};
+  double* d_w64 = nullptr;
+  long long* d_keys = nullptr;
+  unsigned long long* d_count = nullptr;
+  double* d_F[2] = {nullptr, nullptr};
+  double* d_U = nullptr;
+  double* d_T = nullptr;
+  // host mirror of the state
+  int mode = SRC_SCALED;
+  int cur = 0, curF = 0;
+  double scale = 1.0;
+  bool field_valid = false;
+  long long iteration = 0;
+  bool converged = false;
+  bool degenerate = false;
+  bool prepared = false;
+  long long fast_iters = 0, generic_iters = 0;
+  // fast-path batch bookkeeping: output buffer of each launched iteration
+  std::vector<std::pair<long long, int>> launched;
+  // profiling
+  bool prof = false;
+  std::vector<cudaEvent_t> evpool;
+  size_t evused = 0;
+  struct EvRec { cudaEvent_t e0, e1, e2; bool part; };
+  std::vector<EvRec> evrec;
+  double t_update = 0, t_part = 0;
+  long long n_update = 0, n_part = 0;
+  int grid_update = 0, grid_part = 0;
+};
+
+namespace {
+
+FastParams fast_params(lse_run* r) {
+  FastParams P{};
+  P.pbits = r->d_P;
+  P.mbits = r->d_M;
+  P.data32 = r->d_data32;
+  P.lut_t = r->d_lut_t;
+  P.lut_s = r->d_lut_s;
+  P.part = r->d_part;
+  P.scal = r->d_scal;
+  P.ctx = r->d_ctx;
+  P.g = r->g;
+  for (int d = 0; d < 8; ++d) P.w32[d] = d <= r->R ? (float)r->h_ctx.w64[d] : 0.f;
+  P.dt32 = (float)r->p.dt;
+  P.scale32 = (float)r->scale;
+  return P;
+}
+
+dim3 grid2(int W, int H, int bx = 128) { return dim3((W + bx - 1) / bx, H); }
+
+int upload_ctx(lse_run* r) {
+  r->h_ctx.scale = r->scale;
+  CK(cudaMemcpyAsync(r->d_ctx, &r->h_ctx, sizeof(ExactCtx), cudaMemcpyHostToDevice, r->st));
+  return LSE_OK;
+}
+
+int ensure_generic(lse_run* r) {
+  if (r->d_F[0]) return LSE_OK;
+  TRY(dalloc(&r->d_F[0], r->npx));
+  TRY(dalloc(&r->d_F[1], r->npx));
+  TRY(dalloc(&r->d_U, r->npx));
+  TRY(dalloc(&r->d_T, r->npx));
+  return LSE_OK;
+}
+
+// current state -> dense exact field in F[curF]
+int materialize(lse_run* r) {
+  if (r->field_valid) return LSE_OK;
+  TRY(ensure_generic(r));
+  TRY(upload_ctx(r));
+  k_phi_from_bits<<<grid2(r->W, r->H), 128, 0, r->st>>>(r->d_bits[r->cur], r->d_F[r->curF],
+                                                         r->d_ctx, r->mode);
+  CKL();
+  r->field_valid = true;
+  return LSE_OK;
+}
+
+int launch_partition_abs(lse_run* r, int src, bool part, bool ckpt, bool mask_only,
+                         uint32_t* mbits) {
+  const double* field = src == SRC_FIELD ? r->d_F[r->curF] : nullptr;
+  int grid = std::min(r->g.ntiles, num_sms() * 8);
+  k_partition_abs<<<grid, r->nthr, 0, r->st>>>(field, r->d_bits[r->cur], r->d_ctx, src, r->d_P,
+                                               mbits, part, ckpt, mask_only, r->d_part, r->g);
+  CKL();
+  return LSE_OK;
+}
+
+// partition sums / coefficients for the current state (region model)
+int prepare(lse_run* r) {
+  if (r->prepared) return LSE_OK;
+  TRY(upload_ctx(r));
+  if (r->p.model == LSE_MODEL_REGION) {
+    TRY(launch_partition_abs(r, r->mode == SRC_FIELD ? SRC_FIELD : r->mode, true, false, false,
+                             r->d_M));
+    k_finalize<<<1, kThreads, 0, r->st>>>(r->d_part, r->g.ntiles, r->d_scal, 0, 1, 0,
+                                          r->iteration);
+    CKL();
+  }
+  r->prepared = true;
+  return LSE_OK;
+}
+
+cudaEvent_t next_event(lse_run* r) {
+  if (r->evused == r->evpool.size()) {
+    cudaEvent_t e;
+    cudaEventCreate(&e);
+    r->evpool.push_back(e);
+  }
+  return r->evpool[r->evused++];
+}
+
+template <int R, int MODEL>
+int launch_fast_R(lse_run* r, long long it, bool ckpt) {
+  FastParams P = fast_params(r);
+  P.bits_in = r->d_bits[r->cur];
+  P.bits_out = r->d_bits[r->cur ^ 1];
+  P.iter = it;
+  cudaEvent_t e0 = nullptr, e1 = nullptr, e2 = nullptr;
+  if (r->prof) {
+    e0 = next_event(r);
+    e1 = next_event(r);
+    e2 = next_event(r);
+    cudaEventRecord(e0, r->st);
+  }
+  if (r->mode == SRC_SCALED) {
+    if (!r->grid_update) r->grid_update = std::min(r->g.ntiles, num_sms() * 4);
+    k_update<R, MODEL, SRC_SCALED><<<r->grid_update, r->nthr, 0, r->st>>>(P);
+  } else {
+    if (!r->grid_update) r->grid_update = std::min(r->g.ntiles, num_sms() * 4);
+    k_update<R, MODEL, SRC_SMOOTH><<<r->grid_update, r->nthr, 0, r->st>>>(P);
+  }
+  CKL();
+  if (r->prof) cudaEventRecord(e1, r->st);
+  P.bits_in = r->d_bits[r->cur ^ 1];
+  if (!r->grid_part) r->grid_part = std::min(r->g.ntiles, num_sms() * 4);
+  bool launched_part = false;
+  if (MODEL == REGION) {
+    if (ckpt) k_partition<R, true, true, false><<<r->grid_part, r->nthr, 0, r->st>>>(P);
+    else k_partition<R, true, false, false><<<r->grid_part, r->nthr, 0, r->st>>>(P);
+    launched_part = true;
+  } else if (ckpt) {
+    k_partition<R, false, true, false><<<r->grid_part, r->nthr, 0, r->st>>>(P);
+    launched_part = true;
+  }
+  CKL();
+  if (r->prof) {
+    cudaEventRecord(e2, r->st);
+    r->evrec.push_back({e0, e1, e2, launched_part});
+  }
+  r->cur ^= 1;
+  r->mode = SRC_SMOOTH;
+  r->field_valid = false;
+  r->launched.emplace_back(it, r->cur);
+  return LSE_OK;
+}
+
+template <int MODEL>
+int launch_fast_model(lse_run* r, long long it, bool ckpt) {
+  switch (r->R) {
+    case 1: return launch_fast_R<1, MODEL>(r, it, ckpt);
+    case 2: return launch_fast_R<2, MODEL>(r, it, ckpt);
+    case 3: return launch_fast_R<3, MODEL>(r, it, ckpt);
+    case 4: return launch_fast_R<4, MODEL>(r, it, ckpt);
+  }
+  return fail(LSE_ERR_ARG, "unsupported template radius");
+}
+
+int launch_fast(lse_run* r, long long it, bool ckpt) {
+  if (r->p.model == LSE_MODEL_REGION) return launch_fast_model<REGION>(r, it, ckpt);
+  return launch_fast_model<EDGE>(r, it, ckpt);
+}
+
+// wait for the device, fold profiling events, detect convergence
+int collect(lse_run* r) {
+  CK(cudaMemcpyAsync(r->h_scal, r->d_scal, sizeof(Scalars), cudaMemcpyDeviceToHost, r->st));
+  CK(cudaStreamSynchronize(r->st));
+  if (r->prof) {
+    for (auto& e : r->evrec) {
+      float ms = 0.f;
+      cudaEventElapsedTime(&ms, e.e0, e.e1);
+      r->t_update += ms;
+      r->n_update++;
+      if (e.part) {
+        cudaEventElapsedTime(&ms, e.e1, e.e2);
+        r->t_part += ms;
+        r->n_part++;
+      }
+    }
+  }
+  r->evrec.clear();
+  r->evused = 0;
+  const Scalars& s = *r->h_scal;
+  r->degenerate = s.degenerate != 0;
+  if (s.converged && !r->converged) {
+    r->converged = true;
+    r->iteration = s.converged_iter;
+    for (auto& pr : r->launched)
+      if (pr.first == s.converged_iter) r->cur = pr.second;
+  }
+  r->launched.clear();
+  return LSE_OK;
+}
+
+bool fp32_ok(lse_run* r) {
+  if (r->R < 1 || r->R > 4) return false;
+  if (!(r->p.dt <= 1e6)) return false;
+  if (r->p.model == LSE_MODEL_REGION && !(r->img_absmax <= 1e6)) return false;
+  if (r->mode == SRC_SCALED && !(r->scale >= 1e-3 && r->scale <= 1e6)) return false;
+  return true;
+}
+
+int generic_iteration(lse_run* r, long long it, bool reinit_now, bool reg_now, bool ckpt) {
+  TRY(ensure_generic(r));
+  TRY(materialize(r));
+  CK(cudaMemsetAsync(&r->d_scal->nonfinite, 0, sizeof(int), r->st));
+  const double* phi = r->d_F[r->curF];
+  if (r->p.model == LSE_MODEL_REGION)
+    k_gen_update<REGION><<<grid2(r->W, r->H), 128, 0, r->st>>>(
+        phi, r->d_U, r->H, r->W, r->d_data32, r->d_data64, r->g.data_pitch, r->d_scal, r->p.dt);
+  else
+    k_gen_update<EDGE><<<grid2(r->W, r->H), 128, 0, r->st>>>(
+        phi, r->d_U, r->H, r->W, r->d_data32, r->d_data64, r->g.data_pitch, r->d_scal, r->p.dt);
+  CKL();
+  // the reference skips reinit/smoothing when u is not finite and raises
+  // either way; computing them regardless is harmless (phi is not committed)
+  if (reinit_now) {
+    k_binarize<<<num_sms() * 8, 256, 0, r->st>>>(r->d_U, r->d_U, r->npx);
+    CKL();
+  }
+  double* out = r->d_F[r->curF ^ 1];
+  if (reg_now) {
+    k_corr<0><<<grid2(r->W, r->H), 128, 0, r->st>>>(r->d_U, r->d_T, r->H, r->W, r->d_w64, r->R);
+    k_corr<1><<<grid2(r->W, r->H), 128, 0, r->st>>>(r->d_T, out, r->H, r->W, r->d_w64, r->R);
+    CKL();
+  } else {
+    CK(cudaMemcpyAsync(out, r->d_U, r->npx * sizeof(double), cudaMemcpyDeviceToDevice, r->st));
+  }
+  k_check_finite<<<num_sms() * 8, 256, 0, r->st>>>(out, r->npx, r->d_scal);
+  CKL();
+  int nonfinite = 0;
+  CK(cudaMemcpyAsync(&r->h_scal->nonfinite, &r->d_scal->nonfinite, sizeof(int),
+                     cudaMemcpyDeviceToHost, r->st));
+  CK(cudaStreamSynchronize(r->st));
+  nonfinite = r->h_scal->nonfinite;
+  if (nonfinite) return LSE_ERR_INSTABILITY;   // engine.py:172-173; phi untouched
+  // commit
+  r->curF ^= 1;
+  r->mode = SRC_FIELD;
+  r->field_valid = true;
+  if (reinit_now && reg_now && r->R >= 1 && r->R <= 4) {
+    // phi = G * b exactly: carry the state as bits from here on
+    k_pack_bits<<<dim3((r->g.pitch_w + 127) / 128, r->g.HR), 128, 0, r->st>>>(r->d_U,
+                                                                              r->d_bits[r->cur],
+                                                                              r->g);
+    CKL();
+    r->mode = SRC_SMOOTH;
+  }
+  const bool region = r->p.model == LSE_MODEL_REGION;
+  if (region || ckpt) {
+    // partition from the exact field (field_valid => F[curF] is phi^{n+1})
+    const double* field = r->d_F[r->curF];
+    int grid = std::min(r->g.ntiles, num_sms() * 8);
+    k_partition_abs<<<grid, r->nthr, 0, r->st>>>(field, r->d_bits[r->cur], r->d_ctx, SRC_FIELD,
+                                                 r->d_P, r->d_M, region, ckpt, 0, r->d_part, r->g);
+    CKL();
+    k_finalize<<<1, kThreads, 0, r->st>>>(r->d_part, r->g.ntiles, r->d_scal, 0, region, ckpt, it);
+    CKL();
+  }
+  r->iteration = it;
+  r->generic_iters++;
+  TRY(collect(r));
+  return LSE_OK;
+}
+
+void fill_status(lse_run* r, lse_status* s, long long instab) {
+  if (!s) return;
+  s->iteration = r->iteration;
+  s->converged = r->converged;
+  s->degenerate = r->degenerate;
+  s->instability_iteration = instab;
+  s->exact_fallbacks = r->h_scal ? (long long)r->h_scal->fallbacks : 0;
+  s->fast_iterations = r->fast_iters;
+  s->generic_iterations = r->generic_iters;
+}
+
+int upload_image(lse_run* r, const void* image, int is_f32) {
+  const int H = r->H, W = r->W;
+  const long long pitch = r->g.data_pitch;
+  double* tmp64 = nullptr;
+  int* d_flag = nullptr;
+  TRY(dalloc(&d_flag, 1));
+  CK(cudaMemsetAsync(d_flag, 0, sizeof(int), r->st));
+  if (is_f32) {
+    CK(cudaMemcpy2DAsync(r->d_data32, pitch * sizeof(float), image, W * sizeof(float),
+                         W * sizeof(float), H, cudaMemcpyHostToDevice, r->st));
+    r->fp32_exact = true;
+  } else {
+    TRY(dalloc(&tmp64, r->npx));
+    CK(cudaMemcpyAsync(tmp64, image, r->npx * sizeof(double), cudaMemcpyHostToDevice, r->st));
+    k_to_f32<<<grid2(W, H), 128, 0, r->st>>>(tmp64, r->d_data32, H, W, pitch, d_flag);
+    CKL();
+    int inexact = 0;
+    CK(cudaMemcpyAsync(&inexact, d_flag, sizeof(int), cudaMemcpyDeviceToHost, r->st));
+    CK(cudaStreamSynchronize(r->st));
+    r->fp32_exact = !inexact;
+  }
+  if (r->p.model == LSE_MODEL_REGION) {
+    if (!r->fp32_exact) {
+      if (!r->d_data64) TRY(dalloc(&r->d_data64, (size_t)pitch * H));
+      k_pitch64<<<grid2(W, H), 128, 0, r->st>>>(tmp64, r->d_data64, H, W, pitch);
+      CKL();
+    } else if (r->d_data64) {
+      cudaFree(r->d_data64);
+      r->d_data64 = nullptr;
+    }
+  } else {
+    // edge model: g = edge_function(I) on the device (engine.py:210-211)
+    double* I64 = tmp64;
+    if (!I64) {
+      TRY(dalloc(&I64, r->npx));
+      k_widen<<<grid2(W, H), 128, 0, r->st>>>(r->d_data32, I64, H, W, pitch);
+      CKL();
+      tmp64 = I64;
+    }
+    double *T = nullptr, *S = nullptr, *wpre = nullptr;
+    TRY(dalloc(&T, r->npx));
+    TRY(dalloc(&S, r->npx));
+    const int Rp = (int)r->wpre.size() / 2;
+    std::vector<double> wp(Rp + 1);
+    for (int d = 0; d <= Rp; ++d) wp[d] = r->wpre[Rp - d];
+    TRY(dalloc(&wpre, wp.size()));
+    CK(cudaMemcpyAsync(wpre, wp.data(), wp.size() * sizeof(double), cudaMemcpyHostToDevice, r->st));
+    k_corr<0><<<grid2(W, H), 128, 0, r->st>>>(I64, T, H, W, wpre, Rp);
+    k_corr<1><<<grid2(W, H), 128, 0, r->st>>>(T, S, H, W, wpre, Rp);
+    if (!r->d_data64) TRY(dalloc(&r->d_data64, (size_t)pitch * H));
+    k_edge_g<<<grid2(W, H), 128, 0, r->st>>>(S, H, W, r->p.edge_gain, r->d_data64, r->d_data32,
+                                              pitch);
+    CKL();
+    CK(cudaStreamSynchronize(r->st));
+    cudaFree(T);
+    cudaFree(S);
+    cudaFree(wpre);
+    r->fp32_exact = false;
+  }
+  // image statistics for the closed-form normalizer / guards
+  long long init[3] = {LLONG_MAX, LLONG_MIN, LLONG_MIN};
+  CK(cudaMemcpyAsync(r->d_keys, init, sizeof(init), cudaMemcpyHostToDevice, r->st));
+  k_minmax<<<num_sms() * 4, 256, 0, r->st>>>(r->d_data32, r->d_data64, H, W, pitch, r->d_keys);
+  k_store_minmax<<<1, 1, 0, r->st>>>(r->d_keys, r->d_scal);
+  CKL();
+  CK(cudaMemcpyAsync(r->h_scal, r->d_scal, sizeof(Scalars), cudaMemcpyDeviceToHost, r->st));
+  CK(cudaStreamSynchronize(r->st));
+  r->img_absmax = r->h_scal->img_absmax;
+  if (tmp64) cudaFree(tmp64);
+  cudaFree(d_flag);
+  r->h_ctx.data32 = r->d_data32;
+  r->h_ctx.data64 = r->d_data64;
+  r->prepared = false;
+  return LSE_OK;
+}
+
+int set_state(lse_run* r, const lse_phi0* s) {
+  if (!s) return fail(LSE_ERR_ARG, "null state");
+  const int H = r->H, W = r->W;
+  dim3 gw((r->g.pitch_w + 127) / 128, r->g.HR);
+  r->launched.clear();
+  if (s->kind == LSE_PHI0_POLYGONS) {
+    if (s->n_polys < 1) return fail(LSE_ERR_ARG, "at least one seed polygon is required");
+    std::vector<long long> offs(s->n_polys + 1, 0);
+    for (long long k = 0; k < s->n_polys; ++k) offs[k + 1] = offs[k] + s->poly_counts[k];
+    double* dxy = nullptr;
+    long long* doffs = nullptr;
+    TRY(dalloc(&dxy, 2 * offs.back()));
+    TRY(dalloc(&doffs, offs.size()));
+    CK(cudaMemcpyAsync(dxy, s->poly_xy, 2 * offs.back() * sizeof(double), cudaMemcpyHostToDevice,
+                       r->st));
+    CK(cudaMemcpyAsync(doffs, offs.data(), offs.size() * sizeof(long long), cudaMemcpyHostToDevice,
+                       r->st));
+    CK(cudaMemsetAsync(r->d_count, 0, sizeof(unsigned long long), r->st));
+    k_rasterize<<<gw, 128, 0, r->st>>>(dxy, doffs, (int)s->n_polys, s->inside_sign,
+                                       r->d_bits[r->cur], nullptr, r->g, r->d_count);
+    CKL();
+    unsigned long long cnt = 0;
+    CK(cudaMemcpyAsync(&cnt, r->d_count, sizeof(cnt), cudaMemcpyDeviceToHost, r->st));
+    CK(cudaStreamSynchronize(r->st));
+    cudaFree(dxy);
+    cudaFree(doffs);
+    if (cnt == 0) return fail(LSE_ERR_DEGENERATE_SEED, "seed polygons cover no pixel centers");
+    if ((long long)cnt == r->npx)
+      return fail(LSE_ERR_DEGENERATE_SEED, "seed polygons cover the entire grid");
+    r->mode = SRC_SCALED;
+    r->scale = 1.0;
+    r->field_valid = false;
+  } else if (s->kind == LSE_PHI0_SIGNS) {
+    if (!(s->scale > 0.0) || !std::isfinite(s->scale)) return fail(LSE_ERR_ARG, "bad sign scale");
+    signed char* d = nullptr;
+    TRY(dalloc(&d, r->npx));
+    CK(cudaMemcpyAsync(d, s->signs, r->npx, cudaMemcpyHostToDevice, r->st));
+    k_pack_signs<<<gw, 128, 0, r->st>>>(d, r->d_bits[r->cur], r->g);
+    CKL();
+    CK(cudaStreamSynchronize(r->st));
+    cudaFree(d);
+    r->mode = SRC_SCALED;
+    r->scale = s->scale;
+    r->field_valid = false;
+  } else if (s->kind == LSE_PHI0_FIELD) {
+    TRY(ensure_generic(r));
+    r->curF = 0;
+    CK(cudaMemcpyAsync(r->d_F[0], s->field, r->npx * sizeof(double), cudaMemcpyHostToDevice,
+                       r->st));
+    r->mode = SRC_FIELD;
+    r->field_valid = true;
+    // recognise fields the bit state represents exactly: +-s, or G * b
+    if (r->R >= 1 && r->R <= 4) {
+      k_pack_bits<<<gw, 128, 0, r->st>>>(r->d_F[0], r->d_bits[r->cur], r->g);
+      CKL();
+      double first = 0.0;
+      CK(cudaMemcpyAsync(&first, r->d_F[0], sizeof(double), cudaMemcpyDeviceToHost, r->st));
+      CK(cudaStreamSynchronize(r->st));
+      const double sc = std::fabs(first);
+      int cand[2] = {SRC_SCALED, SRC_SMOOTH};
+      for (int src : cand) {
+        if (src == SRC_SCALED && !(sc > 0.0 && std::isfinite(sc))) continue;
+        r->scale = sc;
+        TRY(upload_ctx(r));
+        k_phi_from_bits<<<grid2(W, H), 128, 0, r->st>>>(r->d_bits[r->cur], r->d_F[1], r->d_ctx,
+                                                         src);
+        CKL();
+        // compare bitwise
+        int* d_ne = nullptr;
+        TRY(dalloc(&d_ne, 1));
+        CK(cudaMemsetAsync(d_ne, 0, sizeof(int), r->st));
+        const long long n = r->npx;
+        const double* a = r->d_F[0];
+        const double* b = r->d_F[1];
+        k_bits_differ<<<num_sms() * 8, 256, 0, r->st>>>(a, b, n, d_ne);
+        CKL();
+        int ne = 1;
+        CK(cudaMemcpyAsync(&ne, d_ne, sizeof(int), cudaMemcpyDeviceToHost, r->st));
+        CK(cudaStreamSynchronize(r->st));
+        cudaFree(d_ne);
+        if (!ne) {
+          r->mode = src;
+          break;
+        }
+      }
+      if (r->mode != SRC_SCALED) r->scale = 1.0;
+    }
+  } else {
+    return fail(LSE_ERR_ARG, "unknown state kind");
+  }
+  r->iteration = s->iteration;
+  r->converged = s->converged != 0;
+  r->degenerate = s->degenerate != 0;
+  // device bookkeeping: sticky degenerate from the state, no stop; the
+  // checkpoint history (n_ckpt, equal_run, M) is kept as in the reference
+  CK(cudaMemcpyAsync(r->h_scal, r->d_scal, sizeof(Scalars), cudaMemcpyDeviceToHost, r->st));
+  CK(cudaStreamSynchronize(r->st));
+  r->h_scal->degenerate = r->degenerate;
+  r->h_scal->stop = 0;
+  r->h_scal->converged = 0;
+  r->h_scal->ticket = 0;
+  CK(cudaMemcpyAsync(r->d_scal, r->h_scal, sizeof(Scalars), cudaMemcpyHostToDevice, r->st));
+  TRY(upload_ctx(r));
+  CK(cudaStreamSynchronize(r->st));
+  r->prepared = false;
+  return LSE_OK;
+}
+
+}  // namespace
+
+// ======================================================================= C ABI
+extern "C" {
+
+int lse_abi_version(void) { return LSE_ABI_VERSION; }
+const char* lse_last_error(void) { return g_err.c_str(); }
+int lse_device_count(void) {
+  int n = 0;
+  if (cudaGetDeviceCount(&n) != cudaSuccess) return 0;
+  return n;
+}
+
+int lse_run_create(lse_run** out, const lse_params* p, long long height, long long width,
+                   const void* image, int image_is_f32, const lse_phi0* init) {
+  if (!out || !p || !image || !init) return fail(LSE_ERR_ARG, "null argument");
+  *out = nullptr;
+  if (height < 2 || width < 2) return fail(LSE_ERR_ARG, "gradient needs at least a 2x2 field");
+  if (height > (1LL << 30) || width > (1LL << 30)) return fail(LSE_ERR_ARG, "grid too large");
+  if (p->model != LSE_MODEL_REGION && p->model != LSE_MODEL_EDGE)
+    return fail(LSE_ERR_UNSUPPORTED, "only the region and edge models run on the device path");
+  if (p->ts_reg < 1 || p->ts_reg % 2 == 0 || !p->reg_weights)
+    return fail(LSE_ERR_ARG, "ts_reg must be an odd number >= 1");
+  if (p->ts_reg > 63) return fail(LSE_ERR_ARG, "ts_reg > 63 is not supported");
+  if (p->model == LSE_MODEL_EDGE && (p->ts_pre < 1 || p->ts_pre % 2 == 0 || !p->pre_weights))
+    return fail(LSE_ERR_ARG, "ts_pre must be an odd number >= 1");
+  TRY(check_device());
+  lse_run* r = new lse_run();
+  r->p = *p;
+  r->wreg.assign(p->reg_weights, p->reg_weights + p->ts_reg);
+  if (p->model == LSE_MODEL_EDGE) r->wpre.assign(p->pre_weights, p->pre_weights + p->ts_pre);
+  r->p.reg_weights = nullptr;
+  r->p.pre_weights = nullptr;
+  r->H = (int)height;
+  r->W = (int)width;
+  r->R = p->ts_reg / 2;
+  r->npx = height * width;
+  r->g.H = r->H;
+  r->g.W = r->W;
+  r->g.HR = (r->H + 31) / 32;
+  r->g.pitch_w = (int)round_up(r->W, 8);
+  r->g.data_pitch = round_up(r->W, 8);
+  long long need_thr = round_up((r->W + kColsPerThread - 1) / kColsPerThread, 32);
+  r->nthr = (int)std::min<long long>(kThreads, need_thr);
+  r->g.ncb = (r->W + kColsPerThread * r->nthr - 1) / (kColsPerThread * r->nthr);
+  r->g.ntiles = r->g.HR * r->g.ncb;
+  auto cleanup = [&](int rc) {
+    lse_run_destroy(r);
+    return rc;
+  };
+  if (cudaStreamCreateWithFlags(&r->st, cudaStreamNonBlocking) != cudaSuccess)
+    return cleanup(fail(LSE_ERR_CUDA, "stream creation failed"));
+  const size_t nbits = (size_t)r->g.HR * r->g.pitch_w;
+  int rc = LSE_OK;
+  if ((rc = dalloc(&r->d_data32, (size_t)r->g.data_pitch * r->H)) ||
+      (rc = dalloc(&r->d_bits[0], nbits)) || (rc = dalloc(&r->d_bits[1], nbits)) ||
+      (rc = dalloc(&r->d_P, nbits)) || (rc = dalloc(&r->d_M, nbits)) ||
+      (rc = dalloc(&r->d_mask, nbits)) || (rc = dalloc(&r->d_part, r->g.ntiles)) ||
+      (rc = dalloc(&r->d_scal, 1)) || (rc = dalloc(&r->d_lut_t, 512)) ||
+      (rc = dalloc(&r->d_lut_s, 512)) || (rc = dalloc(&r->d_ctx, 1)) ||
+      (rc = dalloc(&r->d_w64, 32)) || (rc = dalloc(&r->d_keys, 3)) ||
+      (rc = dalloc(&r->d_count, 1)))
+    return cleanup(rc);
+  if (cudaMallocHost((void**)&r->h_scal, sizeof(Scalars)) != cudaSuccess)
+    return cleanup(fail(LSE_ERR_CUDA, "pinned alloc failed"));
+  cudaMemsetAsync(r->d_bits[0], 0, nbits * 4, r->st);
+  cudaMemsetAsync(r->d_bits[1], 0, nbits * 4, r->st);
+  cudaMemsetAsync(r->d_P, 0, nbits * 4, r->st);
+  cudaMemsetAsync(r->d_M, 0, nbits * 4, r->st);
+  // weights: w64[d] = weight at distance d (axis_weights[R - d])
+  std::memset(&r->h_ctx, 0, sizeof(ExactCtx));
+  for (int d = 0; d <= r->R; ++d) r->h_ctx.w64[d] = r->wreg[r->R - d];
+  r->h_ctx.H = r->H;
+  r->h_ctx.W = r->W;
+  r->h_ctx.R = r->R;
+  r->h_ctx.pitch_w = r->g.pitch_w;
+  r->h_ctx.data_pitch = r->g.data_pitch;
+  r->h_ctx.dt = p->dt;
+  r->h_ctx.scale = 1.0;
+  r->h_ctx.scal = r->d_scal;
+  r->h_ctx.model = p->model == LSE_MODEL_REGION ? REGION : EDGE;
+  cudaMemcpyAsync(r->d_w64, r->h_ctx.w64, 32 * sizeof(double), cudaMemcpyHostToDevice, r->st);
+  // LUTs for the fast path (R <= 4)
+  if (r->R >= 1 && r->R <= 4) {
+    const int np = 1 << (2 * r->R + 1);
+    std::vector<float> lt(512, 0.f), ls(512, 0.f);
+    for (int q = 0; q < np; ++q) {
+      lt[q] = (float)host_t64((unsigned)q, r->R, r->h_ctx.w64);
+      double s = 0.0;
+      for (int k = 0; k <= 2 * r->R; ++k)
+        if ((q >> k) & 1) s += r->h_ctx.w64[std::abs(k - r->R)];
+      ls[q] = (float)s;
+    }
+    cudaMemcpyAsync(r->d_lut_t, lt.data(), 512 * sizeof(float), cudaMemcpyHostToDevice, r->st);
+    cudaMemcpyAsync(r->d_lut_s, ls.data(), 512 * sizeof(float), cudaMemcpyHostToDevice, r->st);
+    cudaStreamSynchronize(r->st);
+  }
+  // scalars
+  Scalars s0;
+  std::memset(&s0, 0, sizeof(s0));
+  s0.n_total = r->npx;
+  s0.dt = p->dt;
+  s0.model = r->h_ctx.model;
+  s0.conv_window = p->conv_window;
+  s0.eps_phi = (float)kEpsPhi;
+  s0.eps_u = (float)edge_eps_u(p->dt);
+  if (cudaMemcpyAsync(r->d_scal, &s0, sizeof(s0), cudaMemcpyHostToDevice, r->st) != cudaSuccess)
+    return cleanup(fail(LSE_ERR_CUDA, "scalar upload failed"));
+  if ((rc = upload_image(r, image, image_is_f32))) return cleanup(rc);
+  if ((rc = set_state(r, init))) return cleanup(rc);
+  *out = r;
+  return LSE_OK;
+}
+
+int lse_run_load_image(lse_run* r, const void* image, int image_is_f32) {
+  if (!r || !image) return fail(LSE_ERR_ARG, "null argument");
+  return upload_image(r, image, image_is_f32);
+}
+
+int lse_run_set_state(lse_run* r, const lse_phi0* st) {
+  if (!r) return fail(LSE_ERR_ARG, "null run");
+  return set_state(r, st);
+}
+
+int lse_run_advance(lse_run* r, long long n_steps, lse_status* st) {
+  if (!r) return fail(LSE_ERR_ARG, "null run");
+  if (n_steps < 0) return fail(LSE_ERR_ARG, "n_steps must be >= 0");
+  if (r->converged || r->iteration >= r->p.max_iters || n_steps == 0) {
+    fill_status(r, st, -1);
+    return LSE_OK;
+  }
+  const long long steps = std::min(n_steps, r->p.max_iters - r->iteration);
+  TRY(prepare(r));
+  const long long it0 = r->iteration;
+  bool pending = false;
+  for (long long it = it0 + 1; it <= it0 + steps; ++it) {
+    const bool reinit_now = r->p.reinit_period > 0 && it % r->p.reinit_period == 0;
+    const bool reg_now = it % r->p.reg_period == 0;
+    const bool ckpt = it % r->p.conv_check_every == 0;
+    if (reinit_now && reg_now && r->mode != SRC_FIELD && fp32_ok(r)) {
+      TRY(launch_fast(r, it, ckpt));
+      r->iteration = it;
+      r->fast_iters++;
+      pending = true;
+    } else {
+      if (pending) {
+        TRY(collect(r));
+        pending = false;
+        if (r->converged) break;
+      }
+      int rc = generic_iteration(r, it, reinit_now, reg_now, ckpt);
+      if (rc == LSE_ERR_INSTABILITY) {
+        fill_status(r, st, it);
+        char msg[160];
+        std::snprintf(msg, sizeof(msg), "numerical instability: non-finite level-set values at "
+                                        "iteration %lld", it);
+        return fail(LSE_ERR_INSTABILITY, msg);
+      }
+      TRY(rc);
+      if (r->converged) break;
+    }
+  }
+  if (pending) TRY(collect(r));
+  fill_status(r, st, -1);
+  return LSE_OK;
+}
+
+int lse_run_status(lse_run* r, lse_status* st) {
+  if (!r || !st) return fail(LSE_ERR_ARG, "null argument");
+  fill_status(r, st, -1);
+  return LSE_OK;
+}
+
+int lse_run_read_phi(lse_run* r, double* out) {
+  if (!r || !out) return fail(LSE_ERR_ARG, "null argument");
+  TRY(ensure_generic(r));
+  const double* src;
+  if (r->field_valid) {
+    src = r->d_F[r->curF];
+  } else {
+    TRY(upload_ctx(r));
+    k_phi_from_bits<<<grid2(r->W, r->H), 128, 0, r->st>>>(r->d_bits[r->cur], r->d_U, r->d_ctx,
+                                                           r->mode);
+    CKL();
+    src = r->d_U;
+  }
+  CK(cudaMemcpyAsync(out, src, r->npx * sizeof(double), cudaMemcpyDeviceToHost, r->st));
+  CK(cudaStreamSynchronize(r->st));
+  return LSE_OK;
+}
+
+int lse_run_read_mask(lse_run* r, unsigned char* out, int inside_sign, int packed) {
+  if (!r || !out) return fail(LSE_ERR_ARG, "null argument");
+  TRY(upload_ctx(r));
+  if (r->mode == SRC_SMOOTH && !r->field_valid && r->R >= 1 && r->R <= 4) {
+    FastParams P = fast_params(r);
+    P.bits_in = r->d_bits[r->cur];
+    P.mbits = r->d_mask;
+    const int grid = std::min(r->g.ntiles, num_sms() * 4);
+    switch (r->R) {
+      case 1: k_partition<1, false, false, true><<<grid, r->nthr, 0, r->st>>>(P); break;
+      case 2: k_partition<2, false, false, true><<<grid, r->nthr, 0, r->st>>>(P); break;
+      case 3: k_partition<3, false, false, true><<<grid, r->nthr, 0, r->st>>>(P); break;
+      case 4: k_partition<4, false, false, true><<<grid, r->nthr, 0, r->st>>>(P); break;
+    }
+    CKL();
+  } else {
+    const int src = r->field_valid ? SRC_FIELD : r->mode;
+    if (src == SRC_SMOOTH) TRY(materialize(r));
+    TRY(launch_partition_abs(r, r->field_valid ? SRC_FIELD : src, false, false, true, r->d_mask));
+  }
+  const int invert = inside_sign > 0 ? 0 : 1;
+  unsigned char* d_out = nullptr;
+  if (packed) {
+    const long long nbytes = (r->npx + 7) / 8;
+    TRY(dalloc(&d_out, nbytes));
+    k_mask_packed<<<(unsigned)((nbytes + 255) / 256), 256, 0, r->st>>>(r->d_mask, r->g, invert,
+                                                                      d_out, nbytes);
+    CKL();
+    CK(cudaMemcpyAsync(out, d_out, nbytes, cudaMemcpyDeviceToHost, r->st));
+  } else {
+    TRY(dalloc(&d_out, r->npx));
+    k_mask_u8<<<grid2(r->W, r->H), 128, 0, r->st>>>(r->d_mask, r->g, invert, d_out);
+    CKL();
+    CK(cudaMemcpyAsync(out, d_out, r->npx, cudaMemcpyDeviceToHost, r->st));
+  }
+  CK(cudaStreamSynchronize(r->st));
+  cudaFree(d_out);
+  return LSE_OK;
+}
+
+int lse_run_set_profiling(lse_run* r, int enabled) {
+  if (!r) return fail(LSE_ERR_ARG, "null run");
+  r->prof = enabled != 0;
+  r->t_update = r->t_part = 0;
+  r->n_update = r->n_part = 0;
+  return LSE_OK;
+}
+
+int lse_run_kernel_times(lse_run* r, double* update_ms, long long* update_launches,
+                         double* partition_ms, long long* partition_launches) {
+  if (!r) return fail(LSE_ERR_ARG, "null run");
+  if (update_ms) *update_ms = r->t_update;
+  if (update_launches) *update_launches = r->n_update;
+  if (partition_ms) *partition_ms = r->t_part;
+  if (partition_launches) *partition_launches = r->n_part;
+  return LSE_OK;
+}
+
+void lse_run_destroy(lse_run* r) {
+  if (!r) return;
+  if (r->st) cudaStreamSynchronize(r->st);
+  void* ptrs[] = {r->d_data32, r->d_data64, r->d_bits[0], r->d_bits[1], r->d_P, r->d_M,
+                  r->d_mask, r->d_part, r->d_scal, r->d_lut_t, r->d_lut_s, r->d_ctx,
+                  r->d_w64, r->d_keys, r->d_count, r->d_F[0], r->d_F[1], r->d_U, r->d_T};
+  for (void* q : ptrs)
+    if (q) cudaFree(q);
+  if (r->h_scal) cudaFreeHost(r->h_scal);
+  for (auto e : r->evpool) cudaEventDestroy(e);
+  if (r->st) cudaStreamDestroy(r->st);
+  delete r;
+}
+
+
+}  // extern "C"
+
+// ------------------------------------------------------- stateless kernels
+namespace {
+
+struct DevBuf {
+  void* p = nullptr;
+  ~DevBuf() { if (p) cudaFree(p); }
+};
+
+template <typename T>
+int dbuf(DevBuf& b, size_t n) {
+  T* q = nullptr;
+  TRY(dalloc(&q, n));
+  b.p = q;
+  return LSE_OK;
+}
+
+std::vector<double> taps_from_axis(const double* w, int ts) {
+  const int R = ts / 2;
+  std::vector<double> out(R + 1);
+  for (int d = 0; d <= R; ++d) out[d] = w[R - d];
+  return out;
+}
+
+int conv_device(const double* d_in, double* d_tmp, double* d_out, int H, int W, const double* w,
+                int ts) {
+  auto taps = taps_from_axis(w, ts);
+  DevBuf dw;
+  TRY(dbuf<double>(dw, taps.size()));
+  CK(cudaMemcpy(dw.p, taps.data(), taps.size() * sizeof(double), cudaMemcpyHostToDevice));
+  k_corr<0><<<grid2(W, H), 128>>>(d_in, d_tmp, H, W, (double*)dw.p, ts / 2);
+  k_corr<1><<<grid2(W, H), 128>>>(d_tmp, d_out, H, W, (double*)dw.p, ts / 2);
+  CKL();
+  CK(cudaDeviceSynchronize());
+  return LSE_OK;
+}
+
+// region coefficients (c+, c-, peak) of (image, phi) into a device Scalars
+int region_scalars(const double* d_img, const double* d_phi, int H, int W, Scalars* d_sc,
+                   Scalars* h_sc) {
+  const long long n = (long long)H * W;
+  const int blocks = std::min<long long>((n + 255) / 256, num_sms() * 4);
+  DevBuf part, keys;
+  TRY(dbuf<TilePartial>(part, blocks));
+  TRY(dbuf<long long>(keys, 3));
+  Scalars s0;
+  std::memset(&s0, 0, sizeof(s0));
+  s0.n_total = n;
+  CK(cudaMemcpy(d_sc, &s0, sizeof(s0), cudaMemcpyHostToDevice));
+  long long init[3] = {LLONG_MAX, LLONG_MIN, LLONG_MIN};
+  CK(cudaMemcpy(keys.p, init, sizeof(init), cudaMemcpyHostToDevice));
+  k_minmax<<<num_sms() * 4, 256>>>(nullptr, d_img, H, W, W, (long long*)keys.p);
+  k_store_minmax<<<1, 1>>>((long long*)keys.p, d_sc);
+  k_region_sums<<<blocks, 256>>>(d_img, d_phi, n, (TilePartial*)part.p);
+  k_finalize<<<1, kThreads>>>((TilePartial*)part.p, blocks, d_sc, 0, 1, 0, 0);
+  CKL();
+  CK(cudaMemcpy(h_sc, d_sc, sizeof(Scalars), cudaMemcpyDeviceToHost));
+  return LSE_OK;
+}
+
+}  // namespace
+
+extern "C" {
+
+int lse_edge_function(const double* image, long long h, long long w, const double* weights,
+                      int ts, double gain, double* g_out) {
+  if (!image || !weights || !g_out || ts < 1 || ts % 2 == 0) return fail(LSE_ERR_ARG, "bad arguments");
+  if (h < 2 || w < 2) return fail(LSE_ERR_ARG, "gradient needs at least a 2x2 field");
+  TRY(check_device());
+  const long long n = h * w;
+  DevBuf a, b, c;
+  TRY(dbuf<double>(a, n));
+  TRY(dbuf<double>(b, n));
+  TRY(dbuf<double>(c, n));
+  CK(cudaMemcpy(a.p, image, n * sizeof(double), cudaMemcpyHostToDevice));
+  TRY(conv_device((double*)a.p, (double*)b.p, (double*)c.p, (int)h, (int)w, weights, ts));
+  k_edge_g<<<grid2((int)w, (int)h), 128>>>((double*)c.p, (int)h, (int)w, gain, (double*)a.p,
+                                           nullptr, w);
+  CKL();
+  CK(cudaMemcpy(g_out, a.p, n * sizeof(double), cudaMemcpyDeviceToHost));
+  return LSE_OK;
+}
+
+int lse_convolve_same(const double* f, long long h, long long w, const double* weights, int ts,
+                      double* out) {
+  if (!f || !weights || !out || ts < 1 || ts % 2 == 0 || h < 1 || w < 1)
+    return fail(LSE_ERR_ARG, "bad arguments");
+  TRY(check_device());
+  const long long n = h * w;
+  DevBuf a, b, c;
+  TRY(dbuf<double>(a, n));
+  TRY(dbuf<double>(b, n));
+  TRY(dbuf<double>(c, n));
+  CK(cudaMemcpy(a.p, f, n * sizeof(double), cudaMemcpyHostToDevice));
+  TRY(conv_device((double*)a.p, (double*)b.p, (double*)c.p, (int)h, (int)w, weights, ts));
+  CK(cudaMemcpy(out, c.p, n * sizeof(double), cudaMemcpyDeviceToHost));
+  return LSE_OK;
+}
+
+int lse_correlate2d(const double* f, long long h, long long w, const double* weights, int ts,
+                    double* out) {
+  if (!f || !weights || !out || ts < 1 || ts % 2 == 0 || h < 1 || w < 1)
+    return fail(LSE_ERR_ARG, "bad arguments");
+  TRY(check_device());
+  const long long n = h * w;
+  DevBuf a, b, dw;
+  TRY(dbuf<double>(a, n));
+  TRY(dbuf<double>(b, n));
+  TRY(dbuf<double>(dw, (size_t)ts * ts));
+  CK(cudaMemcpy(a.p, f, n * sizeof(double), cudaMemcpyHostToDevice));
+  CK(cudaMemcpy(dw.p, weights, (size_t)ts * ts * sizeof(double), cudaMemcpyHostToDevice));
+  k_corr2d<<<grid2((int)w, (int)h), 128>>>((double*)a.p, (double*)b.p, (int)h, (int)w,
+                                           (double*)dw.p, ts);
+  CKL();
+  CK(cudaMemcpy(out, b.p, n * sizeof(double), cudaMemcpyDeviceToHost));
+  return LSE_OK;
+}
+
+int lse_gradient(const double* f, long long h, long long w, double* fx, double* fy,
+                 double* magnitude) {
+  if (!f) return fail(LSE_ERR_ARG, "bad arguments");
+  if (h < 2 || w < 2) return fail(LSE_ERR_ARG, "gradient needs at least a 2x2 field");
+  TRY(check_device());
+  const long long n = h * w;
+  DevBuf a, bx, by, bm;
+  TRY(dbuf<double>(a, n));
+  TRY(dbuf<double>(bx, n));
+  TRY(dbuf<double>(by, n));
+  TRY(dbuf<double>(bm, n));
+  CK(cudaMemcpy(a.p, f, n * sizeof(double), cudaMemcpyHostToDevice));
+  k_gradient<<<grid2((int)w, (int)h), 128>>>((double*)a.p, (int)h, (int)w, (double*)bx.p,
+                                             (double*)by.p, (double*)bm.p);
+  CKL();
+  if (fx) CK(cudaMemcpy(fx, bx.p, n * sizeof(double), cudaMemcpyDeviceToHost));
+  if (fy) CK(cudaMemcpy(fy, by.p, n * sizeof(double), cudaMemcpyDeviceToHost));
+  if (magnitude) CK(cudaMemcpy(magnitude, bm.p, n * sizeof(double), cudaMemcpyDeviceToHost));
+  return LSE_OK;
+}
+
+int lse_binarize(const double* phi, long long n, double* out) {
+  if (!phi || !out || n < 0) return fail(LSE_ERR_ARG, "bad arguments");
+  if (n == 0) return LSE_OK;
+  TRY(check_device());
+  DevBuf a;
+  TRY(dbuf<double>(a, n));
+  CK(cudaMemcpy(a.p, phi, n * sizeof(double), cudaMemcpyHostToDevice));
+  k_binarize<<<num_sms() * 8, 256>>>((double*)a.p, (double*)a.p, n);
+  CKL();
+  CK(cudaMemcpy(out, a.p, n * sizeof(double), cudaMemcpyDeviceToHost));
+  return LSE_OK;
+}
+
+int lse_region_means(const double* image, const double* phi, long long h, long long w,
+                     double* c_plus, double* c_minus) {
+  if (!image || !phi || h < 1 || w < 1) return fail(LSE_ERR_ARG, "bad arguments");
+  TRY(check_device());
+  const long long n = h * w;
+  DevBuf a, b, sc;
+  TRY(dbuf<double>(a, n));
+  TRY(dbuf<double>(b, n));
+  TRY(dbuf<Scalars>(sc, 1));
+  CK(cudaMemcpy(a.p, image, n * sizeof(double), cudaMemcpyHostToDevice));
+  CK(cudaMemcpy(b.p, phi, n * sizeof(double), cudaMemcpyHostToDevice));
+  Scalars hs;
+  TRY(region_scalars((double*)a.p, (double*)b.p, (int)h, (int)w, (Scalars*)sc.p, &hs));
+  if (hs.n_pos == 0 || hs.n_pos == n)
+    return fail(LSE_ERR_DEGENERATE, "one side of the partition is empty");
+  if (c_plus) *c_plus = hs.c_pos;
+  if (c_minus) *c_minus = hs.c_neg;
+  return LSE_OK;
+}
+
+int lse_region_velocity(const double* image, const double* phi, long long h, long long w,
+                        double* v_out, int* degenerate) {
+  if (!image || !phi || !v_out || h < 1 || w < 1) return fail(LSE_ERR_ARG, "bad arguments");
+  TRY(check_device());
+  const long long n = h * w;
+  DevBuf a, b, v, sc;
+  TRY(dbuf<double>(a, n));
+  TRY(dbuf<double>(b, n));
+  TRY(dbuf<double>(v, n));
+  TRY(dbuf<Scalars>(sc, 1));
+  CK(cudaMemcpy(a.p, image, n * sizeof(double), cudaMemcpyHostToDevice));
+  CK(cudaMemcpy(b.p, phi, n * sizeof(double), cudaMemcpyHostToDevice));
+  Scalars hs;
+  TRY(region_scalars((double*)a.p, (double*)b.p, (int)h, (int)w, (Scalars*)sc.p, &hs));
+  if (degenerate) *degenerate = hs.zero_vel;
+  if (hs.zero_vel) {
+    // models.py:111-118: zero field, degenerate = True, gradient not evaluated
+    std::memset(v_out, 0, n * sizeof(double));
+    return LSE_OK;
+  }
+  if (h < 2 || w < 2) return fail(LSE_ERR_ARG, "gradient needs at least a 2x2 field");
+  k_velocity<REGION><<<grid2((int)w, (int)h), 128>>>((double*)b.p, (double*)v.p, (int)h, (int)w,
+                                                     (double*)a.p, (Scalars*)sc.p);
+  CKL();
+  CK(cudaMemcpy(v_out, v.p, n * sizeof(double), cudaMemcpyDeviceToHost));
+  return LSE_OK;
+}
+
+int lse_edge_velocity(const double* g, const double* phi, long long h, long long w, double* v_out) {
+  if (!g || !phi || !v_out) return fail(LSE_ERR_ARG, "bad arguments");
+  if (h < 2 || w < 2) return fail(LSE_ERR_ARG, "gradient needs at least a 2x2 field");
+  TRY(check_device());
+  const long long n = h * w;
+  DevBuf a, b, v;
+  TRY(dbuf<double>(a, n));
+  TRY(dbuf<double>(b, n));
+  TRY(dbuf<double>(v, n));
+  CK(cudaMemcpy(a.p, g, n * sizeof(double), cudaMemcpyHostToDevice));
+  CK(cudaMemcpy(b.p, phi, n * sizeof(double), cudaMemcpyHostToDevice));
+  k_velocity<EDGE><<<grid2((int)w, (int)h), 128>>>((double*)b.p, (double*)v.p, (int)h, (int)w,
+                                                   (double*)a.p, nullptr);
+  CKL();
+  CK(cudaMemcpy(v_out, v.p, n * sizeof(double), cudaMemcpyDeviceToHost));
+  return LSE_OK;
+}
+
+int lse_rasterize_seeds(const double* poly_xy, const long long* poly_counts, long long n_polys,
+                        int inside_sign, long long h, long long w, signed char* out) {
+  if (!poly_xy || !poly_counts || !out || n_polys < 1 || h < 1 || w < 1)
+    return fail(LSE_ERR_ARG, "bad arguments");
+  TRY(check_device());
+  std::vector<long long> offs(n_polys + 1, 0);
+  for (long long k = 0; k < n_polys; ++k) offs[k + 1] = offs[k] + poly_counts[k];
+  RunGeom g{};
+  g.H = (int)h;
+  g.W = (int)w;
+  g.HR = (int)((h + 31) / 32);
+  g.pitch_w = (int)w;
+  DevBuf dxy, doffs, dsig, dcnt;
+  TRY(dbuf<double>(dxy, 2 * offs.back()));
+  TRY(dbuf<long long>(doffs, offs.size()));
+  TRY(dbuf<signed char>(dsig, h * w));
+  TRY(dbuf<unsigned long long>(dcnt, 1));
+  CK(cudaMemcpy(dxy.p, poly_xy, 2 * offs.back() * sizeof(double), cudaMemcpyHostToDevice));
+  CK(cudaMemcpy(doffs.p, offs.data(), offs.size() * sizeof(long long), cudaMemcpyHostToDevice));
+  CK(cudaMemset(dcnt.p, 0, sizeof(unsigned long long)));
+  k_rasterize<<<dim3((unsigned)((w + 127) / 128), g.HR), 128>>>(
+      (double*)dxy.p, (long long*)doffs.p, (int)n_polys, inside_sign, nullptr,
+      (signed char*)dsig.p, g, (unsigned long long*)dcnt.p);
+  CKL();
+  unsigned long long cnt = 0;
+  CK(cudaMemcpy(&cnt, dcnt.p, sizeof(cnt), cudaMemcpyDeviceToHost));
+  if (cnt == 0) return fail(LSE_ERR_DEGENERATE_SEED, "seed polygons cover no pixel centers");
+  if ((long long)cnt == h * w) return fail(LSE_ERR_DEGENERATE_SEED, "seed polygons cover the entire grid");
+  CK(cudaMemcpy(out, dsig.p, h * w, cudaMemcpyDeviceToHost));
+  return LSE_OK;
+}
+
+}  // extern "C"

@@ -1,0 +1,487 @@
+// lse_generic.cuh -- exact fp64 field kernels.
+//
+// These carry a float64 phi field through _advance_once step by step, in
+// the reference's operation order, for the iterations the binary-state path
+// cannot represent: reinit_period != 1 or reg_period != 1 (engine.py:160-169),
+// an injected non-binary state, template sizes outside 3..9, or inputs
+// outside the fp32 guard's range (huge dt / intensities).  They also
+// implement the stateless public kernels (edge_function, convolve_same,
+// gradients, velocities) and the one-time setup passes (seed rasterization,
+// image statistics, edge indicator).
+#pragma once
+#include "lse_device.cuh"
+#include "lse_fast.cuh"
+
+namespace lse {
+
+// Separable correlation pass, scipy order (kernels.py:72-76 ->
+// scipy NI_Correlate1D symmetric branch), zero padding.
+// AXIS 0: along rows (vertical), AXIS 1: along columns (horizontal).
+template <int AXIS>
+__global__ void k_corr(const double* __restrict__ in, double* __restrict__ out, int H, int W,
+                       const double* __restrict__ w, int R) {
+  const int x = blockIdx.x * blockDim.x + threadIdx.x;
+  const int i = blockIdx.y;
+  if (x >= W) return;
+  auto f = [&](int ii, int xx) -> double {
+    if (AXIS == 0) return (ii < 0 || ii >= H) ? 0.0 : in[(size_t)ii * W + xx];
+    return (xx < 0 || xx >= W) ? 0.0 : in[(size_t)ii * W + xx];
+  };
+  double acc = dmul(f(i, x), w[0]);
+  for (int d = R; d >= 1; --d) {
+    double l = AXIS == 0 ? f(i - d, x) : f(i, x - d);
+    double r = AXIS == 0 ? f(i + d, x) : f(i, x + d);
+    acc = dadd(acc, dmul(dadd(l, r), w[d]));
+  }
+  out[(size_t)i * W + x] = acc;
+}
+
+// full 2-D correlation (ndimage.correlate, mode constant 0): footprint of the
+// non-zero weights, row-major order
+__global__ void k_corr2d(const double* __restrict__ in, double* __restrict__ out, int H, int W,
+                         const double* __restrict__ w2, int ts) {
+  const int x = blockIdx.x * blockDim.x + threadIdx.x;
+  const int i = blockIdx.y;
+  if (x >= W) return;
+  const int R = ts / 2;
+  double acc = 0.0;
+  bool first = true;
+  for (int a = 0; a < ts; ++a)
+    for (int b = 0; b < ts; ++b) {
+      const double wv = w2[a * ts + b];
+      if (wv == 0.0) continue;
+      const int ii = i + a - R, xx = x + b - R;
+      const double v = (ii < 0 || ii >= H || xx < 0 || xx >= W) ? 0.0 : in[(size_t)ii * W + xx];
+      if (first) { acc = dmul(v, wv); first = false; }
+      else acc = dadd(acc, dmul(v, wv));
+    }
+  out[(size_t)i * W + x] = acc;
+}
+
+// np.gradient (kernels.py:81-90) of a dense field at (i, x)
+__device__ __forceinline__ void np_gradient(const double* f, int H, int W, int i, int x,
+                                            double& fx, double& fy) {
+  auto v = [&](int ii, int xx) { return f[(size_t)ii * W + xx]; };
+  const double c = v(i, x);
+  if (x == 0) fx = dsub(v(i, 1), c);
+  else if (x == W - 1) fx = dsub(c, v(i, W - 2));
+  else fx = dmul(dsub(v(i, x + 1), v(i, x - 1)), 0.5);
+  if (i == 0) fy = dsub(v(1, x), c);
+  else if (i == H - 1) fy = dsub(c, v(H - 2, x));
+  else fy = dmul(dsub(v(i + 1, x), v(i - 1, x)), 0.5);
+}
+
+// edge indicator (models.py:78-81) from the smoothed image S
+__global__ void k_edge_g(const double* __restrict__ S, int H, int W, double gain,
+                         double* __restrict__ g64, float* __restrict__ g32, long long pitch) {
+  const int x = blockIdx.x * blockDim.x + threadIdx.x;
+  const int i = blockIdx.y;
+  if (x >= W) return;
+  double fx, fy;
+  np_gradient(S, H, W, i, x, fx, fy);
+  const double a = dmul(gain, fx), b = dmul(gain, fy);
+  const double g = ddiv(1.0, dadd(dadd(1.0, dmul(a, a)), dmul(b, b)));
+  if (g64) g64[(size_t)i * pitch + x] = g;
+  if (g32) g32[(size_t)i * pitch + x] = (float)g;
+}
+
+__global__ void k_gradient(const double* __restrict__ f, int H, int W, double* fx_out,
+                           double* fy_out, double* mag_out) {
+  const int x = blockIdx.x * blockDim.x + threadIdx.x;
+  const int i = blockIdx.y;
+  if (x >= W) return;
+  double fx, fy;
+  np_gradient(f, H, W, i, x, fx, fy);
+  const size_t o = (size_t)i * W + x;
+  if (fx_out) fx_out[o] = fx;
+  if (fy_out) fy_out[o] = fy;
+  if (mag_out) mag_out[o] = np_hypot(fx, fy);
+}
+
+// u = phi + dt * v on a dense field (engine.py:155-157) + finiteness flag
+// (engine.py:159).  data: I (region) or g (edge), exact values.
+template <int MODEL>
+__global__ void k_gen_update(const double* __restrict__ phi, double* __restrict__ u, int H, int W,
+                             const float* __restrict__ data32, const double* __restrict__ data64,
+                             long long dpitch, Scalars* sc, double dt) {
+  const int x = blockIdx.x * blockDim.x + threadIdx.x;
+  const int i = blockIdx.y;
+  if (MODEL == REGION && x == 0 && i == 0 && sc->zero_vel) sc->degenerate = 1;
+  if (x >= W) return;
+  double fx, fy;
+  np_gradient(phi, H, W, i, x, fx, fy);
+  const double h = np_hypot(fx, fy);
+  const size_t od = (size_t)i * dpitch + x;
+  const double d = data64 ? data64[od] : (double)data32[od];
+  double v;
+  if (MODEL == REGION) {
+    if (sc->zero_vel) v = 0.0;
+    else v = dmul(ddiv(dmul(sc->dc, dsub(dsub(dmul(2.0, d), sc->c_pos), sc->c_neg)), sc->peak), h);
+  } else {
+    v = dmul(d, h);
+  }
+  const double out = dadd(phi[(size_t)i * W + x], dmul(dt, v));
+  u[(size_t)i * W + x] = out;
+  if (!isfinite(out)) sc->nonfinite = 1;
+}
+
+// velocity only (public region_velocity / edge_velocity)
+template <int MODEL>
+__global__ void k_velocity(const double* __restrict__ phi, double* __restrict__ v_out, int H, int W,
+                           const double* __restrict__ data, const Scalars* sc) {
+  const int x = blockIdx.x * blockDim.x + threadIdx.x;
+  const int i = blockIdx.y;
+  if (x >= W) return;
+  double fx, fy;
+  np_gradient(phi, H, W, i, x, fx, fy);
+  const double h = np_hypot(fx, fy);
+  const double d = data[(size_t)i * W + x];
+  double v;
+  if (MODEL == REGION) {
+    if (sc->zero_vel) v = 0.0;
+    else v = dmul(ddiv(dmul(sc->dc, dsub(dsub(dmul(2.0, d), sc->c_pos), sc->c_neg)), sc->peak), h);
+  } else {
+    v = dmul(d, h);
+  }
+  v_out[(size_t)i * W + x] = v;
+}
+
+__global__ void k_binarize(const double* __restrict__ in, double* __restrict__ out, long long n) {
+  long long k = (long long)blockIdx.x * blockDim.x + threadIdx.x;
+  for (; k < n; k += (long long)gridDim.x * blockDim.x) out[k] = in[k] > 0.0 ? 1.0 : -1.0;
+}
+
+__global__ void k_check_finite(const double* __restrict__ f, long long n, Scalars* sc) {
+  long long k = (long long)blockIdx.x * blockDim.x + threadIdx.x;
+  bool bad = false;
+  for (; k < n; k += (long long)gridDim.x * blockDim.x) bad |= !isfinite(f[k]);
+  if (__any_sync(0xffffffffu, bad) && (threadIdx.x & 31) == 0) sc->nonfinite = 1;
+}
+
+// dense field (pitch W) -> vertical-word bits of (f > 0)
+__global__ void k_pack_bits(const double* __restrict__ f, uint32_t* __restrict__ bits, RunGeom g) {
+  const int x = blockIdx.x * blockDim.x + threadIdx.x;
+  const int r = blockIdx.y;
+  if (x >= g.pitch_w) return;
+  uint32_t w = 0u;
+  if (x < g.W) {
+    for (int k = 0; k < 32; ++k) {
+      const int i = r * 32 + k;
+      if (i >= g.H) break;
+      w |= (f[(size_t)i * g.W + x] > 0.0 ? 1u : 0u) << k;
+    }
+  }
+  bits[(size_t)r * g.pitch_w + x] = w;
+}
+
+// int8 signs -> bits (b = sign > 0)
+__global__ void k_pack_signs(const signed char* __restrict__ s, uint32_t* __restrict__ bits, RunGeom g) {
+  const int x = blockIdx.x * blockDim.x + threadIdx.x;
+  const int r = blockIdx.y;
+  if (x >= g.pitch_w) return;
+  uint32_t w = 0u;
+  if (x < g.W) {
+    for (int k = 0; k < 32; ++k) {
+      const int i = r * 32 + k;
+      if (i >= g.H) break;
+      w |= (s[(size_t)i * g.W + x] > 0 ? 1u : 0u) << k;
+    }
+  }
+  bits[(size_t)r * g.pitch_w + x] = w;
+}
+
+// state -> exact float64 phi (SMOOTH: G*b in scipy order; SCALED: +-s)
+__global__ void k_phi_from_bits(const uint32_t* __restrict__ bits, double* __restrict__ out,
+                                const ExactCtx* c, int src) {
+  const int x = blockIdx.x * blockDim.x + threadIdx.x;
+  const int i = blockIdx.y;
+  if (x >= c->W) return;
+  double v;
+  if (src == SRC_SCALED) v = get_bit(bits, c->pitch_w, i, x) ? c->scale : -c->scale;
+  else v = exact_phi_smooth(bits, c->pitch_w, c->H, c->W, c->R, c->w64, i, x);
+  out[(size_t)i * c->W + x] = v;
+}
+
+// Partition / checkpoint pass over any state representation, ABSOLUTE sums
+// (grid.py:112-117 with double-double accumulation) + checkpoint mask
+// (engine.py:229) + mismatch count vs the previous checkpoint.
+// src: SRC_FIELD (phi dense), SRC_SCALED or SRC_SMOOTH (bits, exact phi).
+__global__ void __launch_bounds__(kThreads) k_partition_abs(const double* __restrict__ field,
+                                                            const uint32_t* __restrict__ bits,
+                                                            const ExactCtx* c, int src,
+                                                            uint32_t* pbits, uint32_t* mbits,
+                                                            int do_part, int do_ckpt,
+                                                            int write_mask_only,
+                                                            TilePartial* part, RunGeom g) {
+  __shared__ TilePartial s_warp[kThreads / 32];
+  const int cbw = kColsPerThread * blockDim.x;
+  for (int tile = blockIdx.x; tile < g.ntiles; tile += gridDim.x) {
+    const int r = tile / g.ncb;
+    const int cx0 = (tile - r * g.ncb) * cbw;
+    const int x0 = cx0 + kColsPerThread * threadIdx.x;
+    double ah = 0, al = 0, bh = 0, bl = 0;
+    long long na = 0, nb = 0;
+    unsigned long long mm = 0;
+    if (x0 < g.W) {
+      for (int cc = 0; cc < 8; ++cc) {
+        const int x = x0 + cc;
+        uint32_t pw = 0u, mw = 0u;
+        if (x < g.W) {
+          for (int k = 0; k < 32; ++k) {
+            const int i = r * 32 + k;
+            if (i >= g.H) break;
+            double f;
+            if (src == SRC_FIELD) f = field[(size_t)i * g.W + x];
+            else if (src == SRC_SCALED) f = get_bit(bits, g.pitch_w, i, x) ? c->scale : -c->scale;
+            else f = exact_phi_smooth(bits, g.pitch_w, g.H, g.W, c->R, c->w64, i, x);
+            const uint32_t ge = f >= 0.0, gt = f > 0.0;
+            pw |= ge << k;
+            mw |= gt << k;
+            if (do_part) {
+              const double I = data_exact(c, i, x);
+              if (ge) { dd_add(ah, al, I); ++na; }
+              else { dd_add(bh, bl, I); ++nb; }
+            }
+          }
+        }
+        const size_t o = (size_t)r * g.pitch_w + x;
+        if (do_part) pbits[o] = pw;
+        if (write_mask_only) {
+          mbits[o] = mw;
+        } else if (do_ckpt) {
+          mm += __popc(mbits[o] ^ mw);
+          mbits[o] = mw;
+        }
+      }
+    }
+    // fixed-order CTA reduction (double-double)
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    for (int o = 16; o > 0; o >>= 1) {
+      double h2 = __shfl_xor_sync(0xffffffffu, ah, o), l2 = __shfl_xor_sync(0xffffffffu, al, o);
+      dd_add_dd(ah, al, h2, l2);
+      h2 = __shfl_xor_sync(0xffffffffu, bh, o);
+      l2 = __shfl_xor_sync(0xffffffffu, bl, o);
+      dd_add_dd(bh, bl, h2, l2);
+      na += __shfl_xor_sync(0xffffffffu, na, o);
+      nb += __shfl_xor_sync(0xffffffffu, nb, o);
+      mm += __shfl_xor_sync(0xffffffffu, mm, o);
+    }
+    __syncthreads();
+    if (lane == 0) {
+      s_warp[warp].a_hi = ah; s_warp[warp].a_lo = al;
+      s_warp[warp].b_hi = bh; s_warp[warp].b_lo = bl;
+      s_warp[warp].n_a = na; s_warp[warp].n_b = nb; s_warp[warp].mism = mm;
+    }
+    __syncthreads();
+    if (threadIdx.x == 0) {
+      TilePartial t{};
+      for (int w = 0; w < (int)(blockDim.x >> 5); ++w) {
+        dd_add_dd(t.a_hi, t.a_lo, s_warp[w].a_hi, s_warp[w].a_lo);
+        dd_add_dd(t.b_hi, t.b_lo, s_warp[w].b_hi, s_warp[w].b_lo);
+        t.n_a += s_warp[w].n_a;
+        t.n_b += s_warp[w].n_b;
+        t.mism += s_warp[w].mism;
+      }
+      part[tile] = t;
+    }
+  }
+}
+
+__global__ void __launch_bounds__(kThreads) k_finalize(const TilePartial* part, int n, Scalars* sc,
+                                                       int delta, int region, int ckpt,
+                                                       long long iter) {
+  finalize_cta(part, n, sc, delta != 0, region != 0, ckpt != 0, iter);
+}
+
+// image statistics: min, max, max|.| (order-preserving integer atomics)
+__device__ __forceinline__ long long dkey(double v) {
+  long long b = __double_as_longlong(v);
+  return b ^ ((b >> 63) & 0x7fffffffffffffffLL);
+}
+__device__ __forceinline__ double dkey_inv(long long k) {
+  return __longlong_as_double(k ^ ((k >> 63) & 0x7fffffffffffffffLL));
+}
+__global__ void k_minmax(const float* __restrict__ d32, const double* __restrict__ d64, int H, int W,
+                         long long pitch, long long* keys /* [min, max, absmax] */) {
+  long long kmin = LLONG_MAX, kmax = LLONG_MIN, kabs = LLONG_MIN;
+  const long long n = (long long)H * W;
+  for (long long q = (long long)blockIdx.x * blockDim.x + threadIdx.x; q < n;
+       q += (long long)gridDim.x * blockDim.x) {
+    const long long i = q / W, x = q - i * W;
+    const double v = d64 ? d64[i * pitch + x] : (double)d32[i * pitch + x];
+    const long long k = dkey(v), ka = dkey(fabs(v));
+    kmin = k < kmin ? k : kmin;
+    kmax = k > kmax ? k : kmax;
+    kabs = ka > kabs ? ka : kabs;
+  }
+  for (int o = 16; o > 0; o >>= 1) {
+    long long a = __shfl_xor_sync(0xffffffffu, kmin, o);
+    long long b = __shfl_xor_sync(0xffffffffu, kmax, o);
+    long long e = __shfl_xor_sync(0xffffffffu, kabs, o);
+    kmin = a < kmin ? a : kmin;
+    kmax = b > kmax ? b : kmax;
+    kabs = e > kabs ? e : kabs;
+  }
+  if ((threadIdx.x & 31) == 0) {
+    atomicMin(&keys[0], kmin);
+    atomicMax(&keys[1], kmax);
+    atomicMax(&keys[2], kabs);
+  }
+}
+__global__ void k_store_minmax(const long long* keys, Scalars* sc) {
+  sc->img_min = dkey_inv(keys[0]);
+  sc->img_max = dkey_inv(keys[1]);
+  sc->img_absmax = dkey_inv(keys[2]);
+}
+
+// float64 image -> fp32 plane (+ flag when fp32 is not exact)
+__global__ void k_to_f32(const double* __restrict__ in, float* __restrict__ out, int H, int W,
+                         long long pitch, int* inexact) {
+  const int x = blockIdx.x * blockDim.x + threadIdx.x;
+  const int i = blockIdx.y;
+  if (x >= W) return;
+  const double v = in[(size_t)i * W + x];
+  const float f = (float)v;
+  out[(size_t)i * pitch + x] = f;
+  if ((double)f != v) *inexact = 1;
+}
+// float64 dense -> pitched float64
+__global__ void k_pitch64(const double* __restrict__ in, double* __restrict__ out, int H, int W,
+                          long long pitch) {
+  const int x = blockIdx.x * blockDim.x + threadIdx.x;
+  const int i = blockIdx.y;
+  if (x >= W) return;
+  out[(size_t)i * pitch + x] = in[(size_t)i * W + x];
+}
+// pitched fp32 plane -> dense float64
+__global__ void k_widen(const float* __restrict__ in, double* __restrict__ out, int H, int W,
+                        long long pitch) {
+  const int x = blockIdx.x * blockDim.x + threadIdx.x;
+  const int i = blockIdx.y;
+  if (x >= W) return;
+  out[(size_t)i * W + x] = (double)in[(size_t)i * pitch + x];
+}
+
+// Even-odd seed rasterization at pixel centres (grid.py:58-93), union of
+// polygons; emits the state bits of phi0 = where(inside, s, -s) and counts
+// the inside pixels (DegenerateSeedError check).
+__global__ void k_rasterize(const double* __restrict__ xy, const long long* __restrict__ offs,
+                            int n_polys, int inside_sign, uint32_t* bits, signed char* signs,
+                            RunGeom g, unsigned long long* n_inside) {
+  const int x = blockIdx.x * blockDim.x + threadIdx.x;
+  const int r = blockIdx.y;
+  unsigned long long cnt = 0;
+  if (x < g.pitch_w) {
+    uint32_t w = 0u;
+    if (x < g.W) {
+      const double cx = dadd((double)x, 0.5);
+      for (int k = 0; k < 32; ++k) {
+        const int i = r * 32 + k;
+        if (i >= g.H) break;
+        const double cy = dadd((double)i, 0.5);
+        bool inside = false;
+        for (int p = 0; p < n_polys && !inside; ++p) {
+          const long long a = offs[p], e = offs[p + 1];
+          const long long nv = e - a;
+          bool in_p = false;
+          for (long long q = 0; q < nv; ++q) {
+            const double x1 = xy[2 * (a + q)], y1 = xy[2 * (a + q) + 1];
+            const long long q2 = (q + 1) % nv;
+            const double x2 = xy[2 * (a + q2)], y2 = xy[2 * (a + q2) + 1];
+            if (y1 == y2) continue;
+            const bool crosses = (y1 > cy) != (y2 > cy);
+            const double x_hit = dadd(x1, ddiv(dmul(dsub(cy, y1), dsub(x2, x1)), dsub(y2, y1)));
+            if (crosses && (cx < x_hit)) in_p = !in_p;
+          }
+          inside = in_p;
+        }
+        cnt += inside;
+        const bool pos = inside ? (inside_sign > 0) : (inside_sign < 0);
+        w |= (pos ? 1u : 0u) << k;
+        if (signs) signs[(size_t)i * g.W + x] = pos ? 1 : -1;
+      }
+    }
+    if (bits) bits[(size_t)r * g.pitch_w + x] = w;
+  }
+  for (int o = 16; o > 0; o >>= 1) cnt += __shfl_xor_sync(0xffffffffu, cnt, o);
+  if ((threadIdx.x & 31) == 0 && cnt) atomicAdd(n_inside, cnt);
+}
+
+// checkpoint-style mask bits -> host layout.  mask = (phi > 0) for
+// inside_sign > 0, else (phi <= 0) (engine.py:256-259).
+__global__ void k_mask_u8(const uint32_t* __restrict__ mbits, RunGeom g, int invert,
+                          unsigned char* out) {
+  const int x = blockIdx.x * blockDim.x + threadIdx.x;
+  const int i = blockIdx.y;
+  if (x >= g.W) return;
+  const int b = get_bit(mbits, g.pitch_w, i, x);
+  out[(size_t)i * g.W + x] = (unsigned char)(invert ? !b : b);
+}
+__global__ void k_mask_packed(const uint32_t* __restrict__ mbits, RunGeom g, int invert,
+                              unsigned char* out, long long nbytes) {
+  const long long q = (long long)blockIdx.x * blockDim.x + threadIdx.x;
+  if (q >= nbytes) return;
+  const long long npx = (long long)g.H * g.W;
+  unsigned v = 0;
+  for (int k = 0; k < 8; ++k) {
+    const long long f = q * 8 + k;
+    unsigned bit = 0;
+    if (f < npx) {
+      const int i = (int)(f / g.W), x = (int)(f - (long long)i * g.W);
+      bit = get_bit(mbits, g.pitch_w, i, x);
+      if (invert) bit ^= 1u;
+    }
+    v |= bit << (7 - k);
+  }
+  out[q] = (unsigned char)v;
+}
+
+__global__ void k_bits_differ(const double* a, const double* b, long long n, int* ne) {
+  long long k = (long long)blockIdx.x * blockDim.x + threadIdx.x;
+  bool d = false;
+  for (; k < n; k += (long long)gridDim.x * blockDim.x)
+    d |= __double_as_longlong(a[k]) != __double_as_longlong(b[k]);
+  if (__any_sync(0xffffffffu, d) && (threadIdx.x & 31) == 0) *ne = 1;
+}
+
+// dense region sums over {phi >= 0} / {phi < 0} (grid.py:112-117), per-block
+// double-double partials
+__global__ void k_region_sums(const double* __restrict__ img, const double* __restrict__ phi,
+                              long long n, TilePartial* part) {
+  __shared__ TilePartial s_warp[32];
+  double ah = 0, al = 0, bh = 0, bl = 0;
+  long long na = 0, nb = 0;
+  for (long long k = (long long)blockIdx.x * blockDim.x + threadIdx.x; k < n;
+       k += (long long)gridDim.x * blockDim.x) {
+    if (phi[k] >= 0.0) { dd_add(ah, al, img[k]); ++na; }
+    else { dd_add(bh, bl, img[k]); ++nb; }
+  }
+  for (int o = 16; o > 0; o >>= 1) {
+    double h2 = __shfl_xor_sync(0xffffffffu, ah, o), l2 = __shfl_xor_sync(0xffffffffu, al, o);
+    dd_add_dd(ah, al, h2, l2);
+    h2 = __shfl_xor_sync(0xffffffffu, bh, o);
+    l2 = __shfl_xor_sync(0xffffffffu, bl, o);
+    dd_add_dd(bh, bl, h2, l2);
+    na += __shfl_xor_sync(0xffffffffu, na, o);
+    nb += __shfl_xor_sync(0xffffffffu, nb, o);
+  }
+  const int warp = threadIdx.x >> 5;
+  if ((threadIdx.x & 31) == 0) {
+    s_warp[warp].a_hi = ah; s_warp[warp].a_lo = al;
+    s_warp[warp].b_hi = bh; s_warp[warp].b_lo = bl;
+    s_warp[warp].n_a = na; s_warp[warp].n_b = nb;
+  }
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    TilePartial t{};
+    for (int w = 0; w < (int)(blockDim.x >> 5); ++w) {
+      dd_add_dd(t.a_hi, t.a_lo, s_warp[w].a_hi, s_warp[w].a_lo);
+      dd_add_dd(t.b_hi, t.b_lo, s_warp[w].b_hi, s_warp[w].b_lo);
+      t.n_a += s_warp[w].n_a;
+      t.n_b += s_warp[w].n_b;
+    }
+    part[blockIdx.x] = t;
+  }
+}
+
+}  // namespace lse
