@@ -7,7 +7,7 @@ LIB := paper_1409_7474_b200/_lib/liblse_b200.so
 SRC := paper_1409_7474_b200/csrc/lse_api.cu
 HDR := $(wildcard paper_1409_7474_b200/csrc/*.cuh) include/lse_b200.h
 
-all: $(LIB)
+all: $(LIB) oracle
 
 $(LIB): $(SRC) $(HDR)
 	@mkdir -p $(dir $@)

@@ -1,0 +1,365 @@
+#!/usr/bin/env python
+"""Benchmark of the fused LSE iteration on B200 (BASELINE.json metric).
+
+Workload (BASELINE.json configs[4], SURVEY.md section 8d "C5"): one
+32768 x 32768 float32 panchromatic scene (1.07 Gpx) with 20000 seeded
+rectangles, region-based LSE (R_Td), Gaussian sigma 1.5 (9x9, radius 4),
+dt = 15, 500 fixed iterations (conv_check_every = 501), seed box
+[2048, 30720]^2.  Synthetic data (seeded numpy PCG64), inputs larger than L2.
+
+One *step* = one complete extraction job: seed rasterization + partition
+init + 500 iterations, inputs resident in HBM (`value`); `e2e` repeats the
+job through the C ABI with host buffers: pinned H2D of the image each step,
+device work, D2H of the packed object mask.
+
+Metric: Gpixel-iterations/s (whole job, all ranks).  Roofline: canonical
+algorithmic bytes of one iteration (read I 4 B + read phi 4 B
++ write phi 4 B = 12 B/px-it) over the measured device time of one
+iteration's two kernels (k_update + k_partition), against the measured HBM
+copy bandwidth in MEASURED_PEAKS.json.  The bit-state design actually moves
+~4.3 B/px-it; both fractions are reported.
+
+`--impl reference` times the CPU restatement of the reference loop
+(oracle/lse_oracle.c, all host threads, bit-exact to the reference) on a
+bounded sample of the same workload.
+"""
+
+from __future__ import annotations
+
+import argparse
+import ctypes as C
+import json
+import os
+import statistics
+import subprocess
+import sys
+import tempfile
+import time
+
+import numpy as np
+
+REPO = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, REPO)
+
+HBM_FALLBACK_GBS = 6650.0
+
+
+def parse():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=3)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--impl", choices=["b200", "reference"], default="b200")
+    ap.add_argument("--size", type=int, default=32768, help="scene side (C5: 32768)")
+    ap.add_argument("--iters", type=int, default=500)
+    ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--cpu-seconds", type=float, default=12.0)
+    return ap.parse_args()
+
+
+def dist_env():
+    ws = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    return ws, rank, local
+
+
+def measured_peaks():
+    p = os.path.join(REPO, "MEASURED_PEAKS.json")
+    try:
+        with open(p) as f:
+            d = json.load(f)
+        return float(d["hbm_gbs"]), "measured"
+    except Exception:
+        return HBM_FALLBACK_GBS, "fallback"
+
+
+class ClockSampler:
+    """nvidia-smi clocks/throttle reasons sampled during the timed region."""
+
+    FIELDS = ("clocks.sm,clocks.max.sm,clocks_event_reasons.hw_slowdown,"
+              "clocks_event_reasons.hw_thermal_slowdown,"
+              "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, dev):
+        self.dev = dev
+        self.proc = None
+        self.f = None
+
+    def start(self):
+        self.f = tempfile.NamedTemporaryFile("w+", suffix=".csv", delete=False)
+        try:
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", "-i", str(self.dev), f"--query-gpu={self.FIELDS}",
+                 "--format=csv,noheader,nounits", "-lms", "200"],
+                stdout=self.f, stderr=subprocess.DEVNULL)
+        except Exception:
+            self.proc = None
+
+    def stop(self):
+        if self.proc is None:
+            return None
+        self.proc.terminate()
+        try:
+            self.proc.wait(timeout=5)
+        except Exception:
+            self.proc.kill()
+        self.f.flush()
+        rows = []
+        with open(self.f.name) as fh:
+            for line in fh:
+                parts = [x.strip() for x in line.split(",")]
+                if len(parts) != 6:
+                    continue
+                try:
+                    rows.append((float(parts[0]), float(parts[1]), parts[2:]))
+                except ValueError:
+                    continue
+        os.unlink(self.f.name)
+        if not rows:
+            return None
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        reasons = sorted({names[k] for _, _, r in rows for k, v in enumerate(r)
+                          if v.lower().startswith("active")})
+        loaded = [s for s, _, _ in rows if s > 200] or [s for s, _, _ in rows]
+        return {"sm_mhz": statistics.median(loaded), "sm_max_mhz": max(m for _, m, _ in rows),
+                "reasons": reasons, "samples": len(rows)}
+
+
+# ----------------------------------------------------------------- CPU side
+def cpu_oracle_rate(seconds, size=2048):
+    """The reference loop restated in C (bit-exact to lsekit), all host threads,
+    on a C5-density crop; returns (Mpx-it/s, cores, sample description)."""
+    sys.path.insert(0, os.path.join(REPO, "oracle"))
+    import lse_oracle as O
+    import lse_oracle_c as OC
+    from paper_1409_7474_b200 import scenes
+    sc = scenes.config5_crop(size, 10 ** 6)
+    img = sc.image.astype(np.float64)
+    phi0 = O.rasterize_seeds(list(sc.polygons), sc.inside_sign, size, size)
+    p = O.OracleParams(model="region", dt=15.0, sigma2=1.5, ts_reg=9, max_iters=10 ** 6,
+                       conv_check_every=10 ** 6 + 1)
+    r = OC.COracleRun(img, phi0, p, O.gaussian_weights)
+    r.advance(1)                              # warm-up (allocations, page faults)
+    t0 = time.perf_counter()
+    r.advance(2)
+    per_it = (time.perf_counter() - t0) / 2
+    n = int(max(2, min(200, seconds / max(per_it, 1e-6))))
+    t0 = time.perf_counter()
+    r.advance(n)
+    dt = time.perf_counter() - t0
+    rate = size * size * n / dt / 1e6
+    return rate, r.threads(), f"C5-density crop {size}x{size}, {n} iterations, {dt:.1f} s"
+
+
+def run_reference(args, rank):
+    """--impl reference: CPU restatement of the reference path, bounded sample."""
+    if rank != 0:
+        return
+    sys.path.insert(0, os.path.join(REPO, "oracle"))
+    import lse_oracle as O
+    import lse_oracle_c as OC
+    from paper_1409_7474_b200 import scenes
+    size = 2048
+    sc = scenes.config5_crop(size, 10 ** 6)
+    img = sc.image.astype(np.float64)
+    phi0 = O.rasterize_seeds(list(sc.polygons), sc.inside_sign, size, size)
+    p = O.OracleParams(model="region", dt=15.0, sigma2=1.5, ts_reg=9, max_iters=10 ** 6,
+                       conv_check_every=10 ** 6 + 1)
+    r = OC.COracleRun(img, phi0, p, O.gaussian_weights)
+    its = 5
+    for _ in range(args.warmup):
+        r.advance(its)
+    t0 = time.perf_counter()
+    for _ in range(args.steps):
+        r.advance(its)
+    dt = time.perf_counter() - t0
+    val = size * size * its * args.steps / dt / 1e9
+    line = {
+        "impl": "reference", "metric": "Gpixel-iterations/s of the LSE update", "value": val,
+        "unit": "Gpix-it/s", "n_gpus": args.gpus, "steps": args.steps, "warmup": args.warmup,
+        "ms_per_step": dt / args.steps * 1e3, "higher_is_better": True, "scaling": "weak",
+        "vs_baseline": None, "dtype": "f64", "data": "synthetic (seeded C5 statistics)",
+        "config": {"workload": "C5 region LSE, sigma 1.5 (9x9), dt 15 -- CPU sample",
+                   "sample": f"{size}x{size} C5-density crop, {its} iterations per step"},
+        "cpu_baseline": {"value": val, "unit": "Gpix-it/s", "cores": r.threads(), "kind": "port",
+                         "sample": f"{size}x{size} crop x {its} its/step x {args.steps} steps"},
+        "e2e": {"value": val, "unit": "Gpix-it/s", "h2d_bytes_per_step": 0,
+                "d2h_bytes_per_step": 0},
+    }
+    print(json.dumps(line), flush=True)
+
+
+# ----------------------------------------------------------------- GPU side
+def main():
+    args = parse()
+    ws, rank, local = dist_env()
+    if args.impl == "reference":
+        return run_reference(args, rank)
+
+    import torch
+    torch.cuda.set_device(local)
+    dist = None
+    if ws > 1:
+        import torch.distributed as dist
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+
+    from paper_1409_7474_b200 import _native as N
+    from paper_1409_7474_b200 import scenes
+    from paper_1409_7474_b200.engine import _native_params
+    from paper_1409_7474_b200 import default_params, ModelKind
+
+    n_rects = max(1, int(round(20000 * (args.size / 32768.0) ** 2)))
+    t_gen = time.perf_counter()
+    sc = scenes.config5(size=args.size, n_rects=n_rects, iters=args.iters, seed_offset=rank)
+    t_gen = time.perf_counter() - t_gen
+    H, W = sc.image.shape
+    npx = H * W
+    prm = default_params(ModelKind.REGION, **sc.params)
+    p, keep_w = _native_params(prm)
+
+    # pinned host copies for the end-to-end leg
+    img_pin = torch.empty((H, W), dtype=torch.float32, pin_memory=True)
+    img_pin.numpy()[...] = sc.image
+    nbytes_mask = (npx + 7) // 8
+    mask_pin = torch.empty(nbytes_mask, dtype=torch.uint8, pin_memory=True)
+    del sc.image
+
+    polys = np.ascontiguousarray(np.concatenate(sc.polygons), dtype=np.float64)
+    counts = np.ascontiguousarray([len(q) for q in sc.polygons], dtype=np.int64)
+    init = N.LsePhi0()
+    init.kind = N.LSE_PHI0_POLYGONS
+    init.poly_xy = N.dptr(polys)
+    init.poly_counts = counts.ctypes.data_as(N._llp)
+    init.n_polys = len(counts)
+    init.inside_sign = sc.inside_sign
+
+    h = C.c_void_p()
+    N.check(N.lib.lse_run_create(C.byref(h), C.byref(p), H, W,
+                                 C.c_void_p(img_pin.data_ptr()), 1, C.byref(init)))
+    st = N.LseStatus()
+
+    def job():
+        N.check(N.lib.lse_run_set_state(h, C.byref(init)))
+        N.check(N.lib.lse_run_advance(h, args.iters, C.byref(st)))
+        assert st.iteration == args.iters, st.iteration
+
+    def job_e2e():
+        N.check(N.lib.lse_run_load_image(h, C.c_void_p(img_pin.data_ptr()), 1))
+        job()
+        N.check(N.lib.lse_run_read_mask(h, C.cast(C.c_void_p(mask_pin.data_ptr()),
+                                                  C.POINTER(C.c_ubyte)), sc.inside_sign, 1))
+
+    def barrier():
+        if dist is not None:
+            dist.barrier()
+        torch.cuda.synchronize()
+
+    def max_over_ranks(x):
+        if dist is None:
+            return x
+        t = torch.tensor([x], dtype=torch.float64, device="cuda")
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        return float(t.item())
+
+    for _ in range(args.warmup):
+        job()
+    # ---- timed region: inputs resident in HBM
+    clocks = ClockSampler(local)
+    barrier()
+    clocks.start()
+    N.check(N.lib.lse_run_set_profiling(h, 1))
+    launches0 = N.lib.lse_launch_count()
+    N.check(N.lib.lse_run_begin_timing(h))
+    for _ in range(args.steps):
+        job()
+    ms = C.c_double()
+    N.check(N.lib.lse_run_end_timing(h, C.byref(ms)))
+    launches = N.lib.lse_launch_count() - launches0
+    barrier()
+    clk = clocks.stop()
+    t_ms = max_over_ranks(ms.value)
+    upd_ms, part_ms = C.c_double(), C.c_double()
+    n_upd, n_part = C.c_longlong(), C.c_longlong()
+    N.check(N.lib.lse_run_kernel_times(h, C.byref(upd_ms), C.byref(n_upd), C.byref(part_ms),
+                                       C.byref(n_part)))
+    N.check(N.lib.lse_run_set_profiling(h, 0))
+    fallbacks = st.exact_fallbacks
+    px_its = npx * args.iters * args.steps * ws
+    value = px_its / (t_ms / 1e3) / 1e9
+
+    # ---- end to end through the C ABI with host buffers
+    e2e = None
+    if not args.no_e2e:
+        for _ in range(1):
+            job_e2e()
+        barrier()
+        N.check(N.lib.lse_run_begin_timing(h))
+        for _ in range(args.steps):
+            job_e2e()
+        N.check(N.lib.lse_run_end_timing(h, C.byref(ms)))
+        barrier()
+        e_ms = max_over_ranks(ms.value)
+        e2e = {"value": px_its / (e_ms / 1e3) / 1e9, "unit": "Gpix-it/s",
+               "h2d_bytes_per_step": npx * 4 + polys.nbytes + counts.nbytes,
+               "d2h_bytes_per_step": nbytes_mask, "ms_per_step": e_ms / args.steps}
+
+    N.lib.lse_run_destroy(h)
+
+    # ---- roofline of one iteration (k_update + k_partition)
+    peak, peak_kind = measured_peaks()
+    t_upd = upd_ms.value / max(1, n_upd.value)
+    t_part = part_ms.value / max(1, n_part.value)
+    t_iter = t_upd + t_part
+    canon = 12.0 * npx
+    actual = (4.0 + 2.0 / 8.0 + 3.0 / 8.0) * npx     # I + b in/out (update) + b, P in/out (partition)
+    traffic = None
+    tp = os.path.join(REPO, "profiles", "traffic_latest.json")
+    if os.path.exists(tp):
+        try:
+            with open(tp) as f:
+                td = json.load(f)
+            if int(td.get("size", 0)) == args.size:
+                traffic = float(td["bytes_per_iteration"])
+        except Exception:
+            traffic = None
+    roof = {"bound": "hbm", "kernel": "k_update + k_partition (one LSE iteration)",
+            "achieved": canon / (t_iter / 1e3) / 1e9 if t_iter > 0 else None,
+            "peak": peak, "unit": "GB/s",
+            "frac": (canon / (t_iter / 1e3) / 1e9) / peak if t_iter > 0 else None,
+            "traffic": traffic, "peak_source": peak_kind,
+            "algorithmic_bytes_per_px_it": 12.0, "actual_bytes_per_px_it": actual / npx,
+            "achieved_actual_gbs": actual / (t_iter / 1e3) / 1e9 if t_iter > 0 else None,
+            "frac_actual": (actual / (t_iter / 1e3) / 1e9) / peak if t_iter > 0 else None,
+            "update_ms": t_upd, "partition_ms": t_part,
+            "update_share_of_iteration": t_upd / t_iter if t_iter > 0 else None}
+
+    cpu = None
+    if rank == 0 and ws == 1 and not args.no_cpu_baseline:
+        rate, cores, sample = cpu_oracle_rate(args.cpu_seconds)
+        cpu = {"value": rate / 1e3, "unit": "Gpix-it/s", "cores": cores, "kind": "port",
+               "sample": sample + " (oracle/lse_oracle.c, bit-exact restatement of lsekit)"}
+
+    if rank == 0:
+        line = {
+            "metric": "Gpixel-iterations/s of the LSE update", "value": value,
+            "unit": "Gpix-it/s", "n_gpus": ws, "steps": args.steps, "warmup": args.warmup,
+            "ms_per_step": t_ms / args.steps, "higher_is_better": True,
+            "scaling": "weak", "vs_baseline": None, "dtype": "f32+f64-guard (bit state)",
+            "data": "synthetic (seeded, BASELINE C5 statistics)",
+            "config": {"workload": f"C5: {H}x{W} region LSE, 20000-rect density, sigma 1.5 "
+                                   f"(9x9), dt 15, {args.iters} fixed iterations per step",
+                       "parallelism": f"replicas x{ws}" if ws > 1 else "single GPU",
+                       "l2": "inputs (4.3 GB image) larger than L2"},
+            "roofline": roof, "cpu_baseline": cpu, "e2e": e2e, "gpu_launches": int(launches),
+            "clocks": clk, "exact_fallbacks": int(fallbacks),
+            "scene_gen_s": round(t_gen, 2),
+        }
+        print(json.dumps(line), flush=True)
+    if dist is not None:
+        dist.destroy_process_group()
+
+
+if __name__ == "__main__":
+    main()

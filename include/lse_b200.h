@@ -125,6 +125,19 @@ int lse_run_read_phi(lse_run* run, double* out);
  * bits, numpy.packbits(mask, axis=None) order (ceil(H*W/8) bytes). */
 int lse_run_read_mask(lse_run* run, unsigned char* out, int inside_sign, int packed);
 
+/* Device-event timing on the run's stream: everything the run enqueues
+ * between begin and end (bench support). */
+int lse_run_begin_timing(lse_run* run);
+int lse_run_end_timing(lse_run* run, double* ms);
+
+/* Run options.  "skip_uniform" (default 1): let the fused kernels copy warp
+ * blocks whose whole stencil window is uniform (exactly unchanged by the
+ * update) instead of recomputing them; 0 forces the dense pass. */
+int lse_run_set_option(lse_run* run, const char* name, long long value);
+
+/* Number of kernel launches this library has issued (process-wide). */
+long long lse_launch_count(void);
+
 /* Device-event timing of the fused kernels (bench/roofline support). */
 int lse_run_set_profiling(lse_run* run, int enabled);
 int lse_run_kernel_times(lse_run* run, double* update_ms, long long* update_launches,

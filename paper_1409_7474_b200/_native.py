@@ -79,6 +79,10 @@ _SIGS = {
     "lse_run_status": (_i, [_vp, C.POINTER(LseStatus)]),
     "lse_run_read_phi": (_i, [_vp, _dp]),
     "lse_run_read_mask": (_i, [_vp, C.POINTER(C.c_ubyte), _i, _i]),
+    "lse_run_begin_timing": (_i, [_vp]),
+    "lse_run_end_timing": (_i, [_vp, _dp]),
+    "lse_launch_count": (_ll, []),
+    "lse_run_set_option": (_i, [_vp, C.c_char_p, _ll]),
     "lse_run_set_profiling": (_i, [_vp, _i]),
     "lse_run_kernel_times": (_i, [_vp, _dp, _llp, _dp, _llp]),
     "lse_run_destroy": (None, [_vp]),

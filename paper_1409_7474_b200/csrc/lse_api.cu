@@ -12,6 +12,7 @@
 #include <cuda_runtime.h>
 
 #include <algorithm>
+#include <atomic>
 #include <climits>
 #include <cmath>
 #include <cstdio>
@@ -42,8 +43,11 @@ int fail(int code, const std::string& msg) {
       return fail(LSE_ERR_CUDA, std::string(#x) + ": " + cudaGetErrorString(e_));        \
   } while (0)
 
+std::atomic<long long> g_launches{0};
+
 #define CKL()                                                                            \
   do {                                                                                   \
+    g_launches.fetch_add(1, std::memory_order_relaxed);                                  \
     cudaError_t e_ = cudaGetLastError();                                                 \
     if (e_ != cudaSuccess)                                                               \
       return fail(LSE_ERR_CUDA, std::string("launch: ") + cudaGetErrorString(e_));       \
@@ -157,6 +161,9 @@ struct lse_run {
   double t_update = 0, t_part = 0;
   long long n_update = 0, n_part = 0;
   int grid_update = 0, grid_part = 0;
+  int skip_uniform = 1;
+  int nchunk = 1, nseg = 1;
+  cudaEvent_t t_begin = nullptr, t_end = nullptr;
 };
 
 namespace {
@@ -175,7 +182,15 @@ FastParams fast_params(lse_run* r) {
   for (int d = 0; d < 8; ++d) P.w32[d] = d <= r->R ? (float)r->h_ctx.w64[d] : 0.f;
   P.dt32 = (float)r->p.dt;
   P.scale32 = (float)r->scale;
+  P.skip_uniform = r->skip_uniform;
+  P.nchunk = r->nchunk;
+  P.nseg = r->nseg;
   return P;
+}
+
+int fast_grid(long long warp_units) {
+  const long long ctas = (warp_units + 3) / 4;
+  return (int)std::max<long long>(1, std::min<long long>(ctas, (long long)num_sms() * 4));
 }
 
 dim3 grid2(int W, int H, int bx = 128) { return dim3((W + bx - 1) / bx, H); }
@@ -254,24 +269,22 @@ int launch_fast_R(lse_run* r, long long it, bool ckpt) {
     e2 = next_event(r);
     cudaEventRecord(e0, r->st);
   }
-  if (r->mode == SRC_SCALED) {
-    if (!r->grid_update) r->grid_update = std::min(r->g.ntiles, num_sms() * 4);
-    k_update<R, MODEL, SRC_SCALED><<<r->grid_update, r->nthr, 0, r->st>>>(P);
-  } else {
-    if (!r->grid_update) r->grid_update = std::min(r->g.ntiles, num_sms() * 4);
-    k_update<R, MODEL, SRC_SMOOTH><<<r->grid_update, r->nthr, 0, r->st>>>(P);
-  }
+  if (!r->grid_update) r->grid_update = fast_grid((long long)r->g.HR * r->nchunk);
+  if (r->mode == SRC_SCALED)
+    k_update<R, MODEL, SRC_SCALED><<<r->grid_update, kThreads, 0, r->st>>>(P);
+  else
+    k_update<R, MODEL, SRC_SMOOTH><<<r->grid_update, kThreads, 0, r->st>>>(P);
   CKL();
   if (r->prof) cudaEventRecord(e1, r->st);
   P.bits_in = r->d_bits[r->cur ^ 1];
-  if (!r->grid_part) r->grid_part = std::min(r->g.ntiles, num_sms() * 4);
+  if (!r->grid_part) r->grid_part = fast_grid((long long)r->g.HR * r->nseg);
   bool launched_part = false;
   if (MODEL == REGION) {
-    if (ckpt) k_partition<R, true, true, false><<<r->grid_part, r->nthr, 0, r->st>>>(P);
-    else k_partition<R, true, false, false><<<r->grid_part, r->nthr, 0, r->st>>>(P);
+    if (ckpt) k_partition<R, true, true, false><<<r->grid_part, kThreads, 0, r->st>>>(P);
+    else k_partition<R, true, false, false><<<r->grid_part, kThreads, 0, r->st>>>(P);
     launched_part = true;
   } else if (ckpt) {
-    k_partition<R, false, true, false><<<r->grid_part, r->nthr, 0, r->st>>>(P);
+    k_partition<R, false, true, false><<<r->grid_part, kThreads, 0, r->st>>>(P);
     launched_part = true;
   }
   CKL();
@@ -362,6 +375,7 @@ int generic_iteration(lse_run* r, long long it, bool reinit_now, bool reg_now, b
   double* out = r->d_F[r->curF ^ 1];
   if (reg_now) {
     k_corr<0><<<grid2(r->W, r->H), 128, 0, r->st>>>(r->d_U, r->d_T, r->H, r->W, r->d_w64, r->R);
+    CKL();
     k_corr<1><<<grid2(r->W, r->H), 128, 0, r->st>>>(r->d_T, out, r->H, r->W, r->d_w64, r->R);
     CKL();
   } else {
@@ -463,7 +477,9 @@ int upload_image(lse_run* r, const void* image, int is_f32) {
     TRY(dalloc(&wpre, wp.size()));
     CK(cudaMemcpyAsync(wpre, wp.data(), wp.size() * sizeof(double), cudaMemcpyHostToDevice, r->st));
     k_corr<0><<<grid2(W, H), 128, 0, r->st>>>(I64, T, H, W, wpre, Rp);
+    CKL();
     k_corr<1><<<grid2(W, H), 128, 0, r->st>>>(T, S, H, W, wpre, Rp);
+    CKL();
     if (!r->d_data64) TRY(dalloc(&r->d_data64, (size_t)pitch * H));
     k_edge_g<<<grid2(W, H), 128, 0, r->st>>>(S, H, W, r->p.edge_gain, r->d_data64, r->d_data32,
                                               pitch);
@@ -478,6 +494,7 @@ int upload_image(lse_run* r, const void* image, int is_f32) {
   long long init[3] = {LLONG_MAX, LLONG_MIN, LLONG_MIN};
   CK(cudaMemcpyAsync(r->d_keys, init, sizeof(init), cudaMemcpyHostToDevice, r->st));
   k_minmax<<<num_sms() * 4, 256, 0, r->st>>>(r->d_data32, r->d_data64, H, W, pitch, r->d_keys);
+  CKL();
   k_store_minmax<<<1, 1, 0, r->st>>>(r->d_keys, r->d_scal);
   CKL();
   CK(cudaMemcpyAsync(r->h_scal, r->d_scal, sizeof(Scalars), cudaMemcpyDeviceToHost, r->st));
@@ -645,6 +662,9 @@ int lse_run_create(lse_run** out, const lse_params* p, long long height, long lo
   r->nthr = (int)std::min<long long>(kThreads, need_thr);
   r->g.ncb = (r->W + kColsPerThread * r->nthr - 1) / (kColsPerThread * r->nthr);
   r->g.ntiles = r->g.HR * r->g.ncb;
+  r->nchunk = (r->W + kChunk - 1) / kChunk;
+  r->nseg = (r->nchunk + kSegChunks - 1) / kSegChunks;
+  const long long nparts = std::max<long long>(r->g.ntiles, (long long)r->g.HR * r->nseg);
   auto cleanup = [&](int rc) {
     lse_run_destroy(r);
     return rc;
@@ -656,7 +676,7 @@ int lse_run_create(lse_run** out, const lse_params* p, long long height, long lo
   if ((rc = dalloc(&r->d_data32, (size_t)r->g.data_pitch * r->H)) ||
       (rc = dalloc(&r->d_bits[0], nbits)) || (rc = dalloc(&r->d_bits[1], nbits)) ||
       (rc = dalloc(&r->d_P, nbits)) || (rc = dalloc(&r->d_M, nbits)) ||
-      (rc = dalloc(&r->d_mask, nbits)) || (rc = dalloc(&r->d_part, r->g.ntiles)) ||
+      (rc = dalloc(&r->d_mask, nbits)) || (rc = dalloc(&r->d_part, nparts)) ||
       (rc = dalloc(&r->d_scal, 1)) || (rc = dalloc(&r->d_lut_t, 512)) ||
       (rc = dalloc(&r->d_lut_s, 512)) || (rc = dalloc(&r->d_ctx, 1)) ||
       (rc = dalloc(&r->d_w64, 32)) || (rc = dalloc(&r->d_keys, 3)) ||
@@ -797,12 +817,12 @@ int lse_run_read_mask(lse_run* r, unsigned char* out, int inside_sign, int packe
     FastParams P = fast_params(r);
     P.bits_in = r->d_bits[r->cur];
     P.mbits = r->d_mask;
-    const int grid = std::min(r->g.ntiles, num_sms() * 4);
+    const int grid = fast_grid((long long)r->g.HR * r->nseg);
     switch (r->R) {
-      case 1: k_partition<1, false, false, true><<<grid, r->nthr, 0, r->st>>>(P); break;
-      case 2: k_partition<2, false, false, true><<<grid, r->nthr, 0, r->st>>>(P); break;
-      case 3: k_partition<3, false, false, true><<<grid, r->nthr, 0, r->st>>>(P); break;
-      case 4: k_partition<4, false, false, true><<<grid, r->nthr, 0, r->st>>>(P); break;
+      case 1: k_partition<1, false, false, true><<<grid, kThreads, 0, r->st>>>(P); break;
+      case 2: k_partition<2, false, false, true><<<grid, kThreads, 0, r->st>>>(P); break;
+      case 3: k_partition<3, false, false, true><<<grid, kThreads, 0, r->st>>>(P); break;
+      case 4: k_partition<4, false, false, true><<<grid, kThreads, 0, r->st>>>(P); break;
     }
     CKL();
   } else {
@@ -827,6 +847,36 @@ int lse_run_read_mask(lse_run* r, unsigned char* out, int inside_sign, int packe
   }
   CK(cudaStreamSynchronize(r->st));
   cudaFree(d_out);
+  return LSE_OK;
+}
+
+long long lse_launch_count(void) { return g_launches.load(); }
+
+int lse_run_set_option(lse_run* r, const char* name, long long value) {
+  if (!r || !name) return fail(LSE_ERR_ARG, "null argument");
+  if (!std::strcmp(name, "skip_uniform")) {
+    r->skip_uniform = value != 0;
+    return LSE_OK;
+  }
+  return fail(LSE_ERR_ARG, std::string("unknown option ") + name);
+}
+
+int lse_run_begin_timing(lse_run* r) {
+  if (!r) return fail(LSE_ERR_ARG, "null run");
+  if (!r->t_begin) CK(cudaEventCreate(&r->t_begin));
+  if (!r->t_end) CK(cudaEventCreate(&r->t_end));
+  CK(cudaEventRecord(r->t_begin, r->st));
+  return LSE_OK;
+}
+
+int lse_run_end_timing(lse_run* r, double* ms) {
+  if (!r || !ms) return fail(LSE_ERR_ARG, "null argument");
+  if (!r->t_begin || !r->t_end) return fail(LSE_ERR_ARG, "timing not started");
+  CK(cudaEventRecord(r->t_end, r->st));
+  CK(cudaEventSynchronize(r->t_end));
+  float f = 0.f;
+  CK(cudaEventElapsedTime(&f, r->t_begin, r->t_end));
+  *ms = f;
   return LSE_OK;
 }
 
@@ -858,6 +908,8 @@ void lse_run_destroy(lse_run* r) {
     if (q) cudaFree(q);
   if (r->h_scal) cudaFreeHost(r->h_scal);
   for (auto e : r->evpool) cudaEventDestroy(e);
+  if (r->t_begin) cudaEventDestroy(r->t_begin);
+  if (r->t_end) cudaEventDestroy(r->t_end);
   if (r->st) cudaStreamDestroy(r->st);
   delete r;
 }
@@ -895,6 +947,7 @@ int conv_device(const double* d_in, double* d_tmp, double* d_out, int H, int W, 
   TRY(dbuf<double>(dw, taps.size()));
   CK(cudaMemcpy(dw.p, taps.data(), taps.size() * sizeof(double), cudaMemcpyHostToDevice));
   k_corr<0><<<grid2(W, H), 128>>>(d_in, d_tmp, H, W, (double*)dw.p, ts / 2);
+  CKL();
   k_corr<1><<<grid2(W, H), 128>>>(d_tmp, d_out, H, W, (double*)dw.p, ts / 2);
   CKL();
   CK(cudaDeviceSynchronize());
@@ -916,8 +969,11 @@ int region_scalars(const double* d_img, const double* d_phi, int H, int W, Scala
   long long init[3] = {LLONG_MAX, LLONG_MIN, LLONG_MIN};
   CK(cudaMemcpy(keys.p, init, sizeof(init), cudaMemcpyHostToDevice));
   k_minmax<<<num_sms() * 4, 256>>>(nullptr, d_img, H, W, W, (long long*)keys.p);
+  CKL();
   k_store_minmax<<<1, 1>>>((long long*)keys.p, d_sc);
+  CKL();
   k_region_sums<<<blocks, 256>>>(d_img, d_phi, n, (TilePartial*)part.p);
+  CKL();
   k_finalize<<<1, kThreads>>>((TilePartial*)part.p, blocks, d_sc, 0, 1, 0, 0);
   CKL();
   CK(cudaMemcpy(h_sc, d_sc, sizeof(Scalars), cudaMemcpyDeviceToHost));

@@ -54,7 +54,13 @@ struct FastParams {
   float dt32;
   float scale32;
   long long iter;            // iteration produced by this launch
+  int skip_uniform;          // skip warp blocks whose whole stencil window is uniform
+  int nchunk;                // 256-column chunks per word-row
+  int nseg;                  // partition segments (kSegChunks chunks) per word-row
 };
+
+constexpr int kChunk = 256;      // columns per warp chunk (32 lanes x 8 columns)
+constexpr int kSegChunks = 16;   // chunks per partition segment (partial granularity)
 
 __device__ __forceinline__ double data_exact(const ExactCtx* c, int i, int x) {
   size_t o = (size_t)i * c->data_pitch + x;
@@ -107,10 +113,11 @@ __device__ __forceinline__ uint32_t row_valid_mask(int i, int H) {
   return ((2u << hi) - 1u) & ~((1u << lo) - 1u);
 }
 
-// One row of phi for NOUT consecutive columns starting at t-index R (the
-// t array covers NOUT + 2R columns).  INT: every window row/column lies in
-// the image, so the exact-rounded LUT applies; otherwise zero padding
-// (b = 0 outside) via the weight-sum LUT: t = 2*S(set & valid) - S(valid).
+// One row of phi for NOUT consecutive columns; the t array covers NOUT + 2R
+// columns and phi column c is centred on t index c + R.  INT: all window rows
+// and columns lie in the image, so the exact-rounded LUT applies; otherwise
+// zero padding (b = 0 outside) via the weight-sum LUT:
+// t = 2*S(set & valid) - S(valid).
 template <int R, int SRC, bool INT, int NT, int NOUT>
 __device__ __forceinline__ void phi_row(const FastParams& P, const uint32_t (&win)[NT],
                                         const uint32_t (&cm)[NT], int m0, int i,
@@ -131,12 +138,9 @@ __device__ __forceinline__ void phi_row(const FastParams& P, const uint32_t (&wi
   float t[NT];
 #pragma unroll
   for (int j = 0; j < NT; ++j) {
-    uint32_t p = (win[j] >> m0) & PM;
-    if (INT) {
-      t[j] = s_lt[p];
-    } else {
-      t[j] = fmaf(2.f, s_ls[p & vr & cm[j]], cm[j] ? -Lv : 0.f);
-    }
+    const uint32_t p = (win[j] >> m0) & PM;
+    if (INT) t[j] = s_lt[p];
+    else t[j] = fmaf(2.f, s_ls[p & vr & cm[j]], cm[j] ? -Lv : 0.f);
   }
 #pragma unroll
   for (int c = 0; c < NOUT; ++c) {
@@ -152,8 +156,8 @@ __device__ __forceinline__ void load_data_row(const FastParams& P, int i, int x0
   if (i >= P.g.H) return;
   const float* rowp = P.data32 + (size_t)i * P.g.data_pitch + x0;
   if (INT) {
-    float4 a = __ldcs(reinterpret_cast<const float4*>(rowp));
-    float4 b = __ldcs(reinterpret_cast<const float4*>(rowp) + 1);
+    const float4 a = __ldcs(reinterpret_cast<const float4*>(rowp));
+    const float4 b = __ldcs(reinterpret_cast<const float4*>(rowp) + 1);
     d[0] = a.x; d[1] = a.y; d[2] = a.z; d[3] = a.w;
     d[4] = b.x; d[5] = b.y; d[6] = b.z; d[7] = b.w;
   } else {
@@ -162,129 +166,102 @@ __device__ __forceinline__ void load_data_row(const FastParams& P, int i, int x0
   }
 }
 
+__device__ __forceinline__ float sqrt_approx(float x) {
+  float y;
+  asm("sqrt.approx.f32 %0, %1;" : "=f"(y) : "f"(x));
+  return y;
+}
+
+// state words of column xc in word-row wr (0 outside the image)
+template <bool INT>
+__device__ __forceinline__ uint32_t word_at(const FastParams& P, int wr, int xc) {
+  if (!INT && (wr < 0 || wr >= P.g.HR || xc < 0 || xc >= P.g.W)) return 0u;
+  return __ldg(&P.bits_in[(size_t)wr * P.g.pitch_w + xc]);
+}
+
 // ---------------------------------------------------------------- update
+// One lane: columns x0..x0+7 of word-row r (32 rows).  phi rows -1..32 are
+// rebuilt from the bit state (t columns x0-R-1 .. x0+8+R); three phi rows
+// are kept in registers while walking down the rows.
 template <int R, int MODEL, int SRC, bool INT>
-__device__ __forceinline__ void update_tile(const FastParams& P, const uint32_t (*sw)[kSpanMax],
-                                            const float* s_lt, const float* s_ls, int r, int x0,
-                                            int sbase, float A, float B, float eps_u) {
+__device__ __forceinline__ void update_block(const FastParams& P, const float* s_lt,
+                                             const float* s_ls, int r, int x0, float A, float B,
+                                             float eps_u, const uint32_t (&prev)[8 + 2 * (R + 1)],
+                                             const uint32_t (&cur)[8 + 2 * (R + 1)]) {
   constexpr int NT = kColsPerThread + 2 * (R + 1);
   const int H = P.g.H, W = P.g.W;
   const int y0 = r * 32;
-  uint32_t cm[NT];
+  const float hdt = 0.5f * P.dt32;        // h below is 2|grad phi|
+  uint32_t cm[NT], win[NT];
 #pragma unroll
   for (int j = 0; j < NT; ++j) {
-    int xc = x0 - (R + 1) + j;
+    const int xc = x0 - (R + 1) + j;
     cm[j] = (INT || (xc >= 0 && xc < W)) ? 0xffffffffu : 0u;
+    win[j] = __funnelshift_r(prev[j], cur[j], 31 - R);   // base row y0-1-R
   }
-  uint32_t win[NT];
-  float ra[10], rb[10], rc[10];
-  float dcur[8], dnext[8];
+  float pm[10], p0[10], pn[10], dcur[8], dnext[8];
   uint32_t ow[8];
 #pragma unroll
   for (int c = 0; c < 8; ++c) { ow[c] = 0u; dcur[c] = 0.f; dnext[c] = 0.f; }
-
-  // u on row i from phi rows i-1 (pm), i (p0), i+1 (pp); bit k of the words
-  auto u_row = [&](int k, const float (&pm)[10], const float (&p0)[10], const float (&pp)[10],
-                   const float (&d)[8]) {
-    const int i = y0 + k;
-    if (i >= H) return;
-    uint32_t fb = 0u;
-#pragma unroll
-    for (int c = 0; c < 8; ++c) {
-      const int x = x0 + c;
-      float dx, dy;
-      if (INT) {
-        dx = p0[c + 2] - p0[c];
-        dy = pp[c + 1] - pm[c + 1];
-      } else {
-        if (x >= W) continue;
-        dx = (x == 0) ? 2.f * (p0[c + 2] - p0[c + 1])
-                      : (x == W - 1) ? 2.f * (p0[c + 1] - p0[c]) : (p0[c + 2] - p0[c]);
-        dy = (i == 0) ? 2.f * (pp[c + 1] - p0[c + 1])
-                      : (i == H - 1) ? 2.f * (p0[c + 1] - pm[c + 1]) : (pp[c + 1] - pm[c + 1]);
-      }
-      float s2 = fmaf(dx, dx, dy * dy);
-      float hg = 0.5f * s2 * rsqrtf(fmaxf(s2, 1e-30f));
-      float vf = (MODEL == REGION) ? fmaf(A, d[c], B) : d[c];
-      float u = fmaf(P.dt32, vf * hg, p0[c + 1]);
-      ow[c] |= (u > 0.f ? 1u : 0u) << k;
-      if (fabsf(u) <= eps_u) fb |= 1u << c;
-    }
-    while (fb) {
-      const int c = __ffs(fb) - 1;
-      fb &= fb - 1;
-      double ue = exact_u(P.ctx, P.bits_in, SRC, i, x0 + c);
-      ow[c] = (ow[c] & ~(1u << k)) | ((ue > 0.0 ? 1u : 0u) << k);
-    }
-  };
-
-  // ---- rows -1 .. 15 of phi: window base row y0-1-R
-#pragma unroll
-  for (int j = 0; j < NT; ++j) win[j] = __funnelshift_r(sw[0][sbase + j], sw[1][sbase + j], 31 - R);
-  phi_row<R, SRC, INT, NT, 10>(P, win, cm, 0, y0 - 1, s_lt, s_ls, ra);
-  phi_row<R, SRC, INT, NT, 10>(P, win, cm, 1, y0, s_lt, s_ls, rb);
+  phi_row<R, SRC, INT, NT, 10>(P, win, cm, 0, y0 - 1, s_lt, s_ls, pm);
+  phi_row<R, SRC, INT, NT, 10>(P, win, cm, 1, y0, s_lt, s_ls, p0);
   load_data_row<INT>(P, y0, x0, dcur);
-  // three-way register rotation: (ra, rb, rc) = rows (k-1, k, k+1)
-  int k = 0;
 #pragma unroll 1
-  for (; k + 3 <= 15; k += 3) {
-    load_data_row<INT>(P, y0 + k + 1, x0, dnext);
-    phi_row<R, SRC, INT, NT, 10>(P, win, cm, k + 2, y0 + k + 1, s_lt, s_ls, rc);
-    u_row(k, ra, rb, rc, dcur);
-    load_data_row<INT>(P, y0 + k + 2, x0, dcur);
-    phi_row<R, SRC, INT, NT, 10>(P, win, cm, k + 3, y0 + k + 2, s_lt, s_ls, ra);
-    u_row(k + 1, rb, rc, ra, dnext);
-    load_data_row<INT>(P, y0 + k + 3, x0, dnext);
-    phi_row<R, SRC, INT, NT, 10>(P, win, cm, k + 4, y0 + k + 3, s_lt, s_ls, rb);
-    u_row(k + 2, rc, ra, rb, dcur);
+  for (int k = 0; k < 32; ++k) {
+    const int kk = k + 1;                  // phi row produced in this step
+    if (kk == 16) {                        // switch to window base y0+16-R
+#pragma unroll
+      for (int j = 0; j < NT; ++j) {
+        const int xc = x0 - (R + 1) + j;
+        win[j] = __funnelshift_r(word_at<INT>(P, r, xc), word_at<INT>(P, r + 1, xc), 16 - R);
+      }
+    }
+    const int m0 = kk < 16 ? kk + 1 : kk - 16;
+    if (kk < 32) load_data_row<INT>(P, y0 + kk, x0, dnext);
+    phi_row<R, SRC, INT, NT, 10>(P, win, cm, m0, y0 + kk, s_lt, s_ls, pn);
+    const int i = y0 + k;
+    if (i < H) {
+      const uint32_t bitk = 1u << k;
+      uint32_t fb = 0u;
+#pragma unroll
+      for (int c = 0; c < 8; ++c) {
+        const int x = x0 + c;
+        float dx, dy;
+        if (INT) {
+          dx = p0[c + 2] - p0[c];
+          dy = pn[c + 1] - pm[c + 1];
+        } else {
+          if (x >= W) continue;
+          dx = (x == 0) ? 2.f * (p0[c + 2] - p0[c + 1])
+                        : (x == W - 1) ? 2.f * (p0[c + 1] - p0[c]) : (p0[c + 2] - p0[c]);
+          dy = (i == 0) ? 2.f * (pn[c + 1] - p0[c + 1])
+                        : (i == H - 1) ? 2.f * (p0[c + 1] - pm[c + 1]) : (pn[c + 1] - pm[c + 1]);
+        }
+        const float h = sqrt_approx(fmaf(dx, dx, dy * dy));
+        const float vf = (MODEL == REGION) ? fmaf(A, dcur[c], B) : dcur[c];
+        const float u = fmaf(hdt, vf * h, p0[c + 1]);
+        if (u > 0.f) ow[c] |= bitk;
+        if (fabsf(u) <= eps_u) fb |= 1u << c;
+      }
+      while (fb) {                          // near-tie: exact fp64 decision
+        const int c = __ffs(fb) - 1;
+        fb &= fb - 1;
+        const double ue = exact_u(P.ctx, P.bits_in, SRC, i, x0 + c);
+        ow[c] = ue > 0.0 ? (ow[c] | bitk) : (ow[c] & ~bitk);
+      }
+    }
+#pragma unroll
+    for (int c = 0; c < 10; ++c) { pm[c] = p0[c]; p0[c] = pn[c]; }
 #pragma unroll
     for (int c = 0; c < 8; ++c) dcur[c] = dnext[c];
   }
-  // k == 15: rows (k-1,k) are in (ra, rb); switch to window base y0+16-R
-#pragma unroll
-  for (int j = 0; j < NT; ++j) win[j] = __funnelshift_r(sw[1][sbase + j], sw[2][sbase + j], 16 - R);
-#pragma unroll 1
-  for (; k + 3 <= 30; k += 3) {
-    load_data_row<INT>(P, y0 + k + 1, x0, dnext);
-    phi_row<R, SRC, INT, NT, 10>(P, win, cm, k + 1 - 16, y0 + k + 1, s_lt, s_ls, rc);
-    u_row(k, ra, rb, rc, dcur);
-    load_data_row<INT>(P, y0 + k + 2, x0, dcur);
-    phi_row<R, SRC, INT, NT, 10>(P, win, cm, k + 2 - 16, y0 + k + 2, s_lt, s_ls, ra);
-    u_row(k + 1, rb, rc, ra, dnext);
-    load_data_row<INT>(P, y0 + k + 3, x0, dnext);
-    phi_row<R, SRC, INT, NT, 10>(P, win, cm, k + 3 - 16, y0 + k + 3, s_lt, s_ls, rb);
-    u_row(k + 2, rc, ra, rb, dcur);
-#pragma unroll
-    for (int c = 0; c < 8; ++c) dcur[c] = dnext[c];
-  }
-  // k == 30, 31
-  load_data_row<INT>(P, y0 + 31, x0, dnext);
-  phi_row<R, SRC, INT, NT, 10>(P, win, cm, 31 - 16, y0 + 31, s_lt, s_ls, rc);
-  u_row(30, ra, rb, rc, dcur);
-  phi_row<R, SRC, INT, NT, 10>(P, win, cm, 32 - 16, y0 + 32, s_lt, s_ls, ra);
-  u_row(31, rb, rc, ra, dnext);
-
-  uint32_t* dst = P.bits_out + (size_t)r * P.g.pitch_w + x0;
   if (!INT) {
 #pragma unroll
     for (int c = 0; c < 8; ++c) if (x0 + c >= W) ow[c] = 0u;
   }
+  uint32_t* dst = P.bits_out + (size_t)r * P.g.pitch_w + x0;
   reinterpret_cast<uint4*>(dst)[0] = make_uint4(ow[0], ow[1], ow[2], ow[3]);
   reinterpret_cast<uint4*>(dst)[1] = make_uint4(ow[4], ow[5], ow[6], ow[7]);
-}
-
-__device__ __forceinline__ void stage_words(const uint32_t* bits, const RunGeom& g, int r, int cx0,
-                                            uint32_t (*sw)[kSpanMax]) {
-  const int span = kColsPerThread * blockDim.x + 16;
-  for (int q = threadIdx.x; q < 3 * span; q += blockDim.x) {
-    int rr = q / span;
-    int cc = q - rr * span;
-    int x = cx0 - 8 + cc;
-    int wr = r - 1 + rr;
-    uint32_t v = 0u;
-    if (x >= 0 && x < g.W && wr >= 0 && wr < g.HR) v = __ldg(&bits[(size_t)wr * g.pitch_w + x]);
-    sw[rr][cc] = v;
-  }
 }
 
 template <int R>
@@ -296,33 +273,62 @@ __device__ __forceinline__ void load_luts(const FastParams& P, float* s_lt, floa
   }
 }
 
+// Work unit = (word-row, 256-column chunk), one warp each, grid-strided.  A
+// chunk whose every lane sees a uniform stencil window (all bits of rows
+// y0-32 .. y0+63 equal over its t columns, away from the image border) has
+// phi constant there, hence |grad phi| == 0, v == 0 and u == phi exactly, so
+// b^{n+1} == b^n: the chunk is copied without touching the data plane.
 template <int R, int MODEL, int SRC>
-__global__ void __launch_bounds__(kThreads) k_update(FastParams P) {
+__global__ void __launch_bounds__(kThreads, 4) k_update(FastParams P) {
   constexpr int NPAT = 1 << (2 * R + 1);
+  constexpr int NT = kColsPerThread + 2 * (R + 1);
   __shared__ float s_lt[NPAT], s_ls[NPAT];
-  __shared__ uint32_t sw[3][kSpanMax];
   const Scalars* sc = P.scal;
   if (*(volatile const int*)&sc->stop) return;
   if (MODEL == REGION && blockIdx.x == 0 && threadIdx.x == 0 && sc->zero_vel) P.scal->degenerate = 1;
   const float A = sc->A, B = sc->B, eps_u = sc->eps_u;
   load_luts<R>(P, s_lt, s_ls);
-  const int cbw = kColsPerThread * blockDim.x;
-  for (int tile = blockIdx.x; tile < P.g.ntiles; tile += gridDim.x) {
-    const int r = tile / P.g.ncb;
-    const int cx0 = (tile - r * P.g.ncb) * cbw;
-    __syncthreads();
-    stage_words(P.bits_in, P.g, r, cx0, sw);
-    __syncthreads();
-    const int x0 = cx0 + kColsPerThread * threadIdx.x;
-    if (x0 >= P.g.W) continue;
+  __syncthreads();
+  const int lane = threadIdx.x & 31;
+  const int nwarp = gridDim.x * (blockDim.x >> 5);
+  const int nunits = P.g.HR * P.nchunk;
+  for (int unit = blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5); unit < nunits;
+       unit += nwarp) {
+    const int r = unit / P.nchunk;
+    const int cx = (unit - r * P.nchunk) * kChunk;
+    const int x0 = cx + kColsPerThread * lane;
     const int y0 = r * 32;
-    const int wx0 = cx0 + kColsPerThread * (threadIdx.x & ~31);
-    const int wx1 = wx0 + kColsPerThread * 32 - 1;
     const bool interior = SRC == SRC_SMOOTH && y0 - 1 - R >= 0 && y0 + 32 + R <= P.g.H - 1 &&
-                          wx0 - (R + 1) >= 0 && wx1 + (R + 1) <= P.g.W - 1;
-    const int sbase = x0 - cx0 + 8 - (R + 1);
-    if (interior) update_tile<R, MODEL, SRC, true>(P, sw, s_lt, s_ls, r, x0, sbase, A, B, eps_u);
-    else update_tile<R, MODEL, SRC, false>(P, sw, s_lt, s_ls, r, x0, sbase, A, B, eps_u);
+                          cx - (R + 1) >= 0 && cx + kChunk - 1 + (R + 1) <= P.g.W - 1;
+    uint32_t prev[NT], cur[NT];
+    if (interior) {
+      uint32_t a = ~0u, o = 0u;
+#pragma unroll
+      for (int j = 0; j < NT; ++j) {
+        const int xc = x0 - (R + 1) + j;
+        prev[j] = word_at<true>(P, r - 1, xc);
+        cur[j] = word_at<true>(P, r, xc);
+        const uint32_t nx = word_at<true>(P, r + 1, xc);
+        a &= prev[j] & cur[j] & nx;
+        o |= prev[j] | cur[j] | nx;
+      }
+      if (P.skip_uniform && __all_sync(0xffffffffu, a == ~0u || o == 0u)) {
+        uint32_t* dst = P.bits_out + (size_t)r * P.g.pitch_w + x0;
+        reinterpret_cast<uint4*>(dst)[0] = make_uint4(cur[R + 1], cur[R + 2], cur[R + 3], cur[R + 4]);
+        reinterpret_cast<uint4*>(dst)[1] = make_uint4(cur[R + 5], cur[R + 6], cur[R + 7], cur[R + 8]);
+        continue;
+      }
+      update_block<R, MODEL, SRC, true>(P, s_lt, s_ls, r, x0, A, B, eps_u, prev, cur);
+    } else {
+      if (x0 >= P.g.W) continue;
+#pragma unroll
+      for (int j = 0; j < NT; ++j) {
+        const int xc = x0 - (R + 1) + j;
+        prev[j] = word_at<false>(P, r - 1, xc);
+        cur[j] = word_at<false>(P, r, xc);
+      }
+      update_block<R, MODEL, SRC, false>(P, s_lt, s_ls, r, x0, A, B, eps_u, prev, cur);
+    }
   }
 }
 
@@ -436,168 +442,182 @@ __device__ void finalize_cta(const TilePartial* part, int n, Scalars* sc, bool d
 }
 
 // ------------------------------------------------------------- partition
-template <int R, bool INT, bool PART, bool CKPT, bool MASKONLY>
-__device__ __forceinline__ void partition_tile(const FastParams& P, const uint32_t (*sw)[kSpanMax],
-                                               const float* s_lt, const float* s_ls, int r, int x0,
-                                               int sbase, float eps_phi, double& acc_in,
-                                               double& acc_out, long long& n_in, long long& n_out,
-                                               unsigned long long& mism) {
+// One lane: columns x0..x0+7 of word-row r.  Signs of phi^{n+1} = G*b^{n+1}
+// (t columns x0-R .. x0+7+R, no row halo), partition bits {phi >= 0} with the
+// incremental c+/c- sums, checkpoint mask {phi > 0} with the mismatch count.
+template <int R, bool INT>
+__device__ __forceinline__ void partition_block(const FastParams& P, const float* s_lt,
+                                                const float* s_ls, int r, int x0, float eps_phi,
+                                                const uint32_t (&prev)[8 + 2 * R],
+                                                const uint32_t (&cur)[8 + 2 * R],
+                                                uint32_t (&pw)[8], uint32_t (&mw)[8]) {
   constexpr int NT = kColsPerThread + 2 * R;
   const int H = P.g.H, W = P.g.W;
   const int y0 = r * 32;
-  uint32_t cm[NT];
+  uint32_t cm[NT], win[NT];
 #pragma unroll
   for (int j = 0; j < NT; ++j) {
-    int xc = x0 - R + j;
+    const int xc = x0 - R + j;
     cm[j] = (INT || (xc >= 0 && xc < W)) ? 0xffffffffu : 0u;
+    win[j] = __funnelshift_r(prev[j], cur[j], 32 - R);     // base row y0-R
   }
-  uint32_t win[NT];
-  uint32_t pw[8], mw[8];
   float ph[8];
 #pragma unroll
   for (int c = 0; c < 8; ++c) { pw[c] = 0u; mw[c] = 0u; }
-  auto do_row = [&](int k, int m0) {
+#pragma unroll 1
+  for (int k = 0; k < 32; ++k) {
+    if (k == 16) {                                          // base row y0+16-R
+#pragma unroll
+      for (int j = 0; j < NT; ++j) {
+        const int xc = x0 - R + j;
+        win[j] = __funnelshift_r(word_at<INT>(P, r, xc), word_at<INT>(P, r + 1, xc), 16 - R);
+      }
+    }
     const int i = y0 + k;
-    if (i >= H) return;
-    phi_row<R, SRC_SMOOTH, INT, NT, 8>(P, win, cm, m0, i, s_lt, s_ls, ph);
+    if (i >= H) break;
+    phi_row<R, SRC_SMOOTH, INT, NT, 8>(P, win, cm, k < 16 ? k : k - 16, i, s_lt, s_ls, ph);
+    const uint32_t bitk = 1u << k;
+    uint32_t fb = 0u;
 #pragma unroll
     for (int c = 0; c < 8; ++c) {
       if (!INT && x0 + c >= W) continue;
-      const float f = ph[c];
-      uint32_t ge, gt;
-      if (fabsf(f) <= eps_phi) {
-        double e = exact_phi(P.ctx, P.bits_in, SRC_SMOOTH, i, x0 + c);
-        ge = e >= 0.0;
-        gt = e > 0.0;
-        atomicAdd(&P.scal->fallbacks, 1ull);
-      } else {
-        ge = gt = f > 0.f;
-      }
-      pw[c] |= ge << k;
-      mw[c] |= gt << k;
+      if (ph[c] > 0.f) { pw[c] |= bitk; mw[c] |= bitk; }
+      if (fabsf(ph[c]) <= eps_phi) fb |= 1u << c;
     }
-  };
-#pragma unroll
-  for (int j = 0; j < NT; ++j) win[j] = __funnelshift_r(sw[0][sbase + j], sw[1][sbase + j], 32 - R);
-#pragma unroll 1
-  for (int k = 0; k < 16; ++k) do_row(k, k);
-#pragma unroll
-  for (int j = 0; j < NT; ++j) win[j] = __funnelshift_r(sw[1][sbase + j], sw[2][sbase + j], 16 - R);
-#pragma unroll 1
-  for (int k = 16; k < 32; ++k) do_row(k, k - 16);
-
-  const size_t base = (size_t)r * P.g.pitch_w + x0;
-  if (PART) {
-    uint4 o0 = reinterpret_cast<const uint4*>(P.pbits + base)[0];
-    uint4 o1 = reinterpret_cast<const uint4*>(P.pbits + base)[1];
-    uint32_t old[8] = {o0.x, o0.y, o0.z, o0.w, o1.x, o1.y, o1.z, o1.w};
-#pragma unroll
-    for (int c = 0; c < 8; ++c) {
-      if (!INT && x0 + c >= W) { pw[c] = 0u; continue; }
-      uint32_t ch = old[c] ^ pw[c];
-      while (ch) {
-        const int b = __ffs(ch) - 1;
-        ch &= ch - 1;
-        const double I = data_exact(P.ctx, y0 + b, x0 + c);
-        if ((pw[c] >> b) & 1u) { acc_in += I; ++n_in; }
-        else { acc_out += I; ++n_out; }
-      }
+    while (fb) {
+      const int c = __ffs(fb) - 1;
+      fb &= fb - 1;
+      const double e = exact_phi(P.ctx, P.bits_in, SRC_SMOOTH, i, x0 + c);
+      atomicAdd(&P.scal->fallbacks, 1ull);
+      pw[c] = e >= 0.0 ? (pw[c] | bitk) : (pw[c] & ~bitk);
+      mw[c] = e > 0.0 ? (mw[c] | bitk) : (mw[c] & ~bitk);
     }
-    reinterpret_cast<uint4*>(P.pbits + base)[0] = make_uint4(pw[0], pw[1], pw[2], pw[3]);
-    reinterpret_cast<uint4*>(P.pbits + base)[1] = make_uint4(pw[4], pw[5], pw[6], pw[7]);
-  }
-  if (MASKONLY) {
-#pragma unroll
-    for (int c = 0; c < 8; ++c)
-      if (!INT && x0 + c >= W) mw[c] = 0u;
-    reinterpret_cast<uint4*>(P.mbits + base)[0] = make_uint4(mw[0], mw[1], mw[2], mw[3]);
-    reinterpret_cast<uint4*>(P.mbits + base)[1] = make_uint4(mw[4], mw[5], mw[6], mw[7]);
-  } else if (CKPT) {
-    uint4 o0 = reinterpret_cast<const uint4*>(P.mbits + base)[0];
-    uint4 o1 = reinterpret_cast<const uint4*>(P.mbits + base)[1];
-    uint32_t old[8] = {o0.x, o0.y, o0.z, o0.w, o1.x, o1.y, o1.z, o1.w};
-#pragma unroll
-    for (int c = 0; c < 8; ++c) {
-      if (!INT && x0 + c >= W) mw[c] = 0u;
-      mism += __popc(old[c] ^ mw[c]);
-    }
-    reinterpret_cast<uint4*>(P.mbits + base)[0] = make_uint4(mw[0], mw[1], mw[2], mw[3]);
-    reinterpret_cast<uint4*>(P.mbits + base)[1] = make_uint4(mw[4], mw[5], mw[6], mw[7]);
   }
 }
 
-// Deterministic CTA reduction of the per-thread partials into one tile
-// partial (fixed shuffle pattern, warps combined in index order).
-__device__ __forceinline__ void cta_tile_partial(TilePartial* dst, double a, double b, long long na,
-                                                 long long nb, unsigned long long mm,
-                                                 TilePartial* s_w) {
-#pragma unroll
-  for (int o = 16; o > 0; o >>= 1) {
-    a += __shfl_xor_sync(0xffffffffu, a, o);
-    b += __shfl_xor_sync(0xffffffffu, b, o);
-    na += __shfl_xor_sync(0xffffffffu, na, o);
-    nb += __shfl_xor_sync(0xffffffffu, nb, o);
-    mm += __shfl_xor_sync(0xffffffffu, mm, o);
-  }
-  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  if (lane == 0) {
-    s_w[warp].a_hi = a; s_w[warp].b_hi = b;
-    s_w[warp].n_a = na; s_w[warp].n_b = nb; s_w[warp].mism = mm;
-  }
-  __syncthreads();
-  if (threadIdx.x == 0) {
-    TilePartial t{};
-    double ah = 0, al = 0, bh = 0, bl = 0;
-    for (int w = 0; w < (int)(blockDim.x >> 5); ++w) {
-      dd_add(ah, al, s_w[w].a_hi);
-      dd_add(bh, bl, s_w[w].b_hi);
-      t.n_a += s_w[w].n_a;
-      t.n_b += s_w[w].n_b;
-      t.mism += s_w[w].mism;
-    }
-    t.a_hi = ah; t.a_lo = al; t.b_hi = bh; t.b_lo = bl;
-    *dst = t;
-  }
-}
-
+// Work unit = (word-row, segment of kSegChunks chunks), one warp each; the
+// warp's deltas over the segment form one partial (fixed geometry =>
+// deterministic and independent of how the rows are split across GPUs).
 template <int R, bool PART, bool CKPT, bool MASKONLY>
-__global__ void __launch_bounds__(kThreads) k_partition(FastParams P) {
+__global__ void __launch_bounds__(kThreads, 4) k_partition(FastParams P) {
   constexpr int NPAT = 1 << (2 * R + 1);
+  constexpr int NT = kColsPerThread + 2 * R;
   __shared__ float s_lt[NPAT], s_ls[NPAT];
-  __shared__ uint32_t sw[3][kSpanMax];
-  __shared__ TilePartial s_warp[kThreads / 32];
   __shared__ unsigned int s_ticket;
   Scalars* sc = P.scal;
   if (!MASKONLY && *(volatile const int*)&sc->stop) return;
   const float eps_phi = sc->eps_phi;
   load_luts<R>(P, s_lt, s_ls);
-  const int cbw = kColsPerThread * blockDim.x;
-  for (int tile = blockIdx.x; tile < P.g.ntiles; tile += gridDim.x) {
-    const int r = tile / P.g.ncb;
-    const int cx0 = (tile - r * P.g.ncb) * cbw;
-    __syncthreads();
-    stage_words(P.bits_in, P.g, r, cx0, sw);
-    __syncthreads();
-    const int x0 = cx0 + kColsPerThread * threadIdx.x;
-    double a = 0.0, b = 0.0;
-    long long na = 0, nb = 0;
-    unsigned long long mm = 0;
-    if (x0 < P.g.W) {
+  __syncthreads();
+  const int lane = threadIdx.x & 31;
+  const int nwarp = gridDim.x * (blockDim.x >> 5);
+  const int nunits = P.g.HR * P.nseg;
+  for (int unit = blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5); unit < nunits;
+       unit += nwarp) {
+    const int r = unit / P.nseg;
+    const int seg = unit - r * P.nseg;
+    double a_in = 0.0, a_out = 0.0;
+    long long n_in = 0, n_out = 0;
+    unsigned long long mism = 0;
+    for (int ch = seg * kSegChunks; ch < (seg + 1) * kSegChunks && ch < P.nchunk; ++ch) {
+      const int cx = ch * kChunk;
+      const int x0 = cx + kColsPerThread * lane;
       const int y0 = r * 32;
-      const int wx0 = cx0 + kColsPerThread * (threadIdx.x & ~31);
-      const int wx1 = wx0 + kColsPerThread * 32 - 1;
-      const bool interior = y0 - R >= 0 && y0 + 31 + R <= P.g.H - 1 && wx0 - R >= 0 &&
-                            wx1 + R <= P.g.W - 1;
-      const int sbase = x0 - cx0 + 8 - R;
-      if (interior)
-        partition_tile<R, true, PART, CKPT, MASKONLY>(P, sw, s_lt, s_ls, r, x0, sbase, eps_phi, a, b, na, nb, mm);
-      else
-        partition_tile<R, false, PART, CKPT, MASKONLY>(P, sw, s_lt, s_ls, r, x0, sbase, eps_phi, a, b, na, nb, mm);
+      const bool interior = y0 - R >= 0 && y0 + 31 + R <= P.g.H - 1 && cx - R >= 0 &&
+                            cx + kChunk - 1 + R <= P.g.W - 1;
+      uint32_t pw[8], mw[8], prev[NT], cur[NT];
+      if (interior) {
+        uint32_t a = ~0u, o = 0u;
+#pragma unroll
+        for (int j = 0; j < NT; ++j) {
+          const int xc = x0 - R + j;
+          prev[j] = word_at<true>(P, r - 1, xc);
+          cur[j] = word_at<true>(P, r, xc);
+          const uint32_t nx = word_at<true>(P, r + 1, xc);
+          a &= prev[j] & cur[j] & nx;
+          o |= prev[j] | cur[j] | nx;
+        }
+        if (P.skip_uniform && __all_sync(0xffffffffu, a == ~0u || o == 0u)) {
+          // phi = +-c everywhere in the block: sign(phi) = b
+#pragma unroll
+          for (int c = 0; c < 8; ++c) pw[c] = mw[c] = cur[R + c];
+        } else {
+          partition_block<R, true>(P, s_lt, s_ls, r, x0, eps_phi, prev, cur, pw, mw);
+        }
+      } else {
+        if (x0 >= P.g.W) continue;
+#pragma unroll
+        for (int j = 0; j < NT; ++j) {
+          const int xc = x0 - R + j;
+          prev[j] = word_at<false>(P, r - 1, xc);
+          cur[j] = word_at<false>(P, r, xc);
+        }
+        partition_block<R, false>(P, s_lt, s_ls, r, x0, eps_phi, prev, cur, pw, mw);
+        if (x0 + 8 > P.g.W) {
+#pragma unroll
+          for (int c = 0; c < 8; ++c) if (x0 + c >= P.g.W) { pw[c] = 0u; mw[c] = 0u; }
+        }
+      }
+      const size_t base = (size_t)r * P.g.pitch_w + x0;
+      if (MASKONLY) {
+        reinterpret_cast<uint4*>(P.mbits + base)[0] = make_uint4(mw[0], mw[1], mw[2], mw[3]);
+        reinterpret_cast<uint4*>(P.mbits + base)[1] = make_uint4(mw[4], mw[5], mw[6], mw[7]);
+        continue;
+      }
+      if (PART) {
+        const uint4 o0 = reinterpret_cast<const uint4*>(P.pbits + base)[0];
+        const uint4 o1 = reinterpret_cast<const uint4*>(P.pbits + base)[1];
+        const uint32_t old[8] = {o0.x, o0.y, o0.z, o0.w, o1.x, o1.y, o1.z, o1.w};
+        uint32_t any = 0u;
+#pragma unroll
+        for (int c = 0; c < 8; ++c) {
+          uint32_t ch2 = old[c] ^ pw[c];
+          any |= ch2;
+          while (ch2) {
+            const int b = __ffs(ch2) - 1;
+            ch2 &= ch2 - 1;
+            const double I = data_exact(P.ctx, y0 + b, x0 + c);
+            if ((pw[c] >> b) & 1u) { a_in += I; ++n_in; }
+            else { a_out += I; ++n_out; }
+          }
+        }
+        if (any) {
+          reinterpret_cast<uint4*>(P.pbits + base)[0] = make_uint4(pw[0], pw[1], pw[2], pw[3]);
+          reinterpret_cast<uint4*>(P.pbits + base)[1] = make_uint4(pw[4], pw[5], pw[6], pw[7]);
+        }
+      }
+      if (CKPT) {
+        const uint4 o0 = reinterpret_cast<const uint4*>(P.mbits + base)[0];
+        const uint4 o1 = reinterpret_cast<const uint4*>(P.mbits + base)[1];
+        const uint32_t old[8] = {o0.x, o0.y, o0.z, o0.w, o1.x, o1.y, o1.z, o1.w};
+#pragma unroll
+        for (int c = 0; c < 8; ++c) mism += __popc(old[c] ^ mw[c]);
+        reinterpret_cast<uint4*>(P.mbits + base)[0] = make_uint4(mw[0], mw[1], mw[2], mw[3]);
+        reinterpret_cast<uint4*>(P.mbits + base)[1] = make_uint4(mw[4], mw[5], mw[6], mw[7]);
+      }
     }
-    if (!MASKONLY) cta_tile_partial(P.part + tile, a, b, na, nb, mm, s_warp);
+    if (MASKONLY) continue;
+    // warp partial for this unit (fixed xor-shuffle order)
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) {
+      a_in += __shfl_xor_sync(0xffffffffu, a_in, o);
+      a_out += __shfl_xor_sync(0xffffffffu, a_out, o);
+      n_in += __shfl_xor_sync(0xffffffffu, n_in, o);
+      n_out += __shfl_xor_sync(0xffffffffu, n_out, o);
+      mism += __shfl_xor_sync(0xffffffffu, mism, o);
+    }
+    if (lane == 0) {
+      TilePartial t{};
+      t.a_hi = a_in;
+      t.b_hi = a_out;
+      t.n_a = n_in;
+      t.n_b = n_out;
+      t.mism = mism;
+      P.part[unit] = t;
+    }
   }
   if (MASKONLY) return;
-  // last CTA to finish reduces every tile partial (threadFenceReduction idiom)
+  // last CTA to finish reduces every unit partial (threadFenceReduction idiom)
   __syncthreads();
   if (threadIdx.x == 0) {
     __threadfence();
@@ -606,7 +626,7 @@ __global__ void __launch_bounds__(kThreads) k_partition(FastParams P) {
   __syncthreads();
   if (s_ticket == gridDim.x - 1) {
     __threadfence();
-    finalize_cta(P.part, P.g.ntiles, sc, /*delta=*/true, PART, CKPT, P.iter);
+    finalize_cta(P.part, nunits, sc, /*delta=*/true, PART, CKPT, P.iter);
   }
 }
 
