@@ -55,6 +55,8 @@ def parse():
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--cpu-seconds", type=float, default=12.0)
+    ap.add_argument("--skip-steps", type=int, default=None,
+                    help="steps of the uniform-window-skip measurement (default: --steps)")
     return ap.parse_args()
 
 
@@ -263,6 +265,8 @@ def main():
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
         return float(t.item())
 
+    # ---- dense pass (every pixel recomputed every iteration): the headline
+    N.check(N.lib.lse_run_set_option(h, b"skip_uniform", 0))
     for _ in range(args.warmup):
         job()
     # ---- timed region: inputs resident in HBM
@@ -288,6 +292,33 @@ def main():
     fallbacks = st.exact_fallbacks
     px_its = npx * args.iters * args.steps * ws
     value = px_its / (t_ms / 1e3) / 1e9
+
+    # ---- same jobs with the exact uniform-window skip (product default)
+    skip_steps = args.steps if args.skip_steps is None else args.skip_steps
+    skip = None
+    if skip_steps > 0:
+        N.check(N.lib.lse_run_set_option(h, b"skip_uniform", 1))
+        job()
+        barrier()
+        N.check(N.lib.lse_run_set_profiling(h, 1))
+        N.check(N.lib.lse_run_begin_timing(h))
+        for _ in range(skip_steps):
+            job()
+        N.check(N.lib.lse_run_end_timing(h, C.byref(ms)))
+        barrier()
+        s_ms = max_over_ranks(ms.value)
+        su, sp, nsu, nsp = C.c_double(), C.c_double(), C.c_longlong(), C.c_longlong()
+        N.check(N.lib.lse_run_kernel_times(h, C.byref(su), C.byref(nsu), C.byref(sp),
+                                           C.byref(nsp)))
+        N.check(N.lib.lse_run_set_profiling(h, 0))
+        skip = {"value": npx * args.iters * skip_steps * ws / (s_ms / 1e3) / 1e9,
+                "unit": "Gpix-it/s", "ms_per_step": s_ms / skip_steps,
+                "update_ms": su.value / max(1, nsu.value),
+                "partition_ms": sp.value / max(1, nsp.value),
+                "note": "skip_uniform=1: warp blocks whose whole stencil window is uniform "
+                        "are copied (|grad phi| == 0 there, so u == phi exactly); results "
+                        "bit-identical to the dense pass"}
+        N.check(N.lib.lse_run_set_option(h, b"skip_uniform", 0))
 
     # ---- end to end through the C ABI with host buffers
     e2e = None
@@ -346,6 +377,7 @@ def main():
             "metric": "Gpixel-iterations/s of the LSE update", "value": value,
             "unit": "Gpix-it/s", "n_gpus": ws, "steps": args.steps, "warmup": args.warmup,
             "ms_per_step": t_ms / args.steps, "higher_is_better": True,
+            "mode": "dense (skip_uniform=0: every pixel recomputed every iteration)",
             "scaling": "weak", "vs_baseline": None, "dtype": "f32+f64-guard (bit state)",
             "data": "synthetic (seeded, BASELINE C5 statistics)",
             "config": {"workload": f"C5: {H}x{W} region LSE, 20000-rect density, sigma 1.5 "
@@ -353,6 +385,7 @@ def main():
                        "parallelism": f"replicas x{ws}" if ws > 1 else "single GPU",
                        "l2": "inputs (4.3 GB image) larger than L2"},
             "roofline": roof, "cpu_baseline": cpu, "e2e": e2e, "gpu_launches": int(launches),
+            "uniform_skip": skip,
             "clocks": clk, "exact_fallbacks": int(fallbacks),
             "scene_gen_s": round(t_gen, 2),
         }

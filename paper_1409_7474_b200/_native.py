@@ -14,7 +14,7 @@ import threading
 import numpy as np
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(_HERE, "_lib", "liblse_b200.so")
+LIB_PATH = os.environ.get("LSE_LIB_PATH") or os.path.join(_HERE, "_lib", "liblse_b200.so")
 
 LSE_OK = 0
 LSE_ERR_ARG = 1

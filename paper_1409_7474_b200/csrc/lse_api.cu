@@ -162,7 +162,11 @@ struct lse_run {
   long long n_update = 0, n_part = 0;
   int grid_update = 0, grid_part = 0;
   int skip_uniform = 1;
-  int nchunk = 1, nseg = 1;
+  int nchunk = 1, nchunk_u = 1, nseg = 1, seg_chunks = 1;
+  UnitRect ru{0, 0, 0, 0}, rp{0, 0, 0, 0};   // interior unit rectangles
+  long long ni_upd = 0, nb_upd[2] = {0, 0}, ni_part = 0, nb_part = 0;
+  unsigned long long* d_work = nullptr;
+  unsigned long long work_next = 0;   // host mirror of the monotonic work counter
   cudaEvent_t t_begin = nullptr, t_end = nullptr;
 };
 
@@ -184,7 +188,13 @@ FastParams fast_params(lse_run* r) {
   P.scale32 = (float)r->scale;
   P.skip_uniform = r->skip_uniform;
   P.nchunk = r->nchunk;
+  P.nchunk_u = r->nchunk_u;
   P.nseg = r->nseg;
+  P.seg_chunks = r->seg_chunks;
+  P.work = r->d_work;
+  P.ru = r->ru;
+  P.rp = r->rp;
+  P.n_int_part = (int)r->ni_part;
   return P;
 }
 
@@ -256,6 +266,50 @@ cudaEvent_t next_event(lse_run* r) {
   return r->evpool[r->evused++];
 }
 
+// reserve the work-counter window of one dynamically scheduled launch
+unsigned long long take_work(lse_run* r, long long units, int grid) {
+  const unsigned long long base = r->work_next;
+  r->work_next += (unsigned long long)units + (unsigned long long)grid * 4;
+  return base;
+}
+
+template <int R, int MODEL, int SRC>
+int launch_update(lse_run* r, FastParams P) {
+  const long long nb = r->nb_upd[SRC == SRC_SCALED];
+  const long long ni = SRC == SRC_SCALED ? 0 : r->ni_upd;
+  if (nb > 0) {
+    const int g = fast_grid(nb);
+    P.work_base = take_work(r, nb, g);
+    if (SRC == SRC_SCALED) P.ru = UnitRect{0, 0, 0, 0};
+    k_update<R, MODEL, SRC, false><<<g, kThreads, 0, r->st>>>(P);
+    CKL();
+  }
+  if (ni > 0) {
+    const int g = fast_grid(ni);
+    P.work_base = take_work(r, ni, g);
+    k_update<R, MODEL, SRC, true><<<g, kThreads, 0, r->st>>>(P);
+    CKL();
+  }
+  return LSE_OK;
+}
+
+template <int R, bool PART, bool CKPT, bool MASKONLY>
+int launch_partition(lse_run* r, FastParams P) {
+  if (r->nb_part > 0) {
+    const int g = fast_grid(r->nb_part);
+    P.work_base = take_work(r, r->nb_part, g);
+    k_partition<R, PART, CKPT, MASKONLY, false><<<g, kThreads, 0, r->st>>>(P);
+    CKL();
+  }
+  // the interior launch always runs (possibly with no units): its last CTA
+  // reduces all partials and writes the next update's coefficients
+  const int g = fast_grid(std::max<long long>(1, r->ni_part));
+  P.work_base = take_work(r, r->ni_part, g);
+  k_partition<R, PART, CKPT, MASKONLY, true><<<g, kThreads, 0, r->st>>>(P);
+  CKL();
+  return LSE_OK;
+}
+
 template <int R, int MODEL>
 int launch_fast_R(lse_run* r, long long it, bool ckpt) {
   FastParams P = fast_params(r);
@@ -269,25 +323,19 @@ int launch_fast_R(lse_run* r, long long it, bool ckpt) {
     e2 = next_event(r);
     cudaEventRecord(e0, r->st);
   }
-  if (!r->grid_update) r->grid_update = fast_grid((long long)r->g.HR * r->nchunk);
-  if (r->mode == SRC_SCALED)
-    k_update<R, MODEL, SRC_SCALED><<<r->grid_update, kThreads, 0, r->st>>>(P);
-  else
-    k_update<R, MODEL, SRC_SMOOTH><<<r->grid_update, kThreads, 0, r->st>>>(P);
-  CKL();
+  if (r->mode == SRC_SCALED) TRY((launch_update<R, MODEL, SRC_SCALED>(r, P)));
+  else TRY((launch_update<R, MODEL, SRC_SMOOTH>(r, P)));
   if (r->prof) cudaEventRecord(e1, r->st);
   P.bits_in = r->d_bits[r->cur ^ 1];
-  if (!r->grid_part) r->grid_part = fast_grid((long long)r->g.HR * r->nseg);
   bool launched_part = false;
   if (MODEL == REGION) {
-    if (ckpt) k_partition<R, true, true, false><<<r->grid_part, kThreads, 0, r->st>>>(P);
-    else k_partition<R, true, false, false><<<r->grid_part, kThreads, 0, r->st>>>(P);
+    if (ckpt) TRY((launch_partition<R, true, true, false>(r, P)));
+    else TRY((launch_partition<R, true, false, false>(r, P)));
     launched_part = true;
   } else if (ckpt) {
-    k_partition<R, false, true, false><<<r->grid_part, kThreads, 0, r->st>>>(P);
+    TRY((launch_partition<R, false, true, false>(r, P)));
     launched_part = true;
   }
-  CKL();
   if (r->prof) {
     cudaEventRecord(e2, r->st);
     r->evrec.push_back({e0, e1, e2, launched_part});
@@ -663,8 +711,36 @@ int lse_run_create(lse_run** out, const lse_params* p, long long height, long lo
   r->g.ncb = (r->W + kColsPerThread * r->nthr - 1) / (kColsPerThread * r->nthr);
   r->g.ntiles = r->g.HR * r->g.ncb;
   r->nchunk = (r->W + kChunk - 1) / kChunk;
-  r->nseg = (r->nchunk + kSegChunks - 1) / kSegChunks;
-  const long long nparts = std::max<long long>(r->g.ntiles, (long long)r->g.HR * r->nseg);
+  r->nchunk_u = (r->W + kUpdChunk - 1) / kUpdChunk;
+  {
+    const int R = r->R, H = r->H, W = r->W, HR = r->g.HR, nc = r->nchunk;
+    auto fdiv = [](long long a, long long b) { return a >= 0 ? a / b : -((-a + b - 1) / b); };
+    auto mk = [&](long long rh, long long ch, int ncols) {
+      UnitRect u{1, (int)std::min<long long>(HR, rh + 1), 1, (int)std::min<long long>(ncols, ch + 1)};
+      if (u.r_hi <= u.r_lo || u.c_hi <= u.c_lo || R > 31) u = UnitRect{0, 0, 0, 0};
+      return u;
+    };
+    // update: rows y0-1-R .. y0+32+R and columns x-(R+1) .. x+8+R inside
+    const int ncu = r->nchunk_u;
+    r->ru = mk(fdiv(H - 33 - R, 32), fdiv(W - kUpdChunk - 1 - R, kUpdChunk), ncu);
+    // partition: rows y0-R .. y0+31+R and columns x-R .. x+7+R inside
+    r->rp = mk(fdiv(H - 32 - R, 32), fdiv(W - 256 - R, 256), nc);
+    const long long cu = (long long)(r->ru.r_hi - r->ru.r_lo) * (r->ru.c_hi - r->ru.c_lo);
+    r->ni_upd = cu;
+    r->nb_upd[0] = (long long)HR * ncu - cu;
+    r->nb_upd[1] = (long long)HR * ncu;
+    // partition segments: >= ~8 interior units per resident warp, <= 16 chunks
+    // (fixed by the image geometry only)
+    const long long warps = (long long)num_sms() * 16;
+    const long long wi = r->rp.c_hi - r->rp.c_lo, hi_rows = r->rp.r_hi - r->rp.r_lo;
+    long long sc = wi > 0 ? (hi_rows * wi) / (8 * warps) : 1;
+    sc = std::max<long long>(1, std::min<long long>(16, sc));
+    r->seg_chunks = (int)sc;
+    r->nseg = wi > 0 ? (int)((wi + sc - 1) / sc) : 0;
+    r->ni_part = hi_rows * r->nseg;
+    r->nb_part = (long long)HR * nc - hi_rows * wi;
+  }
+  const long long nparts = std::max<long long>(r->g.ntiles, r->ni_part + r->nb_part);
   auto cleanup = [&](int rc) {
     lse_run_destroy(r);
     return rc;
@@ -680,10 +756,11 @@ int lse_run_create(lse_run** out, const lse_params* p, long long height, long lo
       (rc = dalloc(&r->d_scal, 1)) || (rc = dalloc(&r->d_lut_t, 512)) ||
       (rc = dalloc(&r->d_lut_s, 512)) || (rc = dalloc(&r->d_ctx, 1)) ||
       (rc = dalloc(&r->d_w64, 32)) || (rc = dalloc(&r->d_keys, 3)) ||
-      (rc = dalloc(&r->d_count, 1)))
+      (rc = dalloc(&r->d_count, 1)) || (rc = dalloc(&r->d_work, 1)))
     return cleanup(rc);
   if (cudaMallocHost((void**)&r->h_scal, sizeof(Scalars)) != cudaSuccess)
     return cleanup(fail(LSE_ERR_CUDA, "pinned alloc failed"));
+  cudaMemsetAsync(r->d_work, 0, sizeof(unsigned long long), r->st);
   cudaMemsetAsync(r->d_bits[0], 0, nbits * 4, r->st);
   cudaMemsetAsync(r->d_bits[1], 0, nbits * 4, r->st);
   cudaMemsetAsync(r->d_P, 0, nbits * 4, r->st);
@@ -752,6 +829,9 @@ int lse_run_advance(lse_run* r, long long n_steps, lse_status* st) {
   }
   const long long steps = std::min(n_steps, r->p.max_iters - r->iteration);
   TRY(prepare(r));
+  // re-base the dynamic work counter (a stopped launch makes no grabs)
+  CK(cudaMemsetAsync(r->d_work, 0, sizeof(unsigned long long), r->st));
+  r->work_next = 0;
   const long long it0 = r->iteration;
   bool pending = false;
   for (long long it = it0 + 1; it <= it0 + steps; ++it) {
@@ -817,12 +897,13 @@ int lse_run_read_mask(lse_run* r, unsigned char* out, int inside_sign, int packe
     FastParams P = fast_params(r);
     P.bits_in = r->d_bits[r->cur];
     P.mbits = r->d_mask;
-    const int grid = fast_grid((long long)r->g.HR * r->nseg);
+    CK(cudaMemsetAsync(r->d_work, 0, sizeof(unsigned long long), r->st));
+    r->work_next = 0;
     switch (r->R) {
-      case 1: k_partition<1, false, false, true><<<grid, kThreads, 0, r->st>>>(P); break;
-      case 2: k_partition<2, false, false, true><<<grid, kThreads, 0, r->st>>>(P); break;
-      case 3: k_partition<3, false, false, true><<<grid, kThreads, 0, r->st>>>(P); break;
-      case 4: k_partition<4, false, false, true><<<grid, kThreads, 0, r->st>>>(P); break;
+      case 1: TRY((launch_partition<1, false, false, true>(r, P))); break;
+      case 2: TRY((launch_partition<2, false, false, true>(r, P))); break;
+      case 3: TRY((launch_partition<3, false, false, true>(r, P))); break;
+      case 4: TRY((launch_partition<4, false, false, true>(r, P))); break;
     }
     CKL();
   } else {
@@ -901,7 +982,7 @@ int lse_run_kernel_times(lse_run* r, double* update_ms, long long* update_launch
 void lse_run_destroy(lse_run* r) {
   if (!r) return;
   if (r->st) cudaStreamSynchronize(r->st);
-  void* ptrs[] = {r->d_data32, r->d_data64, r->d_bits[0], r->d_bits[1], r->d_P, r->d_M,
+  void* ptrs[] = {r->d_work, r->d_data32, r->d_data64, r->d_bits[0], r->d_bits[1], r->d_P, r->d_M,
                   r->d_mask, r->d_part, r->d_scal, r->d_lut_t, r->d_lut_s, r->d_ctx,
                   r->d_w64, r->d_keys, r->d_count, r->d_F[0], r->d_F[1], r->d_U, r->d_T};
   for (void* q : ptrs)

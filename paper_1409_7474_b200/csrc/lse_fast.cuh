@@ -38,6 +38,13 @@ struct ExactCtx {
   int model;
 };
 
+// Interior rectangle of work units: word-rows [r_lo, r_hi) x chunks [c_lo, c_hi)
+// whose whole stencil footprint lies inside the image.  Units outside it
+// ("border units") run the zero-padding / one-sided-gradient variant.
+struct UnitRect {
+  int r_lo, r_hi, c_lo, c_hi;
+};
+
 struct FastParams {
   const uint32_t* bits_in;   // b^n (update) / b^{n+1} (partition)
   uint32_t* bits_out;        // b^{n+1} (update)
@@ -55,12 +62,20 @@ struct FastParams {
   float scale32;
   long long iter;            // iteration produced by this launch
   int skip_uniform;          // skip warp blocks whose whole stencil window is uniform
-  int nchunk;                // 256-column chunks per word-row
-  int nseg;                  // partition segments (kSegChunks chunks) per word-row
+  int nchunk;                // partition chunks (kChunk columns) per word-row
+  int nchunk_u;              // update chunks (kUpdChunk columns) per word-row
+  int nseg;                  // partition segments per interior word-row
+  int seg_chunks;            // chunks per partition segment (partial granularity)
+  UnitRect ru, rp;           // interior rectangles (word-rows x chunks): update / partition
+  int n_int_part;            // interior partition units (their partials come first)
+  unsigned long long* work;  // dynamic work counter (monotonic across launches)
+  unsigned long long work_base;  // value of *work when this launch started
 };
 
-constexpr int kChunk = 256;      // columns per warp chunk (32 lanes x 8 columns)
-constexpr int kSegChunks = 16;   // chunks per partition segment (partial granularity)
+constexpr int kChunk = 256;      // partition: columns per warp chunk (32 lanes x 8 columns)
+constexpr int kUpdCols = 8;      // update: columns per lane
+constexpr int kUpdChunk = 32 * kUpdCols;   // update: columns per warp chunk
+
 
 __device__ __forceinline__ double data_exact(const ExactCtx* c, int i, int x) {
   size_t o = (size_t)i * c->data_pitch + x;
@@ -93,6 +108,114 @@ __device__ __noinline__ double exact_u(const ExactCtx* c, const uint32_t* bits, 
     } else {
       double I = data_exact(c, i, x);
       double D = dmul(sc->dc, dsub(dsub(dmul(2.0, I), sc->c_pos), sc->c_neg));
+      v = dmul(ddiv(D, sc->peak), h);
+    }
+  } else {
+    v = dmul(data_exact(c, i, x), h);
+  }
+  atomicAdd(&c->scal->fallbacks, 1ull);
+  return dadd(pc, dmul(c->dt, v));
+}
+
+// ------------------------------------------------ fast exact evaluators
+// Same arithmetic as exact_u / exact_phi, but the bit window around the
+// pixel is gathered up front (two independent word loads per column), so a
+// near-tie costs one round of L2 latency instead of hundreds of dependent
+// loads.  val/valid hold, per window column, the signs and the in-image mask
+// of window rows r0 .. r0+NR-1.
+template <int NR, int NC>
+__device__ __forceinline__ void gather_window(const ExactCtx* c, const uint32_t* bits, int r0,
+                                              int xc0, uint32_t (&val)[NC], uint32_t (&valid)[NC]) {
+  const int H = c->H, W = c->W, HR = (H + 31) >> 5;
+  const int wr = r0 >> 5;                      // arithmetic shift: r0 may be negative
+  const int sh = r0 & 31;
+  uint32_t rows_ok = 0u;
+#pragma unroll
+  for (int k = 0; k < NR; ++k) rows_ok |= (r0 + k >= 0 && r0 + k < H) ? (1u << k) : 0u;
+#pragma unroll
+  for (int cc = 0; cc < NC; ++cc) {
+    const int xc = xc0 + cc;
+    uint32_t lo = 0u, hi = 0u;
+    if (xc >= 0 && xc < W) {
+      if (wr >= 0 && wr < HR) lo = __ldg(&bits[(size_t)wr * c->pitch_w + xc]);
+      if (wr + 1 >= 0 && wr + 1 < HR) hi = __ldg(&bits[(size_t)(wr + 1) * c->pitch_w + xc]);
+      valid[cc] = rows_ok;
+    } else {
+      valid[cc] = 0u;
+    }
+    val[cc] = __funnelshift_r(lo, hi, sh);
+  }
+}
+
+// exact vertical scipy pass at window row rr (centre), column cc
+template <int R, int NC>
+__device__ __forceinline__ double wt(const ExactCtx* c, const uint32_t (&val)[NC],
+                                     const uint32_t (&valid)[NC], int rr, int cc) {
+  auto b = [&](int k) -> double {
+    if (!((valid[cc] >> k) & 1u)) return 0.0;
+    return ((val[cc] >> k) & 1u) ? 1.0 : -1.0;
+  };
+  double acc = dmul(b(rr), c->w64[0]);
+#pragma unroll
+  for (int d = R; d >= 1; --d) acc = dadd(acc, dmul(dadd(b(rr - d), b(rr + d)), c->w64[d]));
+  return acc;
+}
+
+// exact horizontal pass at window row rr, window column cc (t zero outside)
+template <int R, int NC>
+__device__ __forceinline__ double wphi(const ExactCtx* c, const uint32_t (&val)[NC],
+                                       const uint32_t (&valid)[NC], int rr, int cc) {
+  double acc = dmul(wt<R, NC>(c, val, valid, rr, cc), c->w64[0]);
+#pragma unroll
+  for (int d = R; d >= 1; --d)
+    acc = dadd(acc, dmul(dadd(wt<R, NC>(c, val, valid, rr, cc - d),
+                              wt<R, NC>(c, val, valid, rr, cc + d)), c->w64[d]));
+  return acc;
+}
+
+// phi^{n+1} at (i, x) exactly (partition near-ties)
+template <int R>
+__device__ __noinline__ double exact_phi_fast(const ExactCtx* c, const uint32_t* bits, int i, int x) {
+  constexpr int NR = 2 * R + 1, NC = 2 * R + 1;
+  uint32_t val[NC], valid[NC];
+  gather_window<NR, NC>(c, bits, i - R, x - R, val, valid);
+  atomicAdd(&c->scal->fallbacks, 1ull);
+  return wphi<R, NC>(c, val, valid, R, R);
+}
+
+// u at (i, x) exactly (update near-ties): phi at the pixel and its four
+// neighbours (np.gradient one-sided at the image border), glibc hypot,
+// the model's velocity, u = phi + dt * v.
+template <int R, int SRC>
+__device__ __noinline__ double exact_u_fast(const ExactCtx* c, const uint32_t* bits, int i, int x) {
+  constexpr int NR = 2 * R + 3, NC = 2 * R + 3;
+  const int H = c->H, W = c->W;
+  uint32_t val[NC], valid[NC];
+  gather_window<NR, NC>(c, bits, i - 1 - R, x - 1 - R, val, valid);
+  auto ph = [&](int di, int dx) -> double {      // phi at (i + di, x + dx)
+    if (SRC == SRC_SCALED) {
+      const int cc = R + 1 + dx, rr = R + 1 + di;
+      return ((val[cc] >> rr) & 1u) ? c->scale : -c->scale;
+    }
+    return wphi<R, NC>(c, val, valid, R + 1 + di, R + 1 + dx);
+  };
+  const double pc = ph(0, 0);
+  double fx, fy;
+  if (x == 0) fx = dsub(ph(0, 1), pc);
+  else if (x == W - 1) fx = dsub(pc, ph(0, -1));
+  else fx = dmul(dsub(ph(0, 1), ph(0, -1)), 0.5);
+  if (i == 0) fy = dsub(ph(1, 0), pc);
+  else if (i == H - 1) fy = dsub(pc, ph(-1, 0));
+  else fy = dmul(dsub(ph(1, 0), ph(-1, 0)), 0.5);
+  const double h = np_hypot(fx, fy);
+  double v;
+  const Scalars* sc = c->scal;
+  if (c->model == REGION) {
+    if (sc->zero_vel) {
+      v = 0.0;
+    } else {
+      const double I = data_exact(c, i, x);
+      const double D = dmul(sc->dc, dsub(dsub(dmul(2.0, I), sc->c_pos), sc->c_neg));
       v = dmul(ddiv(D, sc->peak), h);
     }
   } else {
@@ -135,40 +258,44 @@ __device__ __forceinline__ void phi_row(const FastParams& P, const uint32_t (&wi
     vr = row_valid_mask<R>(i, P.g.H);
     Lv = s_ls[vr];
   }
-  float t[NT];
+  // each t (vertical pass of one column) is folded into the <= 2R+1 outputs
+  // it touches as soon as it is looked up: no t[] array stays live
 #pragma unroll
   for (int j = 0; j < NT; ++j) {
     const uint32_t p = (win[j] >> m0) & PM;
-    if (INT) t[j] = s_lt[p];
-    else t[j] = fmaf(2.f, s_ls[p & vr & cm[j]], cm[j] ? -Lv : 0.f);
-  }
+    float t;
+    if (INT) t = s_lt[p];
+    else t = fmaf(2.f, s_ls[p & vr & cm[j]], cm[j] ? -Lv : 0.f);
 #pragma unroll
-  for (int c = 0; c < NOUT; ++c) {
-    float acc = P.w32[0] * t[c + R];
-#pragma unroll
-    for (int d = 1; d <= R; ++d) acc = fmaf(P.w32[d], t[c + R - d] + t[c + R + d], acc);
-    out[c] = acc;
+    for (int c = 0; c < NOUT; ++c) {
+      const int d = j - c - R;                     // t column offset from output c
+      if (d < -R || d > R) continue;
+      const float wd = P.w32[d < 0 ? -d : d];
+      if (d == -R) out[c] = wd * t;                // first contribution to out[c]
+      else out[c] = fmaf(wd, t, out[c]);
+    }
   }
 }
 
-template <bool INT>
-__device__ __forceinline__ void load_data_row(const FastParams& P, int i, int x0, float (&d)[8]) {
+template <bool INT, int CPL>
+__device__ __forceinline__ void load_data_row(const FastParams& P, int i, int x0, float (&d)[CPL]) {
   if (i >= P.g.H) return;
   const float* rowp = P.data32 + (size_t)i * P.g.data_pitch + x0;
   if (INT) {
-    const float4 a = __ldcs(reinterpret_cast<const float4*>(rowp));
-    const float4 b = __ldcs(reinterpret_cast<const float4*>(rowp) + 1);
-    d[0] = a.x; d[1] = a.y; d[2] = a.z; d[3] = a.w;
-    d[4] = b.x; d[5] = b.y; d[6] = b.z; d[7] = b.w;
+#pragma unroll
+    for (int q = 0; q < CPL / 4; ++q) {
+      const float4 a = __ldcs(reinterpret_cast<const float4*>(rowp) + q);
+      d[4 * q + 0] = a.x; d[4 * q + 1] = a.y; d[4 * q + 2] = a.z; d[4 * q + 3] = a.w;
+    }
   } else {
 #pragma unroll
-    for (int c = 0; c < 8; ++c) d[c] = (x0 + c < P.g.W) ? __ldcs(rowp + c) : 0.f;
+    for (int c = 0; c < CPL; ++c) d[c] = (x0 + c < P.g.W) ? __ldcs(rowp + c) : 0.f;
   }
 }
 
 __device__ __forceinline__ float sqrt_approx(float x) {
   float y;
-  asm("sqrt.approx.f32 %0, %1;" : "=f"(y) : "f"(x));
+  asm("sqrt.approx.ftz.f32 %0, %1;" : "=f"(y) : "f"(x));
   return y;
 }
 
@@ -180,15 +307,16 @@ __device__ __forceinline__ uint32_t word_at(const FastParams& P, int wr, int xc)
 }
 
 // ---------------------------------------------------------------- update
-// One lane: columns x0..x0+7 of word-row r (32 rows).  phi rows -1..32 are
-// rebuilt from the bit state (t columns x0-R-1 .. x0+8+R); three phi rows
-// are kept in registers while walking down the rows.
-template <int R, int MODEL, int SRC, bool INT>
+// One lane: columns x0 .. x0+CPL-1 of word-row r (32 rows).  phi rows -1..32
+// are rebuilt from the bit state (t columns x0-R-1 .. x0+CPL+R); three phi
+// rows are kept in registers while walking down the rows.
+template <int R, int MODEL, int SRC, bool INT, int CPL>
 __device__ __forceinline__ void update_block(const FastParams& P, const float* s_lt,
                                              const float* s_ls, int r, int x0, float A, float B,
-                                             float eps_u, const uint32_t (&prev)[8 + 2 * (R + 1)],
-                                             const uint32_t (&cur)[8 + 2 * (R + 1)]) {
-  constexpr int NT = kColsPerThread + 2 * (R + 1);
+                                             float eps_u, const uint32_t (&prev)[CPL + 2 * (R + 1)],
+                                             const uint32_t (&cur)[CPL + 2 * (R + 1)]) {
+  constexpr int NT = CPL + 2 * (R + 1);
+  constexpr int NP = CPL + 2;             // phi columns x0-1 .. x0+CPL
   const int H = P.g.H, W = P.g.W;
   const int y0 = r * 32;
   const float hdt = 0.5f * P.dt32;        // h below is 2|grad phi|
@@ -199,32 +327,38 @@ __device__ __forceinline__ void update_block(const FastParams& P, const float* s
     cm[j] = (INT || (xc >= 0 && xc < W)) ? 0xffffffffu : 0u;
     win[j] = __funnelshift_r(prev[j], cur[j], 31 - R);   // base row y0-1-R
   }
-  float pm[10], p0[10], pn[10], dcur[8], dnext[8];
-  uint32_t ow[8];
+  float pm[NP], p0[NP], pn[NP], dcur[CPL], dnext[CPL];
+  uint32_t ow[CPL];
+  uint32_t fbrows = 0u;                    // rows holding a near-tie pixel
 #pragma unroll
-  for (int c = 0; c < 8; ++c) { ow[c] = 0u; dcur[c] = 0.f; dnext[c] = 0.f; }
-  phi_row<R, SRC, INT, NT, 10>(P, win, cm, 0, y0 - 1, s_lt, s_ls, pm);
-  phi_row<R, SRC, INT, NT, 10>(P, win, cm, 1, y0, s_lt, s_ls, p0);
-  load_data_row<INT>(P, y0, x0, dcur);
+  for (int c = 0; c < CPL; ++c) { ow[c] = 0u; dcur[c] = 0.f; dnext[c] = 0.f; }
+  phi_row<R, SRC, INT, NT, NP>(P, win, cm, 0, y0 - 1, s_lt, s_ls, pm);
+  phi_row<R, SRC, INT, NT, NP>(P, win, cm, 1, y0, s_lt, s_ls, p0);
+  load_data_row<INT, CPL>(P, y0, x0, dcur);
+  const uint32_t* wrow = P.bits_in + (size_t)r * P.g.pitch_w + (x0 - (R + 1));
 #pragma unroll 1
   for (int k = 0; k < 32; ++k) {
     const int kk = k + 1;                  // phi row produced in this step
     if (kk == 16) {                        // switch to window base y0+16-R
 #pragma unroll
       for (int j = 0; j < NT; ++j) {
-        const int xc = x0 - (R + 1) + j;
-        win[j] = __funnelshift_r(word_at<INT>(P, r, xc), word_at<INT>(P, r + 1, xc), 16 - R);
+        if (INT) {
+          win[j] = __funnelshift_r(__ldg(wrow + j), __ldg(wrow + P.g.pitch_w + j), 16 - R);
+        } else {
+          const int xc = x0 - (R + 1) + j;
+          win[j] = __funnelshift_r(word_at<false>(P, r, xc), word_at<false>(P, r + 1, xc), 16 - R);
+        }
       }
     }
     const int m0 = kk < 16 ? kk + 1 : kk - 16;
-    if (kk < 32) load_data_row<INT>(P, y0 + kk, x0, dnext);
-    phi_row<R, SRC, INT, NT, 10>(P, win, cm, m0, y0 + kk, s_lt, s_ls, pn);
+    if (kk < 32) load_data_row<INT, CPL>(P, y0 + kk, x0, dnext);
+    phi_row<R, SRC, INT, NT, NP>(P, win, cm, m0, y0 + kk, s_lt, s_ls, pn);
     const int i = y0 + k;
     if (i < H) {
       const uint32_t bitk = 1u << k;
       uint32_t fb = 0u;
 #pragma unroll
-      for (int c = 0; c < 8; ++c) {
+      for (int c = 0; c < CPL; ++c) {
         const int x = x0 + c;
         float dx, dy;
         if (INT) {
@@ -243,25 +377,181 @@ __device__ __forceinline__ void update_block(const FastParams& P, const float* s
         if (u > 0.f) ow[c] |= bitk;
         if (fabsf(u) <= eps_u) fb |= 1u << c;
       }
-      while (fb) {                          // near-tie: exact fp64 decision
-        const int c = __ffs(fb) - 1;
-        fb &= fb - 1;
-        const double ue = exact_u(P.ctx, P.bits_in, SRC, i, x0 + c);
-        ow[c] = ue > 0.0 ? (ow[c] | bitk) : (ow[c] & ~bitk);
-      }
+      if (fb) fbrows |= bitk;               // near tie somewhere in this row
     }
 #pragma unroll
-    for (int c = 0; c < 10; ++c) { pm[c] = p0[c]; p0[c] = pn[c]; }
+    for (int c = 0; c < NP; ++c) { pm[c] = p0[c]; p0[c] = pn[c]; }
 #pragma unroll
-    for (int c = 0; c < 8; ++c) dcur[c] = dnext[c];
+    for (int c = 0; c < CPL; ++c) dcur[c] = dnext[c];
+  }
+  // near ties: the row's decisions are redone in fp64 with the reference's
+  // operation order (outside the row loop, so the call does not force the
+  // loop state through local memory); non-tie pixels re-derive the same bit
+  while (fbrows) {
+    const int k = __ffs(fbrows) - 1;
+    fbrows &= fbrows - 1;
+    const uint32_t bitk = 1u << k;
+#pragma unroll 1
+    for (int c = 0; c < CPL; ++c) {
+      if (!INT && x0 + c >= W) break;
+      const bool pos = exact_u_fast<R, SRC>(P.ctx, P.bits_in, y0 + k, x0 + c) > 0.0;
+#pragma unroll
+      for (int q = 0; q < CPL; ++q)
+        if (q == c) ow[q] = pos ? (ow[q] | bitk) : (ow[q] & ~bitk);
+    }
   }
   if (!INT) {
 #pragma unroll
-    for (int c = 0; c < 8; ++c) if (x0 + c >= W) ow[c] = 0u;
+    for (int c = 0; c < CPL; ++c) if (x0 + c >= W) ow[c] = 0u;
   }
   uint32_t* dst = P.bits_out + (size_t)r * P.g.pitch_w + x0;
-  reinterpret_cast<uint4*>(dst)[0] = make_uint4(ow[0], ow[1], ow[2], ow[3]);
-  reinterpret_cast<uint4*>(dst)[1] = make_uint4(ow[4], ow[5], ow[6], ow[7]);
+#pragma unroll
+  for (int q = 0; q < CPL / 4; ++q)
+    reinterpret_cast<uint4*>(dst)[q] = make_uint4(ow[4 * q], ow[4 * q + 1], ow[4 * q + 2], ow[4 * q + 3]);
+}
+
+// ------------------------------------------------- interior update block
+// Specialised copy of update_block for interior units (the >98% case):
+//  * LUT addressing is one SHF + one LOP3 per t: the windows are kept
+//    pre-shifted by 2 (byte offsets) and the 2 KB LUT is 2 KB-aligned in
+//    shared memory, so ((win >> m0) & mask) | base is the LDS address;
+//  * the data plane (I or g) streams through a 4-row cp.async ring in shared
+//    memory, issued 3 rows ahead, so no register copies wait on HBM.
+constexpr int kRing = 4;                        // rows in flight per warp (power of 2)
+
+__device__ __forceinline__ float lds_f32(uint32_t addr) {
+  float v;
+  asm volatile("ld.shared.f32 %0, [%1];" : "=f"(v) : "r"(addr));
+  return v;
+}
+__device__ __forceinline__ void cp_async16(uint32_t saddr, const void* g) {
+  asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(saddr), "l"(g));
+}
+__device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;"); }
+template <int N>
+__device__ __forceinline__ void cp_async_wait() { asm volatile("cp.async.wait_group %0;" ::"n"(N)); }
+
+template <int R, int NT, int NOUT>
+__device__ __forceinline__ void phi_row_int(const FastParams& P, const uint32_t (&win4)[NT],
+                                            int m0, uint32_t lut_base, float (&out)[NOUT]) {
+  constexpr uint32_t PM4 = ((1u << (2 * R + 1)) - 1u) << 2;
+#pragma unroll
+  for (int j = 0; j < NT; ++j) {
+    const float t = lds_f32(((win4[j] >> m0) & PM4) | lut_base);
+#pragma unroll
+    for (int c = 0; c < NOUT; ++c) {
+      const int d = j - c - R;
+      if (d < -R || d > R) continue;
+      const float wd = P.w32[d < 0 ? -d : d];
+      if (d == -R) out[c] = wd * t;
+      else out[c] = fmaf(wd, t, out[c]);
+    }
+  }
+}
+
+template <int R, int MODEL, int CPL>
+__device__ __forceinline__ void update_block_int(const FastParams& P, uint32_t lut_base,
+                                                 float* ring, int r, int x0, float A, float B,
+                                                 float eps_u,
+                                                 const uint32_t (&prev)[CPL + 2 * (R + 1)],
+                                                 const uint32_t (&cur)[CPL + 2 * (R + 1)]) {
+  constexpr int NT = CPL + 2 * (R + 1);
+  constexpr int NP = CPL + 2;
+  const int y0 = r * 32;
+  const float hdt = 0.5f * P.dt32;
+  const int lane = threadIdx.x & 31;
+  uint32_t win4[NT];
+#pragma unroll
+  for (int j = 0; j < NT; ++j) win4[j] = __funnelshift_r(prev[j], cur[j], 31 - R) << 2;
+  // ring slot q holds this lane's CPL floats of one row: ring[(q*32 + lane)*CPL ..]
+  const uint32_t ring_s = (uint32_t)__cvta_generic_to_shared(ring) + lane * CPL * 4;
+  const float* gdata = P.data32 + (size_t)y0 * P.g.data_pitch + x0;
+  const size_t dpitch = P.g.data_pitch;
+#pragma unroll
+  for (int q = 0; q < kRing - 1; ++q) {        // rows 0 .. kRing-2 in flight
+#pragma unroll
+    for (int v = 0; v < CPL / 4; ++v)
+      cp_async16(ring_s + q * 32 * CPL * 4 + v * 16, gdata + q * dpitch + 4 * v);
+    cp_async_commit();
+  }
+  float pm[NP], p0[NP], pn[NP];
+  uint32_t ow[CPL];
+  uint32_t fbrows = 0u;
+#pragma unroll
+  for (int c = 0; c < CPL; ++c) ow[c] = 0u;
+  phi_row_int<R, NT, NP>(P, win4, 0, lut_base, pm);
+  phi_row_int<R, NT, NP>(P, win4, 1, lut_base, p0);
+  const uint32_t* wrow = P.bits_in + (size_t)r * P.g.pitch_w + (x0 - (R + 1));
+#pragma unroll 1
+  for (int k = 0; k < 32; ++k) {
+    const int kk = k + 1;
+    {   // keep kRing-1 rows in flight (empty groups past the tile keep the count)
+      const int kn = k + kRing - 1;
+      if (kn < 32) {
+#pragma unroll
+        for (int v = 0; v < CPL / 4; ++v)
+          cp_async16(ring_s + (kn & (kRing - 1)) * 32 * CPL * 4 + v * 16,
+                     gdata + kn * dpitch + 4 * v);
+      }
+      cp_async_commit();
+    }
+    if (kk == 16) {
+#pragma unroll
+      for (int j = 0; j < NT; ++j)
+        win4[j] = __funnelshift_r(__ldg(wrow + j), __ldg(wrow + P.g.pitch_w + j), 16 - R) << 2;
+    }
+    phi_row_int<R, NT, NP>(P, win4, kk < 16 ? kk + 1 : kk - 16, lut_base, pn);
+    cp_async_wait<kRing - 1>();                 // row k has landed (this lane's copy)
+    float d[CPL];
+    {
+      const float4* rs = reinterpret_cast<const float4*>(ring + ((k & (kRing - 1)) * 32 + lane) * CPL);
+#pragma unroll
+      for (int v = 0; v < CPL / 4; ++v) {
+        const float4 q4 = rs[v];
+        d[4 * v] = q4.x; d[4 * v + 1] = q4.y; d[4 * v + 2] = q4.z; d[4 * v + 3] = q4.w;
+      }
+    }
+    const uint32_t bitk = 1u << k;
+    bool tie = false;
+#pragma unroll
+    for (int c = 0; c < CPL; ++c) {
+      const float dx = p0[c + 2] - p0[c];
+      const float dy = pn[c + 1] - pm[c + 1];
+      const float h = sqrt_approx(fmaf(dx, dx, dy * dy));
+      const float vf = (MODEL == REGION) ? fmaf(A, d[c], B) : d[c];
+      const float u = fmaf(hdt, vf * h, p0[c + 1]);
+      if (u > 0.f) ow[c] |= bitk;
+      tie |= fabsf(u) <= eps_u;
+    }
+    if (tie) fbrows |= bitk;
+#pragma unroll
+    for (int c = 0; c < NP; ++c) { pm[c] = p0[c]; p0[c] = pn[c]; }
+  }
+  cp_async_wait<0>();
+  while (fbrows) {
+    const int k = __ffs(fbrows) - 1;
+    fbrows &= fbrows - 1;
+    const uint32_t bitk = 1u << k;
+#pragma unroll 1
+    for (int c = 0; c < CPL; ++c) {
+      const bool pos = exact_u_fast<R, SRC_SMOOTH>(P.ctx, P.bits_in, y0 + k, x0 + c) > 0.0;
+#pragma unroll
+      for (int q = 0; q < CPL; ++q)
+        if (q == c) ow[q] = pos ? (ow[q] | bitk) : (ow[q] & ~bitk);
+    }
+  }
+  uint32_t* dst = P.bits_out + (size_t)r * P.g.pitch_w + x0;
+#pragma unroll
+  for (int q = 0; q < CPL / 4; ++q)
+    reinterpret_cast<uint4*>(dst)[q] = make_uint4(ow[4 * q], ow[4 * q + 1], ow[4 * q + 2], ow[4 * q + 3]);
+}
+
+// The 2 KB t-LUT must sit at a 2 KB-aligned shared address for the OR-based
+// addressing of phi_row_int; static __shared__ alignment is not guaranteed
+// relative to the CTA's shared window, so it is carved out of a 4 KB buffer.
+__device__ __forceinline__ float* aligned_lut(float* raw4k) {
+  const uint32_t a = (uint32_t)__cvta_generic_to_shared(raw4k);
+  return raw4k + (((a + 2047u) & ~2047u) - a) / 4;
 }
 
 template <int R>
@@ -273,52 +563,98 @@ __device__ __forceinline__ void load_luts(const FastParams& P, float* s_lt, floa
   }
 }
 
-// Work unit = (word-row, 256-column chunk), one warp each, grid-strided.  A
-// chunk whose every lane sees a uniform stencil window (all bits of rows
-// y0-32 .. y0+63 equal over its t columns, away from the image border) has
-// phi constant there, hence |grad phi| == 0, v == 0 and u == phi exactly, so
-// b^{n+1} == b^n: the chunk is copied without touching the data plane.
-template <int R, int MODEL, int SRC>
-__global__ void __launch_bounds__(kThreads, 4) k_update(FastParams P) {
+// Unit <-> (word-row, chunk) maps.  Interior units tile the rectangle I;
+// border units enumerate its complement (top rows, left/right chunks of the
+// middle rows, bottom rows) in a fixed order.
+__device__ __forceinline__ int rect_count(const UnitRect& I) {
+  return (I.r_hi - I.r_lo) * (I.c_hi - I.c_lo);
+}
+__device__ __forceinline__ void interior_unit(int q, const UnitRect& I, int& r, int& ch) {
+  const int w = I.c_hi - I.c_lo;
+  r = I.r_lo + q / w;
+  ch = I.c_lo + q % w;
+}
+__device__ __forceinline__ int border_count(const UnitRect& I, int HR, int nchunk) {
+  return HR * nchunk - rect_count(I);
+}
+__device__ __forceinline__ void border_unit(int q, const UnitRect& I, int nchunk, int& r, int& ch) {
+  const int top = I.r_lo * nchunk;
+  if (q < top) { r = q / nchunk; ch = q % nchunk; return; }
+  q -= top;
+  const int left = I.c_lo, per = I.c_lo + (nchunk - I.c_hi);
+  const int mid = (I.r_hi - I.r_lo) * per;
+  if (q < mid) {
+    r = I.r_lo + q / per;
+    const int k = q % per;
+    ch = k < left ? k : I.c_hi + (k - left);
+    return;
+  }
+  q -= mid;
+  r = I.r_hi + q / nchunk;
+  ch = q % nchunk;
+}
+
+__device__ __forceinline__ int grab_unit(const FastParams& P, int lane) {
+  // dynamic unit scheduling: grabs are counted from this launch's base, so the
+  // counter never needs a reset (each warp makes exactly one failing grab)
+  unsigned long long g = 0;
+  if (lane == 0) g = atomicAdd(P.work, 1ull) - P.work_base;
+  return (int)__shfl_sync(0xffffffffu, (long long)g, 0);
+}
+
+// INT = true : interior units (exact-rounded LUT, central differences, and
+// the uniform-window skip: a chunk whose every lane sees all-equal bits over
+// rows y0-32 .. y0+63 of its t columns has phi constant there, hence
+// |grad phi| == 0, v == 0 and u == phi exactly, so b^{n+1} == b^n and the
+// chunk is copied without reading the data plane).
+// INT = false: border units (zero padding, one-sided gradients).
+template <int R, int MODEL, int SRC, bool INT>
+__global__ void __launch_bounds__(kThreads, INT ? 5 : 3) k_update(FastParams P) {
+  constexpr int CPL = kUpdCols;
   constexpr int NPAT = 1 << (2 * R + 1);
-  constexpr int NT = kColsPerThread + 2 * (R + 1);
-  __shared__ float s_lt[NPAT], s_ls[NPAT];
+  constexpr int NT = CPL + 2 * (R + 1);
+  __shared__ __align__(16) float s_lt_raw[1024];
+  __shared__ float s_ls[NPAT];
+  __shared__ __align__(16) float s_ring[INT ? (kThreads / 32) * kRing * 32 * CPL : 1];
+  float* const s_lt = aligned_lut(s_lt_raw);
   const Scalars* sc = P.scal;
   if (*(volatile const int*)&sc->stop) return;
-  if (MODEL == REGION && blockIdx.x == 0 && threadIdx.x == 0 && sc->zero_vel) P.scal->degenerate = 1;
+  if (MODEL == REGION && blockIdx.x == 0 && threadIdx.x == 0 && sc->zero_vel)
+    P.scal->degenerate = 1;
   const float A = sc->A, B = sc->B, eps_u = sc->eps_u;
   load_luts<R>(P, s_lt, s_ls);
   __syncthreads();
   const int lane = threadIdx.x & 31;
-  const int nwarp = gridDim.x * (blockDim.x >> 5);
-  const int nunits = P.g.HR * P.nchunk;
-  for (int unit = blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5); unit < nunits;
-       unit += nwarp) {
-    const int r = unit / P.nchunk;
-    const int cx = (unit - r * P.nchunk) * kChunk;
-    const int x0 = cx + kColsPerThread * lane;
-    const int y0 = r * 32;
-    const bool interior = SRC == SRC_SMOOTH && y0 - 1 - R >= 0 && y0 + 32 + R <= P.g.H - 1 &&
-                          cx - (R + 1) >= 0 && cx + kChunk - 1 + (R + 1) <= P.g.W - 1;
+  const int nunits = INT ? rect_count(P.ru) : border_count(P.ru, P.g.HR, P.nchunk_u);
+  for (;;) {
+    const int unit = grab_unit(P, lane);
+    if (unit >= nunits) break;
+    int r, ch;
+    if (INT) interior_unit(unit, P.ru, r, ch);
+    else border_unit(unit, P.ru, P.nchunk_u, r, ch);
+    const int x0 = ch * kUpdChunk + CPL * lane;
     uint32_t prev[NT], cur[NT];
-    if (interior) {
+    if (INT) {
+      const uint32_t* wp = P.bits_in + (size_t)(r - 1) * P.g.pitch_w + (x0 - (R + 1));
       uint32_t a = ~0u, o = 0u;
 #pragma unroll
       for (int j = 0; j < NT; ++j) {
-        const int xc = x0 - (R + 1) + j;
-        prev[j] = word_at<true>(P, r - 1, xc);
-        cur[j] = word_at<true>(P, r, xc);
-        const uint32_t nx = word_at<true>(P, r + 1, xc);
-        a &= prev[j] & cur[j] & nx;
-        o |= prev[j] | cur[j] | nx;
+        prev[j] = __ldg(wp + j);
+        cur[j] = __ldg(wp + P.g.pitch_w + j);
+        if (P.skip_uniform) {
+          const uint32_t nx = __ldg(wp + 2 * (size_t)P.g.pitch_w + j);
+          a &= prev[j] & cur[j] & nx;
+          o |= prev[j] | cur[j] | nx;
+        }
       }
       if (P.skip_uniform && __all_sync(0xffffffffu, a == ~0u || o == 0u)) {
         uint32_t* dst = P.bits_out + (size_t)r * P.g.pitch_w + x0;
-        reinterpret_cast<uint4*>(dst)[0] = make_uint4(cur[R + 1], cur[R + 2], cur[R + 3], cur[R + 4]);
-        reinterpret_cast<uint4*>(dst)[1] = make_uint4(cur[R + 5], cur[R + 6], cur[R + 7], cur[R + 8]);
+#pragma unroll
+        for (int q = 0; q < CPL / 4; ++q)
+          reinterpret_cast<uint4*>(dst)[q] = make_uint4(cur[R + 1 + 4 * q], cur[R + 2 + 4 * q],
+                                                        cur[R + 3 + 4 * q], cur[R + 4 + 4 * q]);
         continue;
       }
-      update_block<R, MODEL, SRC, true>(P, s_lt, s_ls, r, x0, A, B, eps_u, prev, cur);
     } else {
       if (x0 >= P.g.W) continue;
 #pragma unroll
@@ -327,8 +663,13 @@ __global__ void __launch_bounds__(kThreads, 4) k_update(FastParams P) {
         prev[j] = word_at<false>(P, r - 1, xc);
         cur[j] = word_at<false>(P, r, xc);
       }
-      update_block<R, MODEL, SRC, false>(P, s_lt, s_ls, r, x0, A, B, eps_u, prev, cur);
     }
+    if (INT && SRC == SRC_SMOOTH)
+      update_block_int<R, MODEL, CPL>(P, (uint32_t)__cvta_generic_to_shared(s_lt),
+                                      s_ring + (threadIdx.x >> 5) * kRing * 32 * CPL, r, x0, A, B,
+                                      eps_u, prev, cur);
+    else
+      update_block<R, MODEL, SRC, INT, CPL>(P, s_lt, s_ls, r, x0, A, B, eps_u, prev, cur);
   }
 }
 
@@ -447,7 +788,8 @@ __device__ void finalize_cta(const TilePartial* part, int n, Scalars* sc, bool d
 // incremental c+/c- sums, checkpoint mask {phi > 0} with the mismatch count.
 template <int R, bool INT>
 __device__ __forceinline__ void partition_block(const FastParams& P, const float* s_lt,
-                                                const float* s_ls, int r, int x0, float eps_phi,
+                                                const float* s_ls, uint32_t lut_base, int r,
+                                                int x0, float eps_phi,
                                                 const uint32_t (&prev)[8 + 2 * R],
                                                 const uint32_t (&cur)[8 + 2 * R],
                                                 uint32_t (&pw)[8], uint32_t (&mw)[8]) {
@@ -460,8 +802,10 @@ __device__ __forceinline__ void partition_block(const FastParams& P, const float
     const int xc = x0 - R + j;
     cm[j] = (INT || (xc >= 0 && xc < W)) ? 0xffffffffu : 0u;
     win[j] = __funnelshift_r(prev[j], cur[j], 32 - R);     // base row y0-R
+    if (INT) win[j] <<= 2;                                  // byte offsets for phi_row_int
   }
   float ph[8];
+  uint32_t fbrows = 0u;
 #pragma unroll
   for (int c = 0; c < 8; ++c) { pw[c] = 0u; mw[c] = 0u; }
 #pragma unroll 1
@@ -471,78 +815,103 @@ __device__ __forceinline__ void partition_block(const FastParams& P, const float
       for (int j = 0; j < NT; ++j) {
         const int xc = x0 - R + j;
         win[j] = __funnelshift_r(word_at<INT>(P, r, xc), word_at<INT>(P, r + 1, xc), 16 - R);
+        if (INT) win[j] <<= 2;
       }
     }
     const int i = y0 + k;
     if (i >= H) break;
-    phi_row<R, SRC_SMOOTH, INT, NT, 8>(P, win, cm, k < 16 ? k : k - 16, i, s_lt, s_ls, ph);
+    if (INT) phi_row_int<R, NT, 8>(P, win, k < 16 ? k : k - 16, lut_base, ph);
+    else phi_row<R, SRC_SMOOTH, INT, NT, 8>(P, win, cm, k < 16 ? k : k - 16, i, s_lt, s_ls, ph);
     const uint32_t bitk = 1u << k;
-    uint32_t fb = 0u;
+    bool tie = false;
 #pragma unroll
     for (int c = 0; c < 8; ++c) {
       if (!INT && x0 + c >= W) continue;
-      if (ph[c] > 0.f) { pw[c] |= bitk; mw[c] |= bitk; }
-      if (fabsf(ph[c]) <= eps_phi) fb |= 1u << c;
+      if (ph[c] > 0.f) pw[c] |= bitk;
+      tie |= fabsf(ph[c]) <= eps_phi;
     }
-    while (fb) {
-      const int c = __ffs(fb) - 1;
-      fb &= fb - 1;
-      const double e = exact_phi(P.ctx, P.bits_in, SRC_SMOOTH, i, x0 + c);
-      atomicAdd(&P.scal->fallbacks, 1ull);
-      pw[c] = e >= 0.0 ? (pw[c] | bitk) : (pw[c] & ~bitk);
-      mw[c] = e > 0.0 ? (mw[c] | bitk) : (mw[c] & ~bitk);
+    if (tie) fbrows |= bitk;
+  }
+#pragma unroll
+  for (int c = 0; c < 8; ++c) mw[c] = pw[c];               // phi > 0 unless phi == 0 (tie path)
+  // near ties: exact fp64 sign for every column of the flagged rows
+  while (fbrows) {
+    const int k = __ffs(fbrows) - 1;
+    fbrows &= fbrows - 1;
+    const uint32_t bitk = 1u << k;
+#pragma unroll 1
+    for (int c = 0; c < 8; ++c) {
+      if (!INT && x0 + c >= W) break;
+      const double e = exact_phi_fast<R>(P.ctx, P.bits_in, y0 + k, x0 + c);
+#pragma unroll
+      for (int q = 0; q < 8; ++q) {
+        if (q == c) {
+          pw[q] = e >= 0.0 ? (pw[q] | bitk) : (pw[q] & ~bitk);
+          mw[q] = e > 0.0 ? (mw[q] | bitk) : (mw[q] & ~bitk);
+        }
+      }
     }
   }
 }
 
-// Work unit = (word-row, segment of kSegChunks chunks), one warp each; the
-// warp's deltas over the segment form one partial (fixed geometry =>
-// deterministic and independent of how the rows are split across GPUs).
-template <int R, bool PART, bool CKPT, bool MASKONLY>
+// Interior units = (word-row, segment of seg_chunks chunks); border units =
+// single chunks.  Each unit's deltas form one partial; partials are laid
+// out [interior units][border units] (fixed geometry => deterministic).
+// The interior launch runs last and its last CTA reduces all partials.
+template <int R, bool PART, bool CKPT, bool MASKONLY, bool INT>
 __global__ void __launch_bounds__(kThreads, 4) k_partition(FastParams P) {
   constexpr int NPAT = 1 << (2 * R + 1);
   constexpr int NT = kColsPerThread + 2 * R;
-  __shared__ float s_lt[NPAT], s_ls[NPAT];
+  __shared__ __align__(16) float s_lt_raw[1024];
+  __shared__ float s_ls[NPAT];
   __shared__ unsigned int s_ticket;
+  float* const s_lt = aligned_lut(s_lt_raw);
   Scalars* sc = P.scal;
   if (!MASKONLY && *(volatile const int*)&sc->stop) return;
   const float eps_phi = sc->eps_phi;
   load_luts<R>(P, s_lt, s_ls);
   __syncthreads();
   const int lane = threadIdx.x & 31;
-  const int nwarp = gridDim.x * (blockDim.x >> 5);
-  const int nunits = P.g.HR * P.nseg;
-  for (int unit = blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5); unit < nunits;
-       unit += nwarp) {
-    const int r = unit / P.nseg;
-    const int seg = unit - r * P.nseg;
+  const int nseg = P.nseg;
+  const int nunits = INT ? (P.rp.r_hi - P.rp.r_lo) * nseg
+                         : border_count(P.rp, P.g.HR, P.nchunk);
+  for (;;) {
+    const int unit = grab_unit(P, lane);
+    if (unit >= nunits) break;
+    int r, ch0, ch1;
+    if (INT) {
+      r = P.rp.r_lo + unit / nseg;
+      ch0 = P.rp.c_lo + (unit % nseg) * P.seg_chunks;
+      ch1 = min(ch0 + P.seg_chunks, P.rp.c_hi);
+    } else {
+      border_unit(unit, P.rp, P.nchunk, r, ch0);
+      ch1 = ch0 + 1;
+    }
+    const int y0 = r * 32;
     double a_in = 0.0, a_out = 0.0;
     long long n_in = 0, n_out = 0;
     unsigned long long mism = 0;
-    for (int ch = seg * kSegChunks; ch < (seg + 1) * kSegChunks && ch < P.nchunk; ++ch) {
-      const int cx = ch * kChunk;
-      const int x0 = cx + kColsPerThread * lane;
-      const int y0 = r * 32;
-      const bool interior = y0 - R >= 0 && y0 + 31 + R <= P.g.H - 1 && cx - R >= 0 &&
-                            cx + kChunk - 1 + R <= P.g.W - 1;
+    for (int ch = ch0; ch < ch1; ++ch) {
+      const int x0 = ch * kChunk + kColsPerThread * lane;
       uint32_t pw[8], mw[8], prev[NT], cur[NT];
-      if (interior) {
+      if (INT) {
         uint32_t a = ~0u, o = 0u;
 #pragma unroll
         for (int j = 0; j < NT; ++j) {
           const int xc = x0 - R + j;
           prev[j] = word_at<true>(P, r - 1, xc);
           cur[j] = word_at<true>(P, r, xc);
-          const uint32_t nx = word_at<true>(P, r + 1, xc);
-          a &= prev[j] & cur[j] & nx;
-          o |= prev[j] | cur[j] | nx;
+          if (P.skip_uniform) {
+            const uint32_t nx = word_at<true>(P, r + 1, xc);
+            a &= prev[j] & cur[j] & nx;
+            o |= prev[j] | cur[j] | nx;
+          }
         }
         if (P.skip_uniform && __all_sync(0xffffffffu, a == ~0u || o == 0u)) {
-          // phi = +-c everywhere in the block: sign(phi) = b
 #pragma unroll
-          for (int c = 0; c < 8; ++c) pw[c] = mw[c] = cur[R + c];
+          for (int c = 0; c < 8; ++c) pw[c] = mw[c] = cur[R + c];   // sign(phi) = b
         } else {
-          partition_block<R, true>(P, s_lt, s_ls, r, x0, eps_phi, prev, cur, pw, mw);
+          partition_block<R, true>(P, s_lt, s_ls, (uint32_t)__cvta_generic_to_shared(s_lt), r, x0, eps_phi, prev, cur, pw, mw);
         }
       } else {
         if (x0 >= P.g.W) continue;
@@ -552,7 +921,7 @@ __global__ void __launch_bounds__(kThreads, 4) k_partition(FastParams P) {
           prev[j] = word_at<false>(P, r - 1, xc);
           cur[j] = word_at<false>(P, r, xc);
         }
-        partition_block<R, false>(P, s_lt, s_ls, r, x0, eps_phi, prev, cur, pw, mw);
+        partition_block<R, false>(P, s_lt, s_ls, 0u, r, x0, eps_phi, prev, cur, pw, mw);
         if (x0 + 8 > P.g.W) {
 #pragma unroll
           for (int c = 0; c < 8; ++c) if (x0 + c >= P.g.W) { pw[c] = 0u; mw[c] = 0u; }
@@ -571,11 +940,11 @@ __global__ void __launch_bounds__(kThreads, 4) k_partition(FastParams P) {
         uint32_t any = 0u;
 #pragma unroll
         for (int c = 0; c < 8; ++c) {
-          uint32_t ch2 = old[c] ^ pw[c];
-          any |= ch2;
-          while (ch2) {
-            const int b = __ffs(ch2) - 1;
-            ch2 &= ch2 - 1;
+          uint32_t chg = old[c] ^ pw[c];
+          any |= chg;
+          while (chg) {
+            const int b = __ffs(chg) - 1;
+            chg &= chg - 1;
             const double I = data_exact(P.ctx, y0 + b, x0 + c);
             if ((pw[c] >> b) & 1u) { a_in += I; ++n_in; }
             else { a_out += I; ++n_out; }
@@ -597,7 +966,6 @@ __global__ void __launch_bounds__(kThreads, 4) k_partition(FastParams P) {
       }
     }
     if (MASKONLY) continue;
-    // warp partial for this unit (fixed xor-shuffle order)
 #pragma unroll
     for (int o = 16; o > 0; o >>= 1) {
       a_in += __shfl_xor_sync(0xffffffffu, a_in, o);
@@ -613,10 +981,10 @@ __global__ void __launch_bounds__(kThreads, 4) k_partition(FastParams P) {
       t.n_a = n_in;
       t.n_b = n_out;
       t.mism = mism;
-      P.part[unit] = t;
+      P.part[INT ? unit : P.n_int_part + unit] = t;
     }
   }
-  if (MASKONLY) return;
+  if (MASKONLY || !INT) return;
   // last CTA to finish reduces every unit partial (threadFenceReduction idiom)
   __syncthreads();
   if (threadIdx.x == 0) {
@@ -626,7 +994,8 @@ __global__ void __launch_bounds__(kThreads, 4) k_partition(FastParams P) {
   __syncthreads();
   if (s_ticket == gridDim.x - 1) {
     __threadfence();
-    finalize_cta(P.part, nunits, sc, /*delta=*/true, PART, CKPT, P.iter);
+    finalize_cta(P.part, P.n_int_part + border_count(P.rp, P.g.HR, P.nchunk), sc,
+                 /*delta=*/true, PART, CKPT, P.iter);
   }
 }
 
