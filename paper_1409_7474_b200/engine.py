@@ -348,6 +348,10 @@ class EvolutionRun:
             converged=bool(st.converged), degenerate=bool(st.degenerate),
             trace=None)
 
+    def set_native_option(self, name: str, value: int) -> None:
+        """Tune the device run (e.g. "skip_uniform" 0/1); results are unchanged."""
+        N.check(N.lib.lse_run_set_option(self._dev.h, name.encode(), int(value)))
+
     def fallback_count(self) -> int:
         """fp64 re-evaluations of near-tie pixels so far (diagnostics)."""
         return int(self._dev.status().exact_fallbacks)

@@ -165,3 +165,21 @@ def test_c5_density_crop_matches_oracle(size, iters):
                       iters)
     assert ref.iteration == iters
     assert np.array_equal(phi, ref.phi)
+
+
+@pytest.mark.parametrize("model", ["region", "edge"])
+def test_uniform_skip_is_bit_identical_to_dense(model):
+    """The exact uniform-window skip must not change a single bit."""
+    sc = scenes.config5_crop(1024, 60)
+    kw = dict(sc.params)
+    if model == "edge":
+        kw.update(sigma1=1.0, ts_pre=9)
+    prm = L.default_params(L.ModelKind.from_name(model), **kw)
+    seeds = L.SeedSpec(polygons=sc.polygons, inside_sign=sc.inside_sign)
+    out = []
+    for skip in (0, 1):
+        r = L.EvolutionRun(sc.image, seeds, prm)
+        r.set_native_option("skip_uniform", skip)
+        r.advance(60)
+        out.append(r.state.phi)
+    assert np.array_equal(out[0], out[1])
