@@ -530,7 +530,7 @@ int upload_image(lse_run* r, const void* image, int is_f32) {
     CKL();
     if (!r->d_data64) TRY(dalloc(&r->d_data64, (size_t)pitch * H));
     k_edge_g<<<grid2(W, H), 128, 0, r->st>>>(S, H, W, r->p.edge_gain, r->d_data64, r->d_data32,
-                                              pitch);
+                                              pitch, 0.5 * r->p.dt);
     CKL();
     CK(cudaStreamSynchronize(r->st));
     cudaFree(T);
@@ -1078,7 +1078,7 @@ int lse_edge_function(const double* image, long long h, long long w, const doubl
   CK(cudaMemcpy(a.p, image, n * sizeof(double), cudaMemcpyHostToDevice));
   TRY(conv_device((double*)a.p, (double*)b.p, (double*)c.p, (int)h, (int)w, weights, ts));
   k_edge_g<<<grid2((int)w, (int)h), 128>>>((double*)c.p, (int)h, (int)w, gain, (double*)a.p,
-                                           nullptr, w);
+                                           nullptr, w, 1.0);
   CKL();
   CK(cudaMemcpy(g_out, a.p, n * sizeof(double), cudaMemcpyDeviceToHost));
   return LSE_OK;

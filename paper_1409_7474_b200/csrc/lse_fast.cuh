@@ -319,7 +319,6 @@ __device__ __forceinline__ void update_block(const FastParams& P, const float* s
   constexpr int NP = CPL + 2;             // phi columns x0-1 .. x0+CPL
   const int H = P.g.H, W = P.g.W;
   const int y0 = r * 32;
-  const float hdt = 0.5f * P.dt32;        // h below is 2|grad phi|
   uint32_t cm[NT], win[NT];
 #pragma unroll
   for (int j = 0; j < NT; ++j) {
@@ -372,8 +371,9 @@ __device__ __forceinline__ void update_block(const FastParams& P, const float* s
                         : (i == H - 1) ? 2.f * (p0[c + 1] - pm[c + 1]) : (pn[c + 1] - pm[c + 1]);
         }
         const float h = sqrt_approx(fmaf(dx, dx, dy * dy));
+        // h = 2|grad phi|; A, B (region) and the g plane (edge) carry dt/2
         const float vf = (MODEL == REGION) ? fmaf(A, dcur[c], B) : dcur[c];
-        const float u = fmaf(hdt, vf * h, p0[c + 1]);
+        const float u = fmaf(vf, h, p0[c + 1]);
         if (u > 0.f) ow[c] |= bitk;
         if (fabsf(u) <= eps_u) fb |= 1u << c;
       }
@@ -458,7 +458,6 @@ __device__ __forceinline__ void update_block_int(const FastParams& P, uint32_t l
   constexpr int NT = CPL + 2 * (R + 1);
   constexpr int NP = CPL + 2;
   const int y0 = r * 32;
-  const float hdt = 0.5f * P.dt32;
   const int lane = threadIdx.x & 31;
   uint32_t win4[NT];
 #pragma unroll
@@ -479,10 +478,11 @@ __device__ __forceinline__ void update_block_int(const FastParams& P, uint32_t l
   uint32_t fbrows = 0u;
 #pragma unroll
   for (int c = 0; c < CPL; ++c) ow[c] = 0u;
+  (void)eps_u;
   phi_row_int<R, NT, NP>(P, win4, 0, lut_base, pm);
   phi_row_int<R, NT, NP>(P, win4, 1, lut_base, p0);
   const uint32_t* wrow = P.bits_in + (size_t)r * P.g.pitch_w + (x0 - (R + 1));
-#pragma unroll 1
+#pragma unroll 2
   for (int k = 0; k < 32; ++k) {
     const int kk = k + 1;
     {   // keep kRing-1 rows in flight (empty groups past the tile keep the count)
@@ -511,23 +511,26 @@ __device__ __forceinline__ void update_block_int(const FastParams& P, uint32_t l
         d[4 * v] = q4.x; d[4 * v + 1] = q4.y; d[4 * v + 2] = q4.z; d[4 * v + 3] = q4.w;
       }
     }
-    const uint32_t bitk = 1u << k;
-    bool tie = false;
+    float umin = 3.0e38f;
 #pragma unroll
     for (int c = 0; c < CPL; ++c) {
       const float dx = p0[c + 2] - p0[c];
       const float dy = pn[c + 1] - pm[c + 1];
-      const float h = sqrt_approx(fmaf(dx, dx, dy * dy));
+      const float h = sqrt_approx(fmaf(dx, dx, dy * dy));          // 2|grad phi|
+      // A, B (region) and the g plane (edge) carry the factor dt/2
       const float vf = (MODEL == REGION) ? fmaf(A, d[c], B) : d[c];
-      const float u = fmaf(hdt, vf * h, p0[c + 1]);
-      if (u > 0.f) ow[c] |= bitk;
-      tie |= fabsf(u) <= eps_u;
+      const float u = fmaf(vf, h, p0[c + 1]);
+      // sign bits shift in from the bottom; bit order is reversed once at the end
+      ow[c] = __funnelshift_l(__float_as_uint(u), ow[c], 1);
+      umin = fminf(umin, fabsf(u));
     }
-    if (tie) fbrows |= bitk;
+    if (umin <= eps_u) fbrows |= 1u << k;
 #pragma unroll
     for (int c = 0; c < NP; ++c) { pm[c] = p0[c]; p0[c] = pn[c]; }
   }
   cp_async_wait<0>();
+#pragma unroll
+  for (int c = 0; c < CPL; ++c) ow[c] = ~__brev(ow[c]);   // bit k = (u_k >= +0) = (u_k > 0) off ties
   while (fbrows) {
     const int k = __ffs(fbrows) - 1;
     fbrows &= fbrows - 1;
@@ -699,8 +702,8 @@ __device__ inline void region_coeffs(Scalars* sc) {
     } else {
       double a = 2.0 * dc / peak;
       double b = -dc * (cp + cm) / peak;
-      sc->A = (float)a;
-      sc->B = (float)b;
+      sc->A = (float)(0.5 * dt * a);    // kernels evaluate u = phi + (A I + B) * 2|grad phi|
+      sc->B = (float)(0.5 * dt * b);
       double eps_d = 0x1p-21 * (fabs(a) * sc->img_absmax + fabs(b) + 1.0);
       sc->eps_u = (float)(4.0 * (0x1p-18 + dt * (0x1p-16 + 1.5 * eps_d + 0x1p-21) +
                                  0x1p-22 * (1.0 + 1.5 * dt)));
@@ -819,18 +822,32 @@ __device__ __forceinline__ void partition_block(const FastParams& P, const float
       }
     }
     const int i = y0 + k;
-    if (i >= H) break;
-    if (INT) phi_row_int<R, NT, 8>(P, win, k < 16 ? k : k - 16, lut_base, ph);
-    else phi_row<R, SRC_SMOOTH, INT, NT, 8>(P, win, cm, k < 16 ? k : k - 16, i, s_lt, s_ls, ph);
-    const uint32_t bitk = 1u << k;
-    bool tie = false;
+    if (!INT && i >= H) break;
+    if (INT) {
+      phi_row_int<R, NT, 8>(P, win, k < 16 ? k : k - 16, lut_base, ph);
+      float pmin = 3.0e38f;
 #pragma unroll
-    for (int c = 0; c < 8; ++c) {
-      if (!INT && x0 + c >= W) continue;
-      if (ph[c] > 0.f) pw[c] |= bitk;
-      tie |= fabsf(ph[c]) <= eps_phi;
+      for (int c = 0; c < 8; ++c) {
+        pw[c] = __funnelshift_l(__float_as_uint(ph[c]), pw[c], 1);   // sign bits, reversed
+        pmin = fminf(pmin, fabsf(ph[c]));
+      }
+      if (pmin <= eps_phi) fbrows |= 1u << k;
+    } else {
+      phi_row<R, SRC_SMOOTH, INT, NT, 8>(P, win, cm, k < 16 ? k : k - 16, i, s_lt, s_ls, ph);
+      const uint32_t bitk = 1u << k;
+      bool tie = false;
+#pragma unroll
+      for (int c = 0; c < 8; ++c) {
+        if (x0 + c >= W) continue;
+        if (ph[c] > 0.f) pw[c] |= bitk;
+        tie |= fabsf(ph[c]) <= eps_phi;
+      }
+      if (tie) fbrows |= bitk;
     }
-    if (tie) fbrows |= bitk;
+  }
+  if (INT) {
+#pragma unroll
+    for (int c = 0; c < 8; ++c) pw[c] = ~__brev(pw[c]);    // bit k = phi_k >= +0 off ties
   }
 #pragma unroll
   for (int c = 0; c < 8; ++c) mw[c] = pw[c];               // phi > 0 unless phi == 0 (tie path)

@@ -72,8 +72,10 @@ __device__ __forceinline__ void np_gradient(const double* f, int H, int W, int i
 }
 
 // edge indicator (models.py:78-81) from the smoothed image S
+// g32 (the fast path's data plane) is stored pre-multiplied by g32_scale = dt/2.
 __global__ void k_edge_g(const double* __restrict__ S, int H, int W, double gain,
-                         double* __restrict__ g64, float* __restrict__ g32, long long pitch) {
+                         double* __restrict__ g64, float* __restrict__ g32, long long pitch,
+                         double g32_scale) {
   const int x = blockIdx.x * blockDim.x + threadIdx.x;
   const int i = blockIdx.y;
   if (x >= W) return;
@@ -82,7 +84,7 @@ __global__ void k_edge_g(const double* __restrict__ S, int H, int W, double gain
   const double a = dmul(gain, fx), b = dmul(gain, fy);
   const double g = ddiv(1.0, dadd(dadd(1.0, dmul(a, a)), dmul(b, b)));
   if (g64) g64[(size_t)i * pitch + x] = g;
-  if (g32) g32[(size_t)i * pitch + x] = (float)g;
+  if (g32) g32[(size_t)i * pitch + x] = (float)(g * g32_scale);
 }
 
 __global__ void k_gradient(const double* __restrict__ f, int H, int W, double* fx_out,
