@@ -249,7 +249,7 @@ int prepare(lse_run* r) {
   if (r->p.model == LSE_MODEL_REGION) {
     TRY(launch_partition_abs(r, r->mode == SRC_FIELD ? SRC_FIELD : r->mode, true, false, false,
                              r->d_M));
-    k_finalize<<<1, kThreads, 0, r->st>>>(r->d_part, r->g.ntiles, r->d_scal, 0, 1, 0,
+    k_finalize<<<1, 1024, 0, r->st>>>(r->d_part, r->g.ntiles, r->d_scal, 0, 1, 0,
                                           r->iteration);
     CKL();
   }
@@ -301,12 +301,18 @@ int launch_partition(lse_run* r, FastParams P) {
     k_partition<R, PART, CKPT, MASKONLY, false><<<g, kThreads, 0, r->st>>>(P);
     CKL();
   }
-  // the interior launch always runs (possibly with no units): its last CTA
-  // reduces all partials and writes the next update's coefficients
-  const int g = fast_grid(std::max<long long>(1, r->ni_part));
-  P.work_base = take_work(r, r->ni_part, g);
-  k_partition<R, PART, CKPT, MASKONLY, true><<<g, kThreads, 0, r->st>>>(P);
-  CKL();
+  if (r->ni_part > 0) {
+    const int g = fast_grid(r->ni_part);
+    P.work_base = take_work(r, r->ni_part, g);
+    k_partition<R, PART, CKPT, MASKONLY, true><<<g, kThreads, 0, r->st>>>(P);
+    CKL();
+  }
+  if (!MASKONLY) {
+    // fixed-order reduction of all unit partials -> next update's coefficients
+    k_finalize_run<<<1, 1024, 0, r->st>>>(r->d_part, (int)(r->ni_part + r->nb_part), r->d_scal,
+                                          PART ? 1 : 0, CKPT ? 1 : 0, P.iter);
+    CKL();
+  }
   return LSE_OK;
 }
 
@@ -457,7 +463,7 @@ int generic_iteration(lse_run* r, long long it, bool reinit_now, bool reg_now, b
     k_partition_abs<<<grid, r->nthr, 0, r->st>>>(field, r->d_bits[r->cur], r->d_ctx, SRC_FIELD,
                                                  r->d_P, r->d_M, region, ckpt, 0, r->d_part, r->g);
     CKL();
-    k_finalize<<<1, kThreads, 0, r->st>>>(r->d_part, r->g.ntiles, r->d_scal, 0, region, ckpt, it);
+    k_finalize<<<1, 1024, 0, r->st>>>(r->d_part, r->g.ntiles, r->d_scal, 0, region, ckpt, it);
     CKL();
   }
   r->iteration = it;
@@ -1055,7 +1061,7 @@ int region_scalars(const double* d_img, const double* d_phi, int H, int W, Scala
   CKL();
   k_region_sums<<<blocks, 256>>>(d_img, d_phi, n, (TilePartial*)part.p);
   CKL();
-  k_finalize<<<1, kThreads>>>((TilePartial*)part.p, blocks, d_sc, 0, 1, 0, 0);
+  k_finalize<<<1, 1024>>>((TilePartial*)part.p, blocks, d_sc, 0, 1, 0, 0);
   CKL();
   CK(cudaMemcpy(h_sc, d_sc, sizeof(Scalars), cudaMemcpyDeviceToHost));
   return LSE_OK;

@@ -462,16 +462,18 @@ __device__ __forceinline__ void update_block_int(const FastParams& P, uint32_t l
   uint32_t win4[NT];
 #pragma unroll
   for (int j = 0; j < NT; ++j) win4[j] = __funnelshift_r(prev[j], cur[j], 31 - R) << 2;
-  // ring slot q holds this lane's CPL floats of one row: ring[(q*32 + lane)*CPL ..]
+  // ring slot q holds this lane's CPL floats of one row at byte
+  // ring_s + q * kSlot (kSlot = one row of the warp = 32 * CPL floats)
+  constexpr uint32_t kSlot = 32 * CPL * 4;
   const uint32_t ring_s = (uint32_t)__cvta_generic_to_shared(ring) + lane * CPL * 4;
-  const float* gdata = P.data32 + (size_t)y0 * P.g.data_pitch + x0;
   const size_t dpitch = P.g.data_pitch;
+  const float* gsrc = P.data32 + (size_t)y0 * dpitch + x0;
 #pragma unroll
   for (int q = 0; q < kRing - 1; ++q) {        // rows 0 .. kRing-2 in flight
 #pragma unroll
-    for (int v = 0; v < CPL / 4; ++v)
-      cp_async16(ring_s + q * 32 * CPL * 4 + v * 16, gdata + q * dpitch + 4 * v);
+    for (int v = 0; v < CPL / 4; ++v) cp_async16(ring_s + q * kSlot + v * 16, gsrc + 4 * v);
     cp_async_commit();
+    gsrc += dpitch;
   }
   float pm[NP], p0[NP], pn[NP];
   uint32_t ow[CPL];
@@ -482,16 +484,15 @@ __device__ __forceinline__ void update_block_int(const FastParams& P, uint32_t l
   phi_row_int<R, NT, NP>(P, win4, 0, lut_base, pm);
   phi_row_int<R, NT, NP>(P, win4, 1, lut_base, p0);
   const uint32_t* wrow = P.bits_in + (size_t)r * P.g.pitch_w + (x0 - (R + 1));
-#pragma unroll 2
+#pragma unroll 4
   for (int k = 0; k < 32; ++k) {
     const int kk = k + 1;
     {   // keep kRing-1 rows in flight (empty groups past the tile keep the count)
-      const int kn = k + kRing - 1;
-      if (kn < 32) {
+      if (k + kRing - 1 < 32) {
+        const uint32_t dsts = ring_s + ((k + kRing - 1) & (kRing - 1)) * kSlot;
 #pragma unroll
-        for (int v = 0; v < CPL / 4; ++v)
-          cp_async16(ring_s + (kn & (kRing - 1)) * 32 * CPL * 4 + v * 16,
-                     gdata + kn * dpitch + 4 * v);
+        for (int v = 0; v < CPL / 4; ++v) cp_async16(dsts + v * 16, gsrc + 4 * v);
+        gsrc += dpitch;
       }
       cp_async_commit();
     }
@@ -504,10 +505,12 @@ __device__ __forceinline__ void update_block_int(const FastParams& P, uint32_t l
     cp_async_wait<kRing - 1>();                 // row k has landed (this lane's copy)
     float d[CPL];
     {
-      const float4* rs = reinterpret_cast<const float4*>(ring + ((k & (kRing - 1)) * 32 + lane) * CPL);
+      const uint32_t srcs = ring_s + (k & (kRing - 1)) * kSlot;
 #pragma unroll
       for (int v = 0; v < CPL / 4; ++v) {
-        const float4 q4 = rs[v];
+        float4 q4;
+        asm volatile("ld.shared.v4.f32 {%0, %1, %2, %3}, [%4];"
+                     : "=f"(q4.x), "=f"(q4.y), "=f"(q4.z), "=f"(q4.w) : "r"(srcs + v * 16));
         d[4 * v] = q4.x; d[4 * v + 1] = q4.y; d[4 * v + 2] = q4.z; d[4 * v + 3] = q4.w;
       }
     }
@@ -716,13 +719,21 @@ __device__ inline void region_coeffs(Scalars* sc) {
   }
 }
 
-// Whole-CTA reduction of the tile partials in a fixed order, then the
-// scalar bookkeeping (single thread).
+// Whole-CTA reduction of the unit partials in a fixed order (each thread a
+// contiguous range, then a fixed xor-shuffle tree, then warps in index order;
+// deterministic for a given n and blockDim), followed by the scalar
+// bookkeeping on one thread.  Launched as its own 1-CTA x 1024-thread kernel.
+__device__ __forceinline__ void dd_shfl_add(double& hi, double& lo, int o) {
+  const double h2 = __shfl_xor_sync(0xffffffffu, hi, o);
+  const double l2 = __shfl_xor_sync(0xffffffffu, lo, o);
+  dd_add_dd(hi, lo, h2, l2);
+}
+
 __device__ void finalize_cta(const TilePartial* part, int n, Scalars* sc, bool delta, bool region,
                              bool ckpt, long long iter) {
-  __shared__ double f_ah[kThreads], f_al[kThreads], f_bh[kThreads], f_bl[kThreads];
-  __shared__ long long f_na[kThreads], f_nb[kThreads];
-  __shared__ unsigned long long f_mm[kThreads];
+  __shared__ double f_ah[32], f_al[32], f_bh[32], f_bl[32];
+  __shared__ long long f_na[32], f_nb[32];
+  __shared__ unsigned long long f_mm[32];
   const int T = blockDim.x, tid = threadIdx.x;
   double ah = 0, al = 0, bh = 0, bl = 0;
   long long na = 0, nb = 0;
@@ -730,49 +741,81 @@ __device__ void finalize_cta(const TilePartial* part, int n, Scalars* sc, bool d
   const int per = (n + T - 1) / T;
   const int lo = tid * per;
   const int hi = lo + per < n ? lo + per : n;
-  for (int t = lo; t < hi; ++t) {
-    const TilePartial* q = part + t;
-    dd_add_dd(ah, al, __ldcg(&q->a_hi), __ldcg(&q->a_lo));
-    dd_add_dd(bh, bl, __ldcg(&q->b_hi), __ldcg(&q->b_lo));
-    na += __ldcg(&q->n_a);
-    nb += __ldcg(&q->n_b);
-    mm += __ldcg(&q->mism);
-  }
-  f_ah[tid] = ah; f_al[tid] = al; f_bh[tid] = bh; f_bl[tid] = bl;
-  f_na[tid] = na; f_nb[tid] = nb; f_mm[tid] = mm;
-  __syncthreads();
-  for (int s = T / 2; s > 0; s >>= 1) {
-    if (tid < s) {
-      double h1 = f_ah[tid], l1 = f_al[tid];
-      dd_add_dd(h1, l1, f_ah[tid + s], f_al[tid + s]);
-      f_ah[tid] = h1; f_al[tid] = l1;
-      double h2 = f_bh[tid], l2 = f_bl[tid];
-      dd_add_dd(h2, l2, f_bh[tid + s], f_bl[tid + s]);
-      f_bh[tid] = h2; f_bl[tid] = l2;
-      f_na[tid] += f_na[tid + s];
-      f_nb[tid] += f_nb[tid + s];
-      f_mm[tid] += f_mm[tid + s];
+  int t = lo;
+  for (; t + 4 <= hi; t += 4) {          // 4 partials in flight per thread
+    double2 A[4], B[4];
+    longlong2 NN[4];
+    unsigned long long M[4];
+#pragma unroll
+    for (int q = 0; q < 4; ++q) {
+      const TilePartial* p = part + t + q;
+      A[q] = __ldcg(reinterpret_cast<const double2*>(&p->a_hi));
+      B[q] = __ldcg(reinterpret_cast<const double2*>(&p->b_hi));
+      NN[q] = __ldcg(reinterpret_cast<const longlong2*>(&p->n_a));
+      M[q] = __ldcg(&p->mism);
     }
-    __syncthreads();
+#pragma unroll
+    for (int q = 0; q < 4; ++q) {
+      dd_add_dd(ah, al, A[q].x, A[q].y);
+      dd_add_dd(bh, bl, B[q].x, B[q].y);
+      na += NN[q].x;
+      nb += NN[q].y;
+      mm += M[q];
+    }
   }
+  for (; t < hi; ++t) {
+    const TilePartial* p = part + t;
+    const double2 A = __ldcg(reinterpret_cast<const double2*>(&p->a_hi));
+    const double2 B = __ldcg(reinterpret_cast<const double2*>(&p->b_hi));
+    const longlong2 NN = __ldcg(reinterpret_cast<const longlong2*>(&p->n_a));
+    dd_add_dd(ah, al, A.x, A.y);
+    dd_add_dd(bh, bl, B.x, B.y);
+    na += NN.x;
+    nb += NN.y;
+    mm += __ldcg(&p->mism);
+  }
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) {
+    dd_shfl_add(ah, al, o);
+    dd_shfl_add(bh, bl, o);
+    na += __shfl_xor_sync(0xffffffffu, na, o);
+    nb += __shfl_xor_sync(0xffffffffu, nb, o);
+    mm += __shfl_xor_sync(0xffffffffu, mm, o);
+  }
+  const int warp = tid >> 5, lane = tid & 31;
+  if (lane == 0) {
+    f_ah[warp] = ah; f_al[warp] = al; f_bh[warp] = bh; f_bl[warp] = bl;
+    f_na[warp] = na; f_nb[warp] = nb; f_mm[warp] = mm;
+  }
+  __syncthreads();
   if (tid == 0) {
+    double sah = 0, sal = 0, sbh = 0, sbl = 0;
+    long long sna = 0, snb = 0;
+    unsigned long long smm = 0;
+    for (int w = 0; w < (T + 31) / 32; ++w) {
+      dd_add_dd(sah, sal, f_ah[w], f_al[w]);
+      dd_add_dd(sbh, sbl, f_bh[w], f_bl[w]);
+      sna += f_na[w];
+      snb += f_nb[w];
+      smm += f_mm[w];
+    }
     if (region) {
       if (delta) {
-        dd_add_dd(sc->sp_hi, sc->sp_lo, f_ah[0], f_al[0]);
-        dd_add_dd(sc->sp_hi, sc->sp_lo, -f_bh[0], -f_bl[0]);
-        dd_add_dd(sc->sn_hi, sc->sn_lo, f_bh[0], f_bl[0]);
-        dd_add_dd(sc->sn_hi, sc->sn_lo, -f_ah[0], -f_al[0]);
-        sc->n_pos += f_na[0] - f_nb[0];
+        dd_add_dd(sc->sp_hi, sc->sp_lo, sah, sal);
+        dd_add_dd(sc->sp_hi, sc->sp_lo, -sbh, -sbl);
+        dd_add_dd(sc->sn_hi, sc->sn_lo, sbh, sbl);
+        dd_add_dd(sc->sn_hi, sc->sn_lo, -sah, -sal);
+        sc->n_pos += sna - snb;
       } else {
-        sc->sp_hi = f_ah[0]; sc->sp_lo = f_al[0];
-        sc->sn_hi = f_bh[0]; sc->sn_lo = f_bl[0];
-        sc->n_pos = f_na[0];
+        sc->sp_hi = sah; sc->sp_lo = sal;
+        sc->sn_hi = sbh; sc->sn_lo = sbl;
+        sc->n_pos = sna;
       }
       region_coeffs(sc);
     }
     if (ckpt) {                                    // engine.py:228-236
       sc->n_ckpt += 1;
-      if (sc->n_ckpt >= 2) sc->equal_run = (f_mm[0] == 0) ? sc->equal_run + 1 : 0;
+      if (sc->n_ckpt >= 2) sc->equal_run = (smm == 0) ? sc->equal_run + 1 : 0;
       const long long cw = sc->conv_window;
       if (cw == 1 || (sc->n_ckpt >= cw && sc->equal_run >= cw - 1)) {
         sc->stop = 1;
@@ -780,8 +823,6 @@ __device__ void finalize_cta(const TilePartial* part, int n, Scalars* sc, bool d
         sc->converged_iter = iter;
       }
     }
-    sc->ticket = 0u;
-    __threadfence();
   }
 }
 
@@ -874,14 +915,13 @@ __device__ __forceinline__ void partition_block(const FastParams& P, const float
 // Interior units = (word-row, segment of seg_chunks chunks); border units =
 // single chunks.  Each unit's deltas form one partial; partials are laid
 // out [interior units][border units] (fixed geometry => deterministic).
-// The interior launch runs last and its last CTA reduces all partials.
+// A separate 1-CTA finalize kernel then reduces all partials.
 template <int R, bool PART, bool CKPT, bool MASKONLY, bool INT>
 __global__ void __launch_bounds__(kThreads, 4) k_partition(FastParams P) {
   constexpr int NPAT = 1 << (2 * R + 1);
   constexpr int NT = kColsPerThread + 2 * R;
   __shared__ __align__(16) float s_lt_raw[1024];
   __shared__ float s_ls[NPAT];
-  __shared__ unsigned int s_ticket;
   float* const s_lt = aligned_lut(s_lt_raw);
   Scalars* sc = P.scal;
   if (!MASKONLY && *(volatile const int*)&sc->stop) return;
@@ -1000,19 +1040,6 @@ __global__ void __launch_bounds__(kThreads, 4) k_partition(FastParams P) {
       t.mism = mism;
       P.part[INT ? unit : P.n_int_part + unit] = t;
     }
-  }
-  if (MASKONLY || !INT) return;
-  // last CTA to finish reduces every unit partial (threadFenceReduction idiom)
-  __syncthreads();
-  if (threadIdx.x == 0) {
-    __threadfence();
-    s_ticket = atomicAdd(&sc->ticket, 1u);
-  }
-  __syncthreads();
-  if (s_ticket == gridDim.x - 1) {
-    __threadfence();
-    finalize_cta(P.part, P.n_int_part + border_count(P.rp, P.g.HR, P.nchunk), sc,
-                 /*delta=*/true, PART, CKPT, P.iter);
   }
 }
 

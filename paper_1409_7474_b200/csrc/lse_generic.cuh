@@ -289,10 +289,17 @@ __global__ void __launch_bounds__(kThreads) k_partition_abs(const double* __rest
   }
 }
 
-__global__ void __launch_bounds__(kThreads) k_finalize(const TilePartial* part, int n, Scalars* sc,
+__global__ void __launch_bounds__(1024) k_finalize(const TilePartial* part, int n, Scalars* sc,
                                                        int delta, int region, int ckpt,
                                                        long long iter) {
   finalize_cta(part, n, sc, delta != 0, region != 0, ckpt != 0, iter);
+}
+
+// per-iteration finalize of the fast path (DELTA partials); no-op once stopped
+__global__ void __launch_bounds__(1024) k_finalize_run(const TilePartial* part, int n, Scalars* sc,
+                                                       int region, int ckpt, long long iter) {
+  if (*(volatile const int*)&sc->stop) return;
+  finalize_cta(part, n, sc, true, region != 0, ckpt != 0, iter);
 }
 
 // image statistics: min, max, max|.| (order-preserving integer atomics)
