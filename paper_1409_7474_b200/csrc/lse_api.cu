@@ -163,7 +163,7 @@ struct lse_run {
   int grid_update = 0, grid_part = 0;
   int skip_uniform = 1;
   int nchunk = 1, nchunk_u = 1, nseg = 1, seg_chunks = 1;
-  UnitRect ru{0, 0, 0, 0}, rp{0, 0, 0, 0};   // interior unit rectangles
+  Geo gu{}, gu_all{}, gp{};   // work geometry: update, update with no interior, partition
   long long ni_upd = 0, nb_upd[2] = {0, 0}, ni_part = 0, nb_part = 0;
   unsigned long long* d_work = nullptr;
   unsigned long long work_next = 0;   // host mirror of the monotonic work counter
@@ -192,8 +192,8 @@ FastParams fast_params(lse_run* r) {
   P.nseg = r->nseg;
   P.seg_chunks = r->seg_chunks;
   P.work = r->d_work;
-  P.ru = r->ru;
-  P.rp = r->rp;
+  P.gu = r->gu;
+  P.gp = r->gp;
   P.n_int_part = (int)r->ni_part;
   return P;
 }
@@ -280,7 +280,7 @@ int launch_update(lse_run* r, FastParams P) {
   if (nb > 0) {
     const int g = fast_grid(nb);
     P.work_base = take_work(r, nb, g);
-    if (SRC == SRC_SCALED) P.ru = UnitRect{0, 0, 0, 0};
+    if (SRC == SRC_SCALED) P.gu = r->gu_all;
     k_update<R, MODEL, SRC, false><<<g, kThreads, 0, r->st>>>(P);
     CKL();
   }
@@ -371,8 +371,18 @@ int launch_fast(lse_run* r, long long it, bool ckpt) {
 
 // wait for the device, fold profiling events, detect convergence
 int collect(lse_run* r) {
+  unsigned long long work = 0;
   CK(cudaMemcpyAsync(r->h_scal, r->d_scal, sizeof(Scalars), cudaMemcpyDeviceToHost, r->st));
+  CK(cudaMemcpyAsync(&work, r->d_work, sizeof(work), cudaMemcpyDeviceToHost, r->st));
   CK(cudaStreamSynchronize(r->st));
+  // every dynamically scheduled launch must have made exactly its reserved
+  // number of grabs (units + one failing grab per warp) unless it was stopped
+  if (!r->h_scal->stop && work != r->work_next) {
+    char msg[128];
+    std::snprintf(msg, sizeof(msg), "work-counter mismatch: device %llu, expected %llu", work,
+                  r->work_next);
+    return fail(LSE_ERR_CUDA, msg);
+  }
   if (r->prof) {
     for (auto& e : r->evrec) {
       float ms = 0.f;
@@ -719,32 +729,23 @@ int lse_run_create(lse_run** out, const lse_params* p, long long height, long lo
   r->nchunk = (r->W + kChunk - 1) / kChunk;
   r->nchunk_u = (r->W + kUpdChunk - 1) / kUpdChunk;
   {
-    const int R = r->R, H = r->H, W = r->W, HR = r->g.HR, nc = r->nchunk;
-    auto fdiv = [](long long a, long long b) { return a >= 0 ? a / b : -((-a + b - 1) / b); };
-    auto mk = [&](long long rh, long long ch, int ncols) {
-      UnitRect u{1, (int)std::min<long long>(HR, rh + 1), 1, (int)std::min<long long>(ncols, ch + 1)};
-      if (u.r_hi <= u.r_lo || u.c_hi <= u.c_lo || R > 31) u = UnitRect{0, 0, 0, 0};
-      return u;
-    };
-    // update: rows y0-1-R .. y0+32+R and columns x-(R+1) .. x+8+R inside
-    const int ncu = r->nchunk_u;
-    r->ru = mk(fdiv(H - 33 - R, 32), fdiv(W - kUpdChunk - 1 - R, kUpdChunk), ncu);
-    // partition: rows y0-R .. y0+31+R and columns x-R .. x+7+R inside
-    r->rp = mk(fdiv(H - 32 - R, 32), fdiv(W - 256 - R, 256), nc);
-    const long long cu = (long long)(r->ru.r_hi - r->ru.r_lo) * (r->ru.c_hi - r->ru.c_lo);
-    r->ni_upd = cu;
-    r->nb_upd[0] = (long long)HR * ncu - cu;
-    r->nb_upd[1] = (long long)HR * ncu;
+    const int R = r->R, H = r->H, W = r->W;
+    r->gu = make_geo(H, W, R, 1 + R, 1 + R, R + 1);   // update reaches R+1 rows/columns
+    r->gp = make_geo(H, W, R, R, R, R);               // partition reaches R
+    r->gu_all = geo_all_border(r->gu, H);
+    r->ni_upd = (long long)(r->gu.r_hi - r->gu.r_lo) * r->gu.nci + (r->gu.nB1 + 31) / 32;
+    r->nb_upd[0] = r->gu.nA + (r->gu.nB2 + 31) / 32;
+    r->nb_upd[1] = r->gu_all.nA;
     // partition segments: >= ~8 interior units per resident warp, <= 16 chunks
     // (fixed by the image geometry only)
     const long long warps = (long long)num_sms() * 16;
-    const long long wi = r->rp.c_hi - r->rp.c_lo, hi_rows = r->rp.r_hi - r->rp.r_lo;
+    const long long wi = r->gp.nci, hi_rows = r->gp.r_hi - r->gp.r_lo;
     long long sc = wi > 0 ? (hi_rows * wi) / (8 * warps) : 1;
     sc = std::max<long long>(1, std::min<long long>(16, sc));
     r->seg_chunks = (int)sc;
     r->nseg = wi > 0 ? (int)((wi + sc - 1) / sc) : 0;
-    r->ni_part = hi_rows * r->nseg;
-    r->nb_part = (long long)HR * nc - hi_rows * wi;
+    r->ni_part = hi_rows * r->nseg + (r->gp.nB1 + 31) / 32;
+    r->nb_part = r->gp.nA + (r->gp.nB2 + 31) / 32;
   }
   const long long nparts = std::max<long long>(r->g.ntiles, r->ni_part + r->nb_part);
   auto cleanup = [&](int rc) {

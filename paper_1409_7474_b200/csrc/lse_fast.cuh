@@ -22,6 +22,7 @@
 // reference's fp64 decision.
 #pragma once
 #include "lse_device.cuh"
+#include "lse_geometry.cuh"
 
 namespace lse {
 
@@ -36,13 +37,6 @@ struct ExactCtx {
   double scale;           // +-scale state (SRC_SCALED)
   Scalars* scal;
   int model;
-};
-
-// Interior rectangle of work units: word-rows [r_lo, r_hi) x chunks [c_lo, c_hi)
-// whose whole stencil footprint lies inside the image.  Units outside it
-// ("border units") run the zero-padding / one-sided-gradient variant.
-struct UnitRect {
-  int r_lo, r_hi, c_lo, c_hi;
 };
 
 struct FastParams {
@@ -66,7 +60,7 @@ struct FastParams {
   int nchunk_u;              // update chunks (kUpdChunk columns) per word-row
   int nseg;                  // partition segments per interior word-row
   int seg_chunks;            // chunks per partition segment (partial granularity)
-  UnitRect ru, rp;           // interior rectangles (word-rows x chunks): update / partition
+  Geo gu, gp;                // work geometry: update / partition
   int n_int_part;            // interior partition units (their partials come first)
   unsigned long long* work;  // dynamic work counter (monotonic across launches)
   unsigned long long work_base;  // value of *work when this launch started
@@ -569,43 +563,13 @@ __device__ __forceinline__ void load_luts(const FastParams& P, float* s_lt, floa
   }
 }
 
-// Unit <-> (word-row, chunk) maps.  Interior units tile the rectangle I;
-// border units enumerate its complement (top rows, left/right chunks of the
-// middle rows, bottom rows) in a fixed order.
-__device__ __forceinline__ int rect_count(const UnitRect& I) {
-  return (I.r_hi - I.r_lo) * (I.c_hi - I.c_lo);
-}
-__device__ __forceinline__ void interior_unit(int q, const UnitRect& I, int& r, int& ch) {
-  const int w = I.c_hi - I.c_lo;
-  r = I.r_lo + q / w;
-  ch = I.c_lo + q % w;
-}
-__device__ __forceinline__ int border_count(const UnitRect& I, int HR, int nchunk) {
-  return HR * nchunk - rect_count(I);
-}
-__device__ __forceinline__ void border_unit(int q, const UnitRect& I, int nchunk, int& r, int& ch) {
-  const int top = I.r_lo * nchunk;
-  if (q < top) { r = q / nchunk; ch = q % nchunk; return; }
-  q -= top;
-  const int left = I.c_lo, per = I.c_lo + (nchunk - I.c_hi);
-  const int mid = (I.r_hi - I.r_lo) * per;
-  if (q < mid) {
-    r = I.r_lo + q / per;
-    const int k = q % per;
-    ch = k < left ? k : I.c_hi + (k - left);
-    return;
-  }
-  q -= mid;
-  r = I.r_hi + q / nchunk;
-  ch = q % nchunk;
-}
-
 __device__ __forceinline__ int grab_unit(const FastParams& P, int lane) {
   // dynamic unit scheduling: grabs are counted from this launch's base, so the
   // counter never needs a reset (each warp makes exactly one failing grab)
   unsigned long long g = 0;
   if (lane == 0) g = atomicAdd(P.work, 1ull) - P.work_base;
-  return (int)__shfl_sync(0xffffffffu, (long long)g, 0);
+  g = (unsigned long long)__shfl_sync(0xffffffffu, (long long)g, 0);
+  return g > 0x7fffffffull ? 0x7fffffff : (int)g;     // out of window: treated as "no work" 
 }
 
 // INT = true : interior units (exact-rounded LUT, central differences, and
@@ -615,7 +579,7 @@ __device__ __forceinline__ int grab_unit(const FastParams& P, int lane) {
 // chunk is copied without reading the data plane).
 // INT = false: border units (zero padding, one-sided gradients).
 template <int R, int MODEL, int SRC, bool INT>
-__global__ void __launch_bounds__(kThreads, INT ? 5 : 3) k_update(FastParams P) {
+__global__ void __launch_bounds__(kThreads, INT ? 4 : 3) k_update(FastParams P) {
   constexpr int CPL = kUpdCols;
   constexpr int NPAT = 1 << (2 * R + 1);
   constexpr int NT = CPL + 2 * (R + 1);
@@ -631,29 +595,41 @@ __global__ void __launch_bounds__(kThreads, INT ? 5 : 3) k_update(FastParams P) 
   load_luts<R>(P, s_lt, s_ls);
   __syncthreads();
   const int lane = threadIdx.x & 31;
-  const int nunits = INT ? rect_count(P.ru) : border_count(P.ru, P.g.HR, P.nchunk_u);
+  const int nunits = INT ? interior_units(P.gu) : border_units(P.gu);
   for (;;) {
     const int unit = grab_unit(P, lane);
     if (unit >= nunits) break;
-    int r, ch;
-    if (INT) interior_unit(unit, P.ru, r, ch);
-    else border_unit(unit, P.ru, P.nchunk_u, r, ch);
-    const int x0 = ch * kUpdChunk + CPL * lane;
+    int r = 0, x0 = 0;
+    bool act = true;
+    if (INT) {
+      const int nch = chunk_units(P.gu);
+      if (unit < nch) {
+        r = P.gu.r_lo + unit / P.gu.nci;
+        x0 = P.gu.xoff + (unit % P.gu.nci) * kUpdChunk + CPL * lane;
+      } else {
+        act = b1_lane(P.gu, unit - nch, lane, r, x0);
+      }
+    } else if (!border_lane(P.gu, unit, lane, P.g.W, r, x0)) {
+      continue;
+    }
     uint32_t prev[NT], cur[NT];
     if (INT) {
-      const uint32_t* wp = P.bits_in + (size_t)(r - 1) * P.g.pitch_w + (x0 - (R + 1));
       uint32_t a = ~0u, o = 0u;
+      if (act) {
+        const uint32_t* wp = P.bits_in + (size_t)(r - 1) * P.g.pitch_w + (x0 - (R + 1));
 #pragma unroll
-      for (int j = 0; j < NT; ++j) {
-        prev[j] = __ldg(wp + j);
-        cur[j] = __ldg(wp + P.g.pitch_w + j);
-        if (P.skip_uniform) {
-          const uint32_t nx = __ldg(wp + 2 * (size_t)P.g.pitch_w + j);
-          a &= prev[j] & cur[j] & nx;
-          o |= prev[j] | cur[j] | nx;
+        for (int j = 0; j < NT; ++j) {
+          prev[j] = __ldg(wp + j);
+          cur[j] = __ldg(wp + P.g.pitch_w + j);
+          if (P.skip_uniform) {
+            const uint32_t nx = __ldg(wp + 2 * (size_t)P.g.pitch_w + j);
+            a &= prev[j] & cur[j] & nx;
+            o |= prev[j] | cur[j] | nx;
+          }
         }
       }
-      if (P.skip_uniform && __all_sync(0xffffffffu, a == ~0u || o == 0u)) {
+      if (P.skip_uniform && __all_sync(0xffffffffu, !act || a == ~0u || o == 0u)) {
+        if (!act) continue;
         uint32_t* dst = P.bits_out + (size_t)r * P.g.pitch_w + x0;
 #pragma unroll
         for (int q = 0; q < CPL / 4; ++q)
@@ -662,7 +638,6 @@ __global__ void __launch_bounds__(kThreads, INT ? 5 : 3) k_update(FastParams P) 
         continue;
       }
     } else {
-      if (x0 >= P.g.W) continue;
 #pragma unroll
       for (int j = 0; j < NT; ++j) {
         const int xc = x0 - (R + 1) + j;
@@ -670,6 +645,7 @@ __global__ void __launch_bounds__(kThreads, INT ? 5 : 3) k_update(FastParams P) 
         cur[j] = word_at<false>(P, r, xc);
       }
     }
+    if (INT && !act) continue;
     if (INT && SRC == SRC_SMOOTH)
       update_block_int<R, MODEL, CPL>(P, (uint32_t)__cvta_generic_to_shared(s_lt),
                                       s_ring + (threadIdx.x >> 5) * kRing * 32 * CPL, r, x0, A, B,
@@ -930,48 +906,60 @@ __global__ void __launch_bounds__(kThreads, 4) k_partition(FastParams P) {
   __syncthreads();
   const int lane = threadIdx.x & 31;
   const int nseg = P.nseg;
-  const int nunits = INT ? (P.rp.r_hi - P.rp.r_lo) * nseg
-                         : border_count(P.rp, P.g.HR, P.nchunk);
+  const int nunits = INT ? (P.gp.r_hi - P.gp.r_lo) * nseg + (P.gp.nB1 + 31) / 32
+                         : border_units(P.gp);
   for (;;) {
     const int unit = grab_unit(P, lane);
     if (unit >= nunits) break;
-    int r, ch0, ch1;
+    int r = 0, c0 = 0, c1 = 1, xb = 0;
+    bool active = true, chunked = false;
     if (INT) {
-      r = P.rp.r_lo + unit / nseg;
-      ch0 = P.rp.c_lo + (unit % nseg) * P.seg_chunks;
-      ch1 = min(ch0 + P.seg_chunks, P.rp.c_hi);
+      const int nsu = (P.gp.r_hi - P.gp.r_lo) * nseg;
+      if (unit < nsu) {
+        chunked = true;
+        r = P.gp.r_lo + unit / nseg;
+        c0 = (unit % nseg) * P.seg_chunks;
+        c1 = min(c0 + P.seg_chunks, P.gp.nci);
+        xb = P.gp.xoff + kColsPerThread * lane;
+      } else {
+        active = b1_lane(P.gp, unit - nsu, lane, r, xb);
+      }
     } else {
-      border_unit(unit, P.rp, P.nchunk, r, ch0);
-      ch1 = ch0 + 1;
+      active = border_lane(P.gp, unit, lane, P.g.W, r, xb);
     }
     const int y0 = r * 32;
     double a_in = 0.0, a_out = 0.0;
     long long n_in = 0, n_out = 0;
     unsigned long long mism = 0;
-    for (int ch = ch0; ch < ch1; ++ch) {
-      const int x0 = ch * kChunk + kColsPerThread * lane;
+    for (int ch = c0; ch < c1; ++ch) {
+      const int x0 = chunked ? xb + ch * kChunk : xb;
       uint32_t pw[8], mw[8], prev[NT], cur[NT];
       if (INT) {
         uint32_t a = ~0u, o = 0u;
+        if (active) {
 #pragma unroll
-        for (int j = 0; j < NT; ++j) {
-          const int xc = x0 - R + j;
-          prev[j] = word_at<true>(P, r - 1, xc);
-          cur[j] = word_at<true>(P, r, xc);
-          if (P.skip_uniform) {
-            const uint32_t nx = word_at<true>(P, r + 1, xc);
-            a &= prev[j] & cur[j] & nx;
-            o |= prev[j] | cur[j] | nx;
+          for (int j = 0; j < NT; ++j) {
+            const int xc = x0 - R + j;
+            prev[j] = word_at<true>(P, r - 1, xc);
+            cur[j] = word_at<true>(P, r, xc);
+            if (P.skip_uniform) {
+              const uint32_t nx = word_at<true>(P, r + 1, xc);
+              a &= prev[j] & cur[j] & nx;
+              o |= prev[j] | cur[j] | nx;
+            }
           }
         }
-        if (P.skip_uniform && __all_sync(0xffffffffu, a == ~0u || o == 0u)) {
+        if (P.skip_uniform && __all_sync(0xffffffffu, !active || a == ~0u || o == 0u)) {
+          if (!active) continue;
 #pragma unroll
           for (int c = 0; c < 8; ++c) pw[c] = mw[c] = cur[R + c];   // sign(phi) = b
+        } else if (!active) {
+          continue;
         } else {
           partition_block<R, true>(P, s_lt, s_ls, (uint32_t)__cvta_generic_to_shared(s_lt), r, x0, eps_phi, prev, cur, pw, mw);
         }
       } else {
-        if (x0 >= P.g.W) continue;
+        if (!active) continue;
 #pragma unroll
         for (int j = 0; j < NT; ++j) {
           const int xc = x0 - R + j;
@@ -1038,7 +1026,7 @@ __global__ void __launch_bounds__(kThreads, 4) k_partition(FastParams P) {
       t.n_a = n_in;
       t.n_b = n_out;
       t.mism = mism;
-      P.part[INT ? unit : P.n_int_part + unit] = t;
+      P.part[INT ? unit : P.n_int_part + unit] = t;   // [interior units][border units]
     }
   }
 }

@@ -1,0 +1,105 @@
+// lse_geometry.cuh -- work decomposition of the fused kernels (host + device).
+//
+// Kept free of CUDA-only constructs so the host driver and a plain C++ unit
+// test (tests/test_geometry.py) share the exact code the kernels run.
+#pragma once
+#ifdef __CUDACC__
+#define LSE_HD __host__ __device__ __forceinline__
+#else
+#define LSE_HD inline
+#endif
+
+namespace lse {
+
+// Work geometry of one kernel family (update or partition).
+//  interior work: (1) chunks -- word-rows [r_lo, r_hi) x c in [0, nci), chunk c
+//  = columns [xoff + 256c, xoff + 256c + 256), one warp each; (2) "B1" lane
+//  groups -- the 8-column groups of the right strip [x1, W) of interior rows
+//  whose stencil still lies inside the image, packed 32 per warp (each lane
+//  its own row); every lane of (1)/(2) runs the interior code.
+//  border work: (A) word-rows outside [r_lo, r_hi), whole width, 256-column
+//  warp units; (B2) per interior row the left strip [0, xoff) and the right
+//  tail beyond the B1 groups, 8-column lane groups packed 32 per warp.
+struct Geo {
+  int r_lo, r_hi, nci, xoff, x1;
+  int nchunk_full;   // ceil(W / 256): chunks of a part-A row
+  int nb1_row;       // B1 lane groups per interior row
+  int nb2_left;      // B2 left-strip groups per interior row (xoff / 8)
+  int nb2_row;       // B2 lane groups per interior row (left + right tail)
+  int nA;            // part-A warp units
+  int nB1, nB2;      // lane groups
+};
+
+// Build the geometry of a kernel whose stencil reaches `top` rows up, `bot`
+// rows down and `right` columns right (the left reach must be <= xoff = 8).
+LSE_HD long long geo_fdiv(long long a, long long b) { return a >= 0 ? a / b : -((-a + b - 1) / b); }
+LSE_HD Geo make_geo(int H, int W, int R, int top, int bot, int right) {
+  const int HR = (H + 31) / 32;
+  Geo g{};
+  g.xoff = 8;
+  g.nchunk_full = (W + 255) / 256;
+  long long rlo = (top + 31) / 32;
+  long long rhi = geo_fdiv(H - 32 - bot, 32) + 1;
+  if (rhi > HR) rhi = HR;
+  long long nci = geo_fdiv(W - 1 - right - 255 - g.xoff, 256) + 1;
+  if (R > 7 || rlo >= rhi || nci <= 0) { rlo = rhi = 0; nci = 0; }
+  g.r_lo = (int)rlo;
+  g.r_hi = (int)rhi;
+  g.nci = (int)nci;
+  g.x1 = g.xoff + 256 * g.nci;
+  const int ngr = g.nci > 0 ? (W - g.x1 + 7) / 8 : 0;           // right-strip groups
+  long long nb1 = g.nci > 0 ? geo_fdiv(W - 8 - right - g.x1, 8) + 1 : 0;
+  if (nb1 < 0) nb1 = 0;
+  if (nb1 > ngr) nb1 = ngr;
+  g.nb1_row = (int)nb1;
+  g.nb2_left = g.nci > 0 ? g.xoff / 8 : 0;
+  g.nb2_row = g.nb2_left + (ngr - g.nb1_row);
+  g.nA = (g.r_lo + HR - g.r_hi) * g.nchunk_full;
+  g.nB1 = (g.r_hi - g.r_lo) * g.nb1_row;
+  g.nB2 = (g.r_hi - g.r_lo) * g.nb2_row;
+  return g;
+}
+
+// the same geometry with no interior (every unit runs the border code)
+LSE_HD Geo geo_all_border(const Geo& in, int H) {
+  Geo g = in;
+  g.r_lo = g.r_hi = 0;
+  g.nci = 0;
+  g.nb1_row = g.nb2_row = g.nb2_left = 0;
+  g.nA = ((H + 31) / 32) * g.nchunk_full;
+  g.nB1 = g.nB2 = 0;
+  return g;
+}
+
+// Unit -> lane coordinates.
+LSE_HD int chunk_units(const Geo& G) { return (G.r_hi - G.r_lo) * G.nci; }
+LSE_HD int interior_units(const Geo& G) {
+  return chunk_units(G) + (G.nB1 + 31) / 32;
+}
+LSE_HD int border_units(const Geo& G) { return G.nA + (G.nB2 + 31) / 32; }
+// B1 pack: lane -> (row, x0); false for the unused lanes of the last pack
+LSE_HD bool b1_lane(const Geo& G, int pack, int lane, int& r, int& x0) {
+  const int g = pack * 32 + lane;
+  if (g >= G.nB1) return false;
+  r = G.r_lo + g / G.nb1_row;
+  x0 = G.x1 + 8 * (g - (r - G.r_lo) * G.nb1_row);
+  return true;
+}
+LSE_HD bool border_lane(const Geo& G, int unit, int lane, int W, int& r,
+                                            int& x0) {
+  if (unit < G.nA) {
+    const int rowidx = unit / G.nchunk_full;
+    const int c = unit - rowidx * G.nchunk_full;
+    r = rowidx < G.r_lo ? rowidx : G.r_hi + (rowidx - G.r_lo);
+    x0 = c * 256 + 8 * lane;
+    return x0 < W;
+  }
+  const int g = (unit - G.nA) * 32 + lane;
+  if (g >= G.nB2) return false;
+  r = G.r_lo + g / G.nb2_row;
+  const int j = g - (r - G.r_lo) * G.nb2_row;
+  x0 = j < G.nb2_left ? 8 * j : G.x1 + 8 * (G.nb1_row + j - G.nb2_left);
+  return true;
+}
+
+}  // namespace lse
