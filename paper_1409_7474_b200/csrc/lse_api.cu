@@ -194,7 +194,6 @@ FastParams fast_params(lse_run* r) {
   P.work = r->d_work;
   P.gu = r->gu;
   P.gp = r->gp;
-  P.n_int_part = (int)r->ni_part;
   return P;
 }
 
@@ -275,42 +274,26 @@ unsigned long long take_work(lse_run* r, long long units, int grid) {
 
 template <int R, int MODEL, int SRC>
 int launch_update(lse_run* r, FastParams P) {
-  const long long nb = r->nb_upd[SRC == SRC_SCALED];
-  const long long ni = SRC == SRC_SCALED ? 0 : r->ni_upd;
-  if (nb > 0) {
-    const int g = fast_grid(nb);
-    P.work_base = take_work(r, nb, g);
-    if (SRC == SRC_SCALED) P.gu = r->gu_all;
-    k_update<R, MODEL, SRC, false><<<g, kThreads, 0, r->st>>>(P);
-    CKL();
-  }
-  if (ni > 0) {
-    const int g = fast_grid(ni);
-    P.work_base = take_work(r, ni, g);
-    k_update<R, MODEL, SRC, true><<<g, kThreads, 0, r->st>>>(P);
-    CKL();
-  }
+  if (SRC == SRC_SCALED) P.gu = r->gu_all;
+  const long long n = SRC == SRC_SCALED ? r->nb_upd[1] : r->nb_upd[0] + r->ni_upd;
+  const int g = fast_grid(n);
+  P.work_base = take_work(r, n, g);
+  k_update<R, MODEL, SRC><<<g, kThreads, 0, r->st>>>(P);
+  CKL();
   return LSE_OK;
 }
 
 template <int R, bool PART, bool CKPT, bool MASKONLY>
 int launch_partition(lse_run* r, FastParams P) {
-  if (r->nb_part > 0) {
-    const int g = fast_grid(r->nb_part);
-    P.work_base = take_work(r, r->nb_part, g);
-    k_partition<R, PART, CKPT, MASKONLY, false><<<g, kThreads, 0, r->st>>>(P);
-    CKL();
-  }
-  if (r->ni_part > 0) {
-    const int g = fast_grid(r->ni_part);
-    P.work_base = take_work(r, r->ni_part, g);
-    k_partition<R, PART, CKPT, MASKONLY, true><<<g, kThreads, 0, r->st>>>(P);
-    CKL();
-  }
+  const long long n = r->nb_part + r->ni_part;
+  const int g = fast_grid(n);
+  P.work_base = take_work(r, n, g);
+  k_partition<R, PART, CKPT, MASKONLY><<<g, kThreads, 0, r->st>>>(P);
+  CKL();
   if (!MASKONLY) {
     // fixed-order reduction of all unit partials -> next update's coefficients
-    k_finalize_run<<<1, 1024, 0, r->st>>>(r->d_part, (int)(r->ni_part + r->nb_part), r->d_scal,
-                                          PART ? 1 : 0, CKPT ? 1 : 0, P.iter);
+    k_finalize_run<<<1, 1024, 0, r->st>>>(r->d_part, (int)n, r->d_scal, PART ? 1 : 0,
+                                          CKPT ? 1 : 0, P.iter);
     CKL();
   }
   return LSE_OK;

@@ -61,7 +61,6 @@ struct FastParams {
   int nseg;                  // partition segments per interior word-row
   int seg_chunks;            // chunks per partition segment (partial granularity)
   Geo gu, gp;                // work geometry: update / partition
-  int n_int_part;            // interior partition units (their partials come first)
   unsigned long long* work;  // dynamic work counter (monotonic across launches)
   unsigned long long work_base;  // value of *work when this launch started
 };
@@ -578,14 +577,34 @@ __device__ __forceinline__ int grab_unit(const FastParams& P, int lane) {
 // |grad phi| == 0, v == 0 and u == phi exactly, so b^{n+1} == b^n and the
 // chunk is copied without reading the data plane).
 // INT = false: border units (zero padding, one-sided gradients).
-template <int R, int MODEL, int SRC, bool INT>
-__global__ void __launch_bounds__(kThreads, INT ? 4 : 3) k_update(FastParams P) {
+// Border lane block: zero padding / one-sided gradients.  Not inlined, so its
+// register needs do not constrain the interior loop (it runs on ~1% of units).
+template <int R, int MODEL, int SRC>
+__device__ __noinline__ void border_update_lane(const FastParams& P, const float* s_lt,
+                                                const float* s_ls, int r, int x0, float A,
+                                                float B, float eps_u) {
+  constexpr int CPL = kUpdCols;
+  constexpr int NT = CPL + 2 * (R + 1);
+  uint32_t prev[NT], cur[NT];
+#pragma unroll
+  for (int j = 0; j < NT; ++j) {
+    const int xc = x0 - (R + 1) + j;
+    prev[j] = word_at<false>(P, r - 1, xc);
+    cur[j] = word_at<false>(P, r, xc);
+  }
+  update_block<R, MODEL, SRC, false, CPL>(P, s_lt, s_ls, r, x0, A, B, eps_u, prev, cur);
+}
+
+// One launch covers every unit: [border units][interior units] (border first,
+// so their longer latency overlaps the interior work of the other warps).
+template <int R, int MODEL, int SRC>
+__global__ void __launch_bounds__(kThreads, 4) k_update(FastParams P) {
   constexpr int CPL = kUpdCols;
   constexpr int NPAT = 1 << (2 * R + 1);
   constexpr int NT = CPL + 2 * (R + 1);
   __shared__ __align__(16) float s_lt_raw[1024];
   __shared__ float s_ls[NPAT];
-  __shared__ __align__(16) float s_ring[INT ? (kThreads / 32) * kRing * 32 * CPL : 1];
+  __shared__ __align__(16) float s_ring[(kThreads / 32) * kRing * 32 * CPL];
   float* const s_lt = aligned_lut(s_lt_raw);
   const Scalars* sc = P.scal;
   if (*(volatile const int*)&sc->stop) return;
@@ -595,63 +614,56 @@ __global__ void __launch_bounds__(kThreads, INT ? 4 : 3) k_update(FastParams P) 
   load_luts<R>(P, s_lt, s_ls);
   __syncthreads();
   const int lane = threadIdx.x & 31;
-  const int nunits = INT ? interior_units(P.gu) : border_units(P.gu);
+  const int nb = border_units(P.gu);
+  const int nunits = nb + (SRC == SRC_SMOOTH ? interior_units(P.gu) : 0);
   for (;;) {
     const int unit = grab_unit(P, lane);
     if (unit >= nunits) break;
     int r = 0, x0 = 0;
-    bool act = true;
-    if (INT) {
-      const int nch = chunk_units(P.gu);
-      if (unit < nch) {
-        r = P.gu.r_lo + unit / P.gu.nci;
-        x0 = P.gu.xoff + (unit % P.gu.nci) * kUpdChunk + CPL * lane;
-      } else {
-        act = b1_lane(P.gu, unit - nch, lane, r, x0);
-      }
-    } else if (!border_lane(P.gu, unit, lane, P.g.W, r, x0)) {
+    if (unit < nb) {
+      if (border_lane(P.gu, unit, lane, P.g.W, r, x0))
+        border_update_lane<R, MODEL, SRC>(P, s_lt, s_ls, r, x0, A, B, eps_u);
       continue;
     }
-    uint32_t prev[NT], cur[NT];
-    if (INT) {
-      uint32_t a = ~0u, o = 0u;
-      if (act) {
-        const uint32_t* wp = P.bits_in + (size_t)(r - 1) * P.g.pitch_w + (x0 - (R + 1));
-#pragma unroll
-        for (int j = 0; j < NT; ++j) {
-          prev[j] = __ldg(wp + j);
-          cur[j] = __ldg(wp + P.g.pitch_w + j);
-          if (P.skip_uniform) {
-            const uint32_t nx = __ldg(wp + 2 * (size_t)P.g.pitch_w + j);
-            a &= prev[j] & cur[j] & nx;
-            o |= prev[j] | cur[j] | nx;
-          }
-        }
-      }
-      if (P.skip_uniform && __all_sync(0xffffffffu, !act || a == ~0u || o == 0u)) {
-        if (!act) continue;
-        uint32_t* dst = P.bits_out + (size_t)r * P.g.pitch_w + x0;
-#pragma unroll
-        for (int q = 0; q < CPL / 4; ++q)
-          reinterpret_cast<uint4*>(dst)[q] = make_uint4(cur[R + 1 + 4 * q], cur[R + 2 + 4 * q],
-                                                        cur[R + 3 + 4 * q], cur[R + 4 + 4 * q]);
-        continue;
-      }
+    if (SRC != SRC_SMOOTH) continue;
+    const int iu = unit - nb;
+    bool act = true;
+    const int nch = chunk_units(P.gu);
+    if (iu < nch) {
+      r = P.gu.r_lo + iu / P.gu.nci;
+      x0 = P.gu.xoff + (iu % P.gu.nci) * kUpdChunk + CPL * lane;
     } else {
+      act = b1_lane(P.gu, iu - nch, lane, r, x0);
+    }
+    uint32_t prev[NT], cur[NT];
+    uint32_t a = ~0u, o = 0u;
+    if (act) {
+      const uint32_t* wp = P.bits_in + (size_t)(r - 1) * P.g.pitch_w + (x0 - (R + 1));
 #pragma unroll
       for (int j = 0; j < NT; ++j) {
-        const int xc = x0 - (R + 1) + j;
-        prev[j] = word_at<false>(P, r - 1, xc);
-        cur[j] = word_at<false>(P, r, xc);
+        prev[j] = __ldg(wp + j);
+        cur[j] = __ldg(wp + P.g.pitch_w + j);
+        if (P.skip_uniform) {
+          const uint32_t nx = __ldg(wp + 2 * (size_t)P.g.pitch_w + j);
+          a &= prev[j] & cur[j] & nx;
+          o |= prev[j] | cur[j] | nx;
+        }
       }
     }
-    if (INT && !act) continue;
-    if (INT && SRC == SRC_SMOOTH)
-      update_block_int<R, MODEL, CPL>(P, (uint32_t)__cvta_generic_to_shared(s_lt),
-                                      s_ring + (threadIdx.x >> 5) * kRing * 32 * CPL, r, x0, A, B,
-                                      eps_u, prev, cur);
-    else
-      update_block<R, MODEL, SRC, INT, CPL>(P, s_lt, s_ls, r, x0, A, B, eps_u, prev, cur);
+    // uniform-window skip: phi constant over the block's stencil => b unchanged
+    if (P.skip_uniform && __all_sync(0xffffffffu, !act || a == ~0u || o == 0u)) {
+      if (!act) continue;
+      uint32_t* dst = P.bits_out + (size_t)r * P.g.pitch_w + x0;
+#pragma unroll
+      for (int q = 0; q < CPL / 4; ++q)
+        reinterpret_cast<uint4*>(dst)[q] = make_uint4(cur[R + 1 + 4 * q], cur[R + 2 + 4 * q],
+                                                      cur[R + 3 + 4 * q], cur[R + 4 + 4 * q]);
+      continue;
+    }
+    if (!act) continue;
+    update_block_int<R, MODEL, CPL>(P, (uint32_t)__cvta_generic_to_shared(s_lt),
+                                    s_ring + (threadIdx.x >> 5) * kRing * 32 * CPL, r, x0, A, B,
+                                    eps_u, prev, cur);
   }
 }
 
@@ -888,11 +900,82 @@ __device__ __forceinline__ void partition_block(const FastParams& P, const float
   }
 }
 
-// Interior units = (word-row, segment of seg_chunks chunks); border units =
-// single chunks.  Each unit's deltas form one partial; partials are laid
-// out [interior units][border units] (fixed geometry => deterministic).
-// A separate 1-CTA finalize kernel then reduces all partials.
-template <int R, bool PART, bool CKPT, bool MASKONLY, bool INT>
+struct LaneDelta {
+  double a_in, a_out;
+  long long n_in, n_out;
+  unsigned long long mism;
+};
+
+// P / M bit bookkeeping of one lane block (8 words) + the partition deltas.
+template <bool PART, bool CKPT, bool MASKONLY>
+__device__ __forceinline__ void partition_commit(const FastParams& P, int r, int x0,
+                                                 const uint32_t (&pw)[8], const uint32_t (&mw)[8],
+                                                 LaneDelta& d) {
+  const int y0 = r * 32;
+  const size_t base = (size_t)r * P.g.pitch_w + x0;
+  if (MASKONLY) {
+    reinterpret_cast<uint4*>(P.mbits + base)[0] = make_uint4(mw[0], mw[1], mw[2], mw[3]);
+    reinterpret_cast<uint4*>(P.mbits + base)[1] = make_uint4(mw[4], mw[5], mw[6], mw[7]);
+    return;
+  }
+  if (PART) {
+    const uint4 o0 = reinterpret_cast<const uint4*>(P.pbits + base)[0];
+    const uint4 o1 = reinterpret_cast<const uint4*>(P.pbits + base)[1];
+    const uint32_t old[8] = {o0.x, o0.y, o0.z, o0.w, o1.x, o1.y, o1.z, o1.w};
+    uint32_t any = 0u;
+#pragma unroll
+    for (int c = 0; c < 8; ++c) {
+      uint32_t chg = old[c] ^ pw[c];
+      any |= chg;
+      while (chg) {
+        const int b = __ffs(chg) - 1;
+        chg &= chg - 1;
+        const double I = data_exact(P.ctx, y0 + b, x0 + c);
+        if ((pw[c] >> b) & 1u) { d.a_in += I; ++d.n_in; }
+        else { d.a_out += I; ++d.n_out; }
+      }
+    }
+    if (any) {
+      reinterpret_cast<uint4*>(P.pbits + base)[0] = make_uint4(pw[0], pw[1], pw[2], pw[3]);
+      reinterpret_cast<uint4*>(P.pbits + base)[1] = make_uint4(pw[4], pw[5], pw[6], pw[7]);
+    }
+  }
+  if (CKPT) {
+    const uint4 o0 = reinterpret_cast<const uint4*>(P.mbits + base)[0];
+    const uint4 o1 = reinterpret_cast<const uint4*>(P.mbits + base)[1];
+    const uint32_t old[8] = {o0.x, o0.y, o0.z, o0.w, o1.x, o1.y, o1.z, o1.w};
+#pragma unroll
+    for (int c = 0; c < 8; ++c) d.mism += __popc(old[c] ^ mw[c]);
+    reinterpret_cast<uint4*>(P.mbits + base)[0] = make_uint4(mw[0], mw[1], mw[2], mw[3]);
+    reinterpret_cast<uint4*>(P.mbits + base)[1] = make_uint4(mw[4], mw[5], mw[6], mw[7]);
+  }
+}
+
+template <int R, bool PART, bool CKPT, bool MASKONLY>
+__device__ __noinline__ void border_partition_lane(const FastParams& P, const float* s_lt,
+                                                   const float* s_ls, int r, int x0,
+                                                   float eps_phi, LaneDelta& d) {
+  constexpr int NT = kColsPerThread + 2 * R;
+  uint32_t pw[8], mw[8], prev[NT], cur[NT];
+#pragma unroll
+  for (int j = 0; j < NT; ++j) {
+    const int xc = x0 - R + j;
+    prev[j] = word_at<false>(P, r - 1, xc);
+    cur[j] = word_at<false>(P, r, xc);
+  }
+  partition_block<R, false>(P, s_lt, s_ls, 0u, r, x0, eps_phi, prev, cur, pw, mw);
+  if (x0 + 8 > P.g.W) {
+#pragma unroll
+    for (int c = 0; c < 8; ++c) if (x0 + c >= P.g.W) { pw[c] = 0u; mw[c] = 0u; }
+  }
+  partition_commit<PART, CKPT, MASKONLY>(P, r, x0, pw, mw, d);
+}
+
+// Units: [border units][interior (word-row, segment of seg_chunks chunks)]
+// [interior B1 packs]; each unit's deltas form one partial at part[unit]
+// (fixed geometry => deterministic).  A separate 1-CTA finalize kernel then
+// reduces all partials.
+template <int R, bool PART, bool CKPT, bool MASKONLY>
 __global__ void __launch_bounds__(kThreads, 4) k_partition(FastParams P) {
   constexpr int NPAT = 1 << (2 * R + 1);
   constexpr int NT = kColsPerThread + 2 * R;
@@ -906,35 +989,33 @@ __global__ void __launch_bounds__(kThreads, 4) k_partition(FastParams P) {
   __syncthreads();
   const int lane = threadIdx.x & 31;
   const int nseg = P.nseg;
-  const int nunits = INT ? (P.gp.r_hi - P.gp.r_lo) * nseg + (P.gp.nB1 + 31) / 32
-                         : border_units(P.gp);
+  const int nb = border_units(P.gp);
+  const int nsu = (P.gp.r_hi - P.gp.r_lo) * nseg;
+  const int nunits = nb + nsu + (P.gp.nB1 + 31) / 32;
   for (;;) {
     const int unit = grab_unit(P, lane);
     if (unit >= nunits) break;
-    int r = 0, c0 = 0, c1 = 1, xb = 0;
-    bool active = true, chunked = false;
-    if (INT) {
-      const int nsu = (P.gp.r_hi - P.gp.r_lo) * nseg;
-      if (unit < nsu) {
+    LaneDelta d{0.0, 0.0, 0, 0, 0ull};
+    if (unit < nb) {
+      int r, x0;
+      if (border_lane(P.gp, unit, lane, P.g.W, r, x0))
+        border_partition_lane<R, PART, CKPT, MASKONLY>(P, s_lt, s_ls, r, x0, eps_phi, d);
+    } else {
+      const int iu = unit - nb;
+      int r = 0, c0 = 0, c1 = 1, xb = 0;
+      bool active = true, chunked = false;
+      if (iu < nsu) {
         chunked = true;
-        r = P.gp.r_lo + unit / nseg;
-        c0 = (unit % nseg) * P.seg_chunks;
+        r = P.gp.r_lo + iu / nseg;
+        c0 = (iu % nseg) * P.seg_chunks;
         c1 = min(c0 + P.seg_chunks, P.gp.nci);
         xb = P.gp.xoff + kColsPerThread * lane;
       } else {
-        active = b1_lane(P.gp, unit - nsu, lane, r, xb);
+        active = b1_lane(P.gp, iu - nsu, lane, r, xb);
       }
-    } else {
-      active = border_lane(P.gp, unit, lane, P.g.W, r, xb);
-    }
-    const int y0 = r * 32;
-    double a_in = 0.0, a_out = 0.0;
-    long long n_in = 0, n_out = 0;
-    unsigned long long mism = 0;
-    for (int ch = c0; ch < c1; ++ch) {
-      const int x0 = chunked ? xb + ch * kChunk : xb;
-      uint32_t pw[8], mw[8], prev[NT], cur[NT];
-      if (INT) {
+      for (int ch = c0; ch < c1; ++ch) {
+        const int x0 = chunked ? xb + ch * kChunk : xb;
+        uint32_t pw[8], mw[8], prev[NT], cur[NT];
         uint32_t a = ~0u, o = 0u;
         if (active) {
 #pragma unroll
@@ -956,77 +1037,29 @@ __global__ void __launch_bounds__(kThreads, 4) k_partition(FastParams P) {
         } else if (!active) {
           continue;
         } else {
-          partition_block<R, true>(P, s_lt, s_ls, (uint32_t)__cvta_generic_to_shared(s_lt), r, x0, eps_phi, prev, cur, pw, mw);
+          partition_block<R, true>(P, s_lt, s_ls, (uint32_t)__cvta_generic_to_shared(s_lt), r,
+                                   x0, eps_phi, prev, cur, pw, mw);
         }
-      } else {
-        if (!active) continue;
-#pragma unroll
-        for (int j = 0; j < NT; ++j) {
-          const int xc = x0 - R + j;
-          prev[j] = word_at<false>(P, r - 1, xc);
-          cur[j] = word_at<false>(P, r, xc);
-        }
-        partition_block<R, false>(P, s_lt, s_ls, 0u, r, x0, eps_phi, prev, cur, pw, mw);
-        if (x0 + 8 > P.g.W) {
-#pragma unroll
-          for (int c = 0; c < 8; ++c) if (x0 + c >= P.g.W) { pw[c] = 0u; mw[c] = 0u; }
-        }
-      }
-      const size_t base = (size_t)r * P.g.pitch_w + x0;
-      if (MASKONLY) {
-        reinterpret_cast<uint4*>(P.mbits + base)[0] = make_uint4(mw[0], mw[1], mw[2], mw[3]);
-        reinterpret_cast<uint4*>(P.mbits + base)[1] = make_uint4(mw[4], mw[5], mw[6], mw[7]);
-        continue;
-      }
-      if (PART) {
-        const uint4 o0 = reinterpret_cast<const uint4*>(P.pbits + base)[0];
-        const uint4 o1 = reinterpret_cast<const uint4*>(P.pbits + base)[1];
-        const uint32_t old[8] = {o0.x, o0.y, o0.z, o0.w, o1.x, o1.y, o1.z, o1.w};
-        uint32_t any = 0u;
-#pragma unroll
-        for (int c = 0; c < 8; ++c) {
-          uint32_t chg = old[c] ^ pw[c];
-          any |= chg;
-          while (chg) {
-            const int b = __ffs(chg) - 1;
-            chg &= chg - 1;
-            const double I = data_exact(P.ctx, y0 + b, x0 + c);
-            if ((pw[c] >> b) & 1u) { a_in += I; ++n_in; }
-            else { a_out += I; ++n_out; }
-          }
-        }
-        if (any) {
-          reinterpret_cast<uint4*>(P.pbits + base)[0] = make_uint4(pw[0], pw[1], pw[2], pw[3]);
-          reinterpret_cast<uint4*>(P.pbits + base)[1] = make_uint4(pw[4], pw[5], pw[6], pw[7]);
-        }
-      }
-      if (CKPT) {
-        const uint4 o0 = reinterpret_cast<const uint4*>(P.mbits + base)[0];
-        const uint4 o1 = reinterpret_cast<const uint4*>(P.mbits + base)[1];
-        const uint32_t old[8] = {o0.x, o0.y, o0.z, o0.w, o1.x, o1.y, o1.z, o1.w};
-#pragma unroll
-        for (int c = 0; c < 8; ++c) mism += __popc(old[c] ^ mw[c]);
-        reinterpret_cast<uint4*>(P.mbits + base)[0] = make_uint4(mw[0], mw[1], mw[2], mw[3]);
-        reinterpret_cast<uint4*>(P.mbits + base)[1] = make_uint4(mw[4], mw[5], mw[6], mw[7]);
+        partition_commit<PART, CKPT, MASKONLY>(P, r, x0, pw, mw, d);
       }
     }
     if (MASKONLY) continue;
 #pragma unroll
     for (int o = 16; o > 0; o >>= 1) {
-      a_in += __shfl_xor_sync(0xffffffffu, a_in, o);
-      a_out += __shfl_xor_sync(0xffffffffu, a_out, o);
-      n_in += __shfl_xor_sync(0xffffffffu, n_in, o);
-      n_out += __shfl_xor_sync(0xffffffffu, n_out, o);
-      mism += __shfl_xor_sync(0xffffffffu, mism, o);
+      d.a_in += __shfl_xor_sync(0xffffffffu, d.a_in, o);
+      d.a_out += __shfl_xor_sync(0xffffffffu, d.a_out, o);
+      d.n_in += __shfl_xor_sync(0xffffffffu, d.n_in, o);
+      d.n_out += __shfl_xor_sync(0xffffffffu, d.n_out, o);
+      d.mism += __shfl_xor_sync(0xffffffffu, d.mism, o);
     }
     if (lane == 0) {
       TilePartial t{};
-      t.a_hi = a_in;
-      t.b_hi = a_out;
-      t.n_a = n_in;
-      t.n_b = n_out;
-      t.mism = mism;
-      P.part[INT ? unit : P.n_int_part + unit] = t;   // [interior units][border units]
+      t.a_hi = d.a_in;
+      t.b_hi = d.a_out;
+      t.n_a = d.n_in;
+      t.n_b = d.n_out;
+      t.mism = d.mism;
+      P.part[unit] = t;
     }
   }
 }
