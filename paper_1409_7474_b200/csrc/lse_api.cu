@@ -166,6 +166,8 @@ struct lse_run {
   Geo gu{}, gu_all{}, gp{};   // work geometry: update, update with no interior, partition
   long long ni_upd = 0, nb_upd[2] = {0, 0}, ni_part = 0, nb_part = 0;
   unsigned long long* d_work = nullptr;
+  TilePartial* d_part_fin = nullptr;
+  TilePartial* d_part_init = nullptr;
   unsigned long long work_next = 0;   // host mirror of the monotonic work counter
   cudaEvent_t t_begin = nullptr, t_end = nullptr;
 };
@@ -246,11 +248,22 @@ int prepare(lse_run* r) {
   if (r->prepared) return LSE_OK;
   TRY(upload_ctx(r));
   if (r->p.model == LSE_MODEL_REGION) {
-    TRY(launch_partition_abs(r, r->mode == SRC_FIELD ? SRC_FIELD : r->mode, true, false, false,
-                             r->d_M));
-    k_finalize<<<1, 1024, 0, r->st>>>(r->d_part, r->g.ntiles, r->d_scal, 0, 1, 0,
-                                          r->iteration);
-    CKL();
+    if (r->mode == SRC_SCALED && !r->field_valid) {
+      // +-s state: P = b; coalesced double-double sums, one partial per CTA
+      const dim3 gr((r->g.pitch_w + 1023) / 1024, r->g.HR);
+      k_partition_init_bits<<<gr, 256, 0, r->st>>>(r->d_bits[r->cur], r->d_ctx, r->d_P,
+                                                   r->d_part_init, r->g);
+      CKL();
+      k_finalize<<<1, 1024, 0, r->st>>>(r->d_part_init, (int)(gr.x * gr.y), r->d_scal, 0, 1, 0,
+                                        r->iteration);
+      CKL();
+    } else {
+      TRY(launch_partition_abs(r, r->mode == SRC_FIELD ? SRC_FIELD : r->mode, true, false, false,
+                               r->d_M));
+      k_finalize<<<1, 1024, 0, r->st>>>(r->d_part, r->g.ntiles, r->d_scal, 0, 1, 0,
+                                        r->iteration);
+      CKL();
+    }
   }
   r->prepared = true;
   return LSE_OK;
@@ -274,8 +287,7 @@ unsigned long long take_work(lse_run* r, long long units, int grid) {
 
 template <int R, int MODEL, int SRC>
 int launch_update(lse_run* r, FastParams P) {
-  if (SRC == SRC_SCALED) P.gu = r->gu_all;
-  const long long n = SRC == SRC_SCALED ? r->nb_upd[1] : r->nb_upd[0] + r->ni_upd;
+  const long long n = r->nb_upd[0] + r->ni_upd;
   const int g = fast_grid(n);
   P.work_base = take_work(r, n, g);
   k_update<R, MODEL, SRC><<<g, kThreads, 0, r->st>>>(P);
@@ -291,9 +303,13 @@ int launch_partition(lse_run* r, FastParams P) {
   k_partition<R, PART, CKPT, MASKONLY><<<g, kThreads, 0, r->st>>>(P);
   CKL();
   if (!MASKONLY) {
-    // fixed-order reduction of all unit partials -> next update's coefficients
-    k_finalize_run<<<1, 1024, 0, r->st>>>(r->d_part, (int)n, r->d_scal, PART ? 1 : 0,
-                                          CKPT ? 1 : 0, P.iter);
+    // two-stage fixed-order reduction of all unit partials -> the next
+    // update's coefficients (64 CTAs reduce contiguous slices, 1 CTA the rest)
+    PartRanges R3{{r->d_part, r->d_part, r->d_part}, {(int)n, 0, 0}};
+    k_finalize_stage1<<<kFinSlices, 256, 0, r->st>>>(R3, r->d_part_fin, r->d_scal);
+    CKL();
+    PartRanges R1{{r->d_part_fin, r->d_part_fin, r->d_part_fin}, {kFinSlices, 0, 0}};
+    k_finalize_run<<<1, 1024, 0, r->st>>>(R1, r->d_scal, PART ? 1 : 0, CKPT ? 1 : 0, P.iter);
     CKL();
   }
   return LSE_OK;
@@ -540,7 +556,8 @@ int upload_image(lse_run* r, const void* image, int is_f32) {
   // image statistics for the closed-form normalizer / guards
   long long init[3] = {LLONG_MAX, LLONG_MIN, LLONG_MIN};
   CK(cudaMemcpyAsync(r->d_keys, init, sizeof(init), cudaMemcpyHostToDevice, r->st));
-  k_minmax<<<num_sms() * 4, 256, 0, r->st>>>(r->d_data32, r->d_data64, H, W, pitch, r->d_keys);
+  k_minmax<<<std::min(H, num_sms() * 8), 256, 0, r->st>>>(r->d_data32, r->d_data64, H, W, pitch,
+                                                          r->d_keys);
   CKL();
   k_store_minmax<<<1, 1, 0, r->st>>>(r->d_keys, r->d_scal);
   CKL();
@@ -573,8 +590,12 @@ int set_state(lse_run* r, const lse_phi0* s) {
     CK(cudaMemcpyAsync(doffs, offs.data(), offs.size() * sizeof(long long), cudaMemcpyHostToDevice,
                        r->st));
     CK(cudaMemsetAsync(r->d_count, 0, sizeof(unsigned long long), r->st));
-    k_rasterize<<<gw, 128, 0, r->st>>>(dxy, doffs, (int)s->n_polys, s->inside_sign,
-                                       r->d_bits[r->cur], nullptr, r->g, r->d_count);
+    if (offs.back() <= kRastEdges)
+      k_rasterize_rows<<<dim3((r->g.pitch_w + 255) / 256, r->g.HR), 256, 0, r->st>>>(
+          dxy, doffs, (int)s->n_polys, s->inside_sign, r->d_bits[r->cur], r->g, r->d_count);
+    else
+      k_rasterize<<<gw, 128, 0, r->st>>>(dxy, doffs, (int)s->n_polys, s->inside_sign,
+                                         r->d_bits[r->cur], nullptr, r->g, r->d_count);
     CKL();
     unsigned long long cnt = 0;
     CK(cudaMemcpyAsync(&cnt, r->d_count, sizeof(cnt), cudaMemcpyDeviceToHost, r->st));
@@ -746,7 +767,9 @@ int lse_run_create(lse_run** out, const lse_params* p, long long height, long lo
       (rc = dalloc(&r->d_scal, 1)) || (rc = dalloc(&r->d_lut_t, 512)) ||
       (rc = dalloc(&r->d_lut_s, 512)) || (rc = dalloc(&r->d_ctx, 1)) ||
       (rc = dalloc(&r->d_w64, 32)) || (rc = dalloc(&r->d_keys, 3)) ||
-      (rc = dalloc(&r->d_count, 1)) || (rc = dalloc(&r->d_work, 1)))
+      (rc = dalloc(&r->d_count, 1)) || (rc = dalloc(&r->d_work, 1)) ||
+      (rc = dalloc(&r->d_part_fin, kFinSlices)) ||
+      (rc = dalloc(&r->d_part_init, (size_t)r->g.HR * ((r->g.pitch_w + 1023) / 1024))))
     return cleanup(rc);
   if (cudaMallocHost((void**)&r->h_scal, sizeof(Scalars)) != cudaSuccess)
     return cleanup(fail(LSE_ERR_CUDA, "pinned alloc failed"));
@@ -972,7 +995,7 @@ int lse_run_kernel_times(lse_run* r, double* update_ms, long long* update_launch
 void lse_run_destroy(lse_run* r) {
   if (!r) return;
   if (r->st) cudaStreamSynchronize(r->st);
-  void* ptrs[] = {r->d_work, r->d_data32, r->d_data64, r->d_bits[0], r->d_bits[1], r->d_P, r->d_M,
+  void* ptrs[] = {r->d_work, r->d_part_fin, r->d_part_init, r->d_data32, r->d_data64, r->d_bits[0], r->d_bits[1], r->d_P, r->d_M,
                   r->d_mask, r->d_part, r->d_scal, r->d_lut_t, r->d_lut_s, r->d_ctx,
                   r->d_w64, r->d_keys, r->d_count, r->d_F[0], r->d_F[1], r->d_U, r->d_T};
   for (void* q : ptrs)
@@ -1039,7 +1062,7 @@ int region_scalars(const double* d_img, const double* d_phi, int H, int W, Scala
   CK(cudaMemcpy(d_sc, &s0, sizeof(s0), cudaMemcpyHostToDevice));
   long long init[3] = {LLONG_MAX, LLONG_MIN, LLONG_MIN};
   CK(cudaMemcpy(keys.p, init, sizeof(init), cudaMemcpyHostToDevice));
-  k_minmax<<<num_sms() * 4, 256>>>(nullptr, d_img, H, W, W, (long long*)keys.p);
+  k_minmax<<<std::min(H, num_sms() * 8), 256>>>(nullptr, d_img, H, W, W, (long long*)keys.p);
   CKL();
   k_store_minmax<<<1, 1>>>((long long*)keys.p, d_sc);
   CKL();

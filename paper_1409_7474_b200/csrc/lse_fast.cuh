@@ -424,10 +424,16 @@ __device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commi
 template <int N>
 __device__ __forceinline__ void cp_async_wait() { asm volatile("cp.async.wait_group %0;" ::"n"(N)); }
 
-template <int R, int NT, int NOUT>
+template <int R, int NT, int NOUT, int SRC = SRC_SMOOTH>
 __device__ __forceinline__ void phi_row_int(const FastParams& P, const uint32_t (&win4)[NT],
                                             int m0, uint32_t lut_base, float (&out)[NOUT]) {
   constexpr uint32_t PM4 = ((1u << (2 * R + 1)) - 1u) << 2;
+  if (SRC == SRC_SCALED) {                       // phi = +-s (binary initial state)
+#pragma unroll
+    for (int c = 0; c < NOUT; ++c)
+      out[c] = ((win4[c + R] >> (m0 + R + 2)) & 1u) ? P.scale32 : -P.scale32;
+    return;
+  }
 #pragma unroll
   for (int j = 0; j < NT; ++j) {
     const float t = lds_f32(((win4[j] >> m0) & PM4) | lut_base);
@@ -442,7 +448,7 @@ __device__ __forceinline__ void phi_row_int(const FastParams& P, const uint32_t 
   }
 }
 
-template <int R, int MODEL, int CPL>
+template <int R, int MODEL, int CPL, int SRC>
 __device__ __forceinline__ void update_block_int(const FastParams& P, uint32_t lut_base,
                                                  float* ring, int r, int x0, float A, float B,
                                                  float eps_u,
@@ -474,8 +480,8 @@ __device__ __forceinline__ void update_block_int(const FastParams& P, uint32_t l
 #pragma unroll
   for (int c = 0; c < CPL; ++c) ow[c] = 0u;
   (void)eps_u;
-  phi_row_int<R, NT, NP>(P, win4, 0, lut_base, pm);
-  phi_row_int<R, NT, NP>(P, win4, 1, lut_base, p0);
+  phi_row_int<R, NT, NP, SRC>(P, win4, 0, lut_base, pm);
+  phi_row_int<R, NT, NP, SRC>(P, win4, 1, lut_base, p0);
   const uint32_t* wrow = P.bits_in + (size_t)r * P.g.pitch_w + (x0 - (R + 1));
 #pragma unroll 4
   for (int k = 0; k < 32; ++k) {
@@ -494,7 +500,7 @@ __device__ __forceinline__ void update_block_int(const FastParams& P, uint32_t l
       for (int j = 0; j < NT; ++j)
         win4[j] = __funnelshift_r(__ldg(wrow + j), __ldg(wrow + P.g.pitch_w + j), 16 - R) << 2;
     }
-    phi_row_int<R, NT, NP>(P, win4, kk < 16 ? kk + 1 : kk - 16, lut_base, pn);
+    phi_row_int<R, NT, NP, SRC>(P, win4, kk < 16 ? kk + 1 : kk - 16, lut_base, pn);
     cp_async_wait<kRing - 1>();                 // row k has landed (this lane's copy)
     float d[CPL];
     {
@@ -533,7 +539,7 @@ __device__ __forceinline__ void update_block_int(const FastParams& P, uint32_t l
     const uint32_t bitk = 1u << k;
 #pragma unroll 1
     for (int c = 0; c < CPL; ++c) {
-      const bool pos = exact_u_fast<R, SRC_SMOOTH>(P.ctx, P.bits_in, y0 + k, x0 + c) > 0.0;
+      const bool pos = exact_u_fast<R, SRC>(P.ctx, P.bits_in, y0 + k, x0 + c) > 0.0;
 #pragma unroll
       for (int q = 0; q < CPL; ++q)
         if (q == c) ow[q] = pos ? (ow[q] | bitk) : (ow[q] & ~bitk);
@@ -615,7 +621,7 @@ __global__ void __launch_bounds__(kThreads, 4) k_update(FastParams P) {
   __syncthreads();
   const int lane = threadIdx.x & 31;
   const int nb = border_units(P.gu);
-  const int nunits = nb + (SRC == SRC_SMOOTH ? interior_units(P.gu) : 0);
+  const int nunits = nb + interior_units(P.gu);
   for (;;) {
     const int unit = grab_unit(P, lane);
     if (unit >= nunits) break;
@@ -625,7 +631,6 @@ __global__ void __launch_bounds__(kThreads, 4) k_update(FastParams P) {
         border_update_lane<R, MODEL, SRC>(P, s_lt, s_ls, r, x0, A, B, eps_u);
       continue;
     }
-    if (SRC != SRC_SMOOTH) continue;
     const int iu = unit - nb;
     bool act = true;
     const int nch = chunk_units(P.gu);
@@ -661,7 +666,7 @@ __global__ void __launch_bounds__(kThreads, 4) k_update(FastParams P) {
       continue;
     }
     if (!act) continue;
-    update_block_int<R, MODEL, CPL>(P, (uint32_t)__cvta_generic_to_shared(s_lt),
+    update_block_int<R, MODEL, CPL, SRC>(P, (uint32_t)__cvta_generic_to_shared(s_lt),
                                     s_ring + (threadIdx.x >> 5) * kRing * 32 * CPL, r, x0, A, B,
                                     eps_u, prev, cur);
   }
@@ -717,8 +722,75 @@ __device__ __forceinline__ void dd_shfl_add(double& hi, double& lo, int o) {
   dd_add_dd(hi, lo, h2, l2);
 }
 
-__device__ void finalize_cta(const TilePartial* part, int n, Scalars* sc, bool delta, bool region,
+// The partials form one virtual array: part0[0..n0) ++ part1[0..n1) ++ part2[0..n2).
+struct PartRanges {
+  const TilePartial* p[3];
+  int n[3];
+};
+
+__device__ __forceinline__ const TilePartial* part_at(const PartRanges& R3, int t) {
+  if (t < R3.n[0]) return R3.p[0] + t;
+  t -= R3.n[0];
+  if (t < R3.n[1]) return R3.p[1] + t;
+  return R3.p[2] + (t - R3.n[1]);
+}
+
+// Fixed-order CTA reduction of the virtual partial array slice [t0, t1) into
+// one double-double partial (written by thread 0 to *out) -- stage 1 of the
+// finalize, run by many CTAs.
+__device__ void reduce_slice(const PartRanges& R3, int t0, int t1, TilePartial* out) {
+  __shared__ double g_ah[32], g_al[32], g_bh[32], g_bl[32];
+  __shared__ long long g_na[32], g_nb[32];
+  __shared__ unsigned long long g_mm[32];
+  const int T = blockDim.x, tid = threadIdx.x;
+  double ah = 0, al = 0, bh = 0, bl = 0;
+  long long na = 0, nb = 0;
+  unsigned long long mm = 0;
+  const int n = t1 - t0;
+  const int per = (n + T - 1) / T;
+  const int lo = t0 + tid * per;
+  const int hi = min(lo + per, t1);
+  for (int t = lo; t < hi; ++t) {
+    const TilePartial* p = part_at(R3, t);
+    const double2 A = __ldcg(reinterpret_cast<const double2*>(&p->a_hi));
+    const double2 B = __ldcg(reinterpret_cast<const double2*>(&p->b_hi));
+    const longlong2 NN = __ldcg(reinterpret_cast<const longlong2*>(&p->n_a));
+    dd_add_dd(ah, al, A.x, A.y);
+    dd_add_dd(bh, bl, B.x, B.y);
+    na += NN.x;
+    nb += NN.y;
+    mm += __ldcg(&p->mism);
+  }
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) {
+    dd_shfl_add(ah, al, o);
+    dd_shfl_add(bh, bl, o);
+    na += __shfl_xor_sync(0xffffffffu, na, o);
+    nb += __shfl_xor_sync(0xffffffffu, nb, o);
+    mm += __shfl_xor_sync(0xffffffffu, mm, o);
+  }
+  const int warp = tid >> 5, lane = tid & 31;
+  if (lane == 0) {
+    g_ah[warp] = ah; g_al[warp] = al; g_bh[warp] = bh; g_bl[warp] = bl;
+    g_na[warp] = na; g_nb[warp] = nb; g_mm[warp] = mm;
+  }
+  __syncthreads();
+  if (tid == 0) {
+    TilePartial t{};
+    for (int w = 0; w < (T + 31) / 32; ++w) {
+      dd_add_dd(t.a_hi, t.a_lo, g_ah[w], g_al[w]);
+      dd_add_dd(t.b_hi, t.b_lo, g_bh[w], g_bl[w]);
+      t.n_a += g_na[w];
+      t.n_b += g_nb[w];
+      t.mism += g_mm[w];
+    }
+    *out = t;
+  }
+}
+
+__device__ void finalize_cta(const PartRanges& R3, Scalars* sc, bool delta, bool region,
                              bool ckpt, long long iter) {
+  const int n = R3.n[0] + R3.n[1] + R3.n[2];
   __shared__ double f_ah[32], f_al[32], f_bh[32], f_bl[32];
   __shared__ long long f_na[32], f_nb[32];
   __shared__ unsigned long long f_mm[32];
@@ -736,7 +808,7 @@ __device__ void finalize_cta(const TilePartial* part, int n, Scalars* sc, bool d
     unsigned long long M[4];
 #pragma unroll
     for (int q = 0; q < 4; ++q) {
-      const TilePartial* p = part + t + q;
+      const TilePartial* p = part_at(R3, t + q);
       A[q] = __ldcg(reinterpret_cast<const double2*>(&p->a_hi));
       B[q] = __ldcg(reinterpret_cast<const double2*>(&p->b_hi));
       NN[q] = __ldcg(reinterpret_cast<const longlong2*>(&p->n_a));
@@ -752,7 +824,7 @@ __device__ void finalize_cta(const TilePartial* part, int n, Scalars* sc, bool d
     }
   }
   for (; t < hi; ++t) {
-    const TilePartial* p = part + t;
+    const TilePartial* p = part_at(R3, t);
     const double2 A = __ldcg(reinterpret_cast<const double2*>(&p->a_hi));
     const double2 B = __ldcg(reinterpret_cast<const double2*>(&p->b_hi));
     const longlong2 NN = __ldcg(reinterpret_cast<const longlong2*>(&p->n_a));

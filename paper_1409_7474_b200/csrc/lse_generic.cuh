@@ -292,14 +292,26 @@ __global__ void __launch_bounds__(kThreads) k_partition_abs(const double* __rest
 __global__ void __launch_bounds__(1024) k_finalize(const TilePartial* part, int n, Scalars* sc,
                                                        int delta, int region, int ckpt,
                                                        long long iter) {
-  finalize_cta(part, n, sc, delta != 0, region != 0, ckpt != 0, iter);
+  PartRanges R3{{part, part, part}, {n, 0, 0}};
+  finalize_cta(R3, sc, delta != 0, region != 0, ckpt != 0, iter);
+}
+
+// stage 1 of the fast path's finalize: CTA b reduces slice b of the partials
+constexpr int kFinSlices = 64;
+__global__ void __launch_bounds__(256) k_finalize_stage1(PartRanges R3, TilePartial* out,
+                                                         const Scalars* sc) {
+  if (*(volatile const int*)&sc->stop) return;
+  const int n = R3.n[0] + R3.n[1] + R3.n[2];
+  const int per = (n + gridDim.x - 1) / gridDim.x;
+  const int t0 = min(n, (int)blockIdx.x * per), t1 = min(n, t0 + per);
+  reduce_slice(R3, t0, t1, out + blockIdx.x);
 }
 
 // per-iteration finalize of the fast path (DELTA partials); no-op once stopped
-__global__ void __launch_bounds__(1024) k_finalize_run(const TilePartial* part, int n, Scalars* sc,
-                                                       int region, int ckpt, long long iter) {
+__global__ void __launch_bounds__(1024) k_finalize_run(PartRanges R3, Scalars* sc, int region,
+                                                       int ckpt, long long iter) {
   if (*(volatile const int*)&sc->stop) return;
-  finalize_cta(part, n, sc, true, region != 0, ckpt != 0, iter);
+  finalize_cta(R3, sc, true, region != 0, ckpt != 0, iter);
 }
 
 // image statistics: min, max, max|.| (order-preserving integer atomics)
@@ -313,15 +325,15 @@ __device__ __forceinline__ double dkey_inv(long long k) {
 __global__ void k_minmax(const float* __restrict__ d32, const double* __restrict__ d64, int H, int W,
                          long long pitch, long long* keys /* [min, max, absmax] */) {
   long long kmin = LLONG_MAX, kmax = LLONG_MIN, kabs = LLONG_MIN;
-  const long long n = (long long)H * W;
-  for (long long q = (long long)blockIdx.x * blockDim.x + threadIdx.x; q < n;
-       q += (long long)gridDim.x * blockDim.x) {
-    const long long i = q / W, x = q - i * W;
-    const double v = d64 ? d64[i * pitch + x] : (double)d32[i * pitch + x];
-    const long long k = dkey(v), ka = dkey(fabs(v));
-    kmin = k < kmin ? k : kmin;
-    kmax = k > kmax ? k : kmax;
-    kabs = ka > kabs ? ka : kabs;
+  for (int i = blockIdx.x; i < H; i += gridDim.x) {
+    for (int x = threadIdx.x; x < W; x += blockDim.x) {
+      const size_t o = (size_t)i * pitch + x;
+      const double v = d64 ? d64[o] : (double)__ldcs(d32 + o);
+      const long long k = dkey(v), ka = dkey(fabs(v));
+      kmin = k < kmin ? k : kmin;
+      kmax = k > kmax ? k : kmax;
+      kabs = ka > kabs ? ka : kabs;
+    }
   }
   for (int o = 16; o > 0; o >>= 1) {
     long long a = __shfl_xor_sync(0xffffffffu, kmin, o);
@@ -414,6 +426,122 @@ __global__ void k_rasterize(const double* __restrict__ xy, const long long* __re
   }
   for (int o = 16; o > 0; o >>= 1) cnt += __shfl_xor_sync(0xffffffffu, cnt, o);
   if ((threadIdx.x & 31) == 0 && cnt) atomicAdd(n_inside, cnt);
+}
+
+// Same fill, for polygons with at most kRastEdges edges in total: per block of
+// 32 rows the crossing flags and x_hit of every (row, edge) are computed once
+// (exactly as grid.py:70-71 evaluates them) and shared by the block's columns.
+constexpr int kRastEdges = 64;
+__global__ void __launch_bounds__(256) k_rasterize_rows(const double* __restrict__ xy,
+                                                        const long long* __restrict__ offs,
+                                                        int n_polys, int inside_sign,
+                                                        uint32_t* bits, RunGeom g,
+                                                        unsigned long long* n_inside) {
+  __shared__ double s_xhit[32][kRastEdges];
+  __shared__ unsigned char s_cross[32][kRastEdges];
+  __shared__ short s_poly[kRastEdges];
+  const int r = blockIdx.y;
+  const int ne = (int)offs[n_polys];
+  for (int q = threadIdx.x; q < 32 * ne; q += blockDim.x) {
+    const int k = q / ne, e = q - k * ne;
+    int p = 0;
+    while (offs[p + 1] <= e) ++p;
+    const long long a = offs[p], nv = offs[p + 1] - a, qv = e - a;
+    const double x1 = xy[2 * e], y1 = xy[2 * e + 1];
+    const long long e2 = a + (qv + 1) % nv;
+    const double x2 = xy[2 * e2], y2 = xy[2 * e2 + 1];
+    const double cy = dadd((double)(r * 32 + k), 0.5);
+    bool crosses = false;
+    double xh = 0.0;
+    if (y1 != y2) {
+      crosses = (y1 > cy) != (y2 > cy);
+      xh = dadd(x1, ddiv(dmul(dsub(cy, y1), dsub(x2, x1)), dsub(y2, y1)));
+    }
+    s_xhit[k][e] = xh;
+    s_cross[k][e] = crosses;
+    if (k == 0) s_poly[e] = (short)p;
+  }
+  __syncthreads();
+  const int x = blockIdx.x * blockDim.x + threadIdx.x;
+  unsigned long long cnt = 0;
+  if (x < g.pitch_w) {
+    uint32_t w = 0u;
+    if (x < g.W) {
+      const double cx = dadd((double)x, 0.5);
+      for (int k = 0; k < 32; ++k) {
+        const int i = r * 32 + k;
+        if (i >= g.H) break;
+        bool inside = false, par = false;
+        int cur = 0;
+        for (int e = 0; e < ne; ++e) {
+          if (s_poly[e] != cur) {          // next polygon: union of even-odd fills
+            inside |= par;
+            par = false;
+            cur = s_poly[e];
+          }
+          if (s_cross[k][e] && cx < s_xhit[k][e]) par = !par;
+        }
+        inside |= par;
+        cnt += inside;
+        const bool pos = inside ? (inside_sign > 0) : (inside_sign < 0);
+        w |= (pos ? 1u : 0u) << k;
+      }
+    }
+    bits[(size_t)r * g.pitch_w + x] = w;
+  }
+  for (int o = 16; o > 0; o >>= 1) cnt += __shfl_xor_sync(0xffffffffu, cnt, o);
+  if ((threadIdx.x & 31) == 0 && cnt) atomicAdd(n_inside, cnt);
+}
+
+// Initial partition of a +-s state: P = b, sums of I over b = +1 / b = -1
+// (double-double), coalesced (lanes on consecutive columns), one partial per
+// CTA (1024 columns x 32 rows) in a fixed order.
+__global__ void __launch_bounds__(256) k_partition_init_bits(const uint32_t* __restrict__ bits,
+                                                             const ExactCtx* c, uint32_t* pbits,
+                                                             TilePartial* part, RunGeom g) {
+  __shared__ TilePartial s_w[8];
+  const int r = blockIdx.y;
+  double ah = 0, al = 0, bh = 0, bl = 0;
+  long long na = 0, nb = 0;
+  for (int j = 0; j < 4; ++j) {
+    const int x = blockIdx.x * 1024 + j * 256 + threadIdx.x;
+    if (x >= g.pitch_w) continue;
+    const uint32_t w = bits[(size_t)r * g.pitch_w + x];
+    pbits[(size_t)r * g.pitch_w + x] = w;
+    if (x >= g.W) continue;
+    for (int k = 0; k < 32; ++k) {
+      const int i = r * 32 + k;
+      if (i >= g.H) break;
+      const double I = data_exact(c, i, x);
+      if ((w >> k) & 1u) { dd_add(ah, al, I); ++na; }
+      else { dd_add(bh, bl, I); ++nb; }
+    }
+  }
+  for (int o = 16; o > 0; o >>= 1) {
+    double h2 = __shfl_xor_sync(0xffffffffu, ah, o), l2 = __shfl_xor_sync(0xffffffffu, al, o);
+    dd_add_dd(ah, al, h2, l2);
+    h2 = __shfl_xor_sync(0xffffffffu, bh, o);
+    l2 = __shfl_xor_sync(0xffffffffu, bl, o);
+    dd_add_dd(bh, bl, h2, l2);
+    na += __shfl_xor_sync(0xffffffffu, na, o);
+    nb += __shfl_xor_sync(0xffffffffu, nb, o);
+  }
+  const int warp = threadIdx.x >> 5;
+  if ((threadIdx.x & 31) == 0) {
+    s_w[warp].a_hi = ah; s_w[warp].a_lo = al; s_w[warp].b_hi = bh; s_w[warp].b_lo = bl;
+    s_w[warp].n_a = na; s_w[warp].n_b = nb;
+  }
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    TilePartial t{};
+    for (int w = 0; w < 8; ++w) {
+      dd_add_dd(t.a_hi, t.a_lo, s_w[w].a_hi, s_w[w].a_lo);
+      dd_add_dd(t.b_hi, t.b_lo, s_w[w].b_hi, s_w[w].b_lo);
+      t.n_a += s_w[w].n_a;
+      t.n_b += s_w[w].n_b;
+    }
+    part[(size_t)r * gridDim.x + blockIdx.x] = t;
+  }
 }
 
 // checkpoint-style mask bits -> host layout.  mask = (phi > 0) for
