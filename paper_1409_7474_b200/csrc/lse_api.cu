@@ -185,7 +185,10 @@ FastParams fast_params(lse_run* r) {
   P.scal = r->d_scal;
   P.ctx = r->d_ctx;
   P.g = r->g;
-  for (int d = 0; d < 8; ++d) P.w32[d] = d <= r->R ? (float)r->h_ctx.w64[d] : 0.f;
+  for (int d = 0; d < 8; ++d) {
+    P.w32[d] = d <= r->R ? (float)r->h_ctx.w64[d] : 0.f;
+    P.w2[d] = make_float2(P.w32[d], P.w32[d]);
+  }
   P.dt32 = (float)r->p.dt;
   P.scale32 = (float)r->scale;
   P.skip_uniform = r->skip_uniform;

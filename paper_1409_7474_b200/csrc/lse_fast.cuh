@@ -52,6 +52,7 @@ struct FastParams {
   const ExactCtx* ctx;
   RunGeom g;
   float w32[8];
+  float2 w2[8];              // (w, w) pairs: uniform operands of the packed FFMA2 pass
   float dt32;
   float scale32;
   long long iter;            // iteration produced by this launch
@@ -448,6 +449,181 @@ __device__ __forceinline__ void phi_row_int(const FastParams& P, const uint32_t 
   }
 }
 
+// ---- packed fp32x2 arithmetic (FFMA2 / FMUL2 / FADD2 on sm_100a)
+__device__ __forceinline__ float2 ffma2(float2 a, float2 b, float2 c) {
+  float2 d;
+  asm("{.reg .b64 ra, rb, rc, rd;\n\t"
+      "mov.b64 ra, {%2, %3};\n\tmov.b64 rb, {%4, %5};\n\tmov.b64 rc, {%6, %7};\n\t"
+      "fma.rn.f32x2 rd, ra, rb, rc;\n\tmov.b64 {%0, %1}, rd;}"
+      : "=f"(d.x), "=f"(d.y)
+      : "f"(a.x), "f"(a.y), "f"(b.x), "f"(b.y), "f"(c.x), "f"(c.y));
+  return d;
+}
+__device__ __forceinline__ float2 fmul2(float2 a, float2 b) {
+  float2 d;
+  asm("{.reg .b64 ra, rb, rd;\n\t"
+      "mov.b64 ra, {%2, %3};\n\tmov.b64 rb, {%4, %5};\n\t"
+      "mul.rn.f32x2 rd, ra, rb;\n\tmov.b64 {%0, %1}, rd;}"
+      : "=f"(d.x), "=f"(d.y) : "f"(a.x), "f"(a.y), "f"(b.x), "f"(b.y));
+  return d;
+}
+__device__ __forceinline__ float2 fsub2(float2 a, float2 b) {
+  float2 d;
+  asm("{.reg .b64 ra, rb, rd;\n\t"
+      "mov.b64 ra, {%2, %3};\n\tmov.b64 rb, {%4, %5};\n\t"
+      "sub.rn.f32x2 rd, ra, rb;\n\tmov.b64 {%0, %1}, rd;}"
+      : "=f"(d.x), "=f"(d.y) : "f"(a.x), "f"(a.y), "f"(b.x), "f"(b.y));
+  return d;
+}
+
+// Two phi rows at once (window offsets m0 and m0+1) as (row, row+1) pairs, so
+// the horizontal pass runs on the packed FFMA2 pipe: out[c] = sum_d w_d t(c+d).
+template <int R, int NT, int NOUT, int SRC = SRC_SMOOTH>
+__device__ __forceinline__ void phi_rows2_int(const FastParams& P, const uint32_t (&win4)[NT],
+                                              int m0, uint32_t lut_base, float2 (&out)[NOUT]) {
+  constexpr uint32_t PM4 = ((1u << (2 * R + 1)) - 1u) << 2;
+  if (SRC == SRC_SCALED) {
+#pragma unroll
+    for (int c = 0; c < NOUT; ++c) {
+      const uint32_t w = win4[c + R] >> (m0 + R + 2);
+      out[c] = make_float2((w & 1u) ? P.scale32 : -P.scale32,
+                           (w & 2u) ? P.scale32 : -P.scale32);
+    }
+    return;
+  }
+#pragma unroll
+  for (int j = 0; j < NT; ++j) {
+    float2 t;
+    t.x = lds_f32(((win4[j] >> m0) & PM4) | lut_base);
+    t.y = lds_f32(((win4[j] >> (m0 + 1)) & PM4) | lut_base);
+#pragma unroll
+    for (int c = 0; c < NOUT; ++c) {
+      const int d = j - c - R;
+      if (d < -R || d > R) continue;
+      const float2 wd = P.w2[d < 0 ? -d : d];
+      if (d == -R) out[c] = fmul2(wd, t);
+      else out[c] = ffma2(wd, t, out[c]);
+    }
+  }
+}
+
+constexpr int kRing2 = 8;                       // data rows buffered per warp (2-row steps)
+
+// Interior update block, two rows per step (see update_block_int for the
+// design); phi rows are kept as (row, row+1) pairs.
+template <int R, int MODEL, int CPL, int SRC>
+__device__ __forceinline__ void update_block_int2(const FastParams& P, uint32_t lut_base,
+                                                  float* ring, int r, int x0, float A, float B,
+                                                  float eps_u,
+                                                  const uint32_t (&prev)[CPL + 2 * (R + 1)],
+                                                  const uint32_t (&cur)[CPL + 2 * (R + 1)]) {
+  constexpr int NT = CPL + 2 * (R + 1);
+  constexpr int NP = CPL + 2;
+  constexpr uint32_t kSlot = 32 * CPL * 4;
+  const int y0 = r * 32;
+  const int lane = threadIdx.x & 31;
+  uint32_t win4[NT];
+#pragma unroll
+  for (int j = 0; j < NT; ++j) win4[j] = __funnelshift_r(prev[j], cur[j], 31 - R) << 2;
+  const uint32_t ring_s = (uint32_t)__cvta_generic_to_shared(ring) + lane * CPL * 4;
+  const size_t dpitch = P.g.data_pitch;
+  const float* gsrc = P.data32 + (size_t)y0 * dpitch + x0;
+#pragma unroll
+  for (int q = 0; q < kRing2 - 2; q += 2) {    // rows 0 .. 5 in flight, 2 per group
+#pragma unroll
+    for (int v = 0; v < CPL / 4; ++v) {
+      cp_async16(ring_s + q * kSlot + v * 16, gsrc + 4 * v);
+      cp_async16(ring_s + (q + 1) * kSlot + v * 16, gsrc + dpitch + 4 * v);
+    }
+    cp_async_commit();
+    gsrc += 2 * dpitch;
+  }
+  float2 pp[NP], pn[NP];
+  uint32_t ow[CPL];
+  uint32_t fbrows = 0u;
+#pragma unroll
+  for (int c = 0; c < CPL; ++c) ow[c] = 0u;
+  phi_rows2_int<R, NT, NP, SRC>(P, win4, 0, lut_base, pp);     // rows -1, 0
+  const uint32_t* wrow = P.bits_in + (size_t)r * P.g.pitch_w + (x0 - (R + 1));
+#pragma unroll 2
+  for (int s = 0; s < 16; ++s) {
+    {
+      if (2 * s + kRing2 - 2 < 32) {
+        const uint32_t d0 = ring_s + ((2 * s + kRing2 - 2) & (kRing2 - 1)) * kSlot;
+#pragma unroll
+        for (int v = 0; v < CPL / 4; ++v) {
+          cp_async16(d0 + v * 16, gsrc + 4 * v);
+          cp_async16(d0 + kSlot + v * 16, gsrc + dpitch + 4 * v);
+        }
+        gsrc += 2 * dpitch;
+      }
+      cp_async_commit();
+    }
+    if (s == 8) {                               // window base y0+16-R for rows >= 17
+#pragma unroll
+      for (int j = 0; j < NT; ++j)
+        win4[j] = __funnelshift_r(__ldg(wrow + j), __ldg(wrow + P.g.pitch_w + j), 16 - R) << 2;
+    }
+    const int kn = 2 * s + 1;                   // first phi row of this step's pair
+    phi_rows2_int<R, NT, NP, SRC>(P, win4, s < 8 ? kn + 1 : kn - 16, lut_base, pn);
+    cp_async_wait<kRing2 / 2 - 1>();            // rows 2s, 2s+1 have landed
+    float d0[CPL], d1[CPL];
+    {
+      const uint32_t src0 = ring_s + ((2 * s) & (kRing2 - 1)) * kSlot;
+#pragma unroll
+      for (int v = 0; v < CPL / 4; ++v) {
+        float4 q0, q1;
+        asm volatile("ld.shared.v4.f32 {%0, %1, %2, %3}, [%4];"
+                     : "=f"(q0.x), "=f"(q0.y), "=f"(q0.z), "=f"(q0.w) : "r"(src0 + v * 16));
+        asm volatile("ld.shared.v4.f32 {%0, %1, %2, %3}, [%4];"
+                     : "=f"(q1.x), "=f"(q1.y), "=f"(q1.z), "=f"(q1.w) : "r"(src0 + kSlot + v * 16));
+        d0[4 * v] = q0.x; d0[4 * v + 1] = q0.y; d0[4 * v + 2] = q0.z; d0[4 * v + 3] = q0.w;
+        d1[4 * v] = q1.x; d1[4 * v + 1] = q1.y; d1[4 * v + 2] = q1.z; d1[4 * v + 3] = q1.w;
+      }
+    }
+    float umin0 = 3.0e38f, umin1 = 3.0e38f;
+#pragma unroll
+    for (int c = 0; c < CPL; ++c) {
+      // rows 2s (centre pp.y) and 2s+1 (centre pn.x); dy = phi(k+1) - phi(k-1)
+      const float2 dy = fsub2(pn[c + 1], pp[c + 1]);
+      const float2 dx = make_float2(pp[c + 2].y - pp[c].y, pn[c + 2].x - pn[c].x);
+      const float2 s2 = ffma2(dx, dx, fmul2(dy, dy));
+      const float h0 = sqrt_approx(s2.x), h1 = sqrt_approx(s2.y);      // 2|grad phi|
+      const float vf0 = (MODEL == REGION) ? fmaf(A, d0[c], B) : d0[c];
+      const float vf1 = (MODEL == REGION) ? fmaf(A, d1[c], B) : d1[c];
+      const float u0 = fmaf(vf0, h0, pp[c + 1].y);
+      const float u1 = fmaf(vf1, h1, pn[c + 1].x);
+      ow[c] = __funnelshift_l(__float_as_uint(u0), ow[c], 1);
+      ow[c] = __funnelshift_l(__float_as_uint(u1), ow[c], 1);
+      umin0 = fminf(umin0, fabsf(u0));
+      umin1 = fminf(umin1, fabsf(u1));
+    }
+    if (umin0 <= eps_u) fbrows |= 1u << (2 * s);
+    if (umin1 <= eps_u) fbrows |= 2u << (2 * s);
+#pragma unroll
+    for (int c = 0; c < NP; ++c) pp[c] = pn[c];
+  }
+  cp_async_wait<0>();
+#pragma unroll
+  for (int c = 0; c < CPL; ++c) ow[c] = ~__brev(ow[c]);   // bit k = (u_k > 0) off ties
+  while (fbrows) {
+    const int k = __ffs(fbrows) - 1;
+    fbrows &= fbrows - 1;
+    const uint32_t bitk = 1u << k;
+#pragma unroll 1
+    for (int c = 0; c < CPL; ++c) {
+      const bool pos = exact_u_fast<R, SRC>(P.ctx, P.bits_in, y0 + k, x0 + c) > 0.0;
+#pragma unroll
+      for (int q = 0; q < CPL; ++q)
+        if (q == c) ow[q] = pos ? (ow[q] | bitk) : (ow[q] & ~bitk);
+    }
+  }
+  uint32_t* dst = P.bits_out + (size_t)r * P.g.pitch_w + x0;
+#pragma unroll
+  for (int q = 0; q < CPL / 4; ++q)
+    reinterpret_cast<uint4*>(dst)[q] = make_uint4(ow[4 * q], ow[4 * q + 1], ow[4 * q + 2], ow[4 * q + 3]);
+}
+
 template <int R, int MODEL, int CPL, int SRC>
 __device__ __forceinline__ void update_block_int(const FastParams& P, uint32_t lut_base,
                                                  float* ring, int r, int x0, float A, float B,
@@ -610,7 +786,7 @@ __global__ void __launch_bounds__(kThreads, 4) k_update(FastParams P) {
   constexpr int NT = CPL + 2 * (R + 1);
   __shared__ __align__(16) float s_lt_raw[1024];
   __shared__ float s_ls[NPAT];
-  __shared__ __align__(16) float s_ring[(kThreads / 32) * kRing * 32 * CPL];
+  __shared__ __align__(16) float s_ring[(kThreads / 32) * kRing2 * 32 * CPL];
   float* const s_lt = aligned_lut(s_lt_raw);
   const Scalars* sc = P.scal;
   if (*(volatile const int*)&sc->stop) return;
@@ -666,9 +842,9 @@ __global__ void __launch_bounds__(kThreads, 4) k_update(FastParams P) {
       continue;
     }
     if (!act) continue;
-    update_block_int<R, MODEL, CPL, SRC>(P, (uint32_t)__cvta_generic_to_shared(s_lt),
-                                    s_ring + (threadIdx.x >> 5) * kRing * 32 * CPL, r, x0, A, B,
-                                    eps_u, prev, cur);
+    update_block_int2<R, MODEL, CPL, SRC>(P, (uint32_t)__cvta_generic_to_shared(s_lt),
+                                          s_ring + (threadIdx.x >> 5) * kRing2 * 32 * CPL, r, x0,
+                                          A, B, eps_u, prev, cur);
   }
 }
 
@@ -925,14 +1101,19 @@ __device__ __forceinline__ void partition_block(const FastParams& P, const float
     const int i = y0 + k;
     if (!INT && i >= H) break;
     if (INT) {
-      phi_row_int<R, NT, 8>(P, win, k < 16 ? k : k - 16, lut_base, ph);
-      float pmin = 3.0e38f;
+      if (k & 1) continue;                                  // rows k, k+1 done as a pair
+      float2 ph2[8];
+      phi_rows2_int<R, NT, 8>(P, win, k < 16 ? k : k - 16, lut_base, ph2);
+      float pmin0 = 3.0e38f, pmin1 = 3.0e38f;
 #pragma unroll
       for (int c = 0; c < 8; ++c) {
-        pw[c] = __funnelshift_l(__float_as_uint(ph[c]), pw[c], 1);   // sign bits, reversed
-        pmin = fminf(pmin, fabsf(ph[c]));
+        pw[c] = __funnelshift_l(__float_as_uint(ph2[c].x), pw[c], 1);   // sign bits, reversed
+        pw[c] = __funnelshift_l(__float_as_uint(ph2[c].y), pw[c], 1);
+        pmin0 = fminf(pmin0, fabsf(ph2[c].x));
+        pmin1 = fminf(pmin1, fabsf(ph2[c].y));
       }
-      if (pmin <= eps_phi) fbrows |= 1u << k;
+      if (pmin0 <= eps_phi) fbrows |= 1u << k;
+      if (pmin1 <= eps_phi) fbrows |= 2u << k;
     } else {
       phi_row<R, SRC_SMOOTH, INT, NT, 8>(P, win, cm, k < 16 ? k : k - 16, i, s_lt, s_ls, ph);
       const uint32_t bitk = 1u << k;
