@@ -19,7 +19,7 @@
 extern "C" {
 #endif
 
-#define LSE_ABI_VERSION 1
+#define LSE_ABI_VERSION 2
 
 #define LSE_OK 0
 #define LSE_ERR_ARG 1            /* ValueError in the reference               */
@@ -28,10 +28,11 @@ extern "C" {
 #define LSE_ERR_DEGENERATE 4     /* DegeneratePartitionError (grid.py:20)     */
 #define LSE_ERR_NODEVICE 5       /* no CUDA device visible                    */
 #define LSE_ERR_DEGENERATE_SEED 6 /* DegenerateSeedError (grid.py:16)         */
-#define LSE_ERR_UNSUPPORTED 7    /* model outside the hot path (cv / zhang)   */
+#define LSE_ERR_UNSUPPORTED 7    /* model outside the device path (cv)        */
 
 #define LSE_MODEL_EDGE 0         /* ModelKind.EDGE   (models.py:30)  E_Td, Eq. 14 */
 #define LSE_MODEL_REGION 1       /* ModelKind.REGION (models.py:31)  R_Td, Eq. 17 */
+#define LSE_MODEL_ZHANG 2        /* ModelKind.ZHANG  (models.py:33)  mean separation (models.py:144-162) */
 
 /* EvolutionParams + ModelParams (engine.py:40-81, models.py:44-68).  The
  * Gaussian 1-D weights are passed in exactly as
@@ -52,6 +53,7 @@ typedef struct lse_params {
   double edge_gain;
   const double* reg_weights; /* ts_reg values */
   const double* pre_weights; /* ts_pre values (edge model) */
+  double nu;                 /* ModelParams.nu (zhang model speed constant) */
 } lse_params;
 
 #define LSE_PHI0_FIELD 0     /* float64 (H, W) level-set field                 */
@@ -174,6 +176,9 @@ int lse_region_means(const double* image, const double* phi, long long h, long l
 /* region_velocity (models.py:101-119) and edge_velocity (models.py:84-90). */
 int lse_region_velocity(const double* image, const double* phi, long long h, long long w,
                         double* v_out, int* degenerate);
+/* zhang_velocity (models.py:144-162); *degenerate as region_velocity. */
+int lse_zhang_velocity(const double* image, const double* phi, long long h, long long w, double nu,
+                       double* v_out, int* degenerate);
 int lse_edge_velocity(const double* g, const double* phi, long long h, long long w,
                       double* v_out);
 

@@ -7,6 +7,7 @@
  *   engine.py:148-174  _advance_once      (update, finiteness, reinit, smoothing)
  *   engine.py:222-254  EvolutionRun._step_once / advance (checkpoint convergence)
  *   models.py:84-119   edge_velocity / region_velocity
+ *   models.py:144-162  zhang_velocity (mean separation)
  *   models.py:71-81    edge_function
  *   grid.py:102-118    region_means  (numpy pairwise summation of the masked,
  *                                     row-major-compacted array, then / n)
@@ -24,7 +25,7 @@
 #endif
 
 typedef struct {
-  int model; /* 0 edge, 1 region */
+  int model; /* 0 edge, 1 region, 2 zhang */
   double dt;
   int ts_reg;
   int reinit_period;
@@ -36,6 +37,7 @@ typedef struct {
   int ts_pre;
   const double* reg_w; /* axis weights, ts_reg */
   const double* pre_w; /* axis weights, ts_pre */
+  double nu;           /* zhang speed constant */
 } oracle_params;
 
 /* scipy correlate1d, symmetric branch, zero padding. axis 0 = along rows. */
@@ -246,18 +248,28 @@ long long oracle_advance(oracle_ctx* c, long long n_iters) {
   for (long long s = 0; s < n_iters; ++s) {
     if (c->converged || c->iteration >= p->max_iters) break;
     const long long it = c->iteration + 1;
-    double cp = 0, cm = 0, dc = 0, peak = 0;
+    double cp = 0, cm = 0, dc = 0, peak = 0, mid = 0;
     int zero = 0;
-    if (p->model == 1) {
+    const int two_mean = p->model == 1 || p->model == 2;
+    if (two_mean) {
       if (!region_means(img, phi, H, W, c->bp, c->bn, c->rows, &cp, &cm)) {
         zero = 1;
       } else {
         dc = cp - cm;
+        mid = 0.5 * (cp + cm);                       /* models.py:153 */
         double pk = 0.0;
+        if (p->model == 1) {
 #pragma omp parallel for reduction(max : pk) schedule(static)
-        for (long long k = 0; k < (long long)n; ++k) {
-          double d = fabs(dc * (2.0 * img[k] - cp - cm));
-          if (d > pk) pk = d;
+          for (long long k = 0; k < (long long)n; ++k) {
+            double d = fabs(dc * (2.0 * img[k] - cp - cm));
+            if (d > pk) pk = d;
+          }
+        } else {
+#pragma omp parallel for reduction(max : pk) schedule(static)
+          for (long long k = 0; k < (long long)n; ++k) {
+            double d = fabs(img[k] - mid);             /* models.py:154 */
+            if (d > pk) pk = d;
+          }
         }
         peak = pk;
         if (peak == 0.0) zero = 1;
@@ -269,13 +281,14 @@ long long oracle_advance(oracle_ctx* c, long long n_iters) {
       for (int x = 0; x < W; ++x) {
         const size_t q = (size_t)i * W + x;
         double v;
-        if (p->model == 1 && zero) {
+        if (two_mean && zero) {
           v = 0.0;
         } else {
           double fx, fy;
           np_gradient(phi, H, W, i, x, &fx, &fy);
           double h = hypot(fx, fy);
           if (p->model == 1) v = (dc * (2.0 * img[q] - cp - cm) / peak) * h;
+          else if (p->model == 2) v = (p->nu * ((img[q] - mid) / peak)) * h;   /* models.py:162 */
           else v = g[q] * h;
         }
         double out = phi[q] + p->dt * v;
@@ -301,7 +314,7 @@ long long oracle_advance(oracle_ctx* c, long long n_iters) {
     }
     memcpy(phi, res, n * sizeof(double));
     c->iteration = it;
-    if (p->model == 1 && zero) c->degenerate = 1;
+    if (two_mean && zero) c->degenerate = 1;
     if (it % p->conv_check_every == 0) {
       const long long cw = p->conv_window;
       unsigned char* slot = c->ck + (size_t)(c->n_ck % (cw + 1)) * n;

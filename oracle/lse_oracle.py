@@ -32,6 +32,7 @@ import numpy as np
 
 REGION = "region"
 EDGE = "edge"
+ZHANG = "zhang"
 DT_STABILITY_LIMIT = 25.0          # engine.py:26
 
 
@@ -254,6 +255,19 @@ def region_velocity(image: np.ndarray, phi: np.ndarray):
     return (data / peak) * gradient_magnitude(phi), False
 
 
+def zhang_velocity(image: np.ndarray, phi: np.ndarray, nu: float):
+    """models.py:144-162 -- nu * ((I - m) / max|I - m|) * |grad phi|, m = (c+ + c-)/2."""
+    means = region_means(image, phi)
+    if means is None:
+        return np.zeros_like(phi), True
+    c_plus, c_minus = means
+    centered = image - 0.5 * (c_plus + c_minus)
+    peak = float(np.abs(centered).max())
+    if peak == 0.0:
+        return np.zeros_like(phi), True
+    return nu * (centered / peak) * gradient_magnitude(phi), False
+
+
 # --------------------------------------------------------------------------
 # engine.py
 # --------------------------------------------------------------------------
@@ -273,12 +287,15 @@ class OracleParams:
     sigma1: float = 1.0
     ts_pre: int = 9
     edge_gain: float = 255.0
+    nu: float = 1.0
 
 
 def advance_once(phi, iteration, image, p: OracleParams, g, w_reg):
     """engine.py:148-174 -- update, finiteness, reinit, regularize, guard."""
     if p.model == EDGE:
         v, degenerate = edge_velocity(g, phi), False
+    elif p.model == ZHANG:
+        v, degenerate = zhang_velocity(image, phi, p.nu)
     else:
         v, degenerate = region_velocity(image, phi)
     out = phi + p.dt * v

@@ -20,7 +20,8 @@ class OracleParamsC(C.Structure):
     _fields_ = [("model", C.c_int), ("dt", C.c_double), ("ts_reg", C.c_int),
                 ("reinit_period", C.c_int), ("reg_period", C.c_int), ("max_iters", C.c_longlong),
                 ("conv_check_every", C.c_longlong), ("conv_window", C.c_longlong),
-                ("edge_gain", C.c_double), ("ts_pre", C.c_int), ("reg_w", _dp), ("pre_w", _dp)]
+                ("edge_gain", C.c_double), ("ts_pre", C.c_int), ("reg_w", _dp), ("pre_w", _dp),
+                ("nu", C.c_double)]
 
 
 def load():
@@ -51,10 +52,10 @@ class COracleRun:
         self.phi = np.ascontiguousarray(phi0, dtype=np.float64).copy()
         self.wreg = np.ascontiguousarray(gaussian_weights(p.sigma2, p.ts_reg))
         self.wpre = np.ascontiguousarray(gaussian_weights(p.sigma1, p.ts_pre))
-        self.cp = OracleParamsC(1 if p.model == "region" else 0, p.dt, p.ts_reg, p.reinit_period,
+        self.cp = OracleParamsC({"edge": 0, "region": 1, "zhang": 2}[p.model], p.dt, p.ts_reg, p.reinit_period,
                                 p.reg_period, p.max_iters, p.conv_check_every, p.conv_window,
                                 p.edge_gain, p.ts_pre, self.wreg.ctypes.data_as(_dp),
-                                self.wpre.ctypes.data_as(_dp))
+                                self.wpre.ctypes.data_as(_dp), getattr(p, "nu", 1.0))
         h, w = self.image.shape
         self.ctx = self.lib.oracle_create(self.image.ctypes.data_as(_dp), h, w,
                                           C.byref(self.cp), self.phi.ctypes.data_as(_dp))

@@ -27,6 +27,7 @@ LSE_ERR_UNSUPPORTED = 7
 
 LSE_MODEL_EDGE = 0
 LSE_MODEL_REGION = 1
+LSE_MODEL_ZHANG = 2
 
 LSE_PHI0_FIELD = 0
 LSE_PHI0_SIGNS = 1
@@ -41,7 +42,8 @@ class LseParams(C.Structure):
                 ("ts_reg", C.c_int), ("reinit_period", C.c_int), ("reg_period", C.c_int),
                 ("max_iters", C.c_longlong), ("conv_check_every", C.c_longlong),
                 ("conv_window", C.c_longlong), ("sigma1", C.c_double), ("ts_pre", C.c_int),
-                ("edge_gain", C.c_double), ("reg_weights", _dp), ("pre_weights", _dp)]
+                ("edge_gain", C.c_double), ("reg_weights", _dp), ("pre_weights", _dp),
+                ("nu", C.c_double)]
 
 
 class LsePhi0(C.Structure):
@@ -93,6 +95,7 @@ _SIGS = {
     "lse_binarize": (_i, [_dp, _ll, _dp]),
     "lse_region_means": (_i, [_dp, _dp, _ll, _ll, _dp, _dp]),
     "lse_region_velocity": (_i, [_dp, _dp, _ll, _ll, _dp, C.POINTER(C.c_int)]),
+    "lse_zhang_velocity": (_i, [_dp, _dp, _ll, _ll, C.c_double, _dp, C.POINTER(C.c_int)]),
     "lse_edge_velocity": (_i, [_dp, _dp, _ll, _ll, _dp]),
     "lse_rasterize_seeds": (_i, [_dp, _llp, _ll, _i, _ll, _ll, C.POINTER(C.c_byte)]),
 }

@@ -246,11 +246,13 @@ int launch_partition_abs(lse_run* r, int src, bool part, bool ckpt, bool mask_on
   return LSE_OK;
 }
 
-// partition sums / coefficients for the current state (region model)
+bool two_mean(int model) { return model == LSE_MODEL_REGION || model == LSE_MODEL_ZHANG; }
+
+// partition sums / coefficients for the current state (region / zhang models)
 int prepare(lse_run* r) {
   if (r->prepared) return LSE_OK;
   TRY(upload_ctx(r));
-  if (r->p.model == LSE_MODEL_REGION) {
+  if (two_mean(r->p.model)) {
     if (r->mode == SRC_SCALED && !r->field_valid) {
       // +-s state: P = b; coalesced double-double sums, one partial per CTA
       const dim3 gr((r->g.pitch_w + 1023) / 1024, r->g.HR);
@@ -367,7 +369,8 @@ int launch_fast_model(lse_run* r, long long it, bool ckpt) {
 }
 
 int launch_fast(lse_run* r, long long it, bool ckpt) {
-  if (r->p.model == LSE_MODEL_REGION) return launch_fast_model<REGION>(r, it, ckpt);
+  // the mean-separation model differs only in its finalize coefficients
+  if (two_mean(r->p.model)) return launch_fast_model<REGION>(r, it, ckpt);
   return launch_fast_model<EDGE>(r, it, ckpt);
 }
 
@@ -415,7 +418,8 @@ int collect(lse_run* r) {
 bool fp32_ok(lse_run* r) {
   if (r->R < 1 || r->R > 4) return false;
   if (!(r->p.dt <= 1e6)) return false;
-  if (r->p.model == LSE_MODEL_REGION && !(r->img_absmax <= 1e6)) return false;
+  if (two_mean(r->p.model) && !(r->img_absmax <= 1e6)) return false;
+  if (r->p.model == LSE_MODEL_ZHANG && !(std::fabs(r->p.nu) <= 1e6)) return false;
   if (r->mode == SRC_SCALED && !(r->scale >= 1e-3 && r->scale <= 1e6)) return false;
   return true;
 }
@@ -425,7 +429,7 @@ int generic_iteration(lse_run* r, long long it, bool reinit_now, bool reg_now, b
   TRY(materialize(r));
   CK(cudaMemsetAsync(&r->d_scal->nonfinite, 0, sizeof(int), r->st));
   const double* phi = r->d_F[r->curF];
-  if (r->p.model == LSE_MODEL_REGION)
+  if (two_mean(r->p.model))
     k_gen_update<REGION><<<grid2(r->W, r->H), 128, 0, r->st>>>(
         phi, r->d_U, r->H, r->W, r->d_data32, r->d_data64, r->g.data_pitch, r->d_scal, r->p.dt);
   else
@@ -467,7 +471,7 @@ int generic_iteration(lse_run* r, long long it, bool reinit_now, bool reg_now, b
     CKL();
     r->mode = SRC_SMOOTH;
   }
-  const bool region = r->p.model == LSE_MODEL_REGION;
+  const bool region = two_mean(r->p.model);
   if (region || ckpt) {
     // partition from the exact field (field_valid => F[curF] is phi^{n+1})
     const double* field = r->d_F[r->curF];
@@ -516,7 +520,7 @@ int upload_image(lse_run* r, const void* image, int is_f32) {
     CK(cudaStreamSynchronize(r->st));
     r->fp32_exact = !inexact;
   }
-  if (r->p.model == LSE_MODEL_REGION) {
+  if (two_mean(r->p.model)) {
     if (!r->fp32_exact) {
       if (!r->d_data64) TRY(dalloc(&r->d_data64, (size_t)pitch * H));
       k_pitch64<<<grid2(W, H), 128, 0, r->st>>>(tmp64, r->d_data64, H, W, pitch);
@@ -706,8 +710,8 @@ int lse_run_create(lse_run** out, const lse_params* p, long long height, long lo
   *out = nullptr;
   if (height < 2 || width < 2) return fail(LSE_ERR_ARG, "gradient needs at least a 2x2 field");
   if (height > (1LL << 30) || width > (1LL << 30)) return fail(LSE_ERR_ARG, "grid too large");
-  if (p->model != LSE_MODEL_REGION && p->model != LSE_MODEL_EDGE)
-    return fail(LSE_ERR_UNSUPPORTED, "only the region and edge models run on the device path");
+  if (!two_mean(p->model) && p->model != LSE_MODEL_EDGE)
+    return fail(LSE_ERR_UNSUPPORTED, "only the region, zhang and edge models run on the device path");
   if (p->ts_reg < 1 || p->ts_reg % 2 == 0 || !p->reg_weights)
     return fail(LSE_ERR_ARG, "ts_reg must be an odd number >= 1");
   if (p->ts_reg > 63) return fail(LSE_ERR_ARG, "ts_reg > 63 is not supported");
@@ -792,7 +796,7 @@ int lse_run_create(lse_run** out, const lse_params* p, long long height, long lo
   r->h_ctx.dt = p->dt;
   r->h_ctx.scale = 1.0;
   r->h_ctx.scal = r->d_scal;
-  r->h_ctx.model = p->model == LSE_MODEL_REGION ? REGION : EDGE;
+  r->h_ctx.model = p->model == LSE_MODEL_REGION ? REGION : p->model == LSE_MODEL_ZHANG ? ZHANG : EDGE;
   cudaMemcpyAsync(r->d_w64, r->h_ctx.w64, 32 * sizeof(double), cudaMemcpyHostToDevice, r->st);
   // LUTs for the fast path (R <= 4)
   if (r->R >= 1 && r->R <= 4) {
@@ -815,6 +819,7 @@ int lse_run_create(lse_run** out, const lse_params* p, long long height, long lo
   s0.n_total = r->npx;
   s0.dt = p->dt;
   s0.model = r->h_ctx.model;
+  s0.nu = p->nu;
   s0.conv_window = p->conv_window;
   s0.eps_phi = (float)kEpsPhi;
   s0.eps_u = (float)edge_eps_u(p->dt);
@@ -1053,7 +1058,7 @@ int conv_device(const double* d_in, double* d_tmp, double* d_out, int H, int W, 
 
 // region coefficients (c+, c-, peak) of (image, phi) into a device Scalars
 int region_scalars(const double* d_img, const double* d_phi, int H, int W, Scalars* d_sc,
-                   Scalars* h_sc) {
+                   Scalars* h_sc, int model = REGION, double nu = 0.0) {
   const long long n = (long long)H * W;
   const int blocks = std::min<long long>((n + 255) / 256, num_sms() * 4);
   DevBuf part, keys;
@@ -1062,6 +1067,8 @@ int region_scalars(const double* d_img, const double* d_phi, int H, int W, Scala
   Scalars s0;
   std::memset(&s0, 0, sizeof(s0));
   s0.n_total = n;
+  s0.model = model;
+  s0.nu = nu;
   CK(cudaMemcpy(d_sc, &s0, sizeof(s0), cudaMemcpyHostToDevice));
   long long init[3] = {LLONG_MAX, LLONG_MIN, LLONG_MIN};
   CK(cudaMemcpy(keys.p, init, sizeof(init), cudaMemcpyHostToDevice));
@@ -1189,8 +1196,10 @@ int lse_region_means(const double* image, const double* phi, long long h, long l
   return LSE_OK;
 }
 
-int lse_region_velocity(const double* image, const double* phi, long long h, long long w,
-                        double* v_out, int* degenerate) {
+namespace {
+// region_velocity (models.py:101-119) / zhang_velocity (models.py:144-162)
+int two_mean_velocity(const double* image, const double* phi, long long h, long long w,
+                      int model, double nu, double* v_out, int* degenerate) {
   if (!image || !phi || !v_out || h < 1 || w < 1) return fail(LSE_ERR_ARG, "bad arguments");
   TRY(check_device());
   const long long n = h * w;
@@ -1202,10 +1211,10 @@ int lse_region_velocity(const double* image, const double* phi, long long h, lon
   CK(cudaMemcpy(a.p, image, n * sizeof(double), cudaMemcpyHostToDevice));
   CK(cudaMemcpy(b.p, phi, n * sizeof(double), cudaMemcpyHostToDevice));
   Scalars hs;
-  TRY(region_scalars((double*)a.p, (double*)b.p, (int)h, (int)w, (Scalars*)sc.p, &hs));
+  TRY(region_scalars((double*)a.p, (double*)b.p, (int)h, (int)w, (Scalars*)sc.p, &hs, model, nu));
   if (degenerate) *degenerate = hs.zero_vel;
   if (hs.zero_vel) {
-    // models.py:111-118: zero field, degenerate = True, gradient not evaluated
+    // models.py:111-118, 156-157: zero field, degenerate = True, gradient not evaluated
     std::memset(v_out, 0, n * sizeof(double));
     return LSE_OK;
   }
@@ -1215,6 +1224,17 @@ int lse_region_velocity(const double* image, const double* phi, long long h, lon
   CKL();
   CK(cudaMemcpy(v_out, v.p, n * sizeof(double), cudaMemcpyDeviceToHost));
   return LSE_OK;
+}
+}  // namespace
+
+int lse_region_velocity(const double* image, const double* phi, long long h, long long w,
+                        double* v_out, int* degenerate) {
+  return two_mean_velocity(image, phi, h, w, REGION, 0.0, v_out, degenerate);
+}
+
+int lse_zhang_velocity(const double* image, const double* phi, long long h, long long w, double nu,
+                       double* v_out, int* degenerate) {
+  return two_mean_velocity(image, phi, h, w, ZHANG, nu, v_out, degenerate);
 }
 
 int lse_edge_velocity(const double* g, const double* phi, long long h, long long w, double* v_out) {

@@ -21,7 +21,7 @@ constexpr int kThreads = 128;            // threads per CTA of the tiled kernels
 constexpr int kColsPerThread = 8;        // columns per thread (one 32-row word each)
 constexpr int kSpanMax = kColsPerThread * kThreads + 16;
 
-enum Model : int { EDGE = 0, REGION = 1 };
+enum Model : int { EDGE = 0, REGION = 1, ZHANG = 2 };   // ZHANG runs the REGION kernels
 enum Src : int { SRC_SMOOTH = 0, SRC_SCALED = 1, SRC_FIELD = 2 };
 
 // Per-run scalars shared by the kernels of one run (device resident).
@@ -29,6 +29,7 @@ struct __align__(16) Scalars {
   double sp_hi, sp_lo, sn_hi, sn_lo;  // running sums of I over {phi>=0} / {phi<0} (double-double)
   long long n_pos, n_total;
   double c_pos, c_neg, dc, peak;      // region coefficients of the next update (models.py:109-118)
+  double mid, nu;                     // zhang: m = (c+ + c-)/2, speed constant (models.py:152-162)
   double img_min, img_max, img_absmax;
   float A, B, eps_u, eps_phi;         // fp32 fast path: D/peak ~= A*I + B ; near-tie guards
   int zero_vel;                       // next update has v == 0 (degenerate, models.py:111-118)

@@ -76,6 +76,15 @@ __device__ __forceinline__ double data_exact(const ExactCtx* c, int i, int x) {
   return c->data64 ? c->data64[o] : (double)c->data32[o];
 }
 
+// Exact velocity of the two-mean models at intensity I and |grad phi| = h:
+// region (models.py:109-119) or mean separation (models.py:152-162).
+__device__ __forceinline__ double exact_v_twomean(const Scalars* sc, double I, double h) {
+  if (sc->zero_vel) return 0.0;
+  if (sc->model == ZHANG) return dmul(dmul(sc->nu, ddiv(dsub(I, sc->mid), sc->peak)), h);
+  const double D = dmul(sc->dc, dsub(dsub(dmul(2.0, I), sc->c_pos), sc->c_neg));
+  return dmul(ddiv(D, sc->peak), h);
+}
+
 __device__ __noinline__ double exact_phi(const ExactCtx* c, const uint32_t* bits, int src, int i, int x) {
   if (src == SRC_SCALED) return get_bit(bits, c->pitch_w, i, x) ? c->scale : -c->scale;
   return exact_phi_smooth(bits, c->pitch_w, c->H, c->W, c->R, c->w64, i, x);
@@ -96,14 +105,8 @@ __device__ __noinline__ double exact_u(const ExactCtx* c, const uint32_t* bits, 
   double h = np_hypot(fx, fy);
   double v;
   const Scalars* sc = c->scal;
-  if (c->model == REGION) {
-    if (sc->zero_vel) {
-      v = 0.0;
-    } else {
-      double I = data_exact(c, i, x);
-      double D = dmul(sc->dc, dsub(dsub(dmul(2.0, I), sc->c_pos), sc->c_neg));
-      v = dmul(ddiv(D, sc->peak), h);
-    }
+  if (c->model != EDGE) {
+    v = exact_v_twomean(sc, sc->zero_vel ? 0.0 : data_exact(c, i, x), h);
   } else {
     v = dmul(data_exact(c, i, x), h);
   }
@@ -204,14 +207,8 @@ __device__ __noinline__ double exact_u_fast(const ExactCtx* c, const uint32_t* b
   const double h = np_hypot(fx, fy);
   double v;
   const Scalars* sc = c->scal;
-  if (c->model == REGION) {
-    if (sc->zero_vel) {
-      v = 0.0;
-    } else {
-      const double I = data_exact(c, i, x);
-      const double D = dmul(sc->dc, dsub(dsub(dmul(2.0, I), sc->c_pos), sc->c_neg));
-      v = dmul(ddiv(D, sc->peak), h);
-    }
+  if (c->model != EDGE) {
+    v = exact_v_twomean(sc, sc->zero_vel ? 0.0 : data_exact(c, i, x), h);
   } else {
     v = dmul(data_exact(c, i, x), h);
   }
@@ -865,20 +862,32 @@ __device__ inline void region_coeffs(Scalars* sc) {
     double dmax = fabs(dmul(dc, dsub(dsub(dmul(2.0, sc->img_max), cp), cm)));
     double dmin = fabs(dmul(dc, dsub(dsub(dmul(2.0, sc->img_min), cp), cm)));
     double peak = dmax > dmin ? dmax : dmin;
+    double a, b;
+    if (sc->model == ZHANG) {                      // models.py:152-155
+      const double m = dmul(0.5, dadd(cp, cm));
+      const double pmax = fabs(dsub(sc->img_max, m)), pmin = fabs(dsub(sc->img_min, m));
+      peak = pmax > pmin ? pmax : pmin;
+      sc->mid = m;
+      a = sc->nu / peak;
+      b = -sc->nu * m / peak;
+    } else {
+      a = 2.0 * dc / peak;
+      b = -dc * (cp + cm) / peak;
+    }
     sc->c_pos = cp;
     sc->c_neg = cm;
     sc->dc = dc;
     sc->peak = peak;
-    if (peak == 0.0) {                             // models.py:117-118
+    if (peak == 0.0) {                             // models.py:117-118, 156-157
       sc->zero_vel = 1;
     } else {
-      double a = 2.0 * dc / peak;
-      double b = -dc * (cp + cm) / peak;
       sc->A = (float)(0.5 * dt * a);    // kernels evaluate u = phi + (A I + B) * 2|grad phi|
       sc->B = (float)(0.5 * dt * b);
       double eps_d = 0x1p-21 * (fabs(a) * sc->img_absmax + fabs(b) + 1.0);
-      sc->eps_u = (float)(4.0 * (0x1p-18 + dt * (0x1p-16 + 1.5 * eps_d + 0x1p-21) +
-                                 0x1p-22 * (1.0 + 1.5 * dt)));
+      // |v / |grad phi|| <= 1 for the region model, <= |nu| for zhang
+      const double vs = sc->model == ZHANG ? fmax(1.0, fabs(sc->nu)) : 1.0;
+      sc->eps_u = (float)(4.0 * (0x1p-18 + dt * vs * (0x1p-16 + 1.5 * eps_d + 0x1p-21) +
+                                 0x1p-22 * (1.0 + 1.5 * dt * vs)));
     }
   }
   if (sc->zero_vel) {

@@ -115,13 +115,7 @@ __global__ void k_gen_update(const double* __restrict__ phi, double* __restrict_
   const double h = np_hypot(fx, fy);
   const size_t od = (size_t)i * dpitch + x;
   const double d = data64 ? data64[od] : (double)data32[od];
-  double v;
-  if (MODEL == REGION) {
-    if (sc->zero_vel) v = 0.0;
-    else v = dmul(ddiv(dmul(sc->dc, dsub(dsub(dmul(2.0, d), sc->c_pos), sc->c_neg)), sc->peak), h);
-  } else {
-    v = dmul(d, h);
-  }
+  const double v = MODEL == REGION ? exact_v_twomean(sc, d, h) : dmul(d, h);
   const double out = dadd(phi[(size_t)i * W + x], dmul(dt, v));
   u[(size_t)i * W + x] = out;
   if (!isfinite(out)) sc->nonfinite = 1;
@@ -138,14 +132,7 @@ __global__ void k_velocity(const double* __restrict__ phi, double* __restrict__ 
   np_gradient(phi, H, W, i, x, fx, fy);
   const double h = np_hypot(fx, fy);
   const double d = data[(size_t)i * W + x];
-  double v;
-  if (MODEL == REGION) {
-    if (sc->zero_vel) v = 0.0;
-    else v = dmul(ddiv(dmul(sc->dc, dsub(dsub(dmul(2.0, d), sc->c_pos), sc->c_neg)), sc->peak), h);
-  } else {
-    v = dmul(d, h);
-  }
-  v_out[(size_t)i * W + x] = v;
+  v_out[(size_t)i * W + x] = MODEL == REGION ? exact_v_twomean(sc, d, h) : dmul(d, h);
 }
 
 __global__ void k_binarize(const double* __restrict__ in, double* __restrict__ out, long long n) {

@@ -142,10 +142,10 @@ class _DeviceState(EvolutionState):
 
 
 def _require_device_model(model: ModelKind):
-    if model not in (ModelKind.REGION, ModelKind.EDGE):
+    if model not in (ModelKind.REGION, ModelKind.EDGE, ModelKind.ZHANG):
         raise NotImplementedError(
             f"model {model.value!r} is a classical baseline outside the B200 hot path; "
-            "only 'region' (R_Td) and 'edge' (E_Td) run here")
+            "only 'region' (R_Td), 'edge' (E_Td) and 'zhang' run here")
 
 
 def _native_params(params: EvolutionParams, max_iters=None, conv_check_every=None):
@@ -153,7 +153,8 @@ def _native_params(params: EvolutionParams, max_iters=None, conv_check_every=Non
     wreg = np.ascontiguousarray(gaussian_kernel(params.sigma2, params.ts_reg).axis_weights)
     wpre = np.ascontiguousarray(gaussian_kernel(mp.sigma1, mp.ts_pre).axis_weights)
     p = N.LseParams()
-    p.model = N.LSE_MODEL_REGION if params.model is ModelKind.REGION else N.LSE_MODEL_EDGE
+    p.model = {ModelKind.REGION: N.LSE_MODEL_REGION, ModelKind.ZHANG: N.LSE_MODEL_ZHANG,
+               ModelKind.EDGE: N.LSE_MODEL_EDGE}[params.model]
     p.dt = float(params.dt)
     p.sigma2 = float(params.sigma2)
     p.ts_reg = int(params.ts_reg)
@@ -168,6 +169,7 @@ def _native_params(params: EvolutionParams, max_iters=None, conv_check_every=Non
     p.edge_gain = float(mp.edge_gain)
     p.reg_weights = N.dptr(wreg)
     p.pre_weights = N.dptr(wpre)
+    p.nu = float(mp.nu)
     return p, (wreg, wpre)
 
 

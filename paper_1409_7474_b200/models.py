@@ -2,10 +2,11 @@
 
 The two fast evolutions of the paper run on the device: the edge-based
 E_Td (Eq. 14; speed g * |grad phi|) and the region-based R_Td (Eq. 17;
-max-normalized two-mean contrast times |grad phi|).  The classical
-baselines `cv_velocity` / `zhang_velocity` are outside this build's hot path
-(BASELINE north star names only R_Td / E_Td) and raise NotImplementedError
-rather than silently running on the CPU.
+max-normalized two-mean contrast times |grad phi|), plus the mean-separation
+baseline `zhang_velocity`, which shares the region kernels (only the
+finalize coefficients differ).  The curvature-regularized CV baseline
+(`cv_velocity`) is outside this build and raises NotImplementedError rather
+than silently running on the CPU.
 """
 
 from __future__ import annotations
@@ -109,5 +110,18 @@ def cv_velocity(image, phi, mu, eps_guard=1e-10):
 
 
 def zhang_velocity(image, phi, nu):
-    """models.py:144-162 -- mean-separation baseline; not part of this build."""
-    raise NotImplementedError("the mean-separation (Zhang) baseline is not built here")
+    """models.py:144-162: nu * (I - m) / max|I - m| * |grad phi|, m = (c+ + c-)/2.
+
+    Degenerate partitions / constant images give (zeros, True) (device).
+    """
+    image = N.f64(image)
+    phi = N.f64(phi)
+    if image.shape != phi.shape:
+        raise ValueError(f"shape mismatch: image {image.shape} vs phi {phi.shape}")
+    if phi.ndim != 2:
+        raise ValueError("expected a 2-D field")
+    out = np.empty_like(phi)
+    deg = N.C.c_int(0)
+    N.check(N.lib.lse_zhang_velocity(N.dptr(image), N.dptr(phi), phi.shape[0], phi.shape[1],
+                                     float(nu), N.dptr(out), N.C.byref(deg)))
+    return out, bool(deg.value)

@@ -30,7 +30,8 @@ import lsekit  # noqa: E402  (the reference)
 from lsekit import (EvolutionRun, EvolutionState, ModelKind, SeedSpec,  # noqa: E402
                     NumericalInstabilityError, binarize, convolve_same,
                     default_params, edge_function, gaussian_kernel,
-                    gradient_central, rasterize_seeds, region_means, step)
+                    gradient_central, rasterize_seeds, region_means, step,
+                    zhang_velocity)
 
 import importlib.util  # noqa: E402
 
@@ -126,6 +127,7 @@ def trajectory(name, image, seeds, prm, record, store=None):
                               p.model_params.sigma1, p.model_params.ts_pre,
                               p.model_params.edge_gain])
     out["model"] = np.array(p.model.value)
+    out["nu"] = np.array(p.model_params.nu)
     print(f"{name}: iters={r.state.iteration} conv={r.converged} err={err} "
           f"{time.perf_counter() - t0:.2f}s")
     return out
@@ -214,7 +216,32 @@ def main():
             cfg.name, cfg.image.astype(np.float64), seeds, prm, [cfg.iters], store="hash")
         fixtures[f"traj_{cfg.name}"]["image"] = np.array(0)   # regenerated from scenes.py
 
+    # mean-separation (Zhang) baseline, models.py:144-162 (acceptance A4)
+    zr = np.random.default_rng(41)
+    zh = {}
+    for k, nu in enumerate([1.5, 1.0, -0.7, 4.0]):
+        img, phi = zr.random((14 + k, 19 - k)), zr.standard_normal((14 + k, 19 - k))
+        v, deg = zhang_velocity(img, phi, nu)
+        zh[f"img_{k}"], zh[f"phi_{k}"], zh[f"nu_{k}"] = img, phi, np.array(nu)
+        zh[f"v_{k}"], zh[f"deg_{k}"] = v, np.array(deg)
+    phi = rasterize_seeds(SeedSpec(polygons=(square(2, 2, 6, 6),)), 12, 12)
+    v, deg = zhang_velocity(np.full((12, 12), 0.5), phi, 1.0)
+    zh["img_c"], zh["phi_c"], zh["v_c"], zh["deg_c"] = np.full((12, 12), 0.5), phi, v, np.array(deg)
+    fixtures["zhang"] = zh
+    fixtures["traj_zhang_small"] = trajectory(
+        "zhang_small", img_r, seed_r, params(ModelKind.ZHANG, max_iters=25), [1, 2, 3, 10, 25])
+    fixtures["traj_zhang_nu"] = trajectory(
+        "zhang_nu", img_r, SeedSpec(polygons=(square(6, 8, 30, 38),), inside_sign=1),
+        params(ModelKind.ZHANG, nu=2.5, dt=6.0, max_iters=20), [1, 5, 20])
+    for sign in (-1, 1):
+        fixtures[f"traj_a4_{'neg' if sign < 0 else 'pos'}"] = trajectory(
+            f"a4_{sign}", a1, SeedSpec(polygons=(square(28, 28, 100, 100),), inside_sign=sign),
+            params(ModelKind.ZHANG, nu=1.0, max_iters=1000), [1000], store="hash")
+
+    only = set(sys.argv[1:])
     for name, arrs in fixtures.items():
+        if only and name not in only:
+            continue
         np.savez_compressed(os.path.join(HERE, f"{name}.npz"), **arrs)
     print("wrote", len(fixtures), "fixtures; lsekit", lsekit.__version__)
 

@@ -47,6 +47,23 @@ def test_a3_sign_robustness():
     assert d["e", -1] >= 0.8 and d["e", 1] < 0.5
 
 
+def test_a4_zhang_sign_sensitivity():
+    """test_acceptance.py:95-105: the mean-separation baseline depends on the sign."""
+    image, truth = two_region()
+    ds = {}
+    for sign in (-1, 1):
+        seed = L.SeedSpec(polygons=(square(28, 28, 100, 100),), inside_sign=sign)
+        r = L.run(image, seed, L.default_params(L.ModelKind.ZHANG, nu=1.0, max_iters=1000))
+        ds[sign] = dice(r.mask, truth)
+    assert ds[-1] >= 0.95 and ds[1] < 0.5
+
+
+def test_zhang_init_state_is_binary():
+    image, _ = two_region()
+    st = L.init_state(image, A1_SEED, L.default_params(L.ModelKind.ZHANG))
+    assert set(np.unique(st.phi)) == {-1.0, 1.0} and st.iteration == 0
+
+
 def test_a5_noise_robustness():
     image, truth = two_region()
     rd, ed = [], []

@@ -24,7 +24,8 @@ TRAJ = ["traj_region_small", "traj_edge_small", "traj_region_field", "traj_regio
         "traj_edge_mixed", "traj_degenerate", "traj_odd_ts3", "traj_odd_ts5", "traj_odd_ts7",
         "traj_odd_edge_ts3", "traj_odd_edge_ts5", "traj_odd_edge_ts7", "traj_thin",
         "traj_a1", "traj_a1_cw2", "traj_a1_cw1", "traj_a1_edge", "traj_a2_edge",
-        "traj_a5_region", "traj_a5_edge", "traj_instability"]
+        "traj_a5_region", "traj_a5_edge", "traj_instability", "traj_zhang_small",
+        "traj_zhang_nu", "traj_a4_neg", "traj_a4_pos"]
 
 
 def sha(a):
@@ -40,7 +41,8 @@ def params_from(g):
                                 reinit_period=int(p[3]), reg_period=int(p[4]),
                                 max_iters=int(p[5]), conv_check_every=int(p[6]),
                                 conv_window=int(p[7]), sigma1=float(p[8]), ts_pre=int(p[9]),
-                                edge_gain=float(p[10]))
+                                edge_gain=float(p[10]),
+                                nu=float(g["nu"]) if "nu" in g else 1.0)
 
 
 def exact_expected(prm):
@@ -146,6 +148,19 @@ def test_velocities_match_oracle():
     gg = O.edge_function(img, 1.0, 9)
     assert np.array_equal(L.edge_velocity(gg, phi), O.edge_velocity(gg, phi))
     v, deg = L.region_velocity(np.full((12, 12), 0.5), np.where(rng.random((12, 12)) > .5, 1., -1.))
+    assert deg and not v.any()
+
+
+def test_zhang_velocity_matches_reference():
+    g = load_golden("zhang")
+    for k in range(4):
+        v, deg = L.zhang_velocity(g[f"img_{k}"], g[f"phi_{k}"], float(g[f"nu_{k}"]))
+        assert deg == bool(g[f"deg_{k}"])
+        # c+/c- are correctly rounded on the device, numpy's pairwise mean can be
+        # an ulp off: a few ulp of |v| (same bar as region_velocity below)
+        want = g[f"v_{k}"]
+        assert np.abs(v - want).max() <= 4 * np.finfo(float).eps * np.abs(want).max(), k
+    v, deg = L.zhang_velocity(g["img_c"], g["phi_c"], 1.0)
     assert deg and not v.any()
 
 

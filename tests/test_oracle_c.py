@@ -19,7 +19,9 @@ def sha(a):
                                   "traj_region_mixed", "traj_edge_mixed", "traj_degenerate",
                                   "traj_odd_ts3", "traj_odd_edge_ts7", "traj_thin", "traj_a1",
                                   "traj_a1_cw2", "traj_a1_cw1", "traj_a2_edge",
-                                  "traj_a5_region", "traj_instability", "traj_C1"])
+                                  "traj_a5_region", "traj_instability", "traj_C1",
+                                  "traj_zhang_small", "traj_zhang_nu", "traj_a4_neg",
+                                  "traj_a4_pos"])
 def test_c_oracle_matches_reference(name):
     g = load_golden(name)
     if name == "traj_C1":

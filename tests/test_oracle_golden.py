@@ -46,6 +46,15 @@ def test_rasterize_bit_exact():
     assert np.array_equal(out, g["rast_b1_out"])
 
 
+def test_zhang_velocity_bit_exact():
+    g = load_golden("zhang")
+    for k in range(4):
+        v, deg = O.zhang_velocity(g[f"img_{k}"], g[f"phi_{k}"], float(g[f"nu_{k}"]))
+        assert np.array_equal(v, g[f"v_{k}"]) and deg == bool(g[f"deg_{k}"])
+    v, deg = O.zhang_velocity(g["img_c"], g["phi_c"], 1.0)
+    assert deg and bool(g["deg_c"]) and not v.any() and not g["v_c"].any()
+
+
 def test_glibc_hypot_restatement():
     rng = np.random.default_rng(0)
     for e in (-200, -20, 0, 20, 200):
@@ -60,7 +69,8 @@ def _params(g):
                           ts_reg=int(p[2]), reinit_period=int(p[3]), reg_period=int(p[4]),
                           max_iters=int(p[5]), conv_check_every=int(p[6]),
                           conv_window=int(p[7]), sigma1=float(p[8]), ts_pre=int(p[9]),
-                          edge_gain=float(p[10]))
+                          edge_gain=float(p[10]),
+                          nu=float(g["nu"]) if "nu" in g else 1.0)
 
 
 def _phi0(g, shape):
@@ -74,7 +84,8 @@ def _phi0(g, shape):
                                   "traj_odd_edge_ts3", "traj_odd_edge_ts5", "traj_odd_edge_ts7",
                                   "traj_thin", "traj_a1", "traj_a1_cw2", "traj_a1_cw1",
                                   "traj_a1_edge", "traj_a2_edge", "traj_a5_region",
-                                  "traj_a5_edge", "traj_instability"])
+                                  "traj_a5_edge", "traj_instability", "traj_zhang_small",
+                                  "traj_zhang_nu", "traj_a4_neg", "traj_a4_pos"])
 def test_oracle_trajectories_bit_exact(name):
     g = load_golden(name)
     img = g["image"]
