@@ -19,7 +19,7 @@
 extern "C" {
 #endif
 
-#define LSE_ABI_VERSION 2
+#define LSE_ABI_VERSION 3
 
 #define LSE_OK 0
 #define LSE_ERR_ARG 1            /* ValueError in the reference               */
@@ -74,6 +74,8 @@ typedef struct lse_phi0 {
   long long iteration;            /* EvolutionState.iteration                */
   int converged;                  /* EvolutionState.converged                */
   int degenerate;                 /* EvolutionState.degenerate               */
+  long long row_offset;           /* LSE_PHI0_POLYGONS: global row of local row 0
+                                     (row strips; 0 otherwise)               */
 } lse_phi0;
 
 typedef struct lse_status {
@@ -147,6 +149,39 @@ int lse_run_kernel_times(lse_run* run, double* update_ms, long long* update_laun
 
 void lse_run_destroy(lse_run* run);
 
+/* ---- row strips: one rank's share of a multi-GPU run --------
+ * A rank owns whole word-rows (32 image rows) of the global grid and holds
+ * one halo word-row of each neighbour.  Per iteration of _advance_once
+ * (engine.py:148-174), with the exchanges between the phases done by the
+ * caller's communicator on lse_run_stream(run):
+ *   lse_strip_update      update of iteration n+1 (b^n -> b^{n+1})
+ *   <halo exchange>       own first/last word-row -> neighbours' halo rows
+ *                         (lse_run_bits_row pointers, pitch_words uint32 each)
+ *   lse_strip_partition   partition / checkpoint pass -> one partial
+ *                         (LSE_PARTIAL_BYTES) per rank, if *partition_next
+ *   <allgather>           the ranks' partials, in rank order
+ *   lse_strip_finalize    c+/c-, coefficients, convergence -- identical on
+ *                         every rank (same partials, same fixed order)
+ * Setup: lse_strip_create (local rows incl. halos, seeds in local
+ * coordinates, n_total = global pixel count), lse_strip_image_range ->
+ * allreduce min/max/max|.| -> lse_strip_set_image_range, lse_strip_prepare
+ * -> allgather -> lse_strip_finalize(absolute = 1).  Row strips run the
+ * binary-state fast path only (reinit_period = reg_period = 1). */
+#define LSE_PARTIAL_BYTES 64
+int lse_strip_create(lse_run** out, const lse_params* p, long long height, long long width,
+                     const void* image, int image_is_f32, const lse_phi0* init, int own_lo,
+                     int own_hi, long long n_total);
+int lse_strip_image_range(lse_run* run, double* min_max_absmax);
+int lse_strip_set_image_range(lse_run* run, const double* min_max_absmax);
+int lse_strip_prepare(lse_run* run, void* partial_out);
+int lse_strip_update(lse_run* run, int* partition_next);
+int lse_strip_partition(lse_run* run, void* partial_out);
+int lse_strip_finalize(lse_run* run, const void* partials, int n_partials, int absolute);
+int lse_strip_sync(lse_run* run, lse_status* st);
+void* lse_run_stream(lse_run* run);
+void* lse_run_bits_row(lse_run* run, int word_row);
+int lse_run_geometry(lse_run* run, int* word_rows, int* pitch_words);
+
 /* ---- stateless kernels of the public API --------------------------------- */
 
 /* edge_function (models.py:71-81): g = 1/(1 + (gain fx)^2 + (gain fy)^2). */
@@ -176,11 +211,12 @@ int lse_region_means(const double* image, const double* phi, long long h, long l
 /* region_velocity (models.py:101-119) and edge_velocity (models.py:84-90). */
 int lse_region_velocity(const double* image, const double* phi, long long h, long long w,
                         double* v_out, int* degenerate);
+int lse_edge_velocity(const double* g, const double* phi, long long h, long long w,
+                      double* v_out);
+
 /* zhang_velocity (models.py:144-162); *degenerate as region_velocity. */
 int lse_zhang_velocity(const double* image, const double* phi, long long h, long long w, double nu,
                        double* v_out, int* degenerate);
-int lse_edge_velocity(const double* g, const double* phi, long long h, long long w,
-                      double* v_out);
 
 /* rasterize_seeds (grid.py:76-93): +-1 as int8; LSE_ERR_DEGENERATE_SEED when
  * the union covers no pixel centre or every pixel centre. */

@@ -28,6 +28,7 @@ LSE_ERR_UNSUPPORTED = 7
 LSE_MODEL_EDGE = 0
 LSE_MODEL_REGION = 1
 LSE_MODEL_ZHANG = 2
+LSE_PARTIAL_BYTES = 64
 
 LSE_PHI0_FIELD = 0
 LSE_PHI0_SIGNS = 1
@@ -50,7 +51,8 @@ class LsePhi0(C.Structure):
     _fields_ = [("kind", C.c_int), ("field", _dp), ("signs", C.POINTER(C.c_byte)),
                 ("scale", C.c_double), ("poly_xy", _dp), ("poly_counts", _llp),
                 ("n_polys", C.c_longlong), ("inside_sign", C.c_int),
-                ("iteration", C.c_longlong), ("converged", C.c_int), ("degenerate", C.c_int)]
+                ("iteration", C.c_longlong), ("converged", C.c_int), ("degenerate", C.c_int),
+                ("row_offset", C.c_longlong)]
 
 
 class LseStatus(C.Structure):
@@ -88,6 +90,18 @@ _SIGS = {
     "lse_run_set_profiling": (_i, [_vp, _i]),
     "lse_run_kernel_times": (_i, [_vp, _dp, _llp, _dp, _llp]),
     "lse_run_destroy": (None, [_vp]),
+    "lse_strip_create": (_i, [C.POINTER(_vp), C.POINTER(LseParams), _ll, _ll, _vp, _i,
+                              C.POINTER(LsePhi0), _i, _i, _ll]),
+    "lse_strip_image_range": (_i, [_vp, _dp]),
+    "lse_strip_set_image_range": (_i, [_vp, _dp]),
+    "lse_strip_prepare": (_i, [_vp, _vp]),
+    "lse_strip_update": (_i, [_vp, C.POINTER(C.c_int)]),
+    "lse_strip_partition": (_i, [_vp, _vp]),
+    "lse_strip_finalize": (_i, [_vp, _vp, _i, _i]),
+    "lse_strip_sync": (_i, [_vp, C.POINTER(LseStatus)]),
+    "lse_run_stream": (_vp, [_vp]),
+    "lse_run_bits_row": (_vp, [_vp, _i]),
+    "lse_run_geometry": (_i, [_vp, C.POINTER(C.c_int), C.POINTER(C.c_int)]),
     "lse_edge_function": (_i, [_dp, _ll, _ll, _dp, _i, C.c_double, _dp]),
     "lse_convolve_same": (_i, [_dp, _ll, _ll, _dp, _i, _dp]),
     "lse_correlate2d": (_i, [_dp, _ll, _ll, _dp, _i, _dp]),

@@ -170,6 +170,14 @@ struct lse_run {
   TilePartial* d_part_init = nullptr;
   unsigned long long work_next = 0;   // host mirror of the monotonic work counter
   cudaEvent_t t_begin = nullptr, t_end = nullptr;
+  // row strips (multi-GPU): word-rows [own_lo, own_hi) are this rank's, the
+  // others are halo copies of the neighbours' rows; the partition phase
+  // reduces to one partial at strip_out and the ranks finalize together
+  bool strip = false;
+  int own_lo = 0, own_hi = 0;
+  TilePartial* strip_out = nullptr;
+  bool strip_part = false, strip_ckpt = false;   // phases owed by the last update
+  cudaEvent_t pev[2] = {nullptr, nullptr};       // profiling events of the pending update
 };
 
 namespace {
@@ -199,6 +207,8 @@ FastParams fast_params(lse_run* r) {
   P.work = r->d_work;
   P.gu = r->gu;
   P.gp = r->gp;
+  P.own_lo = r->own_lo;
+  P.own_hi = r->own_hi;
   return P;
 }
 
@@ -257,7 +267,7 @@ int prepare(lse_run* r) {
       // +-s state: P = b; coalesced double-double sums, one partial per CTA
       const dim3 gr((r->g.pitch_w + 1023) / 1024, r->g.HR);
       k_partition_init_bits<<<gr, 256, 0, r->st>>>(r->d_bits[r->cur], r->d_ctx, r->d_P,
-                                                   r->d_part_init, r->g);
+                                                   r->d_part_init, r->g, r->own_lo, r->own_hi);
       CKL();
       k_finalize<<<1, 1024, 0, r->st>>>(r->d_part_init, (int)(gr.x * gr.y), r->d_scal, 0, 1, 0,
                                         r->iteration);
@@ -314,29 +324,48 @@ int launch_partition(lse_run* r, FastParams P) {
     k_finalize_stage1<<<kFinSlices, 256, 0, r->st>>>(R3, r->d_part_fin, r->d_scal);
     CKL();
     PartRanges R1{{r->d_part_fin, r->d_part_fin, r->d_part_fin}, {kFinSlices, 0, 0}};
-    k_finalize_run<<<1, 1024, 0, r->st>>>(R1, r->d_scal, PART ? 1 : 0, CKPT ? 1 : 0, P.iter);
+    if (r->strip) {
+      // row strips: this rank's contribution; the ranks exchange it and
+      // finalize together (lse_strip_finalize)
+      k_reduce_to_one<<<1, 256, 0, r->st>>>(R1, r->strip_out, r->d_scal, 1);
+    } else {
+      k_finalize_run<<<1, 1024, 0, r->st>>>(R1, r->d_scal, PART ? 1 : 0, CKPT ? 1 : 0, P.iter);
+    }
     CKL();
   }
   return LSE_OK;
 }
 
+// One fast iteration in two phases: PH_UPDATE launches the update of
+// iteration `it` (b^n -> b^{n+1}) and makes b^{n+1} the current state;
+// PH_PARTITION launches the partition / checkpoint pass over it.  A single-GPU
+// run does both back to back; a row strip exchanges its halo rows in between.
+enum Phase : int { PH_BOTH = 0, PH_UPDATE = 1, PH_PARTITION = 2 };
+
 template <int R, int MODEL>
-int launch_fast_R(lse_run* r, long long it, bool ckpt) {
+int launch_fast_R(lse_run* r, long long it, bool ckpt, int phase) {
   FastParams P = fast_params(r);
-  P.bits_in = r->d_bits[r->cur];
-  P.bits_out = r->d_bits[r->cur ^ 1];
   P.iter = it;
-  cudaEvent_t e0 = nullptr, e1 = nullptr, e2 = nullptr;
-  if (r->prof) {
-    e0 = next_event(r);
-    e1 = next_event(r);
-    e2 = next_event(r);
-    cudaEventRecord(e0, r->st);
+  if (phase != PH_PARTITION) {
+    P.bits_in = r->d_bits[r->cur];
+    P.bits_out = r->d_bits[r->cur ^ 1];
+    if (r->prof) {
+      r->pev[0] = next_event(r);
+      r->pev[1] = next_event(r);
+      cudaEventRecord(r->pev[0], r->st);
+    }
+    if (r->mode == SRC_SCALED) TRY((launch_update<R, MODEL, SRC_SCALED>(r, P)));
+    else TRY((launch_update<R, MODEL, SRC_SMOOTH>(r, P)));
+    if (r->prof) cudaEventRecord(r->pev[1], r->st);
+    r->cur ^= 1;
+    r->mode = SRC_SMOOTH;
+    r->field_valid = false;
+    r->launched.emplace_back(it, r->cur);
+    r->strip_part = MODEL == REGION || ckpt;
+    r->strip_ckpt = ckpt;
+    if (phase == PH_UPDATE) return LSE_OK;
   }
-  if (r->mode == SRC_SCALED) TRY((launch_update<R, MODEL, SRC_SCALED>(r, P)));
-  else TRY((launch_update<R, MODEL, SRC_SMOOTH>(r, P)));
-  if (r->prof) cudaEventRecord(e1, r->st);
-  P.bits_in = r->d_bits[r->cur ^ 1];
+  P.bits_in = r->d_bits[r->cur];
   bool launched_part = false;
   if (MODEL == REGION) {
     if (ckpt) TRY((launch_partition<R, true, true, false>(r, P)));
@@ -347,31 +376,28 @@ int launch_fast_R(lse_run* r, long long it, bool ckpt) {
     launched_part = true;
   }
   if (r->prof) {
+    cudaEvent_t e2 = next_event(r);
     cudaEventRecord(e2, r->st);
-    r->evrec.push_back({e0, e1, e2, launched_part});
+    r->evrec.push_back({r->pev[0], r->pev[1], e2, launched_part});
   }
-  r->cur ^= 1;
-  r->mode = SRC_SMOOTH;
-  r->field_valid = false;
-  r->launched.emplace_back(it, r->cur);
   return LSE_OK;
 }
 
 template <int MODEL>
-int launch_fast_model(lse_run* r, long long it, bool ckpt) {
+int launch_fast_model(lse_run* r, long long it, bool ckpt, int phase) {
   switch (r->R) {
-    case 1: return launch_fast_R<1, MODEL>(r, it, ckpt);
-    case 2: return launch_fast_R<2, MODEL>(r, it, ckpt);
-    case 3: return launch_fast_R<3, MODEL>(r, it, ckpt);
-    case 4: return launch_fast_R<4, MODEL>(r, it, ckpt);
+    case 1: return launch_fast_R<1, MODEL>(r, it, ckpt, phase);
+    case 2: return launch_fast_R<2, MODEL>(r, it, ckpt, phase);
+    case 3: return launch_fast_R<3, MODEL>(r, it, ckpt, phase);
+    case 4: return launch_fast_R<4, MODEL>(r, it, ckpt, phase);
   }
   return fail(LSE_ERR_ARG, "unsupported template radius");
 }
 
-int launch_fast(lse_run* r, long long it, bool ckpt) {
+int launch_fast(lse_run* r, long long it, bool ckpt, int phase = PH_BOTH) {
   // the mean-separation model differs only in its finalize coefficients
-  if (two_mean(r->p.model)) return launch_fast_model<REGION>(r, it, ckpt);
-  return launch_fast_model<EDGE>(r, it, ckpt);
+  if (two_mean(r->p.model)) return launch_fast_model<REGION>(r, it, ckpt, phase);
+  return launch_fast_model<EDGE>(r, it, ckpt, phase);
 }
 
 // wait for the device, fold profiling events, detect convergence
@@ -599,18 +625,21 @@ int set_state(lse_run* r, const lse_phi0* s) {
     CK(cudaMemsetAsync(r->d_count, 0, sizeof(unsigned long long), r->st));
     if (offs.back() <= kRastEdges)
       k_rasterize_rows<<<dim3((r->g.pitch_w + 255) / 256, r->g.HR), 256, 0, r->st>>>(
-          dxy, doffs, (int)s->n_polys, s->inside_sign, r->d_bits[r->cur], r->g, r->d_count);
+          dxy, doffs, (int)s->n_polys, s->inside_sign, r->d_bits[r->cur], r->g, r->d_count, s->row_offset);
     else
       k_rasterize<<<gw, 128, 0, r->st>>>(dxy, doffs, (int)s->n_polys, s->inside_sign,
-                                         r->d_bits[r->cur], nullptr, r->g, r->d_count);
+                                         r->d_bits[r->cur], nullptr, r->g, r->d_count,
+                                         s->row_offset);
     CKL();
     unsigned long long cnt = 0;
     CK(cudaMemcpyAsync(&cnt, r->d_count, sizeof(cnt), cudaMemcpyDeviceToHost, r->st));
     CK(cudaStreamSynchronize(r->st));
     cudaFree(dxy);
     cudaFree(doffs);
-    if (cnt == 0) return fail(LSE_ERR_DEGENERATE_SEED, "seed polygons cover no pixel centers");
-    if ((long long)cnt == r->npx)
+    // (a row strip's seed count is global: the coordinator checks it)
+    if (cnt == 0 && !r->strip)
+      return fail(LSE_ERR_DEGENERATE_SEED, "seed polygons cover no pixel centers");
+    if ((long long)cnt == r->npx && !r->strip)
       return fail(LSE_ERR_DEGENERATE_SEED, "seed polygons cover the entire grid");
     r->mode = SRC_SCALED;
     r->scale = 1.0;
@@ -704,8 +733,14 @@ int lse_device_count(void) {
   return n;
 }
 
-int lse_run_create(lse_run** out, const lse_params* p, long long height, long long width,
-                   const void* image, int image_is_f32, const lse_phi0* init) {
+namespace {
+struct StripInfo {
+  int own_lo, own_hi;
+  long long n_total;
+};
+
+int create_impl(lse_run** out, const lse_params* p, long long height, long long width,
+                const void* image, int image_is_f32, const lse_phi0* init, const StripInfo* si) {
   if (!out || !p || !image || !init) return fail(LSE_ERR_ARG, "null argument");
   *out = nullptr;
   if (height < 2 || width < 2) return fail(LSE_ERR_ARG, "gradient needs at least a 2x2 field");
@@ -737,6 +772,13 @@ int lse_run_create(lse_run** out, const lse_params* p, long long height, long lo
   r->nthr = (int)std::min<long long>(kThreads, need_thr);
   r->g.ncb = (r->W + kColsPerThread * r->nthr - 1) / (kColsPerThread * r->nthr);
   r->g.ntiles = r->g.HR * r->g.ncb;
+  r->own_lo = 0;
+  r->own_hi = r->g.HR;
+  if (si) {
+    r->strip = true;
+    r->own_lo = si->own_lo;
+    r->own_hi = si->own_hi;
+  }
   r->nchunk = (r->W + kChunk - 1) / kChunk;
   r->nchunk_u = (r->W + kUpdChunk - 1) / kUpdChunk;
   {
@@ -816,7 +858,7 @@ int lse_run_create(lse_run** out, const lse_params* p, long long height, long lo
   // scalars
   Scalars s0;
   std::memset(&s0, 0, sizeof(s0));
-  s0.n_total = r->npx;
+  s0.n_total = si ? si->n_total : r->npx;
   s0.dt = p->dt;
   s0.model = r->h_ctx.model;
   s0.nu = p->nu;
@@ -828,6 +870,129 @@ int lse_run_create(lse_run** out, const lse_params* p, long long height, long lo
   if ((rc = upload_image(r, image, image_is_f32))) return cleanup(rc);
   if ((rc = set_state(r, init))) return cleanup(rc);
   *out = r;
+  return LSE_OK;
+}
+}  // namespace
+
+int lse_run_create(lse_run** out, const lse_params* p, long long height, long long width,
+                   const void* image, int image_is_f32, const lse_phi0* init) {
+  return create_impl(out, p, height, width, image, image_is_f32, init, nullptr);
+}
+
+// ------------------------------------------------------------- row strips
+int lse_strip_create(lse_run** out, const lse_params* p, long long height, long long width,
+                     const void* image, int image_is_f32, const lse_phi0* init, int own_lo,
+                     int own_hi, long long n_total) {
+  if (!out || !p || !init) return fail(LSE_ERR_ARG, "null argument");
+  if (p->reinit_period != 1 || p->reg_period != 1 || p->ts_reg < 3 || p->ts_reg > 9)
+    return fail(LSE_ERR_UNSUPPORTED,
+                "row strips run the binary-state fast path (reinit_period = reg_period = 1, "
+                "3 <= ts_reg <= 9)");
+  if (init->kind == LSE_PHI0_FIELD)
+    return fail(LSE_ERR_UNSUPPORTED, "row strips start from seeds or signs");
+  const long long HR = (height + 31) / 32;
+  if (own_lo < 0 || own_lo > 1 || own_hi <= own_lo || own_hi > HR || own_hi < HR - 1)
+    return fail(LSE_ERR_ARG, "a strip owns all its word-rows but at most one halo row per side");
+  if (n_total < height * width) return fail(LSE_ERR_ARG, "n_total smaller than the strip");
+  StripInfo si{own_lo, own_hi, n_total};
+  return create_impl(out, p, height, width, image, image_is_f32, init, &si);
+}
+
+int lse_strip_image_range(lse_run* r, double* out3) {
+  if (!r || !out3 || !r->strip) return fail(LSE_ERR_ARG, "not a row strip");
+  CK(cudaMemcpyAsync(r->h_scal, r->d_scal, sizeof(Scalars), cudaMemcpyDeviceToHost, r->st));
+  CK(cudaStreamSynchronize(r->st));
+  out3[0] = r->h_scal->img_min;
+  out3[1] = r->h_scal->img_max;
+  out3[2] = r->h_scal->img_absmax;
+  return LSE_OK;
+}
+
+int lse_strip_set_image_range(lse_run* r, const double* in3) {
+  if (!r || !in3 || !r->strip) return fail(LSE_ERR_ARG, "not a row strip");
+  CK(cudaStreamSynchronize(r->st));
+  CK(cudaMemcpy(&r->d_scal->img_min, in3, 3 * sizeof(double), cudaMemcpyHostToDevice));
+  r->img_absmax = in3[2];
+  return LSE_OK;
+}
+
+int lse_strip_prepare(lse_run* r, void* part_out) {
+  if (!r || !part_out || !r->strip) return fail(LSE_ERR_ARG, "not a row strip");
+  if (r->mode != SRC_SCALED || r->field_valid || !fp32_ok(r))
+    return fail(LSE_ERR_UNSUPPORTED, "row strips need a binary state on the fast path");
+  TRY(upload_ctx(r));
+  CK(cudaMemsetAsync(r->d_work, 0, sizeof(unsigned long long), r->st));
+  r->work_next = 0;
+  const dim3 gr((r->g.pitch_w + 1023) / 1024, r->g.HR);
+  k_partition_init_bits<<<gr, 256, 0, r->st>>>(r->d_bits[r->cur], r->d_ctx, r->d_P,
+                                               r->d_part_init, r->g, r->own_lo, r->own_hi);
+  CKL();
+  PartRanges R1{{r->d_part_init, r->d_part_init, r->d_part_init}, {(int)(gr.x * gr.y), 0, 0}};
+  k_reduce_to_one<<<1, 256, 0, r->st>>>(R1, (TilePartial*)part_out, r->d_scal, 0);
+  CKL();
+  return LSE_OK;
+}
+
+int lse_strip_update(lse_run* r, int* partition_next) {
+  if (!r || !r->strip) return fail(LSE_ERR_ARG, "not a row strip");
+  if (!r->prepared) return fail(LSE_ERR_ARG, "lse_strip_prepare / lse_strip_finalize first");
+  if (r->mode == SRC_FIELD || !fp32_ok(r))
+    return fail(LSE_ERR_UNSUPPORTED, "row strips need a binary state on the fast path");
+  const long long it = r->iteration + 1;
+  TRY(launch_fast(r, it, it % r->p.conv_check_every == 0, PH_UPDATE));
+  r->iteration = it;
+  r->fast_iters++;
+  if (partition_next) *partition_next = r->strip_part ? 1 : 0;
+  return LSE_OK;
+}
+
+int lse_strip_partition(lse_run* r, void* part_out) {
+  if (!r || !r->strip) return fail(LSE_ERR_ARG, "not a row strip");
+  if (!r->strip_part) return LSE_OK;
+  if (!part_out) return fail(LSE_ERR_ARG, "null partial");
+  r->strip_out = (TilePartial*)part_out;
+  TRY(launch_fast(r, r->iteration, r->strip_ckpt, PH_PARTITION));
+  return LSE_OK;
+}
+
+int lse_strip_finalize(lse_run* r, const void* parts, int nparts, int absolute) {
+  if (!r || !r->strip || !parts || nparts < 1) return fail(LSE_ERR_ARG, "bad arguments");
+  const TilePartial* tp = (const TilePartial*)parts;
+  if (absolute) {
+    if (two_mean(r->p.model)) {
+      k_finalize<<<1, 1024, 0, r->st>>>(tp, nparts, r->d_scal, 0, 1, 0, r->iteration);
+      CKL();
+    }
+    r->prepared = true;
+    return LSE_OK;
+  }
+  if (!r->strip_part) return LSE_OK;
+  PartRanges R{{tp, tp, tp}, {nparts, 0, 0}};
+  k_finalize_run<<<1, 1024, 0, r->st>>>(R, r->d_scal, two_mean(r->p.model) ? 1 : 0,
+                                        r->strip_ckpt ? 1 : 0, r->iteration);
+  CKL();
+  r->strip_part = false;
+  return LSE_OK;
+}
+
+int lse_strip_sync(lse_run* r, lse_status* st) {
+  if (!r || !r->strip) return fail(LSE_ERR_ARG, "not a row strip");
+  TRY(collect(r));
+  fill_status(r, st, -1);
+  return LSE_OK;
+}
+
+void* lse_run_stream(lse_run* r) { return r ? (void*)r->st : nullptr; }
+
+void* lse_run_bits_row(lse_run* r, int word_row) {
+  if (!r || word_row < 0 || word_row >= r->g.HR) return nullptr;
+  return r->d_bits[r->cur] + (size_t)word_row * r->g.pitch_w;
+}
+
+int lse_run_geometry(lse_run* r, int* word_rows, int* pitch_words) {
+  if (!r) return fail(LSE_ERR_ARG, "null run");
+  if (word_rows) *word_rows = r->g.HR;
+  if (pitch_words) *pitch_words = r->g.pitch_w;
   return LSE_OK;
 }
 
@@ -843,6 +1008,7 @@ int lse_run_set_state(lse_run* r, const lse_phi0* st) {
 
 int lse_run_advance(lse_run* r, long long n_steps, lse_status* st) {
   if (!r) return fail(LSE_ERR_ARG, "null run");
+  if (r->strip) return fail(LSE_ERR_ARG, "row strips advance through the lse_strip_* phases");
   if (n_steps < 0) return fail(LSE_ERR_ARG, "n_steps must be >= 0");
   if (r->converged || r->iteration >= r->p.max_iters || n_steps == 0) {
     fill_status(r, st, -1);
@@ -1277,7 +1443,7 @@ int lse_rasterize_seeds(const double* poly_xy, const long long* poly_counts, lon
   CK(cudaMemset(dcnt.p, 0, sizeof(unsigned long long)));
   k_rasterize<<<dim3((unsigned)((w + 127) / 128), g.HR), 128>>>(
       (double*)dxy.p, (long long*)doffs.p, (int)n_polys, inside_sign, nullptr,
-      (signed char*)dsig.p, g, (unsigned long long*)dcnt.p);
+      (signed char*)dsig.p, g, (unsigned long long*)dcnt.p, 0);
   CKL();
   unsigned long long cnt = 0;
   CK(cudaMemcpy(&cnt, dcnt.p, sizeof(cnt), cudaMemcpyDeviceToHost));

@@ -64,6 +64,7 @@ struct FastParams {
   Geo gu, gp;                // work geometry: update / partition
   unsigned long long* work;  // dynamic work counter (monotonic across launches)
   unsigned long long work_base;  // value of *work when this launch started
+  int own_lo, own_hi;        // word-rows whose pixels count in the partials (row strips)
 };
 
 constexpr int kChunk = 256;      // partition: columns per warp chunk (32 lanes x 8 columns)
@@ -1175,6 +1176,8 @@ __device__ __forceinline__ void partition_commit(const FastParams& P, int r, int
                                                  LaneDelta& d) {
   const int y0 = r * 32;
   const size_t base = (size_t)r * P.g.pitch_w + x0;
+  // a row strip's halo word-rows are owned (and counted) by the neighbour
+  const bool own = r >= P.own_lo && r < P.own_hi;
   if (MASKONLY) {
     reinterpret_cast<uint4*>(P.mbits + base)[0] = make_uint4(mw[0], mw[1], mw[2], mw[3]);
     reinterpret_cast<uint4*>(P.mbits + base)[1] = make_uint4(mw[4], mw[5], mw[6], mw[7]);
@@ -1189,6 +1192,7 @@ __device__ __forceinline__ void partition_commit(const FastParams& P, int r, int
     for (int c = 0; c < 8; ++c) {
       uint32_t chg = old[c] ^ pw[c];
       any |= chg;
+      if (!own) chg = 0u;
       while (chg) {
         const int b = __ffs(chg) - 1;
         chg &= chg - 1;
@@ -1207,7 +1211,7 @@ __device__ __forceinline__ void partition_commit(const FastParams& P, int r, int
     const uint4 o1 = reinterpret_cast<const uint4*>(P.mbits + base)[1];
     const uint32_t old[8] = {o0.x, o0.y, o0.z, o0.w, o1.x, o1.y, o1.z, o1.w};
 #pragma unroll
-    for (int c = 0; c < 8; ++c) d.mism += __popc(old[c] ^ mw[c]);
+    for (int c = 0; c < 8; ++c) d.mism += own ? __popc(old[c] ^ mw[c]) : 0;
     reinterpret_cast<uint4*>(P.mbits + base)[0] = make_uint4(mw[0], mw[1], mw[2], mw[3]);
     reinterpret_cast<uint4*>(P.mbits + base)[1] = make_uint4(mw[4], mw[5], mw[6], mw[7]);
   }

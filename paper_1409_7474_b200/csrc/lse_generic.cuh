@@ -294,6 +294,14 @@ __global__ void __launch_bounds__(256) k_finalize_stage1(PartRanges R3, TilePart
   reduce_slice(R3, t0, t1, out + blockIdx.x);
 }
 
+// row strips: one CTA reduces this rank's slice results to the single partial
+// the ranks exchange (fixed order)
+__global__ void __launch_bounds__(256) k_reduce_to_one(PartRanges R3, TilePartial* out,
+                                                       const Scalars* sc, int check_stop) {
+  if (check_stop && *(volatile const int*)&sc->stop) return;
+  reduce_slice(R3, 0, R3.n[0] + R3.n[1] + R3.n[2], out);
+}
+
 // per-iteration finalize of the fast path (DELTA partials); no-op once stopped
 __global__ void __launch_bounds__(1024) k_finalize_run(PartRanges R3, Scalars* sc, int region,
                                                        int ckpt, long long iter) {
@@ -375,7 +383,7 @@ __global__ void k_widen(const float* __restrict__ in, double* __restrict__ out, 
 // the inside pixels (DegenerateSeedError check).
 __global__ void k_rasterize(const double* __restrict__ xy, const long long* __restrict__ offs,
                             int n_polys, int inside_sign, uint32_t* bits, signed char* signs,
-                            RunGeom g, unsigned long long* n_inside) {
+                            RunGeom g, unsigned long long* n_inside, long long y_off) {
   const int x = blockIdx.x * blockDim.x + threadIdx.x;
   const int r = blockIdx.y;
   unsigned long long cnt = 0;
@@ -386,7 +394,7 @@ __global__ void k_rasterize(const double* __restrict__ xy, const long long* __re
       for (int k = 0; k < 32; ++k) {
         const int i = r * 32 + k;
         if (i >= g.H) break;
-        const double cy = dadd((double)i, 0.5);
+        const double cy = dadd((double)(y_off + i), 0.5);   // global row (row strips)
         bool inside = false;
         for (int p = 0; p < n_polys && !inside; ++p) {
           const long long a = offs[p], e = offs[p + 1];
@@ -423,7 +431,8 @@ __global__ void __launch_bounds__(256) k_rasterize_rows(const double* __restrict
                                                         const long long* __restrict__ offs,
                                                         int n_polys, int inside_sign,
                                                         uint32_t* bits, RunGeom g,
-                                                        unsigned long long* n_inside) {
+                                                        unsigned long long* n_inside,
+                                                        long long y_off) {
   __shared__ double s_xhit[32][kRastEdges];
   __shared__ unsigned char s_cross[32][kRastEdges];
   __shared__ short s_poly[kRastEdges];
@@ -437,7 +446,7 @@ __global__ void __launch_bounds__(256) k_rasterize_rows(const double* __restrict
     const double x1 = xy[2 * e], y1 = xy[2 * e + 1];
     const long long e2 = a + (qv + 1) % nv;
     const double x2 = xy[2 * e2], y2 = xy[2 * e2 + 1];
-    const double cy = dadd((double)(r * 32 + k), 0.5);
+    const double cy = dadd((double)(y_off + r * 32 + k), 0.5);
     bool crosses = false;
     double xh = 0.0;
     if (y1 != y2) {
@@ -485,9 +494,11 @@ __global__ void __launch_bounds__(256) k_rasterize_rows(const double* __restrict
 // CTA (1024 columns x 32 rows) in a fixed order.
 __global__ void __launch_bounds__(256) k_partition_init_bits(const uint32_t* __restrict__ bits,
                                                              const ExactCtx* c, uint32_t* pbits,
-                                                             TilePartial* part, RunGeom g) {
+                                                             TilePartial* part, RunGeom g,
+                                                             int own_lo, int own_hi) {
   __shared__ TilePartial s_w[8];
   const int r = blockIdx.y;
+  const bool own = r >= own_lo && r < own_hi;   // row strips: halo rows are not counted
   double ah = 0, al = 0, bh = 0, bl = 0;
   long long na = 0, nb = 0;
   for (int j = 0; j < 4; ++j) {
@@ -495,7 +506,7 @@ __global__ void __launch_bounds__(256) k_partition_init_bits(const uint32_t* __r
     if (x >= g.pitch_w) continue;
     const uint32_t w = bits[(size_t)r * g.pitch_w + x];
     pbits[(size_t)r * g.pitch_w + x] = w;
-    if (x >= g.W) continue;
+    if (x >= g.W || !own) continue;
     for (int k = 0; k < 32; ++k) {
       const int i = r * 32 + k;
       if (i >= g.H) break;

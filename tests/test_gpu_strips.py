@@ -1,0 +1,72 @@
+"""Row strips on the device: G strips of one grid, driven on one
+GPU exactly as G ranks would drive them (update -> halo exchange -> partition
+-> partial allgather -> finalize), must reproduce the single-run trajectory
+bit-for-bit."""
+import warnings
+
+import numpy as np
+import pytest
+
+import paper_1409_7474_b200 as L
+from paper_1409_7474_b200 import scenes
+from paper_1409_7474_b200.strips import run_local_strips
+from conftest import square
+
+pytestmark = pytest.mark.gpu
+
+
+def params(model, **kw):
+    with warnings.catch_warnings():
+        warnings.simplefilter("ignore")
+        return L.default_params(L.ModelKind.from_name(model), **kw)
+
+
+def scene(h=150, w=70, seed=3):
+    rng = np.random.default_rng(seed)
+    img = np.full((h, w), 0.25)
+    img[30:110, 20:55] = 0.7
+    img = np.clip(img + 0.08 * rng.standard_normal((h, w)), 0, 1)
+    return img, L.SeedSpec(polygons=(square(8, 12, 60, 130),), inside_sign=-1)
+
+
+def single(img, seeds, prm, iters):
+    r = L.EvolutionRun(img, seeds, prm)
+    r.advance(iters)
+    return r
+
+
+def check(img, seeds, prm, iters, world):
+    ref = single(img, seeds, prm, iters)
+    _, strips, st = run_local_strips(img, seeds, prm, world, iters)
+    phi = np.concatenate([s.own_phi() for s in strips])
+    assert np.array_equal(phi, ref.state.phi), np.abs(phi - ref.state.phi).max()
+    mask = np.concatenate([s.own_mask(seeds.inside_sign) for s in strips]).astype(bool)
+    assert np.array_equal(mask, ref.mask())
+    for s in st:
+        assert s.iteration == ref.state.iteration and bool(s.converged) == ref.converged
+
+
+@pytest.mark.parametrize("model,world", [("region", 2), ("region", 4), ("edge", 3),
+                                         ("zhang", 2)])
+def test_small_scene_strips(model, world):
+    img, seeds = scene()
+    check(img, seeds, params(model, max_iters=30), 30, world)
+
+
+def test_strips_converge_together():
+    img, seeds = scene()
+    check(img, seeds, params("region", max_iters=300, conv_check_every=3, conv_window=2), 300, 3)
+
+
+@pytest.mark.parametrize("world", [2, 3, 5])
+def test_c5_crop_strips(world):
+    sc = scenes.config5_crop(1024, 60)
+    seeds = L.SeedSpec(polygons=sc.polygons, inside_sign=sc.inside_sign)
+    check(sc.image, seeds, params("region", **sc.params), 60, world)
+
+
+def test_strip_degenerate_seed_is_global():
+    img, _ = scene()
+    seeds = L.SeedSpec(polygons=(square(0, 0, 70, 150),), inside_sign=1)
+    with pytest.raises(L.DegenerateSeedError):
+        run_local_strips(img, seeds, params("region"), 2, 1)

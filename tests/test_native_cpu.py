@@ -17,7 +17,7 @@ import lse_oracle as O
 
 def header_symbols():
     src = open(os.path.join(REPO, "include", "lse_b200.h")).read()
-    return sorted(set(re.findall(r"^\s*(?:int|void|long long|const char\*)\s+(lse_\w+)\(", src, re.M)))
+    return sorted(set(re.findall(r"^\s*(?:int|void\*?|long long|const char\*)\s+(lse_\w+)\(", src, re.M)))
 
 
 def test_library_exports_every_header_symbol():
@@ -26,7 +26,7 @@ def test_library_exports_every_header_symbol():
     for s in syms:
         assert hasattr(N.lib, s), s
     assert set(syms) == set(N.EXPORTED)
-    assert N.lib.lse_abi_version() == 2
+    assert N.lib.lse_abi_version() == 3
 
 
 def test_struct_layouts_match_header(tmp_path):
