@@ -55,6 +55,11 @@ def parse():
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--cpu-seconds", type=float, default=12.0)
+    ap.add_argument("--mode", choices=["strips", "replicas"], default="strips",
+                    help="N > 1: row strips of one scene (strong scaling) or N replicas")
+    ap.add_argument("--strips-n1", action="store_true",
+                    help="run the row-strip path (NCCL communicator) even at N = 1 "
+                         "(launch under torch.distributed.run)")
     ap.add_argument("--skip-steps", type=int, default=None,
                     help="steps of the uniform-window-skip measurement (default: --steps)")
     return ap.parse_args()
@@ -203,55 +208,83 @@ def main():
     import torch
     torch.cuda.set_device(local)
     dist = None
-    if ws > 1:
+    if ws > 1 or args.strips_n1:
         import torch.distributed as dist
         dist.init_process_group("nccl", device_id=torch.device("cuda", local))
 
     from paper_1409_7474_b200 import _native as N
     from paper_1409_7474_b200 import scenes
     from paper_1409_7474_b200.engine import _native_params
-    from paper_1409_7474_b200 import default_params, ModelKind
+    from paper_1409_7474_b200 import default_params, ModelKind, SeedSpec
+    from paper_1409_7474_b200.strips import DeviceStrip, DistComm, StripDriver, plan_strips
 
     n_rects = max(1, int(round(20000 * (args.size / 32768.0) ** 2)))
+    strips = (ws > 1 and args.mode == "strips") or args.strips_n1
+    win = plan_strips(args.size, args.size, ws)[rank] if strips else None
     t_gen = time.perf_counter()
-    sc = scenes.config5(size=args.size, n_rects=n_rects, iters=args.iters, seed_offset=rank)
+    sc = scenes.config5(size=args.size, n_rects=n_rects, iters=args.iters,
+                        seed_offset=0 if strips else rank,
+                        rows=(win.y_lo, win.y_hi) if strips else None)
     t_gen = time.perf_counter() - t_gen
-    H, W = sc.image.shape
-    npx = H * W
+    Hl, W = sc.image.shape                     # local rows (a strip: owned + halo rows)
+    npx_local = Hl * W
+    npx = args.size * args.size                # pixels of one job (the whole scene)
     prm = default_params(ModelKind.REGION, **sc.params)
     p, keep_w = _native_params(prm)
 
     # pinned host copies for the end-to-end leg
-    img_pin = torch.empty((H, W), dtype=torch.float32, pin_memory=True)
+    img_pin = torch.empty((Hl, W), dtype=torch.float32, pin_memory=True)
     img_pin.numpy()[...] = sc.image
-    nbytes_mask = (npx + 7) // 8
+    nbytes_mask = (npx_local + 7) // 8
     mask_pin = torch.empty(nbytes_mask, dtype=torch.uint8, pin_memory=True)
-    del sc.image
 
     polys = np.ascontiguousarray(np.concatenate(sc.polygons), dtype=np.float64)
     counts = np.ascontiguousarray([len(q) for q in sc.polygons], dtype=np.int64)
-    init = N.LsePhi0()
-    init.kind = N.LSE_PHI0_POLYGONS
-    init.poly_xy = N.dptr(polys)
-    init.poly_counts = counts.ctypes.data_as(N._llp)
-    init.n_polys = len(counts)
-    init.inside_sign = sc.inside_sign
-
-    h = C.c_void_p()
-    N.check(N.lib.lse_run_create(C.byref(h), C.byref(p), H, W,
-                                 C.c_void_p(img_pin.data_ptr()), 1, C.byref(init)))
     st = N.LseStatus()
+    if strips:
+        # one row strip of the scene per rank; halo rows + partials over NCCL
+        strip = DeviceStrip(sc.image, win, SeedSpec(polygons=sc.polygons,
+                                                    inside_sign=sc.inside_sign), prm)
+        del sc.image
+        drv = StripDriver([strip], DistComm(strip))
+        drv.share_image_range()
+        h = strip.h
 
-    def job():
-        N.check(N.lib.lse_run_set_state(h, C.byref(init)))
-        N.check(N.lib.lse_run_advance(h, args.iters, C.byref(st)))
-        assert st.iteration == args.iters, st.iteration
+        def job():
+            strip.reset()
+            drv.initialize()
+            s0 = drv.advance(args.iters)[0]
+            assert s0.iteration == args.iters, s0.iteration
+            st.exact_fallbacks = s0.exact_fallbacks
 
-    def job_e2e():
-        N.check(N.lib.lse_run_load_image(h, C.c_void_p(img_pin.data_ptr()), 1))
-        job()
-        N.check(N.lib.lse_run_read_mask(h, C.cast(C.c_void_p(mask_pin.data_ptr()),
-                                                  C.POINTER(C.c_ubyte)), sc.inside_sign, 1))
+        def job_e2e():
+            strip.load_image(img_pin.data_ptr(), True)
+            drv.share_image_range()
+            job()
+            N.check(N.lib.lse_run_read_mask(h, C.cast(C.c_void_p(mask_pin.data_ptr()),
+                                                      C.POINTER(C.c_ubyte)), sc.inside_sign, 1))
+    else:
+        del sc.image
+        init = N.LsePhi0()
+        init.kind = N.LSE_PHI0_POLYGONS
+        init.poly_xy = N.dptr(polys)
+        init.poly_counts = counts.ctypes.data_as(N._llp)
+        init.n_polys = len(counts)
+        init.inside_sign = sc.inside_sign
+        h = C.c_void_p()
+        N.check(N.lib.lse_run_create(C.byref(h), C.byref(p), Hl, W,
+                                     C.c_void_p(img_pin.data_ptr()), 1, C.byref(init)))
+
+        def job():
+            N.check(N.lib.lse_run_set_state(h, C.byref(init)))
+            N.check(N.lib.lse_run_advance(h, args.iters, C.byref(st)))
+            assert st.iteration == args.iters, st.iteration
+
+        def job_e2e():
+            N.check(N.lib.lse_run_load_image(h, C.c_void_p(img_pin.data_ptr()), 1))
+            job()
+            N.check(N.lib.lse_run_read_mask(h, C.cast(C.c_void_p(mask_pin.data_ptr()),
+                                                      C.POINTER(C.c_ubyte)), sc.inside_sign, 1))
 
     def barrier():
         if dist is not None:
@@ -264,6 +297,10 @@ def main():
         t = torch.tensor([x], dtype=torch.float64, device="cuda")
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
         return float(t.item())
+
+    # whole-job pixel-iterations per step (all ranks): strips share one scene,
+    # replicas each run their own
+    job_px_its = npx * args.iters * (1 if strips else ws)
 
     # ---- dense pass (every pixel recomputed every iteration): the headline
     N.check(N.lib.lse_run_set_option(h, b"skip_uniform", 0))
@@ -290,7 +327,7 @@ def main():
                                        C.byref(n_part)))
     N.check(N.lib.lse_run_set_profiling(h, 0))
     fallbacks = st.exact_fallbacks
-    px_its = npx * args.iters * args.steps * ws
+    px_its = job_px_its * args.steps
     value = px_its / (t_ms / 1e3) / 1e9
 
     # ---- same jobs with the exact uniform-window skip (product default)
@@ -311,7 +348,7 @@ def main():
         N.check(N.lib.lse_run_kernel_times(h, C.byref(su), C.byref(nsu), C.byref(sp),
                                            C.byref(nsp)))
         N.check(N.lib.lse_run_set_profiling(h, 0))
-        skip = {"value": npx * args.iters * skip_steps * ws / (s_ms / 1e3) / 1e9,
+        skip = {"value": job_px_its * skip_steps / (s_ms / 1e3) / 1e9,
                 "unit": "Gpix-it/s", "ms_per_step": s_ms / skip_steps,
                 "update_ms": su.value / max(1, nsu.value),
                 "partition_ms": sp.value / max(1, nsp.value),
@@ -333,25 +370,28 @@ def main():
         barrier()
         e_ms = max_over_ranks(ms.value)
         e2e = {"value": px_its / (e_ms / 1e3) / 1e9, "unit": "Gpix-it/s",
-               "h2d_bytes_per_step": npx * 4 + polys.nbytes + counts.nbytes,
+               "h2d_bytes_per_step": npx_local * 4 + polys.nbytes + counts.nbytes,
                "d2h_bytes_per_step": nbytes_mask, "ms_per_step": e_ms / args.steps}
 
-    N.lib.lse_run_destroy(h)
+    if strips:
+        del drv, strip
+    else:
+        N.lib.lse_run_destroy(h)
 
     # ---- roofline of one iteration (k_update + k_partition)
     peak, peak_kind = measured_peaks()
     t_upd = upd_ms.value / max(1, n_upd.value)
     t_part = part_ms.value / max(1, n_part.value)
     t_iter = t_upd + t_part
-    canon = 12.0 * npx
-    actual = (4.0 + 2.0 / 8.0 + 3.0 / 8.0) * npx     # I + b in/out (update) + b, P in/out (partition)
+    canon = 12.0 * npx_local          # this rank's pixels per launch pair
+    actual = (4.0 + 2.0 / 8.0 + 3.0 / 8.0) * npx_local  # I + b in/out (update) + b, P in/out (partition)
     traffic = None
     tp = os.path.join(REPO, "profiles", "traffic_latest.json")
     if os.path.exists(tp):
         try:
             with open(tp) as f:
                 td = json.load(f)
-            if int(td.get("size", 0)) == args.size:
+            if int(td.get("size", 0)) == args.size and ws == 1:
                 traffic = float(td["bytes_per_iteration"])
         except Exception:
             traffic = None
@@ -360,7 +400,7 @@ def main():
             "peak": peak, "unit": "GB/s",
             "frac": (canon / (t_iter / 1e3) / 1e9) / peak if t_iter > 0 else None,
             "traffic": traffic, "peak_source": peak_kind,
-            "algorithmic_bytes_per_px_it": 12.0, "actual_bytes_per_px_it": actual / npx,
+            "algorithmic_bytes_per_px_it": 12.0, "actual_bytes_per_px_it": actual / npx_local,
             "achieved_actual_gbs": actual / (t_iter / 1e3) / 1e9 if t_iter > 0 else None,
             "frac_actual": (actual / (t_iter / 1e3) / 1e9) / peak if t_iter > 0 else None,
             "update_ms": t_upd, "partition_ms": t_part,
@@ -378,11 +418,14 @@ def main():
             "unit": "Gpix-it/s", "n_gpus": ws, "steps": args.steps, "warmup": args.warmup,
             "ms_per_step": t_ms / args.steps, "higher_is_better": True,
             "mode": "dense (skip_uniform=0: every pixel recomputed every iteration)",
-            "scaling": "weak", "vs_baseline": None, "dtype": "f32+f64-guard (bit state)",
+            "scaling": "strong" if strips else "weak", "vs_baseline": None,
+            "dtype": "f32+f64-guard (bit state)",
             "data": "synthetic (seeded, BASELINE C5 statistics)",
-            "config": {"workload": f"C5: {H}x{W} region LSE, 20000-rect density, sigma 1.5 "
+            "config": {"workload": f"C5: {args.size}x{args.size} region LSE, 20000-rect density, sigma 1.5 "
                                    f"(9x9), dt 15, {args.iters} fixed iterations per step",
-                       "parallelism": f"replicas x{ws}" if ws > 1 else "single GPU",
+                       "parallelism": (f"row strips x{ws} (NCCL halo + partial allgather)"
+                                       if strips else f"replicas x{ws}" if ws > 1
+                                       else "single GPU"),
                        "l2": "inputs (4.3 GB image) larger than L2"},
             "roofline": roof, "cpu_baseline": cpu, "e2e": e2e, "gpu_launches": int(launches),
             "uniform_skip": skip,

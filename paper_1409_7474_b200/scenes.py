@@ -115,31 +115,45 @@ def config2(size=1024):
                  "edge", 500)
 
 
-def config5(size=32768, n_rects=20000, iters=500, seed_offset=0):
+def config5(size=32768, n_rects=20000, iters=500, seed_offset=0, rows=None):
     """C5: large panchromatic scene, 20000 rects 8-64 px, region, sigma 1.5.
 
     ``size``/``n_rects`` may be scaled down together (same object density)
-    for parity crops: n_rects_crop = n_rects * (size/32768)^2.
+    for parity crops: n_rects_crop = n_rects * (size/32768)^2.  ``rows =
+    (y0, y1)`` generates only those image rows (a row strip of a multi-GPU
+    run); the pixels are identical to the same rows of the full image: the
+    background noise comes in fixed row blocks with their own seeded
+    streams, the rectangles from one stream drawn completely by every caller.
     """
-    rng = np.random.default_rng(5000 + seed_offset)
-    img = np.empty((size, size), dtype=np.float32)
-    rows = max(1, (1 << 24) // size)
-    for y in range(0, size, rows):
-        z = rng.standard_normal((min(rows, size - y), size), dtype=np.float32)
-        img[y:y + rows] = np.float32(0.3) + np.float32(0.05) * z
+    y0, y1 = (0, size) if rows is None else (int(rows[0]), int(rows[1]))
+    base = 5000 + seed_offset
+    img = np.empty((y1 - y0, size), dtype=np.float32)
+    block = max(1, (1 << 24) // size)
+    for k, y in enumerate(range(0, size, block)):
+        ye = min(size, y + block)
+        if ye <= y0 or y >= y1:
+            continue
+        z = np.random.default_rng([base, 1, k]).standard_normal((ye - y, size),
+                                                                 dtype=np.float32)
+        a, b = max(y, y0), min(ye, y1)
+        img[a - y0:b - y0] = np.float32(0.3) + np.float32(0.05) * z[a - y:b - y]
+    rng = np.random.default_rng([base, 2])
     for _ in range(n_rects):
         sw = int(rng.integers(8, 65))
         sh = int(rng.integers(8, 65))
         x = int(rng.integers(0, max(1, size - sw)))
         y = int(rng.integers(0, max(1, size - sh)))
-        img[y:y + sh, x:x + sw] = (np.float32(0.7) + np.float32(0.05) *
-                                   rng.standard_normal((sh, sw), dtype=np.float32))
+        vals = np.float32(0.7) + np.float32(0.05) * rng.standard_normal((sh, sw),
+                                                                          dtype=np.float32)
+        a, b = max(y, y0), min(y + sh, y1)
+        if a < b:
+            img[a - y0:b - y0, x:x + sw] = vals[a - y:b - y]
     np.clip(img, 0.0, 1.0, out=img)
     m = size // 16
     return Scene("C5", img, (box_polygon(m, m, size - m, size - m),), -1,
                  dict(dt=15.0, sigma2=1.5, ts_reg=9, max_iters=iters,
                       conv_check_every=iters + 1), "region", iters,
-                 extra=dict(n_rects=n_rects))
+                 extra=dict(n_rects=n_rects, rows=(y0, y1)))
 
 
 def config5_crop(size=4096, iters=500):

@@ -155,10 +155,11 @@ class DistComm:
     def allreduce_range(self, ranges):
         import torch
         (mn, mx, am), = ranges
-        t = torch.tensor([-mn, mx, am], dtype=torch.float64, device=self.strips[0].comm_device)
-        with self._stream():
+        with self._stream():       # H2D, the reduction and D2H all on the strip's stream
+            t = torch.tensor([-mn, mx, am], dtype=torch.float64,
+                             device=self.strips[0].comm_device)
             self.dist.all_reduce(t, op=self.dist.ReduceOp.MAX, group=self.group)
-        t = t.cpu()
+            t = t.cpu()
         return [(-float(t[0]), float(t[1]), float(t[2]))]
 
     def exchange_halos(self):
@@ -212,11 +213,22 @@ class StripDriver:
 
     def setup(self):
         """Global image range, initial partition sums, seed-count check."""
+        self.share_image_range()
+        self.initialize()
+
+    def share_image_range(self):
+        """min / max / max|I| of the whole image on every rank (once per image)."""
         ranges = self.comm.allreduce_range([s.image_range() for s in self.strips])
         for s, g in zip(self.strips, ranges):
             s.set_image_range(g)
+
+    def initialize(self):
+        """Partition sums of the initial state, seed-count check (engine.py:202-216)."""
+        self.iteration = 0
         parts = [s.prepare() for s in self.strips]
         gathered = self.comm.allgather(parts)
+        for s in self.strips:
+            s.synchronize()
         raw = gathered[0].cpu().numpy().view(np.uint8).reshape(-1, PARTIAL_BYTES)
         n_pos = sum(partial_counts(q)[0] for q in raw)     # pixels with b = +1
         w = self.strips[0].win
@@ -280,12 +292,13 @@ class DeviceStrip:
         init.inside_sign = int(seeds.inside_sign)
         init.row_offset = win.y_lo
         self.inside_positive = int(seeds.inside_sign) > 0
+        self._init, self._init_keep = init, (xy, counts)
         h = C.c_void_p()
         N.check(N.lib.lse_strip_create(C.byref(h), C.byref(p), win.rows, win.width,
                                        img.ctypes.data_as(C.c_void_p),
                                        1 if img.dtype == np.float32 else 0, C.byref(init),
                                        win.own_lo, win.own_hi, win.height * win.width))
-        del wkeep, xy, counts
+        del wkeep
         self.h = h
         self._fin = weakref.finalize(self, N.lib.lse_run_destroy, h)
         hr, pw = C.c_int(), C.c_int()
@@ -295,6 +308,16 @@ class DeviceStrip:
         self.comm_device = torch.device("cuda", dev)
         self.stream = torch.cuda.ExternalStream(N.lib.lse_run_stream(h), device=self.comm_device)
         self._part = torch.zeros(PARTIAL_BYTES, dtype=torch.uint8, device=self.comm_device)
+
+    def reset(self):
+        """Back to the seeded initial state (iteration 0); follow with
+        StripDriver.initialize()."""
+        self.N.check(self.N.lib.lse_run_set_state(self.h, C.byref(self._init)))
+
+    def load_image(self, image_rows_ptr, is_f32=True):
+        """Replace the strip's image rows from a host pointer (same shape)."""
+        self.N.check(self.N.lib.lse_run_load_image(self.h, C.c_void_p(image_rows_ptr),
+                                                   1 if is_f32 else 0))
 
     # -- phases ------------------------------------------------------------
     def stream_context(self):

@@ -70,3 +70,33 @@ def test_strip_degenerate_seed_is_global():
     seeds = L.SeedSpec(polygons=(square(0, 0, 70, 150),), inside_sign=1)
     with pytest.raises(L.DegenerateSeedError):
         run_local_strips(img, seeds, params("region"), 2, 1)
+
+
+def test_nccl_communicator_world1():
+    """The NCCL communicator path (allreduce of the image range, allgather of
+    the partials on the strip's stream) in a one-rank process group."""
+    import socket
+    import torch
+    import torch.distributed as dist
+    from paper_1409_7474_b200.strips import DeviceStrip, DistComm, StripDriver, plan_strips
+    with socket.socket() as sk:
+        sk.bind(("127.0.0.1", 0))
+        port = sk.getsockname()[1]
+    dist.init_process_group("nccl", init_method=f"tcp://127.0.0.1:{port}", rank=0,
+                            world_size=1, device_id=torch.device("cuda", 0))
+    try:
+        img, seeds = scene()
+        prm = params("region", max_iters=40)
+        win = plan_strips(img.shape[0], img.shape[1], 1)[0]
+        strip = DeviceStrip(img, win, seeds, prm)
+        drv = StripDriver([strip], DistComm(strip))
+        drv.setup()
+        st = drv.advance(20)[0]
+        strip.reset()                       # the bench's job: reset + initialize + advance
+        drv.initialize()
+        st = drv.advance(40)[0]
+        ref = single(img, seeds, prm, 40)
+        assert st.iteration == ref.state.iteration
+        assert np.array_equal(strip.own_phi(), ref.state.phi)
+    finally:
+        dist.destroy_process_group()
