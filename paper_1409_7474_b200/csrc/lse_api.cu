@@ -785,6 +785,11 @@ int create_impl(lse_run** out, const lse_params* p, long long height, long long 
     const int R = r->R, H = r->H, W = r->W;
     r->gu = make_geo(H, W, R, 1 + R, 1 + R, R + 1);   // update reaches R+1 rows/columns
     r->gp = make_geo(H, W, R, R, R, R);               // partition reaches R
+    if (si && (!geo_restrict_rows(r->gu, si->own_lo, si->own_hi) ||
+               !geo_restrict_rows(r->gp, si->own_lo, si->own_hi))) {
+      delete r;
+      return fail(LSE_ERR_UNSUPPORTED, "strip too thin for its stencil");
+    }
     r->gu_all = geo_all_border(r->gu, H);
     r->ni_upd = (long long)(r->gu.r_hi - r->gu.r_lo) * r->gu.nci + (r->gu.nB1 + 31) / 32;
     r->nb_upd[0] = r->gu.nA + (r->gu.nB2 + 31) / 32;

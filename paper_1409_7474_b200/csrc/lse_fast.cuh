@@ -622,109 +622,6 @@ __device__ __forceinline__ void update_block_int2(const FastParams& P, uint32_t 
     reinterpret_cast<uint4*>(dst)[q] = make_uint4(ow[4 * q], ow[4 * q + 1], ow[4 * q + 2], ow[4 * q + 3]);
 }
 
-template <int R, int MODEL, int CPL, int SRC>
-__device__ __forceinline__ void update_block_int(const FastParams& P, uint32_t lut_base,
-                                                 float* ring, int r, int x0, float A, float B,
-                                                 float eps_u,
-                                                 const uint32_t (&prev)[CPL + 2 * (R + 1)],
-                                                 const uint32_t (&cur)[CPL + 2 * (R + 1)]) {
-  constexpr int NT = CPL + 2 * (R + 1);
-  constexpr int NP = CPL + 2;
-  const int y0 = r * 32;
-  const int lane = threadIdx.x & 31;
-  uint32_t win4[NT];
-#pragma unroll
-  for (int j = 0; j < NT; ++j) win4[j] = __funnelshift_r(prev[j], cur[j], 31 - R) << 2;
-  // ring slot q holds this lane's CPL floats of one row at byte
-  // ring_s + q * kSlot (kSlot = one row of the warp = 32 * CPL floats)
-  constexpr uint32_t kSlot = 32 * CPL * 4;
-  const uint32_t ring_s = (uint32_t)__cvta_generic_to_shared(ring) + lane * CPL * 4;
-  const size_t dpitch = P.g.data_pitch;
-  const float* gsrc = P.data32 + (size_t)y0 * dpitch + x0;
-#pragma unroll
-  for (int q = 0; q < kRing - 1; ++q) {        // rows 0 .. kRing-2 in flight
-#pragma unroll
-    for (int v = 0; v < CPL / 4; ++v) cp_async16(ring_s + q * kSlot + v * 16, gsrc + 4 * v);
-    cp_async_commit();
-    gsrc += dpitch;
-  }
-  float pm[NP], p0[NP], pn[NP];
-  uint32_t ow[CPL];
-  uint32_t fbrows = 0u;
-#pragma unroll
-  for (int c = 0; c < CPL; ++c) ow[c] = 0u;
-  (void)eps_u;
-  phi_row_int<R, NT, NP, SRC>(P, win4, 0, lut_base, pm);
-  phi_row_int<R, NT, NP, SRC>(P, win4, 1, lut_base, p0);
-  const uint32_t* wrow = P.bits_in + (size_t)r * P.g.pitch_w + (x0 - (R + 1));
-#pragma unroll 4
-  for (int k = 0; k < 32; ++k) {
-    const int kk = k + 1;
-    {   // keep kRing-1 rows in flight (empty groups past the tile keep the count)
-      if (k + kRing - 1 < 32) {
-        const uint32_t dsts = ring_s + ((k + kRing - 1) & (kRing - 1)) * kSlot;
-#pragma unroll
-        for (int v = 0; v < CPL / 4; ++v) cp_async16(dsts + v * 16, gsrc + 4 * v);
-        gsrc += dpitch;
-      }
-      cp_async_commit();
-    }
-    if (kk == 16) {
-#pragma unroll
-      for (int j = 0; j < NT; ++j)
-        win4[j] = __funnelshift_r(__ldg(wrow + j), __ldg(wrow + P.g.pitch_w + j), 16 - R) << 2;
-    }
-    phi_row_int<R, NT, NP, SRC>(P, win4, kk < 16 ? kk + 1 : kk - 16, lut_base, pn);
-    cp_async_wait<kRing - 1>();                 // row k has landed (this lane's copy)
-    float d[CPL];
-    {
-      const uint32_t srcs = ring_s + (k & (kRing - 1)) * kSlot;
-#pragma unroll
-      for (int v = 0; v < CPL / 4; ++v) {
-        float4 q4;
-        asm volatile("ld.shared.v4.f32 {%0, %1, %2, %3}, [%4];"
-                     : "=f"(q4.x), "=f"(q4.y), "=f"(q4.z), "=f"(q4.w) : "r"(srcs + v * 16));
-        d[4 * v] = q4.x; d[4 * v + 1] = q4.y; d[4 * v + 2] = q4.z; d[4 * v + 3] = q4.w;
-      }
-    }
-    float umin = 3.0e38f;
-#pragma unroll
-    for (int c = 0; c < CPL; ++c) {
-      const float dx = p0[c + 2] - p0[c];
-      const float dy = pn[c + 1] - pm[c + 1];
-      const float h = sqrt_approx(fmaf(dx, dx, dy * dy));          // 2|grad phi|
-      // A, B (region) and the g plane (edge) carry the factor dt/2
-      const float vf = (MODEL == REGION) ? fmaf(A, d[c], B) : d[c];
-      const float u = fmaf(vf, h, p0[c + 1]);
-      // sign bits shift in from the bottom; bit order is reversed once at the end
-      ow[c] = __funnelshift_l(__float_as_uint(u), ow[c], 1);
-      umin = fminf(umin, fabsf(u));
-    }
-    if (umin <= eps_u) fbrows |= 1u << k;
-#pragma unroll
-    for (int c = 0; c < NP; ++c) { pm[c] = p0[c]; p0[c] = pn[c]; }
-  }
-  cp_async_wait<0>();
-#pragma unroll
-  for (int c = 0; c < CPL; ++c) ow[c] = ~__brev(ow[c]);   // bit k = (u_k >= +0) = (u_k > 0) off ties
-  while (fbrows) {
-    const int k = __ffs(fbrows) - 1;
-    fbrows &= fbrows - 1;
-    const uint32_t bitk = 1u << k;
-#pragma unroll 1
-    for (int c = 0; c < CPL; ++c) {
-      const bool pos = exact_u_fast<R, SRC>(P.ctx, P.bits_in, y0 + k, x0 + c) > 0.0;
-#pragma unroll
-      for (int q = 0; q < CPL; ++q)
-        if (q == c) ow[q] = pos ? (ow[q] | bitk) : (ow[q] & ~bitk);
-    }
-  }
-  uint32_t* dst = P.bits_out + (size_t)r * P.g.pitch_w + x0;
-#pragma unroll
-  for (int q = 0; q < CPL / 4; ++q)
-    reinterpret_cast<uint4*>(dst)[q] = make_uint4(ow[4 * q], ow[4 * q + 1], ow[4 * q + 2], ow[4 * q + 3]);
-}
-
 // The 2 KB t-LUT must sit at a 2 KB-aligned shared address for the OR-based
 // addressing of phi_row_int; static __shared__ alignment is not guaranteed
 // relative to the CTA's shared window, so it is carved out of a 4 KB buffer.

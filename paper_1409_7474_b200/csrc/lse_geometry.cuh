@@ -17,11 +17,14 @@ namespace lse {
 //  groups -- the 8-column groups of the right strip [x1, W) of interior rows
 //  whose stencil still lies inside the image, packed 32 per warp (each lane
 //  its own row); every lane of (1)/(2) runs the interior code.
-//  border work: (A) word-rows outside [r_lo, r_hi), whole width, 256-column
-//  warp units; (B2) per interior row the left strip [0, xoff) and the right
-//  tail beyond the B1 groups, 8-column lane groups packed 32 per warp.
+//  border work: (A) word-rows outside [r_lo, r_hi) -- the blocks [ta, tb) and
+//  [ba, bb) -- whole width, 256-column warp units; (B2) per interior row the
+//  left strip [0, xoff) and the right tail beyond the B1 groups, 8-column lane
+//  groups packed 32 per warp.  A row strip of a multi-GPU run drops the
+//  border rows it does not own (its halo rows, recomputed by their owner).
 struct Geo {
   int r_lo, r_hi, nci, xoff, x1;
+  int ta, tb, ba, bb;  // part-A word-rows: [ta, tb) above and [ba, bb) below the interior
   int nchunk_full;   // ceil(W / 256): chunks of a part-A row
   int nb1_row;       // B1 lane groups per interior row
   int nb2_left;      // B2 left-strip groups per interior row (xoff / 8)
@@ -54,10 +57,28 @@ LSE_HD Geo make_geo(int H, int W, int R, int top, int bot, int right) {
   g.nb1_row = (int)nb1;
   g.nb2_left = g.nci > 0 ? g.xoff / 8 : 0;
   g.nb2_row = g.nb2_left + (ngr - g.nb1_row);
-  g.nA = (g.r_lo + HR - g.r_hi) * g.nchunk_full;
+  g.ta = 0;
+  g.tb = g.r_lo;
+  g.ba = g.r_hi;
+  g.bb = HR;
+  g.nA = (g.tb - g.ta + g.bb - g.ba) * g.nchunk_full;
   g.nB1 = (g.r_hi - g.r_lo) * g.nb1_row;
   g.nB2 = (g.r_hi - g.r_lo) * g.nb2_row;
   return g;
+}
+
+// Row strips: only the word-rows [own_lo, own_hi) are computed.  Returns false
+// if an interior row falls outside them (the strip is then unsupported).
+LSE_HD bool geo_restrict_rows(Geo& g, int own_lo, int own_hi) {
+  if (g.r_lo < g.r_hi && (g.r_lo < own_lo || g.r_hi > own_hi)) return false;
+  g.ta = g.ta > own_lo ? g.ta : own_lo;
+  g.tb = g.tb < own_hi ? g.tb : own_hi;
+  if (g.tb < g.ta) g.tb = g.ta;
+  g.ba = g.ba > own_lo ? g.ba : own_lo;
+  g.bb = g.bb < own_hi ? g.bb : own_hi;
+  if (g.bb < g.ba) g.bb = g.ba;
+  g.nA = (g.tb - g.ta + g.bb - g.ba) * g.nchunk_full;
+  return true;
 }
 
 // the same geometry with no interior (every unit runs the border code)
@@ -66,6 +87,9 @@ LSE_HD Geo geo_all_border(const Geo& in, int H) {
   g.r_lo = g.r_hi = 0;
   g.nci = 0;
   g.nb1_row = g.nb2_row = g.nb2_left = 0;
+  g.ta = 0;
+  g.tb = (H + 31) / 32;
+  g.ba = g.bb = g.tb;
   g.nA = ((H + 31) / 32) * g.nchunk_full;
   g.nB1 = g.nB2 = 0;
   return g;
@@ -90,7 +114,8 @@ LSE_HD bool border_lane(const Geo& G, int unit, int lane, int W, int& r,
   if (unit < G.nA) {
     const int rowidx = unit / G.nchunk_full;
     const int c = unit - rowidx * G.nchunk_full;
-    r = rowidx < G.r_lo ? rowidx : G.r_hi + (rowidx - G.r_lo);
+    const int ntop = G.tb - G.ta;
+    r = rowidx < ntop ? G.ta + rowidx : G.ba + (rowidx - ntop);
     x0 = c * 256 + 8 * lane;
     return x0 < W;
   }

@@ -7,7 +7,8 @@
 #include "../paper_1409_7474_b200/csrc/lse_geometry.cuh"
 using namespace lse;
 
-static int check(int H, int W, int R, int top, int bot, int left, int right, const Geo& G) {
+static int check(int H, int W, int R, int top, int bot, int left, int right, const Geo& G,
+                 int own_lo = 0, int own_hi = 1 << 30) {
   const int HR = (H + 31) / 32, NG = (W + 7) / 8;
   std::vector<int> cover((size_t)HR * NG, 0);
   int bad = 0;
@@ -37,8 +38,10 @@ static int check(int H, int W, int R, int top, int bot, int left, int right, con
       if (r < 0 || r >= HR || x0 < 0 || x0 >= W || x0 % 8) { ++bad; continue; }
       cover[(size_t)r * NG + x0 / 8]++;
     }
-  for (size_t k = 0; k < cover.size(); ++k)
-    if (cover[k] != 1) ++bad;
+  for (size_t k = 0; k < cover.size(); ++k) {
+    const int r = (int)(k / NG);
+    if (cover[k] != ((r >= own_lo && r < own_hi) ? 1 : 0)) ++bad;
+  }
   if (bad) printf("FAIL H=%d W=%d R=%d reach=(%d,%d,%d,%d): %d problems\n", H, W, R, top, bot,
                   left, right, bad);
   return bad;
@@ -56,6 +59,19 @@ int main() {
         Geo a = geo_all_border(make_geo(H, W, R, 1 + R, 1 + R, R + 1), H);
         fails += check(H, W, R, 1 << 20, 1 << 20, 1 << 20, 1 << 20, a) != 0;
         cases += 3;
+        // row strips: halo word-rows (first / last) are left to their owners
+        const int HR = (H + 31) / 32;
+        for (int lo = 0; lo <= 1; ++lo)
+          for (int hi = HR - 1; hi <= HR; ++hi) {
+            if (hi <= lo) continue;
+            Geo s = make_geo(H, W, R, 1 + R, 1 + R, R + 1);
+            if (!geo_restrict_rows(s, lo, hi)) continue;
+            fails += check(H, W, R, 1 + R, 1 + R, R + 1, R + 1, s, lo, hi) != 0;
+            Geo q = make_geo(H, W, R, R, R, R);
+            if (!geo_restrict_rows(q, lo, hi)) continue;
+            fails += check(H, W, R, R, R, R, R, q, lo, hi) != 0;
+            cases += 2;
+          }
       }
   printf("%d cases, %d failing\n", cases, fails);
   return fails != 0;
