@@ -13,10 +13,17 @@ $(LIB): $(SRC) $(HDR)
 	@mkdir -p $(dir $@)
 	$(NVCC) $(FLAGS) -shared -o $@ $(SRC) 2> paper_1409_7474_b200/_lib/ptxas.log || (cat paper_1409_7474_b200/_lib/ptxas.log; false)
 
+# profiling build with per-unit service times (LSE_UNIT_TRACE_FILE=...)
+TRACE_LIB := paper_1409_7474_b200/_lib/liblse_b200_trace.so
+trace: $(TRACE_LIB)
+$(TRACE_LIB): $(SRC) $(HDR)
+	@mkdir -p $(dir $@)
+	$(NVCC) $(FLAGS) -DLSE_UNIT_TRACE -shared -o $@ $(SRC) 2> /dev/null
+
 oracle:
 	$(MAKE) -C oracle
 
 clean:
-	rm -f $(LIB)
+	rm -f $(LIB) $(TRACE_LIB)
 
-.PHONY: all clean oracle
+.PHONY: all clean oracle trace

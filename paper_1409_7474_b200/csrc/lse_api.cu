@@ -300,13 +300,88 @@ unsigned long long take_work(lse_run* r, long long units, int grid) {
   return base;
 }
 
+#ifdef LSE_UNIT_TRACE
+// Profiling builds: LSE_UNIT_TRACE_FILE=path appends, for launches
+// [LSE_UNIT_TRACE_SKIP, +LSE_UNIT_TRACE_COUNT) of the fused kernels, one
+// line per launch: "<kernel> <units> <nb> <grid> s0 e0 ... | exit a b
+// stamps p q" (ns, relative to the launch's first CTA entry; p / q are
+// global-timer stamps taken by 1-thread kernels just before and after).
+// Nothing synchronizes between launches: the buffers are read back when the
+// run next waits for the device (collect), so the pipeline is undisturbed.
+__global__ void k_stamp(unsigned long long* slot) {
+  unsigned long long t;
+  asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+  *slot = t;
+}
+struct TraceRec {
+  unsigned long long* d;
+  long long n, nb, cap;
+  int grid;
+  const char* name;
+};
+std::vector<TraceRec> g_traces;
+long long g_trace_launch = 0;
+constexpr long long kTrCta = 2 * 4096, kTrWarp = 4 * 4096;
+unsigned long long* trace_begin(lse_run* r, long long n, int grid, const char* name,
+                                long long nb) {
+  const char* f = std::getenv("LSE_UNIT_TRACE_FILE");
+  if (!f) return nullptr;
+  const long long skip = std::getenv("LSE_UNIT_TRACE_SKIP") ? std::atoll(std::getenv("LSE_UNIT_TRACE_SKIP")) : 0;
+  const long long cnt = std::getenv("LSE_UNIT_TRACE_COUNT") ? std::atoll(std::getenv("LSE_UNIT_TRACE_COUNT")) : 4;
+  const long long k = g_trace_launch++;
+  if (k < skip || k >= skip + cnt) return nullptr;
+  TraceRec t{nullptr, n, nb, 2 * n + kTrCta + kTrWarp + 2, grid, name};
+  cudaMalloc(&t.d, t.cap * sizeof(unsigned long long));
+  cudaMemsetAsync(t.d, 0, t.cap * sizeof(unsigned long long), r->st);
+  k_stamp<<<1, 1, 0, r->st>>>(t.d + t.cap - 2);
+  g_traces.push_back(t);
+  return t.d;
+}
+void trace_after(lse_run* r, unsigned long long* d) {
+  if (d) k_stamp<<<1, 1, 0, r->st>>>(d + g_traces.back().cap - 1);
+}
+void trace_flush() {
+  if (g_traces.empty()) return;
+  FILE* fp = std::fopen(std::getenv("LSE_UNIT_TRACE_FILE"), "a");
+  for (auto& t : g_traces) {
+    std::vector<unsigned long long> h(t.cap);
+    cudaMemcpy(h.data(), t.d, t.cap * sizeof(unsigned long long), cudaMemcpyDeviceToHost);
+    cudaFree(t.d);
+    if (!fp) continue;
+    const long long m = t.n + t.grid;
+    unsigned long long t0 = ~0ull;
+    for (long long u = 0; u < m; ++u) if (h[2 * u] && h[2 * u] < t0) t0 = h[2 * u];
+    std::fprintf(fp, "%s %lld %lld %d", t.name, t.n, t.nb, t.grid);
+    for (long long u = 0; u < m; ++u)
+      std::fprintf(fp, " %lld %lld", h[2 * u] ? (long long)(h[2 * u] - t0) : -1,
+                   h[2 * u + 1] ? (long long)(h[2 * u + 1] - t0) : -1);
+    unsigned long long emax = 0, emin = ~0ull;
+    for (long long w = 0; w < 4 * t.grid; ++w) {
+      const unsigned long long e = h[2 * t.n + kTrCta + w];
+      if (e) { emax = e > emax ? e : emax; emin = e < emin ? e : emin; }
+    }
+    std::fprintf(fp, " | exit %lld %lld stamps %lld %lld\n", (long long)(emin - t0),
+                 (long long)(emax - t0), (long long)h[t.cap - 2] - (long long)t0,
+                 (long long)h[t.cap - 1] - (long long)t0);
+  }
+  if (fp) std::fclose(fp);
+  g_traces.clear();
+}
+#endif
+
 template <int R, int MODEL, int SRC>
 int launch_update(lse_run* r, FastParams P) {
   const long long n = r->nb_upd[0] + r->ni_upd;
   const int g = fast_grid(n);
   P.work_base = take_work(r, n, g);
+#ifdef LSE_UNIT_TRACE
+  P.trace = trace_begin(r, n, g, "update", r->nb_upd[0]);
+#endif
   k_update<R, MODEL, SRC><<<g, kThreads, 0, r->st>>>(P);
   CKL();
+#ifdef LSE_UNIT_TRACE
+  trace_after(r, P.trace);
+#endif
   return LSE_OK;
 }
 
@@ -315,8 +390,14 @@ int launch_partition(lse_run* r, FastParams P) {
   const long long n = r->nb_part + r->ni_part;
   const int g = fast_grid(n);
   P.work_base = take_work(r, n, g);
+#ifdef LSE_UNIT_TRACE
+  P.trace = MASKONLY ? nullptr : trace_begin(r, n, g, "partition", r->nb_part);
+#endif
   k_partition<R, PART, CKPT, MASKONLY><<<g, kThreads, 0, r->st>>>(P);
   CKL();
+#ifdef LSE_UNIT_TRACE
+  trace_after(r, P.trace);
+#endif
   if (!MASKONLY) {
     // two-stage fixed-order reduction of all unit partials -> the next
     // update's coefficients (64 CTAs reduce contiguous slices, 1 CTA the rest)
@@ -329,7 +410,7 @@ int launch_partition(lse_run* r, FastParams P) {
       // finalize together (lse_strip_finalize)
       k_reduce_to_one<<<1, 256, 0, r->st>>>(R1, r->strip_out, r->d_scal, 1);
     } else {
-      k_finalize_run<<<1, 1024, 0, r->st>>>(R1, r->d_scal, PART ? 1 : 0, CKPT ? 1 : 0, P.iter);
+      k_finalize_run<<<1, 64, 0, r->st>>>(R1, r->d_scal, PART ? 1 : 0, CKPT ? 1 : 0, P.iter);
     }
     CKL();
   }
@@ -406,6 +487,9 @@ int collect(lse_run* r) {
   CK(cudaMemcpyAsync(r->h_scal, r->d_scal, sizeof(Scalars), cudaMemcpyDeviceToHost, r->st));
   CK(cudaMemcpyAsync(&work, r->d_work, sizeof(work), cudaMemcpyDeviceToHost, r->st));
   CK(cudaStreamSynchronize(r->st));
+#ifdef LSE_UNIT_TRACE
+  trace_flush();
+#endif
   // every dynamically scheduled launch must have made exactly its reserved
   // number of grabs (units + one failing grab per warp) unless it was stopped
   if (!r->h_scal->stop && work != r->work_next) {
@@ -792,7 +876,7 @@ int create_impl(lse_run** out, const lse_params* p, long long height, long long 
     }
     r->gu_all = geo_all_border(r->gu, H);
     r->ni_upd = (long long)(r->gu.r_hi - r->gu.r_lo) * r->gu.nci + (r->gu.nB1 + 31) / 32;
-    r->nb_upd[0] = r->gu.nA + (r->gu.nB2 + 31) / 32;
+    r->nb_upd[0] = border_units(r->gu);
     r->nb_upd[1] = r->gu_all.nA;
     // partition segments: >= ~8 interior units per resident warp, <= 16 chunks
     // (fixed by the image geometry only)
@@ -803,7 +887,7 @@ int create_impl(lse_run** out, const lse_params* p, long long height, long long 
     r->seg_chunks = (int)sc;
     r->nseg = wi > 0 ? (int)((wi + sc - 1) / sc) : 0;
     r->ni_part = hi_rows * r->nseg + (r->gp.nB1 + 31) / 32;
-    r->nb_part = r->gp.nA + (r->gp.nB2 + 31) / 32;
+    r->nb_part = border_units(r->gp);
   }
   const long long nparts = std::max<long long>(r->g.ntiles, r->ni_part + r->nb_part);
   auto cleanup = [&](int rc) {
@@ -973,7 +1057,7 @@ int lse_strip_finalize(lse_run* r, const void* parts, int nparts, int absolute) 
   }
   if (!r->strip_part) return LSE_OK;
   PartRanges R{{tp, tp, tp}, {nparts, 0, 0}};
-  k_finalize_run<<<1, 1024, 0, r->st>>>(R, r->d_scal, two_mean(r->p.model) ? 1 : 0,
+  k_finalize_run<<<1, 64, 0, r->st>>>(R, r->d_scal, two_mean(r->p.model) ? 1 : 0,
                                         r->strip_ckpt ? 1 : 0, r->iteration);
   CKL();
   r->strip_part = false;

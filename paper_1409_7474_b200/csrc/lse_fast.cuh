@@ -65,7 +65,42 @@ struct FastParams {
   unsigned long long* work;  // dynamic work counter (monotonic across launches)
   unsigned long long work_base;  // value of *work when this launch started
   int own_lo, own_hi;        // word-rows whose pixels count in the partials (row strips)
+  unsigned long long* trace; // LSE_UNIT_TRACE builds: (start, end) ns of every unit
 };
+
+// Unit tracing (profiling builds only, -DLSE_UNIT_TRACE): each warp stamps the
+// global timer when it grabs a unit; the interval up to its next grab is the
+// unit's service time.
+#ifdef LSE_UNIT_TRACE
+__device__ __forceinline__ unsigned long long lse_now() {
+  unsigned long long t;
+  asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+  return t;
+}
+#define LSE_TRACE_ENTRY const unsigned long long tr_entry = lse_now();
+#define LSE_TRACE_DECL unsigned long long tr_t0 = 0; int tr_prev = -1; bool tr_first = true;
+#define LSE_TRACE_MARK(unit)                                                        \
+  do {                                                                              \
+    const unsigned long long tr_now = lse_now();                                    \
+    if (P.trace && lane == 0 && tr_prev >= 0) {                                     \
+      P.trace[2 * tr_prev] = tr_t0;                                                 \
+      P.trace[2 * tr_prev + 1] = tr_now;                                            \
+    }                                                                               \
+    if (P.trace && tr_first && threadIdx.x == 0) {                                  \
+      P.trace[2 * nunits + 2 * blockIdx.x] = tr_entry;                              \
+      P.trace[2 * nunits + 2 * blockIdx.x + 1] = tr_now;                            \
+    }                                                                               \
+    if (P.trace && lane == 0 && (unit) < 0)                                         \
+      P.trace[2 * nunits + 2 * 4096 + blockIdx.x * (blockDim.x / 32) + threadIdx.x / 32] = tr_now; \
+    tr_first = false;                                                               \
+    tr_t0 = tr_now;                                                                 \
+    tr_prev = (unit);                                                               \
+  } while (0)
+#else
+#define LSE_TRACE_ENTRY
+#define LSE_TRACE_DECL
+#define LSE_TRACE_MARK(unit) do { } while (0)
+#endif
 
 constexpr int kChunk = 256;      // partition: columns per warp chunk (32 lanes x 8 columns)
 constexpr int kUpdCols = 8;      // update: columns per lane
@@ -299,109 +334,6 @@ __device__ __forceinline__ uint32_t word_at(const FastParams& P, int wr, int xc)
 }
 
 // ---------------------------------------------------------------- update
-// One lane: columns x0 .. x0+CPL-1 of word-row r (32 rows).  phi rows -1..32
-// are rebuilt from the bit state (t columns x0-R-1 .. x0+CPL+R); three phi
-// rows are kept in registers while walking down the rows.
-template <int R, int MODEL, int SRC, bool INT, int CPL>
-__device__ __forceinline__ void update_block(const FastParams& P, const float* s_lt,
-                                             const float* s_ls, int r, int x0, float A, float B,
-                                             float eps_u, const uint32_t (&prev)[CPL + 2 * (R + 1)],
-                                             const uint32_t (&cur)[CPL + 2 * (R + 1)]) {
-  constexpr int NT = CPL + 2 * (R + 1);
-  constexpr int NP = CPL + 2;             // phi columns x0-1 .. x0+CPL
-  const int H = P.g.H, W = P.g.W;
-  const int y0 = r * 32;
-  uint32_t cm[NT], win[NT];
-#pragma unroll
-  for (int j = 0; j < NT; ++j) {
-    const int xc = x0 - (R + 1) + j;
-    cm[j] = (INT || (xc >= 0 && xc < W)) ? 0xffffffffu : 0u;
-    win[j] = __funnelshift_r(prev[j], cur[j], 31 - R);   // base row y0-1-R
-  }
-  float pm[NP], p0[NP], pn[NP], dcur[CPL], dnext[CPL];
-  uint32_t ow[CPL];
-  uint32_t fbrows = 0u;                    // rows holding a near-tie pixel
-#pragma unroll
-  for (int c = 0; c < CPL; ++c) { ow[c] = 0u; dcur[c] = 0.f; dnext[c] = 0.f; }
-  phi_row<R, SRC, INT, NT, NP>(P, win, cm, 0, y0 - 1, s_lt, s_ls, pm);
-  phi_row<R, SRC, INT, NT, NP>(P, win, cm, 1, y0, s_lt, s_ls, p0);
-  load_data_row<INT, CPL>(P, y0, x0, dcur);
-  const uint32_t* wrow = P.bits_in + (size_t)r * P.g.pitch_w + (x0 - (R + 1));
-#pragma unroll 1
-  for (int k = 0; k < 32; ++k) {
-    const int kk = k + 1;                  // phi row produced in this step
-    if (kk == 16) {                        // switch to window base y0+16-R
-#pragma unroll
-      for (int j = 0; j < NT; ++j) {
-        if (INT) {
-          win[j] = __funnelshift_r(__ldg(wrow + j), __ldg(wrow + P.g.pitch_w + j), 16 - R);
-        } else {
-          const int xc = x0 - (R + 1) + j;
-          win[j] = __funnelshift_r(word_at<false>(P, r, xc), word_at<false>(P, r + 1, xc), 16 - R);
-        }
-      }
-    }
-    const int m0 = kk < 16 ? kk + 1 : kk - 16;
-    if (kk < 32) load_data_row<INT, CPL>(P, y0 + kk, x0, dnext);
-    phi_row<R, SRC, INT, NT, NP>(P, win, cm, m0, y0 + kk, s_lt, s_ls, pn);
-    const int i = y0 + k;
-    if (i < H) {
-      const uint32_t bitk = 1u << k;
-      uint32_t fb = 0u;
-#pragma unroll
-      for (int c = 0; c < CPL; ++c) {
-        const int x = x0 + c;
-        float dx, dy;
-        if (INT) {
-          dx = p0[c + 2] - p0[c];
-          dy = pn[c + 1] - pm[c + 1];
-        } else {
-          if (x >= W) continue;
-          dx = (x == 0) ? 2.f * (p0[c + 2] - p0[c + 1])
-                        : (x == W - 1) ? 2.f * (p0[c + 1] - p0[c]) : (p0[c + 2] - p0[c]);
-          dy = (i == 0) ? 2.f * (pn[c + 1] - p0[c + 1])
-                        : (i == H - 1) ? 2.f * (p0[c + 1] - pm[c + 1]) : (pn[c + 1] - pm[c + 1]);
-        }
-        const float h = sqrt_approx(fmaf(dx, dx, dy * dy));
-        // h = 2|grad phi|; A, B (region) and the g plane (edge) carry dt/2
-        const float vf = (MODEL == REGION) ? fmaf(A, dcur[c], B) : dcur[c];
-        const float u = fmaf(vf, h, p0[c + 1]);
-        if (u > 0.f) ow[c] |= bitk;
-        if (fabsf(u) <= eps_u) fb |= 1u << c;
-      }
-      if (fb) fbrows |= bitk;               // near tie somewhere in this row
-    }
-#pragma unroll
-    for (int c = 0; c < NP; ++c) { pm[c] = p0[c]; p0[c] = pn[c]; }
-#pragma unroll
-    for (int c = 0; c < CPL; ++c) dcur[c] = dnext[c];
-  }
-  // near ties: the row's decisions are redone in fp64 with the reference's
-  // operation order (outside the row loop, so the call does not force the
-  // loop state through local memory); non-tie pixels re-derive the same bit
-  while (fbrows) {
-    const int k = __ffs(fbrows) - 1;
-    fbrows &= fbrows - 1;
-    const uint32_t bitk = 1u << k;
-#pragma unroll 1
-    for (int c = 0; c < CPL; ++c) {
-      if (!INT && x0 + c >= W) break;
-      const bool pos = exact_u_fast<R, SRC>(P.ctx, P.bits_in, y0 + k, x0 + c) > 0.0;
-#pragma unroll
-      for (int q = 0; q < CPL; ++q)
-        if (q == c) ow[q] = pos ? (ow[q] | bitk) : (ow[q] & ~bitk);
-    }
-  }
-  if (!INT) {
-#pragma unroll
-    for (int c = 0; c < CPL; ++c) if (x0 + c >= W) ow[c] = 0u;
-  }
-  uint32_t* dst = P.bits_out + (size_t)r * P.g.pitch_w + x0;
-#pragma unroll
-  for (int q = 0; q < CPL / 4; ++q)
-    reinterpret_cast<uint4*>(dst)[q] = make_uint4(ow[4 * q], ow[4 * q + 1], ow[4 * q + 2], ow[4 * q + 3]);
-}
-
 // ------------------------------------------------- interior update block
 // Specialised copy of update_block for interior units (the >98% case):
 //  * LUT addressing is one SHF + one LOP3 per t: the windows are kept
@@ -503,6 +435,60 @@ __device__ __forceinline__ void phi_rows2_int(const FastParams& P, const uint32_
       else out[c] = ffma2(wd, t, out[c]);
     }
   }
+}
+
+// Near-tie columns of one interior row.  The fused loops flag whole rows
+// (one running min per row keeps the loop short); these recompute the row's
+// fp32 values with exactly the loop's operations -- phi_rows2_int's packed
+// lanes are independent FMAs, so a row's values do not depend on which row
+// it was paired with -- and return the columns that need the fp64 decision.
+template <int R, int MODEL, int CPL, int SRC>
+__device__ __noinline__ uint32_t update_tie_cols(const FastParams& P, uint32_t lut_base, int r,
+                                                 int x0, int k, float A, float B, float eps_u) {
+  constexpr int NT = CPL + 2 * (R + 1);
+  constexpr int NP = CPL + 2;
+  const int y0 = r * 32;
+  const int base = y0 + k - 1 - R;               // phi rows k-1 .. k+2 at m0 = 0 .. 3
+  const uint32_t* wp = P.bits_in + (size_t)(base >> 5) * P.g.pitch_w + (x0 - (R + 1));
+  uint32_t win4[NT];
+#pragma unroll
+  for (int j = 0; j < NT; ++j)
+    win4[j] = __funnelshift_r(__ldg(wp + j), __ldg(wp + P.g.pitch_w + j), base & 31) << 2;
+  float2 pa[NP], pb[NP];
+  phi_rows2_int<R, NT, NP, SRC>(P, win4, 0, lut_base, pa);     // rows k-1, k
+  phi_rows2_int<R, NT, NP, SRC>(P, win4, 2, lut_base, pb);     // rows k+1, k+2
+  const float* drow = P.data32 + (size_t)(y0 + k) * P.g.data_pitch + x0;
+  uint32_t cols = 0u;
+#pragma unroll
+  for (int c = 0; c < CPL; ++c) {
+    const float dy = __fsub_rn(pb[c + 1].x, pa[c + 1].x);
+    const float dx = __fsub_rn(pa[c + 2].y, pa[c].y);
+    const float h = sqrt_approx(__fmaf_rn(dx, dx, __fmul_rn(dy, dy)));
+    const float d = __ldg(drow + c);
+    const float vf = (MODEL == REGION) ? __fmaf_rn(A, d, B) : d;
+    const float u = __fmaf_rn(vf, h, pa[c + 1].y);
+    if (fabsf(u) <= eps_u) cols |= 1u << c;
+  }
+  return cols ? cols : (1u << CPL) - 1u;         // (all columns if nothing matched)
+}
+
+template <int R>
+__device__ __noinline__ uint32_t partition_tie_cols(const FastParams& P, uint32_t lut_base, int r,
+                                                    int x0, int k, float eps_phi) {
+  constexpr int NT = kColsPerThread + 2 * R;
+  const int base = r * 32 + k - R;               // phi row k at m0 = 0
+  const uint32_t* wp = P.bits_in + (size_t)(base >> 5) * P.g.pitch_w + (x0 - R);
+  uint32_t win4[NT];
+#pragma unroll
+  for (int j = 0; j < NT; ++j)
+    win4[j] = __funnelshift_r(__ldg(wp + j), __ldg(wp + P.g.pitch_w + j), base & 31) << 2;
+  float2 ph[8];
+  phi_rows2_int<R, NT, 8>(P, win4, 0, lut_base, ph);
+  uint32_t cols = 0u;
+#pragma unroll
+  for (int c = 0; c < 8; ++c)
+    if (fabsf(ph[c].x) <= eps_phi) cols |= 1u << c;
+  return cols ? cols : 0xffu;
 }
 
 constexpr int kRing2 = 8;                       // data rows buffered per warp (2-row steps)
@@ -608,8 +594,10 @@ __device__ __forceinline__ void update_block_int2(const FastParams& P, uint32_t 
     const int k = __ffs(fbrows) - 1;
     fbrows &= fbrows - 1;
     const uint32_t bitk = 1u << k;
-#pragma unroll 1
-    for (int c = 0; c < CPL; ++c) {
+    uint32_t cols = update_tie_cols<R, MODEL, CPL, SRC>(P, lut_base, r, x0, k, A, B, eps_u);
+    while (cols) {
+      const int c = __ffs(cols) - 1;
+      cols &= cols - 1;
       const bool pos = exact_u_fast<R, SRC>(P.ctx, P.bits_in, y0 + k, x0 + c) > 0.0;
 #pragma unroll
       for (int q = 0; q < CPL; ++q)
@@ -654,22 +642,107 @@ __device__ __forceinline__ int grab_unit(const FastParams& P, int lane) {
 // |grad phi| == 0, v == 0 and u == phi exactly, so b^{n+1} == b^n and the
 // chunk is copied without reading the data plane).
 // INT = false: border units (zero padding, one-sided gradients).
-// Border lane block: zero padding / one-sided gradients.  Not inlined, so its
-// register needs do not constrain the interior loop (it runs on ~1% of units).
-template <int R, int MODEL, int SRC>
-__device__ __noinline__ void border_update_lane(const FastParams& P, const float* s_lt,
-                                                const float* s_ls, int r, int x0, float A,
-                                                float B, float eps_u) {
-  constexpr int CPL = kUpdCols;
+// Border rows k0 .. k0 + kBorderRows - 1 of the lane block (r, x0): zero
+// padding / one-sided gradients (update_block's arithmetic on a row range).
+// ow[c] gets bit k for the rows of the range only.
+template <int R, int MODEL, int SRC, int CPL>
+__device__ __forceinline__ void update_rows_border(const FastParams& P, const float* s_lt,
+                                                   const float* s_ls, int r, int x0, int k0,
+                                                   float A, float B, float eps_u,
+                                                   uint32_t (&ow)[CPL]) {
   constexpr int NT = CPL + 2 * (R + 1);
-  uint32_t prev[NT], cur[NT];
+  constexpr int NP = CPL + 2;
+  const int H = P.g.H, W = P.g.W;
+  const int y0 = r * 32;
+  const int base = y0 + k0 - 1 - R;              // window row 0 (phi row y0+k0-1 at m0 = 0)
+  const int wr = base >> 5, sh = base & 31;
+  uint32_t cm[NT], win[NT];
 #pragma unroll
   for (int j = 0; j < NT; ++j) {
     const int xc = x0 - (R + 1) + j;
-    prev[j] = word_at<false>(P, r - 1, xc);
-    cur[j] = word_at<false>(P, r, xc);
+    cm[j] = (xc >= 0 && xc < W) ? 0xffffffffu : 0u;
+    win[j] = __funnelshift_r(word_at<false>(P, wr, xc), word_at<false>(P, wr + 1, xc), sh);
   }
-  update_block<R, MODEL, SRC, false, CPL>(P, s_lt, s_ls, r, x0, A, B, eps_u, prev, cur);
+  float pm[NP], p0[NP], pn[NP], dcur[CPL], dnext[CPL];
+  uint32_t fbrows = 0u;
+#pragma unroll
+  for (int c = 0; c < CPL; ++c) { ow[c] = 0u; dcur[c] = 0.f; dnext[c] = 0.f; }
+  phi_row<R, SRC, false, NT, NP>(P, win, cm, 0, y0 + k0 - 1, s_lt, s_ls, pm);
+  phi_row<R, SRC, false, NT, NP>(P, win, cm, 1, y0 + k0, s_lt, s_ls, p0);
+  load_data_row<false, CPL>(P, y0 + k0, x0, dcur);
+#pragma unroll 1
+  for (int k = k0; k < k0 + kBorderRows; ++k) {
+    const int kk = k + 1;                        // phi row produced in this step
+    if (kk < k0 + kBorderRows) load_data_row<false, CPL>(P, y0 + kk, x0, dnext);
+    phi_row<R, SRC, false, NT, NP>(P, win, cm, kk - k0 + 1, y0 + kk, s_lt, s_ls, pn);
+    const int i = y0 + k;
+    if (i < H) {
+      const uint32_t bitk = 1u << k;
+      uint32_t fb = 0u;
+#pragma unroll
+      for (int c = 0; c < CPL; ++c) {
+        const int x = x0 + c;
+        if (x >= W) continue;
+        const float dx = (x == 0) ? 2.f * (p0[c + 2] - p0[c + 1])
+                         : (x == W - 1) ? 2.f * (p0[c + 1] - p0[c]) : (p0[c + 2] - p0[c]);
+        const float dy = (i == 0) ? 2.f * (pn[c + 1] - p0[c + 1])
+                         : (i == H - 1) ? 2.f * (p0[c + 1] - pm[c + 1]) : (pn[c + 1] - pm[c + 1]);
+        const float h = sqrt_approx(fmaf(dx, dx, dy * dy));
+        // h = 2|grad phi|; A, B (region) and the g plane (edge) carry dt/2
+        const float vf = (MODEL == REGION) ? fmaf(A, dcur[c], B) : dcur[c];
+        const float u = fmaf(vf, h, p0[c + 1]);
+        if (u > 0.f) ow[c] |= bitk;
+        if (fabsf(u) <= eps_u) fb |= 1u << c;
+      }
+      if (fb) fbrows |= bitk;
+    }
+#pragma unroll
+    for (int c = 0; c < NP; ++c) { pm[c] = p0[c]; p0[c] = pn[c]; }
+#pragma unroll
+    for (int c = 0; c < CPL; ++c) dcur[c] = dnext[c];
+  }
+  while (fbrows) {                               // near ties: exact fp64 decisions
+    const int k = __ffs(fbrows) - 1;
+    fbrows &= fbrows - 1;
+    const uint32_t bitk = 1u << k;
+#pragma unroll 1
+    for (int c = 0; c < CPL; ++c) {
+      if (x0 + c >= W) break;
+      const bool pos = exact_u_fast<R, SRC>(P.ctx, P.bits_in, y0 + k, x0 + c) > 0.0;
+#pragma unroll
+      for (int q = 0; q < CPL; ++q)
+        if (q == c) ow[q] = pos ? (ow[q] | bitk) : (ow[q] & ~bitk);
+    }
+  }
+}
+
+// Border unit: kBorderItems lane groups x kBorderQ row quarters.  Called by
+// every lane of the warp (the quarters are merged with shuffles); not
+// inlined, so its register needs do not constrain the interior loop.
+template <int R, int MODEL, int SRC>
+__device__ __noinline__ void border_update_unit(const FastParams& P, const float* s_lt,
+                                                const float* s_ls, int unit, float A, float B,
+                                                float eps_u) {
+  constexpr int CPL = kUpdCols;
+  const int lane = threadIdx.x & 31;
+  int r = 0, x0 = 0;
+  const bool act = border_lane(P.gu, unit, lane, P.g.W, r, x0);
+  uint32_t ow[CPL];
+#pragma unroll
+  for (int c = 0; c < CPL; ++c) ow[c] = 0u;
+  if (act)
+    update_rows_border<R, MODEL, SRC, CPL>(P, s_lt, s_ls, r, x0,
+                                           (lane / kBorderItems) * kBorderRows, A, B, eps_u, ow);
+#pragma unroll
+  for (int c = 0; c < CPL; ++c) {
+#pragma unroll
+    for (int o = kBorderItems; o < 32; o <<= 1) ow[c] |= __shfl_xor_sync(0xffffffffu, ow[c], o);
+  }
+  if (!act || lane >= kBorderItems) return;
+  uint32_t* dst = P.bits_out + (size_t)r * P.g.pitch_w + x0;
+#pragma unroll
+  for (int q = 0; q < CPL / 4; ++q)
+    reinterpret_cast<uint4*>(dst)[q] = make_uint4(ow[4 * q], ow[4 * q + 1], ow[4 * q + 2], ow[4 * q + 3]);
 }
 
 // One launch covers every unit: [border units][interior units] (border first,
@@ -682,6 +755,7 @@ __global__ void __launch_bounds__(kThreads, 4) k_update(FastParams P) {
   __shared__ __align__(16) float s_lt_raw[1024];
   __shared__ float s_ls[NPAT];
   __shared__ __align__(16) float s_ring[(kThreads / 32) * kRing2 * 32 * CPL];
+  LSE_TRACE_ENTRY
   float* const s_lt = aligned_lut(s_lt_raw);
   const Scalars* sc = P.scal;
   if (*(volatile const int*)&sc->stop) return;
@@ -693,13 +767,14 @@ __global__ void __launch_bounds__(kThreads, 4) k_update(FastParams P) {
   const int lane = threadIdx.x & 31;
   const int nb = border_units(P.gu);
   const int nunits = nb + interior_units(P.gu);
+  LSE_TRACE_DECL
   for (;;) {
     const int unit = grab_unit(P, lane);
+    LSE_TRACE_MARK(unit < nunits ? unit : -1);
     if (unit >= nunits) break;
     int r = 0, x0 = 0;
     if (unit < nb) {
-      if (border_lane(P.gu, unit, lane, P.g.W, r, x0))
-        border_update_lane<R, MODEL, SRC>(P, s_lt, s_ls, r, x0, A, B, eps_u);
+      border_update_unit<R, MODEL, SRC>(P, s_lt, s_ls, unit, A, B, eps_u);
       continue;
     }
     const int iu = unit - nb;
@@ -1040,13 +1115,15 @@ __device__ __forceinline__ void partition_block(const FastParams& P, const float
   }
 #pragma unroll
   for (int c = 0; c < 8; ++c) mw[c] = pw[c];               // phi > 0 unless phi == 0 (tie path)
-  // near ties: exact fp64 sign for every column of the flagged rows
+  // near ties: exact fp64 sign for the tie columns of the flagged rows
   while (fbrows) {
     const int k = __ffs(fbrows) - 1;
     fbrows &= fbrows - 1;
     const uint32_t bitk = 1u << k;
-#pragma unroll 1
-    for (int c = 0; c < 8; ++c) {
+    uint32_t cols = INT ? partition_tie_cols<R>(P, lut_base, r, x0, k, eps_phi) : 0xffu;
+    while (cols) {
+      const int c = __ffs(cols) - 1;
+      cols &= cols - 1;
       if (!INT && x0 + c >= W) break;
       const double e = exact_phi_fast<R>(P.ctx, P.bits_in, y0 + k, x0 + c);
 #pragma unroll
@@ -1114,23 +1191,90 @@ __device__ __forceinline__ void partition_commit(const FastParams& P, int r, int
   }
 }
 
-template <int R, bool PART, bool CKPT, bool MASKONLY>
-__device__ __noinline__ void border_partition_lane(const FastParams& P, const float* s_lt,
-                                                   const float* s_ls, int r, int x0,
-                                                   float eps_phi, LaneDelta& d) {
+// Border rows k0 .. k0 + kBorderRows - 1 of the partition lane block (r, x0):
+// signs of phi^{n+1} with zero padding (partition_block's arithmetic on a row
+// range); pw / mw get bit k for the rows of the range only.
+template <int R>
+__device__ __forceinline__ void partition_rows_border(const FastParams& P, const float* s_lt,
+                                                      const float* s_ls, int r, int x0, int k0,
+                                                      float eps_phi, uint32_t (&pw)[8],
+                                                      uint32_t (&mw)[8]) {
   constexpr int NT = kColsPerThread + 2 * R;
-  uint32_t pw[8], mw[8], prev[NT], cur[NT];
+  const int H = P.g.H, W = P.g.W;
+  const int y0 = r * 32;
+  const int base = y0 + k0 - R;                  // window row 0 (phi row y0+k0 at m0 = 0)
+  const int wr = base >> 5, sh = base & 31;
+  uint32_t cm[NT], win[NT];
 #pragma unroll
   for (int j = 0; j < NT; ++j) {
     const int xc = x0 - R + j;
-    prev[j] = word_at<false>(P, r - 1, xc);
-    cur[j] = word_at<false>(P, r, xc);
+    cm[j] = (xc >= 0 && xc < W) ? 0xffffffffu : 0u;
+    win[j] = __funnelshift_r(word_at<false>(P, wr, xc), word_at<false>(P, wr + 1, xc), sh);
   }
-  partition_block<R, false>(P, s_lt, s_ls, 0u, r, x0, eps_phi, prev, cur, pw, mw);
-  if (x0 + 8 > P.g.W) {
+  float ph[8];
+  uint32_t fbrows = 0u;
 #pragma unroll
-    for (int c = 0; c < 8; ++c) if (x0 + c >= P.g.W) { pw[c] = 0u; mw[c] = 0u; }
+  for (int c = 0; c < 8; ++c) { pw[c] = 0u; mw[c] = 0u; }
+#pragma unroll 1
+  for (int k = k0; k < k0 + kBorderRows; ++k) {
+    const int i = y0 + k;
+    if (i >= H) break;
+    phi_row<R, SRC_SMOOTH, false, NT, 8>(P, win, cm, k - k0, i, s_lt, s_ls, ph);
+    const uint32_t bitk = 1u << k;
+    bool tie = false;
+#pragma unroll
+    for (int c = 0; c < 8; ++c) {
+      if (x0 + c >= W) continue;
+      if (ph[c] > 0.f) pw[c] |= bitk;
+      tie |= fabsf(ph[c]) <= eps_phi;
+    }
+    if (tie) fbrows |= bitk;
   }
+#pragma unroll
+  for (int c = 0; c < 8; ++c) mw[c] = pw[c];     // phi > 0 unless phi == 0 (tie path)
+  while (fbrows) {                               // near ties: exact fp64 signs
+    const int k = __ffs(fbrows) - 1;
+    fbrows &= fbrows - 1;
+    const uint32_t bitk = 1u << k;
+#pragma unroll 1
+    for (int c = 0; c < 8; ++c) {
+      if (x0 + c >= W) break;
+      const double e = exact_phi_fast<R>(P.ctx, P.bits_in, y0 + k, x0 + c);
+#pragma unroll
+      for (int q = 0; q < 8; ++q) {
+        if (q == c) {
+          pw[q] = e >= 0.0 ? (pw[q] | bitk) : (pw[q] & ~bitk);
+          mw[q] = e > 0.0 ? (mw[q] | bitk) : (mw[q] & ~bitk);
+        }
+      }
+    }
+  }
+}
+
+// Border partition unit (all lanes call it): the row quarters of each lane
+// group are merged, then the group's first lane commits the whole word.
+template <int R, bool PART, bool CKPT, bool MASKONLY>
+__device__ __noinline__ void border_partition_unit(const FastParams& P, const float* s_lt,
+                                                   const float* s_ls, int unit, float eps_phi,
+                                                   LaneDelta& d) {
+  const int lane = threadIdx.x & 31;
+  int r = 0, x0 = 0;
+  const bool act = border_lane(P.gp, unit, lane, P.g.W, r, x0);
+  uint32_t pw[8], mw[8];
+#pragma unroll
+  for (int c = 0; c < 8; ++c) { pw[c] = 0u; mw[c] = 0u; }
+  if (act)
+    partition_rows_border<R>(P, s_lt, s_ls, r, x0, (lane / kBorderItems) * kBorderRows, eps_phi,
+                             pw, mw);
+#pragma unroll
+  for (int c = 0; c < 8; ++c) {
+#pragma unroll
+    for (int o = kBorderItems; o < 32; o <<= 1) {
+      pw[c] |= __shfl_xor_sync(0xffffffffu, pw[c], o);
+      mw[c] |= __shfl_xor_sync(0xffffffffu, mw[c], o);
+    }
+  }
+  if (!act || lane >= kBorderItems) return;
   partition_commit<PART, CKPT, MASKONLY>(P, r, x0, pw, mw, d);
 }
 
@@ -1144,6 +1288,7 @@ __global__ void __launch_bounds__(kThreads, 4) k_partition(FastParams P) {
   constexpr int NT = kColsPerThread + 2 * R;
   __shared__ __align__(16) float s_lt_raw[1024];
   __shared__ float s_ls[NPAT];
+  LSE_TRACE_ENTRY
   float* const s_lt = aligned_lut(s_lt_raw);
   Scalars* sc = P.scal;
   if (!MASKONLY && *(volatile const int*)&sc->stop) return;
@@ -1155,14 +1300,14 @@ __global__ void __launch_bounds__(kThreads, 4) k_partition(FastParams P) {
   const int nb = border_units(P.gp);
   const int nsu = (P.gp.r_hi - P.gp.r_lo) * nseg;
   const int nunits = nb + nsu + (P.gp.nB1 + 31) / 32;
+  LSE_TRACE_DECL
   for (;;) {
     const int unit = grab_unit(P, lane);
+    LSE_TRACE_MARK(unit < nunits ? unit : -1);
     if (unit >= nunits) break;
     LaneDelta d{0.0, 0.0, 0, 0, 0ull};
     if (unit < nb) {
-      int r, x0;
-      if (border_lane(P.gp, unit, lane, P.g.W, r, x0))
-        border_partition_lane<R, PART, CKPT, MASKONLY>(P, s_lt, s_ls, r, x0, eps_phi, d);
+      border_partition_unit<R, PART, CKPT, MASKONLY>(P, s_lt, s_ls, unit, eps_phi, d);
     } else {
       const int iu = unit - nb;
       int r = 0, c0 = 0, c1 = 1, xb = 0;

@@ -303,7 +303,7 @@ __global__ void __launch_bounds__(256) k_reduce_to_one(PartRanges R3, TilePartia
 }
 
 // per-iteration finalize of the fast path (DELTA partials); no-op once stopped
-__global__ void __launch_bounds__(1024) k_finalize_run(PartRanges R3, Scalars* sc, int region,
+__global__ void __launch_bounds__(64) k_finalize_run(PartRanges R3, Scalars* sc, int region,
                                                        int ckpt, long long iter) {
   if (*(volatile const int*)&sc->stop) return;
   finalize_cta(R3, sc, true, region != 0, ckpt != 0, iter);

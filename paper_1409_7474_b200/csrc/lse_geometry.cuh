@@ -18,14 +18,20 @@ namespace lse {
 //  whose stencil still lies inside the image, packed 32 per warp (each lane
 //  its own row); every lane of (1)/(2) runs the interior code.
 //  border work: (A) word-rows outside [r_lo, r_hi) -- the blocks [ta, tb) and
-//  [ba, bb) -- whole width, 256-column warp units; (B2) per interior row the
-//  left strip [0, xoff) and the right tail beyond the B1 groups, 8-column lane
-//  groups packed 32 per warp.  A row strip of a multi-GPU run drops the
-//  border rows it does not own (its halo rows, recomputed by their owner).
+//  [ba, bb) -- whole width; (B2) per interior row the left strip [0, xoff)
+//  and the right tail beyond the B1 groups.  Border work runs the slower
+//  zero-padding code, so its units are short: a border warp unit holds
+//  kBorderItems 8-column lane groups and each group's 32 rows are split over
+//  kBorderQ lanes (lane = quarter * kBorderItems + item).  A row strip of a
+//  multi-GPU run drops the border rows it does not own (its halo rows,
+//  recomputed by their owner).
+constexpr int kBorderQ = 4;                      // row quarters per border lane group
+constexpr int kBorderItems = 32 / kBorderQ;      // lane groups per border warp unit
+constexpr int kBorderRows = 32 / kBorderQ;       // rows per border lane
 struct Geo {
   int r_lo, r_hi, nci, xoff, x1;
   int ta, tb, ba, bb;  // part-A word-rows: [ta, tb) above and [ba, bb) below the interior
-  int nchunk_full;   // ceil(W / 256): chunks of a part-A row
+  int na_row;        // part-A warp units per word-row: ceil(ceil(W / 8) / kBorderItems)
   int nb1_row;       // B1 lane groups per interior row
   int nb2_left;      // B2 left-strip groups per interior row (xoff / 8)
   int nb2_row;       // B2 lane groups per interior row (left + right tail)
@@ -40,7 +46,7 @@ LSE_HD Geo make_geo(int H, int W, int R, int top, int bot, int right) {
   const int HR = (H + 31) / 32;
   Geo g{};
   g.xoff = 8;
-  g.nchunk_full = (W + 255) / 256;
+  g.na_row = ((W + 7) / 8 + kBorderItems - 1) / kBorderItems;
   long long rlo = (top + 31) / 32;
   long long rhi = geo_fdiv(H - 32 - bot, 32) + 1;
   if (rhi > HR) rhi = HR;
@@ -61,7 +67,7 @@ LSE_HD Geo make_geo(int H, int W, int R, int top, int bot, int right) {
   g.tb = g.r_lo;
   g.ba = g.r_hi;
   g.bb = HR;
-  g.nA = (g.tb - g.ta + g.bb - g.ba) * g.nchunk_full;
+  g.nA = (g.tb - g.ta + g.bb - g.ba) * g.na_row;
   g.nB1 = (g.r_hi - g.r_lo) * g.nb1_row;
   g.nB2 = (g.r_hi - g.r_lo) * g.nb2_row;
   return g;
@@ -77,7 +83,7 @@ LSE_HD bool geo_restrict_rows(Geo& g, int own_lo, int own_hi) {
   g.ba = g.ba > own_lo ? g.ba : own_lo;
   g.bb = g.bb < own_hi ? g.bb : own_hi;
   if (g.bb < g.ba) g.bb = g.ba;
-  g.nA = (g.tb - g.ta + g.bb - g.ba) * g.nchunk_full;
+  g.nA = (g.tb - g.ta + g.bb - g.ba) * g.na_row;
   return true;
 }
 
@@ -90,7 +96,7 @@ LSE_HD Geo geo_all_border(const Geo& in, int H) {
   g.ta = 0;
   g.tb = (H + 31) / 32;
   g.ba = g.bb = g.tb;
-  g.nA = ((H + 31) / 32) * g.nchunk_full;
+  g.nA = ((H + 31) / 32) * g.na_row;
   g.nB1 = g.nB2 = 0;
   return g;
 }
@@ -100,7 +106,9 @@ LSE_HD int chunk_units(const Geo& G) { return (G.r_hi - G.r_lo) * G.nci; }
 LSE_HD int interior_units(const Geo& G) {
   return chunk_units(G) + (G.nB1 + 31) / 32;
 }
-LSE_HD int border_units(const Geo& G) { return G.nA + (G.nB2 + 31) / 32; }
+LSE_HD int border_units(const Geo& G) {
+  return G.nA + (G.nB2 + kBorderItems - 1) / kBorderItems;
+}
 // B1 pack: lane -> (row, x0); false for the unused lanes of the last pack
 LSE_HD bool b1_lane(const Geo& G, int pack, int lane, int& r, int& x0) {
   const int g = pack * 32 + lane;
@@ -109,17 +117,20 @@ LSE_HD bool b1_lane(const Geo& G, int pack, int lane, int& r, int& x0) {
   x0 = G.x1 + 8 * (g - (r - G.r_lo) * G.nb1_row);
   return true;
 }
+// Border unit -> the lane group (r, x0) of `lane` (its row quarter is
+// lane / kBorderItems); false for the unused lanes of the last unit.
 LSE_HD bool border_lane(const Geo& G, int unit, int lane, int W, int& r,
                                             int& x0) {
+  const int item = lane % kBorderItems;
   if (unit < G.nA) {
-    const int rowidx = unit / G.nchunk_full;
-    const int c = unit - rowidx * G.nchunk_full;
+    const int rowidx = unit / G.na_row;
+    const int c = unit - rowidx * G.na_row;
     const int ntop = G.tb - G.ta;
     r = rowidx < ntop ? G.ta + rowidx : G.ba + (rowidx - ntop);
-    x0 = c * 256 + 8 * lane;
+    x0 = (c * kBorderItems + item) * 8;
     return x0 < W;
   }
-  const int g = (unit - G.nA) * 32 + lane;
+  const int g = (unit - G.nA) * kBorderItems + item;
   if (g >= G.nB2) return false;
   r = G.r_lo + g / G.nb2_row;
   const int j = g - (r - G.r_lo) * G.nb2_row;

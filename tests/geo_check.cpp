@@ -32,7 +32,7 @@ static int check(int H, int W, int R, int top, int bot, int left, int right, con
       cover[(size_t)r * NG + x0 / 8]++;
     }
   for (int u = 0; u < border_units(G); ++u)
-    for (int lane = 0; lane < 32; ++lane) {
+    for (int lane = 0; lane < kBorderItems; ++lane) {   // quarter 0 stands for its group
       int r, x0;
       if (!border_lane(G, u, lane, W, r, x0)) continue;
       if (r < 0 || r >= HR || x0 < 0 || x0 >= W || x0 % 8) { ++bad; continue; }
