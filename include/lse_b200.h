@@ -95,6 +95,13 @@ int lse_abi_version(void);
 const char* lse_last_error(void);
 int lse_device_count(void);
 
+/* Image formats of lse_run_create / lse_run_load_image (image_is_f32). */
+#define LSE_IMAGE_F64 0     /* float64 (H, W)                                     */
+#define LSE_IMAGE_F32 1     /* float32 (H, W)                                     */
+#define LSE_IMAGE_RGB8 2    /* uint8 (H, W, 3): decoded to the loader's luma
+                               ((0.299 R + 0.587 G) + 0.114 B) / 255 in float64
+                               (fileio.py:28-30, 88) on the device            */
+
 /* ---- the resumable driver: EvolutionRun (engine.py:193-269) -------------- */
 
 /* EvolutionRun.__init__ (engine.py:202-216): uploads the image, builds the
@@ -148,6 +155,21 @@ int lse_run_kernel_times(lse_run* run, double* update_ms, long long* update_laun
                          double* partition_ms, long long* partition_launches);
 
 void lse_run_destroy(lse_run* run);
+
+/* ---- batched tiles -----------------------------------------
+ * Many equal-size runs advanced together with one launch per kernel per
+ * iteration for all of them.  Tiles share size and evolution parameters and
+ * may differ in model (region / zhang / edge), image and seeds; each must be on
+ * the binary-state fast path (reinit_period = reg_period = 1) at the same
+ * iteration.  Each tile evolves exactly as it would alone: the per-tile
+ * reductions keep the single-run order.  After lse_batch_advance the run
+ * handles hold the new states (status, read_phi, read_mask work per tile);
+ * statuses (n entries, optional) receive their lse_status.  The batch
+ * borrows the runs: destroy it before them. */
+typedef struct lse_batch lse_batch;
+int lse_batch_create(lse_batch** out, lse_run* const* runs, int n_runs);
+int lse_batch_advance(lse_batch* batch, long long n_steps, lse_status* statuses);
+void lse_batch_destroy(lse_batch* batch);
 
 /* ---- row strips: one rank's share of a multi-GPU run --------
  * A rank owns whole word-rows (32 image rows) of the global grid and holds

@@ -29,6 +29,7 @@ LSE_MODEL_EDGE = 0
 LSE_MODEL_REGION = 1
 LSE_MODEL_ZHANG = 2
 LSE_PARTIAL_BYTES = 64
+LSE_IMAGE_F64, LSE_IMAGE_F32, LSE_IMAGE_RGB8 = 0, 1, 2
 
 LSE_PHI0_FIELD = 0
 LSE_PHI0_SIGNS = 1
@@ -90,6 +91,9 @@ _SIGS = {
     "lse_run_set_profiling": (_i, [_vp, _i]),
     "lse_run_kernel_times": (_i, [_vp, _dp, _llp, _dp, _llp]),
     "lse_run_destroy": (None, [_vp]),
+    "lse_batch_create": (_i, [C.POINTER(_vp), C.POINTER(_vp), _i]),
+    "lse_batch_advance": (_i, [_vp, _ll, C.POINTER(LseStatus)]),
+    "lse_batch_destroy": (None, [_vp]),
     "lse_strip_create": (_i, [C.POINTER(_vp), C.POINTER(LseParams), _ll, _ll, _vp, _i,
                               C.POINTER(LsePhi0), _i, _i, _ll]),
     "lse_strip_image_range": (_i, [_vp, _dp]),

@@ -209,6 +209,11 @@ FastParams fast_params(lse_run* r) {
   P.gp = r->gp;
   P.own_lo = r->own_lo;
   P.own_hi = r->own_hi;
+  P.ntiles = 1;
+  P.tile_hr = r->g.HR;
+  P.tile_h = r->H;
+  P.tile_words = (long long)r->g.HR * r->g.pitch_w;
+  P.tile_data = (long long)r->H * r->g.data_pitch;
   return P;
 }
 
@@ -377,7 +382,7 @@ int launch_update(lse_run* r, FastParams P) {
 #ifdef LSE_UNIT_TRACE
   P.trace = trace_begin(r, n, g, "update", r->nb_upd[0]);
 #endif
-  k_update<R, MODEL, SRC><<<g, kThreads, 0, r->st>>>(P);
+  k_update<R, MODEL, SRC, false><<<g, kThreads, 0, r->st>>>(P);
   CKL();
 #ifdef LSE_UNIT_TRACE
   trace_after(r, P.trace);
@@ -393,7 +398,7 @@ int launch_partition(lse_run* r, FastParams P) {
 #ifdef LSE_UNIT_TRACE
   P.trace = MASKONLY ? nullptr : trace_begin(r, n, g, "partition", r->nb_part);
 #endif
-  k_partition<R, PART, CKPT, MASKONLY><<<g, kThreads, 0, r->st>>>(P);
+  k_partition<R, PART, CKPT, MASKONLY, false><<<g, kThreads, 0, r->st>>>(P);
   CKL();
 #ifdef LSE_UNIT_TRACE
   trace_after(r, P.trace);
@@ -616,13 +621,24 @@ int upload_image(lse_run* r, const void* image, int is_f32) {
   int* d_flag = nullptr;
   TRY(dalloc(&d_flag, 1));
   CK(cudaMemsetAsync(d_flag, 0, sizeof(int), r->st));
-  if (is_f32) {
+  if (is_f32 == LSE_IMAGE_F32) {
     CK(cudaMemcpy2DAsync(r->d_data32, pitch * sizeof(float), image, W * sizeof(float),
                          W * sizeof(float), H, cudaMemcpyHostToDevice, r->st));
     r->fp32_exact = true;
   } else {
     TRY(dalloc(&tmp64, r->npx));
-    CK(cudaMemcpyAsync(tmp64, image, r->npx * sizeof(double), cudaMemcpyHostToDevice, r->st));
+    if (is_f32 == LSE_IMAGE_RGB8) {
+      // 8-bit RGB, decoded to the loader's float64 luma on the device
+      unsigned char* d8 = nullptr;
+      TRY(dalloc(&d8, 3 * r->npx));
+      CK(cudaMemcpyAsync(d8, image, 3 * r->npx, cudaMemcpyHostToDevice, r->st));
+      k_luma<<<(unsigned)((r->npx + 255) / 256), 256, 0, r->st>>>(d8, tmp64, r->npx);
+      CKL();
+      CK(cudaStreamSynchronize(r->st));
+      cudaFree(d8);
+    } else {
+      CK(cudaMemcpyAsync(tmp64, image, r->npx * sizeof(double), cudaMemcpyHostToDevice, r->st));
+    }
     k_to_f32<<<grid2(W, H), 128, 0, r->st>>>(tmp64, r->d_data32, H, W, pitch, d_flag);
     CKL();
     int inexact = 0;
@@ -954,6 +970,7 @@ int create_impl(lse_run** out, const lse_params* p, long long height, long long 
   s0.conv_window = p->conv_window;
   s0.eps_phi = (float)kEpsPhi;
   s0.eps_u = (float)edge_eps_u(p->dt);
+  if (p->model == LSE_MODEL_EDGE) s0.A = 1.0f;   // vf = 1 * g + 0 in a batched launch
   if (cudaMemcpyAsync(r->d_scal, &s0, sizeof(s0), cudaMemcpyHostToDevice, r->st) != cudaSuccess)
     return cleanup(fail(LSE_ERR_CUDA, "scalar upload failed"));
   if ((rc = upload_image(r, image, image_is_f32))) return cleanup(rc);
@@ -1253,6 +1270,299 @@ int lse_run_kernel_times(lse_run* r, double* update_ms, long long* update_launch
   if (partition_ms) *partition_ms = r->t_part;
   if (partition_launches) *partition_launches = r->n_part;
   return LSE_OK;
+}
+
+// ------------------------------------------------------------ batched tiles
+// lse_batch: many equal-size runs advanced together, one launch per kernel
+// per iteration for all of them (512 tiles of 1024^2 are each
+// far too small to fill a B200).  The tiles' state is stacked in shared
+// arrays while the batch advances and written back to the runs afterwards,
+// so every run stays usable on its own (status, read_phi, read_mask).
+}  // extern "C"
+
+struct lse_batch {
+  std::vector<lse_run*> runs;
+  int T = 0;
+  cudaStream_t st = nullptr;
+  uint32_t* bits[2] = {nullptr, nullptr};
+  uint32_t* P = nullptr;
+  uint32_t* M = nullptr;
+  float* data32 = nullptr;
+  double* data64 = nullptr;
+  Scalars* scal = nullptr;
+  Scalars* h_scal = nullptr;
+  ExactCtx* ctx = nullptr;
+  TilePartial* part = nullptr;
+  TilePartial* part_fin = nullptr;
+  unsigned long long* work = nullptr;
+  unsigned long long work_next = 0;
+  const uint32_t** d_src = nullptr;          // per-tile pointer tables for k_tiles_copy
+  uint32_t** d_dst = nullptr;
+  long long tile_words = 0, tile_data = 0, nb_upd = 0, ni_upd = 0, nb_part = 0, ni_part = 0;
+  int tile_hr = 0;
+  int cur = 0;
+};
+
+namespace {
+
+// copy n uint32 words per tile: src[t] -> dst[t] (device pointer tables)
+int tiles_copy(lse_batch* b, const std::vector<const void*>& src, const std::vector<void*>& dst,
+               long long n_words) {
+  CK(cudaMemcpyAsync(b->d_src, src.data(), b->T * sizeof(void*), cudaMemcpyHostToDevice, b->st));
+  CK(cudaMemcpyAsync(b->d_dst, dst.data(), b->T * sizeof(void*), cudaMemcpyHostToDevice, b->st));
+  const int gx = (int)std::min<long long>(64, (n_words + 255) / 256);
+  k_tiles_copy<<<dim3(gx, b->T), 256, 0, b->st>>>(b->d_src, b->d_dst, n_words);
+  CKL();
+  CK(cudaStreamSynchronize(b->st));             // the host tables are reused at once
+  return LSE_OK;
+}
+
+FastParams batch_params(lse_batch* b, int sel) {
+  lse_run* r0 = b->runs[0];
+  FastParams P = fast_params(r0);
+  P.pbits = b->P;
+  P.mbits = b->M;
+  P.data32 = b->data32;
+  P.part = b->part;
+  P.scal = b->scal;
+  P.ctx = b->ctx;
+  P.work = b->work;
+  P.bits_in = b->bits[sel];
+  P.bits_out = b->bits[sel ^ 1];
+  P.ntiles = b->T;
+  P.tile_hr = b->tile_hr;
+  P.tile_h = r0->H;
+  P.tile_words = b->tile_words;
+  P.tile_data = b->tile_data;
+  P.g.H = b->T * b->tile_hr * 32;             // the stacked arrays
+  P.g.HR = b->T * b->tile_hr;
+  P.own_lo = 0;
+  P.own_hi = P.g.HR;
+  return P;
+}
+
+unsigned long long batch_take_work(lse_batch* b, long long units, int grid) {
+  const unsigned long long base = b->work_next;
+  b->work_next += (unsigned long long)units + (unsigned long long)grid * 4;
+  return base;
+}
+
+template <int R>
+int batch_iteration(lse_batch* b, long long it, bool ckpt, int src, bool any_region) {
+  FastParams P = batch_params(b, b->cur);
+  P.iter = it;
+  {
+    const long long n = (long long)b->T * (b->nb_upd + b->ni_upd);
+    const int g = fast_grid(n);
+    P.work_base = batch_take_work(b, n, g);
+    if (src == SRC_SCALED) k_update<R, REGION, SRC_SCALED, true><<<g, kThreads, 0, b->st>>>(P);
+    else k_update<R, REGION, SRC_SMOOTH, true><<<g, kThreads, 0, b->st>>>(P);
+    CKL();
+  }
+  b->cur ^= 1;
+  if (!any_region && !ckpt) return LSE_OK;
+  P.bits_in = b->bits[b->cur];
+  const long long n = (long long)b->T * (b->nb_part + b->ni_part);
+  const int g = fast_grid(n);
+  P.work_base = batch_take_work(b, n, g);
+  if (ckpt) k_partition<R, true, true, false, true><<<g, kThreads, 0, b->st>>>(P);
+  else k_partition<R, true, false, false, true><<<g, kThreads, 0, b->st>>>(P);
+  CKL();
+  k_finalize_stage1_tiles<<<dim3(kFinSlices, b->T), 256, 0, b->st>>>(
+      b->part, b->part_fin, b->scal, (int)b->nb_part, (int)b->ni_part, b->T, ckpt ? 1 : 0);
+  CKL();
+  k_finalize_run_tiles<<<b->T, 64, 0, b->st>>>(b->part_fin, b->scal, ckpt ? 1 : 0, it);
+  CKL();
+  return LSE_OK;
+}
+
+}  // namespace
+
+extern "C" {
+
+int lse_batch_create(lse_batch** out, lse_run* const* runs, int n) {
+  if (!out || !runs || n < 1) return fail(LSE_ERR_ARG, "bad arguments");
+  *out = nullptr;
+  lse_run* r0 = runs[0];
+  for (int t = 0; t < n; ++t) {
+    lse_run* r = runs[t];
+    if (!r || r->strip) return fail(LSE_ERR_ARG, "batch tiles must be plain runs");
+    if (r->H != r0->H || r->W != r0->W || r->R != r0->R || r->p.dt != r0->p.dt ||
+        r->p.ts_reg != r0->p.ts_reg || r->wreg != r0->wreg ||
+        r->p.conv_check_every != r0->p.conv_check_every ||
+        r->p.conv_window != r0->p.conv_window || r->p.max_iters != r0->p.max_iters ||
+        r->skip_uniform != r0->skip_uniform)
+      return fail(LSE_ERR_ARG, "batch tiles must share size and evolution parameters");
+    if (r->p.reinit_period != 1 || r->p.reg_period != 1 || r->R < 1 || r->R > 4)
+      return fail(LSE_ERR_UNSUPPORTED, "batches run the binary-state fast path only");
+  }
+  lse_batch* b = new lse_batch();
+  b->runs.assign(runs, runs + n);
+  b->T = n;
+  b->tile_hr = r0->g.HR;
+  b->tile_words = (long long)r0->g.HR * r0->g.pitch_w;
+  b->tile_data = (long long)r0->g.HR * 32 * r0->g.data_pitch;
+  b->nb_upd = r0->nb_upd[0];
+  b->ni_upd = r0->ni_upd;
+  b->nb_part = r0->nb_part;
+  b->ni_part = r0->ni_part;
+  auto cleanup = [&](int rc) {
+    lse_batch_destroy(b);
+    return rc;
+  };
+  if (cudaStreamCreateWithFlags(&b->st, cudaStreamNonBlocking) != cudaSuccess)
+    return cleanup(fail(LSE_ERR_CUDA, "stream creation failed"));
+  bool any64 = false;
+  for (auto* r : b->runs) any64 |= r->d_data64 != nullptr;
+  const size_t nw = (size_t)n * b->tile_words, nd = (size_t)n * b->tile_data;
+  int rc;
+  if ((rc = dalloc(&b->bits[0], nw)) || (rc = dalloc(&b->bits[1], nw)) ||
+      (rc = dalloc(&b->P, nw)) || (rc = dalloc(&b->M, nw)) || (rc = dalloc(&b->data32, nd)) ||
+      (any64 && (rc = dalloc(&b->data64, nd))) || (rc = dalloc(&b->scal, n)) ||
+      (rc = dalloc(&b->ctx, n)) ||
+      (rc = dalloc(&b->part, (size_t)n * (b->nb_upd + b->ni_upd + b->nb_part + b->ni_part))) ||
+      (rc = dalloc(&b->part_fin, (size_t)n * kFinSlices)) || (rc = dalloc(&b->work, 1)) ||
+      (rc = dalloc(&b->d_src, n)) || (rc = dalloc(&b->d_dst, n)))
+    return cleanup(rc);
+  if (cudaMallocHost((void**)&b->h_scal, n * sizeof(Scalars)) != cudaSuccess)
+    return cleanup(fail(LSE_ERR_CUDA, "pinned alloc failed"));
+  // static data planes and per-tile contexts (tile t at word-row t * tile_hr)
+  std::vector<ExactCtx> ctx(n);
+  for (int t = 0; t < n; ++t) {
+    lse_run* r = b->runs[t];
+    CK(cudaStreamSynchronize(r->st));
+    CK(cudaMemcpyAsync(b->data32 + t * b->tile_data, r->d_data32,
+                       (size_t)r->H * r->g.data_pitch * sizeof(float), cudaMemcpyDeviceToDevice,
+                       b->st));
+    if (r->d_data64)
+      CK(cudaMemcpyAsync(b->data64 + t * b->tile_data, r->d_data64,
+                         (size_t)r->H * r->g.data_pitch * sizeof(double),
+                         cudaMemcpyDeviceToDevice, b->st));
+    ctx[t] = r->h_ctx;
+    ctx[t].data32 = b->data32 + t * b->tile_data;
+    ctx[t].data64 = r->d_data64 ? b->data64 + t * b->tile_data : nullptr;
+    ctx[t].scal = b->scal + t;
+  }
+  CK(cudaMemcpyAsync(b->ctx, ctx.data(), n * sizeof(ExactCtx), cudaMemcpyHostToDevice, b->st));
+  CK(cudaStreamSynchronize(b->st));
+  *out = b;
+  return LSE_OK;
+}
+
+int lse_batch_advance(lse_batch* b, long long n_steps, lse_status* statuses) {
+  if (!b) return fail(LSE_ERR_ARG, "null batch");
+  if (n_steps < 0) return fail(LSE_ERR_ARG, "n_steps must be >= 0");
+  const int T = b->T;
+  lse_run* r0 = b->runs[0];
+  const long long it0 = r0->iteration;
+  bool all_done = true;
+  for (auto* r : b->runs) {
+    if (r->iteration != it0 && !r->converged)
+      return fail(LSE_ERR_ARG, "batch tiles must be at the same iteration");
+    if (r->mode == SRC_FIELD || !fp32_ok(r) || r->mode != r0->mode || r->scale != r0->scale)
+      return fail(LSE_ERR_UNSUPPORTED, "batch tiles need binary states on the fast path");
+    all_done &= r->converged;
+  }
+  const long long steps = std::min(n_steps, r0->p.max_iters - it0);
+  if (steps > 0 && !all_done) {
+    for (auto* r : b->runs) {
+      TRY(upload_ctx(r));
+      TRY(prepare(r));
+    }
+    for (auto* r : b->runs) CK(cudaStreamSynchronize(r->st));
+    // gather: state, partition and checkpoint bits, scalars
+    std::vector<const void*> src(T);
+    std::vector<void*> dst(T);
+    b->cur = 0;
+    auto gather = [&](auto srcf, uint32_t* base, long long words) -> int {
+      for (int t = 0; t < T; ++t) {
+        src[t] = srcf(b->runs[t]);
+        dst[t] = base + t * b->tile_words;
+      }
+      return tiles_copy(b, src, dst, words);
+    };
+    TRY(gather([](lse_run* r) { return (const void*)r->d_bits[r->cur]; }, b->bits[0], b->tile_words));
+    TRY(gather([](lse_run* r) { return (const void*)r->d_P; }, b->P, b->tile_words));
+    TRY(gather([](lse_run* r) { return (const void*)r->d_M; }, b->M, b->tile_words));
+    for (int t = 0; t < T; ++t) {
+      src[t] = b->runs[t]->d_scal;
+      dst[t] = b->scal + t;
+    }
+    TRY(tiles_copy(b, src, dst, sizeof(Scalars) / 4));
+    CK(cudaMemsetAsync(b->work, 0, sizeof(unsigned long long), b->st));
+    b->work_next = 0;
+    bool any_region = false;
+    for (auto* r : b->runs) any_region |= two_mean(r->p.model);
+    int src_mode = r0->mode;
+    for (long long it = it0 + 1; it <= it0 + steps; ++it) {
+      const bool ckpt = it % r0->p.conv_check_every == 0;
+      int rc = LSE_ERR_ARG;
+      switch (r0->R) {
+        case 1: rc = batch_iteration<1>(b, it, ckpt, src_mode, any_region); break;
+        case 2: rc = batch_iteration<2>(b, it, ckpt, src_mode, any_region); break;
+        case 3: rc = batch_iteration<3>(b, it, ckpt, src_mode, any_region); break;
+        case 4: rc = batch_iteration<4>(b, it, ckpt, src_mode, any_region); break;
+      }
+      TRY(rc);
+      src_mode = SRC_SMOOTH;
+    }
+    // collect + scatter back into the runs
+    unsigned long long work = 0;
+    CK(cudaMemcpyAsync(b->h_scal, b->scal, T * sizeof(Scalars), cudaMemcpyDeviceToHost, b->st));
+    CK(cudaMemcpyAsync(&work, b->work, sizeof(work), cudaMemcpyDeviceToHost, b->st));
+    CK(cudaStreamSynchronize(b->st));
+    if (work != b->work_next) {
+      char msg[128];
+      std::snprintf(msg, sizeof(msg), "batch work-counter mismatch: device %llu, expected %llu",
+                    work, b->work_next);
+      return fail(LSE_ERR_CUDA, msg);
+    }
+    auto scatter = [&](auto dstf, const uint32_t* base, long long words) -> int {
+      for (int t = 0; t < T; ++t) {
+        src[t] = base + t * b->tile_words;
+        dst[t] = dstf(b->runs[t]);
+      }
+      return tiles_copy(b, src, dst, words);
+    };
+    TRY(scatter([](lse_run* r) { return (void*)r->d_bits[r->cur]; }, b->bits[b->cur], b->tile_words));
+    TRY(scatter([](lse_run* r) { return (void*)r->d_P; }, b->P, b->tile_words));
+    TRY(scatter([](lse_run* r) { return (void*)r->d_M; }, b->M, b->tile_words));
+    for (int t = 0; t < T; ++t) {
+      src[t] = b->scal + t;
+      dst[t] = b->runs[t]->d_scal;
+    }
+    TRY(tiles_copy(b, src, dst, sizeof(Scalars) / 4));
+    for (int t = 0; t < T; ++t) {
+      lse_run* r = b->runs[t];
+      const Scalars& s = b->h_scal[t];
+      *r->h_scal = s;
+      if (!r->converged) {
+        r->iteration = s.converged ? s.converged_iter : it0 + steps;
+        r->converged = s.converged != 0;
+        r->fast_iters += steps;
+      }
+      r->degenerate = s.degenerate != 0;
+      r->mode = SRC_SMOOTH;
+      r->field_valid = false;
+      r->prepared = true;
+      r->launched.clear();
+    }
+  }
+  if (statuses)
+    for (int t = 0; t < T; ++t) fill_status(b->runs[t], statuses + t, -1);
+  return LSE_OK;
+}
+
+void lse_batch_destroy(lse_batch* b) {
+  if (!b) return;
+  if (b->st) cudaStreamSynchronize(b->st);
+  void* ptrs[] = {b->bits[0], b->bits[1], b->P, b->M, b->data32, b->data64, b->scal,
+                  b->ctx, b->part, b->part_fin, b->work, (void*)b->d_src, (void*)b->d_dst};
+  for (void* q : ptrs)
+    if (q) cudaFree(q);
+  if (b->h_scal) cudaFreeHost(b->h_scal);
+  if (b->st) cudaStreamDestroy(b->st);
+  delete b;
 }
 
 void lse_run_destroy(lse_run* r) {

@@ -66,7 +66,21 @@ struct FastParams {
   unsigned long long work_base;  // value of *work when this launch started
   int own_lo, own_hi;        // word-rows whose pixels count in the partials (row strips)
   unsigned long long* trace; // LSE_UNIT_TRACE builds: (start, end) ns of every unit
+  // batched tiles (lse_batch): ntiles equal tiles stacked in the arrays above,
+  // tile t at word-row t * tile_hr; scal / ctx are per-tile arrays and gu / gp
+  // the geometry of one tile (single runs: ntiles = 1, tile 0 is the image)
+  int ntiles, tile_hr, tile_h;
+  long long tile_words, tile_data;
 };
+
+// exact-path frame of tile t (its context, state and first image row)
+__device__ __forceinline__ const ExactCtx* tile_ctx(const FastParams& P, int t) {
+  return P.ctx + t;
+}
+__device__ __forceinline__ const uint32_t* tile_bits(const FastParams& P, int t) {
+  return P.bits_in + (size_t)t * P.tile_words;
+}
+__device__ __forceinline__ int tile_y0(const FastParams& P, int t) { return t * P.tile_hr * 32; }
 
 // Unit tracing (profiling builds only, -DLSE_UNIT_TRACE): each warp stamps the
 // global timer when it grabs a unit; the interval up to its next grab is the
@@ -500,7 +514,8 @@ __device__ __forceinline__ void update_block_int2(const FastParams& P, uint32_t 
                                                   float* ring, int r, int x0, float A, float B,
                                                   float eps_u,
                                                   const uint32_t (&prev)[CPL + 2 * (R + 1)],
-                                                  const uint32_t (&cur)[CPL + 2 * (R + 1)]) {
+                                                  const uint32_t (&cur)[CPL + 2 * (R + 1)],
+                                                  int tile) {
   constexpr int NT = CPL + 2 * (R + 1);
   constexpr int NP = CPL + 2;
   constexpr uint32_t kSlot = 32 * CPL * 4;
@@ -598,7 +613,8 @@ __device__ __forceinline__ void update_block_int2(const FastParams& P, uint32_t 
     while (cols) {
       const int c = __ffs(cols) - 1;
       cols &= cols - 1;
-      const bool pos = exact_u_fast<R, SRC>(P.ctx, P.bits_in, y0 + k, x0 + c) > 0.0;
+      const bool pos = exact_u_fast<R, SRC>(tile_ctx(P, tile), tile_bits(P, tile),
+                                            y0 - tile_y0(P, tile) + k, x0 + c) > 0.0;
 #pragma unroll
       for (int q = 0; q < CPL; ++q)
         if (q == c) ow[q] = pos ? (ow[q] | bitk) : (ow[q] & ~bitk);
@@ -720,13 +736,22 @@ __device__ __forceinline__ void update_rows_border(const FastParams& P, const fl
 // every lane of the warp (the quarters are merged with shuffles); not
 // inlined, so its register needs do not constrain the interior loop.
 template <int R, int MODEL, int SRC>
-__device__ __noinline__ void border_update_unit(const FastParams& P, const float* s_lt,
-                                                const float* s_ls, int unit, float A, float B,
-                                                float eps_u) {
+__device__ __forceinline__ void border_update_body(const FastParams& P, const float* s_lt,
+                                                   const float* s_ls, int unit, float A, float B,
+                                                   float eps_u, bool stopped) {
   constexpr int CPL = kUpdCols;
   const int lane = threadIdx.x & 31;
   int r = 0, x0 = 0;
   const bool act = border_lane(P.gu, unit, lane, P.g.W, r, x0);
+  if (stopped) {                                 // converged tile: keep its state
+    if (!act || lane >= kBorderItems) return;
+    const uint32_t* src = P.bits_in + (size_t)r * P.g.pitch_w + x0;
+    uint32_t* dst = P.bits_out + (size_t)r * P.g.pitch_w + x0;
+#pragma unroll
+    for (int q = 0; q < CPL / 4; ++q)
+      reinterpret_cast<uint4*>(dst)[q] = reinterpret_cast<const uint4*>(src)[q];
+    return;
+  }
   uint32_t ow[CPL];
 #pragma unroll
   for (int c = 0; c < CPL; ++c) ow[c] = 0u;
@@ -745,9 +770,38 @@ __device__ __noinline__ void border_update_unit(const FastParams& P, const float
     reinterpret_cast<uint4*>(dst)[q] = make_uint4(ow[4 * q], ow[4 * q + 1], ow[4 * q + 2], ow[4 * q + 3]);
 }
 
+// the tile-local view of a batched launch: every pointer at the tile's first
+// row, the tile's scalars / context, the tile's height
+__device__ __forceinline__ void tile_view(FastParams& Q, int tile) {
+  Q.bits_in += (size_t)tile * Q.tile_words;
+  Q.bits_out += (size_t)tile * Q.tile_words;
+  Q.pbits += (size_t)tile * Q.tile_words;
+  Q.mbits += (size_t)tile * Q.tile_words;
+  Q.data32 += (size_t)tile * Q.tile_data;
+  Q.scal += tile;
+  Q.ctx += tile;
+  Q.g.H = Q.tile_h;
+  Q.g.HR = Q.tile_hr;
+}
+
+template <int R, int MODEL, int SRC, bool BATCH>
+__device__ __noinline__ void border_update_unit(const FastParams& P, const float* s_lt,
+                                                const float* s_ls, int unit, int tile, float A,
+                                                float B, float eps_u, bool stopped) {
+  if (!BATCH) {
+    border_update_body<R, MODEL, SRC>(P, s_lt, s_ls, unit, A, B, eps_u, false);
+    return;
+  }
+  FastParams Q = P;
+  tile_view(Q, tile);
+  border_update_body<R, MODEL, SRC>(Q, s_lt, s_ls, unit, A, B, eps_u, stopped);
+}
+
 // One launch covers every unit: [border units][interior units] (border first,
 // so their longer latency overlaps the interior work of the other warps).
-template <int R, int MODEL, int SRC>
+// BATCH: every unit of every tile, [all border units][all interior units];
+// the tile's scalars (stop, A, B, guards) are read per unit.
+template <int R, int MODEL, int SRC, bool BATCH>
 __global__ void __launch_bounds__(kThreads, 4) k_update(FastParams P) {
   constexpr int CPL = kUpdCols;
   constexpr int NPAT = 1 << (2 * R + 1);
@@ -758,26 +812,48 @@ __global__ void __launch_bounds__(kThreads, 4) k_update(FastParams P) {
   LSE_TRACE_ENTRY
   float* const s_lt = aligned_lut(s_lt_raw);
   const Scalars* sc = P.scal;
-  if (*(volatile const int*)&sc->stop) return;
-  if (MODEL == REGION && blockIdx.x == 0 && threadIdx.x == 0 && sc->zero_vel)
-    P.scal->degenerate = 1;
-  const float A = sc->A, B = sc->B, eps_u = sc->eps_u;
+  if (!BATCH && *(volatile const int*)&sc->stop) return;
+  if (MODEL == REGION && blockIdx.x == 0) {      // sticky degenerate (engine.py:239-240)
+    for (int t = threadIdx.x; t < (BATCH ? P.ntiles : 1); t += blockDim.x)
+      if (P.scal[t].zero_vel && !P.scal[t].stop && P.scal[t].model != EDGE)
+        P.scal[t].degenerate = 1;
+  }
+  float A = sc->A, B = sc->B, eps_u = sc->eps_u;
   load_luts<R>(P, s_lt, s_ls);
   __syncthreads();
   const int lane = threadIdx.x & 31;
   const int nb = border_units(P.gu);
-  const int nunits = nb + interior_units(P.gu);
+  const int ni = interior_units(P.gu);
+  const int T = BATCH ? P.ntiles : 1;
+  const int nunits = T * (nb + ni);
   LSE_TRACE_DECL
   for (;;) {
     const int unit = grab_unit(P, lane);
     LSE_TRACE_MARK(unit < nunits ? unit : -1);
     if (unit >= nunits) break;
+    int tile = 0, lu = unit;
+    bool stopped = false;
+    if (BATCH) {
+      if (unit < T * nb) {
+        tile = unit / nb;
+        lu = unit - tile * nb;
+      } else {
+        const int iu = unit - T * nb;
+        tile = iu / ni;
+        lu = nb + (iu - tile * ni);
+      }
+      const Scalars* st = P.scal + tile;
+      stopped = *(volatile const int*)&st->stop != 0;
+      A = st->A;
+      B = st->B;
+      eps_u = st->eps_u;
+    }
     int r = 0, x0 = 0;
-    if (unit < nb) {
-      border_update_unit<R, MODEL, SRC>(P, s_lt, s_ls, unit, A, B, eps_u);
+    if (lu < nb) {
+      border_update_unit<R, MODEL, SRC, BATCH>(P, s_lt, s_ls, lu, tile, A, B, eps_u, stopped);
       continue;
     }
-    const int iu = unit - nb;
+    const int iu = lu - nb;
     bool act = true;
     const int nch = chunk_units(P.gu);
     if (iu < nch) {
@@ -786,6 +862,7 @@ __global__ void __launch_bounds__(kThreads, 4) k_update(FastParams P) {
     } else {
       act = b1_lane(P.gu, iu - nch, lane, r, x0);
     }
+    if (BATCH) r += tile * P.tile_hr;             // row of the tile in the stacked arrays
     uint32_t prev[NT], cur[NT];
     uint32_t a = ~0u, o = 0u;
     if (act) {
@@ -802,7 +879,8 @@ __global__ void __launch_bounds__(kThreads, 4) k_update(FastParams P) {
       }
     }
     // uniform-window skip: phi constant over the block's stencil => b unchanged
-    if (P.skip_uniform && __all_sync(0xffffffffu, !act || a == ~0u || o == 0u)) {
+    // (a converged tile of a batch keeps its state the same way)
+    if (stopped || (P.skip_uniform && __all_sync(0xffffffffu, !act || a == ~0u || o == 0u))) {
       if (!act) continue;
       uint32_t* dst = P.bits_out + (size_t)r * P.g.pitch_w + x0;
 #pragma unroll
@@ -814,7 +892,7 @@ __global__ void __launch_bounds__(kThreads, 4) k_update(FastParams P) {
     if (!act) continue;
     update_block_int2<R, MODEL, CPL, SRC>(P, (uint32_t)__cvta_generic_to_shared(s_lt),
                                           s_ring + (threadIdx.x >> 5) * kRing2 * 32 * CPL, r, x0,
-                                          A, B, eps_u, prev, cur);
+                                          A, B, eps_u, prev, cur, tile);
   }
 }
 
@@ -1054,7 +1132,7 @@ __device__ __forceinline__ void partition_block(const FastParams& P, const float
                                                 int x0, float eps_phi,
                                                 const uint32_t (&prev)[8 + 2 * R],
                                                 const uint32_t (&cur)[8 + 2 * R],
-                                                uint32_t (&pw)[8], uint32_t (&mw)[8]) {
+                                                uint32_t (&pw)[8], uint32_t (&mw)[8], int tile) {
   constexpr int NT = kColsPerThread + 2 * R;
   const int H = P.g.H, W = P.g.W;
   const int y0 = r * 32;
@@ -1125,7 +1203,8 @@ __device__ __forceinline__ void partition_block(const FastParams& P, const float
       const int c = __ffs(cols) - 1;
       cols &= cols - 1;
       if (!INT && x0 + c >= W) break;
-      const double e = exact_phi_fast<R>(P.ctx, P.bits_in, y0 + k, x0 + c);
+      const double e = exact_phi_fast<R>(tile_ctx(P, tile), tile_bits(P, tile),
+                                         y0 - tile_y0(P, tile) + k, x0 + c);
 #pragma unroll
       for (int q = 0; q < 8; ++q) {
         if (q == c) {
@@ -1147,7 +1226,7 @@ struct LaneDelta {
 template <bool PART, bool CKPT, bool MASKONLY>
 __device__ __forceinline__ void partition_commit(const FastParams& P, int r, int x0,
                                                  const uint32_t (&pw)[8], const uint32_t (&mw)[8],
-                                                 LaneDelta& d) {
+                                                 LaneDelta& d, int tile = 0) {
   const int y0 = r * 32;
   const size_t base = (size_t)r * P.g.pitch_w + x0;
   // a row strip's halo word-rows are owned (and counted) by the neighbour
@@ -1170,7 +1249,7 @@ __device__ __forceinline__ void partition_commit(const FastParams& P, int r, int
       while (chg) {
         const int b = __ffs(chg) - 1;
         chg &= chg - 1;
-        const double I = data_exact(P.ctx, y0 + b, x0 + c);
+        const double I = data_exact(tile_ctx(P, tile), y0 - tile_y0(P, tile) + b, x0 + c);
         if ((pw[c] >> b) & 1u) { d.a_in += I; ++d.n_in; }
         else { d.a_out += I; ++d.n_out; }
       }
@@ -1254,9 +1333,9 @@ __device__ __forceinline__ void partition_rows_border(const FastParams& P, const
 // Border partition unit (all lanes call it): the row quarters of each lane
 // group are merged, then the group's first lane commits the whole word.
 template <int R, bool PART, bool CKPT, bool MASKONLY>
-__device__ __noinline__ void border_partition_unit(const FastParams& P, const float* s_lt,
-                                                   const float* s_ls, int unit, float eps_phi,
-                                                   LaneDelta& d) {
+__device__ __forceinline__ void border_partition_body(const FastParams& P, const float* s_lt,
+                                                      const float* s_ls, int unit, float eps_phi,
+                                                      LaneDelta& d) {
   const int lane = threadIdx.x & 31;
   int r = 0, x0 = 0;
   const bool act = border_lane(P.gp, unit, lane, P.g.W, r, x0);
@@ -1278,11 +1357,26 @@ __device__ __noinline__ void border_partition_unit(const FastParams& P, const fl
   partition_commit<PART, CKPT, MASKONLY>(P, r, x0, pw, mw, d);
 }
 
+template <int R, bool PART, bool CKPT, bool MASKONLY, bool BATCH>
+__device__ __noinline__ void border_partition_unit(const FastParams& P, const float* s_lt,
+                                                   const float* s_ls, int unit, int tile,
+                                                   bool part_t, float eps_phi, LaneDelta& d) {
+  if (!BATCH) {
+    border_partition_body<R, PART, CKPT, MASKONLY>(P, s_lt, s_ls, unit, eps_phi, d);
+    return;
+  }
+  FastParams Q = P;
+  tile_view(Q, tile);
+  if (part_t) border_partition_body<R, true, CKPT, false>(Q, s_lt, s_ls, unit, eps_phi, d);
+  else border_partition_body<R, false, CKPT, false>(Q, s_lt, s_ls, unit, eps_phi, d);
+}
+
 // Units: [border units][interior (word-row, segment of seg_chunks chunks)]
 // [interior B1 packs]; each unit's deltas form one partial at part[unit]
-// (fixed geometry => deterministic).  A separate 1-CTA finalize kernel then
-// reduces all partials.
-template <int R, bool PART, bool CKPT, bool MASKONLY>
+// (fixed geometry => deterministic).  A separate finalize then reduces all
+// partials in a fixed order.  BATCH: [all tiles' border units][all tiles'
+// interior units]; a tile's partials are reduced by its own finalize CTA.
+template <int R, bool PART, bool CKPT, bool MASKONLY, bool BATCH>
 __global__ void __launch_bounds__(kThreads, 4) k_partition(FastParams P) {
   constexpr int NPAT = 1 << (2 * R + 1);
   constexpr int NT = kColsPerThread + 2 * R;
@@ -1291,7 +1385,7 @@ __global__ void __launch_bounds__(kThreads, 4) k_partition(FastParams P) {
   LSE_TRACE_ENTRY
   float* const s_lt = aligned_lut(s_lt_raw);
   Scalars* sc = P.scal;
-  if (!MASKONLY && *(volatile const int*)&sc->stop) return;
+  if (!BATCH && !MASKONLY && *(volatile const int*)&sc->stop) return;
   const float eps_phi = sc->eps_phi;
   load_luts<R>(P, s_lt, s_ls);
   __syncthreads();
@@ -1299,17 +1393,36 @@ __global__ void __launch_bounds__(kThreads, 4) k_partition(FastParams P) {
   const int nseg = P.nseg;
   const int nb = border_units(P.gp);
   const int nsu = (P.gp.r_hi - P.gp.r_lo) * nseg;
-  const int nunits = nb + nsu + (P.gp.nB1 + 31) / 32;
+  const int ni = nsu + (P.gp.nB1 + 31) / 32;
+  const int T = BATCH ? P.ntiles : 1;
+  const int nunits = T * (nb + ni);
   LSE_TRACE_DECL
   for (;;) {
     const int unit = grab_unit(P, lane);
     LSE_TRACE_MARK(unit < nunits ? unit : -1);
     if (unit >= nunits) break;
+    int tile = 0, lu = unit;
+    bool part_t = PART;
+    if (BATCH) {
+      if (unit < T * nb) {
+        tile = unit / nb;
+        lu = unit - tile * nb;
+      } else {
+        const int iu = unit - T * nb;
+        tile = iu / ni;
+        lu = nb + (iu - tile * ni);
+      }
+      const Scalars* st = P.scal + tile;
+      part_t = PART && st->model != EDGE;
+      // converged tiles, and edge tiles off the checkpoints, have nothing to do
+      if (*(volatile const int*)&st->stop || (!part_t && !CKPT)) continue;
+    }
     LaneDelta d{0.0, 0.0, 0, 0, 0ull};
-    if (unit < nb) {
-      border_partition_unit<R, PART, CKPT, MASKONLY>(P, s_lt, s_ls, unit, eps_phi, d);
+    if (lu < nb) {
+      border_partition_unit<R, PART, CKPT, MASKONLY, BATCH>(P, s_lt, s_ls, lu, tile, part_t,
+                                                           eps_phi, d);
     } else {
-      const int iu = unit - nb;
+      const int iu = lu - nb;
       int r = 0, c0 = 0, c1 = 1, xb = 0;
       bool active = true, chunked = false;
       if (iu < nsu) {
@@ -1321,6 +1434,7 @@ __global__ void __launch_bounds__(kThreads, 4) k_partition(FastParams P) {
       } else {
         active = b1_lane(P.gp, iu - nsu, lane, r, xb);
       }
+      if (BATCH) r += tile * P.tile_hr;
       for (int ch = c0; ch < c1; ++ch) {
         const int x0 = chunked ? xb + ch * kChunk : xb;
         uint32_t pw[8], mw[8], prev[NT], cur[NT];
@@ -1346,9 +1460,10 @@ __global__ void __launch_bounds__(kThreads, 4) k_partition(FastParams P) {
           continue;
         } else {
           partition_block<R, true>(P, s_lt, s_ls, (uint32_t)__cvta_generic_to_shared(s_lt), r,
-                                   x0, eps_phi, prev, cur, pw, mw);
+                                   x0, eps_phi, prev, cur, pw, mw, tile);
         }
-        partition_commit<PART, CKPT, MASKONLY>(P, r, x0, pw, mw, d);
+        if (!BATCH || part_t == PART) partition_commit<PART, CKPT, MASKONLY>(P, r, x0, pw, mw, d, tile);
+        else partition_commit<false, CKPT, false>(P, r, x0, pw, mw, d, tile);
       }
     }
     if (MASKONLY) continue;

@@ -302,6 +302,37 @@ __global__ void __launch_bounds__(256) k_reduce_to_one(PartRanges R3, TilePartia
   reduce_slice(R3, 0, R3.n[0] + R3.n[1] + R3.n[2], out);
 }
 
+// batched tiles (lse_batch): stage 1 per tile (blockIdx.y = tile) over the
+// tile's partials in the single-run order [border units][interior units], so a
+// tile's reduction is the one it would get alone
+__global__ void __launch_bounds__(256) k_finalize_stage1_tiles(const TilePartial* part,
+                                                               TilePartial* out,
+                                                               const Scalars* scal, int nb,
+                                                               int ni, int T, int ckpt) {
+  const int t = blockIdx.y;
+  const Scalars* sc = scal + t;
+  if (*(volatile const int*)&sc->stop) return;
+  if (sc->model == EDGE && !ckpt) return;
+  PartRanges R3{{part + (size_t)t * nb, part + (size_t)T * nb + (size_t)t * ni, part},
+                {nb, ni, 0}};
+  const int n = nb + ni;
+  const int per = (n + gridDim.x - 1) / gridDim.x;
+  const int t0 = min(n, (int)blockIdx.x * per), t1 = min(n, t0 + per);
+  reduce_slice(R3, t0, t1, out + (size_t)t * gridDim.x + blockIdx.x);
+}
+
+__global__ void __launch_bounds__(64) k_finalize_run_tiles(const TilePartial* fin, Scalars* scal,
+                                                           int ckpt, long long iter) {
+  const int t = blockIdx.x;
+  Scalars* sc = scal + t;
+  if (*(volatile const int*)&sc->stop) return;
+  const bool region = sc->model != EDGE;
+  if (!region && !ckpt) return;
+  const TilePartial* f = fin + (size_t)t * kFinSlices;
+  PartRanges R1{{f, f, f}, {kFinSlices, 0, 0}};
+  finalize_cta(R1, sc, true, region, ckpt != 0, iter);
+}
+
 // per-iteration finalize of the fast path (DELTA partials); no-op once stopped
 __global__ void __launch_bounds__(64) k_finalize_run(PartRanges R3, Scalars* sc, int region,
                                                        int ckpt, long long iter) {
@@ -376,6 +407,26 @@ __global__ void k_widen(const float* __restrict__ in, double* __restrict__ out, 
   const int i = blockIdx.y;
   if (x >= W) return;
   out[(size_t)i * W + x] = (double)in[(size_t)i * pitch + x];
+}
+
+// 8-bit RGB -> the reference loader's grayscale (fileio.py:28-30, 88): luma
+// in float64, ((0.299 R + 0.587 G) + 0.114 B) / 255, no re-quantization.
+__global__ void k_luma(const unsigned char* __restrict__ rgb, double* __restrict__ out,
+                       long long n) {
+  const long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= n) return;
+  const double R = rgb[3 * i], G = rgb[3 * i + 1], B = rgb[3 * i + 2];
+  out[i] = ddiv(dadd(dadd(dmul(0.299, R), dmul(0.587, G)), dmul(0.114, B)), 255.0);
+}
+
+// Batched tiles: copy n words (or bytes, via uint32 units) from per-tile
+// source pointers into / out of the stacked arrays (blockIdx.y = tile).
+__global__ void k_tiles_copy(const uint32_t* const* srcs, uint32_t* const* dsts, long long n) {
+  const uint32_t* src = srcs[blockIdx.y];
+  uint32_t* dst = dsts[blockIdx.y];
+  for (long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x; i < n;
+       i += (long long)gridDim.x * blockDim.x)
+    dst[i] = src[i];
 }
 
 // Even-odd seed rasterization at pixel centres (grid.py:58-93), union of

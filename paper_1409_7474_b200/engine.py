@@ -202,16 +202,19 @@ class _DeviceRun:
                  max_iters=None, conv_check_every=None):
         p, wkeep = _native_params(params, max_iters, conv_check_every)
         h = C.c_void_p()
-        is_f32 = 1 if image.dtype == np.float32 else 0
+        if image.dtype == np.uint8 and image.ndim == 3 and image.shape[2] == 3:
+            fmt = N.LSE_IMAGE_RGB8       # decoded to the loader's luma on the device
+        else:
+            fmt = N.LSE_IMAGE_F32 if image.dtype == np.float32 else N.LSE_IMAGE_F64
         rc = N.lib.lse_run_create(C.byref(h), C.byref(p), image.shape[0], image.shape[1],
-                                  image.ctypes.data_as(C.c_void_p), is_f32, C.byref(init))
+                                  image.ctypes.data_as(C.c_void_p), fmt, C.byref(init))
         del keep, wkeep
         if rc == N.LSE_ERR_DEGENERATE_SEED:
             from .grid import DegenerateSeedError
             raise DegenerateSeedError(N.lib.lse_last_error().decode())
         N.check(rc)
         self.h = h
-        self.shape = image.shape
+        self.shape = image.shape[:2]
         self._finalizer = weakref.finalize(self, N.lib.lse_run_destroy, h)
 
     def advance(self, n):

@@ -115,6 +115,44 @@ def config2(size=1024):
                  "edge", 500)
 
 
+def config4_tile(k, size=1024, iters=300):
+    """C4 tile k: 8-bit RGB (H, W, 3) urban tile; even tiles region with +inside
+    seeds, odd tiles edge (sigma1 1.0, gain 255) with -inside seeds; centred
+    900^2 seed box.  Background U[40,90], rectangles
+    U[150,220], 10-16 px roads U[100,140], N(0, 6) noise, clipped to 0..255."""
+    rng = np.random.default_rng(4000 + k)
+    img = np.empty((size, size, 3), dtype=np.float64)
+    img[...] = rng.uniform(40, 90, size=3)
+    for _ in range(int(rng.integers(10, 25))):
+        sw, sh = (int(v) for v in rng.integers(24, max(25, size // 5), size=2))
+        x = int(rng.integers(0, max(1, size - sw)))
+        y = int(rng.integers(0, max(1, size - sh)))
+        img[y:y + sh, x:x + sw] = rng.uniform(150, 220, size=3)
+    for _ in range(int(rng.integers(2, 4))):
+        nv = int(rng.integers(2, 5))
+        pts = rng.uniform(0, size, size=(nv, 2))
+        width = float(rng.uniform(10, 16))
+        col = rng.uniform(100, 140, size=3)
+        for ch in range(3):
+            _draw_polyline(img[..., ch], pts, width, np.full((size, size), col[ch]))
+    img += rng.normal(0.0, 6.0, size=img.shape)
+    img = np.clip(np.rint(img), 0, 255).astype(np.uint8)
+    m = (size - min(900, size - 2)) // 2
+    region = k % 2 == 0
+    params = dict(dt=15.0, sigma2=1.0, ts_reg=9, max_iters=iters, conv_check_every=iters + 1)
+    if not region:
+        params.update(sigma1=1.0, ts_pre=9, edge_gain=255.0)
+    return Scene("C4", img, (box_polygon(m, m, size - m, size - m),), 1 if region else -1,
+                 params, "region" if region else "edge", iters, extra=dict(tile=k))
+
+
+def luma(rgb):
+    """The reference loader's grayscale of an 8-bit RGB array (fileio.py:28-30,
+    88): ((0.299 R + 0.587 G) + 0.114 B) / 255 in float64."""
+    x = np.asarray(rgb, dtype=np.float64)
+    return (0.299 * x[..., 0] + 0.587 * x[..., 1] + 0.114 * x[..., 2]) / 255.0
+
+
 def config5(size=32768, n_rects=20000, iters=500, seed_offset=0, rows=None):
     """C5: large panchromatic scene, 20000 rects 8-64 px, region, sigma 1.5.
 

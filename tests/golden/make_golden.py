@@ -238,6 +238,12 @@ def main():
             f"a4_{sign}", a1, SeedSpec(polygons=(square(28, 28, 100, 100),), inside_sign=sign),
             params(ModelKind.ZHANG, nu=1.0, max_iters=1000), [1000], store="hash")
 
+    # 8-bit RGB -> grayscale of the reference loader (fileio.py:28-30, 88)
+    from lsekit import fileio
+    rgb = np.random.default_rng(43).integers(0, 256, size=(16, 19, 3), dtype=np.uint8)
+    fixtures["luma"] = {"rgb": rgb,
+                        "luma": fileio._luma(np.asarray(rgb, dtype=np.float64)) / 255.0}
+
     only = set(sys.argv[1:])
     for name, arrs in fixtures.items():
         if only and name not in only:

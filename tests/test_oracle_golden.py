@@ -109,3 +109,10 @@ def test_oracle_trajectories_bit_exact(name):
     assert r.iteration == int(g["final_iteration"])
     assert r.converged == bool(g["converged"])
     assert r.degenerate == bool(g["degenerate"])
+
+
+def test_luma_restatement_matches_reference_loader():
+    """scenes.luma (the C4 decode the device restates) == fileio._luma / 255."""
+    from paper_1409_7474_b200 import scenes
+    g = load_golden("luma")
+    assert np.array_equal(scenes.luma(g["rgb"]), g["luma"])
