@@ -60,6 +60,8 @@ def parse():
     ap.add_argument("--strips-n1", action="store_true",
                     help="run the row-strip path (NCCL communicator) even at N = 1 "
                          "(launch under torch.distributed.run)")
+    ap.add_argument("--c4-tiles", type=int, default=512,
+                    help="tiles of the C4 batch measured alongside (0: skip the other configs)")
     ap.add_argument("--skip-steps", type=int, default=None,
                     help="steps of the uniform-window-skip measurement (default: --steps)")
     return ap.parse_args()
@@ -152,7 +154,7 @@ def cpu_oracle_rate(seconds, size=2048):
     t0 = time.perf_counter()
     r.advance(2)
     per_it = (time.perf_counter() - t0) / 2
-    n = int(max(2, min(200, seconds / max(per_it, 1e-6))))
+    n = int(max(2, min(5000, seconds / max(per_it, 1e-6))))
     t0 = time.perf_counter()
     r.advance(n)
     dt = time.perf_counter() - t0
@@ -196,6 +198,84 @@ def run_reference(args, rank):
                 "d2h_bytes_per_step": 0},
     }
     print(json.dumps(line), flush=True)
+
+
+# ------------------------------------------------- the other BASELINE configs
+def other_configs(steps, c4_tiles):
+    """C1 / C2 (single small images: L2-resident and launch-latency bound, the
+    HBM roofline does not bind them) and C4 (1024^2 8-bit RGB tiles, batched:
+    one launch per kernel per iteration for all tiles).  Device time of the
+    fixed-iteration evolution, inputs resident, dense pass."""
+    import torch
+    from paper_1409_7474_b200 import _native as N, scenes
+    from paper_1409_7474_b200 import default_params, ModelKind, SeedSpec
+    from paper_1409_7474_b200.batch import TileBatch, _tile_run
+    from paper_1409_7474_b200.engine import _native_params, _phi0_polygons
+    out = {}
+    for sc in (scenes.config1(), scenes.config2()):
+        prm = default_params(ModelKind.from_name(sc.model), **sc.params)
+        p, keep = _native_params(prm)
+        init, ikeep = _phi0_polygons(SeedSpec(polygons=sc.polygons, inside_sign=sc.inside_sign))
+        img = np.ascontiguousarray(sc.image)
+        h = C.c_void_p()
+        N.check(N.lib.lse_run_create(C.byref(h), C.byref(p), img.shape[0], img.shape[1],
+                                     img.ctypes.data_as(C.c_void_p), 1, C.byref(init)))
+        N.check(N.lib.lse_run_set_option(h, b"skip_uniform", 0))
+        st = N.LseStatus()
+
+        def job():
+            N.check(N.lib.lse_run_set_state(h, C.byref(init)))
+            N.check(N.lib.lse_run_advance(h, sc.iters, C.byref(st)))
+
+        for _ in range(2):
+            job()
+        ms = C.c_double()
+        N.check(N.lib.lse_run_begin_timing(h))
+        for _ in range(steps):
+            job()
+        N.check(N.lib.lse_run_end_timing(h, C.byref(ms)))
+        N.lib.lse_run_destroy(h)
+        npx = img.shape[0] * img.shape[1]
+        out[sc.name] = {"value": npx * sc.iters * steps / (ms.value / 1e3) / 1e9,
+                        "unit": "Gpix-it/s", "ms_per_job": ms.value / steps,
+                        "workload": f"{sc.name}: {img.shape[0]}^2 {sc.model}, {sc.iters} its",
+                        "bound": "launch latency / L2 (not HBM)"}
+    if c4_tiles > 0:
+        base = [scenes.config4_tile(k, 1024, 300) for k in range(min(16, c4_tiles))]
+        sc = [base[k % len(base)] for k in range(c4_tiles)]   # tile k keeps k's model parity
+        t0 = time.perf_counter()
+        runs = [_tile_run(s.image, SeedSpec(polygons=s.polygons, inside_sign=s.inside_sign),
+                          default_params(ModelKind.from_name(s.model), **s.params)) for s in sc]
+        t_create = time.perf_counter() - t0
+        inits = [_phi0_polygons(SeedSpec(polygons=s.polygons, inside_sign=s.inside_sign))
+                 for s in sc]
+        for r in runs:
+            r.set_native_option("skip_uniform", 0)
+        tb = TileBatch(runs)
+
+        def reset():
+            for r, (init, _) in zip(runs, inits):
+                N.check(N.lib.lse_run_set_state(r._dev.h, C.byref(init)))
+            torch.cuda.synchronize()
+
+        reset()
+        tb.advance(300)                                     # warm-up
+        times = []
+        for _ in range(steps):
+            reset()
+            t0 = time.perf_counter()
+            tb.advance(300)
+            times.append(time.perf_counter() - t0)
+        t = sum(times) / len(times)
+        out["C4"] = {"value": c4_tiles * 1024 * 1024 * 300 / t / 1e9, "unit": "Gpix-it/s",
+                     "ms_per_job": t * 1e3, "tiles": c4_tiles,
+                     "workload": f"C4: {c4_tiles} x 1024^2 8-bit RGB tiles (luma decoded on "
+                                 "device), region/edge alternating, 300 its, one batch",
+                     "tile_setup_s": round(t_create, 2),
+                     "bound": "hbm (same kernels as C5)"}
+        tb.close()
+        del runs
+    return out
 
 
 # ----------------------------------------------------------------- GPU side
@@ -406,6 +486,10 @@ def main():
             "update_ms": t_upd, "partition_ms": t_part,
             "update_share_of_iteration": t_upd / t_iter if t_iter > 0 else None}
 
+    others = None
+    if rank == 0 and ws == 1 and args.c4_tiles > 0:
+        others = other_configs(max(1, min(args.steps, 3)), args.c4_tiles)
+
     cpu = None
     if rank == 0 and ws == 1 and not args.no_cpu_baseline:
         rate, cores, sample = cpu_oracle_rate(args.cpu_seconds)
@@ -428,7 +512,7 @@ def main():
                                        else "single GPU"),
                        "l2": "inputs (4.3 GB image) larger than L2"},
             "roofline": roof, "cpu_baseline": cpu, "e2e": e2e, "gpu_launches": int(launches),
-            "uniform_skip": skip,
+            "uniform_skip": skip, "other_configs": others,
             "clocks": clk, "exact_fallbacks": int(fallbacks),
             "scene_gen_s": round(t_gen, 2),
         }
