@@ -19,7 +19,7 @@
 extern "C" {
 #endif
 
-#define LSE_ABI_VERSION 3
+#define LSE_ABI_VERSION 4
 
 #define LSE_OK 0
 #define LSE_ERR_ARG 1            /* ValueError in the reference               */
@@ -33,6 +33,8 @@ extern "C" {
 #define LSE_MODEL_EDGE 0         /* ModelKind.EDGE   (models.py:30)  E_Td, Eq. 14 */
 #define LSE_MODEL_REGION 1       /* ModelKind.REGION (models.py:31)  R_Td, Eq. 17 */
 #define LSE_MODEL_ZHANG 2        /* ModelKind.ZHANG  (models.py:33)  mean separation (models.py:144-162) */
+#define LSE_MODEL_BANDS 3        /* region data term summed over n_bands bands (
+                                    a restatement -- the reference is single-band) */
 
 /* EvolutionParams + ModelParams (engine.py:40-81, models.py:44-68).  The
  * Gaussian 1-D weights are passed in exactly as
@@ -54,6 +56,7 @@ typedef struct lse_params {
   const double* reg_weights; /* ts_reg values */
   const double* pre_weights; /* ts_pre values (edge model) */
   double nu;                 /* ModelParams.nu (zhang model speed constant) */
+  int n_bands;               /* LSE_MODEL_BANDS: bands of the image (1..4), band-major */
 } lse_params;
 
 #define LSE_PHI0_FIELD 0     /* float64 (H, W) level-set field                 */

@@ -255,6 +255,29 @@ def region_velocity(image: np.ndarray, phi: np.ndarray):
     return (data / peak) * gradient_magnitude(phi), False
 
 
+def region_velocity_bands(image: np.ndarray, phi: np.ndarray):
+    """Multi-band region data term -- a restatement, the
+    reference is single-band (grid.py:27-28): D = sum_k (c+_k - c-_k)(2 I_k -
+    c+_k - c-_k), bands accumulated in order, then models.py:109-119.  With one
+    band this is region_velocity exactly (its parity is pinned by that)."""
+    image = np.asarray(image, dtype=np.float64)
+    if image.ndim == 2:
+        image = image[None]
+    pos = phi >= 0.0
+    n_pos = int(pos.sum())
+    if n_pos == 0 or n_pos == pos.size:
+        return np.zeros_like(phi), True
+    data = None
+    for band in image:
+        c_plus, c_minus = float(band[pos].mean()), float(band[~pos].mean())
+        term = (c_plus - c_minus) * (2.0 * band - c_plus - c_minus)
+        data = term if data is None else data + term
+    peak = float(np.abs(data).max())
+    if peak == 0.0:
+        return np.zeros_like(phi), True
+    return (data / peak) * gradient_magnitude(phi), False
+
+
 def zhang_velocity(image: np.ndarray, phi: np.ndarray, nu: float):
     """models.py:144-162 -- nu * ((I - m) / max|I - m|) * |grad phi|, m = (c+ + c-)/2."""
     means = region_means(image, phi)
@@ -296,6 +319,8 @@ def advance_once(phi, iteration, image, p: OracleParams, g, w_reg):
         v, degenerate = edge_velocity(g, phi), False
     elif p.model == ZHANG:
         v, degenerate = zhang_velocity(image, phi, p.nu)
+    elif image.ndim == 3:
+        v, degenerate = region_velocity_bands(image, phi)
     else:
         v, degenerate = region_velocity(image, phi)
     out = phi + p.dt * v

@@ -28,6 +28,7 @@ LSE_ERR_UNSUPPORTED = 7
 LSE_MODEL_EDGE = 0
 LSE_MODEL_REGION = 1
 LSE_MODEL_ZHANG = 2
+LSE_MODEL_BANDS = 3
 LSE_PARTIAL_BYTES = 64
 LSE_IMAGE_F64, LSE_IMAGE_F32, LSE_IMAGE_RGB8 = 0, 1, 2
 
@@ -45,7 +46,7 @@ class LseParams(C.Structure):
                 ("max_iters", C.c_longlong), ("conv_check_every", C.c_longlong),
                 ("conv_window", C.c_longlong), ("sigma1", C.c_double), ("ts_pre", C.c_int),
                 ("edge_gain", C.c_double), ("reg_weights", _dp), ("pre_weights", _dp),
-                ("nu", C.c_double)]
+                ("nu", C.c_double), ("n_bands", C.c_int)]
 
 
 class LsePhi0(C.Structure):

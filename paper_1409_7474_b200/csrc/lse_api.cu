@@ -121,6 +121,13 @@ struct lse_run {
   float* d_data32 = nullptr;
   double* d_data64 = nullptr;
   bool fp32_exact = true;
+  // multi-band runs (LSE_MODEL_BANDS): band planes; d_data32 then holds the
+  // per-pass data term D written by k_band_peak
+  int nbands = 1;
+  float* d_bands32 = nullptr;
+  double* d_bands64 = nullptr;
+  uint32_t* d_chg = nullptr;
+  TilePartial* d_bpart = nullptr;
   double img_absmax = 0.0;
   // state
   uint32_t* d_bits[2] = {nullptr, nullptr};
@@ -182,6 +189,11 @@ struct lse_run {
 
 namespace {
 
+bool two_mean(int model) {
+  return model == LSE_MODEL_REGION || model == LSE_MODEL_ZHANG || model == LSE_MODEL_BANDS;
+}
+bool is_bands(const lse_run* r) { return r->p.model == LSE_MODEL_BANDS; }
+
 FastParams fast_params(lse_run* r) {
   FastParams P{};
   P.pbits = r->d_P;
@@ -209,6 +221,7 @@ FastParams fast_params(lse_run* r) {
   P.gp = r->gp;
   P.own_lo = r->own_lo;
   P.own_hi = r->own_hi;
+  P.chg = is_bands(r) ? r->d_chg : nullptr;
   P.ntiles = 1;
   P.tile_hr = r->g.HR;
   P.tile_h = r->H;
@@ -261,13 +274,22 @@ int launch_partition_abs(lse_run* r, int src, bool part, bool ckpt, bool mask_on
   return LSE_OK;
 }
 
-bool two_mean(int model) { return model == LSE_MODEL_REGION || model == LSE_MODEL_ZHANG; }
 
 // partition sums / coefficients for the current state (region / zhang models)
+int band_chain(lse_run* r, bool absolute, bool ckpt, long long it);
+
 int prepare(lse_run* r) {
   if (r->prepared) return LSE_OK;
   TRY(upload_ctx(r));
-  if (two_mean(r->p.model)) {
+  if (is_bands(r)) {
+    if (r->mode != SRC_SCALED || r->field_valid)
+      return fail(LSE_ERR_UNSUPPORTED, "multi-band runs start from seeds or signs");
+    const dim3 gr((r->g.pitch_w + 1023) / 1024, r->g.HR);
+    k_partition_init_bits<<<gr, 256, 0, r->st>>>(r->d_bits[r->cur], r->d_ctx, r->d_P,
+                                                 r->d_part_init, r->g, r->own_lo, r->own_hi);
+    CKL();
+    TRY(band_chain(r, true, false, r->iteration));
+  } else if (two_mean(r->p.model)) {
     if (r->mode == SRC_SCALED && !r->field_valid) {
       // +-s state: P = b; coalesced double-double sums, one partial per CTA
       const dim3 gr((r->g.pitch_w + 1023) / 1024, r->g.HR);
@@ -407,9 +429,15 @@ int launch_partition(lse_run* r, FastParams P) {
     // two-stage fixed-order reduction of all unit partials -> the next
     // update's coefficients (64 CTAs reduce contiguous slices, 1 CTA the rest)
     PartRanges R3{{r->d_part, r->d_part, r->d_part}, {(int)n, 0, 0}};
-    k_finalize_stage1<<<kFinSlices, 256, 0, r->st>>>(R3, r->d_part_fin, r->d_scal);
-    CKL();
+    if (!is_bands(r)) {
+      k_finalize_stage1<<<kFinSlices, 256, 0, r->st>>>(R3, r->d_part_fin, r->d_scal);
+      CKL();
+    }
     PartRanges R1{{r->d_part_fin, r->d_part_fin, r->d_part_fin}, {kFinSlices, 0, 0}};
+    if (is_bands(r)) {
+      TRY(band_chain(r, false, CKPT, P.iter));
+      return LSE_OK;
+    }
     if (r->strip) {
       // row strips: this rank's contribution; the ranks exchange it and
       // finalize together (lse_strip_finalize)
@@ -540,6 +568,9 @@ bool fp32_ok(lse_run* r) {
 }
 
 int generic_iteration(lse_run* r, long long it, bool reinit_now, bool reg_now, bool ckpt) {
+  if (is_bands(r))
+    return fail(LSE_ERR_UNSUPPORTED, "multi-band runs need the binary-state fast path "
+                                     "(reinit_period = reg_period = 1, 3 <= ts_reg <= 9)");
   TRY(ensure_generic(r));
   TRY(materialize(r));
   CK(cudaMemsetAsync(&r->d_scal->nonfinite, 0, sizeof(int), r->st));
@@ -601,6 +632,97 @@ int generic_iteration(lse_run* r, long long it, bool reinit_now, bool reg_now, b
   r->generic_iters++;
   TRY(collect(r));
   return LSE_OK;
+}
+
+// multi-band runs: the pass after each partition -- band sums over the
+// changed pixels (or all pixels), per-band means, the data term D of every
+// pixel (fp32 plane for the fused kernels) and its peak, the coefficients
+int band_chain(lse_run* r, bool absolute, bool ckpt, long long it) {
+  const dim3 gr((r->g.pitch_w + 1023) / 1024, r->g.HR);
+  const int nblk = (int)(gr.x * gr.y);
+  if (absolute)
+    k_band_sums<true><<<gr, 256, 0, r->st>>>(nullptr, r->d_P, r->d_ctx, r->d_bpart, r->g,
+                                             r->d_scal);
+  else
+    k_band_sums<false><<<gr, 256, 0, r->st>>>(r->d_chg, r->d_P, r->d_ctx, r->d_bpart, r->g,
+                                              r->d_scal);
+  CKL();
+  const int n = (int)(r->nb_part + r->ni_part);
+  PartRanges M{{r->d_part, r->d_part, r->d_part}, {ckpt ? n : 0, 0, 0}};
+  k_finalize_bands<<<1, 256, 0, r->st>>>(r->d_bpart, nblk, M, r->d_scal, absolute ? 1 : 0,
+                                         ckpt ? 1 : 0, it);
+  CKL();
+  k_band_peak<<<dim3((r->W + 255) / 256, std::min(r->H, 512)), 256, 0, r->st>>>(
+      r->d_ctx, r->d_scal, r->d_data32, r->g);
+  CKL();
+  k_band_coeffs<<<1, 1, 0, r->st>>>(r->d_scal);
+  CKL();
+  return LSE_OK;
+}
+
+// multi-band image: n_bands planes (band-major, each H x W), float32 or float64
+int upload_bands(lse_run* r, const void* image, int fmt) {
+  if (fmt != LSE_IMAGE_F32 && fmt != LSE_IMAGE_F64)
+    return fail(LSE_ERR_ARG, "multi-band images are float32 or float64 planes");
+  const int H = r->H, W = r->W, K = r->nbands;
+  const long long pitch = r->g.data_pitch, stride = pitch * H;
+  int* d_flag = nullptr;
+  double* tmp64 = nullptr;
+  TRY(dalloc(&d_flag, 1));
+  CK(cudaMemsetAsync(d_flag, 0, sizeof(int), r->st));
+  if (fmt == LSE_IMAGE_F32) {
+    for (int k = 0; k < K; ++k)
+      CK(cudaMemcpy2DAsync(r->d_bands32 + k * stride, pitch * sizeof(float),
+                           (const float*)image + (size_t)k * H * W, W * sizeof(float),
+                           W * sizeof(float), H, cudaMemcpyHostToDevice, r->st));
+  } else {
+    TRY(dalloc(&tmp64, (size_t)K * H * W));
+    CK(cudaMemcpyAsync(tmp64, image, (size_t)K * H * W * sizeof(double), cudaMemcpyHostToDevice,
+                       r->st));
+    for (int k = 0; k < K; ++k) {
+      k_to_f32<<<grid2(W, H), 128, 0, r->st>>>(tmp64 + (size_t)k * H * W,
+                                               r->d_bands32 + k * stride, H, W, pitch, d_flag);
+      CKL();
+    }
+  }
+  int inexact = 0;
+  CK(cudaMemcpyAsync(&inexact, d_flag, sizeof(int), cudaMemcpyDeviceToHost, r->st));
+  CK(cudaStreamSynchronize(r->st));
+  if (inexact) {
+    if (!r->d_bands64) TRY(dalloc(&r->d_bands64, (size_t)K * stride));
+    for (int k = 0; k < K; ++k) {
+      k_pitch64<<<grid2(W, H), 128, 0, r->st>>>(tmp64 + (size_t)k * H * W,
+                                                r->d_bands64 + k * stride, H, W, pitch);
+      CKL();
+    }
+  } else if (r->d_bands64) {
+    cudaFree(r->d_bands64);
+    r->d_bands64 = nullptr;
+  }
+  // max |I| over the bands (fp32 guard preconditions)
+  double absmax = 0.0;
+  for (int k = 0; k < K; ++k) {
+    long long init[3] = {LLONG_MAX, LLONG_MIN, LLONG_MIN};
+    CK(cudaMemcpyAsync(r->d_keys, init, sizeof(init), cudaMemcpyHostToDevice, r->st));
+    k_minmax<<<std::min(H, num_sms() * 8), 256, 0, r->st>>>(
+        r->d_bands32 + k * stride, r->d_bands64 ? r->d_bands64 + k * stride : nullptr, H, W,
+        pitch, r->d_keys);
+    CKL();
+    k_store_minmax<<<1, 1, 0, r->st>>>(r->d_keys, r->d_scal);
+    CKL();
+    CK(cudaMemcpyAsync(r->h_scal, r->d_scal, sizeof(Scalars), cudaMemcpyDeviceToHost, r->st));
+    CK(cudaStreamSynchronize(r->st));
+    absmax = std::max(absmax, r->h_scal->img_absmax);
+  }
+  r->img_absmax = absmax;
+  if (tmp64) cudaFree(tmp64);
+  cudaFree(d_flag);
+  r->fp32_exact = !inexact;
+  r->h_ctx.data32 = r->d_data32;
+  r->h_ctx.data64 = nullptr;
+  r->h_ctx.bands32 = r->d_bands32;
+  r->h_ctx.bands64 = r->d_bands64;
+  return upload_ctx(r);
 }
 
 void fill_status(lse_run* r, lse_status* s, long long instab) {
@@ -850,6 +972,15 @@ int create_impl(lse_run** out, const lse_params* p, long long height, long long 
   if (p->ts_reg < 1 || p->ts_reg % 2 == 0 || !p->reg_weights)
     return fail(LSE_ERR_ARG, "ts_reg must be an odd number >= 1");
   if (p->ts_reg > 63) return fail(LSE_ERR_ARG, "ts_reg > 63 is not supported");
+  if (p->model == LSE_MODEL_BANDS) {
+    if (p->n_bands < 1 || p->n_bands > kMaxBands)
+      return fail(LSE_ERR_ARG, "n_bands must be 1..4");
+    if (p->reinit_period != 1 || p->reg_period != 1 || p->ts_reg < 3 || p->ts_reg > 9)
+      return fail(LSE_ERR_UNSUPPORTED, "multi-band runs need the binary-state fast path "
+                                       "(reinit_period = reg_period = 1, 3 <= ts_reg <= 9)");
+    if (init->kind == LSE_PHI0_FIELD)
+      return fail(LSE_ERR_UNSUPPORTED, "multi-band runs start from seeds or signs");
+  }
   if (p->model == LSE_MODEL_EDGE && (p->ts_pre < 1 || p->ts_pre % 2 == 0 || !p->pre_weights))
     return fail(LSE_ERR_ARG, "ts_pre must be an odd number >= 1");
   TRY(check_device());
@@ -925,6 +1056,11 @@ int create_impl(lse_run** out, const lse_params* p, long long height, long long 
       (rc = dalloc(&r->d_part_fin, kFinSlices)) ||
       (rc = dalloc(&r->d_part_init, (size_t)r->g.HR * ((r->g.pitch_w + 1023) / 1024))))
     return cleanup(rc);
+  if (p->model == LSE_MODEL_BANDS &&
+      ((rc = dalloc(&r->d_bands32, (size_t)p->n_bands * r->g.data_pitch * r->H)) ||
+       (rc = dalloc(&r->d_chg, nbits)) ||
+       (rc = dalloc(&r->d_bpart, (size_t)p->n_bands * r->g.HR * ((r->g.pitch_w + 1023) / 1024)))))
+    return cleanup(rc);
   if (cudaMallocHost((void**)&r->h_scal, sizeof(Scalars)) != cudaSuccess)
     return cleanup(fail(LSE_ERR_CUDA, "pinned alloc failed"));
   cudaMemsetAsync(r->d_work, 0, sizeof(unsigned long long), r->st);
@@ -943,7 +1079,10 @@ int create_impl(lse_run** out, const lse_params* p, long long height, long long 
   r->h_ctx.dt = p->dt;
   r->h_ctx.scale = 1.0;
   r->h_ctx.scal = r->d_scal;
-  r->h_ctx.model = p->model == LSE_MODEL_REGION ? REGION : p->model == LSE_MODEL_ZHANG ? ZHANG : EDGE;
+  r->h_ctx.model = p->model == LSE_MODEL_REGION  ? REGION
+                   : p->model == LSE_MODEL_ZHANG ? ZHANG
+                   : p->model == LSE_MODEL_BANDS ? VECTOR
+                                                 : EDGE;
   cudaMemcpyAsync(r->d_w64, r->h_ctx.w64, 32 * sizeof(double), cudaMemcpyHostToDevice, r->st);
   // LUTs for the fast path (R <= 4)
   if (r->R >= 1 && r->R <= 4) {
@@ -967,13 +1106,21 @@ int create_impl(lse_run** out, const lse_params* p, long long height, long long 
   s0.dt = p->dt;
   s0.model = r->h_ctx.model;
   s0.nu = p->nu;
+  s0.nbands = p->model == LSE_MODEL_BANDS ? p->n_bands : 1;
   s0.conv_window = p->conv_window;
   s0.eps_phi = (float)kEpsPhi;
   s0.eps_u = (float)edge_eps_u(p->dt);
   if (p->model == LSE_MODEL_EDGE) s0.A = 1.0f;   // vf = 1 * g + 0 in a batched launch
   if (cudaMemcpyAsync(r->d_scal, &s0, sizeof(s0), cudaMemcpyHostToDevice, r->st) != cudaSuccess)
     return cleanup(fail(LSE_ERR_CUDA, "scalar upload failed"));
-  if ((rc = upload_image(r, image, image_is_f32))) return cleanup(rc);
+  if (p->model == LSE_MODEL_BANDS) {
+    r->nbands = p->n_bands;
+    r->h_ctx.nbands = p->n_bands;
+    r->h_ctx.band_stride = (long long)r->g.data_pitch * r->H;
+    if ((rc = upload_bands(r, image, image_is_f32))) return cleanup(rc);
+  } else if ((rc = upload_image(r, image, image_is_f32))) {
+    return cleanup(rc);
+  }
   if ((rc = set_state(r, init))) return cleanup(rc);
   *out = r;
   return LSE_OK;
@@ -996,6 +1143,8 @@ int lse_strip_create(lse_run** out, const lse_params* p, long long height, long 
                 "3 <= ts_reg <= 9)");
   if (init->kind == LSE_PHI0_FIELD)
     return fail(LSE_ERR_UNSUPPORTED, "row strips start from seeds or signs");
+  if (p->model == LSE_MODEL_BANDS)
+    return fail(LSE_ERR_UNSUPPORTED, "multi-band runs are single-GPU");
   const long long HR = (height + 31) / 32;
   if (own_lo < 0 || own_lo > 1 || own_hi <= own_lo || own_hi > HR || own_hi < HR - 1)
     return fail(LSE_ERR_ARG, "a strip owns all its word-rows but at most one halo row per side");
@@ -1104,6 +1253,11 @@ int lse_run_geometry(lse_run* r, int* word_rows, int* pitch_words) {
 
 int lse_run_load_image(lse_run* r, const void* image, int image_is_f32) {
   if (!r || !image) return fail(LSE_ERR_ARG, "null argument");
+  if (is_bands(r)) {
+    TRY(upload_bands(r, image, image_is_f32));
+    r->prepared = false;                         // the data term depends on the bands
+    return LSE_OK;
+  }
   return upload_image(r, image, image_is_f32);
 }
 
@@ -1395,6 +1549,7 @@ int lse_batch_create(lse_batch** out, lse_run* const* runs, int n) {
       return fail(LSE_ERR_ARG, "batch tiles must share size and evolution parameters");
     if (r->p.reinit_period != 1 || r->p.reg_period != 1 || r->R < 1 || r->R > 4)
       return fail(LSE_ERR_UNSUPPORTED, "batches run the binary-state fast path only");
+    if (is_bands(r)) return fail(LSE_ERR_UNSUPPORTED, "multi-band runs are not batched");
   }
   lse_batch* b = new lse_batch();
   b->runs.assign(runs, runs + n);
@@ -1568,7 +1723,8 @@ void lse_batch_destroy(lse_batch* b) {
 void lse_run_destroy(lse_run* r) {
   if (!r) return;
   if (r->st) cudaStreamSynchronize(r->st);
-  void* ptrs[] = {r->d_work, r->d_part_fin, r->d_part_init, r->d_data32, r->d_data64, r->d_bits[0], r->d_bits[1], r->d_P, r->d_M,
+  void* ptrs[] = {r->d_bands32, r->d_bands64, r->d_chg, r->d_bpart,
+                  r->d_work, r->d_part_fin, r->d_part_init, r->d_data32, r->d_data64, r->d_bits[0], r->d_bits[1], r->d_P, r->d_M,
                   r->d_mask, r->d_part, r->d_scal, r->d_lut_t, r->d_lut_s, r->d_ctx,
                   r->d_w64, r->d_keys, r->d_count, r->d_F[0], r->d_F[1], r->d_U, r->d_T};
   for (void* q : ptrs)

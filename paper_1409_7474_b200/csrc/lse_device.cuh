@@ -21,7 +21,10 @@ constexpr int kThreads = 128;            // threads per CTA of the tiled kernels
 constexpr int kColsPerThread = 8;        // columns per thread (one 32-row word each)
 constexpr int kSpanMax = kColsPerThread * kThreads + 16;
 
-enum Model : int { EDGE = 0, REGION = 1, ZHANG = 2 };   // ZHANG runs the REGION kernels
+// ZHANG and VECTOR run the REGION kernels (their data term is an affine image
+// of one fp32 data plane); VECTOR = region data term summed over K bands
+enum Model : int { EDGE = 0, REGION = 1, ZHANG = 2, VECTOR = 3 };
+constexpr int kMaxBands = 4;
 enum Src : int { SRC_SMOOTH = 0, SRC_SCALED = 1, SRC_FIELD = 2 };
 
 // Per-run scalars shared by the kernels of one run (device resident).
@@ -30,6 +33,11 @@ struct __align__(16) Scalars {
   long long n_pos, n_total;
   double c_pos, c_neg, dc, peak;      // region coefficients of the next update (models.py:109-118)
   double mid, nu;                     // zhang: m = (c+ + c-)/2, speed constant (models.py:152-162)
+  // vector (multi-band) region model: per-band running sums and means
+  double bsp_hi[kMaxBands], bsp_lo[kMaxBands], bsn_hi[kMaxBands], bsn_lo[kMaxBands];
+  double bcp[kMaxBands], bcm[kMaxBands];
+  unsigned long long peak_bits;       // max |D| of the current pass (ordered double bits)
+  int nbands, pad2_;
   double img_min, img_max, img_absmax;
   float A, B, eps_u, eps_phi;         // fp32 fast path: D/peak ~= A*I + B ; near-tie guards
   int zero_vel;                       // next update has v == 0 (degenerate, models.py:111-118)

@@ -37,6 +37,10 @@ struct ExactCtx {
   double scale;           // +-scale state (SRC_SCALED)
   Scalars* scal;
   int model;
+  int nbands;             // VECTOR: bands of the image (band-major planes)
+  const float* bands32;   // VECTOR: fp32 band planes (data_pitch rows)
+  const double* bands64;  // VECTOR: exact band planes (nullptr -> bands32 exact)
+  long long band_stride;  // elements per band plane
 };
 
 struct FastParams {
@@ -66,6 +70,7 @@ struct FastParams {
   unsigned long long work_base;  // value of *work when this launch started
   int own_lo, own_hi;        // word-rows whose pixels count in the partials (row strips)
   unsigned long long* trace; // LSE_UNIT_TRACE builds: (start, end) ns of every unit
+  uint32_t* chg;             // multi-band runs: changed-partition bits of this pass
   // batched tiles (lse_batch): ntiles equal tiles stacked in the arrays above,
   // tile t at word-row t * tile_hr; scal / ctx are per-tile arrays and gu / gp
   // the geometry of one tile (single runs: ntiles = 1, tile 0 is the image)
@@ -135,6 +140,34 @@ __device__ __forceinline__ double exact_v_twomean(const Scalars* sc, double I, d
   return dmul(ddiv(D, sc->peak), h);
 }
 
+// Band value k at (i, x) exactly.
+__device__ __forceinline__ double band_exact(const ExactCtx* c, int k, int i, int x) {
+  const size_t o = (size_t)k * c->band_stride + (size_t)i * c->data_pitch + x;
+  return c->bands64 ? c->bands64[o] : (double)c->bands32[o];
+}
+
+// Multi-band data term D = sum_k (c+_k - c-_k)(2 I_k - c+_k - c-_k), bands
+// accumulated left to right (oracle/lse_oracle.py region_velocity_bands; K = 1
+// is region_velocity's D exactly).
+__device__ __forceinline__ double vector_D(const ExactCtx* c, const Scalars* sc, int i, int x) {
+  double D = 0.0;
+  for (int k = 0; k < c->nbands; ++k) {
+    const double I = band_exact(c, k, i, x);
+    const double cp = sc->bcp[k], cm = sc->bcm[k];
+    const double t = dmul(dsub(cp, cm), dsub(dsub(dmul(2.0, I), cp), cm));
+    D = k == 0 ? t : dadd(D, t);
+  }
+  return D;
+}
+
+// exact velocity factor of any two-mean model at (i, x), h = |grad phi|
+__device__ __forceinline__ double exact_v_at(const ExactCtx* c, int i, int x, double h) {
+  const Scalars* sc = c->scal;
+  if (sc->zero_vel) return 0.0;
+  if (c->model == VECTOR) return dmul(ddiv(vector_D(c, sc, i, x), sc->peak), h);
+  return exact_v_twomean(sc, data_exact(c, i, x), h);
+}
+
 __device__ __noinline__ double exact_phi(const ExactCtx* c, const uint32_t* bits, int src, int i, int x) {
   if (src == SRC_SCALED) return get_bit(bits, c->pitch_w, i, x) ? c->scale : -c->scale;
   return exact_phi_smooth(bits, c->pitch_w, c->H, c->W, c->R, c->w64, i, x);
@@ -156,7 +189,7 @@ __device__ __noinline__ double exact_u(const ExactCtx* c, const uint32_t* bits, 
   double v;
   const Scalars* sc = c->scal;
   if (c->model != EDGE) {
-    v = exact_v_twomean(sc, sc->zero_vel ? 0.0 : data_exact(c, i, x), h);
+    v = exact_v_at(c, i, x, h);
   } else {
     v = dmul(data_exact(c, i, x), h);
   }
@@ -258,7 +291,7 @@ __device__ __noinline__ double exact_u_fast(const ExactCtx* c, const uint32_t* b
   double v;
   const Scalars* sc = c->scal;
   if (c->model != EDGE) {
-    v = exact_v_twomean(sc, sc->zero_vel ? 0.0 : data_exact(c, i, x), h);
+    v = exact_v_at(c, i, x, h);
   } else {
     v = dmul(data_exact(c, i, x), h);
   }
@@ -1241,6 +1274,18 @@ __device__ __forceinline__ void partition_commit(const FastParams& P, int r, int
     const uint4 o1 = reinterpret_cast<const uint4*>(P.pbits + base)[1];
     const uint32_t old[8] = {o0.x, o0.y, o0.z, o0.w, o1.x, o1.y, o1.z, o1.w};
     uint32_t any = 0u;
+    if (P.chg) {
+      // multi-band runs: record the changed pixels; k_band_sums folds every
+      // band's sums over them (the fused kernel keeps one band's registers)
+      uint32_t cw[8];
+#pragma unroll
+      for (int c = 0; c < 8; ++c) {
+        cw[c] = own ? old[c] ^ pw[c] : 0u;
+        any |= cw[c];
+      }
+      reinterpret_cast<uint4*>(P.chg + base)[0] = make_uint4(cw[0], cw[1], cw[2], cw[3]);
+      reinterpret_cast<uint4*>(P.chg + base)[1] = make_uint4(cw[4], cw[5], cw[6], cw[7]);
+    } else {
 #pragma unroll
     for (int c = 0; c < 8; ++c) {
       uint32_t chg = old[c] ^ pw[c];
@@ -1253,6 +1298,7 @@ __device__ __forceinline__ void partition_commit(const FastParams& P, int r, int
         if ((pw[c] >> b) & 1u) { d.a_in += I; ++d.n_in; }
         else { d.a_out += I; ++d.n_out; }
       }
+    }
     }
     if (any) {
       reinterpret_cast<uint4*>(P.pbits + base)[0] = make_uint4(pw[0], pw[1], pw[2], pw[3]);

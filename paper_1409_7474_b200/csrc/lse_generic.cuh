@@ -409,6 +409,177 @@ __global__ void k_widen(const float* __restrict__ in, double* __restrict__ out, 
   out[(size_t)i * W + x] = (double)in[(size_t)i * pitch + x];
 }
 
+// ---------------------------------------------------- multi-band (VECTOR)
+// Per-band sums of the pixels that changed side (ABS = false: chg bits,
+// split by the new partition bit) or of every pixel (ABS = true: split by P),
+// one double-double partial per (word-row, 1024-column block) and band, in a
+// fixed order.  Partial layout: part[k * nblk + blk], k = band.
+template <bool ABS>
+__global__ void __launch_bounds__(256) k_band_sums(const uint32_t* __restrict__ chg,
+                                                   const uint32_t* __restrict__ pbits,
+                                                   const ExactCtx* c, TilePartial* part,
+                                                   RunGeom g, const Scalars* sc) {
+  if (!ABS && *(volatile const int*)&sc->stop) return;
+  __shared__ TilePartial s_w[kMaxBands][8];
+  const int r = blockIdx.y;
+  const int nblk = gridDim.x * gridDim.y, blk = r * gridDim.x + blockIdx.x;
+  const int K = c->nbands;
+  double ah[kMaxBands], al[kMaxBands], bh[kMaxBands], bl[kMaxBands];
+  long long na = 0, nb = 0;
+#pragma unroll
+  for (int k = 0; k < kMaxBands; ++k) ah[k] = al[k] = bh[k] = bl[k] = 0.0;
+  for (int j = 0; j < 4; ++j) {
+    const int x = blockIdx.x * 1024 + j * 256 + threadIdx.x;
+    if (x >= g.W) continue;
+    const size_t o = (size_t)r * g.pitch_w + x;
+    const uint32_t p = pbits[o];
+    uint32_t m = ABS ? 0xffffffffu : chg[o];
+    if (ABS && r * 32 + 32 > g.H) m = (g.H - r * 32) >= 32 ? m : ((1u << (g.H - r * 32)) - 1u);
+    while (m) {
+      const int b = __ffs(m) - 1;
+      m &= m - 1;
+      const int i = r * 32 + b;
+      const bool in = (p >> b) & 1u;
+      for (int k = 0; k < K; ++k) {
+        const double I = band_exact(c, k, i, x);
+        if (in) dd_add(ah[k], al[k], I);
+        else dd_add(bh[k], bl[k], I);
+      }
+      if (in) ++na; else ++nb;
+    }
+  }
+  for (int o = 16; o > 0; o >>= 1) {
+    for (int k = 0; k < K; ++k) {
+      double h2 = __shfl_xor_sync(0xffffffffu, ah[k], o), l2 = __shfl_xor_sync(0xffffffffu, al[k], o);
+      dd_add_dd(ah[k], al[k], h2, l2);
+      h2 = __shfl_xor_sync(0xffffffffu, bh[k], o);
+      l2 = __shfl_xor_sync(0xffffffffu, bl[k], o);
+      dd_add_dd(bh[k], bl[k], h2, l2);
+    }
+    na += __shfl_xor_sync(0xffffffffu, na, o);
+    nb += __shfl_xor_sync(0xffffffffu, nb, o);
+  }
+  const int warp = threadIdx.x >> 5;
+  if ((threadIdx.x & 31) == 0)
+    for (int k = 0; k < K; ++k) {
+      s_w[k][warp].a_hi = ah[k]; s_w[k][warp].a_lo = al[k];
+      s_w[k][warp].b_hi = bh[k]; s_w[k][warp].b_lo = bl[k];
+      s_w[k][warp].n_a = na; s_w[k][warp].n_b = nb;
+    }
+  __syncthreads();
+  if (threadIdx.x < K) {
+    const int k = threadIdx.x;
+    TilePartial t{};
+    for (int w = 0; w < 8; ++w) {
+      dd_add_dd(t.a_hi, t.a_lo, s_w[k][w].a_hi, s_w[k][w].a_lo);
+      dd_add_dd(t.b_hi, t.b_lo, s_w[k][w].b_hi, s_w[k][w].b_lo);
+      t.n_a += s_w[k][w].n_a;
+      t.n_b += s_w[k][w].n_b;
+    }
+    part[(size_t)k * nblk + blk] = t;
+  }
+}
+
+// Reduce the band partials (fixed order) into the running per-band sums and
+// means; checkpoint bookkeeping from the fused partition's partials (mism).
+// One CTA.  absolute: the partials are full sums (initial state).
+__global__ void __launch_bounds__(256) k_finalize_bands(const TilePartial* bpart, int nblk,
+                                                        PartRanges mism_parts, Scalars* sc,
+                                                        int absolute, int ckpt, long long iter) {
+  if (!absolute && *(volatile const int*)&sc->stop) return;
+  __shared__ TilePartial s_band[kMaxBands];
+  const int K = sc->nbands;
+  for (int k = 0; k < K; ++k) {
+    PartRanges R1{{bpart + (size_t)k * nblk, bpart, bpart}, {nblk, 0, 0}};
+    reduce_slice(R1, 0, nblk, &s_band[k]);
+    __syncthreads();
+  }
+  unsigned long long mm = 0;
+  if (ckpt) {
+    __shared__ TilePartial s_m;
+    reduce_slice(mism_parts, 0, mism_parts.n[0] + mism_parts.n[1] + mism_parts.n[2], &s_m);
+    __syncthreads();
+    mm = s_m.mism;
+  }
+  if (threadIdx.x != 0) return;
+  for (int k = 0; k < K; ++k) {
+    const TilePartial& t = s_band[k];
+    if (absolute) {
+      sc->bsp_hi[k] = t.a_hi; sc->bsp_lo[k] = t.a_lo;
+      sc->bsn_hi[k] = t.b_hi; sc->bsn_lo[k] = t.b_lo;
+    } else {                                       // a: entering P, b: leaving P
+      dd_add_dd(sc->bsp_hi[k], sc->bsp_lo[k], t.a_hi, t.a_lo);
+      dd_add_dd(sc->bsp_hi[k], sc->bsp_lo[k], -t.b_hi, -t.b_lo);
+      dd_add_dd(sc->bsn_hi[k], sc->bsn_lo[k], t.b_hi, t.b_lo);
+      dd_add_dd(sc->bsn_hi[k], sc->bsn_lo[k], -t.a_hi, -t.a_lo);
+    }
+  }
+  sc->n_pos = absolute ? s_band[0].n_a : sc->n_pos + s_band[0].n_a - s_band[0].n_b;
+  const long long np = sc->n_pos, nn = sc->n_total - sc->n_pos;
+  sc->zero_vel = (np == 0 || nn == 0) ? 1 : 0;    // grid.py:114-115, models.py:111-113
+  if (!sc->zero_vel)
+    for (int k = 0; k < K; ++k) {
+      sc->bcp[k] = dd_div(sc->bsp_hi[k], sc->bsp_lo[k], (double)np);
+      sc->bcm[k] = dd_div(sc->bsn_hi[k], sc->bsn_lo[k], (double)nn);
+    }
+  sc->peak_bits = 0ull;
+  if (ckpt) {                                      // engine.py:228-236
+    sc->n_ckpt += 1;
+    if (sc->n_ckpt >= 2) sc->equal_run = (mm == 0) ? sc->equal_run + 1 : 0;
+    const long long cw = sc->conv_window;
+    if (cw == 1 || (sc->n_ckpt >= cw && sc->equal_run >= cw - 1)) {
+      sc->stop = 1;
+      sc->converged = 1;
+      sc->converged_iter = iter;
+    }
+  }
+}
+
+// The multi-band data term of every pixel for the next update: D exactly in
+// fp64 (vector_D), stored rounded to fp32 as the fused kernels' data plane,
+// and max |D| (np.abs(data).max()) via ordered-bits atomics.
+__global__ void __launch_bounds__(256) k_band_peak(const ExactCtx* c, Scalars* sc, float* d32,
+                                                   RunGeom g) {
+  if (*(volatile const int*)&sc->stop || sc->zero_vel) return;
+  unsigned long long m = 0ull;
+  const int x = blockIdx.x * blockDim.x + threadIdx.x;
+  if (x < g.W) {
+    for (int i = blockIdx.y; i < g.H; i += gridDim.y) {
+      const double D = vector_D(c, sc, i, x);
+      d32[(size_t)i * g.data_pitch + x] = (float)D;
+      const unsigned long long b = (unsigned long long)__double_as_longlong(fabs(D));
+      m = b > m ? b : m;
+    }
+  }
+  for (int o = 16; o > 0; o >>= 1) {
+    const unsigned long long v = __shfl_xor_sync(0xffffffffu, m, o);
+    m = v > m ? v : m;
+  }
+  if ((threadIdx.x & 31) == 0 && m) atomicMax(&sc->peak_bits, m);
+}
+
+// Coefficients of the next update from the band peak: the fused kernels see
+// the data plane D (fp32) and vf = A * D with A = (dt / 2) / peak.
+__global__ void k_band_coeffs(Scalars* sc) {
+  if (*(volatile const int*)&sc->stop) return;
+  const double peak = __longlong_as_double((long long)sc->peak_bits);
+  sc->peak = peak;
+  if (sc->zero_vel || peak == 0.0) {               // models.py:117-118
+    sc->zero_vel = 1;
+    sc->A = 0.f;
+    sc->B = 0.f;
+    sc->eps_u = (float)(4.0 * (0x1p-18 + 0x1p-22));
+    return;
+  }
+  const double dt = sc->dt, a = 1.0 / peak;
+  sc->A = (float)(0.5 * dt * a);
+  sc->B = 0.f;
+  // |a| * max|D| = 1; the fp32 plane adds one rounding of D
+  const double eps_d = 0x1p-21 * (2.0 + 1.0 + 1.0);
+  sc->eps_u = (float)(4.0 * (0x1p-18 + dt * (0x1p-16 + 1.5 * eps_d + 0x1p-21) +
+                             0x1p-22 * (1.0 + 1.5 * dt)));
+}
+
 // 8-bit RGB -> the reference loader's grayscale (fileio.py:28-30, 88): luma
 // in float64, ((0.299 R + 0.587 G) + 0.114 B) / 255, no re-quantization.
 __global__ void k_luma(const unsigned char* __restrict__ rgb, double* __restrict__ out,

@@ -115,6 +115,38 @@ def config2(size=1024):
                  "edge", 500)
 
 
+def config3(size=4096, iters=1000, n_shapes=400):
+    """C3: 4-band (B, G, R, NIR) scene, float32 (4, H, W): background
+    N((.25, .30, .28, .45), .05), n_shapes rectangles / convex polygons of
+    10-120 px with N((.60, .62, .65, .35), .04); region model on the vector
+    data term, sigma2 1.0 (9 taps), dt 15; initial state a +-1 checkerboard of
+    64 x 64 cells (extra["signs"], int8), SURVEY section 8d."""
+    rng = np.random.default_rng(3000)
+    bg = np.array([0.25, 0.30, 0.28, 0.45])
+    fg = np.array([0.60, 0.62, 0.65, 0.35])
+    img = bg[:, None, None] + 0.05 * rng.standard_normal((4, size, size))
+    yy, xx = np.mgrid[0:size, 0:size]
+    n_shapes = max(1, int(round(n_shapes * (size / 4096.0) ** 2)))
+    for s in range(n_shapes):
+        w, h = (int(v) for v in rng.integers(10, 121, size=2))
+        x0 = int(rng.integers(0, max(1, size - w)))
+        y0 = int(rng.integers(0, max(1, size - h)))
+        vals = fg[:, None, None] + 0.04 * rng.standard_normal((4, h, w))
+        if s % 2 == 0:                               # rectangle
+            img[:, y0:y0 + h, x0:x0 + w] = vals
+        else:                                        # convex polygon: an inscribed ellipse
+            cy, cx = h / 2.0, w / 2.0
+            m = ((yy[:h, :w] + 0.5 - cy) / cy) ** 2 + ((xx[:h, :w] + 0.5 - cx) / cx) ** 2 <= 1.0
+            sub = img[:, y0:y0 + h, x0:x0 + w]
+            sub[:, m] = vals[:, m]
+    img = np.clip(img, 0.0, 1.0).astype(np.float32)
+    cells = (yy // 64 + xx // 64) % 2
+    signs = np.where(cells == 0, 1, -1).astype(np.int8)
+    return Scene("C3", img, (), 1, dict(dt=15.0, sigma2=1.0, ts_reg=9, max_iters=iters,
+                                        conv_check_every=iters + 1), "region", iters,
+                 extra=dict(signs=signs))
+
+
 def config4_tile(k, size=1024, iters=300):
     """C4 tile k: 8-bit RGB (H, W, 3) urban tile; even tiles region with +inside
     seeds, odd tiles edge (sigma1 1.0, gain 255) with -inside seeds; centred

@@ -26,7 +26,7 @@ def test_library_exports_every_header_symbol():
     for s in syms:
         assert hasattr(N.lib, s), s
     assert set(syms) == set(N.EXPORTED)
-    assert N.lib.lse_abi_version() == 3
+    assert N.lib.lse_abi_version() == 4
 
 
 def test_struct_layouts_match_header(tmp_path):

@@ -116,3 +116,19 @@ def test_luma_restatement_matches_reference_loader():
     from paper_1409_7474_b200 import scenes
     g = load_golden("luma")
     assert np.array_equal(scenes.luma(g["rgb"]), g["luma"])
+
+
+def test_band_restatement_reduces_to_region_model():
+    """C3's multi-band restatement with one band is region_velocity exactly, and
+    runs the reference's region trajectory bit for bit (the pin for K > 1)."""
+    rng = np.random.default_rng(9)
+    img, phi = rng.random((21, 17)), rng.standard_normal((21, 17))
+    v1, d1 = O.region_velocity(img, phi)
+    vk, dk = O.region_velocity_bands(img[None], phi)
+    assert d1 == dk and np.array_equal(v1, vk)
+    g = load_golden("traj_region_small")
+    img = g["image"]
+    r = O.OracleRun(img[None], _phi0(g, img.shape), _params(g))
+    for it in g["iters_recorded"]:
+        r.advance(int(it) - r.iteration)
+        assert np.array_equal(r.phi, g[f"phi_{it}"])
