@@ -240,6 +240,39 @@ def other_configs(steps, c4_tiles):
                         "unit": "Gpix-it/s", "ms_per_job": ms.value / steps,
                         "workload": f"{sc.name}: {img.shape[0]}^2 {sc.model}, {sc.iters} its",
                         "bound": "launch latency / L2 (not HBM)"}
+    # C3: 4096^2 x 4 bands, vector data term, +-1 checkerboard, 1000 its
+    from paper_1409_7474_b200.bands import BandEvolutionRun
+    sc3 = scenes.config3(4096, 1000)
+    prm3 = default_params(ModelKind.REGION, **sc3.params)
+    run3 = BandEvolutionRun(sc3.image, sc3.extra["signs"], prm3)
+    run3.set_native_option("skip_uniform", 0)
+    signs3 = np.ascontiguousarray(sc3.extra["signs"], dtype=np.int8)
+    init3 = N.LsePhi0()
+    init3.kind = N.LSE_PHI0_SIGNS
+    init3.signs = signs3.ctypes.data_as(C.POINTER(C.c_byte))
+    init3.scale = 1.0
+    st3 = N.LseStatus()
+    h3 = run3._dev.h
+
+    def job3():
+        N.check(N.lib.lse_run_set_state(h3, C.byref(init3)))
+        N.check(N.lib.lse_run_advance(h3, sc3.iters, C.byref(st3)))
+
+    job3()
+    ms3 = C.c_double()
+    N.check(N.lib.lse_run_begin_timing(h3))
+    for _ in range(steps):
+        job3()
+    N.check(N.lib.lse_run_end_timing(h3, C.byref(ms3)))
+    peak_gbs, _ = measured_peaks()
+    v3 = 4096 * 4096 * sc3.iters * steps / (ms3.value / 1e3) / 1e9
+    out["C3"] = {"value": v3, "unit": "Gpix-it/s", "ms_per_job": ms3.value / steps,
+                 "workload": "C3: 4096^2 x 4 bands (fp32), vector region term, +-1 "
+                             "checkerboard of 64^2 cells, 1000 its",
+                 "roofline": {"bound": "hbm", "algorithmic_bytes_per_px_it": 24.0,
+                              "achieved": v3 * 24.0, "peak": peak_gbs, "unit": "GB/s",
+                              "frac": v3 * 24.0 / peak_gbs}}
+    del run3
     if c4_tiles > 0:
         base = [scenes.config4_tile(k, 1024, 300) for k in range(min(16, c4_tiles))]
         sc = [base[k % len(base)] for k in range(c4_tiles)]   # tile k keeps k's model parity
@@ -267,8 +300,12 @@ def other_configs(steps, c4_tiles):
             tb.advance(300)
             times.append(time.perf_counter() - t0)
         t = sum(times) / len(times)
-        out["C4"] = {"value": c4_tiles * 1024 * 1024 * 300 / t / 1e9, "unit": "Gpix-it/s",
+        v4 = c4_tiles * 1024 * 1024 * 300 / t / 1e9
+        out["C4"] = {"value": v4, "unit": "Gpix-it/s",
                      "ms_per_job": t * 1e3, "tiles": c4_tiles,
+                     "roofline": {"bound": "hbm", "algorithmic_bytes_per_px_it": 12.0,
+                                  "achieved": v4 * 12.0, "peak": measured_peaks()[0],
+                                  "unit": "GB/s", "frac": v4 * 12.0 / measured_peaks()[0]},
                      "workload": f"C4: {c4_tiles} x 1024^2 8-bit RGB tiles (luma decoded on "
                                  "device), region/edge alternating, 300 its, one batch",
                      "tile_setup_s": round(t_create, 2),

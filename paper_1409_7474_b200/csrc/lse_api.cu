@@ -128,6 +128,7 @@ struct lse_run {
   double* d_bands64 = nullptr;
   uint32_t* d_chg = nullptr;
   TilePartial* d_bpart = nullptr;
+  unsigned long long* d_pmax = nullptr;   // per-CTA maxima of the band peak pass
   double img_absmax = 0.0;
   // state
   uint32_t* d_bits[2] = {nullptr, nullptr};
@@ -652,10 +653,16 @@ int band_chain(lse_run* r, bool absolute, bool ckpt, long long it) {
   k_finalize_bands<<<1, 256, 0, r->st>>>(r->d_bpart, nblk, M, r->d_scal, absolute ? 1 : 0,
                                          ckpt ? 1 : 0, it);
   CKL();
-  k_band_peak<<<dim3((r->W + 255) / 256, std::min(r->H, 512)), 256, 0, r->st>>>(
-      r->d_ctx, r->d_scal, r->d_data32, r->g);
+  const dim3 gp((r->W + 1023) / 1024, r->H);
+  unsigned long long* pmax = r->d_pmax;
+  switch (r->nbands) {
+    case 1: k_band_peak<1><<<gp, 256, 0, r->st>>>(r->d_ctx, r->d_scal, r->d_data32, pmax, r->g); break;
+    case 2: k_band_peak<2><<<gp, 256, 0, r->st>>>(r->d_ctx, r->d_scal, r->d_data32, pmax, r->g); break;
+    case 3: k_band_peak<3><<<gp, 256, 0, r->st>>>(r->d_ctx, r->d_scal, r->d_data32, pmax, r->g); break;
+    default: k_band_peak<4><<<gp, 256, 0, r->st>>>(r->d_ctx, r->d_scal, r->d_data32, pmax, r->g); break;
+  }
   CKL();
-  k_band_coeffs<<<1, 1, 0, r->st>>>(r->d_scal);
+  k_band_coeffs<<<1, 1024, 0, r->st>>>(r->d_scal, pmax, (int)(gp.x * gp.y));
   CKL();
   return LSE_OK;
 }
@@ -1059,6 +1066,7 @@ int create_impl(lse_run** out, const lse_params* p, long long height, long long 
   if (p->model == LSE_MODEL_BANDS &&
       ((rc = dalloc(&r->d_bands32, (size_t)p->n_bands * r->g.data_pitch * r->H)) ||
        (rc = dalloc(&r->d_chg, nbits)) ||
+       (rc = dalloc(&r->d_pmax, (size_t)r->H * ((r->W + 1023) / 1024))) ||
        (rc = dalloc(&r->d_bpart, (size_t)p->n_bands * r->g.HR * ((r->g.pitch_w + 1023) / 1024)))))
     return cleanup(rc);
   if (cudaMallocHost((void**)&r->h_scal, sizeof(Scalars)) != cudaSuccess)
@@ -1723,7 +1731,7 @@ void lse_batch_destroy(lse_batch* b) {
 void lse_run_destroy(lse_run* r) {
   if (!r) return;
   if (r->st) cudaStreamSynchronize(r->st);
-  void* ptrs[] = {r->d_bands32, r->d_bands64, r->d_chg, r->d_bpart,
+  void* ptrs[] = {r->d_bands32, r->d_bands64, r->d_chg, r->d_bpart, r->d_pmax,
                   r->d_work, r->d_part_fin, r->d_part_init, r->d_data32, r->d_data64, r->d_bits[0], r->d_bits[1], r->d_P, r->d_M,
                   r->d_mask, r->d_part, r->d_scal, r->d_lut_t, r->d_lut_s, r->d_ctx,
                   r->d_w64, r->d_keys, r->d_count, r->d_F[0], r->d_F[1], r->d_U, r->d_T};

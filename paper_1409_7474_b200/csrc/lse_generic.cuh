@@ -536,33 +536,95 @@ __global__ void __launch_bounds__(256) k_finalize_bands(const TilePartial* bpart
 }
 
 // The multi-band data term of every pixel for the next update: D exactly in
-// fp64 (vector_D), stored rounded to fp32 as the fused kernels' data plane,
-// and max |D| (np.abs(data).max()) via ordered-bits atomics.
-__global__ void __launch_bounds__(256) k_band_peak(const ExactCtx* c, Scalars* sc, float* d32,
+// fp64 (vector_D's operations; the band constants hoisted), stored rounded to
+// fp32 as the fused kernels' data plane, and max |D| (np.abs(data).max()):
+// one (1024-column, 1-row) block per CTA, every band load issued before any
+// use, one maximum per CTA into pmax (reduced by k_band_coeffs).
+template <int K>
+__global__ void __launch_bounds__(256) k_band_peak(const ExactCtx* __restrict__ c,
+                                                   const Scalars* __restrict__ sc,
+                                                   float* __restrict__ d32,
+                                                   unsigned long long* __restrict__ pmax,
                                                    RunGeom g) {
-  if (*(volatile const int*)&sc->stop || sc->zero_vel) return;
-  unsigned long long m = 0ull;
-  const int x = blockIdx.x * blockDim.x + threadIdx.x;
-  if (x < g.W) {
-    for (int i = blockIdx.y; i < g.H; i += gridDim.y) {
-      const double D = vector_D(c, sc, i, x);
-      d32[(size_t)i * g.data_pitch + x] = (float)D;
-      const unsigned long long b = (unsigned long long)__double_as_longlong(fabs(D));
-      m = b > m ? b : m;
+  const float* b32 = c->bands32;
+  const double* b64 = c->bands64;
+  const long long stride = c->band_stride;
+  const int i = blockIdx.y;
+  const int x0 = (blockIdx.x * blockDim.x + threadIdx.x) * 4;
+  const size_t o = (size_t)i * g.data_pitch + x0;
+  const bool act = x0 < g.W;
+  double I[K][4];
+  if (act) {
+    if (b64) {
+#pragma unroll
+      for (int k = 0; k < K; ++k)
+#pragma unroll
+        for (int q = 0; q < 4; ++q) I[k][q] = b64[k * stride + o + q];
+    } else {
+      float4 v[K];
+#pragma unroll
+      for (int k = 0; k < K; ++k) v[k] = __ldcs(reinterpret_cast<const float4*>(b32 + k * stride + o));
+#pragma unroll
+      for (int k = 0; k < K; ++k) {
+        I[k][0] = v[k].x; I[k][1] = v[k].y; I[k][2] = v[k].z; I[k][3] = v[k].w;
+      }
     }
   }
-  for (int o = 16; o > 0; o >>= 1) {
-    const unsigned long long v = __shfl_xor_sync(0xffffffffu, m, o);
+  const bool live = !sc->stop && !sc->zero_vel;
+  unsigned long long m = 0ull;
+  if (act && live) {
+    double D[4];
+#pragma unroll
+    for (int k = 0; k < K; ++k) {
+      const double cp = sc->bcp[k], cm = sc->bcm[k], dc = dsub(cp, cm);
+#pragma unroll
+      for (int q = 0; q < 4; ++q) {
+        const double t = dmul(dc, dsub(dsub(dmul(2.0, I[k][q]), cp), cm));
+        D[q] = k == 0 ? t : dadd(D[q], t);
+      }
+    }
+    float4 out;
+    out.x = (float)D[0]; out.y = (float)D[1]; out.z = (float)D[2]; out.w = (float)D[3];
+    reinterpret_cast<float4*>(d32 + o)[0] = out;
+#pragma unroll
+    for (int q = 0; q < 4; ++q) {
+      if (x0 + q >= g.W) break;
+      const unsigned long long bb = (unsigned long long)__double_as_longlong(fabs(D[q]));
+      m = bb > m ? bb : m;
+    }
+  }
+  for (int o2 = 16; o2 > 0; o2 >>= 1) {
+    const unsigned long long v = __shfl_xor_sync(0xffffffffu, m, o2);
     m = v > m ? v : m;
   }
-  if ((threadIdx.x & 31) == 0 && m) atomicMax(&sc->peak_bits, m);
+  __shared__ unsigned long long s_m[8];
+  if ((threadIdx.x & 31) == 0) s_m[threadIdx.x >> 5] = m;
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    for (int w = 1; w < (int)(blockDim.x >> 5); ++w) m = s_m[w] > m ? s_m[w] : m;
+    pmax[(size_t)blockIdx.y * gridDim.x + blockIdx.x] = m;
+  }
 }
 
 // Coefficients of the next update from the band peak: the fused kernels see
 // the data plane D (fp32) and vf = A * D with A = (dt / 2) / peak.
-__global__ void k_band_coeffs(Scalars* sc) {
+__global__ void __launch_bounds__(1024) k_band_coeffs(Scalars* sc,
+                                                      const unsigned long long* pmax, int n) {
   if (*(volatile const int*)&sc->stop) return;
-  const double peak = __longlong_as_double((long long)sc->peak_bits);
+  unsigned long long m = 0ull;
+  for (int t = threadIdx.x; t < n; t += blockDim.x) m = pmax[t] > m ? pmax[t] : m;
+  for (int o = 16; o > 0; o >>= 1) {
+    const unsigned long long v = __shfl_xor_sync(0xffffffffu, m, o);
+    m = v > m ? v : m;
+  }
+  __shared__ unsigned long long s_m[32];
+  if ((threadIdx.x & 31) == 0) s_m[threadIdx.x >> 5] = m;
+  __syncthreads();
+  if (threadIdx.x != 0) return;
+  for (int w = 1; w < (int)(blockDim.x >> 5); ++w) m = s_m[w] > m ? s_m[w] : m;
+  if (sc->zero_vel) m = 0ull;
+  sc->peak_bits = m;
+  const double peak = __longlong_as_double((long long)m);
   sc->peak = peak;
   if (sc->zero_vel || peak == 0.0) {               // models.py:117-118
     sc->zero_vel = 1;
