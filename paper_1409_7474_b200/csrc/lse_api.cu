@@ -61,6 +61,33 @@ std::atomic<long long> g_launches{0};
 
 inline long long round_up(long long a, long long b) { return (a + b - 1) / b * b; }
 
+// Per-iteration kernels are launched with programmatic stream serialization
+// (each waits in pdl_wait before reading its predecessor's results), so a
+// kernel's launch and static prologue overlap the previous kernel's tail.
+// LSE_NO_PDL=1 launches them plainly (A/B measurements).
+bool pdl_enabled() {
+  static const bool on = std::getenv("LSE_NO_PDL") == nullptr;
+  return on;
+}
+
+template <typename... KArgs, typename... Args>
+int launch_pdl(void (*kern)(KArgs...), dim3 grid, dim3 block, cudaStream_t st, Args... args) {
+  cudaLaunchConfig_t cfg{};
+  cfg.gridDim = grid;
+  cfg.blockDim = block;
+  cfg.dynamicSmemBytes = 0;
+  cfg.stream = st;
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  attr[0].val.programmaticStreamSerializationAllowed = pdl_enabled() ? 1 : 0;
+  cfg.attrs = attr;
+  cfg.numAttrs = 1;
+  g_launches.fetch_add(1, std::memory_order_relaxed);
+  const cudaError_t e = cudaLaunchKernelEx(&cfg, kern, args...);
+  if (e != cudaSuccess) return fail(LSE_ERR_CUDA, std::string("launch: ") + cudaGetErrorString(e));
+  return LSE_OK;
+}
+
 int num_sms() {
   static int n = 0;
   if (!n) {
@@ -405,8 +432,7 @@ int launch_update(lse_run* r, FastParams P) {
 #ifdef LSE_UNIT_TRACE
   P.trace = trace_begin(r, n, g, "update", r->nb_upd[0]);
 #endif
-  k_update<R, MODEL, SRC, false><<<g, kThreads, 0, r->st>>>(P);
-  CKL();
+  TRY(launch_pdl(k_update<R, MODEL, SRC, false>, g, kThreads, r->st, P));
 #ifdef LSE_UNIT_TRACE
   trace_after(r, P.trace);
 #endif
@@ -421,8 +447,7 @@ int launch_partition(lse_run* r, FastParams P) {
 #ifdef LSE_UNIT_TRACE
   P.trace = MASKONLY ? nullptr : trace_begin(r, n, g, "partition", r->nb_part);
 #endif
-  k_partition<R, PART, CKPT, MASKONLY, false><<<g, kThreads, 0, r->st>>>(P);
-  CKL();
+  TRY(launch_pdl(k_partition<R, PART, CKPT, MASKONLY, false>, g, kThreads, r->st, P));
 #ifdef LSE_UNIT_TRACE
   trace_after(r, P.trace);
 #endif
@@ -431,8 +456,8 @@ int launch_partition(lse_run* r, FastParams P) {
     // update's coefficients (64 CTAs reduce contiguous slices, 1 CTA the rest)
     PartRanges R3{{r->d_part, r->d_part, r->d_part}, {(int)n, 0, 0}};
     if (!is_bands(r)) {
-      k_finalize_stage1<<<kFinSlices, 256, 0, r->st>>>(R3, r->d_part_fin, r->d_scal);
-      CKL();
+      TRY(launch_pdl(k_finalize_stage1, kFinSlices, 256, r->st, R3, r->d_part_fin,
+                     (const Scalars*)r->d_scal));
     }
     PartRanges R1{{r->d_part_fin, r->d_part_fin, r->d_part_fin}, {kFinSlices, 0, 0}};
     if (is_bands(r)) {
@@ -444,7 +469,8 @@ int launch_partition(lse_run* r, FastParams P) {
       // finalize together (lse_strip_finalize)
       k_reduce_to_one<<<1, 256, 0, r->st>>>(R1, r->strip_out, r->d_scal, 1);
     } else {
-      k_finalize_run<<<1, 64, 0, r->st>>>(R1, r->d_scal, PART ? 1 : 0, CKPT ? 1 : 0, P.iter);
+      TRY(launch_pdl(k_finalize_run, 1, 64, r->st, R1, r->d_scal, PART ? 1 : 0, CKPT ? 1 : 0,
+                     (long long)P.iter));
     }
     CKL();
   }
@@ -642,28 +668,29 @@ int band_chain(lse_run* r, bool absolute, bool ckpt, long long it) {
   const dim3 gr((r->g.pitch_w + 1023) / 1024, r->g.HR);
   const int nblk = (int)(gr.x * gr.y);
   if (absolute)
-    k_band_sums<true><<<gr, 256, 0, r->st>>>(nullptr, r->d_P, r->d_ctx, r->d_bpart, r->g,
-                                             r->d_scal);
+    TRY(launch_pdl(k_band_sums<true>, gr, 256, r->st, (const uint32_t*)nullptr,
+                   (const uint32_t*)r->d_P, (const ExactCtx*)r->d_ctx, r->d_bpart, r->g,
+                   (const Scalars*)r->d_scal));
   else
-    k_band_sums<false><<<gr, 256, 0, r->st>>>(r->d_chg, r->d_P, r->d_ctx, r->d_bpart, r->g,
-                                              r->d_scal);
-  CKL();
+    TRY(launch_pdl(k_band_sums<false>, gr, 256, r->st, (const uint32_t*)r->d_chg,
+                   (const uint32_t*)r->d_P, (const ExactCtx*)r->d_ctx, r->d_bpart, r->g,
+                   (const Scalars*)r->d_scal));
   const int n = (int)(r->nb_part + r->ni_part);
   PartRanges M{{r->d_part, r->d_part, r->d_part}, {ckpt ? n : 0, 0, 0}};
-  k_finalize_bands<<<1, 256, 0, r->st>>>(r->d_bpart, nblk, M, r->d_scal, absolute ? 1 : 0,
-                                         ckpt ? 1 : 0, it);
-  CKL();
+  TRY(launch_pdl(k_finalize_bands, 1, 256, r->st, (const TilePartial*)r->d_bpart, nblk, M,
+                 r->d_scal, absolute ? 1 : 0, ckpt ? 1 : 0, it));
   const dim3 gp((r->W + 1023) / 1024, r->H);
   unsigned long long* pmax = r->d_pmax;
+  const ExactCtx* cctx = r->d_ctx;
+  const Scalars* csc = r->d_scal;
   switch (r->nbands) {
-    case 1: k_band_peak<1><<<gp, 256, 0, r->st>>>(r->d_ctx, r->d_scal, r->d_data32, pmax, r->g); break;
-    case 2: k_band_peak<2><<<gp, 256, 0, r->st>>>(r->d_ctx, r->d_scal, r->d_data32, pmax, r->g); break;
-    case 3: k_band_peak<3><<<gp, 256, 0, r->st>>>(r->d_ctx, r->d_scal, r->d_data32, pmax, r->g); break;
-    default: k_band_peak<4><<<gp, 256, 0, r->st>>>(r->d_ctx, r->d_scal, r->d_data32, pmax, r->g); break;
+    case 1: TRY(launch_pdl(k_band_peak<1>, gp, 256, r->st, cctx, csc, r->d_data32, pmax, r->g)); break;
+    case 2: TRY(launch_pdl(k_band_peak<2>, gp, 256, r->st, cctx, csc, r->d_data32, pmax, r->g)); break;
+    case 3: TRY(launch_pdl(k_band_peak<3>, gp, 256, r->st, cctx, csc, r->d_data32, pmax, r->g)); break;
+    default: TRY(launch_pdl(k_band_peak<4>, gp, 256, r->st, cctx, csc, r->d_data32, pmax, r->g)); break;
   }
-  CKL();
-  k_band_coeffs<<<1, 1024, 0, r->st>>>(r->d_scal, pmax, (int)(gp.x * gp.y));
-  CKL();
+  TRY(launch_pdl(k_band_coeffs, 1, 1024, r->st, r->d_scal, (const unsigned long long*)pmax,
+                 (int)(gp.x * gp.y)));
   return LSE_OK;
 }
 
@@ -1517,9 +1544,8 @@ int batch_iteration(lse_batch* b, long long it, bool ckpt, int src, bool any_reg
     const long long n = (long long)b->T * (b->nb_upd + b->ni_upd);
     const int g = fast_grid(n);
     P.work_base = batch_take_work(b, n, g);
-    if (src == SRC_SCALED) k_update<R, REGION, SRC_SCALED, true><<<g, kThreads, 0, b->st>>>(P);
-    else k_update<R, REGION, SRC_SMOOTH, true><<<g, kThreads, 0, b->st>>>(P);
-    CKL();
+    if (src == SRC_SCALED) TRY(launch_pdl(k_update<R, REGION, SRC_SCALED, true>, g, kThreads, b->st, P));
+    else TRY(launch_pdl(k_update<R, REGION, SRC_SMOOTH, true>, g, kThreads, b->st, P));
   }
   b->cur ^= 1;
   if (!any_region && !ckpt) return LSE_OK;
@@ -1527,14 +1553,13 @@ int batch_iteration(lse_batch* b, long long it, bool ckpt, int src, bool any_reg
   const long long n = (long long)b->T * (b->nb_part + b->ni_part);
   const int g = fast_grid(n);
   P.work_base = batch_take_work(b, n, g);
-  if (ckpt) k_partition<R, true, true, false, true><<<g, kThreads, 0, b->st>>>(P);
-  else k_partition<R, true, false, false, true><<<g, kThreads, 0, b->st>>>(P);
-  CKL();
-  k_finalize_stage1_tiles<<<dim3(kFinSlices, b->T), 256, 0, b->st>>>(
-      b->part, b->part_fin, b->scal, (int)b->nb_part, (int)b->ni_part, b->T, ckpt ? 1 : 0);
-  CKL();
-  k_finalize_run_tiles<<<b->T, 64, 0, b->st>>>(b->part_fin, b->scal, ckpt ? 1 : 0, it);
-  CKL();
+  if (ckpt) TRY(launch_pdl(k_partition<R, true, true, false, true>, g, kThreads, b->st, P));
+  else TRY(launch_pdl(k_partition<R, true, false, false, true>, g, kThreads, b->st, P));
+  TRY(launch_pdl(k_finalize_stage1_tiles, dim3(kFinSlices, b->T), 256, b->st,
+                 (const TilePartial*)b->part, b->part_fin, (const Scalars*)b->scal,
+                 (int)b->nb_part, (int)b->ni_part, b->T, ckpt ? 1 : 0));
+  TRY(launch_pdl(k_finalize_run_tiles, b->T, 64, b->st, (const TilePartial*)b->part_fin,
+                 b->scal, ckpt ? 1 : 0, it));
   return LSE_OK;
 }
 

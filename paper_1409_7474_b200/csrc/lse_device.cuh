@@ -71,6 +71,16 @@ struct RunGeom {
   int ncb, ntiles;          // column blocks (of 8*kThreads columns), tiles
 };
 
+// ------------------------------------------------- programmatic dependent launch
+// The per-iteration kernels are launched with programmatic stream
+// serialization: a kernel may start (its static prologue: LUT loads) while its
+// predecessor drains, and waits here before touching the predecessor's
+// results.  Without the launch attribute both are no-ops.
+__device__ __forceinline__ void pdl_wait() { asm volatile("griddepcontrol.wait;" ::: "memory"); }
+__device__ __forceinline__ void pdl_launch_dependents() {
+  asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
+}
+
 // ---------------------------------------------------------------- exact ops
 // numpy / scipy evaluate every float64 operation separately with round-to-
 // nearest (no FMA on x86-64 baseline builds); these wrappers stop nvcc from

@@ -287,6 +287,8 @@ __global__ void __launch_bounds__(1024) k_finalize(const TilePartial* part, int 
 constexpr int kFinSlices = 64;
 __global__ void __launch_bounds__(256) k_finalize_stage1(PartRanges R3, TilePartial* out,
                                                          const Scalars* sc) {
+  pdl_wait();
+  pdl_launch_dependents();
   if (*(volatile const int*)&sc->stop) return;
   const int n = R3.n[0] + R3.n[1] + R3.n[2];
   const int per = (n + gridDim.x - 1) / gridDim.x;
@@ -309,6 +311,8 @@ __global__ void __launch_bounds__(256) k_finalize_stage1_tiles(const TilePartial
                                                                TilePartial* out,
                                                                const Scalars* scal, int nb,
                                                                int ni, int T, int ckpt) {
+  pdl_wait();
+  pdl_launch_dependents();
   const int t = blockIdx.y;
   const Scalars* sc = scal + t;
   if (*(volatile const int*)&sc->stop) return;
@@ -323,6 +327,8 @@ __global__ void __launch_bounds__(256) k_finalize_stage1_tiles(const TilePartial
 
 __global__ void __launch_bounds__(64) k_finalize_run_tiles(const TilePartial* fin, Scalars* scal,
                                                            int ckpt, long long iter) {
+  pdl_wait();
+  pdl_launch_dependents();
   const int t = blockIdx.x;
   Scalars* sc = scal + t;
   if (*(volatile const int*)&sc->stop) return;
@@ -336,6 +342,8 @@ __global__ void __launch_bounds__(64) k_finalize_run_tiles(const TilePartial* fi
 // per-iteration finalize of the fast path (DELTA partials); no-op once stopped
 __global__ void __launch_bounds__(64) k_finalize_run(PartRanges R3, Scalars* sc, int region,
                                                        int ckpt, long long iter) {
+  pdl_wait();
+  pdl_launch_dependents();
   if (*(volatile const int*)&sc->stop) return;
   finalize_cta(R3, sc, true, region != 0, ckpt != 0, iter);
 }
@@ -419,6 +427,8 @@ __global__ void __launch_bounds__(256) k_band_sums(const uint32_t* __restrict__ 
                                                    const uint32_t* __restrict__ pbits,
                                                    const ExactCtx* c, TilePartial* part,
                                                    RunGeom g, const Scalars* sc) {
+  pdl_wait();
+  pdl_launch_dependents();
   if (!ABS && *(volatile const int*)&sc->stop) return;
   __shared__ TilePartial s_w[kMaxBands][8];
   const int r = blockIdx.y;
@@ -486,6 +496,8 @@ __global__ void __launch_bounds__(256) k_band_sums(const uint32_t* __restrict__ 
 __global__ void __launch_bounds__(256) k_finalize_bands(const TilePartial* bpart, int nblk,
                                                         PartRanges mism_parts, Scalars* sc,
                                                         int absolute, int ckpt, long long iter) {
+  pdl_wait();
+  pdl_launch_dependents();
   if (!absolute && *(volatile const int*)&sc->stop) return;
   __shared__ TilePartial s_band[kMaxBands];
   const int K = sc->nbands;
@@ -546,6 +558,8 @@ __global__ void __launch_bounds__(256) k_band_peak(const ExactCtx* __restrict__ 
                                                    float* __restrict__ d32,
                                                    unsigned long long* __restrict__ pmax,
                                                    RunGeom g) {
+  pdl_wait();
+  pdl_launch_dependents();
   const float* b32 = c->bands32;
   const double* b64 = c->bands64;
   const long long stride = c->band_stride;
@@ -610,6 +624,8 @@ __global__ void __launch_bounds__(256) k_band_peak(const ExactCtx* __restrict__ 
 // the data plane D (fp32) and vf = A * D with A = (dt / 2) / peak.
 __global__ void __launch_bounds__(1024) k_band_coeffs(Scalars* sc,
                                                       const unsigned long long* pmax, int n) {
+  pdl_wait();
+  pdl_launch_dependents();
   if (*(volatile const int*)&sc->stop) return;
   unsigned long long m = 0ull;
   for (int t = threadIdx.x; t < n; t += blockDim.x) m = pmax[t] > m ? pmax[t] : m;
