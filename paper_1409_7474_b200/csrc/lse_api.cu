@@ -200,6 +200,8 @@ struct lse_run {
   int nchunk = 1, nchunk_u = 1, nseg = 1, seg_chunks = 1;
   Geo gu{}, gu_all{}, gp{};   // work geometry: update, update with no interior, partition
   long long ni_upd = 0, nb_upd[2] = {0, 0}, ni_part = 0, nb_part = 0;
+  long long ni_upd_half = 0;   // interior update units in split-warp (half) mode
+  bool half_units = false;     // small images: 128-column split-warp update units
   unsigned long long* d_work = nullptr;
   TilePartial* d_part_fin = nullptr;
   TilePartial* d_part_init = nullptr;
@@ -426,13 +428,15 @@ void trace_flush() {
 
 template <int R, int MODEL, int SRC>
 int launch_update(lse_run* r, FastParams P) {
-  const long long n = r->nb_upd[0] + r->ni_upd;
+  const bool half = r->half_units;
+  const long long n = r->nb_upd[0] + (half ? r->ni_upd_half : r->ni_upd);
   const int g = fast_grid(n);
   P.work_base = take_work(r, n, g);
 #ifdef LSE_UNIT_TRACE
   P.trace = trace_begin(r, n, g, "update", r->nb_upd[0]);
 #endif
-  TRY(launch_pdl(k_update<R, MODEL, SRC, false>, g, kThreads, r->st, P));
+  if (half) TRY(launch_pdl(k_update<R, MODEL, SRC, false, true>, g, kThreads, r->st, P));
+  else TRY(launch_pdl(k_update<R, MODEL, SRC, false, false>, g, kThreads, r->st, P));
 #ifdef LSE_UNIT_TRACE
   trace_after(r, P.trace);
 #endif
@@ -1057,6 +1061,10 @@ int create_impl(lse_run** out, const lse_params* p, long long height, long long 
     }
     r->gu_all = geo_all_border(r->gu, H);
     r->ni_upd = (long long)(r->gu.r_hi - r->gu.r_lo) * r->gu.nci + (r->gu.nB1 + 31) / 32;
+    r->ni_upd_half = 2LL * (r->gu.r_hi - r->gu.r_lo) * r->gu.nci + (r->gu.nB1 + 15) / 16;
+    // too few full units to keep every warp busy for several rounds: halve them
+    const char* hv = std::getenv("LSE_HALF_UNITS");
+    r->half_units = hv ? std::atoi(hv) != 0 : r->ni_upd < 4LL * num_sms() * 16;
     r->nb_upd[0] = border_units(r->gu);
     r->nb_upd[1] = r->gu_all.nA;
     // partition segments: >= ~8 interior units per resident warp, <= 16 chunks
@@ -1544,8 +1552,10 @@ int batch_iteration(lse_batch* b, long long it, bool ckpt, int src, bool any_reg
     const long long n = (long long)b->T * (b->nb_upd + b->ni_upd);
     const int g = fast_grid(n);
     P.work_base = batch_take_work(b, n, g);
-    if (src == SRC_SCALED) TRY(launch_pdl(k_update<R, REGION, SRC_SCALED, true>, g, kThreads, b->st, P));
-    else TRY(launch_pdl(k_update<R, REGION, SRC_SMOOTH, true>, g, kThreads, b->st, P));
+    if (src == SRC_SCALED)
+      TRY(launch_pdl(k_update<R, REGION, SRC_SCALED, true, false>, g, kThreads, b->st, P));
+    else
+      TRY(launch_pdl(k_update<R, REGION, SRC_SMOOTH, true, false>, g, kThreads, b->st, P));
   }
   b->cur ^= 1;
   if (!any_region && !ckpt) return LSE_OK;

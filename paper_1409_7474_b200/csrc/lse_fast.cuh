@@ -659,6 +659,131 @@ __device__ __forceinline__ void update_block_int2(const FastParams& P, uint32_t 
     reinterpret_cast<uint4*>(dst)[q] = make_uint4(ow[4 * q], ow[4 * q + 1], ow[4 * q + 2], ow[4 * q + 3]);
 }
 
+// Split-warp interior block for small images: lanes 0-15 take rows 0-15 and
+// lanes 16-31 rows 16-31 of the same 8-column groups (a warp unit covers 128
+// columns), so a unit is 8 row pairs long instead of 16.  Each half keeps its
+// own window with base row h0 - 1 - R, so the window offsets -- and the whole
+// instruction stream -- are the same in both halves; the two 16-bit halves of
+// each state word are merged by one shuffle.  Every lane of the warp calls it
+// (act = false: no work, still shuffles).
+template <int R, int MODEL, int CPL, int SRC>
+__device__ __forceinline__ void update_block_half(const FastParams& P, uint32_t lut_base,
+                                                  float* ring, int r, int x0, float A, float B,
+                                                  float eps_u,
+                                                  const uint32_t (&wlo)[CPL + 2 * (R + 1)],
+                                                  const uint32_t (&whi)[CPL + 2 * (R + 1)],
+                                                  int tile, bool act) {
+  constexpr int NT = CPL + 2 * (R + 1);
+  constexpr int NP = CPL + 2;
+  constexpr uint32_t kSlot = 32 * CPL * 4;
+  const int lane = threadIdx.x & 31;
+  const int h0 = (lane >> 4) * 16;              // first row of this lane's half
+  const int y0 = r * 32;
+  uint32_t ow[CPL];
+#pragma unroll
+  for (int c = 0; c < CPL; ++c) ow[c] = 0u;
+  if (act) {
+    uint32_t win4[NT];
+    const int sh = h0 ? 15 - R : 31 - R;        // window base row y0 + h0 - 1 - R
+#pragma unroll
+    for (int j = 0; j < NT; ++j) win4[j] = __funnelshift_r(wlo[j], whi[j], sh) << 2;
+    const uint32_t ring_s = (uint32_t)__cvta_generic_to_shared(ring) + lane * CPL * 4;
+    const size_t dpitch = P.g.data_pitch;
+    const float* gsrc = P.data32 + (size_t)(y0 + h0) * dpitch + x0;
+#pragma unroll
+    for (int q = 0; q < kRing2 - 2; q += 2) {  // rows 0 .. 5 of the half in flight
+#pragma unroll
+      for (int v = 0; v < CPL / 4; ++v) {
+        cp_async16(ring_s + q * kSlot + v * 16, gsrc + 4 * v);
+        cp_async16(ring_s + (q + 1) * kSlot + v * 16, gsrc + dpitch + 4 * v);
+      }
+      cp_async_commit();
+      gsrc += 2 * dpitch;
+    }
+    float2 pp[NP], pn[NP];
+    uint32_t fbrows = 0u;
+    phi_rows2_int<R, NT, NP, SRC>(P, win4, 0, lut_base, pp);   // rows h0-1, h0
+#pragma unroll 2
+    for (int s = 0; s < 8; ++s) {
+      if (2 * s + kRing2 - 2 < 16) {
+        const uint32_t d0 = ring_s + ((2 * s + kRing2 - 2) & (kRing2 - 1)) * kSlot;
+#pragma unroll
+        for (int v = 0; v < CPL / 4; ++v) {
+          cp_async16(d0 + v * 16, gsrc + 4 * v);
+          cp_async16(d0 + kSlot + v * 16, gsrc + dpitch + 4 * v);
+        }
+        gsrc += 2 * dpitch;
+      }
+      cp_async_commit();
+      phi_rows2_int<R, NT, NP, SRC>(P, win4, 2 * s + 2, lut_base, pn);
+      cp_async_wait<kRing2 / 2 - 1>();
+      float d0[CPL], d1[CPL];
+      {
+        const uint32_t src0 = ring_s + ((2 * s) & (kRing2 - 1)) * kSlot;
+#pragma unroll
+        for (int v = 0; v < CPL / 4; ++v) {
+          float4 q0, q1;
+          asm volatile("ld.shared.v4.f32 {%0, %1, %2, %3}, [%4];"
+                       : "=f"(q0.x), "=f"(q0.y), "=f"(q0.z), "=f"(q0.w) : "r"(src0 + v * 16));
+          asm volatile("ld.shared.v4.f32 {%0, %1, %2, %3}, [%4];"
+                       : "=f"(q1.x), "=f"(q1.y), "=f"(q1.z), "=f"(q1.w) : "r"(src0 + kSlot + v * 16));
+          d0[4 * v] = q0.x; d0[4 * v + 1] = q0.y; d0[4 * v + 2] = q0.z; d0[4 * v + 3] = q0.w;
+          d1[4 * v] = q1.x; d1[4 * v + 1] = q1.y; d1[4 * v + 2] = q1.z; d1[4 * v + 3] = q1.w;
+        }
+      }
+      float umin0 = 3.0e38f, umin1 = 3.0e38f;
+#pragma unroll
+      for (int c = 0; c < CPL; ++c) {
+        const float2 dy = fsub2(pn[c + 1], pp[c + 1]);
+        const float2 dx = make_float2(pp[c + 2].y - pp[c].y, pn[c + 2].x - pn[c].x);
+        const float2 s2 = ffma2(dx, dx, fmul2(dy, dy));
+        const float h0v = sqrt_approx(s2.x), h1v = sqrt_approx(s2.y);   // 2|grad phi|
+        const float vf0 = (MODEL == REGION) ? fmaf(A, d0[c], B) : d0[c];
+        const float vf1 = (MODEL == REGION) ? fmaf(A, d1[c], B) : d1[c];
+        const float u0 = fmaf(vf0, h0v, pp[c + 1].y);
+        const float u1 = fmaf(vf1, h1v, pn[c + 1].x);
+        ow[c] = __funnelshift_l(__float_as_uint(u0), ow[c], 1);
+        ow[c] = __funnelshift_l(__float_as_uint(u1), ow[c], 1);
+        umin0 = fminf(umin0, fabsf(u0));
+        umin1 = fminf(umin1, fabsf(u1));
+      }
+      if (umin0 <= eps_u) fbrows |= 1u << (h0 + 2 * s);
+      if (umin1 <= eps_u) fbrows |= 2u << (h0 + 2 * s);
+#pragma unroll
+      for (int c = 0; c < NP; ++c) pp[c] = pn[c];
+    }
+    cp_async_wait<0>();
+    // 16 appended sign bits: after the reversal rows h0 .. h0+15 sit in bits 16..31
+#pragma unroll
+    for (int c = 0; c < CPL; ++c) {
+      const uint32_t v = ~__brev(ow[c]) & 0xffff0000u;
+      ow[c] = h0 ? v : v >> 16;
+    }
+    while (fbrows) {
+      const int k = __ffs(fbrows) - 1;
+      fbrows &= fbrows - 1;
+      const uint32_t bitk = 1u << k;
+      uint32_t cols = update_tie_cols<R, MODEL, CPL, SRC>(P, lut_base, r, x0, k, A, B, eps_u);
+      while (cols) {
+        const int c = __ffs(cols) - 1;
+        cols &= cols - 1;
+        const bool pos = exact_u_fast<R, SRC>(tile_ctx(P, tile), tile_bits(P, tile),
+                                              y0 - tile_y0(P, tile) + k, x0 + c) > 0.0;
+#pragma unroll
+        for (int q = 0; q < CPL; ++q)
+          if (q == c) ow[q] = pos ? (ow[q] | bitk) : (ow[q] & ~bitk);
+      }
+    }
+  }
+#pragma unroll
+  for (int c = 0; c < CPL; ++c) ow[c] |= __shfl_xor_sync(0xffffffffu, ow[c], 16);
+  if (!act || h0) return;
+  uint32_t* dst = P.bits_out + (size_t)r * P.g.pitch_w + x0;
+#pragma unroll
+  for (int q = 0; q < CPL / 4; ++q)
+    reinterpret_cast<uint4*>(dst)[q] = make_uint4(ow[4 * q], ow[4 * q + 1], ow[4 * q + 2], ow[4 * q + 3]);
+}
+
 // The 2 KB t-LUT must sit at a 2 KB-aligned shared address for the OR-based
 // addressing of phi_row_int; static __shared__ alignment is not guaranteed
 // relative to the CTA's shared window, so it is carved out of a 4 KB buffer.
@@ -839,7 +964,8 @@ __device__ __noinline__ void border_update_unit(const FastParams& P, const float
 // so their longer latency overlaps the interior work of the other warps).
 // BATCH: every unit of every tile, [all border units][all interior units];
 // the tile's scalars (stop, A, B, guards) are read per unit.
-template <int R, int MODEL, int SRC, bool BATCH>
+// HALF: split-warp units of 128 columns (update_block_half) for small images.
+template <int R, int MODEL, int SRC, bool BATCH, bool HALF>
 __global__ void __launch_bounds__(kThreads, 4) k_update(FastParams P) {
   constexpr int CPL = kUpdCols;
   constexpr int NPAT = 1 << (2 * R + 1);
@@ -863,7 +989,7 @@ __global__ void __launch_bounds__(kThreads, 4) k_update(FastParams P) {
   float A = sc->A, B = sc->B, eps_u = sc->eps_u;
   const int lane = threadIdx.x & 31;
   const int nb = border_units(P.gu);
-  const int ni = interior_units(P.gu);
+  const int ni = HALF ? 2 * chunk_units(P.gu) + (P.gu.nB1 + 15) / 16 : interior_units(P.gu);
   const int T = BATCH ? P.ntiles : 1;
   const int nunits = T * (nb + ni);
   LSE_TRACE_DECL
@@ -896,13 +1022,51 @@ __global__ void __launch_bounds__(kThreads, 4) k_update(FastParams P) {
     const int iu = lu - nb;
     bool act = true;
     const int nch = chunk_units(P.gu);
-    if (iu < nch) {
+    if (HALF) {                                   // half chunks; lane pairs (L, L+16) share columns
+      if (iu < 2 * nch) {
+        const int ch = iu >> 1;
+        r = P.gu.r_lo + ch / P.gu.nci;
+        x0 = P.gu.xoff + (ch % P.gu.nci) * kUpdChunk + (iu & 1) * (kUpdChunk / 2) +
+             CPL * (lane & 15);
+      } else {
+        act = b1_lane(P.gu, 0, (iu - 2 * nch) * 16 + (lane & 15), r, x0);
+      }
+    } else if (iu < nch) {
       r = P.gu.r_lo + iu / P.gu.nci;
       x0 = P.gu.xoff + (iu % P.gu.nci) * kUpdChunk + CPL * lane;
     } else {
       act = b1_lane(P.gu, iu - nch, lane, r, x0);
     }
     if (BATCH) r += tile * P.tile_hr;             // row of the tile in the stacked arrays
+    if (HALF) {
+      // window words of this lane's half: rows r-1, r (rows 0-15) or r, r+1
+      uint32_t wlo[NT], whi[NT];
+      uint32_t a = ~0u, o = 0u;
+      if (act) {
+        const uint32_t* wp =
+            P.bits_in + (size_t)(r - 1 + (lane >> 4)) * P.g.pitch_w + (x0 - (R + 1));
+#pragma unroll
+        for (int j = 0; j < NT; ++j) {
+          wlo[j] = __ldg(wp + j);
+          whi[j] = __ldg(wp + P.g.pitch_w + j);
+          a &= wlo[j] & whi[j];
+          o |= wlo[j] | whi[j];
+        }
+      }
+      if (stopped || (P.skip_uniform && __all_sync(0xffffffffu, !act || a == ~0u || o == 0u))) {
+        if (!act || lane >= 16) continue;
+        uint32_t* dst = P.bits_out + (size_t)r * P.g.pitch_w + x0;
+#pragma unroll
+        for (int q = 0; q < CPL / 4; ++q)
+          reinterpret_cast<uint4*>(dst)[q] = make_uint4(whi[R + 1 + 4 * q], whi[R + 2 + 4 * q],
+                                                        whi[R + 3 + 4 * q], whi[R + 4 + 4 * q]);
+        continue;
+      }
+      update_block_half<R, MODEL, CPL, SRC>(P, (uint32_t)__cvta_generic_to_shared(s_lt),
+                                            s_ring + (threadIdx.x >> 5) * kRing2 * 32 * CPL, r,
+                                            x0, A, B, eps_u, wlo, whi, tile, act);
+      continue;
+    }
     uint32_t prev[NT], cur[NT];
     uint32_t a = ~0u, o = 0u;
     if (act) {
