@@ -974,8 +974,13 @@ __global__ void __launch_bounds__(kThreads, 4) k_update(FastParams P) {
   __shared__ float s_ls[NPAT];
   __shared__ __align__(16) float s_ring[(kThreads / 32) * kRing2 * 32 * CPL];
   LSE_TRACE_ENTRY
+  // the noinline border path reads the launch parameters from this shared
+  // copy: handing it the kernel parameter block itself would force a
+  // per-thread local-memory copy of the block (taking its address)
+  __shared__ FastParams s_P;
   float* const s_lt = aligned_lut(s_lt_raw);
   load_luts<R>(P, s_lt, s_ls);                   // static data: before the dependency wait
+  if (threadIdx.x == 0) s_P = P;
   __syncthreads();
   pdl_wait();
   pdl_launch_dependents();
@@ -1016,7 +1021,7 @@ __global__ void __launch_bounds__(kThreads, 4) k_update(FastParams P) {
     }
     int r = 0, x0 = 0;
     if (lu < nb) {
-      border_update_unit<R, MODEL, SRC, BATCH>(P, s_lt, s_ls, lu, tile, A, B, eps_u, stopped);
+      border_update_unit<R, MODEL, SRC, BATCH>(s_P, s_lt, s_ls, lu, tile, A, B, eps_u, stopped);
       continue;
     }
     const int iu = lu - nb;
@@ -1600,8 +1605,10 @@ __global__ void __launch_bounds__(kThreads, 4) k_partition(FastParams P) {
   __shared__ __align__(16) float s_lt_raw[1024];
   __shared__ float s_ls[NPAT];
   LSE_TRACE_ENTRY
+  __shared__ FastParams s_P;                     // see k_update
   float* const s_lt = aligned_lut(s_lt_raw);
   load_luts<R>(P, s_lt, s_ls);                   // static data: before the dependency wait
+  if (threadIdx.x == 0) s_P = P;
   __syncthreads();
   pdl_wait();
   pdl_launch_dependents();
@@ -1638,7 +1645,7 @@ __global__ void __launch_bounds__(kThreads, 4) k_partition(FastParams P) {
     }
     LaneDelta d{0.0, 0.0, 0, 0, 0ull};
     if (lu < nb) {
-      border_partition_unit<R, PART, CKPT, MASKONLY, BATCH>(P, s_lt, s_ls, lu, tile, part_t,
+      border_partition_unit<R, PART, CKPT, MASKONLY, BATCH>(s_P, s_lt, s_ls, lu, tile, part_t,
                                                            eps_phi, d);
     } else {
       const int iu = lu - nb;
