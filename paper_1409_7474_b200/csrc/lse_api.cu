@@ -156,6 +156,15 @@ struct lse_run {
   uint32_t* d_chg = nullptr;
   TilePartial* d_bpart = nullptr;
   unsigned long long* d_pmax = nullptr;   // per-CTA maxima of the band peak pass
+  // reusable device scratch for per-call buffers (mask read-back, injected
+  // signs, seed polygons, flags): no cudaMalloc / cudaFree -- each of which
+  // can stall the device -- on the per-job paths
+  unsigned char* d_scratch = nullptr;
+  size_t scratch_cap = 0;
+  double* d_poly = nullptr;
+  long long* d_offs = nullptr;
+  size_t poly_cap = 0, offs_cap = 0;
+  int* d_flag = nullptr;
   double img_absmax = 0.0;
   // state
   uint32_t* d_bits[2] = {nullptr, nullptr};
@@ -223,6 +232,43 @@ bool two_mean(int model) {
   return model == LSE_MODEL_REGION || model == LSE_MODEL_ZHANG || model == LSE_MODEL_BANDS;
 }
 bool is_bands(const lse_run* r) { return r->p.model == LSE_MODEL_BANDS; }
+
+// grow-only per-run scratch (its contents do not survive the call)
+template <typename T>
+int scratch(lse_run* r, size_t n, T** out) {
+  const size_t bytes = std::max<size_t>(n * sizeof(T), 256);
+  if (bytes > r->scratch_cap) {
+    if (r->d_scratch) {
+      cudaStreamSynchronize(r->st);
+      cudaFree(r->d_scratch);
+      r->d_scratch = nullptr;
+      r->scratch_cap = 0;
+    }
+    TRY(dalloc(&r->d_scratch, bytes));
+    r->scratch_cap = bytes;
+  }
+  *out = reinterpret_cast<T*>(r->d_scratch);
+  return LSE_OK;
+}
+
+template <typename T>
+int grow(lse_run* r, T** buf, size_t* cap, size_t n) {
+  if (n <= *cap) return LSE_OK;
+  if (*buf) {
+    cudaStreamSynchronize(r->st);
+    cudaFree(*buf);
+    *buf = nullptr;
+  }
+  TRY(dalloc(buf, n));
+  *cap = n;
+  return LSE_OK;
+}
+
+int run_flag(lse_run* r, int** out) {
+  if (!r->d_flag) TRY(dalloc(&r->d_flag, 4));
+  *out = r->d_flag;
+  return LSE_OK;
+}
 
 FastParams fast_params(lse_run* r) {
   FastParams P{};
@@ -706,7 +752,7 @@ int upload_bands(lse_run* r, const void* image, int fmt) {
   const long long pitch = r->g.data_pitch, stride = pitch * H;
   int* d_flag = nullptr;
   double* tmp64 = nullptr;
-  TRY(dalloc(&d_flag, 1));
+  TRY(run_flag(r, &d_flag));
   CK(cudaMemsetAsync(d_flag, 0, sizeof(int), r->st));
   if (fmt == LSE_IMAGE_F32) {
     for (int k = 0; k < K; ++k)
@@ -754,7 +800,6 @@ int upload_bands(lse_run* r, const void* image, int fmt) {
   }
   r->img_absmax = absmax;
   if (tmp64) cudaFree(tmp64);
-  cudaFree(d_flag);
   r->fp32_exact = !inexact;
   r->h_ctx.data32 = r->d_data32;
   r->h_ctx.data64 = nullptr;
@@ -779,7 +824,7 @@ int upload_image(lse_run* r, const void* image, int is_f32) {
   const long long pitch = r->g.data_pitch;
   double* tmp64 = nullptr;
   int* d_flag = nullptr;
-  TRY(dalloc(&d_flag, 1));
+  TRY(run_flag(r, &d_flag));
   CK(cudaMemsetAsync(d_flag, 0, sizeof(int), r->st));
   if (is_f32 == LSE_IMAGE_F32) {
     CK(cudaMemcpy2DAsync(r->d_data32, pitch * sizeof(float), image, W * sizeof(float),
@@ -858,7 +903,6 @@ int upload_image(lse_run* r, const void* image, int is_f32) {
   CK(cudaStreamSynchronize(r->st));
   r->img_absmax = r->h_scal->img_absmax;
   if (tmp64) cudaFree(tmp64);
-  cudaFree(d_flag);
   r->h_ctx.data32 = r->d_data32;
   r->h_ctx.data64 = r->d_data64;
   r->prepared = false;
@@ -874,10 +918,10 @@ int set_state(lse_run* r, const lse_phi0* s) {
     if (s->n_polys < 1) return fail(LSE_ERR_ARG, "at least one seed polygon is required");
     std::vector<long long> offs(s->n_polys + 1, 0);
     for (long long k = 0; k < s->n_polys; ++k) offs[k + 1] = offs[k] + s->poly_counts[k];
-    double* dxy = nullptr;
-    long long* doffs = nullptr;
-    TRY(dalloc(&dxy, 2 * offs.back()));
-    TRY(dalloc(&doffs, offs.size()));
+    TRY(grow(r, &r->d_poly, &r->poly_cap, 2 * offs.back()));
+    TRY(grow(r, &r->d_offs, &r->offs_cap, offs.size()));
+    double* dxy = r->d_poly;
+    long long* doffs = r->d_offs;
     CK(cudaMemcpyAsync(dxy, s->poly_xy, 2 * offs.back() * sizeof(double), cudaMemcpyHostToDevice,
                        r->st));
     CK(cudaMemcpyAsync(doffs, offs.data(), offs.size() * sizeof(long long), cudaMemcpyHostToDevice,
@@ -894,8 +938,6 @@ int set_state(lse_run* r, const lse_phi0* s) {
     unsigned long long cnt = 0;
     CK(cudaMemcpyAsync(&cnt, r->d_count, sizeof(cnt), cudaMemcpyDeviceToHost, r->st));
     CK(cudaStreamSynchronize(r->st));
-    cudaFree(dxy);
-    cudaFree(doffs);
     // (a row strip's seed count is global: the coordinator checks it)
     if (cnt == 0 && !r->strip)
       return fail(LSE_ERR_DEGENERATE_SEED, "seed polygons cover no pixel centers");
@@ -907,12 +949,11 @@ int set_state(lse_run* r, const lse_phi0* s) {
   } else if (s->kind == LSE_PHI0_SIGNS) {
     if (!(s->scale > 0.0) || !std::isfinite(s->scale)) return fail(LSE_ERR_ARG, "bad sign scale");
     signed char* d = nullptr;
-    TRY(dalloc(&d, r->npx));
+    TRY(scratch(r, r->npx, &d));
     CK(cudaMemcpyAsync(d, s->signs, r->npx, cudaMemcpyHostToDevice, r->st));
     k_pack_signs<<<gw, 128, 0, r->st>>>(d, r->d_bits[r->cur], r->g);
     CKL();
     CK(cudaStreamSynchronize(r->st));
-    cudaFree(d);
     r->mode = SRC_SCALED;
     r->scale = s->scale;
     r->field_valid = false;
@@ -941,7 +982,7 @@ int set_state(lse_run* r, const lse_phi0* s) {
         CKL();
         // compare bitwise
         int* d_ne = nullptr;
-        TRY(dalloc(&d_ne, 1));
+        TRY(run_flag(r, &d_ne));
         CK(cudaMemsetAsync(d_ne, 0, sizeof(int), r->st));
         const long long n = r->npx;
         const double* a = r->d_F[0];
@@ -951,7 +992,6 @@ int set_state(lse_run* r, const lse_phi0* s) {
         int ne = 1;
         CK(cudaMemcpyAsync(&ne, d_ne, sizeof(int), cudaMemcpyDeviceToHost, r->st));
         CK(cudaStreamSynchronize(r->st));
-        cudaFree(d_ne);
         if (!ne) {
           r->mode = src;
           break;
@@ -1405,19 +1445,18 @@ int lse_run_read_mask(lse_run* r, unsigned char* out, int inside_sign, int packe
   unsigned char* d_out = nullptr;
   if (packed) {
     const long long nbytes = (r->npx + 7) / 8;
-    TRY(dalloc(&d_out, nbytes));
+    TRY(scratch(r, nbytes, &d_out));
     k_mask_packed<<<(unsigned)((nbytes + 255) / 256), 256, 0, r->st>>>(r->d_mask, r->g, invert,
                                                                       d_out, nbytes);
     CKL();
     CK(cudaMemcpyAsync(out, d_out, nbytes, cudaMemcpyDeviceToHost, r->st));
   } else {
-    TRY(dalloc(&d_out, r->npx));
+    TRY(scratch(r, r->npx, &d_out));
     k_mask_u8<<<grid2(r->W, r->H), 128, 0, r->st>>>(r->d_mask, r->g, invert, d_out);
     CKL();
     CK(cudaMemcpyAsync(out, d_out, r->npx, cudaMemcpyDeviceToHost, r->st));
   }
   CK(cudaStreamSynchronize(r->st));
-  cudaFree(d_out);
   return LSE_OK;
 }
 
@@ -1766,7 +1805,8 @@ void lse_batch_destroy(lse_batch* b) {
 void lse_run_destroy(lse_run* r) {
   if (!r) return;
   if (r->st) cudaStreamSynchronize(r->st);
-  void* ptrs[] = {r->d_bands32, r->d_bands64, r->d_chg, r->d_bpart, r->d_pmax,
+  void* ptrs[] = {r->d_scratch, r->d_poly, r->d_offs, r->d_flag,
+                  r->d_bands32, r->d_bands64, r->d_chg, r->d_bpart, r->d_pmax,
                   r->d_work, r->d_part_fin, r->d_part_init, r->d_data32, r->d_data64, r->d_bits[0], r->d_bits[1], r->d_P, r->d_M,
                   r->d_mask, r->d_part, r->d_scal, r->d_lut_t, r->d_lut_s, r->d_ctx,
                   r->d_w64, r->d_keys, r->d_count, r->d_F[0], r->d_F[1], r->d_U, r->d_T};

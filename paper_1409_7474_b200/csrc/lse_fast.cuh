@@ -837,30 +837,22 @@ __device__ __forceinline__ void update_rows_border(const FastParams& P, const fl
     cm[j] = (xc >= 0 && xc < W) ? 0xffffffffu : 0u;
     win[j] = __funnelshift_r(word_at<false>(P, wr, xc), word_at<false>(P, wr + 1, xc), sh);
   }
-  // every data row of the range is requested up front (a border lane has
-  // only kBorderRows rows, so its latency is one load round trip)
-  float dd[kBorderRows][CPL];
+  float pm[NP], p0[NP], pn[NP], dcur[CPL], dnext[CPL];
+  uint32_t fbrows = 0u;
 #pragma unroll
-  for (int q = 0; q < kBorderRows; ++q) {
-#pragma unroll
-    for (int c = 0; c < CPL; ++c) dd[q][c] = 0.f;
-    load_data_row<false, CPL>(P, y0 + k0 + q, x0, dd[q]);
-  }
-  float pm[NP], p0[NP], pn[NP];
-  uint32_t tcols[kBorderRows];
-#pragma unroll
-  for (int c = 0; c < CPL; ++c) ow[c] = 0u;
+  for (int c = 0; c < CPL; ++c) { ow[c] = 0u; dcur[c] = 0.f; dnext[c] = 0.f; }
   phi_row<R, SRC, false, NT, NP>(P, win, cm, 0, y0 + k0 - 1, s_lt, s_ls, pm);
   phi_row<R, SRC, false, NT, NP>(P, win, cm, 1, y0 + k0, s_lt, s_ls, p0);
-#pragma unroll
-  for (int q = 0; q < kBorderRows; ++q) {
-    const int k = k0 + q;
+  load_data_row<false, CPL>(P, y0 + k0, x0, dcur);
+#pragma unroll 1
+  for (int k = k0; k < k0 + kBorderRows; ++k) {
     const int kk = k + 1;                        // phi row produced in this step
-    phi_row<R, SRC, false, NT, NP>(P, win, cm, q + 2, y0 + kk, s_lt, s_ls, pn);
+    if (kk < k0 + kBorderRows) load_data_row<false, CPL>(P, y0 + kk, x0, dnext);
+    phi_row<R, SRC, false, NT, NP>(P, win, cm, kk - k0 + 1, y0 + kk, s_lt, s_ls, pn);
     const int i = y0 + k;
-    tcols[q] = 0u;
     if (i < H) {
       const uint32_t bitk = 1u << k;
+      uint32_t fb = 0u;
 #pragma unroll
       for (int c = 0; c < CPL; ++c) {
         const int x = x0 + c;
@@ -871,26 +863,29 @@ __device__ __forceinline__ void update_rows_border(const FastParams& P, const fl
                          : (i == H - 1) ? 2.f * (p0[c + 1] - pm[c + 1]) : (pn[c + 1] - pm[c + 1]);
         const float h = sqrt_approx(fmaf(dx, dx, dy * dy));
         // h = 2|grad phi|; A, B (region) and the g plane (edge) carry dt/2
-        const float vf = (MODEL == REGION) ? fmaf(A, dd[q][c], B) : dd[q][c];
+        const float vf = (MODEL == REGION) ? fmaf(A, dcur[c], B) : dcur[c];
         const float u = fmaf(vf, h, p0[c + 1]);
         if (u > 0.f) ow[c] |= bitk;
-        if (fabsf(u) <= eps_u) tcols[q] |= 1u << c;
+        if (fabsf(u) <= eps_u) fb |= 1u << c;
       }
+      if (fb) fbrows |= bitk;
     }
 #pragma unroll
     for (int c = 0; c < NP; ++c) { pm[c] = p0[c]; p0[c] = pn[c]; }
+#pragma unroll
+    for (int c = 0; c < CPL; ++c) dcur[c] = dnext[c];
   }
+  while (fbrows) {                               // near ties: exact fp64 decisions
+    const int k = __ffs(fbrows) - 1;
+    fbrows &= fbrows - 1;
+    const uint32_t bitk = 1u << k;
+#pragma unroll 1
+    for (int c = 0; c < CPL; ++c) {
+      if (x0 + c >= W) break;
+      const bool pos = exact_u_fast<R, SRC>(P.ctx, P.bits_in, y0 + k, x0 + c) > 0.0;
 #pragma unroll
-  for (int q = 0; q < kBorderRows; ++q) {       // near ties: exact fp64 decisions
-    uint32_t cols = tcols[q];
-    const uint32_t bitk = 1u << (k0 + q);
-    while (cols) {
-      const int c = __ffs(cols) - 1;
-      cols &= cols - 1;
-      const bool pos = exact_u_fast<R, SRC>(P.ctx, P.bits_in, y0 + k0 + q, x0 + c) > 0.0;
-#pragma unroll
-      for (int w = 0; w < CPL; ++w)
-        if (w == c) ow[w] = pos ? (ow[w] | bitk) : (ow[w] & ~bitk);
+      for (int q = 0; q < CPL; ++q)
+        if (q == c) ow[q] = pos ? (ow[q] | bitk) : (ow[q] & ~bitk);
     }
   }
 }

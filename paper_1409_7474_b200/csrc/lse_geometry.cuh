@@ -25,7 +25,7 @@ namespace lse {
 //  kBorderQ lanes (lane = quarter * kBorderItems + item).  A row strip of a
 //  multi-GPU run drops the border rows it does not own (its halo rows,
 //  recomputed by their owner).
-constexpr int kBorderQ = 8;                      // row parts per border lane group
+constexpr int kBorderQ = 4;                      // row parts per border lane group
 constexpr int kBorderItems = 32 / kBorderQ;      // lane groups per border warp unit
 constexpr int kBorderRows = 32 / kBorderQ;       // rows per border lane
 struct Geo {
