@@ -306,9 +306,10 @@ FastParams fast_params(lse_run* r) {
   return P;
 }
 
-int fast_grid(long long warp_units) {
+// one wave of CTAs (ctas_per_sm resident per SM, the kernels' launch bound)
+int fast_grid(long long warp_units, int ctas_per_sm = 4) {
   const long long ctas = (warp_units + 3) / 4;
-  return (int)std::max<long long>(1, std::min<long long>(ctas, (long long)num_sms() * 4));
+  return (int)std::max<long long>(1, std::min<long long>(ctas, (long long)num_sms() * ctas_per_sm));
 }
 
 dim3 grid2(int W, int H, int bx = 128) { return dim3((W + bx - 1) / bx, H); }
@@ -492,7 +493,7 @@ int launch_update(lse_run* r, FastParams P) {
 template <int R, bool PART, bool CKPT, bool MASKONLY>
 int launch_partition(lse_run* r, FastParams P) {
   const long long n = r->nb_part + r->ni_part;
-  const int g = fast_grid(n);
+  const int g = fast_grid(n, kPartitionCtasPerSm);
   P.work_base = take_work(r, n, g);
 #ifdef LSE_UNIT_TRACE
   P.trace = MASKONLY ? nullptr : trace_begin(r, n, g, "partition", r->nb_part);
@@ -1600,7 +1601,7 @@ int batch_iteration(lse_batch* b, long long it, bool ckpt, int src, bool any_reg
   if (!any_region && !ckpt) return LSE_OK;
   P.bits_in = b->bits[b->cur];
   const long long n = (long long)b->T * (b->nb_part + b->ni_part);
-  const int g = fast_grid(n);
+  const int g = fast_grid(n, kPartitionCtasPerSm);
   P.work_base = batch_take_work(b, n, g);
   if (ckpt) TRY(launch_pdl(k_partition<R, true, true, false, true>, g, kThreads, b->st, P));
   else TRY(launch_pdl(k_partition<R, true, false, false, true>, g, kThreads, b->st, P));

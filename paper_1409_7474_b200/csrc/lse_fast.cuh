@@ -122,6 +122,7 @@ __device__ __forceinline__ unsigned long long lse_now() {
 #endif
 
 constexpr int kChunk = 256;      // partition: columns per warp chunk (32 lanes x 8 columns)
+constexpr int kPartitionCtasPerSm = 4;   // partition occupancy (launch bound and grid)
 constexpr int kUpdCols = 8;      // update: columns per lane
 constexpr int kUpdChunk = 32 * kUpdCols;   // update: columns per warp chunk
 
@@ -1594,7 +1595,7 @@ __device__ __noinline__ void border_partition_unit(const FastParams& P, const fl
 // partials in a fixed order.  BATCH: [all tiles' border units][all tiles'
 // interior units]; a tile's partials are reduced by its own finalize CTA.
 template <int R, bool PART, bool CKPT, bool MASKONLY, bool BATCH>
-__global__ void __launch_bounds__(kThreads, 4) k_partition(FastParams P) {
+__global__ void __launch_bounds__(kThreads, kPartitionCtasPerSm) k_partition(FastParams P) {
   constexpr int NPAT = 1 << (2 * R + 1);
   constexpr int NT = kColsPerThread + 2 * R;
   __shared__ __align__(16) float s_lt_raw[1024];
