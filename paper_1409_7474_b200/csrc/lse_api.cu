@@ -1105,7 +1105,7 @@ int create_impl(lse_run** out, const lse_params* p, long long height, long long 
     r->ni_upd_half = 2LL * (r->gu.r_hi - r->gu.r_lo) * r->gu.nci + (r->gu.nB1 + 15) / 16;
     // too few full units to keep every warp busy for several rounds: halve them
     const char* hv = std::getenv("LSE_HALF_UNITS");
-    r->half_units = hv ? std::atoi(hv) != 0 : r->ni_upd < 4LL * num_sms() * 16;
+    r->half_units = hv ? std::atoi(hv) != 0 : r->ni_upd < 2LL * num_sms() * 16;
     r->nb_upd[0] = border_units(r->gu);
     r->nb_upd[1] = r->gu_all.nA;
     // partition segments: >= ~8 interior units per resident warp, <= 16 chunks
