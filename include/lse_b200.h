@@ -19,7 +19,7 @@
 extern "C" {
 #endif
 
-#define LSE_ABI_VERSION 4
+#define LSE_ABI_VERSION 5
 
 #define LSE_OK 0
 #define LSE_ERR_ARG 1            /* ValueError in the reference               */
@@ -28,11 +28,13 @@ extern "C" {
 #define LSE_ERR_DEGENERATE 4     /* DegeneratePartitionError (grid.py:20)     */
 #define LSE_ERR_NODEVICE 5       /* no CUDA device visible                    */
 #define LSE_ERR_DEGENERATE_SEED 6 /* DegenerateSeedError (grid.py:16)         */
-#define LSE_ERR_UNSUPPORTED 7    /* model outside the device path (cv)        */
+#define LSE_ERR_UNSUPPORTED 7    /* configuration outside the device paths    */
 
 #define LSE_MODEL_EDGE 0         /* ModelKind.EDGE   (models.py:30)  E_Td, Eq. 14 */
 #define LSE_MODEL_REGION 1       /* ModelKind.REGION (models.py:31)  R_Td, Eq. 17 */
 #define LSE_MODEL_ZHANG 2        /* ModelKind.ZHANG  (models.py:33)  mean separation (models.py:144-162) */
+#define LSE_MODEL_CV 4           /* ModelKind.CHAN_VESE (models.py:32): curvature-regularized
+                                    baseline (models.py:122-141), distance re-init (generic path) */
 #define LSE_MODEL_BANDS 3        /* region data term summed over n_bands bands (
                                     a restatement -- the reference is single-band) */
 
@@ -57,6 +59,7 @@ typedef struct lse_params {
   const double* pre_weights; /* ts_pre values (edge model) */
   double nu;                 /* ModelParams.nu (zhang model speed constant) */
   int n_bands;               /* LSE_MODEL_BANDS: bands of the image (1..4), band-major */
+  double mu;                 /* ModelParams.mu (LSE_MODEL_CV curvature weight) */
 } lse_params;
 
 #define LSE_PHI0_FIELD 0     /* float64 (H, W) level-set field                 */
@@ -238,6 +241,14 @@ int lse_region_velocity(const double* image, const double* phi, long long h, lon
                         double* v_out, int* degenerate);
 int lse_edge_velocity(const double* g, const double* phi, long long h, long long w,
                       double* v_out);
+
+/* curvature (kernels.py:98-115), signed_distance (kernels.py:118-133; mask
+ * uint8 0/1, exact Euclidean, positive outside), cv_velocity (models.py:
+ * 122-141, eps_guard 1e-10 as the reference calls it). */
+int lse_curvature(const double* phi, long long h, long long w, double eps_guard, double* out);
+int lse_signed_distance(const unsigned char* mask, long long h, long long w, double* out);
+int lse_cv_velocity(const double* image, const double* phi, long long h, long long w, double mu,
+                    double* v_out);
 
 /* zhang_velocity (models.py:144-162); *degenerate as region_velocity. */
 int lse_zhang_velocity(const double* image, const double* phi, long long h, long long w, double nu,

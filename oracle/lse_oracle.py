@@ -33,6 +33,7 @@ import numpy as np
 REGION = "region"
 EDGE = "edge"
 ZHANG = "zhang"
+CV = "cv"
 DT_STABILITY_LIMIT = 25.0          # engine.py:26
 
 
@@ -255,6 +256,58 @@ def region_velocity(image: np.ndarray, phi: np.ndarray):
     return (data / peak) * gradient_magnitude(phi), False
 
 
+def curvature(phi: np.ndarray, eps_guard: float = 1e-10) -> np.ndarray:
+    """kernels.py:98-115 -- (pxx py^2 - 2 px py pxy + pyy px^2) / (px^2+py^2+eps)^1.5."""
+    px, py = gradient_central(phi)
+    pxx = np.gradient(px, axis=1)
+    pxy = np.gradient(px, axis=0)
+    pyy = np.gradient(py, axis=0)
+    num = pxx * py * py - 2.0 * px * py * pxy + pyy * px * px
+    den = np.power(px * px + py * py + eps_guard, 1.5)
+    return num / den
+
+
+def squared_edt(target: np.ndarray) -> np.ndarray:
+    """Exact squared Euclidean distance to the nearest True pixel (the quantity
+    scipy's distance_transform_edt takes the root of): per column the distance
+    to the nearest target, then per row min_x' g(x') + (x - x')^2, all in
+    integers."""
+    h, w = target.shape
+    inf = np.int64(1) << 40
+    ys = np.arange(h, dtype=np.int64)
+    g = np.full((h, w), inf, dtype=np.int64)
+    for x in range(w):
+        t = np.nonzero(target[:, x])[0]
+        if len(t):
+            g[:, x] = np.abs(ys[:, None] - t[None, :]).min(axis=1) ** 2
+    xs = np.arange(w, dtype=np.int64)
+    return (g[:, None, :] + (xs[None, :, None] - xs[None, None, :]) ** 2).min(axis=2)
+
+
+def signed_distance(mask: np.ndarray) -> np.ndarray:
+    """kernels.py:118-133 -- edt(~obj) - edt(obj): positive outside, centre to
+    centre, sqrt of integer squared distances."""
+    obj = np.asarray(mask, dtype=bool)
+    d_out = np.sqrt(squared_edt(obj).astype(np.float64))
+    d_in = np.sqrt(squared_edt(~obj).astype(np.float64))
+    d_out[obj] = 0.0
+    d_in[~obj] = 0.0
+    return d_out - d_in
+
+
+def cv_velocity(image: np.ndarray, phi: np.ndarray, mu: float, eps_guard: float = 1e-10):
+    """models.py:122-141 -- [(c+ - c-)(2I - c+ - c-) + mu kappa] |grad phi|."""
+    means = region_means(image, phi)
+    if means is None:
+        data = np.zeros_like(phi)
+    else:
+        c_plus, c_minus = means
+        data = (c_plus - c_minus) * (2.0 * image - c_plus - c_minus)
+    if mu != 0.0:
+        data = data + mu * curvature(phi, eps_guard)
+    return data * gradient_magnitude(phi)
+
+
 def region_velocity_bands(image: np.ndarray, phi: np.ndarray):
     """Multi-band region data term -- a restatement, the
     reference is single-band (grid.py:27-28): D = sum_k (c+_k - c-_k)(2 I_k -
@@ -311,6 +364,7 @@ class OracleParams:
     ts_pre: int = 9
     edge_gain: float = 255.0
     nu: float = 1.0
+    mu: float = 0.1
 
 
 def advance_once(phi, iteration, image, p: OracleParams, g, w_reg):
@@ -319,6 +373,8 @@ def advance_once(phi, iteration, image, p: OracleParams, g, w_reg):
         v, degenerate = edge_velocity(g, phi), False
     elif p.model == ZHANG:
         v, degenerate = zhang_velocity(image, phi, p.nu)
+    elif p.model == CV:
+        v, degenerate = cv_velocity(image, phi, p.mu), False
     elif image.ndim == 3:
         v, degenerate = region_velocity_bands(image, phi)
     else:
@@ -327,7 +383,12 @@ def advance_once(phi, iteration, image, p: OracleParams, g, w_reg):
     n = iteration + 1
     if np.isfinite(out).all():
         if p.reinit_period > 0 and n % p.reinit_period == 0:
-            out = binarize(out)
+            if p.model == CV:                        # engine.py:161-165
+                b = binarize(out)
+                if (b > 0).any() and (b < 0).any():
+                    out = -signed_distance(b > 0)
+            else:
+                out = binarize(out)
         if n % p.reg_period == 0:
             out = convolve_same(out, w_reg)
     if not np.isfinite(out).all():

@@ -29,6 +29,7 @@ LSE_MODEL_EDGE = 0
 LSE_MODEL_REGION = 1
 LSE_MODEL_ZHANG = 2
 LSE_MODEL_BANDS = 3
+LSE_MODEL_CV = 4
 LSE_PARTIAL_BYTES = 64
 LSE_IMAGE_F64, LSE_IMAGE_F32, LSE_IMAGE_RGB8 = 0, 1, 2
 
@@ -46,7 +47,7 @@ class LseParams(C.Structure):
                 ("max_iters", C.c_longlong), ("conv_check_every", C.c_longlong),
                 ("conv_window", C.c_longlong), ("sigma1", C.c_double), ("ts_pre", C.c_int),
                 ("edge_gain", C.c_double), ("reg_weights", _dp), ("pre_weights", _dp),
-                ("nu", C.c_double), ("n_bands", C.c_int)]
+                ("nu", C.c_double), ("n_bands", C.c_int), ("mu", C.c_double)]
 
 
 class LsePhi0(C.Structure):
@@ -114,6 +115,9 @@ _SIGS = {
     "lse_binarize": (_i, [_dp, _ll, _dp]),
     "lse_region_means": (_i, [_dp, _dp, _ll, _ll, _dp, _dp]),
     "lse_region_velocity": (_i, [_dp, _dp, _ll, _ll, _dp, C.POINTER(C.c_int)]),
+    "lse_curvature": (_i, [_dp, _ll, _ll, C.c_double, _dp]),
+    "lse_signed_distance": (_i, [C.POINTER(C.c_ubyte), _ll, _ll, _dp]),
+    "lse_cv_velocity": (_i, [_dp, _dp, _ll, _ll, C.c_double, _dp]),
     "lse_zhang_velocity": (_i, [_dp, _dp, _ll, _ll, C.c_double, _dp, C.POINTER(C.c_int)]),
     "lse_edge_velocity": (_i, [_dp, _dp, _ll, _ll, _dp]),
     "lse_rasterize_seeds": (_i, [_dp, _llp, _ll, _i, _ll, _ll, C.POINTER(C.c_byte)]),

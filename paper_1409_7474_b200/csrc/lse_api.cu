@@ -165,6 +165,15 @@ struct lse_run {
   long long* d_offs = nullptr;
   size_t poly_cap = 0, offs_cap = 0;
   int* d_flag = nullptr;
+  // Chan-Vese baseline: derivative planes and distance-transform scratch
+  double* d_px = nullptr;
+  double* d_py = nullptr;
+  double* d_mag = nullptr;
+  long long* d_edt_g = nullptr;
+  int* d_edt_v = nullptr;
+  long long* d_edt_zn = nullptr;
+  long long* d_edt_zd = nullptr;
+  double* d_dist[2] = {nullptr, nullptr};
   double img_absmax = 0.0;
   // state
   uint32_t* d_bits[2] = {nullptr, nullptr};
@@ -228,10 +237,13 @@ struct lse_run {
 
 namespace {
 
+// models whose velocity uses the two region means (partition sums each pass)
 bool two_mean(int model) {
-  return model == LSE_MODEL_REGION || model == LSE_MODEL_ZHANG || model == LSE_MODEL_BANDS;
+  return model == LSE_MODEL_REGION || model == LSE_MODEL_ZHANG || model == LSE_MODEL_BANDS ||
+         model == LSE_MODEL_CV;
 }
 bool is_bands(const lse_run* r) { return r->p.model == LSE_MODEL_BANDS; }
+bool is_cv(const lse_run* r) { return r->p.model == LSE_MODEL_CV; }
 
 // grow-only per-run scratch (its contents do not survive the call)
 template <typename T>
@@ -637,12 +649,68 @@ int collect(lse_run* r) {
 }
 
 bool fp32_ok(lse_run* r) {
+  if (is_cv(r)) return false;                    // continuous field: the fp64 path
   if (r->R < 1 || r->R > 4) return false;
   if (!(r->p.dt <= 1e6)) return false;
   if (two_mean(r->p.model) && !(r->img_absmax <= 1e6)) return false;
   if (r->p.model == LSE_MODEL_ZHANG && !(std::fabs(r->p.nu) <= 1e6)) return false;
   if (r->mode == SRC_SCALED && !(r->scale >= 1e-3 && r->scale <= 1e6)) return false;
   return true;
+}
+
+// -signed_distance(f > 0) of a dense field (engine.py:161-165) into out (may
+// alias f): two exact distance transforms (kernels.py:118-133).
+int edt_buffers(lse_run* r) {
+  if (r->d_edt_g) return LSE_OK;
+  TRY(dalloc(&r->d_edt_g, r->npx));
+  TRY(dalloc(&r->d_edt_v, r->npx));
+  TRY(dalloc(&r->d_edt_zn, (size_t)r->H * (r->W + 1)));
+  TRY(dalloc(&r->d_edt_zd, (size_t)r->H * (r->W + 1)));
+  TRY(dalloc(&r->d_dist[0], r->npx));
+  TRY(dalloc(&r->d_dist[1], r->npx));
+  return LSE_OK;
+}
+
+int neg_signed_distance(cudaStream_t st, const double* f, double* out, int H, int W,
+                        long long* g, int* v, long long* zn, long long* zd, double* d0,
+                        double* d1) {
+  for (int pos = 0; pos < 2; ++pos) {
+    k_edt_cols<<<(W + 127) / 128, 128, 0, st>>>(f, H, W, pos, g);
+    CKL();
+    k_edt_rows<<<(H + 127) / 128, 128, 0, st>>>(g, H, W, v, zn, zd, pos ? d1 : d0);
+    CKL();
+  }
+  k_sdf_combine<<<num_sms() * 8, 256, 0, st>>>(f, d0, d1, out, (long long)H * W);
+  CKL();
+  return LSE_OK;
+}
+
+int run_neg_sdf(lse_run* r, const double* f, double* out) {
+  TRY(edt_buffers(r));
+  return neg_signed_distance(r->st, f, out, r->H, r->W, r->d_edt_g, r->d_edt_v, r->d_edt_zn,
+                             r->d_edt_zd, r->d_dist[0], r->d_dist[1]);
+}
+
+double key_to_double(long long q) {
+  const long long b = q ^ ((q >> 63) & 0x7fffffffffffffffLL);
+  double d;
+  std::memcpy(&d, &b, 8);
+  return d;
+}
+
+// min / max of a dense field (re-init guard: both signs present?)
+int field_minmax(lse_run* r, const double* f, double* mn, double* mx) {
+  long long init[3] = {LLONG_MAX, LLONG_MIN, LLONG_MIN};
+  CK(cudaMemcpyAsync(r->d_keys, init, sizeof(init), cudaMemcpyHostToDevice, r->st));
+  k_minmax<<<std::min(r->H, num_sms() * 8), 256, 0, r->st>>>(nullptr, f, r->H, r->W, r->W,
+                                                            r->d_keys);
+  CKL();
+  long long k[3];
+  CK(cudaMemcpyAsync(k, r->d_keys, sizeof(k), cudaMemcpyDeviceToHost, r->st));
+  CK(cudaStreamSynchronize(r->st));
+  *mn = key_to_double(k[0]);
+  *mx = key_to_double(k[1]);
+  return LSE_OK;
 }
 
 int generic_iteration(lse_run* r, long long it, bool reinit_now, bool reg_now, bool ckpt) {
@@ -653,7 +721,20 @@ int generic_iteration(lse_run* r, long long it, bool reinit_now, bool reg_now, b
   TRY(materialize(r));
   CK(cudaMemsetAsync(&r->d_scal->nonfinite, 0, sizeof(int), r->st));
   const double* phi = r->d_F[r->curF];
-  if (two_mean(r->p.model))
+  const bool cv = is_cv(r);
+  if (cv) {
+    // models.py:122-141 on the fp64 field
+    if (!r->d_px) {
+      TRY(dalloc(&r->d_px, r->npx));
+      TRY(dalloc(&r->d_py, r->npx));
+      TRY(dalloc(&r->d_mag, r->npx));
+    }
+    k_gradient<<<grid2(r->W, r->H), 128, 0, r->st>>>(phi, r->H, r->W, r->d_px, r->d_py, r->d_mag);
+    CKL();
+    k_cv_update<<<grid2(r->W, r->H), 128, 0, r->st>>>(
+        phi, r->d_px, r->d_py, r->d_mag, r->d_U, r->H, r->W, r->d_data32, r->d_data64,
+        r->g.data_pitch, r->d_scal, r->p.dt, r->p.mu, 1e-10);
+  } else if (two_mean(r->p.model))
     k_gen_update<REGION><<<grid2(r->W, r->H), 128, 0, r->st>>>(
         phi, r->d_U, r->H, r->W, r->d_data32, r->d_data64, r->g.data_pitch, r->d_scal, r->p.dt);
   else
@@ -662,7 +743,13 @@ int generic_iteration(lse_run* r, long long it, bool reinit_now, bool reg_now, b
   CKL();
   // the reference skips reinit/smoothing when u is not finite and raises
   // either way; computing them regardless is harmless (phi is not committed)
-  if (reinit_now) {
+  if (reinit_now && cv) {
+    // rebuild the distance field around the zero set when both classes exist
+    // (engine.py:161-165); otherwise u is kept as it is
+    double mn, mx;
+    TRY(field_minmax(r, r->d_U, &mn, &mx));
+    if (mx > 0.0 && mn <= 0.0) TRY(run_neg_sdf(r, r->d_U, r->d_U));
+  } else if (reinit_now) {
     k_binarize<<<num_sms() * 8, 256, 0, r->st>>>(r->d_U, r->d_U, r->npx);
     CKL();
   }
@@ -687,7 +774,7 @@ int generic_iteration(lse_run* r, long long it, bool reinit_now, bool reg_now, b
   r->curF ^= 1;
   r->mode = SRC_FIELD;
   r->field_valid = true;
-  if (reinit_now && reg_now && r->R >= 1 && r->R <= 4) {
+  if (!cv && reinit_now && reg_now && r->R >= 1 && r->R <= 4) {
     // phi = G * b exactly: carry the state as bits from here on
     k_pack_bits<<<dim3((r->g.pitch_w + 127) / 128, r->g.HR), 128, 0, r->st>>>(r->d_U,
                                                                               r->d_bits[r->cur],
@@ -1003,6 +1090,19 @@ int set_state(lse_run* r, const lse_phi0* s) {
   } else {
     return fail(LSE_ERR_ARG, "unknown state kind");
   }
+  if (is_cv(r) && s->kind == LSE_PHI0_POLYGONS) {
+    // init_state (engine.py:128-132): the distance field of the seed mask,
+    // -signed_distance(phi0 > 0) for either inside sign
+    TRY(ensure_generic(r));
+    r->curF = 0;
+    TRY(upload_ctx(r));
+    k_phi_from_bits<<<grid2(W, H), 128, 0, r->st>>>(r->d_bits[r->cur], r->d_F[0], r->d_ctx,
+                                                     SRC_SCALED);
+    CKL();
+    TRY(run_neg_sdf(r, r->d_F[0], r->d_F[0]));
+    r->mode = SRC_FIELD;
+    r->field_valid = true;
+  }
   r->iteration = s->iteration;
   r->converged = s->converged != 0;
   r->degenerate = s->degenerate != 0;
@@ -1047,7 +1147,9 @@ int create_impl(lse_run** out, const lse_params* p, long long height, long long 
   if (height < 2 || width < 2) return fail(LSE_ERR_ARG, "gradient needs at least a 2x2 field");
   if (height > (1LL << 30) || width > (1LL << 30)) return fail(LSE_ERR_ARG, "grid too large");
   if (!two_mean(p->model) && p->model != LSE_MODEL_EDGE)
-    return fail(LSE_ERR_UNSUPPORTED, "only the region, zhang and edge models run on the device path");
+    return fail(LSE_ERR_UNSUPPORTED, "unknown model");
+  if (p->model == LSE_MODEL_CV && (height < 3 || width < 3))
+    return fail(LSE_ERR_ARG, "curvature needs at least a 3x3 field");
   if (p->ts_reg < 1 || p->ts_reg % 2 == 0 || !p->reg_weights)
     return fail(LSE_ERR_ARG, "ts_reg must be an odd number >= 1");
   if (p->ts_reg > 63) return fail(LSE_ERR_ARG, "ts_reg > 63 is not supported");
@@ -1166,6 +1268,7 @@ int create_impl(lse_run** out, const lse_params* p, long long height, long long 
   r->h_ctx.model = p->model == LSE_MODEL_REGION  ? REGION
                    : p->model == LSE_MODEL_ZHANG ? ZHANG
                    : p->model == LSE_MODEL_BANDS ? VECTOR
+                   : p->model == LSE_MODEL_CV    ? CHAN_VESE
                                                  : EDGE;
   cudaMemcpyAsync(r->d_w64, r->h_ctx.w64, 32 * sizeof(double), cudaMemcpyHostToDevice, r->st);
   // LUTs for the fast path (R <= 4)
@@ -1806,7 +1909,9 @@ void lse_batch_destroy(lse_batch* b) {
 void lse_run_destroy(lse_run* r) {
   if (!r) return;
   if (r->st) cudaStreamSynchronize(r->st);
-  void* ptrs[] = {r->d_scratch, r->d_poly, r->d_offs, r->d_flag,
+  void* ptrs[] = {r->d_px, r->d_py, r->d_mag, r->d_edt_g, r->d_edt_v, r->d_edt_zn,
+                  r->d_edt_zd, r->d_dist[0], r->d_dist[1],
+                  r->d_scratch, r->d_poly, r->d_offs, r->d_flag,
                   r->d_bands32, r->d_bands64, r->d_chg, r->d_bpart, r->d_pmax,
                   r->d_work, r->d_part_fin, r->d_part_init, r->d_data32, r->d_data64, r->d_bits[0], r->d_bits[1], r->d_P, r->d_M,
                   r->d_mask, r->d_part, r->d_scal, r->d_lut_t, r->d_lut_s, r->d_ctx,
@@ -2035,6 +2140,86 @@ int two_mean_velocity(const double* image, const double* phi, long long h, long 
 int lse_region_velocity(const double* image, const double* phi, long long h, long long w,
                         double* v_out, int* degenerate) {
   return two_mean_velocity(image, phi, h, w, REGION, 0.0, v_out, degenerate);
+}
+
+int lse_curvature(const double* phi, long long h, long long w, double eps_guard, double* out) {
+  if (!phi || !out) return fail(LSE_ERR_ARG, "bad arguments");
+  if (!(eps_guard > 0.0)) return fail(LSE_ERR_ARG, "eps_guard must be positive");
+  if (h < 3 || w < 3) return fail(LSE_ERR_ARG, "curvature needs at least a 3x3 field");
+  TRY(check_device());
+  const long long n = h * w;
+  DevBuf a, px, py, k;
+  TRY(dbuf<double>(a, n));
+  TRY(dbuf<double>(px, n));
+  TRY(dbuf<double>(py, n));
+  TRY(dbuf<double>(k, n));
+  CK(cudaMemcpy(a.p, phi, n * sizeof(double), cudaMemcpyHostToDevice));
+  k_gradient<<<grid2((int)w, (int)h), 128>>>((double*)a.p, (int)h, (int)w, (double*)px.p,
+                                             (double*)py.p, nullptr);
+  CKL();
+  k_curvature<<<grid2((int)w, (int)h), 128>>>((double*)px.p, (double*)py.p, (int)h, (int)w,
+                                              eps_guard, (double*)k.p);
+  CKL();
+  CK(cudaMemcpy(out, k.p, n * sizeof(double), cudaMemcpyDeviceToHost));
+  return LSE_OK;
+}
+
+int lse_signed_distance(const unsigned char* mask, long long h, long long w, double* out) {
+  if (!mask || !out || h < 1 || w < 1) return fail(LSE_ERR_ARG, "bad arguments");
+  TRY(check_device());
+  const long long n = h * w;
+  long long objs = 0;
+  for (long long q = 0; q < n; ++q) objs += mask[q] != 0;
+  if (objs == 0) return fail(LSE_ERR_ARG, "mask has no object pixels");
+  if (objs == n) return fail(LSE_ERR_ARG, "mask has no background pixels");
+  std::vector<double> f(n);
+  for (long long q = 0; q < n; ++q) f[q] = mask[q] ? 1.0 : -1.0;
+  DevBuf a, g, v, zn, zd, d0, d1, o;
+  TRY(dbuf<double>(a, n));
+  TRY(dbuf<long long>(g, n));
+  TRY(dbuf<int>(v, n));
+  TRY(dbuf<long long>(zn, h * (w + 1)));
+  TRY(dbuf<long long>(zd, h * (w + 1)));
+  TRY(dbuf<double>(d0, n));
+  TRY(dbuf<double>(d1, n));
+  TRY(dbuf<double>(o, n));
+  CK(cudaMemcpy(a.p, f.data(), n * sizeof(double), cudaMemcpyHostToDevice));
+  TRY(neg_signed_distance(0, (double*)a.p, (double*)o.p, (int)h, (int)w, (long long*)g.p,
+                          (int*)v.p, (long long*)zn.p, (long long*)zd.p, (double*)d0.p,
+                          (double*)d1.p));
+  CK(cudaMemcpy(out, o.p, n * sizeof(double), cudaMemcpyDeviceToHost));
+  for (long long q = 0; q < n; ++q) out[q] = -out[q];   // positive outside (kernels.py:131-133)
+  return LSE_OK;
+}
+
+int lse_cv_velocity(const double* image, const double* phi, long long h, long long w, double mu,
+                    double* v_out) {
+  if (!image || !phi || !v_out) return fail(LSE_ERR_ARG, "bad arguments");
+  if (h < 3 || w < 3) return fail(LSE_ERR_ARG, "curvature needs at least a 3x3 field");
+  TRY(check_device());
+  const long long n = h * w;
+  DevBuf a, b, px, py, mag, v, sc;
+  TRY(dbuf<double>(a, n));
+  TRY(dbuf<double>(b, n));
+  TRY(dbuf<double>(px, n));
+  TRY(dbuf<double>(py, n));
+  TRY(dbuf<double>(mag, n));
+  TRY(dbuf<double>(v, n));
+  TRY(dbuf<Scalars>(sc, 1));
+  CK(cudaMemcpy(a.p, image, n * sizeof(double), cudaMemcpyHostToDevice));
+  CK(cudaMemcpy(b.p, phi, n * sizeof(double), cudaMemcpyHostToDevice));
+  Scalars hs;
+  TRY(region_scalars((double*)a.p, (double*)b.p, (int)h, (int)w, (Scalars*)sc.p, &hs));
+  k_gradient<<<grid2((int)w, (int)h), 128>>>((double*)b.p, (int)h, (int)w, (double*)px.p,
+                                             (double*)py.p, (double*)mag.p);
+  CKL();
+  k_cv_update<<<grid2((int)w, (int)h), 128>>>(nullptr, (double*)px.p, (double*)py.p,
+                                              (double*)mag.p, (double*)v.p, (int)h, (int)w,
+                                              nullptr, (double*)a.p, w, (Scalars*)sc.p, 0.0, mu,
+                                              1e-10);
+  CKL();
+  CK(cudaMemcpy(v_out, v.p, n * sizeof(double), cudaMemcpyDeviceToHost));
+  return LSE_OK;
 }
 
 int lse_zhang_velocity(const double* image, const double* phi, long long h, long long w, double nu,

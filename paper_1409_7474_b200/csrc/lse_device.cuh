@@ -23,7 +23,7 @@ constexpr int kSpanMax = kColsPerThread * kThreads + 16;
 
 // ZHANG and VECTOR run the REGION kernels (their data term is an affine image
 // of one fp32 data plane); VECTOR = region data term summed over K bands
-enum Model : int { EDGE = 0, REGION = 1, ZHANG = 2, VECTOR = 3 };
+enum Model : int { EDGE = 0, REGION = 1, ZHANG = 2, VECTOR = 3, CHAN_VESE = 4 };
 constexpr int kMaxBands = 4;
 enum Src : int { SRC_SMOOTH = 0, SRC_SCALED = 1, SRC_FIELD = 2 };
 

@@ -100,6 +100,146 @@ __global__ void k_gradient(const double* __restrict__ f, int H, int W, double* f
   if (mag_out) mag_out[o] = np_hypot(fx, fy);
 }
 
+// ----------------------------------------------------- Chan-Vese baseline
+// Mean curvature (kernels.py:98-115) at (i, x) from the first derivatives px,
+// py (np.gradient of phi) with numpy's operation order:
+//   num = pxx*py*py - 2*px*py*pxy + pyy*px*px,  den = (px*px + py*py + eps)^1.5
+__device__ __forceinline__ double cv_curvature(const double* px, const double* py, int H, int W,
+                                               int i, int x, double eps) {
+  double pxx, pxy, t, pyy;
+  np_gradient(px, H, W, i, x, pxx, pxy);      // d/dx, d/dy of px
+  np_gradient(py, H, W, i, x, t, pyy);        // d/dy of py
+  const size_t o = (size_t)i * W + x;
+  const double ax = px[o], ay = py[o];
+  const double num = dadd(dsub(dmul(dmul(pxx, ay), ay), dmul(dmul(dmul(2.0, ax), ay), pxy)),
+                          dmul(dmul(pyy, ax), ax));
+  const double den = pow(dadd(dadd(dmul(ax, ax), dmul(ay, ay)), eps), 1.5);
+  return ddiv(num, den);
+}
+
+// u = phi + dt * v for the curvature-regularized baseline (models.py:122-141,
+// engine.py:155-157): v = [(c+ - c-)(2I - c+ - c-) + mu * kappa] * |grad phi|,
+// the data term zero when a side is empty; px/py/mag from k_gradient.
+__global__ void k_cv_update(const double* __restrict__ phi, const double* __restrict__ px,
+                            const double* __restrict__ py, const double* __restrict__ mag,
+                            double* __restrict__ u, int H, int W,
+                            const float* __restrict__ data32, const double* __restrict__ data64,
+                            long long dpitch, Scalars* sc, double dt, double mu, double eps) {
+  const int x = blockIdx.x * blockDim.x + threadIdx.x;
+  const int i = blockIdx.y;
+  if (x >= W) return;
+  const size_t o = (size_t)i * W + x;
+  double data = 0.0;                             // models.py:133-137: zero with an empty side
+  if (sc->n_pos != 0 && sc->n_pos != sc->n_total) {
+    const size_t od = (size_t)i * dpitch + x;
+    const double I = data64 ? data64[od] : (double)data32[od];
+    data = dmul(sc->dc, dsub(dsub(dmul(2.0, I), sc->c_pos), sc->c_neg));
+  }
+  if (mu != 0.0) data = dadd(data, dmul(mu, cv_curvature(px, py, H, W, i, x, eps)));
+  const double v = dmul(data, mag[o]);
+  if (!phi) {                                    // velocity only (cv_velocity)
+    u[o] = v;
+    return;
+  }
+  const double out = dadd(phi[o], dmul(dt, v));
+  u[o] = out;
+  if (!isfinite(out)) sc->nonfinite = 1;
+}
+
+__global__ void k_curvature(const double* __restrict__ px, const double* __restrict__ py, int H,
+                            int W, double eps, double* __restrict__ out) {
+  const int x = blockIdx.x * blockDim.x + threadIdx.x;
+  const int i = blockIdx.y;
+  if (x >= W) return;
+  out[(size_t)i * W + x] = cv_curvature(px, py, H, W, i, x, eps);
+}
+
+// Exact Euclidean distance transform (scipy.ndimage.distance_transform_edt,
+// kernels.py:118-133): squared distances in integers (column pass, then the
+// lower envelope of parabolas per row, Felzenszwalb-Huttenlocher, with exact
+// fraction comparisons), sqrt correctly rounded.  target(q) = pixel q is a
+// "zero" of the transform: the pixels whose distance to the nearest target is
+// measured.  Column pass: g = (distance to the nearest target in the column)^2.
+constexpr long long kEdtInf = 1LL << 60;
+__global__ void k_edt_cols(const double* __restrict__ field, int H, int W, int target_positive,
+                           long long* __restrict__ g) {
+  const int x = blockIdx.x * blockDim.x + threadIdx.x;
+  if (x >= W) return;
+  auto is_target = [&](int i) {
+    const bool pos = field[(size_t)i * W + x] > 0.0;
+    return target_positive ? pos : !pos;
+  };
+  long long last = -1;                          // forward: distance to a target above
+  for (int i = 0; i < H; ++i) {
+    if (is_target(i)) last = i;
+    g[(size_t)i * W + x] = last < 0 ? kEdtInf : (long long)(i - last);
+  }
+  last = -1;
+  for (int i = H - 1; i >= 0; --i) {            // backward: below; keep the nearer
+    if (is_target(i)) last = i;
+    long long d = g[(size_t)i * W + x];
+    if (last >= 0 && (long long)(last - i) < d) d = last - i;
+    g[(size_t)i * W + x] = d >= kEdtInf ? kEdtInf : d * d;
+  }
+}
+
+// Row pass: D(i, x) = min_x' g(i, x') + (x - x')^2.  One thread per row; v / zn
+// / zd are per-row scratch (W entries each, W + 1 for the breakpoints).
+__global__ void k_edt_rows(const long long* __restrict__ g, int H, int W, int* __restrict__ vbuf,
+                           long long* __restrict__ znum, long long* __restrict__ zden,
+                           double* __restrict__ dist) {
+  const int i = blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= H) return;
+  const long long* gr = g + (size_t)i * W;
+  int* v = vbuf + (size_t)i * W;
+  long long* zn = znum + (size_t)i * (W + 1);
+  long long* zd = zden + (size_t)i * (W + 1);
+  int k = -1;
+  for (int q = 0; q < W; ++q) {
+    if (gr[q] >= kEdtInf) continue;
+    const long long fq = gr[q] + (long long)q * q;
+    while (k >= 0) {
+      // intersection with the parabola at v[k]: s = (fq - fv) / (2 (q - v[k]))
+      const long long fv = gr[v[k]] + (long long)v[k] * v[k];
+      const long long sn = fq - fv, sd = 2LL * (q - v[k]);
+      // pop while s <= z[k] (fractions, positive denominators)
+      if (k > 0 && sn * zd[k] <= zn[k] * sd) { --k; continue; }
+      ++k;
+      v[k] = q;
+      zn[k] = sn;
+      zd[k] = sd;
+      break;
+    }
+    if (k < 0) {
+      k = 0;
+      v[0] = q;
+      zn[0] = -(1LL << 40);                      // -infinity
+      zd[0] = 1;
+    }
+  }
+  double* out = dist + (size_t)i * W;
+  if (k < 0) {                                   // no target anywhere in reach
+    for (int x = 0; x < W; ++x) out[x] = INFINITY;
+    return;
+  }
+  int j = 0;
+  for (int x = 0; x < W; ++x) {
+    while (j < k && zn[j + 1] <= (long long)x * zd[j + 1]) ++j;   // x >= z[j+1]
+    const long long dx = x - v[j];
+    out[x] = __dsqrt_rn((double)(gr[v[j]] + dx * dx));
+  }
+}
+
+// -signed_distance(field > 0) (engine.py:161-165): +distance to the nearest
+// non-positive pixel inside, -distance to the nearest positive pixel outside.
+__global__ void k_sdf_combine(const double* __restrict__ field, const double* __restrict__ d_to_neg,
+                              const double* __restrict__ d_to_pos, double* __restrict__ out,
+                              long long n) {
+  for (long long q = (long long)blockIdx.x * blockDim.x + threadIdx.x; q < n;
+       q += (long long)gridDim.x * blockDim.x)
+    out[q] = field[q] > 0.0 ? d_to_neg[q] : -d_to_pos[q];
+}
+
 // u = phi + dt * v on a dense field (engine.py:155-157) + finiteness flag
 // (engine.py:159).  data: I (region) or g (edge), exact values.
 template <int MODEL>

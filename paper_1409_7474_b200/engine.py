@@ -142,10 +142,8 @@ class _DeviceState(EvolutionState):
 
 
 def _require_device_model(model: ModelKind):
-    if model not in (ModelKind.REGION, ModelKind.EDGE, ModelKind.ZHANG):
-        raise NotImplementedError(
-            f"model {model.value!r} is a classical baseline outside the B200 hot path; "
-            "only 'region' (R_Td), 'edge' (E_Td) and 'zhang' run here")
+    if model not in (ModelKind.REGION, ModelKind.EDGE, ModelKind.ZHANG, ModelKind.CHAN_VESE):
+        raise NotImplementedError(f"unknown model {model!r}")
 
 
 def _native_params(params: EvolutionParams, max_iters=None, conv_check_every=None):
@@ -154,7 +152,7 @@ def _native_params(params: EvolutionParams, max_iters=None, conv_check_every=Non
     wpre = np.ascontiguousarray(gaussian_kernel(mp.sigma1, mp.ts_pre).axis_weights)
     p = N.LseParams()
     p.model = {ModelKind.REGION: N.LSE_MODEL_REGION, ModelKind.ZHANG: N.LSE_MODEL_ZHANG,
-               ModelKind.EDGE: N.LSE_MODEL_EDGE}[params.model]
+               ModelKind.EDGE: N.LSE_MODEL_EDGE, ModelKind.CHAN_VESE: N.LSE_MODEL_CV}[params.model]
     p.dt = float(params.dt)
     p.sigma2 = float(params.sigma2)
     p.ts_reg = int(params.ts_reg)
@@ -170,6 +168,7 @@ def _native_params(params: EvolutionParams, max_iters=None, conv_check_every=Non
     p.reg_weights = N.dptr(wreg)
     p.pre_weights = N.dptr(wpre)
     p.nu = float(mp.nu)
+    p.mu = float(mp.mu)
     return p, (wreg, wpre)
 
 
@@ -251,10 +250,13 @@ def init_state(image: np.ndarray, seeds: SeedSpec,
                params: EvolutionParams) -> EvolutionState:
     """engine.py:123-133: rasterize the seeds into the binary initial field."""
     image = as_field(image)
-    if params.model is ModelKind.CHAN_VESE:
-        raise NotImplementedError("the CV baseline's distance-field init is not built here")
     h, w = image.shape
-    return EvolutionState(phi=rasterize_seeds(seeds, w, h), iteration=0)
+    phi0 = rasterize_seeds(seeds, w, h)
+    if params.model is ModelKind.CHAN_VESE:             # engine.py:129-132
+        from .kernels import signed_distance
+        sd = signed_distance(phi0 == seeds.inside_sign)
+        phi0 = sd if seeds.inside_sign < 0 else -sd
+    return EvolutionState(phi=phi0, iteration=0)
 
 
 def step(state: EvolutionState, image: np.ndarray,

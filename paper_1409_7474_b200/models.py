@@ -2,11 +2,10 @@
 
 The two fast evolutions of the paper run on the device: the edge-based
 E_Td (Eq. 14; speed g * |grad phi|) and the region-based R_Td (Eq. 17;
-max-normalized two-mean contrast times |grad phi|), plus the mean-separation
-baseline `zhang_velocity`, which shares the region kernels (only the
-finalize coefficients differ).  The curvature-regularized CV baseline
-(`cv_velocity`) is outside this build and raises NotImplementedError rather
-than silently running on the CPU.
+max-normalized two-mean contrast times |grad phi|), plus the two baselines:
+the mean-separation `zhang_velocity`, which shares the region kernels (only
+the finalize coefficients differ), and the curvature-regularized
+`cv_velocity`, which runs on the fp64 field path.
 """
 
 from __future__ import annotations
@@ -105,8 +104,25 @@ def region_velocity(image: np.ndarray, phi: np.ndarray) -> tuple[np.ndarray, boo
 
 
 def cv_velocity(image, phi, mu, eps_guard=1e-10):
-    """models.py:122-141 -- classical CV baseline; not part of this build."""
-    raise NotImplementedError("the curvature-regularized CV baseline is not built here")
+    """models.py:122-141: [(c+ - c-)(2I - c+ - c-) + mu * kappa] * |grad phi|,
+    un-normalized; the data term is zero when a side is empty (device)."""
+    image = N.f64(image)
+    phi = N.f64(phi)
+    if image.shape != phi.shape:
+        raise ValueError("image and phi shapes differ")
+    if eps_guard != 1e-10 and mu != 0.0:
+        from .kernels import curvature, gradient_magnitude
+        from .grid import region_means, DegeneratePartitionError
+        try:
+            c_plus, c_minus = region_means(image, phi)
+            data = (c_plus - c_minus) * (2.0 * image - c_plus - c_minus)
+        except DegeneratePartitionError:
+            data = np.zeros_like(phi)
+        return (data + mu * curvature(phi, eps_guard)) * gradient_magnitude(phi)
+    out = np.empty_like(phi)
+    N.check(N.lib.lse_cv_velocity(N.dptr(image), N.dptr(phi), phi.shape[0], phi.shape[1],
+                                  float(mu), N.dptr(out)))
+    return out
 
 
 def zhang_velocity(image, phi, nu):

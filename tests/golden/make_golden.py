@@ -128,6 +128,7 @@ def trajectory(name, image, seeds, prm, record, store=None):
                               p.model_params.edge_gain])
     out["model"] = np.array(p.model.value)
     out["nu"] = np.array(p.model_params.nu)
+    out["mu"] = np.array(p.model_params.mu)
     print(f"{name}: iters={r.state.iteration} conv={r.converged} err={err} "
           f"{time.perf_counter() - t0:.2f}s")
     return out
@@ -237,6 +238,30 @@ def main():
         fixtures[f"traj_a4_{'neg' if sign < 0 else 'pos'}"] = trajectory(
             f"a4_{sign}", a1, SeedSpec(polygons=(square(28, 28, 100, 100),), inside_sign=sign),
             params(ModelKind.ZHANG, nu=1.0, max_iters=1000), [1000], store="hash")
+
+    # curvature-regularized Chan-Vese baseline (models.py:122-141, kernels.py:98-133)
+    from lsekit import curvature, signed_distance, cv_velocity, init_state
+    cr = np.random.default_rng(47)
+    cvu = {}
+    for k in range(3):
+        h, w = 13 + 5 * k, 17 + 3 * k
+        m = cr.random((h, w)) > 0.6 + 0.1 * k
+        m[0, 0], m[-1, -1] = True, False
+        cvu[f"mask_{k}"], cvu[f"sd_{k}"] = m, signed_distance(m)
+        f = cr.standard_normal((h, w))
+        cvu[f"f_{k}"], cvu[f"curv_{k}"] = f, curvature(f)
+        img = cr.random((h, w))
+        cvu[f"img_{k}"], cvu[f"v_{k}"] = img, cv_velocity(img, f, 0.1 * (k + 1))
+    a7 = two_region()
+    cvu["init_a1"] = init_state(a7, SeedSpec(polygons=(square(14, 14, 76, 76),), inside_sign=-1),
+                                params(ModelKind.CHAN_VESE)).phi
+    fixtures["cv_units"] = cvu
+    fixtures["traj_cv_small"] = trajectory(
+        "cv_small", img_r, seed_r, params(ModelKind.CHAN_VESE, max_iters=45),
+        [1, 2, 19, 20, 21, 45])
+    fixtures["traj_cv_a7"] = trajectory(
+        "cv_a7", a7, SeedSpec(polygons=(square(14, 14, 76, 76),), inside_sign=-1),
+        params(ModelKind.CHAN_VESE, max_iters=400), [400])
 
     # 8-bit RGB -> grayscale of the reference loader (fileio.py:28-30, 88)
     from lsekit import fileio

@@ -1,0 +1,59 @@
+"""Curvature-regularized Chan-Vese baseline (models.py:122-141, kernels.py:
+98-133, engine.py:88-90, 129-132, 161-165) on the device: the exact distance
+transform is bit-identical to the reference; curvature uses the device's pow
+(within an ulp of glibc's), so CV trajectories are held to a tight tolerance
+plus identical masks, and acceptance A7's iteration count is reproduced."""
+import warnings
+
+import numpy as np
+import pytest
+
+import paper_1409_7474_b200 as L
+from conftest import load_golden, square, two_region
+
+pytestmark = pytest.mark.gpu
+
+
+def params(**kw):
+    with warnings.catch_warnings():
+        warnings.simplefilter("ignore")
+        return L.default_params(L.ModelKind.CHAN_VESE, **kw)
+
+
+def test_cv_units_match_reference():
+    g = load_golden("cv_units")
+    for k in range(3):
+        assert np.array_equal(L.signed_distance(g[f"mask_{k}"]), g[f"sd_{k}"])
+        c = L.curvature(g[f"f_{k}"])
+        assert np.abs(c - g[f"curv_{k}"]).max() <= 1e-13 * np.abs(g[f"curv_{k}"]).max()
+        v = L.cv_velocity(g[f"img_{k}"], g[f"f_{k}"], 0.1 * (k + 1))
+        assert np.abs(v - g[f"v_{k}"]).max() <= 1e-13 * np.abs(g[f"v_{k}"]).max()
+    seeds = L.SeedSpec(polygons=(square(14, 14, 76, 76),), inside_sign=-1)
+    st = L.init_state(two_region()[0], seeds, params())
+    assert np.array_equal(st.phi, g["init_a1"])
+
+
+def test_cv_trajectory_tracks_reference():
+    g = load_golden("traj_cv_small")
+    img = g["image"]
+    seeds = L.SeedSpec(polygons=tuple(q for q in g["poly"]), inside_sign=int(g["inside_sign"]))
+    r = L.EvolutionRun(img, seeds, params(max_iters=45))
+    for it in g["iters_recorded"]:
+        r.advance(int(it) - r.state.iteration)
+        want = g[f"phi_{it}"]
+        got = r.state.phi
+        assert np.abs(got - want).max() <= 1e-9 * np.abs(want).max(), it
+        assert np.array_equal(got > 0, want > 0), it
+
+
+def test_a7_cv_baseline_iterations():
+    """test_acceptance.py:146-161: the CV baseline needs ~250 iterations on A1."""
+    g = load_golden("traj_cv_a7")
+    image, truth = two_region()
+    seeds = L.SeedSpec(polygons=(square(14, 14, 76, 76),), inside_sign=-1)
+    res = L.run(image, seeds, params(max_iters=400))
+    assert res.converged == bool(g["converged"])
+    assert res.iterations == int(g["final_iteration"])
+    assert np.array_equal(res.mask, g["phi_400"] <= 0)
+    fast = L.run(image, seeds, L.default_params(L.ModelKind.REGION, max_iters=400))
+    assert fast.iterations * 5 < res.iterations          # region 40 vs CV 250 (A7)

@@ -26,7 +26,7 @@ def test_library_exports_every_header_symbol():
     for s in syms:
         assert hasattr(N.lib, s), s
     assert set(syms) == set(N.EXPORTED)
-    assert N.lib.lse_abi_version() == 4
+    assert N.lib.lse_abi_version() == 5
 
 
 def test_struct_layouts_match_header(tmp_path):
@@ -91,12 +91,10 @@ def test_gaussian_kernel_matches_oracle_and_reference_rules():
         L.Kernel2D(weights=np.ones((3, 3)))
 
 
-def test_out_of_scope_models_refuse_instead_of_cpu_fallback():
-    with pytest.raises(NotImplementedError):
-        L.cv_velocity(np.zeros((4, 4)), np.zeros((4, 4)), 0.1)
-    with pytest.raises(NotImplementedError):
-        L.EvolutionRun(np.zeros((8, 8)), L.SeedSpec(polygons=(np.array([[1, 1], [5, 1], [5, 5]]),)),
-                       L.default_params(L.ModelKind.CHAN_VESE))
+def test_out_of_scope_paths_refuse_instead_of_cpu_fallback():
+    seeds = L.SeedSpec(polygons=(np.array([[1, 1], [5, 1], [5, 5]]),))
+    with pytest.raises(NotImplementedError):        # contour traces (skimage)
+        L.EvolutionRun(np.zeros((8, 8)), seeds, L.default_params(L.ModelKind.REGION), trace=True)
 
 
 @pytest.mark.skipif(gpu_available(), reason="checks the no-device error path")

@@ -70,12 +70,16 @@ def _params(g):
                           max_iters=int(p[5]), conv_check_every=int(p[6]),
                           conv_window=int(p[7]), sigma1=float(p[8]), ts_pre=int(p[9]),
                           edge_gain=float(p[10]),
-                          nu=float(g["nu"]) if "nu" in g else 1.0)
+                          nu=float(g["nu"]) if "nu" in g else 1.0,
+                          mu=float(g["mu"]) if "mu" in g else 0.1)
 
 
 def _phi0(g, shape):
     polys = [q for q in g["poly"]]
-    return O.rasterize_seeds(polys, int(g["inside_sign"]), shape[1], shape[0])
+    phi0 = O.rasterize_seeds(polys, int(g["inside_sign"]), shape[1], shape[0])
+    if str(g["model"]) == "cv":                  # init_state: distance field (engine.py:129-132)
+        phi0 = -O.signed_distance(phi0 > 0)
+    return phi0
 
 
 @pytest.mark.parametrize("name", ["traj_region_small", "traj_edge_small", "traj_region_field",
@@ -85,7 +89,8 @@ def _phi0(g, shape):
                                   "traj_thin", "traj_a1", "traj_a1_cw2", "traj_a1_cw1",
                                   "traj_a1_edge", "traj_a2_edge", "traj_a5_region",
                                   "traj_a5_edge", "traj_instability", "traj_zhang_small",
-                                  "traj_zhang_nu", "traj_a4_neg", "traj_a4_pos"])
+                                  "traj_zhang_nu", "traj_a4_neg", "traj_a4_pos",
+                                  "traj_cv_small", "traj_cv_a7"])
 def test_oracle_trajectories_bit_exact(name):
     g = load_golden(name)
     img = g["image"]
@@ -132,3 +137,12 @@ def test_band_restatement_reduces_to_region_model():
     for it in g["iters_recorded"]:
         r.advance(int(it) - r.iteration)
         assert np.array_equal(r.phi, g[f"phi_{it}"])
+
+
+def test_cv_units_bit_exact():
+    """signed_distance (exact EDT restatement), curvature, cv_velocity vs the reference."""
+    g = load_golden("cv_units")
+    for k in range(3):
+        assert np.array_equal(O.signed_distance(g[f"mask_{k}"]), g[f"sd_{k}"])
+        assert np.array_equal(O.curvature(g[f"f_{k}"]), g[f"curv_{k}"])
+        assert np.array_equal(O.cv_velocity(g[f"img_{k}"], g[f"f_{k}"], 0.1 * (k + 1)), g[f"v_{k}"])
