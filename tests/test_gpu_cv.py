@@ -1,8 +1,10 @@
 """Curvature-regularized Chan-Vese baseline (models.py:122-141, kernels.py:
 98-133, engine.py:88-90, 129-132, 161-165) on the device: the exact distance
-transform is bit-identical to the reference; curvature uses the device's pow
-(within an ulp of glibc's), so CV trajectories are held to a tight tolerance
-plus identical masks, and acceptance A7's iteration count is reproduced."""
+transform is bit-identical to the reference; the curvature's x^1.5 is rounded
+to nearest on the device while the reference's np.power runs numpy's SIMD code
+(host-dependent, an ulp off in ~5% of cases), so CV trajectories are held to a
+tight tolerance plus identical masks, and acceptance A7's iteration count is
+reproduced."""
 import warnings
 
 import numpy as np
@@ -24,10 +26,13 @@ def test_cv_units_match_reference():
     g = load_golden("cv_units")
     for k in range(3):
         assert np.array_equal(L.signed_distance(g[f"mask_{k}"]), g[f"sd_{k}"])
+        # np.power runs numpy's AVX-512 SIMD code on the reference host (about 5%
+        # of its results are an ulp off libm's pow), so curvature is held to ulps
         c = L.curvature(g[f"f_{k}"])
-        assert np.abs(c - g[f"curv_{k}"]).max() <= 1e-13 * np.abs(g[f"curv_{k}"]).max()
+        assert np.abs(c - g[f"curv_{k}"]).max() <= 1e-13 * np.abs(g[f"curv_{k}"]).max(), k
         v = L.cv_velocity(g[f"img_{k}"], g[f"f_{k}"], 0.1 * (k + 1))
-        assert np.abs(v - g[f"v_{k}"]).max() <= 1e-13 * np.abs(g[f"v_{k}"]).max()
+        # the two means are correctly rounded here, pairwise in numpy: an ulp
+        assert np.abs(v - g[f"v_{k}"]).max() <= 4 * np.finfo(float).eps * np.abs(g[f"v_{k}"]).max()
     seeds = L.SeedSpec(polygons=(square(14, 14, 76, 76),), inside_sign=-1)
     st = L.init_state(two_region()[0], seeds, params())
     assert np.array_equal(st.phi, g["init_a1"])
@@ -42,8 +47,8 @@ def test_cv_trajectory_tracks_reference():
         r.advance(int(it) - r.state.iteration)
         want = g[f"phi_{it}"]
         got = r.state.phi
-        assert np.abs(got - want).max() <= 1e-9 * np.abs(want).max(), it
         assert np.array_equal(got > 0, want > 0), it
+        assert np.abs(got - want).max() <= 1e-9 * np.abs(want).max(), it
 
 
 def test_a7_cv_baseline_iterations():
