@@ -208,3 +208,27 @@ def test_grid_and_model_unit_behaviour():
     assert not deg and abs(np.abs(v).max() - 1.0) <= 1e-12
     g = L.edge_function(np.full((16, 16), 0.4), 1.0, 9)
     assert np.allclose(g[5:-5, 5:-5], 1.0, atol=1e-12) and (g > 0).all() and (g <= 1).all()
+
+
+def test_plain_c_caller_matches_python_api(tmp_path):
+    """examples/c_abi_region.c drives the C ABI directly (no Python in the loop)
+    and must reach the same result as lse.run through the Python API."""
+    import hashlib
+    import os
+    import subprocess
+    repo = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    exe = tmp_path / "c_abi_region"
+    subprocess.check_call(["gcc", "-O2", "-I", os.path.join(repo, "include"),
+                           os.path.join(repo, "examples", "c_abi_region.c"),
+                           "-L", os.path.join(repo, "paper_1409_7474_b200", "_lib"), "-llse_b200",
+                           "-lm", "-o", str(exe)])
+    env = dict(os.environ, LD_LIBRARY_PATH=os.path.join(repo, "paper_1409_7474_b200", "_lib"))
+    it, conv, hsh = subprocess.check_output([str(exe)], env=env).decode().split()
+    image = np.full((128, 128), 0.8)
+    image[40:88, 40:88] = 0.2
+    res = L.run(image, A1_SEED, L.default_params(L.ModelKind.REGION, max_iters=300))
+    h = 1469598103934665603
+    for q in res.mask.astype(np.uint8).ravel():
+        h = ((h ^ int(q)) * 1099511628211) & 0xFFFFFFFFFFFFFFFF
+    assert int(it) == res.iterations and bool(int(conv)) == res.converged
+    assert int(hsh, 16) == h
