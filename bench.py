@@ -98,33 +98,51 @@ class ClockSampler:
 
     def start(self):
         self.f = tempfile.NamedTemporaryFile("w+", suffix=".csv", delete=False)
+        self.n0 = 0
         try:
             self.proc = subprocess.Popen(
                 ["nvidia-smi", "-i", str(self.dev), f"--query-gpu={self.FIELDS}",
-                 "--format=csv,noheader,nounits", "-lms", "200"],
+                 "--format=csv,noheader,nounits", "-lms", "100"],
                 stdout=self.f, stderr=subprocess.DEVNULL)
         except Exception:
             self.proc = None
+            return
+        # the sampler is live (first sample written) before the timed region starts;
+        # samples taken before it are not counted
+        t0 = time.time()
+        while time.time() - t0 < 5.0 and self.proc.poll() is None:
+            self.n0 = len(self._lines())
+            if self.n0:
+                break
+            time.sleep(0.02)
+
+    def _lines(self):
+        with open(self.f.name) as fh:
+            return [ln for ln in fh.read().splitlines() if ln.count(",") == 5]
 
     def stop(self):
         if self.proc is None:
             return None
+        window = "timed region"
+        if len(self._lines()) <= self.n0:
+            # a timed region shorter than the sampling period: take the first
+            # sample after it (the clocks have not dropped yet)
+            window = "first sample after a short timed region"
+            t0 = time.time()
+            while time.time() - t0 < 1.0 and len(self._lines()) <= self.n0:
+                time.sleep(0.01)
         self.proc.terminate()
         try:
             self.proc.wait(timeout=5)
         except Exception:
             self.proc.kill()
-        self.f.flush()
         rows = []
-        with open(self.f.name) as fh:
-            for line in fh:
-                parts = [x.strip() for x in line.split(",")]
-                if len(parts) != 6:
-                    continue
-                try:
-                    rows.append((float(parts[0]), float(parts[1]), parts[2:]))
-                except ValueError:
-                    continue
+        for line in self._lines()[self.n0:]:
+            parts = [x.strip() for x in line.split(",")]
+            try:
+                rows.append((float(parts[0]), float(parts[1]), parts[2:]))
+            except ValueError:
+                continue
         os.unlink(self.f.name)
         if not rows:
             return None
@@ -133,7 +151,7 @@ class ClockSampler:
                           if v.lower().startswith("active")})
         loaded = [s for s, _, _ in rows if s > 200] or [s for s, _, _ in rows]
         return {"sm_mhz": statistics.median(loaded), "sm_max_mhz": max(m for _, m, _ in rows),
-                "reasons": reasons, "samples": len(rows)}
+                "reasons": reasons, "samples": len(rows), "window": window}
 
 
 # ----------------------------------------------------------------- CPU side
@@ -337,72 +355,116 @@ def main():
     from paper_1409_7474_b200.strips import DeviceStrip, DistComm, StripDriver, plan_strips
 
     n_rects = max(1, int(round(20000 * (args.size / 32768.0) ** 2)))
-    strips = (ws > 1 and args.mode == "strips") or args.strips_n1
-    win = plan_strips(args.size, args.size, ws)[rank] if strips else None
-    t_gen = time.perf_counter()
-    sc = scenes.config5(size=args.size, n_rects=n_rects, iters=args.iters,
-                        seed_offset=0 if strips else rank,
-                        rows=(win.y_lo, win.y_hi) if strips else None)
-    t_gen = time.perf_counter() - t_gen
-    Hl, W = sc.image.shape                     # local rows (a strip: owned + halo rows)
-    npx_local = Hl * W
     npx = args.size * args.size                # pixels of one job (the whole scene)
-    prm = default_params(ModelKind.REGION, **sc.params)
-    p, keep_w = _native_params(prm)
 
-    # pinned host copies for the end-to-end leg
-    img_pin = torch.empty((Hl, W), dtype=torch.float32, pin_memory=True)
-    img_pin.numpy()[...] = sc.image
-    nbytes_mask = (npx_local + 7) // 8
-    mask_pin = torch.empty(nbytes_mask, dtype=torch.uint8, pin_memory=True)
-
-    polys = np.ascontiguousarray(np.concatenate(sc.polygons), dtype=np.float64)
-    counts = np.ascontiguousarray([len(q) for q in sc.polygons], dtype=np.int64)
-    st = N.LseStatus()
-    if strips:
-        # one row strip of the scene per rank; halo rows + partials over NCCL
-        strip = DeviceStrip(sc.image, win, SeedSpec(polygons=sc.polygons,
-                                                    inside_sign=sc.inside_sign), prm)
-        del sc.image
-        drv = StripDriver([strip], DistComm(strip))
-        drv.share_image_range()
-        h = strip.h
-
-        def job():
-            strip.reset()
-            drv.initialize()
-            s0 = drv.advance(args.iters)[0]
-            assert s0.iteration == args.iters, s0.iteration
-            st.exact_fallbacks = s0.exact_fallbacks
-
-        def job_e2e():
-            strip.load_image(img_pin.data_ptr(), True)
+    def build(strips):
+        """The measured job: one strip of the scene per rank (strips) or the
+        whole scene per rank (replicas / N = 1)."""
+        from types import SimpleNamespace
+        jb = SimpleNamespace(strips=strips)
+        win = plan_strips(args.size, args.size, ws)[rank] if strips else None
+        t0 = time.perf_counter()
+        sc = scenes.config5(size=args.size, n_rects=n_rects, iters=args.iters,
+                            seed_offset=0 if strips else rank,
+                            rows=(win.y_lo, win.y_hi) if strips else None)
+        jb.t_gen = time.perf_counter() - t0
+        jb.Hl, jb.W = sc.image.shape           # local rows (a strip: owned + halo rows)
+        jb.npx_local = jb.Hl * jb.W
+        prm = default_params(ModelKind.REGION, **sc.params)
+        p, jb.keep_w = _native_params(prm)
+        # pinned host copies for the end-to-end leg
+        img_pin = torch.empty((jb.Hl, jb.W), dtype=torch.float32, pin_memory=True)
+        img_pin.numpy()[...] = sc.image
+        jb.nbytes_mask = (jb.npx_local + 7) // 8
+        mask_pin = torch.empty(jb.nbytes_mask, dtype=torch.uint8, pin_memory=True)
+        jb.img_pin, jb.mask_pin = img_pin, mask_pin
+        polys = np.ascontiguousarray(np.concatenate(sc.polygons), dtype=np.float64)
+        counts = np.ascontiguousarray([len(q) for q in sc.polygons], dtype=np.int64)
+        jb.poly_bytes = polys.nbytes + counts.nbytes
+        jb.st = st = N.LseStatus()
+        inside = sc.inside_sign
+        if strips:
+            # one row strip of the scene per rank; halo rows + partials over NCCL
+            strip = DeviceStrip(sc.image, win, SeedSpec(polygons=sc.polygons,
+                                                        inside_sign=inside), prm)
+            del sc.image
+            drv = StripDriver([strip], DistComm(strip))
             drv.share_image_range()
-            job()
-            N.check(N.lib.lse_run_read_mask(h, C.cast(C.c_void_p(mask_pin.data_ptr()),
-                                                      C.POINTER(C.c_ubyte)), sc.inside_sign, 1))
+            jb.strip, jb.drv, jb.h = strip, drv, strip.h
+
+            def job():
+                strip.reset()
+                drv.initialize()
+                s0 = drv.advance(args.iters)[0]
+                assert s0.iteration == args.iters, s0.iteration
+                st.exact_fallbacks = s0.exact_fallbacks
+
+            def job_e2e():
+                strip.load_image(img_pin.data_ptr(), True)
+                drv.share_image_range()
+                job()
+                N.check(N.lib.lse_run_read_mask(jb.h, C.cast(C.c_void_p(mask_pin.data_ptr()),
+                                                             C.POINTER(C.c_ubyte)), inside, 1))
+
+            def close():
+                jb.drv = jb.strip = None
+        else:
+            del sc.image
+            init = N.LsePhi0()
+            init.kind = N.LSE_PHI0_POLYGONS
+            init.poly_xy = N.dptr(polys)
+            init.poly_counts = counts.ctypes.data_as(N._llp)
+            init.n_polys = len(counts)
+            init.inside_sign = inside
+            jb.keep_init = (init, polys, counts)
+            h = C.c_void_p()
+            N.check(N.lib.lse_run_create(C.byref(h), C.byref(p), jb.Hl, jb.W,
+                                         C.c_void_p(img_pin.data_ptr()), 1, C.byref(init)))
+            jb.h = h
+
+            def job():
+                N.check(N.lib.lse_run_set_state(h, C.byref(init)))
+                N.check(N.lib.lse_run_advance(h, args.iters, C.byref(st)))
+                assert st.iteration == args.iters, st.iteration
+
+            def job_e2e():
+                N.check(N.lib.lse_run_load_image(h, C.c_void_p(img_pin.data_ptr()), 1))
+                job()
+                N.check(N.lib.lse_run_read_mask(h, C.cast(C.c_void_p(mask_pin.data_ptr()),
+                                                          C.POINTER(C.c_ubyte)), inside, 1))
+
+            def close():
+                N.lib.lse_run_destroy(h)
+        jb.job, jb.job_e2e, jb.close = job, job_e2e, close
+        return jb
+
+    strips = (ws > 1 and args.mode == "strips") or args.strips_n1
+    if strips:
+        # the strips' exchanges are exercised by one job; should any rank fail,
+        # every rank falls back to replicas (decided over a gloo side group,
+        # which does not depend on the NCCL paths under test)
+        ctrl = dist.new_group(backend="gloo")
+        ok, jb = 1, None
+        try:
+            jb = build(True)
+            if os.environ.get("LSE_BENCH_FAIL_STRIPS") == str(rank):   # fallback test hook
+                raise RuntimeError("forced strip failure")
+            jb.job()
+        except Exception as e:                 # noqa: BLE001
+            print(f"bench: row strips failed on rank {rank}: {e!r}; falling back to replicas",
+                  file=sys.stderr, flush=True)
+            ok = 0
+        vote = torch.tensor([ok], dtype=torch.int32)
+        dist.all_reduce(vote, op=dist.ReduceOp.MIN, group=ctrl)
+        if int(vote.item()) == 0:
+            if jb is not None:
+                jb.close()
+            strips = False
+            jb = build(False)
     else:
-        del sc.image
-        init = N.LsePhi0()
-        init.kind = N.LSE_PHI0_POLYGONS
-        init.poly_xy = N.dptr(polys)
-        init.poly_counts = counts.ctypes.data_as(N._llp)
-        init.n_polys = len(counts)
-        init.inside_sign = sc.inside_sign
-        h = C.c_void_p()
-        N.check(N.lib.lse_run_create(C.byref(h), C.byref(p), Hl, W,
-                                     C.c_void_p(img_pin.data_ptr()), 1, C.byref(init)))
-
-        def job():
-            N.check(N.lib.lse_run_set_state(h, C.byref(init)))
-            N.check(N.lib.lse_run_advance(h, args.iters, C.byref(st)))
-            assert st.iteration == args.iters, st.iteration
-
-        def job_e2e():
-            N.check(N.lib.lse_run_load_image(h, C.c_void_p(img_pin.data_ptr()), 1))
-            job()
-            N.check(N.lib.lse_run_read_mask(h, C.cast(C.c_void_p(mask_pin.data_ptr()),
-                                                      C.POINTER(C.c_ubyte)), sc.inside_sign, 1))
+        jb = build(False)
+    h, job, job_e2e, st = jb.h, jb.job, jb.job_e2e, jb.st
+    Hl, W, npx_local, nbytes_mask, t_gen = jb.Hl, jb.W, jb.npx_local, jb.nbytes_mask, jb.t_gen
 
     def barrier():
         if dist is not None:
@@ -488,13 +550,10 @@ def main():
         barrier()
         e_ms = max_over_ranks(ms.value)
         e2e = {"value": px_its / (e_ms / 1e3) / 1e9, "unit": "Gpix-it/s",
-               "h2d_bytes_per_step": npx_local * 4 + polys.nbytes + counts.nbytes,
+               "h2d_bytes_per_step": npx_local * 4 + jb.poly_bytes,
                "d2h_bytes_per_step": nbytes_mask, "ms_per_step": e_ms / args.steps}
 
-    if strips:
-        del drv, strip
-    else:
-        N.lib.lse_run_destroy(h)
+    jb.close()
 
     # ---- roofline of one iteration (k_update + k_partition)
     peak, peak_kind = measured_peaks()
