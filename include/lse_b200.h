@@ -19,7 +19,7 @@
 extern "C" {
 #endif
 
-#define LSE_ABI_VERSION 5
+#define LSE_ABI_VERSION 6
 
 #define LSE_OK 0
 #define LSE_ERR_ARG 1            /* ValueError in the reference               */
@@ -258,6 +258,23 @@ int lse_zhang_velocity(const double* image, const double* phi, long long h, long
  * the union covers no pixel centre or every pixel centre. */
 int lse_rasterize_seeds(const double* poly_xy, const long long* poly_counts, long long n_polys,
                         int inside_sign, long long h, long long w, signed char* out);
+
+/* ---- zero-level contours (extract_contours, engine.py:280-294) ---------- */
+
+/* Marching squares at level 0 (scikit-image find_contours, fully_connected
+ * 'low', positive_orientation 'low'): polylines of (x, y) = (col + 0.5,
+ * row + 0.5) points, in the published assembly's order; none when phi is
+ * single-signed.  The result is host memory owned by the handle. */
+typedef struct lse_contours lse_contours;
+int lse_contours_from_field(const double* phi, int phi_on_device, long long h, long long w,
+                            lse_contours** out);
+/* contours of a run's current phi, computed on the device without a phi
+ * download (EvolutionRun.contours, engine.py:260-261; the trace, 214-238) */
+int lse_run_contours(lse_run* run, lse_contours** out);
+int lse_contours_size(const lse_contours* c, long long* n_contours, long long* n_points);
+/* offsets: n_contours + 1 point offsets; xy: 2 * n_points doubles */
+int lse_contours_read(const lse_contours* c, long long* offsets, double* xy);
+void lse_contours_destroy(lse_contours* c);
 
 #ifdef __cplusplus
 }

@@ -345,6 +345,101 @@ def zhang_velocity(image: np.ndarray, phi: np.ndarray, nu: float):
 
 
 # --------------------------------------------------------------------------
+# engine.py:280-294 extract_contours -> skimage.measure.find_contours
+# (scikit-image >= 0.20, pkg/pyproject.toml:13; absent here, so restated from
+# its published algorithm: marching-squares segments per 2x2 square in
+# row-major order, then the dict-based endpoint join).  Parity with
+# scikit-image itself is unpinned; the reference's own contour tests
+# (tests/test_engine.py:202-228) and hand-derived cases pin this restatement.
+# --------------------------------------------------------------------------
+
+# case -> (from, to) edge pairs; edges 0 top, 1 bottom, 2 left, 3 right;
+# saddles 6 / 9 keep the low values connected (fully_connected='low')
+_MS_CASES = {1: ((0, 2),), 2: ((3, 0),), 3: ((3, 2),), 4: ((2, 1),), 5: ((0, 1),),
+             6: ((3, 0), (2, 1)), 7: ((3, 1),), 8: ((1, 3),), 9: ((0, 2), (1, 3)),
+             10: ((1, 0),), 11: ((1, 2),), 12: ((2, 3),), 13: ((0, 3),), 14: ((2, 0),)}
+
+
+def _ms_fraction(f, t):
+    with np.errstate(divide="ignore", invalid="ignore"):
+        q = (0.0 - f) / (t - f)
+    return np.where(t == f, 0.0, q)
+
+
+def contour_segments(phi: np.ndarray):
+    """Oriented segments ((r, c), (r, c)) of level 0, in square order."""
+    a = np.asarray(phi, dtype=np.float64)
+    ul, ur, ll, lr = a[:-1, :-1], a[:-1, 1:], a[1:, :-1], a[1:, 1:]
+    cs = ((ul > 0).astype(np.int64) + 2 * (ur > 0) + 4 * (ll > 0) + 8 * (lr > 0))
+    nan = np.isnan(ul) | np.isnan(ur) | np.isnan(ll) | np.isnan(lr)
+    r0, c0 = np.meshgrid(np.arange(a.shape[0] - 1, dtype=np.float64),
+                         np.arange(a.shape[1] - 1, dtype=np.float64), indexing="ij")
+    pts = (
+        (r0, c0 + _ms_fraction(ul, ur)),        # top
+        (r0 + 1.0, c0 + _ms_fraction(ll, lr)),  # bottom
+        (r0 + _ms_fraction(ul, ll), c0),        # left
+        (r0 + _ms_fraction(ur, lr), c0 + 1.0),  # right
+    )
+    segs = []
+    rows, cols = np.nonzero((cs != 0) & (cs != 15) & ~nan)
+    for i, j in zip(rows.tolist(), cols.tolist()):
+        for e0, e1 in _MS_CASES[int(cs[i, j])]:
+            segs.append(((float(pts[e0][0][i, j]), float(pts[e0][1][i, j])),
+                         (float(pts[e1][0][i, j]), float(pts[e1][1][i, j]))))
+    return segs
+
+
+def assemble_contours(segments):
+    """Join oriented segments into polylines (the published dict algorithm)."""
+    from collections import deque
+    index = 0
+    contours, starts, ends = {}, {}, {}
+    for p0, p1 in segments:
+        if p0 == p1:
+            continue
+        tail, tail_num = starts.pop(p1, (None, None))
+        head, head_num = ends.pop(p0, (None, None))
+        if tail is not None and head is not None:
+            if tail is head:
+                head.append(p1)
+            elif tail_num > head_num:
+                head.extend(tail)
+                contours.pop(tail_num, None)
+                starts[head[0]] = (head, head_num)
+                ends[head[-1]] = (head, head_num)
+            else:
+                tail.extendleft(reversed(head))
+                starts.pop(head[0], None)
+                contours.pop(head_num, None)
+                starts[tail[0]] = (tail, tail_num)
+                ends[tail[-1]] = (tail, tail_num)
+        elif tail is None and head is None:
+            c = deque((p0, p1))
+            contours[index] = c
+            starts[p0] = (c, index)
+            ends[p1] = (c, index)
+            index += 1
+        elif head is None:
+            tail.appendleft(p0)
+            starts[p0] = (tail, tail_num)
+        else:
+            head.append(p1)
+            ends[p1] = (head, head_num)
+    return [np.array(c) for _, c in sorted(contours.items())]
+
+
+def extract_contours(phi: np.ndarray):
+    """engine.py:280-294: (x, y) = (col + 0.5, row + 0.5) polylines."""
+    phi = np.asarray(phi, dtype=np.float64)
+    if not ((phi > 0).any() and (phi < 0).any()):
+        return []
+    out = []
+    for c in assemble_contours(contour_segments(phi)):
+        out.append(np.stack([c[:, 1] + 0.5, c[:, 0] + 0.5], axis=1))
+    return out
+
+
+# --------------------------------------------------------------------------
 # engine.py
 # --------------------------------------------------------------------------
 
@@ -399,7 +494,7 @@ def advance_once(phi, iteration, image, p: OracleParams, g, w_reg):
 class OracleRun:
     """engine.py:193-269 -- resumable driver with checkpoint convergence."""
 
-    def __init__(self, image, phi0, p: OracleParams, iteration=0):
+    def __init__(self, image, phi0, p: OracleParams, iteration=0, trace=False):
         self.image = np.asarray(image, dtype=np.float64)
         self.p = p
         self.phi = np.asarray(phi0, dtype=np.float64)
@@ -410,6 +505,7 @@ class OracleRun:
         self.g = (edge_function(self.image, p.sigma1, p.ts_pre, p.edge_gain)
                   if p.model == EDGE else None)
         self.checkpoints = []
+        self.trace = [(0, extract_contours(self.phi))] if trace else None   # engine.py:214-216
 
     def step_once(self):
         p = self.p
@@ -424,6 +520,8 @@ class OracleRun:
                     np.array_equal(self.checkpoints[-1], m)
                     for m in self.checkpoints[:-1]):
                 converged = True
+            if self.trace is not None:                      # engine.py:237-238
+                self.trace.append((n, extract_contours(phi)))
         self.phi, self.iteration = phi, n
         self.converged = converged
         self.degenerate = self.degenerate or degenerate

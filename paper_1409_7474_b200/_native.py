@@ -121,6 +121,11 @@ _SIGS = {
     "lse_zhang_velocity": (_i, [_dp, _dp, _ll, _ll, C.c_double, _dp, C.POINTER(C.c_int)]),
     "lse_edge_velocity": (_i, [_dp, _dp, _ll, _ll, _dp]),
     "lse_rasterize_seeds": (_i, [_dp, _llp, _ll, _i, _ll, _ll, C.POINTER(C.c_byte)]),
+    "lse_contours_from_field": (_i, [_vp, _i, _ll, _ll, C.POINTER(_vp)]),
+    "lse_run_contours": (_i, [_vp, C.POINTER(_vp)]),
+    "lse_contours_size": (_i, [_vp, _llp, _llp]),
+    "lse_contours_read": (_i, [_vp, _llp, _dp]),
+    "lse_contours_destroy": (None, [_vp]),
 }
 for _name, (_res, _args) in _SIGS.items():
     _f = getattr(lib, _name)
@@ -149,6 +154,20 @@ def dptr(a: np.ndarray):
 
 def f64(a) -> np.ndarray:
     return np.ascontiguousarray(a, dtype=np.float64)
+
+
+def take_contours(c) -> list:
+    """Reads and frees an lse_contours handle: a list of (n, 2) float64 (x, y)
+    arrays, as extract_contours returns them (engine.py:280-294)."""
+    try:
+        nc, npt = C.c_longlong(), C.c_longlong()
+        check(lib.lse_contours_size(c, C.byref(nc), C.byref(npt)))
+        off = np.empty(nc.value + 1, dtype=np.int64)
+        xy = np.empty((max(npt.value, 1), 2), dtype=np.float64)
+        check(lib.lse_contours_read(c, off.ctypes.data_as(_llp), dptr(xy)))
+    finally:
+        lib.lse_contours_destroy(c)
+    return [xy[off[k]:off[k + 1]].copy() for k in range(nc.value)]
 
 
 def device_count() -> int:

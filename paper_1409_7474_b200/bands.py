@@ -66,8 +66,6 @@ class BandEvolutionRun(EvolutionRun):
     """EvolutionRun (engine.py:193-269) over a (K, H, W) multi-band image."""
 
     def __init__(self, bands, seeds: SeedSpec, params: EvolutionParams, trace: bool = False):
-        if trace:
-            raise NotImplementedError("contour traces are outside the B200 hot path")
         if params.model is not ModelKind.REGION:
             raise NotImplementedError("multi-band images run the region model")
         self.image = as_bands(bands)
@@ -92,7 +90,7 @@ class BandEvolutionRun(EvolutionRun):
         self._version = 0
         self._snapshots = weakref.WeakSet()
         self.wall_time = 0.0
-        self.trace = None
+        self.trace = [(0, self._dev.contours())] if trace else None
 
 
 def run_bands(bands, seeds: SeedSpec, params: EvolutionParams):

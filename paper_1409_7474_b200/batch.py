@@ -59,6 +59,8 @@ class TileBatch:
         self.runs = list(runs)
         if not self.runs:
             raise ValueError("empty batch")
+        if any(r.trace is not None for r in self.runs):
+            raise ValueError("runs with a contour trace advance on their own")
         handles = (C.c_void_p * len(self.runs))(*[r._dev.h.value for r in self.runs])
         h = C.c_void_p()
         N.check(N.lib.lse_batch_create(C.byref(h), handles, len(self.runs)))

@@ -24,6 +24,7 @@
 #include "lse_device.cuh"
 #include "lse_fast.cuh"
 #include "lse_generic.cuh"
+#include "lse_contours.cuh"
 
 using namespace lse;
 
@@ -2276,5 +2277,125 @@ int lse_rasterize_seeds(const double* poly_xy, const long long* poly_counts, lon
   CK(cudaMemcpy(out, dsig.p, h * w, cudaMemcpyDeviceToHost));
   return LSE_OK;
 }
+
+}  // extern "C"
+
+// ------------------------------------------------------------------ contours
+struct lse_contours {
+  std::vector<long long> offsets{0};   // point offsets, n_contours + 1
+  std::vector<double> xy;              // (x, y) = (col + 0.5, row + 0.5) per point
+};
+
+namespace {
+
+// extract_contours (engine.py:280-294) of a dense device field on stream st.
+int contours_device(const double* d_phi, long long H, long long W, cudaStream_t st,
+                    lse_contours* out) {
+  const long long rows = std::max(H - 1, 1LL);
+  DevBuf cnt, off, fl, sg;
+  TRY(dbuf<long long>(cnt, rows));
+  TRY(dbuf<long long>(off, rows + 1));
+  TRY(dbuf<unsigned>(fl, 1));
+  CK(cudaMemsetAsync(fl.p, 0, sizeof(unsigned), st));
+  k_contour_rows<false><<<(unsigned)rows, kContourThreads, 0, st>>>(
+      d_phi, H, W, (long long*)cnt.p, nullptr, nullptr, (unsigned*)fl.p);
+  CKL();
+  k_contour_scan<<<1, 1024, 0, st>>>((const long long*)cnt.p, rows, (long long*)off.p);
+  CKL();
+  long long total = 0;
+  unsigned signs = 0;
+  CK(cudaMemcpyAsync(&total, (long long*)off.p + rows, sizeof(long long), cudaMemcpyDeviceToHost,
+                     st));
+  CK(cudaMemcpyAsync(&signs, fl.p, sizeof(unsigned), cudaMemcpyDeviceToHost, st));
+  CK(cudaStreamSynchronize(st));
+  if (signs != 3u || total == 0) return LSE_OK;      // single-signed: no zero crossing
+  TRY(dbuf<Seg>(sg, total));
+  k_contour_rows<true><<<(unsigned)rows, kContourThreads, 0, st>>>(
+      d_phi, H, W, nullptr, (const long long*)off.p, (Seg*)sg.p, nullptr);
+  CKL();
+  std::vector<Seg> segs(total);
+  CK(cudaMemcpyAsync(segs.data(), sg.p, total * sizeof(Seg), cudaMemcpyDeviceToHost, st));
+  CK(cudaStreamSynchronize(st));
+  const auto lines = ms_assemble(segs);
+  long long npts = 0;
+  for (const auto& l : lines) npts += (long long)l.size();
+  out->offsets.reserve(lines.size() + 1);
+  out->xy.reserve(2 * npts);
+  for (const auto& l : lines) {
+    for (const MsPoint& q : l) {
+      out->xy.push_back(q.c + 0.5);
+      out->xy.push_back(q.r + 0.5);
+    }
+    out->offsets.push_back((long long)out->xy.size() / 2);
+  }
+  return LSE_OK;
+}
+
+}  // namespace
+
+extern "C" {
+
+int lse_contours_from_field(const double* phi, int phi_on_device, long long h, long long w,
+                            lse_contours** out) {
+  if (!phi || !out || h < 1 || w < 1) return fail(LSE_ERR_ARG, "bad arguments");
+  *out = nullptr;
+  TRY(check_device());
+  DevBuf a;
+  const double* d = phi;
+  if (!phi_on_device) {
+    TRY(dbuf<double>(a, h * w));
+    CK(cudaMemcpy(a.p, phi, h * w * sizeof(double), cudaMemcpyHostToDevice));
+    d = (const double*)a.p;
+  }
+  auto* c = new lse_contours();
+  const int rc = contours_device(d, h, w, 0, c);
+  if (rc != LSE_OK) {
+    delete c;
+    return rc;
+  }
+  *out = c;
+  return LSE_OK;
+}
+
+int lse_run_contours(lse_run* r, lse_contours** out) {
+  if (!r || !out) return fail(LSE_ERR_ARG, "null argument");
+  if (r->strip) return fail(LSE_ERR_ARG, "contours of a row strip: gather the strips' phi");
+  *out = nullptr;
+  TRY(ensure_generic(r));
+  const double* src;
+  if (r->field_valid) {
+    src = r->d_F[r->curF];
+  } else {
+    TRY(upload_ctx(r));
+    k_phi_from_bits<<<grid2(r->W, r->H), 128, 0, r->st>>>(r->d_bits[r->cur], r->d_U, r->d_ctx,
+                                                           r->mode);
+    CKL();
+    src = r->d_U;
+  }
+  auto* c = new lse_contours();
+  const int rc = contours_device(src, r->H, r->W, r->st, c);
+  if (rc != LSE_OK) {
+    delete c;
+    return rc;
+  }
+  *out = c;
+  return LSE_OK;
+}
+
+int lse_contours_size(const lse_contours* c, long long* n_contours, long long* n_points) {
+  if (!c || !n_contours || !n_points) return fail(LSE_ERR_ARG, "null argument");
+  *n_contours = (long long)c->offsets.size() - 1;
+  *n_points = c->offsets.back();
+  return LSE_OK;
+}
+
+int lse_contours_read(const lse_contours* c, long long* offsets, double* xy) {
+  if (!c || !offsets || (!xy && c->offsets.back() > 0)) return fail(LSE_ERR_ARG, "null argument");
+  memcpy(offsets, c->offsets.data(), c->offsets.size() * sizeof(long long));
+  if (!c->xy.empty()) memcpy(xy, c->xy.data(), c->xy.size() * sizeof(double));
+  return LSE_OK;
+}
+
+void lse_contours_destroy(lse_contours* c) { delete c; }
 
 }  // extern "C"

@@ -240,6 +240,12 @@ class _DeviceRun:
                                         int(inside_sign), 0))
         return out.view(bool)
 
+    def contours(self):
+        """Zero-level contours of the current phi, computed on the device."""
+        c = C.c_void_p()
+        N.check(N.lib.lse_run_contours(self.h, C.byref(c)))
+        return N.take_contours(c)
+
     def set_state(self, st: EvolutionState):
         s, keep = _phi0_field(st.phi, st.iteration, st.converged, st.degenerate)
         N.check(N.lib.lse_run_set_state(self.h, C.byref(s)))
@@ -284,9 +290,6 @@ class EvolutionRun:
 
     def __init__(self, image: np.ndarray, seeds: SeedSpec,
                  params: EvolutionParams, trace: bool = False):
-        if trace:
-            raise NotImplementedError(
-                "contour traces (skimage marching squares) are outside the B200 hot path")
         _require_device_model(params.model)
         self.image = as_image(image)
         self.seeds = seeds
@@ -298,6 +301,8 @@ class EvolutionRun:
         self._snapshots = weakref.WeakSet()
         self.wall_time = 0.0
         self.trace = None
+        if trace:                                       # engine.py:214-216
+            self.trace = [(0, self._dev.contours())]
 
     # -- state -----------------------------------------------------------
     def _read_phi(self):
@@ -335,17 +340,40 @@ class EvolutionRun:
         self._before_mutation()
         t0 = time.perf_counter()
         try:
-            self._dev.advance(n_steps)
+            if self.trace is None:
+                self._dev.advance(n_steps)
+            else:
+                self._advance_traced(int(n_steps))
         finally:
             self.wall_time += time.perf_counter() - t0
         return self.state
+
+    def _advance_traced(self, n_steps):
+        """Checkpoint to checkpoint, appending the contours of phi at every
+        checkpoint iteration (engine.py:226-238); the device trajectory is the
+        same as one advance(n_steps)."""
+        cce = self.params.conv_check_every
+        left = n_steps
+        while left > 0:
+            st0 = self._dev.status()
+            if st0.converged or st0.iteration >= self.params.max_iters:
+                break
+            k = min(left, cce - int(st0.iteration) % cce)
+            st = self._dev.advance(k)
+            done = int(st.iteration) - int(st0.iteration)
+            left -= done
+            if done > 0 and int(st.iteration) % cce == 0:
+                self.trace.append((int(st.iteration), self._dev.contours()))
+            if done < k:
+                break
 
     def mask(self) -> np.ndarray:
         """engine.py:256-259: the binary class carrying the seed sign."""
         return self._dev.read_mask(self.seeds.inside_sign)
 
     def contours(self):
-        return extract_contours(self.state.phi)
+        """engine.py:260-261, on the device state (no phi download)."""
+        return self._dev.contours()
 
     def result(self) -> ExtractionResult:
         st = self._dev.status()
@@ -353,7 +381,7 @@ class EvolutionRun:
             mask=self.mask(), object_sign=self.seeds.inside_sign,
             iterations=int(st.iteration), wall_time=self.wall_time,
             converged=bool(st.converged), degenerate=bool(st.degenerate),
-            trace=None)
+            trace=tuple(self.trace) if self.trace is not None else None)
 
     def set_native_option(self, name: str, value: int) -> None:
         """Tune the device run (e.g. "skip_uniform" 0/1); results are unchanged."""
@@ -377,9 +405,17 @@ def run(image: np.ndarray, seeds: SeedSpec, params: EvolutionParams,
 
 
 def extract_contours(phi: np.ndarray):
-    """engine.py:280-294.  A single-signed field has no zero crossing and
-    yields []; marching squares itself (skimage) is outside the hot path."""
-    phi = np.asarray(phi, dtype=np.float64)
+    """engine.py:280-294: zero-level polylines of phi as (x, y) arrays.
+
+    Marching squares runs on the device (lse_contours_from_field; the
+    published scikit-image find_contours algorithm the reference calls,
+    level 0, low values fully connected); a single-signed field yields []."""
+    phi = np.ascontiguousarray(phi, dtype=np.float64)
     if not ((phi > 0).any() and (phi < 0).any()):
         return []
-    raise NotImplementedError("marching-squares contours are outside the B200 hot path")
+    if phi.ndim != 2:
+        raise ValueError("Only 2D arrays are supported.")
+    c = C.c_void_p()
+    N.check(N.lib.lse_contours_from_field(phi.ctypes.data_as(C.c_void_p), 0, phi.shape[0],
+                                          phi.shape[1], C.byref(c)))
+    return N.take_contours(c)

@@ -26,7 +26,7 @@ def test_library_exports_every_header_symbol():
     for s in syms:
         assert hasattr(N.lib, s), s
     assert set(syms) == set(N.EXPORTED)
-    assert N.lib.lse_abi_version() == 5
+    assert N.lib.lse_abi_version() == 6
 
 
 def test_struct_layouts_match_header(tmp_path):
@@ -91,9 +91,21 @@ def test_gaussian_kernel_matches_oracle_and_reference_rules():
         L.Kernel2D(weights=np.ones((3, 3)))
 
 
-def test_out_of_scope_paths_refuse_instead_of_cpu_fallback():
+def test_single_signed_contours_need_no_device():
+    # engine.py:288-289: no zero crossing -> [] before any marching squares
+    assert L.extract_contours(np.ones((8, 8))) == []
+    assert L.extract_contours(-np.ones((8, 8))) == []
+    assert L.extract_contours(np.zeros((8, 8))) == []
+
+
+@pytest.mark.skipif(gpu_available(), reason="checks the no-device error path")
+def test_contours_fail_loudly_without_gpu():
+    phi = np.ones((8, 8))
+    phi[2:5, 2:5] = -1.0
+    with pytest.raises(RuntimeError):
+        L.extract_contours(phi)
     seeds = L.SeedSpec(polygons=(np.array([[1, 1], [5, 1], [5, 5]]),))
-    with pytest.raises(NotImplementedError):        # contour traces (skimage)
+    with pytest.raises(RuntimeError):
         L.EvolutionRun(np.zeros((8, 8)), seeds, L.default_params(L.ModelKind.REGION), trace=True)
 
 
