@@ -490,7 +490,7 @@ template <int R, int MODEL, int SRC>
 int launch_update(lse_run* r, FastParams P) {
   const bool half = r->half_units;
   const long long n = r->nb_upd[0] + (half ? r->ni_upd_half : r->ni_upd);
-  const int g = fast_grid(n);
+  const int g = fast_grid(n, kUpdateCtasPerSm);
   P.work_base = take_work(r, n, g);
 #ifdef LSE_UNIT_TRACE
   P.trace = trace_begin(r, n, g, "update", r->nb_upd[0]);
@@ -1694,7 +1694,7 @@ int batch_iteration(lse_batch* b, long long it, bool ckpt, int src, bool any_reg
   P.iter = it;
   {
     const long long n = (long long)b->T * (b->nb_upd + b->ni_upd);
-    const int g = fast_grid(n);
+    const int g = fast_grid(n, kUpdateCtasPerSm);
     P.work_base = batch_take_work(b, n, g);
     if (src == SRC_SCALED)
       TRY(launch_pdl(k_update<R, REGION, SRC_SCALED, true, false>, g, kThreads, b->st, P));

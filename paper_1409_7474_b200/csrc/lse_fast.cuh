@@ -123,6 +123,10 @@ __device__ __forceinline__ unsigned long long lse_now() {
 
 constexpr int kChunk = 256;      // partition: columns per warp chunk (32 lanes x 8 columns)
 constexpr int kPartitionCtasPerSm = 4;   // partition occupancy (launch bound and grid)
+#ifndef LSE_UPDATE_CTAS
+#define LSE_UPDATE_CTAS 4
+#endif
+constexpr int kUpdateCtasPerSm = LSE_UPDATE_CTAS;   // update occupancy (launch bound and grid)
 constexpr int kUpdCols = 8;      // update: columns per lane
 constexpr int kUpdChunk = 32 * kUpdCols;   // update: columns per warp chunk
 
@@ -396,6 +400,11 @@ __device__ __forceinline__ float lds_f32(uint32_t addr) {
   asm volatile("ld.shared.f32 %0, [%1];" : "=f"(v) : "r"(addr));
   return v;
 }
+__device__ __forceinline__ float2 lds_f32x2(uint32_t addr) {
+  float2 v;
+  asm volatile("ld.shared.v2.f32 {%0, %1}, [%2];" : "=f"(v.x), "=f"(v.y) : "r"(addr));
+  return v;
+}
 __device__ __forceinline__ void cp_async16(uint32_t saddr, const void* g) {
   asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(saddr), "l"(g));
 }
@@ -456,14 +465,22 @@ __device__ __forceinline__ float2 fsub2(float2 a, float2 b) {
 
 // Two phi rows at once (window offsets m0 and m0+1) as (row, row+1) pairs, so
 // the horizontal pass runs on the packed FFMA2 pipe: out[c] = sum_d w_d t(c+d).
+// The vertical values of both rows come from one lookup in the pair table:
+// entry i of the 2R+2-bit window is (t(i & low 2R+1 bits), t(i >> 1)) -- the
+// same fp32 values as two t-LUT lookups.  win8 holds the window words
+// pre-shifted by 3 (byte offsets of 8-byte entries).  The table is a
+// file-scope __shared__ array, so its address is a link-time constant that
+// folds into the LDS immediate (offset register + constant, no add).
+__shared__ __align__(16) float2 g_pair_lut[1 << (2 * 4 + 2)];      // R <= 4
+
 template <int R, int NT, int NOUT, int SRC = SRC_SMOOTH>
-__device__ __forceinline__ void phi_rows2_int(const FastParams& P, const uint32_t (&win4)[NT],
-                                              int m0, uint32_t lut_base, float2 (&out)[NOUT]) {
-  constexpr uint32_t PM4 = ((1u << (2 * R + 1)) - 1u) << 2;
+__device__ __forceinline__ void phi_rows2_int(const FastParams& P, const uint32_t (&win8)[NT],
+                                              int m0, uint32_t lut2_base, float2 (&out)[NOUT]) {
+  constexpr uint32_t PM8 = ((1u << (2 * R + 2)) - 1u) << 3;
   if (SRC == SRC_SCALED) {
 #pragma unroll
     for (int c = 0; c < NOUT; ++c) {
-      const uint32_t w = win4[c + R] >> (m0 + R + 2);
+      const uint32_t w = win8[c + R] >> (m0 + R + 3);
       out[c] = make_float2((w & 1u) ? P.scale32 : -P.scale32,
                            (w & 2u) ? P.scale32 : -P.scale32);
     }
@@ -471,9 +488,8 @@ __device__ __forceinline__ void phi_rows2_int(const FastParams& P, const uint32_
   }
 #pragma unroll
   for (int j = 0; j < NT; ++j) {
-    float2 t;
-    t.x = lds_f32(((win4[j] >> m0) & PM4) | lut_base);
-    t.y = lds_f32(((win4[j] >> (m0 + 1)) & PM4) | lut_base);
+    const float2 t = *reinterpret_cast<const float2*>(
+        reinterpret_cast<const char*>(g_pair_lut) + ((win8[j] >> m0) & PM8));
 #pragma unroll
     for (int c = 0; c < NOUT; ++c) {
       const int d = j - c - R;
@@ -501,7 +517,7 @@ __device__ __noinline__ uint32_t update_tie_cols(const FastParams& P, uint32_t l
   uint32_t win4[NT];
 #pragma unroll
   for (int j = 0; j < NT; ++j)
-    win4[j] = __funnelshift_r(__ldg(wp + j), __ldg(wp + P.g.pitch_w + j), base & 31) << 2;
+    win4[j] = __funnelshift_r(__ldg(wp + j), __ldg(wp + P.g.pitch_w + j), base & 31) << 3;
   float2 pa[NP], pb[NP];
   phi_rows2_int<R, NT, NP, SRC>(P, win4, 0, lut_base, pa);     // rows k-1, k
   phi_rows2_int<R, NT, NP, SRC>(P, win4, 2, lut_base, pb);     // rows k+1, k+2
@@ -529,7 +545,7 @@ __device__ __noinline__ uint32_t partition_tie_cols(const FastParams& P, uint32_
   uint32_t win4[NT];
 #pragma unroll
   for (int j = 0; j < NT; ++j)
-    win4[j] = __funnelshift_r(__ldg(wp + j), __ldg(wp + P.g.pitch_w + j), base & 31) << 2;
+    win4[j] = __funnelshift_r(__ldg(wp + j), __ldg(wp + P.g.pitch_w + j), base & 31) << 3;
   float2 ph[8];
   phi_rows2_int<R, NT, 8>(P, win4, 0, lut_base, ph);
   uint32_t cols = 0u;
@@ -557,7 +573,7 @@ __device__ __forceinline__ void update_block_int2(const FastParams& P, uint32_t 
   const int lane = threadIdx.x & 31;
   uint32_t win4[NT];
 #pragma unroll
-  for (int j = 0; j < NT; ++j) win4[j] = __funnelshift_r(prev[j], cur[j], 31 - R) << 2;
+  for (int j = 0; j < NT; ++j) win4[j] = __funnelshift_r(prev[j], cur[j], 31 - R) << 3;
   const uint32_t ring_s = (uint32_t)__cvta_generic_to_shared(ring) + lane * CPL * 4;
   const size_t dpitch = P.g.data_pitch;
   const float* gsrc = P.data32 + (size_t)y0 * dpitch + x0;
@@ -595,7 +611,7 @@ __device__ __forceinline__ void update_block_int2(const FastParams& P, uint32_t 
     if (s == 8) {                               // window base y0+16-R for rows >= 17
 #pragma unroll
       for (int j = 0; j < NT; ++j)
-        win4[j] = __funnelshift_r(__ldg(wrow + j), __ldg(wrow + P.g.pitch_w + j), 16 - R) << 2;
+        win4[j] = __funnelshift_r(__ldg(wrow + j), __ldg(wrow + P.g.pitch_w + j), 16 - R) << 3;
     }
     const int kn = 2 * s + 1;                   // first phi row of this step's pair
     phi_rows2_int<R, NT, NP, SRC>(P, win4, s < 8 ? kn + 1 : kn - 16, lut_base, pn);
@@ -687,7 +703,7 @@ __device__ __forceinline__ void update_block_half(const FastParams& P, uint32_t 
     uint32_t win4[NT];
     const int sh = h0 ? 15 - R : 31 - R;        // window base row y0 + h0 - 1 - R
 #pragma unroll
-    for (int j = 0; j < NT; ++j) win4[j] = __funnelshift_r(wlo[j], whi[j], sh) << 2;
+    for (int j = 0; j < NT; ++j) win4[j] = __funnelshift_r(wlo[j], whi[j], sh) << 3;
     const uint32_t ring_s = (uint32_t)__cvta_generic_to_shared(ring) + lane * CPL * 4;
     const size_t dpitch = P.g.data_pitch;
     const float* gsrc = P.data32 + (size_t)(y0 + h0) * dpitch + x0;
@@ -785,21 +801,26 @@ __device__ __forceinline__ void update_block_half(const FastParams& P, uint32_t 
     reinterpret_cast<uint4*>(dst)[q] = make_uint4(ow[4 * q], ow[4 * q + 1], ow[4 * q + 2], ow[4 * q + 3]);
 }
 
-// The 2 KB t-LUT must sit at a 2 KB-aligned shared address for the OR-based
-// addressing of phi_row_int; static __shared__ alignment is not guaranteed
-// relative to the CTA's shared window, so it is carved out of a 4 KB buffer.
-__device__ __forceinline__ float* aligned_lut(float* raw4k) {
-  const uint32_t a = (uint32_t)__cvta_generic_to_shared(raw4k);
-  return raw4k + (((a + 2047u) & ~2047u) - a) / 4;
-}
+// Shared lookup tables: the t-LUT and s-LUT (2^(2R+1) floats each) and the
+// pair table (2^(2R+2) float2).  phi_rows2_int adds the pair table's shared
+// address to the byte offset; with the table a static __shared__ array that
+// address is a link-time constant the compiler folds into the LDS immediate.
+struct SharedLuts {
+  float* lt;
+  float* ls;
+  uint32_t lt2;                                  // pair table (shared address, g_pair_lut)
+};
 
 template <int R>
-__device__ __forceinline__ void load_luts(const FastParams& P, float* s_lt, float* s_ls) {
+__device__ __forceinline__ void load_luts(const FastParams& P, const SharedLuts& L) {
   constexpr int NPAT = 1 << (2 * R + 1);
   for (int q = threadIdx.x; q < NPAT; q += blockDim.x) {
-    s_lt[q] = __ldg(&P.lut_t[q]);
-    s_ls[q] = __ldg(&P.lut_s[q]);
+    L.lt[q] = __ldg(&P.lut_t[q]);
+    L.ls[q] = __ldg(&P.lut_s[q]);
   }
+  float2* lt2 = g_pair_lut;                     // 2 NPAT entries
+  for (int q = threadIdx.x; q < 2 * NPAT; q += blockDim.x)
+    lt2[q] = make_float2(__ldg(&P.lut_t[q & (NPAT - 1)]), __ldg(&P.lut_t[q >> 1]));
 }
 
 __device__ __forceinline__ int grab_unit(const FastParams& P, int lane) {
@@ -962,11 +983,11 @@ __device__ __noinline__ void border_update_unit(const FastParams& P, const float
 // the tile's scalars (stop, A, B, guards) are read per unit.
 // HALF: split-warp units of 128 columns (update_block_half) for small images.
 template <int R, int MODEL, int SRC, bool BATCH, bool HALF>
-__global__ void __launch_bounds__(kThreads, 4) k_update(FastParams P) {
+__global__ void __launch_bounds__(kThreads, kUpdateCtasPerSm) k_update(FastParams P) {
   constexpr int CPL = kUpdCols;
-  constexpr int NPAT = 1 << (2 * R + 1);
   constexpr int NT = CPL + 2 * (R + 1);
-  __shared__ __align__(16) float s_lt_raw[1024];
+  constexpr int NPAT = 1 << (2 * R + 1);
+  __shared__ float s_lt[NPAT];
   __shared__ float s_ls[NPAT];
   __shared__ __align__(16) float s_ring[(kThreads / 32) * kRing2 * 32 * CPL];
   LSE_TRACE_ENTRY
@@ -974,8 +995,8 @@ __global__ void __launch_bounds__(kThreads, 4) k_update(FastParams P) {
   // copy: handing it the kernel parameter block itself would force a
   // per-thread local-memory copy of the block (taking its address)
   __shared__ FastParams s_P;
-  float* const s_lt = aligned_lut(s_lt_raw);
-  load_luts<R>(P, s_lt, s_ls);                   // static data: before the dependency wait
+  const SharedLuts luts{s_lt, s_ls, (uint32_t)__cvta_generic_to_shared(g_pair_lut)};
+  load_luts<R>(P, luts);                         // static data: before the dependency wait
   if (threadIdx.x == 0) s_P = P;
   __syncthreads();
   pdl_wait();
@@ -1063,7 +1084,7 @@ __global__ void __launch_bounds__(kThreads, 4) k_update(FastParams P) {
                                                         whi[R + 3 + 4 * q], whi[R + 4 + 4 * q]);
         continue;
       }
-      update_block_half<R, MODEL, CPL, SRC>(P, (uint32_t)__cvta_generic_to_shared(s_lt),
+      update_block_half<R, MODEL, CPL, SRC>(P, luts.lt2,
                                             s_ring + (threadIdx.x >> 5) * kRing2 * 32 * CPL, r,
                                             x0, A, B, eps_u, wlo, whi, tile, act);
       continue;
@@ -1095,7 +1116,7 @@ __global__ void __launch_bounds__(kThreads, 4) k_update(FastParams P) {
       continue;
     }
     if (!act) continue;
-    update_block_int2<R, MODEL, CPL, SRC>(P, (uint32_t)__cvta_generic_to_shared(s_lt),
+    update_block_int2<R, MODEL, CPL, SRC>(P, luts.lt2,
                                           s_ring + (threadIdx.x >> 5) * kRing2 * 32 * CPL, r, x0,
                                           A, B, eps_u, prev, cur, tile);
   }
@@ -1347,7 +1368,7 @@ __device__ __forceinline__ void partition_block(const FastParams& P, const float
     const int xc = x0 - R + j;
     cm[j] = (INT || (xc >= 0 && xc < W)) ? 0xffffffffu : 0u;
     win[j] = __funnelshift_r(prev[j], cur[j], 32 - R);     // base row y0-R
-    if (INT) win[j] <<= 2;                                  // byte offsets for phi_row_int
+    if (INT) win[j] <<= 3;                                  // byte offsets for phi_rows2_int
   }
   float ph[8];
   uint32_t fbrows = 0u;
@@ -1360,7 +1381,7 @@ __device__ __forceinline__ void partition_block(const FastParams& P, const float
       for (int j = 0; j < NT; ++j) {
         const int xc = x0 - R + j;
         win[j] = __funnelshift_r(word_at<INT>(P, r, xc), word_at<INT>(P, r + 1, xc), 16 - R);
-        if (INT) win[j] <<= 2;
+        if (INT) win[j] <<= 3;
       }
     }
     const int i = y0 + k;
@@ -1596,14 +1617,14 @@ __device__ __noinline__ void border_partition_unit(const FastParams& P, const fl
 // interior units]; a tile's partials are reduced by its own finalize CTA.
 template <int R, bool PART, bool CKPT, bool MASKONLY, bool BATCH>
 __global__ void __launch_bounds__(kThreads, kPartitionCtasPerSm) k_partition(FastParams P) {
-  constexpr int NPAT = 1 << (2 * R + 1);
   constexpr int NT = kColsPerThread + 2 * R;
-  __shared__ __align__(16) float s_lt_raw[1024];
+  constexpr int NPAT = 1 << (2 * R + 1);
+  __shared__ float s_lt[NPAT];
   __shared__ float s_ls[NPAT];
   LSE_TRACE_ENTRY
   __shared__ FastParams s_P;                     // see k_update
-  float* const s_lt = aligned_lut(s_lt_raw);
-  load_luts<R>(P, s_lt, s_ls);                   // static data: before the dependency wait
+  const SharedLuts luts{s_lt, s_ls, (uint32_t)__cvta_generic_to_shared(g_pair_lut)};
+  load_luts<R>(P, luts);                         // static data: before the dependency wait
   if (threadIdx.x == 0) s_P = P;
   __syncthreads();
   pdl_wait();
@@ -1681,7 +1702,7 @@ __global__ void __launch_bounds__(kThreads, kPartitionCtasPerSm) k_partition(Fas
         } else if (!active) {
           continue;
         } else {
-          partition_block<R, true>(P, s_lt, s_ls, (uint32_t)__cvta_generic_to_shared(s_lt), r,
+          partition_block<R, true>(P, s_lt, s_ls, luts.lt2, r,
                                    x0, eps_phi, prev, cur, pw, mw, tile);
         }
         if (!BATCH || part_t == PART) partition_commit<PART, CKPT, MASKONLY>(P, r, x0, pw, mw, d, tile);
