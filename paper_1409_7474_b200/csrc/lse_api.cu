@@ -156,7 +156,7 @@ struct lse_run {
   double* d_bands64 = nullptr;
   uint32_t* d_chg = nullptr;
   TilePartial* d_bpart = nullptr;
-  unsigned long long* d_pmax = nullptr;   // per-CTA maxima of the band peak pass
+  unsigned long long* d_pmax = nullptr;   // band chain arrival counters (2, zeroed)
   // reusable device scratch for per-call buffers (mask read-back, injected
   // signs, seed polygons, flags): no cudaMalloc / cudaFree -- each of which
   // can stall the device -- on the per-job paths
@@ -219,8 +219,8 @@ struct lse_run {
   int nchunk = 1, nchunk_u = 1, nseg = 1, seg_chunks = 1;
   Geo gu{}, gu_all{}, gp{};   // work geometry: update, update with no interior, partition
   long long ni_upd = 0, nb_upd[2] = {0, 0}, ni_part = 0, nb_part = 0;
-  long long ni_upd_half = 0;   // interior update units in split-warp (half) mode
-  bool half_units = false;     // small images: 128-column split-warp update units
+  long long ni_upd_split = 0;  // interior update units in split-warp mode
+  int split_parts = 1;         // small images: 256/split_parts-column split-warp update units
   unsigned long long* d_work = nullptr;
   TilePartial* d_part_fin = nullptr;
   TilePartial* d_part_init = nullptr;
@@ -488,15 +488,16 @@ void trace_flush() {
 
 template <int R, int MODEL, int SRC>
 int launch_update(lse_run* r, FastParams P) {
-  const bool half = r->half_units;
-  const long long n = r->nb_upd[0] + (half ? r->ni_upd_half : r->ni_upd);
+  const int ns = r->split_parts;
+  const long long n = r->nb_upd[0] + (ns > 1 ? r->ni_upd_split : r->ni_upd);
   const int g = fast_grid(n, kUpdateCtasPerSm);
   P.work_base = take_work(r, n, g);
 #ifdef LSE_UNIT_TRACE
   P.trace = trace_begin(r, n, g, "update", r->nb_upd[0]);
 #endif
-  if (half) TRY(launch_pdl(k_update<R, MODEL, SRC, false, true>, g, kThreads, r->st, P));
-  else TRY(launch_pdl(k_update<R, MODEL, SRC, false, false>, g, kThreads, r->st, P));
+  if (ns == 4) TRY(launch_pdl(k_update<R, MODEL, SRC, false, 4>, g, kThreads, r->st, P));
+  else if (ns == 2) TRY(launch_pdl(k_update<R, MODEL, SRC, false, 2>, g, kThreads, r->st, P));
+  else TRY(launch_pdl(k_update<R, MODEL, SRC, false, 1>, g, kThreads, r->st, P));
 #ifdef LSE_UNIT_TRACE
   trace_after(r, P.trace);
 #endif
@@ -805,31 +806,28 @@ int generic_iteration(lse_run* r, long long it, bool reinit_now, bool reg_now, b
 // pixel (fp32 plane for the fused kernels) and its peak, the coefficients
 int band_chain(lse_run* r, bool absolute, bool ckpt, long long it) {
   const dim3 gr((r->g.pitch_w + 1023) / 1024, r->g.HR);
-  const int nblk = (int)(gr.x * gr.y);
+  const int n = (int)(r->nb_part + r->ni_part);
+  PartRanges M{{r->d_part, r->d_part, r->d_part}, {ckpt ? n : 0, 0, 0}};
+  unsigned long long* cnt = r->d_pmax;          // [0]: band sums, [1]: band peak arrivals
   if (absolute)
     TRY(launch_pdl(k_band_sums<true>, gr, 256, r->st, (const uint32_t*)nullptr,
                    (const uint32_t*)r->d_P, (const ExactCtx*)r->d_ctx, r->d_bpart, r->g,
-                   (const Scalars*)r->d_scal));
+                   r->d_scal, cnt, M, ckpt ? 1 : 0, it));
   else
     TRY(launch_pdl(k_band_sums<false>, gr, 256, r->st, (const uint32_t*)r->d_chg,
                    (const uint32_t*)r->d_P, (const ExactCtx*)r->d_ctx, r->d_bpart, r->g,
-                   (const Scalars*)r->d_scal));
-  const int n = (int)(r->nb_part + r->ni_part);
-  PartRanges M{{r->d_part, r->d_part, r->d_part}, {ckpt ? n : 0, 0, 0}};
-  TRY(launch_pdl(k_finalize_bands, 1, 256, r->st, (const TilePartial*)r->d_bpart, nblk, M,
-                 r->d_scal, absolute ? 1 : 0, ckpt ? 1 : 0, it));
-  const dim3 gp((r->W + 1023) / 1024, r->H);
-  unsigned long long* pmax = r->d_pmax;
+                   r->d_scal, cnt, M, ckpt ? 1 : 0, it));
+  // peak pass: ~8 CTAs per SM, each a 1024-column block of every gy-th row
+  const int gx = (r->W + 1023) / 1024;
+  const int gy = std::max(1, std::min(r->H, num_sms() * 8 / gx));
+  const dim3 gp(gx, gy);
   const ExactCtx* cctx = r->d_ctx;
-  const Scalars* csc = r->d_scal;
   switch (r->nbands) {
-    case 1: TRY(launch_pdl(k_band_peak<1>, gp, 256, r->st, cctx, csc, r->d_data32, pmax, r->g)); break;
-    case 2: TRY(launch_pdl(k_band_peak<2>, gp, 256, r->st, cctx, csc, r->d_data32, pmax, r->g)); break;
-    case 3: TRY(launch_pdl(k_band_peak<3>, gp, 256, r->st, cctx, csc, r->d_data32, pmax, r->g)); break;
-    default: TRY(launch_pdl(k_band_peak<4>, gp, 256, r->st, cctx, csc, r->d_data32, pmax, r->g)); break;
+    case 1: TRY(launch_pdl(k_band_peak<1>, gp, 256, r->st, cctx, r->d_scal, r->d_data32, cnt + 1, r->g)); break;
+    case 2: TRY(launch_pdl(k_band_peak<2>, gp, 256, r->st, cctx, r->d_scal, r->d_data32, cnt + 1, r->g)); break;
+    case 3: TRY(launch_pdl(k_band_peak<3>, gp, 256, r->st, cctx, r->d_scal, r->d_data32, cnt + 1, r->g)); break;
+    default: TRY(launch_pdl(k_band_peak<4>, gp, 256, r->st, cctx, r->d_scal, r->d_data32, cnt + 1, r->g)); break;
   }
-  TRY(launch_pdl(k_band_coeffs, 1, 1024, r->st, r->d_scal, (const unsigned long long*)pmax,
-                 (int)(gp.x * gp.y)));
   return LSE_OK;
 }
 
@@ -1196,8 +1194,20 @@ int create_impl(lse_run** out, const lse_params* p, long long height, long long 
   r->nchunk_u = (r->W + kUpdChunk - 1) / kUpdChunk;
   {
     const int R = r->R, H = r->H, W = r->W;
-    r->gu = make_geo(H, W, R, 1 + R, 1 + R, R + 1);   // update reaches R+1 rows/columns
-    r->gp = make_geo(H, W, R, R, R, R);               // partition reaches R
+    // border row parts (lse_geometry.cuh): border units are the critical path
+    // of small images -- 2-row border lanes when there is no interior at all,
+    // 4-row lanes when the interior units are split (see below), else 8
+    const long long warps_u = (long long)num_sms() * kUpdateCtasPerSm * (kThreads / 32);
+    int bq = kBorderQ;
+    {
+      const Geo g0 = make_geo(H, W, R, 1 + R, 1 + R, R + 1);
+      const long long ni0 = (long long)(g0.r_hi - g0.r_lo) * g0.nci + (g0.nB1 + 31) / 32;
+      bq = ni0 == 0 ? 16 : ni0 < 2 * warps_u ? 8 : kBorderQ;
+    }
+    if (const char* bv = std::getenv("LSE_BORDER_Q"))
+      bq = std::atoi(bv) >= 16 ? 16 : std::atoi(bv) >= 8 ? 8 : 4;
+    r->gu = make_geo(H, W, R, 1 + R, 1 + R, R + 1, bq);   // update reaches R+1 rows/columns
+    r->gp = make_geo(H, W, R, R, R, R, bq);               // partition reaches R
     if (si && (!geo_restrict_rows(r->gu, si->own_lo, si->own_hi) ||
                !geo_restrict_rows(r->gp, si->own_lo, si->own_hi))) {
       delete r;
@@ -1205,10 +1215,17 @@ int create_impl(lse_run** out, const lse_params* p, long long height, long long 
     }
     r->gu_all = geo_all_border(r->gu, H);
     r->ni_upd = (long long)(r->gu.r_hi - r->gu.r_lo) * r->gu.nci + (r->gu.nB1 + 31) / 32;
-    r->ni_upd_half = 2LL * (r->gu.r_hi - r->gu.r_lo) * r->gu.nci + (r->gu.nB1 + 15) / 16;
-    // too few full units to keep every warp busy for several rounds: halve them
-    const char* hv = std::getenv("LSE_HALF_UNITS");
-    r->half_units = hv ? std::atoi(hv) != 0 : r->ni_upd < 2LL * num_sms() * 16;
+    // too few full units to keep every warp busy for several rounds: split
+    // them into 2 or 4 row parts (shorter units, more of them)
+    {
+      int ns = 1;
+      while (ns < 4 && (long long)ns * r->ni_upd < 2 * warps_u) ns *= 2;
+      const char* hv = std::getenv("LSE_SPLIT_PARTS");
+      if (hv) ns = std::atoi(hv) >= 4 ? 4 : std::atoi(hv) >= 2 ? 2 : 1;
+      r->split_parts = ns;
+      r->ni_upd_split = (long long)ns * (r->gu.r_hi - r->gu.r_lo) * r->gu.nci +
+                        (r->gu.nB1 + 32 / ns - 1) / (32 / ns);
+    }
     r->nb_upd[0] = border_units(r->gu);
     r->nb_upd[1] = r->gu_all.nA;
     // partition segments: >= ~8 interior units per resident warp, <= 16 chunks
@@ -1245,9 +1262,11 @@ int create_impl(lse_run** out, const lse_params* p, long long height, long long 
   if (p->model == LSE_MODEL_BANDS &&
       ((rc = dalloc(&r->d_bands32, (size_t)p->n_bands * r->g.data_pitch * r->H)) ||
        (rc = dalloc(&r->d_chg, nbits)) ||
-       (rc = dalloc(&r->d_pmax, (size_t)r->H * ((r->W + 1023) / 1024))) ||
+       (rc = dalloc(&r->d_pmax, 2)) ||
        (rc = dalloc(&r->d_bpart, (size_t)p->n_bands * r->g.HR * ((r->g.pitch_w + 1023) / 1024)))))
     return cleanup(rc);
+  if (r->d_pmax && cudaMemset(r->d_pmax, 0, 2 * sizeof(unsigned long long)) != cudaSuccess)
+    return cleanup(fail(LSE_ERR_CUDA, "cudaMemset"));
   if (cudaMallocHost((void**)&r->h_scal, sizeof(Scalars)) != cudaSuccess)
     return cleanup(fail(LSE_ERR_CUDA, "pinned alloc failed"));
   cudaMemsetAsync(r->d_work, 0, sizeof(unsigned long long), r->st);
@@ -1697,9 +1716,9 @@ int batch_iteration(lse_batch* b, long long it, bool ckpt, int src, bool any_reg
     const int g = fast_grid(n, kUpdateCtasPerSm);
     P.work_base = batch_take_work(b, n, g);
     if (src == SRC_SCALED)
-      TRY(launch_pdl(k_update<R, REGION, SRC_SCALED, true, false>, g, kThreads, b->st, P));
+      TRY(launch_pdl(k_update<R, REGION, SRC_SCALED, true, 1>, g, kThreads, b->st, P));
     else
-      TRY(launch_pdl(k_update<R, REGION, SRC_SMOOTH, true, false>, g, kThreads, b->st, P));
+      TRY(launch_pdl(k_update<R, REGION, SRC_SMOOTH, true, 1>, g, kThreads, b->st, P));
   }
   b->cur ^= 1;
   if (!any_region && !ckpt) return LSE_OK;

@@ -676,15 +676,16 @@ __device__ __forceinline__ void update_block_int2(const FastParams& P, uint32_t 
     reinterpret_cast<uint4*>(dst)[q] = make_uint4(ow[4 * q], ow[4 * q + 1], ow[4 * q + 2], ow[4 * q + 3]);
 }
 
-// Split-warp interior block for small images: lanes 0-15 take rows 0-15 and
-// lanes 16-31 rows 16-31 of the same 8-column groups (a warp unit covers 128
-// columns), so a unit is 8 row pairs long instead of 16.  Each half keeps its
-// own window with base row h0 - 1 - R, so the window offsets -- and the whole
-// instruction stream -- are the same in both halves; the two 16-bit halves of
-// each state word are merged by one shuffle.  Every lane of the warp calls it
-// (act = false: no work, still shuffles).
-template <int R, int MODEL, int CPL, int SRC>
-__device__ __forceinline__ void update_block_half(const FastParams& P, uint32_t lut_base,
+// Split-warp interior block for small images: the warp's lanes form NS row
+// parts of 32/NS lanes; part p takes rows p*RP .. p*RP+RP-1 (RP = 32/NS) of
+// the same 8-column groups (a warp unit covers 256/NS columns), so a unit is
+// RP/2 row pairs long instead of 16.  Each part keeps its own window with base
+// row h0 - 1 - R, so the window offsets -- and the whole instruction stream --
+// are the same in every part; the RP-bit pieces of each state word are merged
+// by log2(NS) shuffles.  Every lane of the warp calls it (act = false: no work,
+// still shuffles).  wlo/whi: word-rows r-1, r (part 0) or r, r+1 (parts >= 1).
+template <int R, int MODEL, int CPL, int SRC, int NS>
+__device__ __forceinline__ void update_block_split(const FastParams& P, uint32_t lut_base,
                                                   float* ring, int r, int x0, float A, float B,
                                                   float eps_u,
                                                   const uint32_t (&wlo)[CPL + 2 * (R + 1)],
@@ -693,22 +694,25 @@ __device__ __forceinline__ void update_block_half(const FastParams& P, uint32_t 
   constexpr int NT = CPL + 2 * (R + 1);
   constexpr int NP = CPL + 2;
   constexpr uint32_t kSlot = 32 * CPL * 4;
+  constexpr int RP = 32 / NS;                   // rows per part
+  static_assert(NS == 2 || NS == 4, "row parts");
+  static_assert(RP >= R + 1, "part window must fit in two words");
   const int lane = threadIdx.x & 31;
-  const int h0 = (lane >> 4) * 16;              // first row of this lane's half
+  const int h0 = (lane / (32 / NS)) * RP;       // first row of this lane's part
   const int y0 = r * 32;
   uint32_t ow[CPL];
 #pragma unroll
   for (int c = 0; c < CPL; ++c) ow[c] = 0u;
   if (act) {
     uint32_t win4[NT];
-    const int sh = h0 ? 15 - R : 31 - R;        // window base row y0 + h0 - 1 - R
+    const int sh = h0 ? h0 - 1 - R : 31 - R;    // window base row y0 + h0 - 1 - R
 #pragma unroll
     for (int j = 0; j < NT; ++j) win4[j] = __funnelshift_r(wlo[j], whi[j], sh) << 3;
     const uint32_t ring_s = (uint32_t)__cvta_generic_to_shared(ring) + lane * CPL * 4;
     const size_t dpitch = P.g.data_pitch;
     const float* gsrc = P.data32 + (size_t)(y0 + h0) * dpitch + x0;
 #pragma unroll
-    for (int q = 0; q < kRing2 - 2; q += 2) {  // rows 0 .. 5 of the half in flight
+    for (int q = 0; q < kRing2 - 2; q += 2) {  // rows 0 .. 5 of the part in flight
 #pragma unroll
       for (int v = 0; v < CPL / 4; ++v) {
         cp_async16(ring_s + q * kSlot + v * 16, gsrc + 4 * v);
@@ -721,8 +725,8 @@ __device__ __forceinline__ void update_block_half(const FastParams& P, uint32_t 
     uint32_t fbrows = 0u;
     phi_rows2_int<R, NT, NP, SRC>(P, win4, 0, lut_base, pp);   // rows h0-1, h0
 #pragma unroll 2
-    for (int s = 0; s < 8; ++s) {
-      if (2 * s + kRing2 - 2 < 16) {
+    for (int s = 0; s < RP / 2; ++s) {
+      if (2 * s + kRing2 - 2 < RP) {
         const uint32_t d0 = ring_s + ((2 * s + kRing2 - 2) & (kRing2 - 1)) * kSlot;
 #pragma unroll
         for (int v = 0; v < CPL / 4; ++v) {
@@ -770,11 +774,12 @@ __device__ __forceinline__ void update_block_half(const FastParams& P, uint32_t 
       for (int c = 0; c < NP; ++c) pp[c] = pn[c];
     }
     cp_async_wait<0>();
-    // 16 appended sign bits: after the reversal rows h0 .. h0+15 sit in bits 16..31
+    // RP appended sign bits: after the reversal rows h0 .. h0+RP-1 sit in the
+    // top RP bits
 #pragma unroll
     for (int c = 0; c < CPL; ++c) {
-      const uint32_t v = ~__brev(ow[c]) & 0xffff0000u;
-      ow[c] = h0 ? v : v >> 16;
+      const uint32_t v = ~__brev(ow[c]) & (0xffffffffu << (32 - RP));
+      ow[c] = v >> (32 - RP - h0);
     }
     while (fbrows) {
       const int k = __ffs(fbrows) - 1;
@@ -793,7 +798,9 @@ __device__ __forceinline__ void update_block_half(const FastParams& P, uint32_t 
     }
   }
 #pragma unroll
-  for (int c = 0; c < CPL; ++c) ow[c] |= __shfl_xor_sync(0xffffffffu, ow[c], 16);
+  for (int m = 32 / NS; m < 32; m <<= 1)
+#pragma unroll
+    for (int c = 0; c < CPL; ++c) ow[c] |= __shfl_xor_sync(0xffffffffu, ow[c], m);
   if (!act || h0) return;
   uint32_t* dst = P.bits_out + (size_t)r * P.g.pitch_w + x0;
 #pragma unroll
@@ -838,13 +845,13 @@ __device__ __forceinline__ int grab_unit(const FastParams& P, int lane) {
 // |grad phi| == 0, v == 0 and u == phi exactly, so b^{n+1} == b^n and the
 // chunk is copied without reading the data plane).
 // INT = false: border units (zero padding, one-sided gradients).
-// Border rows k0 .. k0 + kBorderRows - 1 of the lane block (r, x0): zero
+// Border rows k0 .. k0 + nrows - 1 of the lane block (r, x0): zero
 // padding / one-sided gradients (update_block's arithmetic on a row range).
 // ow[c] gets bit k for the rows of the range only.
 template <int R, int MODEL, int SRC, int CPL>
 __device__ __forceinline__ void update_rows_border(const FastParams& P, const float* s_lt,
                                                    const float* s_ls, int r, int x0, int k0,
-                                                   float A, float B, float eps_u,
+                                                   int nrows, float A, float B, float eps_u,
                                                    uint32_t (&ow)[CPL]) {
   constexpr int NT = CPL + 2 * (R + 1);
   constexpr int NP = CPL + 2;
@@ -867,9 +874,9 @@ __device__ __forceinline__ void update_rows_border(const FastParams& P, const fl
   phi_row<R, SRC, false, NT, NP>(P, win, cm, 1, y0 + k0, s_lt, s_ls, p0);
   load_data_row<false, CPL>(P, y0 + k0, x0, dcur);
 #pragma unroll 1
-  for (int k = k0; k < k0 + kBorderRows; ++k) {
+  for (int k = k0; k < k0 + nrows; ++k) {
     const int kk = k + 1;                        // phi row produced in this step
-    if (kk < k0 + kBorderRows) load_data_row<false, CPL>(P, y0 + kk, x0, dnext);
+    if (kk < k0 + nrows) load_data_row<false, CPL>(P, y0 + kk, x0, dnext);
     phi_row<R, SRC, false, NT, NP>(P, win, cm, kk - k0 + 1, y0 + kk, s_lt, s_ls, pn);
     const int i = y0 + k;
     if (i < H) {
@@ -912,8 +919,8 @@ __device__ __forceinline__ void update_rows_border(const FastParams& P, const fl
   }
 }
 
-// Border unit: kBorderItems lane groups x kBorderQ row quarters.  Called by
-// every lane of the warp (the quarters are merged with shuffles); not
+// Border unit: bitems lane groups x bq row parts.  Called by every lane of
+// the warp (the parts are merged with shuffles); not
 // inlined, so its register needs do not constrain the interior loop.
 template <int R, int MODEL, int SRC>
 __device__ __forceinline__ void border_update_body(const FastParams& P, const float* s_lt,
@@ -923,8 +930,9 @@ __device__ __forceinline__ void border_update_body(const FastParams& P, const fl
   const int lane = threadIdx.x & 31;
   int r = 0, x0 = 0;
   const bool act = border_lane(P.gu, unit, lane, P.g.W, r, x0);
+  const int items = P.gu.bitems;                 // lane groups per unit = rows per lane
   if (stopped) {                                 // converged tile: keep its state
-    if (!act || lane >= kBorderItems) return;
+    if (!act || lane >= items) return;
     const uint32_t* src = P.bits_in + (size_t)r * P.g.pitch_w + x0;
     uint32_t* dst = P.bits_out + (size_t)r * P.g.pitch_w + x0;
 #pragma unroll
@@ -936,14 +944,13 @@ __device__ __forceinline__ void border_update_body(const FastParams& P, const fl
 #pragma unroll
   for (int c = 0; c < CPL; ++c) ow[c] = 0u;
   if (act)
-    update_rows_border<R, MODEL, SRC, CPL>(P, s_lt, s_ls, r, x0,
-                                           (lane / kBorderItems) * kBorderRows, A, B, eps_u, ow);
+    update_rows_border<R, MODEL, SRC, CPL>(P, s_lt, s_ls, r, x0, (lane / items) * items, items,
+                                           A, B, eps_u, ow);
+  for (int o = items; o < 32; o <<= 1) {
 #pragma unroll
-  for (int c = 0; c < CPL; ++c) {
-#pragma unroll
-    for (int o = kBorderItems; o < 32; o <<= 1) ow[c] |= __shfl_xor_sync(0xffffffffu, ow[c], o);
+    for (int c = 0; c < CPL; ++c) ow[c] |= __shfl_xor_sync(0xffffffffu, ow[c], o);
   }
-  if (!act || lane >= kBorderItems) return;
+  if (!act || lane >= items) return;
   uint32_t* dst = P.bits_out + (size_t)r * P.g.pitch_w + x0;
 #pragma unroll
   for (int q = 0; q < CPL / 4; ++q)
@@ -981,8 +988,9 @@ __device__ __noinline__ void border_update_unit(const FastParams& P, const float
 // so their longer latency overlaps the interior work of the other warps).
 // BATCH: every unit of every tile, [all border units][all interior units];
 // the tile's scalars (stop, A, B, guards) are read per unit.
-// HALF: split-warp units of 128 columns (update_block_half) for small images.
-template <int R, int MODEL, int SRC, bool BATCH, bool HALF>
+// NS > 1: split-warp units of 256/NS columns (update_block_split) for small
+// images.
+template <int R, int MODEL, int SRC, bool BATCH, int NS>
 __global__ void __launch_bounds__(kThreads, kUpdateCtasPerSm) k_update(FastParams P) {
   constexpr int CPL = kUpdCols;
   constexpr int NT = CPL + 2 * (R + 1);
@@ -1011,7 +1019,9 @@ __global__ void __launch_bounds__(kThreads, kUpdateCtasPerSm) k_update(FastParam
   float A = sc->A, B = sc->B, eps_u = sc->eps_u;
   const int lane = threadIdx.x & 31;
   const int nb = border_units(P.gu);
-  const int ni = HALF ? 2 * chunk_units(P.gu) + (P.gu.nB1 + 15) / 16 : interior_units(P.gu);
+  constexpr int LPP = 32 / NS;                   // lanes per row part
+  const int ni = NS > 1 ? NS * chunk_units(P.gu) + (P.gu.nB1 + LPP - 1) / LPP
+                        : interior_units(P.gu);
   const int T = BATCH ? P.ntiles : 1;
   const int nunits = T * (nb + ni);
   LSE_TRACE_DECL
@@ -1044,14 +1054,14 @@ __global__ void __launch_bounds__(kThreads, kUpdateCtasPerSm) k_update(FastParam
     const int iu = lu - nb;
     bool act = true;
     const int nch = chunk_units(P.gu);
-    if (HALF) {                                   // half chunks; lane pairs (L, L+16) share columns
-      if (iu < 2 * nch) {
-        const int ch = iu >> 1;
+    if (NS > 1) {                                 // sub-chunks; lanes L, L+LPP, .. share columns
+      if (iu < NS * nch) {
+        const int ch = iu / NS;
         r = P.gu.r_lo + ch / P.gu.nci;
-        x0 = P.gu.xoff + (ch % P.gu.nci) * kUpdChunk + (iu & 1) * (kUpdChunk / 2) +
-             CPL * (lane & 15);
+        x0 = P.gu.xoff + (ch % P.gu.nci) * kUpdChunk + (iu % NS) * (kUpdChunk / NS) +
+             CPL * (lane % LPP);
       } else {
-        act = b1_lane(P.gu, 0, (iu - 2 * nch) * 16 + (lane & 15), r, x0);
+        act = b1_lane(P.gu, 0, (iu - NS * nch) * LPP + (lane % LPP), r, x0);
       }
     } else if (iu < nch) {
       r = P.gu.r_lo + iu / P.gu.nci;
@@ -1060,13 +1070,13 @@ __global__ void __launch_bounds__(kThreads, kUpdateCtasPerSm) k_update(FastParam
       act = b1_lane(P.gu, iu - nch, lane, r, x0);
     }
     if (BATCH) r += tile * P.tile_hr;             // row of the tile in the stacked arrays
-    if (HALF) {
-      // window words of this lane's half: rows r-1, r (rows 0-15) or r, r+1
+    if constexpr (NS > 1) {
+      // window words of this lane's part: rows r-1, r (part 0) or r, r+1
       uint32_t wlo[NT], whi[NT];
       uint32_t a = ~0u, o = 0u;
       if (act) {
         const uint32_t* wp =
-            P.bits_in + (size_t)(r - 1 + (lane >> 4)) * P.g.pitch_w + (x0 - (R + 1));
+            P.bits_in + (size_t)(r - 1 + (lane >= LPP)) * P.g.pitch_w + (x0 - (R + 1));
 #pragma unroll
         for (int j = 0; j < NT; ++j) {
           wlo[j] = __ldg(wp + j);
@@ -1076,7 +1086,7 @@ __global__ void __launch_bounds__(kThreads, kUpdateCtasPerSm) k_update(FastParam
         }
       }
       if (stopped || (P.skip_uniform && __all_sync(0xffffffffu, !act || a == ~0u || o == 0u))) {
-        if (!act || lane >= 16) continue;
+        if (!act || lane >= LPP) continue;
         uint32_t* dst = P.bits_out + (size_t)r * P.g.pitch_w + x0;
 #pragma unroll
         for (int q = 0; q < CPL / 4; ++q)
@@ -1084,7 +1094,7 @@ __global__ void __launch_bounds__(kThreads, kUpdateCtasPerSm) k_update(FastParam
                                                         whi[R + 3 + 4 * q], whi[R + 4 + 4 * q]);
         continue;
       }
-      update_block_half<R, MODEL, CPL, SRC>(P, luts.lt2,
+      update_block_split<R, MODEL, CPL, SRC, NS>(P, luts.lt2,
                                             s_ring + (threadIdx.x >> 5) * kRing2 * 32 * CPL, r,
                                             x0, A, B, eps_u, wlo, whi, tile, act);
       continue;
@@ -1509,13 +1519,13 @@ __device__ __forceinline__ void partition_commit(const FastParams& P, int r, int
   }
 }
 
-// Border rows k0 .. k0 + kBorderRows - 1 of the partition lane block (r, x0):
+// Border rows k0 .. k0 + nrows - 1 of the partition lane block (r, x0):
 // signs of phi^{n+1} with zero padding (partition_block's arithmetic on a row
 // range); pw / mw get bit k for the rows of the range only.
 template <int R>
 __device__ __forceinline__ void partition_rows_border(const FastParams& P, const float* s_lt,
                                                       const float* s_ls, int r, int x0, int k0,
-                                                      float eps_phi, uint32_t (&pw)[8],
+                                                      int nrows, float eps_phi, uint32_t (&pw)[8],
                                                       uint32_t (&mw)[8]) {
   constexpr int NT = kColsPerThread + 2 * R;
   const int H = P.g.H, W = P.g.W;
@@ -1534,7 +1544,7 @@ __device__ __forceinline__ void partition_rows_border(const FastParams& P, const
 #pragma unroll
   for (int c = 0; c < 8; ++c) { pw[c] = 0u; mw[c] = 0u; }
 #pragma unroll 1
-  for (int k = k0; k < k0 + kBorderRows; ++k) {
+  for (int k = k0; k < k0 + nrows; ++k) {
     const int i = y0 + k;
     if (i >= H) break;
     phi_row<R, SRC_SMOOTH, false, NT, 8>(P, win, cm, k - k0, i, s_lt, s_ls, ph);
@@ -1578,21 +1588,21 @@ __device__ __forceinline__ void border_partition_body(const FastParams& P, const
   const int lane = threadIdx.x & 31;
   int r = 0, x0 = 0;
   const bool act = border_lane(P.gp, unit, lane, P.g.W, r, x0);
+  const int items = P.gp.bitems;                 // lane groups per unit = rows per lane
   uint32_t pw[8], mw[8];
 #pragma unroll
   for (int c = 0; c < 8; ++c) { pw[c] = 0u; mw[c] = 0u; }
   if (act)
-    partition_rows_border<R>(P, s_lt, s_ls, r, x0, (lane / kBorderItems) * kBorderRows, eps_phi,
-                             pw, mw);
+    partition_rows_border<R>(P, s_lt, s_ls, r, x0, (lane / items) * items, items, eps_phi, pw,
+                             mw);
+  for (int o = items; o < 32; o <<= 1) {
 #pragma unroll
-  for (int c = 0; c < 8; ++c) {
-#pragma unroll
-    for (int o = kBorderItems; o < 32; o <<= 1) {
+    for (int c = 0; c < 8; ++c) {
       pw[c] |= __shfl_xor_sync(0xffffffffu, pw[c], o);
       mw[c] |= __shfl_xor_sync(0xffffffffu, mw[c], o);
     }
   }
-  if (!act || lane >= kBorderItems) return;
+  if (!act || lane >= items) return;
   partition_commit<PART, CKPT, MASKONLY>(P, r, x0, pw, mw, d);
 }
 

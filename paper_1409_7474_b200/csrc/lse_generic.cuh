@@ -570,94 +570,102 @@ __global__ void k_widen(const float* __restrict__ in, double* __restrict__ out, 
 }
 
 // ---------------------------------------------------- multi-band (VECTOR)
-// Per-band sums of the pixels that changed side (ABS = false: chg bits,
-// split by the new partition bit) or of every pixel (ABS = true: split by P),
-// one double-double partial per (word-row, 1024-column block) and band, in a
-// fixed order.  Partial layout: part[k * nblk + blk], k = band.
-template <bool ABS>
-__global__ void __launch_bounds__(256) k_band_sums(const uint32_t* __restrict__ chg,
-                                                   const uint32_t* __restrict__ pbits,
-                                                   const ExactCtx* c, TilePartial* part,
-                                                   RunGeom g, const Scalars* sc) {
-  pdl_wait();
-  pdl_launch_dependents();
-  if (!ABS && *(volatile const int*)&sc->stop) return;
-  __shared__ TilePartial s_w[kMaxBands][8];
-  const int r = blockIdx.y;
-  const int nblk = gridDim.x * gridDim.y, blk = r * gridDim.x + blockIdx.x;
-  const int K = c->nbands;
+// One iteration's band chain after the fused partition:
+//   k_band_sums  per-band sums of the pixels that changed side, one partial per
+//                (word-row, 1024-column block); the last CTA to finish folds
+//                them (fixed order) into the running sums, the means, the
+//                checkpoint bookkeeping (finalize_bands_cta);
+//   k_band_peak  D of every pixel exactly (fp64), the fp32 data plane of the
+//                fused kernels and max |D| (atomicMax on the ordered bits);
+//                the last CTA derives the coefficients of the next update.
+// Both "last CTA" hand-offs use a per-run arrival counter (cnt[0], cnt[1]),
+// reset by the CTA that consumed it.
+
+// Arrival at the end of a kernel: true in exactly one (the last) CTA, after
+// which every other CTA's global writes are visible to it.
+__device__ __forceinline__ bool last_cta_arrival(unsigned long long* cnt) {
+  __shared__ bool s_last;
+  __threadfence();
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    const unsigned long long total = (unsigned long long)gridDim.x * gridDim.y;
+    s_last = atomicAdd(cnt, 1ull) == total - 1;
+  }
+  __syncthreads();
+  if (!s_last) return false;
+  __threadfence();
+  if (threadIdx.x == 0) *cnt = 0ull;             // ready for the next launch
+  return true;
+}
+
+// Fixed-order CTA reduction of K band partial arrays at once: the order of
+// reduce_slice for every band (each thread a contiguous range, then the xor
+// tree, then warps in index order), with the K bands' loads issued together.
+__device__ void reduce_bands(const TilePartial* bpart, int nblk, int K, TilePartial* out) {
+  __shared__ double g_h[kMaxBands][2][32], g_l[kMaxBands][2][32];
+  __shared__ long long g_n[kMaxBands][2][32];
+  const int T = blockDim.x, tid = threadIdx.x;
   double ah[kMaxBands], al[kMaxBands], bh[kMaxBands], bl[kMaxBands];
-  long long na = 0, nb = 0;
+  long long na[kMaxBands], nb[kMaxBands];
 #pragma unroll
-  for (int k = 0; k < kMaxBands; ++k) ah[k] = al[k] = bh[k] = bl[k] = 0.0;
-  for (int j = 0; j < 4; ++j) {
-    const int x = blockIdx.x * 1024 + j * 256 + threadIdx.x;
-    if (x >= g.W) continue;
-    const size_t o = (size_t)r * g.pitch_w + x;
-    const uint32_t p = pbits[o];
-    uint32_t m = ABS ? 0xffffffffu : chg[o];
-    if (ABS && r * 32 + 32 > g.H) m = (g.H - r * 32) >= 32 ? m : ((1u << (g.H - r * 32)) - 1u);
-    while (m) {
-      const int b = __ffs(m) - 1;
-      m &= m - 1;
-      const int i = r * 32 + b;
-      const bool in = (p >> b) & 1u;
-      for (int k = 0; k < K; ++k) {
-        const double I = band_exact(c, k, i, x);
-        if (in) dd_add(ah[k], al[k], I);
-        else dd_add(bh[k], bl[k], I);
-      }
-      if (in) ++na; else ++nb;
+  for (int k = 0; k < kMaxBands; ++k) { ah[k] = al[k] = bh[k] = bl[k] = 0.0; na[k] = nb[k] = 0; }
+  const int per = (nblk + T - 1) / T;
+  const int lo = tid * per;
+  const int hi = min(lo + per, nblk);
+  for (int t = lo; t < hi; ++t) {
+#pragma unroll
+    for (int k = 0; k < kMaxBands; ++k) {
+      if (k >= K) break;
+      const TilePartial* p = bpart + (size_t)k * nblk + t;
+      const double2 A = __ldcg(reinterpret_cast<const double2*>(&p->a_hi));
+      const double2 B = __ldcg(reinterpret_cast<const double2*>(&p->b_hi));
+      const longlong2 NN = __ldcg(reinterpret_cast<const longlong2*>(&p->n_a));
+      dd_add_dd(ah[k], al[k], A.x, A.y);
+      dd_add_dd(bh[k], bl[k], B.x, B.y);
+      na[k] += NN.x;
+      nb[k] += NN.y;
     }
   }
+#pragma unroll
   for (int o = 16; o > 0; o >>= 1) {
-    for (int k = 0; k < K; ++k) {
-      double h2 = __shfl_xor_sync(0xffffffffu, ah[k], o), l2 = __shfl_xor_sync(0xffffffffu, al[k], o);
-      dd_add_dd(ah[k], al[k], h2, l2);
-      h2 = __shfl_xor_sync(0xffffffffu, bh[k], o);
-      l2 = __shfl_xor_sync(0xffffffffu, bl[k], o);
-      dd_add_dd(bh[k], bl[k], h2, l2);
+#pragma unroll
+    for (int k = 0; k < kMaxBands; ++k) {
+      if (k >= K) break;
+      dd_shfl_add(ah[k], al[k], o);
+      dd_shfl_add(bh[k], bl[k], o);
+      na[k] += __shfl_xor_sync(0xffffffffu, na[k], o);
+      nb[k] += __shfl_xor_sync(0xffffffffu, nb[k], o);
     }
-    na += __shfl_xor_sync(0xffffffffu, na, o);
-    nb += __shfl_xor_sync(0xffffffffu, nb, o);
   }
-  const int warp = threadIdx.x >> 5;
-  if ((threadIdx.x & 31) == 0)
+  const int warp = tid >> 5, lane = tid & 31;
+  if (lane == 0)
     for (int k = 0; k < K; ++k) {
-      s_w[k][warp].a_hi = ah[k]; s_w[k][warp].a_lo = al[k];
-      s_w[k][warp].b_hi = bh[k]; s_w[k][warp].b_lo = bl[k];
-      s_w[k][warp].n_a = na; s_w[k][warp].n_b = nb;
+      g_h[k][0][warp] = ah[k]; g_l[k][0][warp] = al[k]; g_n[k][0][warp] = na[k];
+      g_h[k][1][warp] = bh[k]; g_l[k][1][warp] = bl[k]; g_n[k][1][warp] = nb[k];
     }
   __syncthreads();
-  if (threadIdx.x < K) {
-    const int k = threadIdx.x;
+  if (tid < K) {
+    const int k = tid;
     TilePartial t{};
-    for (int w = 0; w < 8; ++w) {
-      dd_add_dd(t.a_hi, t.a_lo, s_w[k][w].a_hi, s_w[k][w].a_lo);
-      dd_add_dd(t.b_hi, t.b_lo, s_w[k][w].b_hi, s_w[k][w].b_lo);
-      t.n_a += s_w[k][w].n_a;
-      t.n_b += s_w[k][w].n_b;
+    for (int w = 0; w < (T + 31) / 32; ++w) {
+      dd_add_dd(t.a_hi, t.a_lo, g_h[k][0][w], g_l[k][0][w]);
+      dd_add_dd(t.b_hi, t.b_lo, g_h[k][1][w], g_l[k][1][w]);
+      t.n_a += g_n[k][0][w];
+      t.n_b += g_n[k][1][w];
     }
-    part[(size_t)k * nblk + blk] = t;
+    out[k] = t;
   }
+  __syncthreads();
 }
 
 // Reduce the band partials (fixed order) into the running per-band sums and
 // means; checkpoint bookkeeping from the fused partition's partials (mism).
-// One CTA.  absolute: the partials are full sums (initial state).
-__global__ void __launch_bounds__(256) k_finalize_bands(const TilePartial* bpart, int nblk,
-                                                        PartRanges mism_parts, Scalars* sc,
-                                                        int absolute, int ckpt, long long iter) {
-  pdl_wait();
-  pdl_launch_dependents();
-  if (!absolute && *(volatile const int*)&sc->stop) return;
+// Run by one CTA.  absolute: the partials are full sums (initial state).
+__device__ void finalize_bands_cta(const TilePartial* bpart, int nblk, const PartRanges& mism_parts,
+                                   Scalars* sc, bool absolute, bool ckpt, long long iter) {
   __shared__ TilePartial s_band[kMaxBands];
   const int K = sc->nbands;
-  for (int k = 0; k < K; ++k) {
-    PartRanges R1{{bpart + (size_t)k * nblk, bpart, bpart}, {nblk, 0, 0}};
-    reduce_slice(R1, 0, nblk, &s_band[k]);
-    __syncthreads();
-  }
+  reduce_bands(bpart, nblk, K, s_band);
   unsigned long long mm = 0;
   if (ckpt) {
     __shared__ TilePartial s_m;
@@ -686,7 +694,7 @@ __global__ void __launch_bounds__(256) k_finalize_bands(const TilePartial* bpart
       sc->bcp[k] = dd_div(sc->bsp_hi[k], sc->bsp_lo[k], (double)np);
       sc->bcm[k] = dd_div(sc->bsn_hi[k], sc->bsn_lo[k], (double)nn);
     }
-  sc->peak_bits = 0ull;
+  sc->peak_bits = 0ull;                            // k_band_peak's atomicMax target
   if (ckpt) {                                      // engine.py:228-236
     sc->n_ckpt += 1;
     if (sc->n_ckpt >= 2) sc->equal_run = (mm == 0) ? sc->equal_run + 1 : 0;
@@ -699,64 +707,169 @@ __global__ void __launch_bounds__(256) k_finalize_bands(const TilePartial* bpart
   }
 }
 
+// Per-band sums of the pixels that changed side (ABS = false: chg bits,
+// split by the new partition bit) or of every pixel (ABS = true: split by P),
+// one double-double partial per (word-row, 1024-column block) and band, in a
+// fixed order (bit order within a word, words in column order per thread, the
+// xor tree, warps in index order).  Partial layout: part[k * nblk + blk].
+// The changed bits of a word are taken four at a time, so the band loads of
+// four pixels are in flight together; they are accumulated in bit order.
+template <bool ABS>
+__global__ void __launch_bounds__(256) k_band_sums(const uint32_t* __restrict__ chg,
+                                                   const uint32_t* __restrict__ pbits,
+                                                   const ExactCtx* c, TilePartial* part,
+                                                   RunGeom g, Scalars* sc,
+                                                   unsigned long long* cnt, PartRanges mism_parts,
+                                                   int ckpt, long long iter) {
+  pdl_wait();
+  pdl_launch_dependents();
+  if (!ABS && *(volatile const int*)&sc->stop) return;
+  __shared__ TilePartial s_w[kMaxBands][8];
+  const int r = blockIdx.y;
+  const int nblk = gridDim.x * gridDim.y, blk = r * gridDim.x + blockIdx.x;
+  const int K = c->nbands;
+  const float* b32 = c->bands32;
+  const double* b64 = c->bands64;
+  const size_t bstride = (size_t)c->band_stride, dpitch = (size_t)c->data_pitch;
+  double ah[kMaxBands], al[kMaxBands], bh[kMaxBands], bl[kMaxBands];
+  long long na = 0, nb = 0;
+#pragma unroll
+  for (int k = 0; k < kMaxBands; ++k) ah[k] = al[k] = bh[k] = bl[k] = 0.0;
+  for (int j = 0; j < 4; ++j) {
+    const int x = blockIdx.x * 1024 + j * 256 + threadIdx.x;
+    if (x >= g.W) continue;
+    const size_t o = (size_t)r * g.pitch_w + x;
+    const uint32_t p = pbits[o];
+    uint32_t m = ABS ? 0xffffffffu : chg[o];
+    if (ABS && r * 32 + 32 > g.H) m = (g.H - r * 32) >= 32 ? m : ((1u << (g.H - r * 32)) - 1u);
+    while (m) {
+      int bs[4];
+#pragma unroll
+      for (int q = 0; q < 4; ++q) {
+        bs[q] = m ? __ffs(m) - 1 : -1;
+        m &= m - 1;
+      }
+      double I[4][kMaxBands];
+#pragma unroll
+      for (int q = 0; q < 4; ++q)
+#pragma unroll
+        for (int k = 0; k < kMaxBands; ++k) {
+          I[q][k] = 0.0;
+          if (bs[q] >= 0 && k < K) {
+            const size_t e = (size_t)k * bstride + (size_t)(r * 32 + bs[q]) * dpitch + x;
+            I[q][k] = b64 ? b64[e] : (double)b32[e];
+          }
+        }
+#pragma unroll
+      for (int q = 0; q < 4; ++q) {
+        if (bs[q] < 0) break;
+        const bool in = (p >> bs[q]) & 1u;
+#pragma unroll
+        for (int k = 0; k < kMaxBands; ++k) {
+          if (k >= K) break;
+          if (in) dd_add(ah[k], al[k], I[q][k]);
+          else dd_add(bh[k], bl[k], I[q][k]);
+        }
+        if (in) ++na; else ++nb;
+      }
+    }
+  }
+  for (int o = 16; o > 0; o >>= 1) {
+#pragma unroll
+    for (int k = 0; k < kMaxBands; ++k) {
+      if (k >= K) break;
+      dd_shfl_add(ah[k], al[k], o);
+      dd_shfl_add(bh[k], bl[k], o);
+    }
+    na += __shfl_xor_sync(0xffffffffu, na, o);
+    nb += __shfl_xor_sync(0xffffffffu, nb, o);
+  }
+  const int warp = threadIdx.x >> 5;
+  if ((threadIdx.x & 31) == 0)
+    for (int k = 0; k < K; ++k) {
+      s_w[k][warp].a_hi = ah[k]; s_w[k][warp].a_lo = al[k];
+      s_w[k][warp].b_hi = bh[k]; s_w[k][warp].b_lo = bl[k];
+      s_w[k][warp].n_a = na; s_w[k][warp].n_b = nb;
+    }
+  __syncthreads();
+  if (threadIdx.x < K) {
+    const int k = threadIdx.x;
+    TilePartial t{};
+    for (int w = 0; w < 8; ++w) {
+      dd_add_dd(t.a_hi, t.a_lo, s_w[k][w].a_hi, s_w[k][w].a_lo);
+      dd_add_dd(t.b_hi, t.b_lo, s_w[k][w].b_hi, s_w[k][w].b_lo);
+      t.n_a += s_w[k][w].n_a;
+      t.n_b += s_w[k][w].n_b;
+    }
+    part[(size_t)k * nblk + blk] = t;
+  }
+  if (!last_cta_arrival(cnt)) return;
+  finalize_bands_cta(part, nblk, mism_parts, sc, ABS, ckpt != 0, iter);
+}
+
 // The multi-band data term of every pixel for the next update: D exactly in
 // fp64 (vector_D's operations; the band constants hoisted), stored rounded to
-// fp32 as the fused kernels' data plane, and max |D| (np.abs(data).max()):
-// one (1024-column, 1-row) block per CTA, every band load issued before any
-// use, one maximum per CTA into pmax (reduced by k_band_coeffs).
+// fp32 as the fused kernels' data plane, and max |D| (np.abs(data).max()).
+// Each CTA takes one 1024-column block of the rows blockIdx.y, +gridDim.y, ..
+// (every band load of a row issued before any use), then one atomicMax of
+// its maximum on sc->peak_bits (non-negative doubles order like their bits);
+// the last CTA turns the peak into the coefficients of the next update.
 template <int K>
 __global__ void __launch_bounds__(256) k_band_peak(const ExactCtx* __restrict__ c,
-                                                   const Scalars* __restrict__ sc,
+                                                   Scalars* __restrict__ sc,
                                                    float* __restrict__ d32,
-                                                   unsigned long long* __restrict__ pmax,
-                                                   RunGeom g) {
+                                                   unsigned long long* cnt, RunGeom g) {
   pdl_wait();
   pdl_launch_dependents();
   const float* b32 = c->bands32;
   const double* b64 = c->bands64;
   const long long stride = c->band_stride;
-  const int i = blockIdx.y;
   const int x0 = (blockIdx.x * blockDim.x + threadIdx.x) * 4;
-  const size_t o = (size_t)i * g.data_pitch + x0;
   const bool act = x0 < g.W;
-  double I[K][4];
-  if (act) {
-    if (b64) {
+  const bool live = !sc->stop && !sc->zero_vel;
+  double cp[K], cm[K], dc[K];
+#pragma unroll
+  for (int k = 0; k < K; ++k) {
+    cp[k] = sc->bcp[k];
+    cm[k] = sc->bcm[k];
+    dc[k] = dsub(cp[k], cm[k]);
+  }
+  unsigned long long m = 0ull;
+  if (live && act) {
+    for (int i = blockIdx.y; i < g.H; i += gridDim.y) {
+      const size_t o = (size_t)i * g.data_pitch + x0;
+      double I[K][4];
+      if (b64) {
+#pragma unroll
+        for (int k = 0; k < K; ++k)
+#pragma unroll
+          for (int q = 0; q < 4; ++q) I[k][q] = b64[k * stride + o + q];
+      } else {
+        float4 v[K];
+#pragma unroll
+        for (int k = 0; k < K; ++k) v[k] = __ldcs(reinterpret_cast<const float4*>(b32 + k * stride + o));
+#pragma unroll
+        for (int k = 0; k < K; ++k) {
+          I[k][0] = v[k].x; I[k][1] = v[k].y; I[k][2] = v[k].z; I[k][3] = v[k].w;
+        }
+      }
+      double D[4];
 #pragma unroll
       for (int k = 0; k < K; ++k)
 #pragma unroll
-        for (int q = 0; q < 4; ++q) I[k][q] = b64[k * stride + o + q];
-    } else {
-      float4 v[K];
-#pragma unroll
-      for (int k = 0; k < K; ++k) v[k] = __ldcs(reinterpret_cast<const float4*>(b32 + k * stride + o));
-#pragma unroll
-      for (int k = 0; k < K; ++k) {
-        I[k][0] = v[k].x; I[k][1] = v[k].y; I[k][2] = v[k].z; I[k][3] = v[k].w;
-      }
-    }
-  }
-  const bool live = !sc->stop && !sc->zero_vel;
-  unsigned long long m = 0ull;
-  if (act && live) {
-    double D[4];
-#pragma unroll
-    for (int k = 0; k < K; ++k) {
-      const double cp = sc->bcp[k], cm = sc->bcm[k], dc = dsub(cp, cm);
+        for (int q = 0; q < 4; ++q) {
+          const double t = dmul(dc[k], dsub(dsub(dmul(2.0, I[k][q]), cp[k]), cm[k]));
+          D[q] = k == 0 ? t : dadd(D[q], t);
+        }
+      float4 out;
+      out.x = (float)D[0]; out.y = (float)D[1]; out.z = (float)D[2]; out.w = (float)D[3];
+      reinterpret_cast<float4*>(d32 + o)[0] = out;
 #pragma unroll
       for (int q = 0; q < 4; ++q) {
-        const double t = dmul(dc, dsub(dsub(dmul(2.0, I[k][q]), cp), cm));
-        D[q] = k == 0 ? t : dadd(D[q], t);
+        if (x0 + q >= g.W) break;
+        const unsigned long long bb = (unsigned long long)__double_as_longlong(fabs(D[q]));
+        m = bb > m ? bb : m;
       }
-    }
-    float4 out;
-    out.x = (float)D[0]; out.y = (float)D[1]; out.z = (float)D[2]; out.w = (float)D[3];
-    reinterpret_cast<float4*>(d32 + o)[0] = out;
-#pragma unroll
-    for (int q = 0; q < 4; ++q) {
-      if (x0 + q >= g.W) break;
-      const unsigned long long bb = (unsigned long long)__double_as_longlong(fabs(D[q]));
-      m = bb > m ? bb : m;
     }
   }
   for (int o2 = 16; o2 > 0; o2 >>= 1) {
@@ -768,29 +881,13 @@ __global__ void __launch_bounds__(256) k_band_peak(const ExactCtx* __restrict__ 
   __syncthreads();
   if (threadIdx.x == 0) {
     for (int w = 1; w < (int)(blockDim.x >> 5); ++w) m = s_m[w] > m ? s_m[w] : m;
-    pmax[(size_t)blockIdx.y * gridDim.x + blockIdx.x] = m;
+    if (m) atomicMax(&sc->peak_bits, m);
   }
-}
-
-// Coefficients of the next update from the band peak: the fused kernels see
-// the data plane D (fp32) and vf = A * D with A = (dt / 2) / peak.
-__global__ void __launch_bounds__(1024) k_band_coeffs(Scalars* sc,
-                                                      const unsigned long long* pmax, int n) {
-  pdl_wait();
-  pdl_launch_dependents();
-  if (*(volatile const int*)&sc->stop) return;
-  unsigned long long m = 0ull;
-  for (int t = threadIdx.x; t < n; t += blockDim.x) m = pmax[t] > m ? pmax[t] : m;
-  for (int o = 16; o > 0; o >>= 1) {
-    const unsigned long long v = __shfl_xor_sync(0xffffffffu, m, o);
-    m = v > m ? v : m;
-  }
-  __shared__ unsigned long long s_m[32];
-  if ((threadIdx.x & 31) == 0) s_m[threadIdx.x >> 5] = m;
-  __syncthreads();
-  if (threadIdx.x != 0) return;
-  for (int w = 1; w < (int)(blockDim.x >> 5); ++w) m = s_m[w] > m ? s_m[w] : m;
-  if (sc->zero_vel) m = 0ull;
+  if (!last_cta_arrival(cnt)) return;
+  if (threadIdx.x != 0 || *(volatile const int*)&sc->stop) return;
+  // coefficients of the next update: the fused kernels see the data plane D
+  // (fp32) and vf = A * D with A = (dt / 2) / peak
+  m = sc->zero_vel ? 0ull : *(volatile unsigned long long*)&sc->peak_bits;
   sc->peak_bits = m;
   const double peak = __longlong_as_double((long long)m);
   sc->peak = peak;

@@ -21,17 +21,18 @@ namespace lse {
 //  [ba, bb) -- whole width; (B2) per interior row the left strip [0, xoff)
 //  and the right tail beyond the B1 groups.  Border work runs the slower
 //  zero-padding code, so its units are short: a border warp unit holds
-//  kBorderItems 8-column lane groups and each group's 32 rows are split over
-//  kBorderQ lanes (lane = quarter * kBorderItems + item).  A row strip of a
+//  bitems = 32 / bq 8-column lane groups and each group's 32 rows are split
+//  over bq lanes of 32 / bq rows (lane = part * bitems + item); bq = 4 by
+//  default, 8 or 16 for small images whose border units are the critical
+//  path.  A row strip of a
 //  multi-GPU run drops the border rows it does not own (its halo rows,
 //  recomputed by their owner).
-constexpr int kBorderQ = 4;                      // row parts per border lane group
-constexpr int kBorderItems = 32 / kBorderQ;      // lane groups per border warp unit
-constexpr int kBorderRows = 32 / kBorderQ;       // rows per border lane
+constexpr int kBorderQ = 4;                      // default row parts per border lane group
 struct Geo {
+  int bq, bitems;    // border row parts per lane group; lane groups (= rows per lane) per unit
   int r_lo, r_hi, nci, xoff, x1;
   int ta, tb, ba, bb;  // part-A word-rows: [ta, tb) above and [ba, bb) below the interior
-  int na_row;        // part-A warp units per word-row: ceil(ceil(W / 8) / kBorderItems)
+  int na_row;        // part-A warp units per word-row: ceil(ceil(W / 8) / bitems)
   int nb1_row;       // B1 lane groups per interior row
   int nb2_left;      // B2 left-strip groups per interior row (xoff / 8)
   int nb2_row;       // B2 lane groups per interior row (left + right tail)
@@ -42,11 +43,13 @@ struct Geo {
 // Build the geometry of a kernel whose stencil reaches `top` rows up, `bot`
 // rows down and `right` columns right (the left reach must be <= xoff = 8).
 LSE_HD long long geo_fdiv(long long a, long long b) { return a >= 0 ? a / b : -((-a + b - 1) / b); }
-LSE_HD Geo make_geo(int H, int W, int R, int top, int bot, int right) {
+LSE_HD Geo make_geo(int H, int W, int R, int top, int bot, int right, int bq = kBorderQ) {
   const int HR = (H + 31) / 32;
   Geo g{};
+  g.bq = bq;
+  g.bitems = 32 / bq;
   g.xoff = 8;
-  g.na_row = ((W + 7) / 8 + kBorderItems - 1) / kBorderItems;
+  g.na_row = ((W + 7) / 8 + g.bitems - 1) / g.bitems;
   long long rlo = (top + 31) / 32;
   long long rhi = geo_fdiv(H - 32 - bot, 32) + 1;
   if (rhi > HR) rhi = HR;
@@ -107,7 +110,7 @@ LSE_HD int interior_units(const Geo& G) {
   return chunk_units(G) + (G.nB1 + 31) / 32;
 }
 LSE_HD int border_units(const Geo& G) {
-  return G.nA + (G.nB2 + kBorderItems - 1) / kBorderItems;
+  return G.nA + (G.nB2 + G.bitems - 1) / G.bitems;
 }
 // B1 pack: lane -> (row, x0); false for the unused lanes of the last pack
 LSE_HD bool b1_lane(const Geo& G, int pack, int lane, int& r, int& x0) {
@@ -117,20 +120,20 @@ LSE_HD bool b1_lane(const Geo& G, int pack, int lane, int& r, int& x0) {
   x0 = G.x1 + 8 * (g - (r - G.r_lo) * G.nb1_row);
   return true;
 }
-// Border unit -> the lane group (r, x0) of `lane` (its row quarter is
-// lane / kBorderItems); false for the unused lanes of the last unit.
+// Border unit -> the lane group (r, x0) of `lane` (its row part is
+// lane / bitems); false for the unused lanes of the last unit.
 LSE_HD bool border_lane(const Geo& G, int unit, int lane, int W, int& r,
                                             int& x0) {
-  const int item = lane % kBorderItems;
+  const int item = lane % G.bitems;
   if (unit < G.nA) {
     const int rowidx = unit / G.na_row;
     const int c = unit - rowidx * G.na_row;
     const int ntop = G.tb - G.ta;
     r = rowidx < ntop ? G.ta + rowidx : G.ba + (rowidx - ntop);
-    x0 = (c * kBorderItems + item) * 8;
+    x0 = (c * G.bitems + item) * 8;
     return x0 < W;
   }
-  const int g = (unit - G.nA) * kBorderItems + item;
+  const int g = (unit - G.nA) * G.bitems + item;
   if (g >= G.nB2) return false;
   r = G.r_lo + g / G.nb2_row;
   const int j = g - (r - G.r_lo) * G.nb2_row;

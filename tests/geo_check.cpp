@@ -32,7 +32,7 @@ static int check(int H, int W, int R, int top, int bot, int left, int right, con
       cover[(size_t)r * NG + x0 / 8]++;
     }
   for (int u = 0; u < border_units(G); ++u)
-    for (int lane = 0; lane < kBorderItems; ++lane) {   // quarter 0 stands for its group
+    for (int lane = 0; lane < G.bitems; ++lane) {   // row part 0 stands for its group
       int r, x0;
       if (!border_lane(G, u, lane, W, r, x0)) continue;
       if (r < 0 || r >= HR || x0 < 0 || x0 >= W || x0 % 8) { ++bad; continue; }
@@ -53,10 +53,11 @@ int main() {
   const int Ws[] = {2, 7, 8, 9, 255, 256, 257, 264, 270, 512, 530, 1024, 1300, 4096, 32768};
   for (int H : Hs)
     for (int W : Ws)
-      for (int R = 1; R <= 4; ++R) {
-        fails += check(H, W, R, 1 + R, 1 + R, R + 1, R + 1, make_geo(H, W, R, 1 + R, 1 + R, R + 1)) != 0;
-        fails += check(H, W, R, R, R, R, R, make_geo(H, W, R, R, R, R)) != 0;
-        Geo a = geo_all_border(make_geo(H, W, R, 1 + R, 1 + R, R + 1), H);
+      for (int R = 1; R <= 4; ++R)
+      for (int bq = 4; bq <= 16; bq *= 2) {
+        fails += check(H, W, R, 1 + R, 1 + R, R + 1, R + 1, make_geo(H, W, R, 1 + R, 1 + R, R + 1, bq)) != 0;
+        fails += check(H, W, R, R, R, R, R, make_geo(H, W, R, R, R, R, bq)) != 0;
+        Geo a = geo_all_border(make_geo(H, W, R, 1 + R, 1 + R, R + 1, bq), H);
         fails += check(H, W, R, 1 << 20, 1 << 20, 1 << 20, 1 << 20, a) != 0;
         cases += 3;
         // row strips: halo word-rows (first / last) are left to their owners
@@ -64,10 +65,10 @@ int main() {
         for (int lo = 0; lo <= 1; ++lo)
           for (int hi = HR - 1; hi <= HR; ++hi) {
             if (hi <= lo) continue;
-            Geo s = make_geo(H, W, R, 1 + R, 1 + R, R + 1);
+            Geo s = make_geo(H, W, R, 1 + R, 1 + R, R + 1, bq);
             if (!geo_restrict_rows(s, lo, hi)) continue;
             fails += check(H, W, R, 1 + R, 1 + R, R + 1, R + 1, s, lo, hi) != 0;
-            Geo q = make_geo(H, W, R, R, R, R);
+            Geo q = make_geo(H, W, R, R, R, R, bq);
             if (!geo_restrict_rows(q, lo, hi)) continue;
             fails += check(H, W, R, R, R, R, R, q, lo, hi) != 0;
             cases += 2;

@@ -41,3 +41,29 @@ def test_random_geometry_matches_oracle(h, w, model, ts):
     op = O.OracleParams(model=model, ts_reg=ts, max_iters=iters, conv_check_every=iters + 1)
     ref = O.run_fixed(img, phi0, op, iters)
     assert np.array_equal(r.state.phi, ref.phi), np.abs(r.state.phi - ref.phi).max()
+
+
+# Every forced work decomposition (split-warp row parts x border row parts,
+# lse_api.cu reads LSE_SPLIT_PARTS / LSE_BORDER_Q when a run is created) gives
+# the oracle's trajectory bit for bit.
+@pytest.mark.parametrize("h,w", [(96, 300), (200, 520), (257, 263), (300, 1100)])
+@pytest.mark.parametrize("split,bq", [(1, 4), (2, 8), (4, 4), (4, 16), (1, 16)])
+@pytest.mark.parametrize("model", ["region", "edge"])
+def test_forced_decomposition_matches_oracle(h, w, split, bq, model, monkeypatch):
+    monkeypatch.setenv("LSE_SPLIT_PARTS", str(split))
+    monkeypatch.setenv("LSE_BORDER_Q", str(bq))
+    rng = np.random.default_rng(h * 7 + w + split * 100 + bq)
+    img = np.clip(0.3 + 0.4 * (rng.random((h, w)) > 0.6) + 0.05 * rng.standard_normal((h, w)),
+                  0, 1)
+    poly = np.array([[w * 0.1, h * 0.15], [w * 0.85, h * 0.1], [w * 0.9, h * 0.8],
+                     [w * 0.2, h * 0.9]])
+    sign = -1 if model == "edge" else 1
+    phi0 = O.rasterize_seeds([poly], sign, w, h)
+    iters = 15
+    p = L.default_params(L.ModelKind.from_name(model), max_iters=iters,
+                         conv_check_every=iters + 1)
+    r = L.EvolutionRun(img, L.SeedSpec(polygons=(poly,), inside_sign=sign), p)
+    r.advance(iters)
+    op = O.OracleParams(model=model, max_iters=iters, conv_check_every=iters + 1)
+    ref = O.run_fixed(img, phi0, op, iters)
+    assert np.array_equal(r.state.phi, ref.phi), np.abs(r.state.phi - ref.phi).max()
