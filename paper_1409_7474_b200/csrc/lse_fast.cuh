@@ -469,8 +469,11 @@ __device__ __forceinline__ float2 fsub2(float2 a, float2 b) {
 // entry i of the 2R+2-bit window is (t(i & low 2R+1 bits), t(i >> 1)) -- the
 // same fp32 values as two t-LUT lookups.  win8 holds the window words
 // pre-shifted by 3 (byte offsets of 8-byte entries).  The table is a
-// file-scope __shared__ array, so its address is a link-time constant that
-// folds into the LDS immediate (offset register + constant, no add).
+// file-scope __shared__ array: the partition addresses it as [offset + UR]
+// (no add); in the update ptxas keeps the base in a per-thread register and
+// spends one IADD per lookup.  (An OR-with-aligned-base variant removed that
+// add but measured no faster, and static __shared__ alignment is relative to
+// the user window, so it was dropped.)
 __shared__ __align__(16) float2 g_pair_lut[1 << (2 * 4 + 2)];      // R <= 4
 
 template <int R, int NT, int NOUT, int SRC = SRC_SMOOTH>

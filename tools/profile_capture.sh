@@ -15,4 +15,12 @@ for k in k_update k_partition; do
       -o gpurun_out/${tag}_$k python bench.py --steps 1 --warmup 1 --iters 20 --no-e2e \
       --no-cpu-baseline --skip-steps 0 --c4-tiles 0 > /dev/null 2>&1
 done
+# export on the box (reports with source are too big to travel back whole)
+for k in k_update k_partition; do
+  ncu -i gpurun_out/${tag}_$k.ncu-rep --page raw --csv > gpurun_out/${tag}_${k}_raw.csv
+  ncu -i gpurun_out/${tag}_$k.ncu-rep --page details > gpurun_out/${tag}_${k}_details.txt
+  ncu -i gpurun_out/${tag}_$k.ncu-rep --page source --csv --print-source sass \
+      > gpurun_out/${tag}_${k}_sass.csv 2>/dev/null
+  rm -f gpurun_out/${tag}_$k.ncu-rep
+done
 ls -la gpurun_out/${tag}_*

@@ -35,8 +35,12 @@ METRICS = ["gpu__time_duration.sum", "dram__bytes_read.sum", "dram__bytes_write.
            "l1tex__t_bytes_pipe_lsu_mem_local_op_st.sum"]
 kern = {}
 for k in ("k_update", "k_partition"):
-    out = subprocess.run(["ncu", "-i", f"{src}/{tag}_{k}.ncu-rep", "--page", "raw", "--csv"],
-                         capture_output=True, text=True).stdout
+    # exported on the GPU box (profile_capture.sh) when the report is too big
+    # to travel; else read from the .ncu-rep here
+    raw = f"{src}/{tag}_{k}_raw.csv"
+    out = open(raw).read() if os.path.exists(raw) else subprocess.run(
+        ["ncu", "-i", f"{src}/{tag}_{k}.ncu-rep", "--page", "raw", "--csv"],
+        capture_output=True, text=True).stdout
     rr = list(csv.reader(out.splitlines()))
     h, u, v = rr[0], rr[1], rr[2]
     d = {}
@@ -45,8 +49,10 @@ for k in ("k_update", "k_partition"):
             i = h.index(m)
             d[m] = (v[i], u[i])
     kern[k] = d
-    det = subprocess.run(["ncu", "-i", f"{src}/{tag}_{k}.ncu-rep", "--page", "details"],
-                         capture_output=True, text=True).stdout
+    dpath = f"{src}/{tag}_{k}_details.txt"
+    det = open(dpath).read() if os.path.exists(dpath) else subprocess.run(
+        ["ncu", "-i", f"{src}/{tag}_{k}.ncu-rep", "--page", "details"],
+        capture_output=True, text=True).stdout
     with open(f"{dst}/{tag}_ncu_{k}_details.txt", "w") as f:
         f.write(det)
 

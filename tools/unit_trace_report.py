@@ -21,7 +21,8 @@ for line in open(sys.argv[1]):
     b, i = dur[:nb][ok[:nb]], dur[nb:][ok[nb:]]
     print(f"{name}: units {n} (border {nb}) span {span/1e3:.1f} us | "
           f"border mean {b.mean()/1e3 if b.size else 0:.1f} max {b.max()/1e3 if b.size else 0:.1f} us | "
-          f"interior mean {i.mean()/1e3:.1f} p99 {np.percentile(i, 99)/1e3:.1f} max {i.max()/1e3:.1f} us | "
+          f"interior mean {i.mean()/1e3 if i.size else 0:.1f} p99 {np.percentile(i, 99)/1e3 if i.size else 0:.1f} "
+          f"max {i.max()/1e3 if i.size else 0:.1f} us | "
           f"last start {a[ok,0].max()/1e3:.1f} us")
     if e:
         print(f"   warps exit by {int(e[2])/1e3:.1f} us; stamps before {int(e[4])/1e3:.1f} "
