@@ -1387,20 +1387,19 @@ __device__ __forceinline__ void partition_block(const FastParams& P, const float
   uint32_t fbrows = 0u;
 #pragma unroll
   for (int c = 0; c < 8; ++c) { pw[c] = 0u; mw[c] = 0u; }
+  if (INT) {
+    // row pairs (k, k+1), k = 2 kk
 #pragma unroll 1
-  for (int k = 0; k < 32; ++k) {
-    if (k == 16) {                                          // base row y0+16-R
+    for (int kk = 0; kk < 16; ++kk) {
+      const int k = 2 * kk;
+      if (kk == 8) {                                        // base row y0+16-R
 #pragma unroll
-      for (int j = 0; j < NT; ++j) {
-        const int xc = x0 - R + j;
-        win[j] = __funnelshift_r(word_at<INT>(P, r, xc), word_at<INT>(P, r + 1, xc), 16 - R);
-        if (INT) win[j] <<= 3;
+        for (int j = 0; j < NT; ++j) {
+          const int xc = x0 - R + j;
+          win[j] = __funnelshift_r(word_at<INT>(P, r, xc), word_at<INT>(P, r + 1, xc), 16 - R)
+                   << 3;
+        }
       }
-    }
-    const int i = y0 + k;
-    if (!INT && i >= H) break;
-    if (INT) {
-      if (k & 1) continue;                                  // rows k, k+1 done as a pair
       float2 ph2[8];
       phi_rows2_int<R, NT, 8>(P, win, k < 16 ? k : k - 16, lut_base, ph2);
       float pmin0 = 3.0e38f, pmin1 = 3.0e38f;
@@ -1413,7 +1412,19 @@ __device__ __forceinline__ void partition_block(const FastParams& P, const float
       }
       if (pmin0 <= eps_phi) fbrows |= 1u << k;
       if (pmin1 <= eps_phi) fbrows |= 2u << k;
-    } else {
+    }
+  } else {
+#pragma unroll 1
+    for (int k = 0; k < 32; ++k) {
+      if (k == 16) {                                        // base row y0+16-R
+#pragma unroll
+        for (int j = 0; j < NT; ++j) {
+          const int xc = x0 - R + j;
+          win[j] = __funnelshift_r(word_at<INT>(P, r, xc), word_at<INT>(P, r + 1, xc), 16 - R);
+        }
+      }
+      const int i = y0 + k;
+      if (i >= H) break;
       phi_row<R, SRC_SMOOTH, INT, NT, 8>(P, win, cm, k < 16 ? k : k - 16, i, s_lt, s_ls, ph);
       const uint32_t bitk = 1u << k;
       bool tie = false;
