@@ -24,6 +24,7 @@
 #include "lse_device.cuh"
 #include "lse_fast.cuh"
 #include "lse_generic.cuh"
+#include "lse_fine.cuh"
 #include "lse_contours.cuh"
 
 using namespace lse;
@@ -230,6 +231,7 @@ struct lse_run {
   // others are halo copies of the neighbours' rows; the partition phase
   // reduces to one partial at strip_out and the ranks finalize together
   bool strip = false;
+  bool fine = false;           // small image: per-pixel kernels (lse_fine.cuh)
   int own_lo = 0, own_hi = 0;
   TilePartial* strip_out = nullptr;
   bool strip_part = false, strip_ckpt = false;   // phases owed by the last update
@@ -488,6 +490,11 @@ void trace_flush() {
 
 template <int R, int MODEL, int SRC>
 int launch_update(lse_run* r, FastParams P) {
+  if (r->fine) {
+    const dim3 g((r->W + kFineCols - 1) / kFineCols, r->g.HR);
+    TRY(launch_pdl(k_update_fine<R, MODEL, SRC>, g, 32 * kFineCols, r->st, P));
+    return LSE_OK;
+  }
   const int ns = r->split_parts;
   const long long n = r->nb_upd[0] + (ns > 1 ? r->ni_upd_split : r->ni_upd);
   const int g = fast_grid(n, kUpdateCtasPerSm);
@@ -506,7 +513,12 @@ int launch_update(lse_run* r, FastParams P) {
 
 template <int R, bool PART, bool CKPT, bool MASKONLY>
 int launch_partition(lse_run* r, FastParams P) {
-  const long long n = r->nb_part + r->ni_part;
+  const bool fine = r->fine && !MASKONLY;
+  const long long n = fine ? (long long)r->g.HR * r->W : r->nb_part + r->ni_part;
+  if (fine) {
+    const dim3 gf((r->W + kFineCols - 1) / kFineCols, r->g.HR);
+    TRY(launch_pdl(k_partition_fine<R, PART, CKPT>, gf, 32 * kFineCols, r->st, P));
+  } else {
   const int g = fast_grid(n, kPartitionCtasPerSm);
   P.work_base = take_work(r, n, g);
 #ifdef LSE_UNIT_TRACE
@@ -516,6 +528,7 @@ int launch_partition(lse_run* r, FastParams P) {
 #ifdef LSE_UNIT_TRACE
   trace_after(r, P.trace);
 #endif
+  }
   if (!MASKONLY) {
     // two-stage fixed-order reduction of all unit partials -> the next
     // update's coefficients (64 CTAs reduce contiguous slices, 1 CTA the rest)
@@ -806,7 +819,7 @@ int generic_iteration(lse_run* r, long long it, bool reinit_now, bool reg_now, b
 // pixel (fp32 plane for the fused kernels) and its peak, the coefficients
 int band_chain(lse_run* r, bool absolute, bool ckpt, long long it) {
   const dim3 gr((r->g.pitch_w + 1023) / 1024, r->g.HR);
-  const int n = (int)(r->nb_part + r->ni_part);
+  const int n = (int)(r->fine ? (long long)r->g.HR * r->W : r->nb_part + r->ni_part);
   PartRanges M{{r->d_part, r->d_part, r->d_part}, {ckpt ? n : 0, 0, 0}};
   unsigned long long* cnt = r->d_pmax;          // [0]: band sums, [1]: band peak arrivals
   if (absolute)
@@ -1239,7 +1252,16 @@ int create_impl(lse_run** out, const lse_params* p, long long height, long long 
     r->ni_part = hi_rows * r->nseg + (r->gp.nB1 + 31) / 32;
     r->nb_part = border_units(r->gp);
   }
-  const long long nparts = std::max<long long>(r->g.ntiles, r->ni_part + r->nb_part);
+  // small single images run the per-pixel kernels: an iteration is then
+  // bound by one pixel's latency instead of one lane block's
+  {
+    long long fine_max = 360000;                  // ~600^2: measured crossover
+    if (const char* fv = std::getenv("LSE_FINE_MAX_PX")) fine_max = std::atoll(fv);
+    r->fine = !r->strip && r->R >= 1 && r->R <= 4 && r->npx <= fine_max;
+  }
+  const long long nparts = std::max<long long>(
+      std::max<long long>(r->g.ntiles, r->ni_part + r->nb_part),
+      r->fine ? (long long)r->g.HR * r->W : 0LL);
   auto cleanup = [&](int rc) {
     lse_run_destroy(r);
     return rc;

@@ -1,0 +1,256 @@
+// lse_fine.cuh -- per-pixel update / partition kernels for small images.
+//
+// The tiled kernels (lse_fast.cuh) give each lane a block of 8 columns x
+// 32 (or 32/NS) rows; on a small image there are only a few such blocks per
+// SM, so an iteration costs the serial latency of one block rather than its
+// throughput.  Here every thread owns one pixel: a warp is one state word
+// (lane k = row 32r + k of column x), a CTA eight adjacent columns of one
+// word-row.  The state word of the next iteration is one __ballot_sync.
+//
+// The arithmetic is the tiled kernels' arithmetic pixel by pixel: the same
+// vertical LUT values (exact-rounded t for windows inside the image, the
+// zero-padding weight-sum form otherwise), the same left-to-right horizontal
+// FMA order, the same gradient / velocity / u expressions and the same
+// near-tie guards, so the fp32 values, and with them every decision (fp32
+// outside the guard band, the fp64 restatement inside it), are the same.
+// The only difference is the partial granularity of the partition sums (one
+// per state word), i.e. the grouping of the c+/c- sums.
+#pragma once
+
+namespace lse {
+
+constexpr int kFineCols = 8;                     // columns (warps) per CTA
+
+// phi at window row offset m (window bit 0 = first window row) for window
+// columns j0 .. j0 + 2R: sum_d w_|d| t(j0 + R + d), d = -R..R, left to right.
+template <int R, int NC, bool INT>
+__device__ __forceinline__ float fine_phi(const FastParams& P, const uint32_t (&win)[NC],
+                                          const uint32_t (&cm)[NC], int j0, int m, uint32_t vr,
+                                          float Lv, const float* s_lt, const float* s_ls) {
+  constexpr uint32_t PM = (1u << (2 * R + 1)) - 1u;
+  float out = 0.f;
+#pragma unroll
+  for (int d = -R; d <= R; ++d) {
+    const int j = j0 + R + d;
+    const uint32_t p = (win[j] >> m) & PM;
+    const float t = INT ? s_lt[p] : fmaf(2.f, s_ls[p & vr & cm[j]], cm[j] ? -Lv : 0.f);
+    const float wd = P.w32[d < 0 ? -d : d];
+    out = (d == -R) ? wd * t : fmaf(wd, t, out);
+  }
+  return out;
+}
+
+template <int R>
+__device__ __forceinline__ void fine_load_luts(const FastParams& P, float* s_lt, float* s_ls) {
+  constexpr int NPAT = 1 << (2 * R + 1);
+  for (int q = threadIdx.x; q < NPAT; q += blockDim.x) {
+    s_lt[q] = __ldg(&P.lut_t[q]);
+    s_ls[q] = __ldg(&P.lut_s[q]);
+  }
+}
+
+// t values (vertical pass) of window row offset m for window columns j,
+// exact-rounded LUT inside the image, zero padding via the weight-sum form
+template <int R, int NC>
+__device__ __forceinline__ void fine_trow(const uint32_t (&win)[NC], const uint32_t (&cm)[NC],
+                                          int m, bool in, uint32_t vr, float Lv,
+                                          const float* s_lt, const float* s_ls, float (&t)[NC]) {
+  constexpr uint32_t PM = (1u << (2 * R + 1)) - 1u;
+#pragma unroll
+  for (int j = 0; j < NC; ++j) {
+    const uint32_t p = (win[j] >> m) & PM;
+    t[j] = in ? s_lt[p] : fmaf(2.f, s_ls[p & vr & cm[j]], cm[j] ? -Lv : 0.f);
+  }
+}
+// horizontal pass centred on window column j0 + R, left to right
+template <int R, int NC>
+__device__ __forceinline__ float fine_hsum(const FastParams& P, const float (&t)[NC], int j0) {
+  float out = 0.f;
+#pragma unroll
+  for (int d = -R; d <= R; ++d) {
+    const float wd = P.w32[d < 0 ? -d : d];
+    out = (d == -R) ? wd * t[j0 + R + d] : fmaf(wd, t[j0 + R + d], out);
+  }
+  return out;
+}
+
+// b^n -> b^{n+1} (engine.py:155-169 for one pixel per thread).  Grid:
+// (ceil(W / kFineCols), HR), block kFineCols warps.  Each lane computes phi
+// of its own row at columns x-1, x, x+1; phi at rows i-1 / i+1 comes from the
+// neighbouring lanes (lanes 0 and 31 compute their outside neighbour).
+template <int R, int MODEL, int SRC>
+__global__ void __launch_bounds__(32 * kFineCols, 4) k_update_fine(FastParams P) {
+  constexpr int NPAT = 1 << (2 * R + 1);
+  constexpr int NC = 2 * R + 3;                  // window columns x-R-1 .. x+R+1
+  __shared__ float s_lt[NPAT];
+  __shared__ float s_ls[NPAT];
+  fine_load_luts<R>(P, s_lt, s_ls);
+  __syncthreads();
+  pdl_wait();
+  pdl_launch_dependents();
+  Scalars* sc = P.scal;
+  if (*(volatile const int*)&sc->stop) return;
+  if (MODEL == REGION && blockIdx.x == 0 && blockIdx.y == 0 && threadIdx.x == 0 &&
+      sc->zero_vel && sc->model != EDGE)
+    sc->degenerate = 1;                          // sticky degenerate (engine.py:239-240)
+  const float A = sc->A, B = sc->B, eps_u = sc->eps_u;
+  const int lane = threadIdx.x & 31;
+  const int x = blockIdx.x * kFineCols + (threadIdx.x >> 5);
+  const int r = blockIdx.y;
+  const int H = P.g.H, W = P.g.W;
+  if (x >= W) return;                            // whole warps
+  const int i = r * 32 + lane;
+  // window of each column: 32 rows from i-R-1, from word-rows (r-1, r) for
+  // the first R+1 lanes and (r, r+1) for the others
+  const int up = lane > R ? 1 : 0;
+  const int sh = up ? lane - R - 1 : lane + 31 - R;
+  uint32_t win[NC], cm[NC];
+#pragma unroll
+  for (int j = 0; j < NC; ++j) {
+    const int xc = x - (R + 1) + j;
+    cm[j] = (xc >= 0 && xc < W) ? 0xffffffffu : 0u;
+    win[j] = __funnelshift_r(word_at<false>(P, r - 1 + up, xc), word_at<false>(P, r + up, xc), sh);
+  }
+  const bool cols_in = x - R - 1 >= 0 && x + R + 1 <= W - 1;
+  auto row_in = [&](int row) { return cols_in && row - R >= 0 && row + R <= H - 1; };
+  float pm, p0, pn, pl, pr;                      // phi at (i-1,x) (i,x) (i+1,x) (i,x-1) (i,x+1)
+  if (SRC == SRC_SCALED) {                       // phi = +-s (binary initial state)
+    auto ps = [&](int j, int m) { return ((win[j] >> (m + R)) & 1u) ? P.scale32 : -P.scale32; };
+    pm = ps(R + 1, 0);
+    p0 = ps(R + 1, 1);
+    pn = ps(R + 1, 2);
+    pl = ps(R, 1);
+    pr = ps(R + 2, 1);
+  } else {
+    float t[NC];
+    {
+      const bool in = row_in(i);
+      const uint32_t v0 = in ? 0u : row_valid_mask<R>(i, H);
+      fine_trow<R, NC>(win, cm, 1, in, v0, in ? 0.f : s_ls[v0], s_lt, s_ls, t);
+      pl = fine_hsum<R, NC>(P, t, 0);
+      p0 = fine_hsum<R, NC>(P, t, 1);
+      pr = fine_hsum<R, NC>(P, t, 2);
+    }
+    pm = __shfl_up_sync(0xffffffffu, p0, 1);
+    pn = __shfl_down_sync(0xffffffffu, p0, 1);
+    if (lane == 0 || lane == 31) {               // the row outside this warp
+      const int m = lane == 0 ? 0 : 2, row = i - 1 + m;
+      const bool in = row_in(row);
+      const uint32_t v = in ? 0u : row_valid_mask<R>(row, H);
+      fine_trow<R, NC>(win, cm, m, in, v, in ? 0.f : s_ls[v], s_lt, s_ls, t);
+      const float pe = fine_hsum<R, NC>(P, t, 1);
+      if (lane == 0) pm = pe;
+      else pn = pe;
+    }
+  }
+  bool bit = false;
+  if (i < H) {
+    // np.gradient: central differences, one-sided at the image border
+    const float dx = (x == 0) ? 2.f * (pr - p0) : (x == W - 1) ? 2.f * (p0 - pl) : (pr - pl);
+    const float dy = (i == 0) ? 2.f * (pn - p0) : (i == H - 1) ? 2.f * (p0 - pm) : (pn - pm);
+    const float h = sqrt_approx(fmaf(dx, dx, dy * dy));     // 2 |grad phi|
+    const float d = __ldg(P.data32 + (size_t)i * P.g.data_pitch + x);
+    const float vf = (MODEL == REGION) ? fmaf(A, d, B) : d; // A, B / the g plane carry dt/2
+    const float u = fmaf(vf, h, p0);
+    bit = u > 0.f;
+    if (fabsf(u) <= eps_u)                       // near tie: the reference's fp64 decision
+      bit = exact_u_fast<R, SRC>(P.ctx, P.bits_in, i, x) > 0.0;
+  }
+  const uint32_t word = __ballot_sync(0xffffffffu, bit);
+  if (lane == 0) P.bits_out[(size_t)r * P.g.pitch_w + x] = word;
+}
+
+// Partition / checkpoint pass over b^{n+1} (engine.py:168-169, grid.py:102-118,
+// engine.py:228-236): P = {phi >= 0} and M = {phi > 0} words, the sums over
+// the pixels that changed side (one partial per state word, index r * W + x),
+// multi-band runs record the changed bits instead.
+// (The two-stage finalize of the tiled path follows; folding it into the
+// last CTA of this kernel measured slower: one CTA then reduces every word's
+// partial.)
+template <int R, bool PART, bool CKPT>
+__global__ void __launch_bounds__(32 * kFineCols) k_partition_fine(FastParams P) {
+  constexpr int NPAT = 1 << (2 * R + 1);
+  constexpr int NC = 2 * R + 1;                  // window columns x-R .. x+R
+  __shared__ float s_lt[NPAT];
+  __shared__ float s_ls[NPAT];
+  fine_load_luts<R>(P, s_lt, s_ls);
+  __syncthreads();
+  pdl_wait();
+  pdl_launch_dependents();
+  Scalars* sc = P.scal;
+  if (*(volatile const int*)&sc->stop) return;
+  const float eps_phi = sc->eps_phi;
+  const int lane = threadIdx.x & 31;
+  const int x = blockIdx.x * kFineCols + (threadIdx.x >> 5);
+  const int r = blockIdx.y;
+  const int H = P.g.H, W = P.g.W;
+  if (x >= W) return;                            // whole warps
+  const int i = r * 32 + lane;
+  // window of each column: 32 rows from i-R (word-rows (r-1, r) for the
+  // first R lanes, (r, r+1) for the others)
+  const int up = lane >= R ? 1 : 0;
+  const int sh = up ? lane - R : lane + 32 - R;
+  uint32_t win[NC], cm[NC];
+#pragma unroll
+  for (int j = 0; j < NC; ++j) {
+    const int xc = x - R + j;
+    cm[j] = (xc >= 0 && xc < W) ? 0xffffffffu : 0u;
+    win[j] = __funnelshift_r(word_at<false>(P, r - 1 + up, xc), word_at<false>(P, r + up, xc), sh);
+  }
+  const bool act = i < H;
+  const bool in = i - R >= 0 && i + R <= H - 1 && x - R >= 0 && x + R <= W - 1;
+  float ph;
+  if (in) {
+    ph = fine_phi<R, NC, true>(P, win, cm, 0, 0, 0u, 0.f, s_lt, s_ls);
+  } else {
+    const uint32_t v0 = row_valid_mask<R>(i, H);
+    ph = fine_phi<R, NC, false>(P, win, cm, 0, 0, v0, s_ls[v0], s_lt, s_ls);
+  }
+  bool pb = act && ph > 0.f, mb = pb;
+  if (act && fabsf(ph) <= eps_phi) {             // near tie: exact fp64 sign
+    const double e = exact_phi_fast<R>(P.ctx, P.bits_in, i, x);
+    pb = e >= 0.0;
+    mb = e > 0.0;
+  }
+  const uint32_t pw = __ballot_sync(0xffffffffu, pb);
+  const uint32_t mw = __ballot_sync(0xffffffffu, mb);
+  const size_t o = (size_t)r * P.g.pitch_w + x;
+  double a_in = 0.0, a_out = 0.0;
+  long long n_in = 0, n_out = 0;
+  unsigned long long mism = 0ull;
+  if (PART) {
+    const uint32_t chg = P.pbits[o] ^ pw;
+    if (P.chg) {
+      if (lane == 0) P.chg[o] = chg;
+    } else if ((chg >> lane) & 1u) {
+      const double I = data_exact(P.ctx, i, x);
+      if (pb) { a_in = I; n_in = 1; }
+      else { a_out = I; n_out = 1; }
+    }
+    if (chg && lane == 0) P.pbits[o] = pw;
+  }
+  if (CKPT) {
+    if (lane == 0) {
+      mism = __popc(P.mbits[o] ^ mw);
+      P.mbits[o] = mw;
+    }
+  }
+#pragma unroll
+  for (int s = 16; s > 0; s >>= 1) {
+    a_in += __shfl_xor_sync(0xffffffffu, a_in, s);
+    a_out += __shfl_xor_sync(0xffffffffu, a_out, s);
+    n_in += __shfl_xor_sync(0xffffffffu, n_in, s);
+    n_out += __shfl_xor_sync(0xffffffffu, n_out, s);
+  }
+  if (lane == 0) {
+    TilePartial t{};
+    t.a_hi = a_in;
+    t.b_hi = a_out;
+    t.n_a = n_in;
+    t.n_b = n_out;
+    t.mism = mism;
+    P.part[(size_t)r * W + x] = t;
+  }
+}
+
+}  // namespace lse

@@ -43,16 +43,22 @@ def test_random_geometry_matches_oracle(h, w, model, ts):
     assert np.array_equal(r.state.phi, ref.phi), np.abs(r.state.phi - ref.phi).max()
 
 
-# Every forced work decomposition (split-warp row parts x border row parts,
-# lse_api.cu reads LSE_SPLIT_PARTS / LSE_BORDER_Q when a run is created) gives
-# the oracle's trajectory bit for bit.
+# Every forced work decomposition (the tiled kernels' split-warp row parts x
+# border row parts, or the per-pixel kernels; lse_api.cu reads LSE_FINE_MAX_PX,
+# LSE_SPLIT_PARTS and LSE_BORDER_Q when a run is created) gives the oracle's
+# trajectory bit for bit.
 @pytest.mark.parametrize("h,w", [(96, 300), (200, 520), (257, 263), (300, 1100)])
-@pytest.mark.parametrize("split,bq", [(1, 4), (2, 8), (4, 4), (4, 16), (1, 16)])
+@pytest.mark.parametrize("split,bq", [(1, 4), (2, 8), (4, 4), (4, 16), (1, 16), ("fine", 0)])
 @pytest.mark.parametrize("model", ["region", "edge"])
 def test_forced_decomposition_matches_oracle(h, w, split, bq, model, monkeypatch):
+    if split == "fine":
+        monkeypatch.setenv("LSE_FINE_MAX_PX", str(1 << 30))
+        split, bq = 1, 4
+    else:
+        monkeypatch.setenv("LSE_FINE_MAX_PX", "0")
     monkeypatch.setenv("LSE_SPLIT_PARTS", str(split))
     monkeypatch.setenv("LSE_BORDER_Q", str(bq))
-    rng = np.random.default_rng(h * 7 + w + split * 100 + bq)
+    rng = np.random.default_rng(h * 7 + w + bq)
     img = np.clip(0.3 + 0.4 * (rng.random((h, w)) > 0.6) + 0.05 * rng.standard_normal((h, w)),
                   0, 1)
     poly = np.array([[w * 0.1, h * 0.15], [w * 0.85, h * 0.1], [w * 0.9, h * 0.8],
@@ -67,3 +73,12 @@ def test_forced_decomposition_matches_oracle(h, w, split, bq, model, monkeypatch
     op = O.OracleParams(model=model, max_iters=iters, conv_check_every=iters + 1)
     ref = O.run_fixed(img, phi0, op, iters)
     assert np.array_equal(r.state.phi, ref.phi), np.abs(r.state.phi - ref.phi).max()
+
+
+# The random-geometry sweep above runs the per-pixel kernels (small images);
+# the same sweep through the tiled kernels.
+@pytest.mark.parametrize("h,w", CASES)
+@pytest.mark.parametrize("model,ts", [("region", 9), ("edge", 9), ("zhang", 7)])
+def test_random_geometry_tiled_matches_oracle(h, w, model, ts, monkeypatch):
+    monkeypatch.setenv("LSE_FINE_MAX_PX", "0")
+    test_random_geometry_matches_oracle(h, w, model, ts)

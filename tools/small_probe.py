@@ -22,7 +22,9 @@ for cfg in a.configs:
         mk = lambda: BandEvolutionRun(sc.image, sc.extra["signs"],  # noqa: E731
                                       L.default_params(L.ModelKind.REGION, **sc.params))
     else:
-        sc = scenes.config1() if cfg == "C1" else scenes.config2()
+        # C1, C2, or X<size>: a C5-density crop of that side, 200 iterations
+        sc = (scenes.config1() if cfg == "C1" else scenes.config2() if cfg == "C2"
+              else scenes.config5_crop(int(cfg[1:]), 200))
         kind = L.ModelKind.from_name(sc.model)
         mk = lambda: L.EvolutionRun(sc.image, L.SeedSpec(polygons=sc.polygons, inside_sign=sc.inside_sign),  # noqa: E731
                                     L.default_params(kind, **sc.params))
