@@ -1255,7 +1255,7 @@ int create_impl(lse_run** out, const lse_params* p, long long height, long long 
   // small single images run the per-pixel kernels: an iteration is then
   // bound by one pixel's latency instead of one lane block's
   {
-    long long fine_max = 360000;                  // ~600^2: measured crossover
+    long long fine_max = 450000;                  // ~670^2: measured crossover
     if (const char* fv = std::getenv("LSE_FINE_MAX_PX")) fine_max = std::atoll(fv);
     r->fine = !r->strip && r->R >= 1 && r->R <= 4 && r->npx <= fine_max;
   }

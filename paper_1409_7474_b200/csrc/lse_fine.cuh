@@ -40,6 +40,19 @@ __device__ __forceinline__ float fine_phi(const FastParams& P, const uint32_t (&
   return out;
 }
 
+// The CTA's state words: word-rows r-1, r, r+1 (r = blockIdx.y) of columns
+// xb .. xb+SW-1, 0 outside the image; the LUT stores made before are published
+// by the same barrier.
+template <int SW>
+__device__ __forceinline__ void fine_stage_words(const FastParams& P, int xb, uint32_t (&s_w)[3][SW]) {
+  const int r = blockIdx.y;
+  for (int q = threadIdx.x; q < 3 * SW; q += blockDim.x) {
+    const int row = q / SW, col = q - row * SW;
+    s_w[row][col] = word_at<false>(P, r - 1 + row, xb + col);
+  }
+  __syncthreads();
+}
+
 template <int R>
 __device__ __forceinline__ void fine_load_luts(const FastParams& P, float* s_lt, float* s_ls) {
   constexpr int NPAT = 1 << (2 * R + 1);
@@ -82,14 +95,16 @@ template <int R, int MODEL, int SRC>
 __global__ void __launch_bounds__(32 * kFineCols, 4) k_update_fine(FastParams P) {
   constexpr int NPAT = 1 << (2 * R + 1);
   constexpr int NC = 2 * R + 3;                  // window columns x-R-1 .. x+R+1
+  constexpr int SW = kFineCols + 2 * (R + 1);   // state words staged per word-row
   __shared__ float s_lt[NPAT];
   __shared__ float s_ls[NPAT];
+  __shared__ uint32_t s_w[3][SW];                // word-rows r-1, r, r+1; 0 outside
   fine_load_luts<R>(P, s_lt, s_ls);
-  __syncthreads();
   pdl_wait();
   pdl_launch_dependents();
   Scalars* sc = P.scal;
   if (*(volatile const int*)&sc->stop) return;
+  fine_stage_words<SW>(P, blockIdx.x * kFineCols - (R + 1), s_w);
   if (MODEL == REGION && blockIdx.x == 0 && blockIdx.y == 0 && threadIdx.x == 0 &&
       sc->zero_vel && sc->model != EDGE)
     sc->degenerate = 1;                          // sticky degenerate (engine.py:239-240)
@@ -104,12 +119,13 @@ __global__ void __launch_bounds__(32 * kFineCols, 4) k_update_fine(FastParams P)
   // the first R+1 lanes and (r, r+1) for the others
   const int up = lane > R ? 1 : 0;
   const int sh = up ? lane - R - 1 : lane + 31 - R;
+  const int wq = threadIdx.x >> 5;               // this column's first staged word
   uint32_t win[NC], cm[NC];
 #pragma unroll
   for (int j = 0; j < NC; ++j) {
     const int xc = x - (R + 1) + j;
     cm[j] = (xc >= 0 && xc < W) ? 0xffffffffu : 0u;
-    win[j] = __funnelshift_r(word_at<false>(P, r - 1 + up, xc), word_at<false>(P, r + up, xc), sh);
+    win[j] = __funnelshift_r(s_w[up][wq + j], s_w[up + 1][wq + j], sh);
   }
   const bool cols_in = x - R - 1 >= 0 && x + R + 1 <= W - 1;
   auto row_in = [&](int row) { return cols_in && row - R >= 0 && row + R <= H - 1; };
@@ -171,14 +187,16 @@ template <int R, bool PART, bool CKPT>
 __global__ void __launch_bounds__(32 * kFineCols) k_partition_fine(FastParams P) {
   constexpr int NPAT = 1 << (2 * R + 1);
   constexpr int NC = 2 * R + 1;                  // window columns x-R .. x+R
+  constexpr int SW = kFineCols + 2 * R;
   __shared__ float s_lt[NPAT];
   __shared__ float s_ls[NPAT];
+  __shared__ uint32_t s_w[3][SW];
   fine_load_luts<R>(P, s_lt, s_ls);
-  __syncthreads();
   pdl_wait();
   pdl_launch_dependents();
   Scalars* sc = P.scal;
   if (*(volatile const int*)&sc->stop) return;
+  fine_stage_words<SW>(P, blockIdx.x * kFineCols - R, s_w);
   const float eps_phi = sc->eps_phi;
   const int lane = threadIdx.x & 31;
   const int x = blockIdx.x * kFineCols + (threadIdx.x >> 5);
@@ -190,12 +208,13 @@ __global__ void __launch_bounds__(32 * kFineCols) k_partition_fine(FastParams P)
   // first R lanes, (r, r+1) for the others)
   const int up = lane >= R ? 1 : 0;
   const int sh = up ? lane - R : lane + 32 - R;
+  const int wq = threadIdx.x >> 5;
   uint32_t win[NC], cm[NC];
 #pragma unroll
   for (int j = 0; j < NC; ++j) {
     const int xc = x - R + j;
     cm[j] = (xc >= 0 && xc < W) ? 0xffffffffu : 0u;
-    win[j] = __funnelshift_r(word_at<false>(P, r - 1 + up, xc), word_at<false>(P, r + up, xc), sh);
+    win[j] = __funnelshift_r(s_w[up][wq + j], s_w[up + 1][wq + j], sh);
   }
   const bool act = i < H;
   const bool in = i - R >= 0 && i + R <= H - 1 && x - R >= 0 && x + R <= W - 1;
