@@ -441,8 +441,8 @@ struct TraceRec {
 std::vector<TraceRec> g_traces;
 long long g_trace_launch = 0;
 constexpr long long kTrCta = 2 * 4096, kTrWarp = 4 * 4096;
-unsigned long long* trace_begin(lse_run* r, long long n, int grid, const char* name,
-                                long long nb) {
+unsigned long long* trace_begin_st(cudaStream_t st, long long n, int grid, const char* name,
+                                   long long nb) {
   const char* f = std::getenv("LSE_UNIT_TRACE_FILE");
   if (!f) return nullptr;
   const long long skip = std::getenv("LSE_UNIT_TRACE_SKIP") ? std::atoll(std::getenv("LSE_UNIT_TRACE_SKIP")) : 0;
@@ -451,14 +451,18 @@ unsigned long long* trace_begin(lse_run* r, long long n, int grid, const char* n
   if (k < skip || k >= skip + cnt) return nullptr;
   TraceRec t{nullptr, n, nb, 2 * n + kTrCta + kTrWarp + 2, grid, name};
   cudaMalloc(&t.d, t.cap * sizeof(unsigned long long));
-  cudaMemsetAsync(t.d, 0, t.cap * sizeof(unsigned long long), r->st);
-  k_stamp<<<1, 1, 0, r->st>>>(t.d + t.cap - 2);
+  cudaMemsetAsync(t.d, 0, t.cap * sizeof(unsigned long long), st);
+  k_stamp<<<1, 1, 0, st>>>(t.d + t.cap - 2);
   g_traces.push_back(t);
   return t.d;
 }
-void trace_after(lse_run* r, unsigned long long* d) {
-  if (d) k_stamp<<<1, 1, 0, r->st>>>(d + g_traces.back().cap - 1);
+void trace_after_st(cudaStream_t st, unsigned long long* d) {
+  if (d) k_stamp<<<1, 1, 0, st>>>(d + g_traces.back().cap - 1);
 }
+unsigned long long* trace_begin(lse_run* r, long long n, int grid, const char* name, long long nb) {
+  return trace_begin_st(r->st, n, grid, name, nb);
+}
+void trace_after(lse_run* r, unsigned long long* d) { trace_after_st(r->st, d); }
 void trace_flush() {
   if (g_traces.empty()) return;
   FILE* fp = std::fopen(std::getenv("LSE_UNIT_TRACE_FILE"), "a");
@@ -1217,10 +1221,13 @@ int create_impl(lse_run** out, const lse_params* p, long long height, long long 
       const long long ni0 = (long long)(g0.r_hi - g0.r_lo) * g0.nci + (g0.nB1 + 31) / 32;
       bq = ni0 == 0 ? 16 : ni0 < 2 * warps_u ? 8 : kBorderQ;
     }
+    // the partition keeps the default border lanes (its units carry the
+    // partials, so a batched tile and the same tile alone group them alike)
+    int bqp = kBorderQ;
     if (const char* bv = std::getenv("LSE_BORDER_Q"))
-      bq = std::atoi(bv) >= 16 ? 16 : std::atoi(bv) >= 8 ? 8 : 4;
+      bq = bqp = std::atoi(bv) >= 16 ? 16 : std::atoi(bv) >= 8 ? 8 : 4;
     r->gu = make_geo(H, W, R, 1 + R, 1 + R, R + 1, bq);   // update reaches R+1 rows/columns
-    r->gp = make_geo(H, W, R, R, R, R, bq);               // partition reaches R
+    r->gp = make_geo(H, W, R, R, R, R, bqp);              // partition reaches R
     if (si && (!geo_restrict_rows(r->gu, si->own_lo, si->own_hi) ||
                !geo_restrict_rows(r->gp, si->own_lo, si->own_hi))) {
       delete r;
@@ -1665,6 +1672,11 @@ int lse_run_kernel_times(lse_run* r, double* update_ms, long long* update_launch
 struct lse_batch {
   std::vector<lse_run*> runs;
   int T = 0;
+  // update geometry of one tile: the batch has work for every warp, so its
+  // border units keep the default 8-row lanes whatever a lone tile would
+  // use (the update has no partials, so this changes no reduction order; the
+  // partition uses the single run's geometry and partial grouping)
+  Geo gu{};
   cudaStream_t st = nullptr;
   uint32_t* bits[2] = {nullptr, nullptr};
   uint32_t* P = nullptr;
@@ -1716,6 +1728,7 @@ FastParams batch_params(lse_batch* b, int sel) {
   P.tile_h = r0->H;
   P.tile_words = b->tile_words;
   P.tile_data = b->tile_data;
+  P.gu = b->gu;
   P.g.H = b->T * b->tile_hr * 32;             // the stacked arrays
   P.g.HR = b->T * b->tile_hr;
   P.own_lo = 0;
@@ -1737,10 +1750,17 @@ int batch_iteration(lse_batch* b, long long it, bool ckpt, int src, bool any_reg
     const long long n = (long long)b->T * (b->nb_upd + b->ni_upd);
     const int g = fast_grid(n, kUpdateCtasPerSm);
     P.work_base = batch_take_work(b, n, g);
+#ifdef LSE_UNIT_TRACE
+    P.trace = trace_begin_st(b->st, n, g, "batch-update", (long long)b->T * b->nb_upd);
+#endif
     if (src == SRC_SCALED)
       TRY(launch_pdl(k_update<R, REGION, SRC_SCALED, true, 1>, g, kThreads, b->st, P));
     else
       TRY(launch_pdl(k_update<R, REGION, SRC_SMOOTH, true, 1>, g, kThreads, b->st, P));
+#ifdef LSE_UNIT_TRACE
+    trace_after_st(b->st, P.trace);
+    P.trace = nullptr;
+#endif
   }
   b->cur ^= 1;
   if (!any_region && !ckpt) return LSE_OK;
@@ -1748,8 +1768,14 @@ int batch_iteration(lse_batch* b, long long it, bool ckpt, int src, bool any_reg
   const long long n = (long long)b->T * (b->nb_part + b->ni_part);
   const int g = fast_grid(n, kPartitionCtasPerSm);
   P.work_base = batch_take_work(b, n, g);
+#ifdef LSE_UNIT_TRACE
+  P.trace = trace_begin_st(b->st, n, g, "batch-partition", (long long)b->T * b->nb_part);
+#endif
   if (ckpt) TRY(launch_pdl(k_partition<R, true, true, false, true>, g, kThreads, b->st, P));
   else TRY(launch_pdl(k_partition<R, true, false, false, true>, g, kThreads, b->st, P));
+#ifdef LSE_UNIT_TRACE
+  trace_after_st(b->st, P.trace);
+#endif
   TRY(launch_pdl(k_finalize_stage1_tiles, dim3(kFinSlices, b->T), 256, b->st,
                  (const TilePartial*)b->part, b->part_fin, (const Scalars*)b->scal,
                  (int)b->nb_part, (int)b->ni_part, b->T, ckpt ? 1 : 0));
@@ -1785,7 +1811,11 @@ int lse_batch_create(lse_batch** out, lse_run* const* runs, int n) {
   b->tile_hr = r0->g.HR;
   b->tile_words = (long long)r0->g.HR * r0->g.pitch_w;
   b->tile_data = (long long)r0->g.HR * 32 * r0->g.data_pitch;
-  b->nb_upd = r0->nb_upd[0];
+  b->gu = make_geo(r0->H, r0->W, r0->R, 1 + r0->R, 1 + r0->R, r0->R + 1, kBorderQ);
+  if (const char* bv = std::getenv("LSE_BORDER_Q"))
+    b->gu = make_geo(r0->H, r0->W, r0->R, 1 + r0->R, 1 + r0->R, r0->R + 1,
+                     std::atoi(bv) >= 16 ? 16 : std::atoi(bv) >= 8 ? 8 : 4);
+  b->nb_upd = border_units(b->gu);
   b->ni_upd = r0->ni_upd;
   b->nb_part = r0->nb_part;
   b->ni_part = r0->ni_part;
@@ -1894,6 +1924,9 @@ int lse_batch_advance(lse_batch* b, long long n_steps, lse_status* statuses) {
     CK(cudaMemcpyAsync(b->h_scal, b->scal, T * sizeof(Scalars), cudaMemcpyDeviceToHost, b->st));
     CK(cudaMemcpyAsync(&work, b->work, sizeof(work), cudaMemcpyDeviceToHost, b->st));
     CK(cudaStreamSynchronize(b->st));
+#ifdef LSE_UNIT_TRACE
+    trace_flush();
+#endif
     if (work != b->work_next) {
       char msg[128];
       std::snprintf(msg, sizeof(msg), "batch work-counter mismatch: device %llu, expected %llu",
