@@ -77,6 +77,12 @@ struct RunGeom {
 // predecessor drains, and waits here before touching the predecessor's
 // results.  Without the launch attribute both are no-ops.
 __device__ __forceinline__ void pdl_wait() { asm volatile("griddepcontrol.wait;" ::: "memory"); }
+// A run's stop flag.  It is only written by earlier kernels of the stream
+// (finalize passes), which are complete and visible once pdl_wait() returns,
+// so an L2 (.cg) load suffices -- a volatile access compiles to a
+// system-scope strong load on the critical path of every short kernel.
+template <typename S>
+__device__ __forceinline__ int stop_flag(const S* sc) { return __ldcg(&sc->stop); }
 __device__ __forceinline__ void pdl_launch_dependents() {
   asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
 }

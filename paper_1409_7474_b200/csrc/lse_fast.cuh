@@ -1013,7 +1013,7 @@ __global__ void __launch_bounds__(kThreads, kUpdateCtasPerSm) k_update(FastParam
   pdl_wait();
   pdl_launch_dependents();
   const Scalars* sc = P.scal;
-  if (!BATCH && *(volatile const int*)&sc->stop) return;
+  if (!BATCH && stop_flag(sc)) return;
   if (MODEL == REGION && blockIdx.x == 0) {      // sticky degenerate (engine.py:239-240)
     for (int t = threadIdx.x; t < (BATCH ? P.ntiles : 1); t += blockDim.x)
       if (P.scal[t].zero_vel && !P.scal[t].stop && P.scal[t].model != EDGE)
@@ -1044,7 +1044,7 @@ __global__ void __launch_bounds__(kThreads, kUpdateCtasPerSm) k_update(FastParam
         lu = nb + (iu - tile * ni);
       }
       const Scalars* st = P.scal + tile;
-      stopped = *(volatile const int*)&st->stop != 0;
+      stopped = stop_flag(st) != 0;
       A = st->A;
       B = st->B;
       eps_u = st->eps_u;
@@ -1654,7 +1654,7 @@ __global__ void __launch_bounds__(kThreads, kPartitionCtasPerSm) k_partition(Fas
   pdl_wait();
   pdl_launch_dependents();
   Scalars* sc = P.scal;
-  if (!BATCH && !MASKONLY && *(volatile const int*)&sc->stop) return;
+  if (!BATCH && !MASKONLY && stop_flag(sc)) return;
   const float eps_phi = sc->eps_phi;
   const int lane = threadIdx.x & 31;
   const int nseg = P.nseg;
@@ -1682,7 +1682,7 @@ __global__ void __launch_bounds__(kThreads, kPartitionCtasPerSm) k_partition(Fas
       const Scalars* st = P.scal + tile;
       part_t = PART && st->model != EDGE;
       // converged tiles, and edge tiles off the checkpoints, have nothing to do
-      if (*(volatile const int*)&st->stop || (!part_t && !CKPT)) continue;
+      if (stop_flag(st) || (!part_t && !CKPT)) continue;
     }
     LaneDelta d{0.0, 0.0, 0, 0, 0ull};
     if (lu < nb) {

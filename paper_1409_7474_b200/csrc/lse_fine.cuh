@@ -21,25 +21,6 @@ namespace lse {
 
 constexpr int kFineCols = 8;                     // columns (warps) per CTA
 
-// phi at window row offset m (window bit 0 = first window row) for window
-// columns j0 .. j0 + 2R: sum_d w_|d| t(j0 + R + d), d = -R..R, left to right.
-template <int R, int NC, bool INT>
-__device__ __forceinline__ float fine_phi(const FastParams& P, const uint32_t (&win)[NC],
-                                          const uint32_t (&cm)[NC], int j0, int m, uint32_t vr,
-                                          float Lv, const float* s_lt, const float* s_ls) {
-  constexpr uint32_t PM = (1u << (2 * R + 1)) - 1u;
-  float out = 0.f;
-#pragma unroll
-  for (int d = -R; d <= R; ++d) {
-    const int j = j0 + R + d;
-    const uint32_t p = (win[j] >> m) & PM;
-    const float t = INT ? s_lt[p] : fmaf(2.f, s_ls[p & vr & cm[j]], cm[j] ? -Lv : 0.f);
-    const float wd = P.w32[d < 0 ? -d : d];
-    out = (d == -R) ? wd * t : fmaf(wd, t, out);
-  }
-  return out;
-}
-
 // The CTA's state words: word-rows r-1, r, r+1 (r = blockIdx.y) of columns
 // xb .. xb+SW-1, 0 outside the image; the LUT stores made before are published
 // by the same barrier.
@@ -69,10 +50,13 @@ __device__ __forceinline__ void fine_trow(const uint32_t (&win)[NC], const uint3
                                           int m, bool in, uint32_t vr, float Lv,
                                           const float* s_lt, const float* s_ls, float (&t)[NC]) {
   constexpr uint32_t PM = (1u << (2 * R + 1)) - 1u;
+  if (in) {                                      // one branch per row, not per column
 #pragma unroll
-  for (int j = 0; j < NC; ++j) {
-    const uint32_t p = (win[j] >> m) & PM;
-    t[j] = in ? s_lt[p] : fmaf(2.f, s_ls[p & vr & cm[j]], cm[j] ? -Lv : 0.f);
+    for (int j = 0; j < NC; ++j) t[j] = s_lt[(win[j] >> m) & PM];
+  } else {
+#pragma unroll
+    for (int j = 0; j < NC; ++j)
+      t[j] = fmaf(2.f, s_ls[(win[j] >> m) & PM & vr & cm[j]], cm[j] ? -Lv : 0.f);
   }
 }
 // horizontal pass centred on window column j0 + R, left to right
@@ -103,29 +87,32 @@ __global__ void __launch_bounds__(32 * kFineCols, 4) k_update_fine(FastParams P)
   pdl_wait();
   pdl_launch_dependents();
   Scalars* sc = P.scal;
-  if (*(volatile const int*)&sc->stop) return;
+  if (stop_flag(sc)) return;
+  const int lane = threadIdx.x & 31;
+  const int x = blockIdx.x * kFineCols + (threadIdx.x >> 5);
+  const int r = blockIdx.y;
+  const int H = P.g.H, W = P.g.W;
+  const int i = r * 32 + lane;
+  // this pixel's data value, in flight while the words are staged
+  const float d = (x < W && i < H) ? __ldg(P.data32 + (size_t)i * P.g.data_pitch + x) : 0.f;
   fine_stage_words<SW>(P, blockIdx.x * kFineCols - (R + 1), s_w);
   if (MODEL == REGION && blockIdx.x == 0 && blockIdx.y == 0 && threadIdx.x == 0 &&
       sc->zero_vel && sc->model != EDGE)
     sc->degenerate = 1;                          // sticky degenerate (engine.py:239-240)
   const float A = sc->A, B = sc->B, eps_u = sc->eps_u;
-  const int lane = threadIdx.x & 31;
-  const int x = blockIdx.x * kFineCols + (threadIdx.x >> 5);
-  const int r = blockIdx.y;
-  const int H = P.g.H, W = P.g.W;
   if (x >= W) return;                            // whole warps
-  const int i = r * 32 + lane;
   // window of each column: 32 rows from i-R-1, from word-rows (r-1, r) for
   // the first R+1 lanes and (r, r+1) for the others
   const int up = lane > R ? 1 : 0;
   const int sh = up ? lane - R - 1 : lane + 31 - R;
-  const int wq = threadIdx.x >> 5;               // this column's first staged word
+  const uint32_t* wlo = &s_w[up][threadIdx.x >> 5];   // this column's first staged words
+  const uint32_t* whi = wlo + SW;
   uint32_t win[NC], cm[NC];
 #pragma unroll
   for (int j = 0; j < NC; ++j) {
     const int xc = x - (R + 1) + j;
     cm[j] = (xc >= 0 && xc < W) ? 0xffffffffu : 0u;
-    win[j] = __funnelshift_r(s_w[up][wq + j], s_w[up + 1][wq + j], sh);
+    win[j] = __funnelshift_r(wlo[j], whi[j], sh);
   }
   const bool cols_in = x - R - 1 >= 0 && x + R + 1 <= W - 1;
   auto row_in = [&](int row) { return cols_in && row - R >= 0 && row + R <= H - 1; };
@@ -165,7 +152,6 @@ __global__ void __launch_bounds__(32 * kFineCols, 4) k_update_fine(FastParams P)
     const float dx = (x == 0) ? 2.f * (pr - p0) : (x == W - 1) ? 2.f * (p0 - pl) : (pr - pl);
     const float dy = (i == 0) ? 2.f * (pn - p0) : (i == H - 1) ? 2.f * (p0 - pm) : (pn - pm);
     const float h = sqrt_approx(fmaf(dx, dx, dy * dy));     // 2 |grad phi|
-    const float d = __ldg(P.data32 + (size_t)i * P.g.data_pitch + x);
     const float vf = (MODEL == REGION) ? fmaf(A, d, B) : d; // A, B / the g plane carry dt/2
     const float u = fmaf(vf, h, p0);
     bit = u > 0.f;
@@ -195,7 +181,7 @@ __global__ void __launch_bounds__(32 * kFineCols) k_partition_fine(FastParams P)
   pdl_wait();
   pdl_launch_dependents();
   Scalars* sc = P.scal;
-  if (*(volatile const int*)&sc->stop) return;
+  if (stop_flag(sc)) return;
   fine_stage_words<SW>(P, blockIdx.x * kFineCols - R, s_w);
   const float eps_phi = sc->eps_phi;
   const int lane = threadIdx.x & 31;
@@ -208,23 +194,21 @@ __global__ void __launch_bounds__(32 * kFineCols) k_partition_fine(FastParams P)
   // first R lanes, (r, r+1) for the others)
   const int up = lane >= R ? 1 : 0;
   const int sh = up ? lane - R : lane + 32 - R;
-  const int wq = threadIdx.x >> 5;
+  const uint32_t* wlo = &s_w[up][threadIdx.x >> 5];
+  const uint32_t* whi = wlo + SW;
   uint32_t win[NC], cm[NC];
 #pragma unroll
   for (int j = 0; j < NC; ++j) {
     const int xc = x - R + j;
     cm[j] = (xc >= 0 && xc < W) ? 0xffffffffu : 0u;
-    win[j] = __funnelshift_r(s_w[up][wq + j], s_w[up + 1][wq + j], sh);
+    win[j] = __funnelshift_r(wlo[j], whi[j], sh);
   }
   const bool act = i < H;
   const bool in = i - R >= 0 && i + R <= H - 1 && x - R >= 0 && x + R <= W - 1;
-  float ph;
-  if (in) {
-    ph = fine_phi<R, NC, true>(P, win, cm, 0, 0, 0u, 0.f, s_lt, s_ls);
-  } else {
-    const uint32_t v0 = row_valid_mask<R>(i, H);
-    ph = fine_phi<R, NC, false>(P, win, cm, 0, 0, v0, s_ls[v0], s_lt, s_ls);
-  }
+  float t[NC];
+  const uint32_t v0 = in ? 0u : row_valid_mask<R>(i, H);
+  fine_trow<R, NC>(win, cm, 0, in, v0, in ? 0.f : s_ls[v0], s_lt, s_ls, t);
+  const float ph = fine_hsum<R, NC>(P, t, 0);
   bool pb = act && ph > 0.f, mb = pb;
   if (act && fabsf(ph) <= eps_phi) {             // near tie: exact fp64 sign
     const double e = exact_phi_fast<R>(P.ctx, P.bits_in, i, x);

@@ -441,7 +441,7 @@ __global__ void __launch_bounds__(256) k_finalize_stage1(PartRanges R3, TilePart
                                                          const Scalars* sc) {
   pdl_wait();
   pdl_launch_dependents();
-  if (*(volatile const int*)&sc->stop) return;
+  if (stop_flag(sc)) return;
   const int n = R3.n[0] + R3.n[1] + R3.n[2];
   const int per = (n + gridDim.x - 1) / gridDim.x;
   const int t0 = min(n, (int)blockIdx.x * per), t1 = min(n, t0 + per);
@@ -452,7 +452,7 @@ __global__ void __launch_bounds__(256) k_finalize_stage1(PartRanges R3, TilePart
 // the ranks exchange (fixed order)
 __global__ void __launch_bounds__(256) k_reduce_to_one(PartRanges R3, TilePartial* out,
                                                        const Scalars* sc, int check_stop) {
-  if (check_stop && *(volatile const int*)&sc->stop) return;
+  if (check_stop && stop_flag(sc)) return;
   reduce_slice(R3, 0, R3.n[0] + R3.n[1] + R3.n[2], out);
 }
 
@@ -467,7 +467,7 @@ __global__ void __launch_bounds__(256) k_finalize_stage1_tiles(const TilePartial
   pdl_launch_dependents();
   const int t = blockIdx.y;
   const Scalars* sc = scal + t;
-  if (*(volatile const int*)&sc->stop) return;
+  if (stop_flag(sc)) return;
   if (sc->model == EDGE && !ckpt) return;
   PartRanges R3{{part + (size_t)t * nb, part + (size_t)T * nb + (size_t)t * ni, part},
                 {nb, ni, 0}};
@@ -483,7 +483,7 @@ __global__ void __launch_bounds__(64) k_finalize_run_tiles(const TilePartial* fi
   pdl_launch_dependents();
   const int t = blockIdx.x;
   Scalars* sc = scal + t;
-  if (*(volatile const int*)&sc->stop) return;
+  if (stop_flag(sc)) return;
   const bool region = sc->model != EDGE;
   if (!region && !ckpt) return;
   const TilePartial* f = fin + (size_t)t * kFinSlices;
@@ -496,7 +496,7 @@ __global__ void __launch_bounds__(64) k_finalize_run(PartRanges R3, Scalars* sc,
                                                        int ckpt, long long iter) {
   pdl_wait();
   pdl_launch_dependents();
-  if (*(volatile const int*)&sc->stop) return;
+  if (stop_flag(sc)) return;
   finalize_cta(R3, sc, true, region != 0, ckpt != 0, iter);
 }
 
@@ -723,7 +723,7 @@ __global__ void __launch_bounds__(256) k_band_sums(const uint32_t* __restrict__ 
                                                    int ckpt, long long iter) {
   pdl_wait();
   pdl_launch_dependents();
-  if (!ABS && *(volatile const int*)&sc->stop) return;
+  if (!ABS && stop_flag(sc)) return;
   __shared__ TilePartial s_w[kMaxBands][8];
   const int r = blockIdx.y;
   const int nblk = gridDim.x * gridDim.y, blk = r * gridDim.x + blockIdx.x;
@@ -884,7 +884,7 @@ __global__ void __launch_bounds__(256) k_band_peak(const ExactCtx* __restrict__ 
     if (m) atomicMax(&sc->peak_bits, m);
   }
   if (!last_cta_arrival(cnt)) return;
-  if (threadIdx.x != 0 || *(volatile const int*)&sc->stop) return;
+  if (threadIdx.x != 0 || stop_flag(sc)) return;
   // coefficients of the next update: the fused kernels see the data plane D
   // (fp32) and vf = A * D with A = (dt / 2) / peak
   m = sc->zero_vel ? 0ull : *(volatile unsigned long long*)&sc->peak_bits;
