@@ -190,6 +190,7 @@ struct lse_run {
   ExactCtx* d_ctx = nullptr;
   ExactCtx h_ctx{};
   double* d_w64 = nullptr;
+  double* d_lut64 = nullptr;   // exact vertical-pass values of the interior patterns
   long long* d_keys = nullptr;
   unsigned long long* d_count = nullptr;
   double* d_F[2] = {nullptr, nullptr};
@@ -1331,6 +1332,11 @@ int create_impl(lse_run** out, const lse_params* p, long long height, long long 
         if ((q >> k) & 1) s += r->h_ctx.w64[std::abs(k - r->R)];
       ls[q] = (float)s;
     }
+    std::vector<double> lt64(512, 0.0);
+    for (int q = 0; q < np; ++q) lt64[q] = host_t64((unsigned)q, r->R, r->h_ctx.w64);
+    if (!r->d_lut64 && dalloc(&r->d_lut64, 512) != LSE_OK) return cleanup(LSE_ERR_CUDA);
+    cudaMemcpyAsync(r->d_lut64, lt64.data(), 512 * sizeof(double), cudaMemcpyHostToDevice, r->st);
+    r->h_ctx.lut64 = r->d_lut64;
     cudaMemcpyAsync(r->d_lut_t, lt.data(), 512 * sizeof(float), cudaMemcpyHostToDevice, r->st);
     cudaMemcpyAsync(r->d_lut_s, ls.data(), 512 * sizeof(float), cudaMemcpyHostToDevice, r->st);
     cudaStreamSynchronize(r->st);
@@ -1987,7 +1993,7 @@ void lse_run_destroy(lse_run* r) {
   void* ptrs[] = {r->d_px, r->d_py, r->d_mag, r->d_edt_g, r->d_edt_v, r->d_edt_zn,
                   r->d_edt_zd, r->d_dist[0], r->d_dist[1],
                   r->d_scratch, r->d_poly, r->d_offs, r->d_flag,
-                  r->d_bands32, r->d_bands64, r->d_chg, r->d_bpart, r->d_pmax,
+                  r->d_bands32, r->d_bands64, r->d_chg, r->d_bpart, r->d_pmax, r->d_lut64,
                   r->d_work, r->d_part_fin, r->d_part_init, r->d_data32, r->d_data64, r->d_bits[0], r->d_bits[1], r->d_P, r->d_M,
                   r->d_mask, r->d_part, r->d_scal, r->d_lut_t, r->d_lut_s, r->d_ctx,
                   r->d_w64, r->d_keys, r->d_count, r->d_F[0], r->d_F[1], r->d_U, r->d_T};

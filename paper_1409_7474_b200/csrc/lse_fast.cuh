@@ -41,6 +41,7 @@ struct ExactCtx {
   const float* bands32;   // VECTOR: fp32 band planes (data_pitch rows)
   const double* bands64;  // VECTOR: exact band planes (nullptr -> bands32 exact)
   long long band_stride;  // elements per band plane
+  const double* lut64;    // R <= 4: wt() of every all-valid 2R+1-row pattern (host_t64)
 };
 
 struct FastParams {
@@ -236,6 +237,9 @@ __device__ __forceinline__ void gather_window(const ExactCtx* c, const uint32_t*
 template <int R, int NC>
 __device__ __forceinline__ double wt(const ExactCtx* c, const uint32_t (&val)[NC],
                                      const uint32_t (&valid)[NC], int rr, int cc) {
+  constexpr uint32_t PM = (1u << (2 * R + 1)) - 1u;
+  if (R <= 4 && c->lut64 && ((valid[cc] >> (rr - R)) & PM) == PM)
+    return __ldg(&c->lut64[(val[cc] >> (rr - R)) & PM]);   // the same value, tabulated
   auto b = [&](int k) -> double {
     if (!((valid[cc] >> k) & 1u)) return 0.0;
     return ((val[cc] >> k) & 1u) ? 1.0 : -1.0;
