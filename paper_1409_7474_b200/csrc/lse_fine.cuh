@@ -8,13 +8,14 @@
 // word-row.  The state word of the next iteration is one __ballot_sync.
 //
 // The arithmetic is the tiled kernels' arithmetic pixel by pixel: the same
-// vertical LUT values (exact-rounded t for windows inside the image, the
-// zero-padding weight-sum form otherwise), the same left-to-right horizontal
-// FMA order, the same gradient / velocity / u expressions and the same
-// near-tie guards, so the fp32 values, and with them every decision (fp32
-// outside the guard band, the fp64 restatement inside it), are the same.
-// The only difference is the partial granularity of the partition sums (one
-// per state word), i.e. the grouping of the c+/c- sums.
+// vertical LUT values (exact-rounded t where a pixel's window lies inside the
+// image, the zero-padding weight-sum form otherwise -- chosen per pixel here,
+// per lane block there), the same left-to-right horizontal FMA order, the
+// same gradient / velocity / u expressions and the same near-tie guards.
+// Every decision therefore equals the reference's fp64 decision, as on the
+// tiled path: outside the guard band the fp32 sign is provably right, inside
+// it the fp64 restatement decides.  The partition partials are one per state
+// word, so only the grouping of the c+/c- sums differs from the tiled path.
 #pragma once
 
 namespace lse {
