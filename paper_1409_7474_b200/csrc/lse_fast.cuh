@@ -279,6 +279,9 @@ template <int R, int SRC>
 __device__ __noinline__ double exact_u_fast(const ExactCtx* c, const uint32_t* bits, int i, int x) {
   constexpr int NR = 2 * R + 3, NC = 2 * R + 3;
   const int H = c->H, W = c->W;
+  // the pixel's data value is loaded with the window (one round of latency
+  // for both; the multi-band term reads its bands later)
+  const double Iv = c->model != VECTOR ? data_exact(c, i, x) : 0.0;
   uint32_t val[NC], valid[NC];
   gather_window<NR, NC>(c, bits, i - 1 - R, x - 1 - R, val, valid);
   auto ph = [&](int di, int dx) -> double {      // phi at (i + di, x + dx)
@@ -299,11 +302,9 @@ __device__ __noinline__ double exact_u_fast(const ExactCtx* c, const uint32_t* b
   const double h = np_hypot(fx, fy);
   double v;
   const Scalars* sc = c->scal;
-  if (c->model != EDGE) {
-    v = exact_v_at(c, i, x, h);
-  } else {
-    v = dmul(data_exact(c, i, x), h);
-  }
+  if (c->model == EDGE) v = dmul(Iv, h);
+  else if (c->model == VECTOR) v = exact_v_at(c, i, x, h);
+  else v = exact_v_twomean(sc, Iv, h);           // exact_v_at's two-mean branch
   atomicAdd(&c->scal->fallbacks, 1ull);
   return dadd(pc, dmul(c->dt, v));
 }
