@@ -835,9 +835,20 @@ int band_chain(lse_run* r, bool absolute, bool ckpt, long long it) {
     TRY(launch_pdl(k_band_sums<false>, gr, 256, r->st, (const uint32_t*)r->d_chg,
                    (const uint32_t*)r->d_P, (const ExactCtx*)r->d_ctx, r->d_bpart, r->g,
                    r->d_scal, cnt, M, ckpt ? 1 : 0, it));
-  // peak pass: ~8 CTAs per SM, each a 1024-column block of every gy-th row
+  // peak pass: one wave -- as many CTAs as fit on the SMs at once (a partial
+  // second wave measured ~2 % slower per iteration on C3), each a 1024-column
+  // block of every gy-th row
   const int gx = (r->W + 1023) / 1024;
-  const int gy = std::max(1, std::min(r->H, num_sms() * 8 / gx));
+  int peak_cps = 0;
+  switch (r->nbands) {
+    case 1: cudaOccupancyMaxActiveBlocksPerMultiprocessor(&peak_cps, k_band_peak<1>, 256, 0); break;
+    case 2: cudaOccupancyMaxActiveBlocksPerMultiprocessor(&peak_cps, k_band_peak<2>, 256, 0); break;
+    case 3: cudaOccupancyMaxActiveBlocksPerMultiprocessor(&peak_cps, k_band_peak<3>, 256, 0); break;
+    default: cudaOccupancyMaxActiveBlocksPerMultiprocessor(&peak_cps, k_band_peak<4>, 256, 0); break;
+  }
+  if (const char* v = std::getenv("LSE_PEAK_CPS")) peak_cps = std::atoi(v);
+  peak_cps = std::max(1, peak_cps);
+  const int gy = std::max(1, std::min(r->H, num_sms() * peak_cps / gx));
   const dim3 gp(gx, gy);
   const ExactCtx* cctx = r->d_ctx;
   switch (r->nbands) {
