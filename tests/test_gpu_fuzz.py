@@ -82,3 +82,25 @@ def test_forced_decomposition_matches_oracle(h, w, split, bq, model, monkeypatch
 def test_random_geometry_tiled_matches_oracle(h, w, model, ts, monkeypatch):
     monkeypatch.setenv("LSE_FINE_MAX_PX", "0")
     test_random_geometry_matches_oracle(h, w, model, ts)
+
+
+# Sizes either side of the per-pixel / tiled switch (450 000 pixels) and
+# extreme aspect ratios, through the default decomposition choice.
+@pytest.mark.parametrize("h,w", [(600, 700), (700, 700), (90, 5100), (5100, 90), (33, 16000)])
+@pytest.mark.parametrize("model", ["region", "edge"])
+def test_switch_sizes_match_oracle(h, w, model):
+    rng = np.random.default_rng(h + 7 * w)
+    img = np.clip(0.3 + 0.4 * (rng.random((h, w)) > 0.7) + 0.05 * rng.standard_normal((h, w)),
+                  0, 1)
+    poly = np.array([[w * 0.05, h * 0.1], [w * 0.9, h * 0.05], [w * 0.95, h * 0.85],
+                     [w * 0.1, h * 0.95]])
+    sign = -1 if model == "edge" else 1
+    phi0 = O.rasterize_seeds([poly], sign, w, h)
+    iters = 10
+    p = L.default_params(L.ModelKind.from_name(model), max_iters=iters,
+                         conv_check_every=iters + 1)
+    r = L.EvolutionRun(img, L.SeedSpec(polygons=(poly,), inside_sign=sign), p)
+    r.advance(iters)
+    op = O.OracleParams(model=model, max_iters=iters, conv_check_every=iters + 1)
+    ref = O.run_fixed(img, phi0, op, iters)
+    assert np.array_equal(r.state.phi, ref.phi), np.abs(r.state.phi - ref.phi).max()
