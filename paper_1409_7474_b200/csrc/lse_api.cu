@@ -286,6 +286,17 @@ int run_flag(lse_run* r, int** out) {
   return LSE_OK;
 }
 
+// partials of the per-pixel partition: one per CTA of kFineCols columns up to
+// kFineCtaParts CTAs, else one per state word
+constexpr long long kFineCtaParts = 768;
+bool fine_cta_parts(const lse_run* r) {
+  return (long long)r->g.HR * ((r->W + kFineCols - 1) / kFineCols) <= kFineCtaParts;
+}
+long long fine_parts(const lse_run* r) {
+  return fine_cta_parts(r) ? (long long)r->g.HR * ((r->W + kFineCols - 1) / kFineCols)
+                           : (long long)r->g.HR * r->W;
+}
+
 FastParams fast_params(lse_run* r) {
   FastParams P{};
   P.pbits = r->d_P;
@@ -519,10 +530,23 @@ int launch_update(lse_run* r, FastParams P) {
 template <int R, bool PART, bool CKPT, bool MASKONLY>
 int launch_partition(lse_run* r, FastParams P) {
   const bool fine = r->fine && !MASKONLY;
-  const long long n = fine ? (long long)r->g.HR * r->W : r->nb_part + r->ni_part;
+  const long long n = fine ? fine_parts(r) : r->nb_part + r->ni_part;
   if (fine) {
     const dim3 gf((r->W + kFineCols - 1) / kFineCols, r->g.HR);
-    TRY(launch_pdl(k_partition_fine<R, PART, CKPT>, gf, 32 * kFineCols, r->st, P));
+    // one partial per CTA and a single-stage finalize on small images
+    // (256^2: 13.2 -> 11.5 us per iteration); per-word partials and the
+    // two stages below beyond kFineCtaParts CTAs (512^2: 27.7 vs 29.0 us)
+    if (fine_cta_parts(r)) {
+      TRY(launch_pdl(k_partition_fine<R, PART, CKPT, true>, gf, 32 * kFineCols, r->st, P));
+    } else {
+      TRY(launch_pdl(k_partition_fine<R, PART, CKPT, false>, gf, 32 * kFineCols, r->st, P));
+    }
+    if (fine_cta_parts(r) && !is_bands(r)) {
+      PartRanges RF{{r->d_part, r->d_part, r->d_part}, {(int)n, 0, 0}};
+      TRY(launch_pdl(k_finalize_run, 1, 64, r->st, RF, r->d_scal, PART ? 1 : 0, CKPT ? 1 : 0,
+                     (long long)P.iter));
+      return LSE_OK;
+    }
   } else {
   const int g = fast_grid(n, kPartitionCtasPerSm);
   P.work_base = take_work(r, n, g);
@@ -824,7 +848,7 @@ int generic_iteration(lse_run* r, long long it, bool reinit_now, bool reg_now, b
 // pixel (fp32 plane for the fused kernels) and its peak, the coefficients
 int band_chain(lse_run* r, bool absolute, bool ckpt, long long it) {
   const dim3 gr((r->g.pitch_w + 1023) / 1024, r->g.HR);
-  const int n = (int)(r->fine ? (long long)r->g.HR * r->W : r->nb_part + r->ni_part);
+  const int n = (int)(r->fine ? fine_parts(r) : r->nb_part + r->ni_part);
   PartRanges M{{r->d_part, r->d_part, r->d_part}, {ckpt ? n : 0, 0, 0}};
   unsigned long long* cnt = r->d_pmax;          // [0]: band sums, [1]: band peak arrivals
   if (absolute)
@@ -1280,7 +1304,7 @@ int create_impl(lse_run** out, const lse_params* p, long long height, long long 
   }
   const long long nparts = std::max<long long>(
       std::max<long long>(r->g.ntiles, r->ni_part + r->nb_part),
-      r->fine ? (long long)r->g.HR * r->W : 0LL);
+      r->fine ? fine_parts(r) : 0LL);
   auto cleanup = [&](int rc) {
     lse_run_destroy(r);
     return rc;

@@ -170,7 +170,9 @@ __global__ void __launch_bounds__(32 * kFineCols, 4) k_update_fine(FastParams P)
 // (The two-stage finalize of the tiled path follows; folding it into the
 // last CTA of this kernel measured slower: one CTA then reduces every word's
 // partial.)
-template <int R, bool PART, bool CKPT>
+// CTAP: one partial per CTA (small images: the finalize is then a single
+// stage); else one per state word (the layout the two-stage finalize prefers).
+template <int R, bool PART, bool CKPT, bool CTAP>
 __global__ void __launch_bounds__(32 * kFineCols) k_partition_fine(FastParams P) {
   constexpr int NPAT = 1 << (2 * R + 1);
   constexpr int NC = 2 * R + 1;                  // window columns x-R .. x+R
@@ -189,8 +191,12 @@ __global__ void __launch_bounds__(32 * kFineCols) k_partition_fine(FastParams P)
   const int x = blockIdx.x * kFineCols + (threadIdx.x >> 5);
   const int r = blockIdx.y;
   const int H = P.g.H, W = P.g.W;
-  if (x >= W) return;                            // whole warps
+  if (!CTAP && x >= W) return;                   // whole warps (no CTA barrier below)
   const int i = r * 32 + lane;
+  double a_in = 0.0, a_out = 0.0;
+  long long n_in = 0, n_out = 0;
+  unsigned long long mism = 0ull;
+  if (CTAP ? x < W : true) {                     // (whole warps)
   // window of each column: 32 rows from i-R (word-rows (r-1, r) for the
   // first R lanes, (r, r+1) for the others)
   const int up = lane >= R ? 1 : 0;
@@ -219,9 +225,6 @@ __global__ void __launch_bounds__(32 * kFineCols) k_partition_fine(FastParams P)
   const uint32_t pw = __ballot_sync(0xffffffffu, pb);
   const uint32_t mw = __ballot_sync(0xffffffffu, mb);
   const size_t o = (size_t)r * P.g.pitch_w + x;
-  double a_in = 0.0, a_out = 0.0;
-  long long n_in = 0, n_out = 0;
-  unsigned long long mism = 0ull;
   if (PART) {
     const uint32_t chg = P.pbits[o] ^ pw;
     if (P.chg) {
@@ -239,6 +242,7 @@ __global__ void __launch_bounds__(32 * kFineCols) k_partition_fine(FastParams P)
       P.mbits[o] = mw;
     }
   }
+  }
 #pragma unroll
   for (int s = 16; s > 0; s >>= 1) {
     a_in += __shfl_xor_sync(0xffffffffu, a_in, s);
@@ -246,14 +250,37 @@ __global__ void __launch_bounds__(32 * kFineCols) k_partition_fine(FastParams P)
     n_in += __shfl_xor_sync(0xffffffffu, n_in, s);
     n_out += __shfl_xor_sync(0xffffffffu, n_out, s);
   }
+  if (!CTAP) {
+    if (lane == 0) {
+      TilePartial t{};
+      t.a_hi = a_in;
+      t.b_hi = a_out;
+      t.n_a = n_in;
+      t.n_b = n_out;
+      t.mism = mism;
+      P.part[(size_t)r * W + x] = t;
+    }
+    return;
+  }
+  // one partial per CTA (its words in column order)
+  __shared__ double s_a[kFineCols], s_b[kFineCols];
+  __shared__ long long s_na[kFineCols], s_nb[kFineCols];
+  __shared__ unsigned long long s_m[kFineCols];
+  const int wq = threadIdx.x >> 5;
   if (lane == 0) {
+    s_a[wq] = a_in; s_b[wq] = a_out; s_na[wq] = n_in; s_nb[wq] = n_out; s_m[wq] = mism;
+  }
+  __syncthreads();
+  if (threadIdx.x == 0) {
     TilePartial t{};
-    t.a_hi = a_in;
-    t.b_hi = a_out;
-    t.n_a = n_in;
-    t.n_b = n_out;
-    t.mism = mism;
-    P.part[(size_t)r * W + x] = t;
+    for (int w = 0; w < kFineCols; ++w) {
+      t.a_hi += s_a[w];
+      t.b_hi += s_b[w];
+      t.n_a += s_na[w];
+      t.n_b += s_nb[w];
+      t.mism += s_m[w];
+    }
+    P.part[(size_t)blockIdx.y * gridDim.x + blockIdx.x] = t;
   }
 }
 
