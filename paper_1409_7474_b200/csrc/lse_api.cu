@@ -562,6 +562,12 @@ int launch_partition(lse_run* r, FastParams P) {
     // two-stage fixed-order reduction of all unit partials -> the next
     // update's coefficients (64 CTAs reduce contiguous slices, 1 CTA the rest)
     PartRanges R3{{r->d_part, r->d_part, r->d_part}, {(int)n, 0, 0}};
+    if (!is_bands(r) && !r->strip && n <= kFineCtaParts) {
+      // few partials (small images): a single-stage finalize, one launch less
+      TRY(launch_pdl(k_finalize_run, 1, 64, r->st, R3, r->d_scal, PART ? 1 : 0, CKPT ? 1 : 0,
+                     (long long)P.iter));
+      return LSE_OK;
+    }
     if (!is_bands(r)) {
       TRY(launch_pdl(k_finalize_stage1, kFinSlices, 256, r->st, R3, r->d_part_fin,
                      (const Scalars*)r->d_scal));
@@ -1817,6 +1823,11 @@ int batch_iteration(lse_batch* b, long long it, bool ckpt, int src, bool any_reg
 #ifdef LSE_UNIT_TRACE
   trace_after_st(b->st, P.trace);
 #endif
+  if (b->nb_part + b->ni_part <= kFineCtaParts) {   // as a lone tile: one stage
+    TRY(launch_pdl(k_finalize_tiles_direct, b->T, 64, b->st, (const TilePartial*)b->part, b->scal,
+                   (int)b->nb_part, (int)b->ni_part, b->T, ckpt ? 1 : 0, it));
+    return LSE_OK;
+  }
   TRY(launch_pdl(k_finalize_stage1_tiles, dim3(kFinSlices, b->T), 256, b->st,
                  (const TilePartial*)b->part, b->part_fin, (const Scalars*)b->scal,
                  (int)b->nb_part, (int)b->ni_part, b->T, ckpt ? 1 : 0));

@@ -491,6 +491,25 @@ __global__ void __launch_bounds__(64) k_finalize_run_tiles(const TilePartial* fi
   finalize_cta(R1, sc, true, region, ckpt != 0, iter);
 }
 
+// batched tiles with few partials per tile: a single-stage finalize per tile
+// (blockIdx.x = tile) over the tile's partials in the single-run order
+// [border units][interior units] -- what k_finalize_run does for the same
+// tile run alone, so the reduction order is the same
+__global__ void __launch_bounds__(64) k_finalize_tiles_direct(const TilePartial* part,
+                                                              Scalars* scal, int nb, int ni,
+                                                              int T, int ckpt, long long iter) {
+  pdl_wait();
+  pdl_launch_dependents();
+  const int t = blockIdx.x;
+  Scalars* sc = scal + t;
+  if (stop_flag(sc)) return;
+  const bool region = sc->model != EDGE;
+  if (!region && !ckpt) return;
+  PartRanges R3{{part + (size_t)t * nb, part + (size_t)T * nb + (size_t)t * ni, part},
+                {nb, ni, 0}};
+  finalize_cta(R3, sc, true, region, ckpt != 0, iter);
+}
+
 // per-iteration finalize of the fast path (DELTA partials); no-op once stopped
 __global__ void __launch_bounds__(64) k_finalize_run(PartRanges R3, Scalars* sc, int region,
                                                        int ckpt, long long iter) {
