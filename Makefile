@@ -20,10 +20,18 @@ $(TRACE_LIB): $(SRC) $(HDR)
 	@mkdir -p $(dir $@)
 	$(NVCC) $(FLAGS) -DLSE_UNIT_TRACE -shared -o $@ $(SRC) 2> /dev/null
 
+# guard-certification build: every fp32 decision also evaluated in fp64
+# (lse_check_stats; select with LSE_LIB_PATH)
+CHECK_LIB := paper_1409_7474_b200/_lib/liblse_b200_check.so
+check: $(CHECK_LIB)
+$(CHECK_LIB): $(SRC) $(HDR)
+	@mkdir -p $(dir $@)
+	$(NVCC) $(FLAGS) -DLSE_CHECK_BOUND -shared -o $@ $(SRC) 2> /dev/null
+
 oracle:
 	$(MAKE) -C oracle
 
 clean:
-	rm -f $(LIB) $(TRACE_LIB)
+	rm -f $(LIB) $(TRACE_LIB) $(CHECK_LIB)
 
-.PHONY: all clean oracle trace
+.PHONY: all clean oracle trace check

@@ -147,13 +147,25 @@ int lse_run_read_mask(lse_run* run, unsigned char* out, int inside_sign, int pac
 int lse_run_begin_timing(lse_run* run);
 int lse_run_end_timing(lse_run* run, double* ms);
 
-/* Run options.  "skip_uniform" (default 1): let the fused kernels copy warp
- * blocks whose whole stencil window is uniform (exactly unchanged by the
- * update) instead of recomputing them; 0 forces the dense pass. */
+/* Run options.  "skip_uniform" (default 1, or the environment's
+ * LSE_SKIP_UNIFORM at creation): let the fused kernels copy warp blocks
+ * whose whole stencil window is uniform (exactly unchanged by the update)
+ * instead of recomputing them; 0 forces the dense pass. */
 int lse_run_set_option(lse_run* run, const char* name, long long value);
 
 /* Number of kernel launches this library has issued (process-wide). */
 long long lse_launch_count(void);
+
+/* Guard certification (the validation build liblse_b200_check.so, `make
+ * check`): every fp32 decision value of the fused kernels -- u of the update,
+ * phi of the partition -- is also evaluated in the reference's fp64 order
+ * (every LSE_CHECK_EVERY-th iteration, default 1).  lse_check_stats fills
+ * out[8] = {max |u32-u64|/eps_u, max |phi32-phi64|/eps_phi, min |u64|,
+ * min |phi64|, fp32 decisions outside the guard band that differ from fp64
+ * (u, phi), values checked, thread slots used}; reset != 0 clears them.
+ * lse_check_enabled() is 1 in that build only. */
+int lse_check_enabled(void);
+int lse_check_stats(double* out, int reset);
 
 /* Device-event timing of the fused kernels (bench/roofline support). */
 int lse_run_set_profiling(lse_run* run, int enabled);
@@ -175,6 +187,11 @@ void lse_run_destroy(lse_run* run);
 typedef struct lse_batch lse_batch;
 int lse_batch_create(lse_batch** out, lse_run* const* runs, int n_runs);
 int lse_batch_advance(lse_batch* batch, long long n_steps, lse_status* statuses);
+/* Device-event timing of whole lse_batch_advance calls (gather, iterations,
+ * scatter on the batch's stream): set_timing(1) clears and starts it,
+ * elapsed returns the summed milliseconds and the number of timed calls. */
+int lse_batch_set_timing(lse_batch* batch, int enabled);
+int lse_batch_elapsed(lse_batch* batch, double* ms, long long* calls);
 void lse_batch_destroy(lse_batch* batch);
 
 /* ---- row strips: one rank's share of a multi-GPU run --------

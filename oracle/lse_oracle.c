@@ -5,6 +5,9 @@
  * and by bench.py as the timed CPU baseline ("port").  It restates, in the
  * reference's exact float64 operation order:
  *   engine.py:148-174  _advance_once      (update, finiteness, reinit, smoothing)
+ *   multi-band region term (C3; oracle/lse_oracle.py region_velocity_bands):
+ *                      D = sum_k (c+_k - c-_k)(2 I_k - c+_k - c-_k), bands
+ *                      accumulated left to right, then models.py:109-119
  *   engine.py:222-254  EvolutionRun._step_once / advance (checkpoint convergence)
  *   models.py:84-119   edge_velocity / region_velocity
  *   models.py:144-162  zhang_velocity (mean separation)
@@ -38,6 +41,7 @@ typedef struct {
   const double* reg_w; /* axis weights, ts_reg */
   const double* pre_w; /* axis weights, ts_pre */
   double nu;           /* zhang speed constant */
+  int nbands;          /* model 3 (multi-band region): bands of the image */
 } oracle_params;
 
 /* scipy correlate1d, symmetric branch, zero padding. axis 0 = along rows. */
@@ -127,9 +131,9 @@ static double pairwise_par(const double* a, long long n) {
   return res;
 }
 
-/* grid.py:102-118; returns 0 when a side is empty */
-static int region_means(const double* img, const double* phi, int H, int W, double* buf_pos,
-                        double* buf_neg, long long* row_pos, double* cp, double* cm) {
+/* grid.py:102-118: the row-major prefix counts of {phi >= 0}; returns the
+ * count, or -1 when a side is empty */
+static long long partition_rows(const double* phi, int H, int W, long long* row_pos) {
   const long long n = (long long)H * W;
 #pragma omp parallel for schedule(static)
   for (int i = 0; i < H; ++i) {
@@ -143,7 +147,16 @@ static int region_means(const double* img, const double* phi, int H, int W, doub
     row_pos[i] = total;
     total += c;
   }
-  if (total == 0 || total == n) return 0;
+  return (total == 0 || total == n) ? -1 : total;
+}
+
+/* means of img over {phi >= 0} / {phi < 0} (numpy pairwise sums of the
+ * row-major compacted sides; buf holds the positive side then the negative) */
+static void side_means(const double* img, const double* phi, int H, int W, double* buf,
+                       const long long* row_pos, long long total, double* cp, double* cm) {
+  const long long n = (long long)H * W;
+  double* buf_pos = buf;
+  double* buf_neg = buf + total;
 #pragma omp parallel for schedule(static)
   for (int i = 0; i < H; ++i) {
     long long kp = row_pos[i], kn = (long long)i * W - row_pos[i];
@@ -155,6 +168,14 @@ static int region_means(const double* img, const double* phi, int H, int W, doub
   }
   *cp = pairwise_par(buf_pos, total) / (double)total;
   *cm = pairwise_par(buf_neg, n - total) / (double)(n - total);
+}
+
+/* grid.py:102-118; returns 0 when a side is empty */
+static int region_means(const double* img, const double* phi, int H, int W, double* buf,
+                        long long* row_pos, double* cp, double* cm) {
+  const long long total = partition_rows(phi, H, W, row_pos);
+  if (total < 0) return 0;
+  side_means(img, phi, H, W, buf, row_pos, total, cp, cm);
   return 1;
 }
 
@@ -183,11 +204,11 @@ void oracle_edge_function(const double* img, int H, int W, const double* w, int 
 typedef struct {
   int H, W;
   oracle_params p;
-  const double* img;
+  const double* img;  /* (H, W), or nbands planes for model 3 */
   double* phi; /* caller-owned, in/out */
-  double *u, *t, *o, *g, *bp, *bn;
+  double *u, *t, *g, *buf, *D;
   long long* rows;
-  unsigned char* ck;
+  unsigned char* ck;  /* checkpoint masks, allocated at the first checkpoint */
   long long n_ck;
   long long iteration;
   int converged, degenerate;
@@ -203,15 +224,13 @@ oracle_ctx* oracle_create(const double* img, int H, int W, const oracle_params* 
   c->phi = phi;
   c->u = (double*)malloc(n * sizeof(double));
   c->t = (double*)malloc(n * sizeof(double));
-  c->o = (double*)malloc(n * sizeof(double));
   c->rows = (long long*)malloc((size_t)H * sizeof(long long));
-  c->ck = (unsigned char*)malloc(n * (size_t)(p->conv_window + 1));
   if (p->model == 0) {
     c->g = (double*)malloc(n * sizeof(double));
     oracle_edge_function(img, H, W, p->pre_w, p->ts_pre, p->edge_gain, c->g);
   } else {
-    c->bp = (double*)malloc(n * sizeof(double));
-    c->bn = (double*)malloc(n * sizeof(double));
+    c->buf = (double*)malloc(n * sizeof(double));
+    if (p->model == 3) c->D = (double*)malloc(n * sizeof(double));
   }
   return c;
 }
@@ -220,13 +239,20 @@ void oracle_destroy(oracle_ctx* c) {
   if (!c) return;
   free(c->u);
   free(c->t);
-  free(c->o);
   free(c->g);
-  free(c->bp);
-  free(c->bn);
+  free(c->buf);
+  free(c->D);
   free(c->rows);
   free(c->ck);
   free(c);
+}
+
+void oracle_set_threads(int n) {
+#ifdef _OPENMP
+  omp_set_num_threads(n > 0 ? n : omp_get_num_procs());   /* 0: every host thread */
+#else
+  (void)n;
+#endif
 }
 
 void oracle_state(const oracle_ctx* c, long long* iteration, int* converged, int* degenerate) {
@@ -242,7 +268,7 @@ long long oracle_advance(oracle_ctx* c, long long n_iters) {
   const oracle_params* p = &c->p;
   const double* img = c->img;
   double* phi = c->phi;
-  double *u = c->u, *t = c->t, *o = c->o, *g = c->g;
+  double *u = c->u, *t = c->t, *g = c->g;
   const size_t n = (size_t)H * W;
   long long err = 0;
   for (long long s = 0; s < n_iters; ++s) {
@@ -250,9 +276,36 @@ long long oracle_advance(oracle_ctx* c, long long n_iters) {
     const long long it = c->iteration + 1;
     double cp = 0, cm = 0, dc = 0, peak = 0, mid = 0;
     int zero = 0;
-    const int two_mean = p->model == 1 || p->model == 2;
-    if (two_mean) {
-      if (!region_means(img, phi, H, W, c->bp, c->bn, c->rows, &cp, &cm)) {
+    const int two_mean = p->model == 1 || p->model == 2 || p->model == 3;
+    if (p->model == 3) {
+      /* multi-band region term: per-band means, D accumulated over the bands */
+      const long long total = partition_rows(phi, H, W, c->rows);
+      if (total < 0) {
+        zero = 1;
+      } else {
+        double* D = c->D;
+        for (int k = 0; k < p->nbands; ++k) {
+          const double* band = img + (size_t)k * n;
+          double bcp, bcm;
+          side_means(band, phi, H, W, c->buf, c->rows, total, &bcp, &bcm);
+          const double bdc = bcp - bcm;
+#pragma omp parallel for schedule(static)
+          for (long long q = 0; q < (long long)n; ++q) {
+            const double term = bdc * (2.0 * band[q] - bcp - bcm);
+            D[q] = k == 0 ? term : D[q] + term;
+          }
+        }
+        double pk = 0.0;
+#pragma omp parallel for reduction(max : pk) schedule(static)
+        for (long long q = 0; q < (long long)n; ++q) {
+          const double d = fabs(D[q]);
+          if (d > pk) pk = d;
+        }
+        peak = pk;
+        if (peak == 0.0) zero = 1;
+      }
+    } else if (two_mean) {
+      if (!region_means(img, phi, H, W, c->buf, c->rows, &cp, &cm)) {
         zero = 1;
       } else {
         dc = cp - cm;
@@ -287,7 +340,8 @@ long long oracle_advance(oracle_ctx* c, long long n_iters) {
           double fx, fy;
           np_gradient(phi, H, W, i, x, &fx, &fy);
           double h = hypot(fx, fy);
-          if (p->model == 1) v = (dc * (2.0 * img[q] - cp - cm) / peak) * h;
+          if (p->model == 3) v = (c->D[q] / peak) * h;
+          else if (p->model == 1) v = (dc * (2.0 * img[q] - cp - cm) / peak) * h;
           else if (p->model == 2) v = (p->nu * ((img[q] - mid) / peak)) * h;   /* models.py:162 */
           else v = g[q] * h;
         }
@@ -301,10 +355,7 @@ long long oracle_advance(oracle_ctx* c, long long n_iters) {
 #pragma omp parallel for schedule(static)
         for (long long k = 0; k < (long long)n; ++k) u[k] = u[k] > 0.0 ? 1.0 : -1.0;
       }
-      if (it % p->reg_period == 0) {
-        convolve_same(u, t, o, H, W, p->reg_w, p->ts_reg);
-        res = o;
-      }
+      if (it % p->reg_period == 0) convolve_same(u, t, u, H, W, p->reg_w, p->ts_reg);
 #pragma omp parallel for reduction(| : bad) schedule(static)
       for (long long k = 0; k < (long long)n; ++k) bad |= !isfinite(res[k]);
     }
@@ -317,6 +368,7 @@ long long oracle_advance(oracle_ctx* c, long long n_iters) {
     if (two_mean && zero) c->degenerate = 1;
     if (it % p->conv_check_every == 0) {
       const long long cw = p->conv_window;
+      if (!c->ck) c->ck = (unsigned char*)malloc(n * (size_t)(cw + 1));
       unsigned char* slot = c->ck + (size_t)(c->n_ck % (cw + 1)) * n;
 #pragma omp parallel for schedule(static)
       for (long long k = 0; k < (long long)n; ++k) slot[k] = phi[k] > 0.0;

@@ -89,6 +89,8 @@ _SIGS = {
     "lse_run_begin_timing": (_i, [_vp]),
     "lse_run_end_timing": (_i, [_vp, _dp]),
     "lse_launch_count": (_ll, []),
+    "lse_check_enabled": (_i, []),
+    "lse_check_stats": (_i, [_dp, _i]),
     "lse_run_set_option": (_i, [_vp, C.c_char_p, _ll]),
     "lse_run_set_profiling": (_i, [_vp, _i]),
     "lse_run_kernel_times": (_i, [_vp, _dp, _llp, _dp, _llp]),
@@ -96,6 +98,8 @@ _SIGS = {
     "lse_batch_create": (_i, [C.POINTER(_vp), C.POINTER(_vp), _i]),
     "lse_batch_advance": (_i, [_vp, _ll, C.POINTER(LseStatus)]),
     "lse_batch_destroy": (None, [_vp]),
+    "lse_batch_set_timing": (_i, [_vp, _i]),
+    "lse_batch_elapsed": (_i, [_vp, _dp, _llp]),
     "lse_strip_create": (_i, [C.POINTER(_vp), C.POINTER(LseParams), _ll, _ll, _vp, _i,
                               C.POINTER(LsePhi0), _i, _i, _ll]),
     "lse_strip_image_range": (_i, [_vp, _dp]),

@@ -101,3 +101,53 @@ def run_tiles(images, seeds, params) -> list[ExtractionResult]:
     out = [r.result() for r in runs]
     batch.close()
     return out
+
+
+# ------------------------------------------------------- multi-GPU sharding
+def shard(n_tiles: int, rank: int, world: int) -> list[int]:
+    """Tiles of one rank: k = rank, rank + world, ... (the
+    tiles are independent units, so a rank's share needs no data-path
+    collective; the split is even to within one tile)."""
+    if world < 1 or not 0 <= rank < world:
+        raise ValueError("need 0 <= rank < world")
+    return list(range(rank, n_tiles, world))
+
+
+def run_tiles_sharded(make_tile, n_tiles: int, rank: int | None = None,
+                      world: int | None = None, gather: str = "all", runner=None):
+    """`run` for n_tiles independent tiles spread over the ranks of the
+    default torch.distributed group (one process per GPU).
+
+    make_tile(k) -> (image, seeds, params) builds tile k; each rank runs its
+    shard(n_tiles, rank, world) as one TileBatch on its own GPU (runner:
+    list of (image, seeds, params) -> list of ExtractionResult, default
+    run_tiles).  The only communication is the host-side gather of the
+    per-tile results afterwards: gather = "all" (every rank gets all n_tiles
+    results in tile order), "rank0" (rank 0 does, the others get None) or
+    "none" (each rank returns {k: result} of its own tiles).
+    """
+    import torch.distributed as dist
+    if rank is None or world is None:
+        on = dist.is_available() and dist.is_initialized()
+        rank = dist.get_rank() if on else 0
+        world = dist.get_world_size() if on else 1
+    mine = shard(n_tiles, rank, world)
+    runner = runner or (lambda items: run_tiles([i[0] for i in items], [i[1] for i in items],
+                                                [i[2] for i in items]))
+    items = [make_tile(k) for k in mine]
+    local = dict(zip(mine, runner(items) if items else []))
+    if gather == "none" or world == 1:
+        return local if gather == "none" else [local[k] for k in range(n_tiles)]
+    parts = [None] * world
+    if gather == "all":
+        dist.all_gather_object(parts, local)
+    else:
+        dist.gather_object(local, parts if rank == 0 else None, dst=0)
+        if rank != 0:
+            return None
+    merged = {}
+    for p in parts:
+        merged.update(p)
+    if sorted(merged) != list(range(n_tiles)):
+        raise RuntimeError("tile gather lost tiles")
+    return [merged[k] for k in range(n_tiles)]

@@ -138,6 +138,48 @@ double edge_eps_u(double dt) {
 
 }  // namespace
 
+// Guard certification (validation builds, -DLSE_CHECK_BOUND): process-wide
+// per-thread slots every checked launch accumulates into (lse_check_stats).
+namespace {
+#ifdef LSE_CHECK_BOUND
+constexpr long long kCheckSlots = 1LL << 21;
+CheckSlot* g_chk = nullptr;
+long long g_check_every = 1;
+__global__ void k_check_reset(CheckSlot* s, long long n) {
+  for (long long q = blockIdx.x * (long long)blockDim.x + threadIdx.x; q < n;
+       q += (long long)gridDim.x * blockDim.x)
+    s[q] = CheckSlot{0.f, 0.f, 3.0e38f, 3.0e38f, 0u, 0u, 0ull};
+}
+CheckSlot* check_slots() {
+  if (!g_chk) {
+    if (cudaMalloc(&g_chk, kCheckSlots * sizeof(CheckSlot)) != cudaSuccess) return nullptr;
+    k_check_reset<<<512, 256>>>(g_chk, kCheckSlots);
+    cudaDeviceSynchronize();
+    if (const char* e = std::getenv("LSE_CHECK_EVERY")) g_check_every = std::max(1LL, std::atoll(e));
+  }
+  return g_chk;
+}
+#endif
+// the certification slots of the launches of iteration `it` (null: unchecked)
+void set_check(FastParams& P, long long it) {
+#ifdef LSE_CHECK_BOUND
+  CheckSlot* s = check_slots();
+  const bool on = s && it % g_check_every == 0;
+  P.chk = on ? s : nullptr;
+  P.chk_cap = on ? kCheckSlots : 0;
+#else
+  (void)it;
+  P.chk = nullptr;
+  P.chk_cap = 0;
+#endif
+}
+}  // namespace
+
+// one-stage finalize cutoff of the tiled kernels (lone runs and every tile of
+// a batch: both sites read the run's copy, so a batched tile and the same
+// tile alone reduce alike); LSE_ONESTAGE_MAX_PARTS overrides it at creation
+constexpr long long kOneStageMaxParts = 768;
+
 struct lse_run {
   lse_params p{};
   std::vector<double> wreg, wpre;
@@ -233,6 +275,7 @@ struct lse_run {
   // reduces to one partial at strip_out and the ranks finalize together
   bool strip = false;
   bool fine = false;           // small image: per-pixel kernels (lse_fine.cuh)
+  long long onestage_max = kOneStageMaxParts;   // tiled partition: one-stage finalize cutoff
   int own_lo = 0, own_hi = 0;
   TilePartial* strip_out = nullptr;
   bool strip_part = false, strip_ckpt = false;   // phases owed by the last update
@@ -562,7 +605,7 @@ int launch_partition(lse_run* r, FastParams P) {
     // two-stage fixed-order reduction of all unit partials -> the next
     // update's coefficients (64 CTAs reduce contiguous slices, 1 CTA the rest)
     PartRanges R3{{r->d_part, r->d_part, r->d_part}, {(int)n, 0, 0}};
-    if (!is_bands(r) && !r->strip && n <= kFineCtaParts) {
+    if (!is_bands(r) && !r->strip && n <= r->onestage_max) {
       // few partials (small images): a single-stage finalize, one launch less
       TRY(launch_pdl(k_finalize_run, 1, 64, r->st, R3, r->d_scal, PART ? 1 : 0, CKPT ? 1 : 0,
                      (long long)P.iter));
@@ -600,6 +643,7 @@ template <int R, int MODEL>
 int launch_fast_R(lse_run* r, long long it, bool ckpt, int phase) {
   FastParams P = fast_params(r);
   P.iter = it;
+  set_check(P, it);
   if (phase != PH_PARTITION) {
     P.bits_in = r->d_bits[r->cur];
     P.bits_out = r->d_bits[r->cur ^ 1];
@@ -1307,6 +1351,10 @@ int create_impl(lse_run** out, const lse_params* p, long long height, long long 
     long long fine_max = 450000;                  // ~670^2: measured crossover
     if (const char* fv = std::getenv("LSE_FINE_MAX_PX")) fine_max = std::atoll(fv);
     r->fine = !r->strip && r->R >= 1 && r->R <= 4 && r->npx <= fine_max;
+    if (const char* ov = std::getenv("LSE_ONESTAGE_MAX_PARTS")) r->onestage_max = std::atoll(ov);
+    // product default of the exact uniform-window skip (lse_run_set_option
+    // changes it per run); LSE_SKIP_UNIFORM=0 makes every new run dense
+    if (const char* sv = std::getenv("LSE_SKIP_UNIFORM")) r->skip_uniform = std::atoi(sv) != 0;
   }
   const long long nparts = std::max<long long>(
       std::max<long long>(r->g.ntiles, r->ni_part + r->nb_part),
@@ -1662,6 +1710,47 @@ int lse_run_read_mask(lse_run* r, unsigned char* out, int inside_sign, int packe
 
 long long lse_launch_count(void) { return g_launches.load(); }
 
+int lse_check_enabled(void) {
+#ifdef LSE_CHECK_BOUND
+  return 1;
+#else
+  return 0;
+#endif
+}
+
+int lse_check_stats(double* out, int reset) {
+  if (!out) return fail(LSE_ERR_ARG, "null argument");
+#ifdef LSE_CHECK_BOUND
+  CheckSlot* d = check_slots();
+  if (!d) return fail(LSE_ERR_CUDA, "no certification slots");
+  CK(cudaDeviceSynchronize());
+  std::vector<CheckSlot> h(kCheckSlots);
+  CK(cudaMemcpy(h.data(), d, kCheckSlots * sizeof(CheckSlot), cudaMemcpyDeviceToHost));
+  double ru = 0, rp = 0, umin = 3.0e38, pmin = 3.0e38, bu = 0, bp = 0, n = 0, used = 0;
+  for (const CheckSlot& k : h) {
+    if (!k.n) continue;
+    ru = std::max(ru, (double)k.ru);
+    rp = std::max(rp, (double)k.rp);
+    umin = std::min(umin, (double)k.umin);
+    pmin = std::min(pmin, (double)k.pmin);
+    bu += k.bad_u;
+    bp += k.bad_p;
+    n += (double)k.n;
+    used += 1;
+  }
+  const double v[8] = {ru, rp, umin, pmin, bu, bp, n, used};
+  std::memcpy(out, v, sizeof(v));
+  if (reset) {
+    k_check_reset<<<512, 256>>>(d, kCheckSlots);
+    CK(cudaDeviceSynchronize());
+  }
+  return LSE_OK;
+#else
+  (void)reset;
+  return fail(LSE_ERR_UNSUPPORTED, "not a certification build (make check)");
+#endif
+}
+
 int lse_run_set_option(lse_run* r, const char* name, long long value) {
   if (!r || !name) return fail(LSE_ERR_ARG, "null argument");
   if (!std::strcmp(name, "skip_uniform")) {
@@ -1742,6 +1831,11 @@ struct lse_batch {
   long long tile_words = 0, tile_data = 0, nb_upd = 0, ni_upd = 0, nb_part = 0, ni_part = 0;
   int tile_hr = 0;
   int cur = 0;
+  // device-event timing of whole lse_batch_advance calls (bench support)
+  bool timing = false;
+  cudaEvent_t ev[2] = {nullptr, nullptr};
+  double t_ms = 0.0;
+  long long t_calls = 0;
 };
 
 namespace {
@@ -1793,6 +1887,7 @@ template <int R>
 int batch_iteration(lse_batch* b, long long it, bool ckpt, int src, bool any_region) {
   FastParams P = batch_params(b, b->cur);
   P.iter = it;
+  set_check(P, it);
   {
     const long long n = (long long)b->T * (b->nb_upd + b->ni_upd);
     const int g = fast_grid(n, kUpdateCtasPerSm);
@@ -1823,7 +1918,7 @@ int batch_iteration(lse_batch* b, long long it, bool ckpt, int src, bool any_reg
 #ifdef LSE_UNIT_TRACE
   trace_after_st(b->st, P.trace);
 #endif
-  if (b->nb_part + b->ni_part <= kFineCtaParts) {   // as a lone tile: one stage
+  if (b->nb_part + b->ni_part <= b->runs[0]->onestage_max) {   // as a lone tile: one stage
     TRY(launch_pdl(k_finalize_tiles_direct, b->T, 64, b->st, (const TilePartial*)b->part, b->scal,
                    (int)b->nb_part, (int)b->ni_part, b->T, ckpt ? 1 : 0, it));
     return LSE_OK;
@@ -1935,6 +2030,7 @@ int lse_batch_advance(lse_batch* b, long long n_steps, lse_status* statuses) {
       TRY(prepare(r));
     }
     for (auto* r : b->runs) CK(cudaStreamSynchronize(r->st));
+    if (b->timing) CK(cudaEventRecord(b->ev[0], b->st));
     // gather: state, partition and checkpoint bits, scalars
     std::vector<const void*> src(T);
     std::vector<void*> dst(T);
@@ -2000,6 +2096,14 @@ int lse_batch_advance(lse_batch* b, long long n_steps, lse_status* statuses) {
       dst[t] = b->runs[t]->d_scal;
     }
     TRY(tiles_copy(b, src, dst, sizeof(Scalars) / 4));
+    if (b->timing) {
+      CK(cudaEventRecord(b->ev[1], b->st));
+      CK(cudaEventSynchronize(b->ev[1]));
+      float ms = 0.f;
+      CK(cudaEventElapsedTime(&ms, b->ev[0], b->ev[1]));
+      b->t_ms += ms;
+      b->t_calls += 1;
+    }
     for (int t = 0; t < T; ++t) {
       lse_run* r = b->runs[t];
       const Scalars& s = b->h_scal[t];
@@ -2021,9 +2125,30 @@ int lse_batch_advance(lse_batch* b, long long n_steps, lse_status* statuses) {
   return LSE_OK;
 }
 
+int lse_batch_set_timing(lse_batch* b, int enabled) {
+  if (!b) return fail(LSE_ERR_ARG, "null batch");
+  if (enabled && !b->ev[0]) {
+    CK(cudaEventCreate(&b->ev[0]));
+    CK(cudaEventCreate(&b->ev[1]));
+  }
+  b->timing = enabled != 0;
+  b->t_ms = 0.0;
+  b->t_calls = 0;
+  return LSE_OK;
+}
+
+int lse_batch_elapsed(lse_batch* b, double* ms, long long* calls) {
+  if (!b || !ms) return fail(LSE_ERR_ARG, "null argument");
+  *ms = b->t_ms;
+  if (calls) *calls = b->t_calls;
+  return LSE_OK;
+}
+
 void lse_batch_destroy(lse_batch* b) {
   if (!b) return;
   if (b->st) cudaStreamSynchronize(b->st);
+  for (cudaEvent_t e : b->ev)
+    if (e) cudaEventDestroy(e);
   void* ptrs[] = {b->bits[0], b->bits[1], b->P, b->M, b->data32, b->data64, b->scal,
                   b->ctx, b->part, b->part_fin, b->work, (void*)b->d_src, (void*)b->d_dst};
   for (void* q : ptrs)

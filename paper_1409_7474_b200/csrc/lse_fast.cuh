@@ -44,6 +44,16 @@ struct ExactCtx {
   const double* lut64;    // R <= 4: wt() of every all-valid 2R+1-row pattern (host_t64)
 };
 
+// Guard certification (validation builds, -DLSE_CHECK_BOUND): every fp32
+// decision value of the fused kernels is compared with the reference's fp64
+// value; each thread accumulates into its own slot (no contention).
+struct CheckSlot {
+  float ru, rp;              // max |u32 - u64| / eps_u, max |phi32 - phi64| / eps_phi
+  float umin, pmin;          // min |u64|, min |phi64| (the closest decision to a tie)
+  unsigned bad_u, bad_p;     // fp32 decisions outside the guard band that differ from fp64
+  unsigned long long n;      // decision values checked
+};
+
 struct FastParams {
   const uint32_t* bits_in;   // b^n (update) / b^{n+1} (partition)
   uint32_t* bits_out;        // b^{n+1} (update)
@@ -77,6 +87,8 @@ struct FastParams {
   // the geometry of one tile (single runs: ntiles = 1, tile 0 is the image)
   int ntiles, tile_hr, tile_h;
   long long tile_words, tile_data;
+  CheckSlot* chk;            // validation builds: per-thread certification slots (or null)
+  long long chk_cap;
 };
 
 // exact-path frame of tile t (its context, state and first image row)
@@ -264,11 +276,12 @@ __device__ __forceinline__ double wphi(const ExactCtx* c, const uint32_t (&val)[
 
 // phi^{n+1} at (i, x) exactly (partition near-ties)
 template <int R>
-__device__ __noinline__ double exact_phi_fast(const ExactCtx* c, const uint32_t* bits, int i, int x) {
+__device__ __noinline__ double exact_phi_fast(const ExactCtx* c, const uint32_t* bits, int i, int x,
+                                              bool count = true) {
   constexpr int NR = 2 * R + 1, NC = 2 * R + 1;
   uint32_t val[NC], valid[NC];
   gather_window<NR, NC>(c, bits, i - R, x - R, val, valid);
-  atomicAdd(&c->scal->fallbacks, 1ull);
+  if (count) atomicAdd(&c->scal->fallbacks, 1ull);
   return wphi<R, NC>(c, val, valid, R, R);
 }
 
@@ -276,7 +289,8 @@ __device__ __noinline__ double exact_phi_fast(const ExactCtx* c, const uint32_t*
 // neighbours (np.gradient one-sided at the image border), glibc hypot,
 // the model's velocity, u = phi + dt * v.
 template <int R, int SRC>
-__device__ __noinline__ double exact_u_fast(const ExactCtx* c, const uint32_t* bits, int i, int x) {
+__device__ __noinline__ double exact_u_fast(const ExactCtx* c, const uint32_t* bits, int i, int x,
+                                            bool count = true) {
   constexpr int NR = 2 * R + 3, NC = 2 * R + 3;
   const int H = c->H, W = c->W;
   // the pixel's data value is loaded with the window (one round of latency
@@ -305,9 +319,48 @@ __device__ __noinline__ double exact_u_fast(const ExactCtx* c, const uint32_t* b
   if (c->model == EDGE) v = dmul(Iv, h);
   else if (c->model == VECTOR) v = exact_v_at(c, i, x, h);
   else v = exact_v_twomean(sc, Iv, h);           // exact_v_at's two-mean branch
-  atomicAdd(&c->scal->fallbacks, 1ull);
+  if (count) atomicAdd(&c->scal->fallbacks, 1ull);
   return dadd(pc, dmul(c->dt, v));
 }
+
+#ifdef LSE_CHECK_BOUND
+__device__ __forceinline__ CheckSlot* check_slot(const FastParams& P) {
+  if (!P.chk) return nullptr;
+  const long long s =
+      ((long long)blockIdx.y * gridDim.x + blockIdx.x) * blockDim.x + threadIdx.x;
+  return s < P.chk_cap ? P.chk + s : nullptr;
+}
+// u32: the fused kernel's fp32 u at (i, x) (frame of ctx / bits); the kernel's
+// decision off the guard band is u32 > 0
+template <int R, int SRC>
+__device__ __noinline__ void check_u(const FastParams& P, const ExactCtx* c, const uint32_t* bits,
+                                     int i, int x, float u32, float eps) {
+  CheckSlot* k = check_slot(P);
+  if (!k) return;
+  const double u64 = exact_u_fast<R, SRC>(c, bits, i, x, false);
+  k->ru = fmaxf(k->ru, (float)(fabs((double)u32 - u64) / (double)eps));
+  k->umin = fminf(k->umin, (float)fabs(u64));
+  if (fabsf(u32) > eps && ((u32 > 0.f) != (u64 > 0.0))) k->bad_u += 1u;
+  k->n += 1ull;
+}
+// phi32: the partition's fp32 phi^{n+1}; decisions phi >= 0 and phi > 0
+template <int R>
+__device__ __noinline__ void check_phi(const FastParams& P, const ExactCtx* c, const uint32_t* bits,
+                                       int i, int x, float p32, float eps) {
+  CheckSlot* k = check_slot(P);
+  if (!k) return;
+  const double p64 = exact_phi_fast<R>(c, bits, i, x, false);
+  k->rp = fmaxf(k->rp, (float)(fabs((double)p32 - p64) / (double)eps));
+  k->pmin = fminf(k->pmin, (float)fabs(p64));
+  if (fabsf(p32) > eps && ((p32 > 0.f) != (p64 > 0.0))) k->bad_p += 1u;
+  k->n += 1ull;
+}
+#define LSE_CHECK_U(R_, SRC_, P_, C_, B_, I_, X_, U_, E_) check_u<R_, SRC_>(P_, C_, B_, I_, X_, U_, E_)
+#define LSE_CHECK_PHI(R_, P_, C_, B_, I_, X_, V_, E_) check_phi<R_>(P_, C_, B_, I_, X_, V_, E_)
+#else
+#define LSE_CHECK_U(...) do { } while (0)
+#define LSE_CHECK_PHI(...) do { } while (0)
+#endif
 
 // valid-row mask of the window rows i-R .. i+R (bit d <-> row i-R+d)
 template <int R>
@@ -654,6 +707,10 @@ __device__ __forceinline__ void update_block_int2(const FastParams& P, uint32_t 
       ow[c] = __funnelshift_l(__float_as_uint(u1), ow[c], 1);
       umin0 = fminf(umin0, fabsf(u0));
       umin1 = fminf(umin1, fabsf(u1));
+      LSE_CHECK_U(R, SRC, P, tile_ctx(P, tile), tile_bits(P, tile),
+                  y0 - tile_y0(P, tile) + 2 * s, x0 + c, u0, eps_u);
+      LSE_CHECK_U(R, SRC, P, tile_ctx(P, tile), tile_bits(P, tile),
+                  y0 - tile_y0(P, tile) + 2 * s + 1, x0 + c, u1, eps_u);
     }
     if (umin0 <= eps_u) fbrows |= 1u << (2 * s);
     if (umin1 <= eps_u) fbrows |= 2u << (2 * s);
@@ -775,6 +832,10 @@ __device__ __forceinline__ void update_block_split(const FastParams& P, uint32_t
         ow[c] = __funnelshift_l(__float_as_uint(u1), ow[c], 1);
         umin0 = fminf(umin0, fabsf(u0));
         umin1 = fminf(umin1, fabsf(u1));
+        LSE_CHECK_U(R, SRC, P, tile_ctx(P, tile), tile_bits(P, tile),
+                    y0 - tile_y0(P, tile) + h0 + 2 * s, x0 + c, u0, eps_u);
+        LSE_CHECK_U(R, SRC, P, tile_ctx(P, tile), tile_bits(P, tile),
+                    y0 - tile_y0(P, tile) + h0 + 2 * s + 1, x0 + c, u1, eps_u);
       }
       if (umin0 <= eps_u) fbrows |= 1u << (h0 + 2 * s);
       if (umin1 <= eps_u) fbrows |= 2u << (h0 + 2 * s);
@@ -904,6 +965,7 @@ __device__ __forceinline__ void update_rows_border(const FastParams& P, const fl
         const float u = fmaf(vf, h, p0[c + 1]);
         if (u > 0.f) ow[c] |= bitk;
         if (fabsf(u) <= eps_u) fb |= 1u << c;
+        LSE_CHECK_U(R, SRC, P, P.ctx, P.bits_in, y0 + k, x, u, eps_u);
       }
       if (fb) fbrows |= bitk;
     }
@@ -1414,6 +1476,10 @@ __device__ __forceinline__ void partition_block(const FastParams& P, const float
         pw[c] = __funnelshift_l(__float_as_uint(ph2[c].y), pw[c], 1);
         pmin0 = fminf(pmin0, fabsf(ph2[c].x));
         pmin1 = fminf(pmin1, fabsf(ph2[c].y));
+        LSE_CHECK_PHI(R, P, tile_ctx(P, tile), tile_bits(P, tile), y0 - tile_y0(P, tile) + k,
+                      x0 + c, ph2[c].x, eps_phi);
+        LSE_CHECK_PHI(R, P, tile_ctx(P, tile), tile_bits(P, tile), y0 - tile_y0(P, tile) + k + 1,
+                      x0 + c, ph2[c].y, eps_phi);
       }
       if (pmin0 <= eps_phi) fbrows |= 1u << k;
       if (pmin1 <= eps_phi) fbrows |= 2u << k;
@@ -1574,6 +1640,7 @@ __device__ __forceinline__ void partition_rows_border(const FastParams& P, const
       if (x0 + c >= W) continue;
       if (ph[c] > 0.f) pw[c] |= bitk;
       tie |= fabsf(ph[c]) <= eps_phi;
+      LSE_CHECK_PHI(R, P, P.ctx, P.bits_in, i, x0 + c, ph[c], eps_phi);
     }
     if (tie) fbrows |= bitk;
   }

@@ -14,8 +14,11 @@
 // same gradient / velocity / u expressions and the same near-tie guards.
 // Every decision therefore equals the reference's fp64 decision, as on the
 // tiled path: outside the guard band the fp32 sign is provably right, inside
-// it the fp64 restatement decides.  The partition partials are one per state
-// word, so only the grouping of the c+/c- sums differs from the tiled path.
+// it the fp64 restatement decides.  The partition partials are one per CTA
+// of kFineCols state words (CTAP: images of at most kFineCtaParts CTAs, the
+// words' sums added in plain fp64 in column order) or one per state word
+// (larger images), so only the grouping of the c+/c- sums differs from the
+// tiled path.
 #pragma once
 
 namespace lse {
@@ -156,6 +159,7 @@ __global__ void __launch_bounds__(32 * kFineCols, 4) k_update_fine(FastParams P)
     const float vf = (MODEL == REGION) ? fmaf(A, d, B) : d; // A, B / the g plane carry dt/2
     const float u = fmaf(vf, h, p0);
     bit = u > 0.f;
+    LSE_CHECK_U(R, SRC, P, P.ctx, P.bits_in, i, x, u, eps_u);
     if (fabsf(u) <= eps_u)                       // near tie: the reference's fp64 decision
       bit = exact_u_fast<R, SRC>(P.ctx, P.bits_in, i, x) > 0.0;
   }
@@ -165,7 +169,8 @@ __global__ void __launch_bounds__(32 * kFineCols, 4) k_update_fine(FastParams P)
 
 // Partition / checkpoint pass over b^{n+1} (engine.py:168-169, grid.py:102-118,
 // engine.py:228-236): P = {phi >= 0} and M = {phi > 0} words, the sums over
-// the pixels that changed side (one partial per state word, index r * W + x),
+// the pixels that changed side (CTAP: one partial per CTA, its words' plain
+// fp64 sums added in column order; else one per state word, index r * W + x),
 // multi-band runs record the changed bits instead.
 // (The two-stage finalize of the tiled path follows; folding it into the
 // last CTA of this kernel measured slower: one CTA then reduces every word's
@@ -217,6 +222,7 @@ __global__ void __launch_bounds__(32 * kFineCols) k_partition_fine(FastParams P)
   fine_trow<R, NC>(win, cm, 0, in, v0, in ? 0.f : s_ls[v0], s_lt, s_ls, t);
   const float ph = fine_hsum<R, NC>(P, t, 0);
   bool pb = act && ph > 0.f, mb = pb;
+  if (act) LSE_CHECK_PHI(R, P, P.ctx, P.bits_in, i, x, ph, eps_phi);
   if (act && fabsf(ph) <= eps_phi) {             // near tie: exact fp64 sign
     const double e = exact_phi_fast<R>(P.ctx, P.bits_in, i, x);
     pb = e >= 0.0;

@@ -9,7 +9,7 @@ import pytest
 import lse_oracle as O
 import paper_1409_7474_b200 as L
 from paper_1409_7474_b200 import scenes
-from paper_1409_7474_b200.batch import TileBatch, _tile_run, run_tiles
+from paper_1409_7474_b200.batch import TileBatch, _tile_run, run_tiles, run_tiles_sharded
 from conftest import load_golden, square, two_region
 
 pytestmark = pytest.mark.gpu
@@ -37,20 +37,63 @@ def check_same(batch_runs, single_runs):
         assert np.array_equal(b.mask(), s.mask())
 
 
-@pytest.mark.parametrize("h", [100, 96])
-def test_mixed_models_match_single_runs(h):
+def mixed_case(h):
     kinds = ["region", "edge", "zhang", "region", "edge"]
     kw = dict(max_iters=60, conv_check_every=4, conv_window=2)
     seeds = [L.SeedSpec(polygons=(square(6, 8, 70, h - 10),), inside_sign=(-1) ** k)
              for k in range(len(kinds))]
     prm = [params(m, **kw) for m in kinds]
     imgs = [tile(k, h) for k in range(len(kinds))]
-    single = [L.EvolutionRun(imgs[k], seeds[k], prm[k]) for k in range(len(kinds))]
+    return imgs, seeds, prm
+
+
+@pytest.mark.parametrize("h", [100, 96])
+def test_mixed_models_match_single_runs(h, monkeypatch):
+    """A batched tile equals the same tile run alone on the tiled kernels
+    (LSE_FINE_MAX_PX=0: the lone tile groups its partials as the batch does)."""
+    imgs, seeds, prm = mixed_case(h)
+    monkeypatch.setenv("LSE_FINE_MAX_PX", "0")
+    single = [L.EvolutionRun(imgs[k], seeds[k], prm[k]) for k in range(len(imgs))]
     for r in single:
         r.advance(60)
-    batch = [L.EvolutionRun(imgs[k], seeds[k], prm[k]) for k in range(len(kinds))]
+    batch = [L.EvolutionRun(imgs[k], seeds[k], prm[k]) for k in range(len(imgs))]
     TileBatch(batch).advance(60)
     check_same(batch, single)
+
+
+@pytest.mark.parametrize("h", [100, 96])
+def test_mixed_models_match_single_runs_across_paths(h):
+    """Cross-path check: the lone tiles run the per-pixel kernels (their c+/c-
+    partials are grouped per CTA, the batch's per tiled unit); the
+    trajectories still agree here."""
+    imgs, seeds, prm = mixed_case(h)
+    single = [L.EvolutionRun(imgs[k], seeds[k], prm[k]) for k in range(len(imgs))]
+    for r in single:
+        r.advance(60)
+    batch = [L.EvolutionRun(imgs[k], seeds[k], prm[k]) for k in range(len(imgs))]
+    TileBatch(batch).advance(60)
+    check_same(batch, single)
+
+
+def test_two_stage_batched_finalize_matches_single_runs(monkeypatch):
+    """LSE_ONESTAGE_MAX_PARTS=0 forces the two-stage per-tile finalize
+    (k_finalize_stage1_tiles + k_finalize_run_tiles) that tiles of >= ~3000^2
+    take; a batched tile still equals the tile alone (tiled path, two-stage)."""
+    imgs, seeds, prm = mixed_case(100)
+    monkeypatch.setenv("LSE_FINE_MAX_PX", "0")
+    monkeypatch.setenv("LSE_ONESTAGE_MAX_PARTS", "0")
+    single = [L.EvolutionRun(imgs[k], seeds[k], prm[k]) for k in range(len(imgs))]
+    for r in single:
+        r.advance(60)
+    batch = [L.EvolutionRun(imgs[k], seeds[k], prm[k]) for k in range(len(imgs))]
+    TileBatch(batch).advance(60)
+    check_same(batch, single)
+    # and the two-stage result equals the default (one-stage) one
+    monkeypatch.setenv("LSE_ONESTAGE_MAX_PARTS", "768")
+    one = [L.EvolutionRun(imgs[k], seeds[k], prm[k]) for k in range(len(imgs))]
+    TileBatch(one).advance(60)
+    for a, b in zip(one, batch):
+        assert np.array_equal(a.mask(), b.mask())
 
 
 def test_chunked_batch_advance_and_degenerate_tile():
@@ -113,3 +156,19 @@ def test_batch_rejects_mismatched_tiles():
                        params("region"))
     with pytest.raises(RuntimeError):
         TileBatch([a, b])
+
+
+def test_sharded_runner_single_rank_equals_run_tiles():
+    n, size, iters = 3, 128, 20
+    sc = [scenes.config4_tile(k, size, iters) for k in range(n)]
+
+    def make(k):
+        s = sc[k]
+        return s.image, L.SeedSpec(polygons=s.polygons, inside_sign=s.inside_sign), \
+            params(s.model, **s.params)
+
+    a = run_tiles_sharded(make, n, rank=0, world=1)
+    b = run_tiles([make(k)[0] for k in range(n)], [make(k)[1] for k in range(n)],
+                  [make(k)[2] for k in range(n)])
+    for x, y in zip(a, b):
+        assert np.array_equal(x.mask, y.mask) and x.iterations == y.iterations == iters

@@ -65,3 +65,47 @@ def test_c_edge_function_bit_exact():
                                  w.ctypes.data_as(OC._dp), int(ts), float(gain),
                                  out.ctypes.data_as(OC._dp))
         assert np.array_equal(out, g[f"edge_out_{k}"])
+
+
+def _band_scene(k, h=72, w=64, seed=9):
+    rng = np.random.default_rng(seed)
+    base = np.array([0.25, 0.30, 0.28, 0.45])[:k]
+    fg = np.array([0.60, 0.62, 0.65, 0.35])[:k]
+    bands = base[:, None, None] + 0.05 * rng.standard_normal((k, h, w))
+    bands[:, 20:55, 15:50] = fg[:, None, None] + 0.04 * rng.standard_normal((k, 35, 35))
+    return np.clip(bands, 0, 1)
+
+
+@pytest.mark.parametrize("k", [1, 2, 4])
+def test_c_oracle_bands_match_numpy_restatement(k):
+    """The C restatement of C3's multi-band term equals the numpy one bit for
+    bit (and K = 1 is the region model: pinned to the reference goldens)."""
+    bands = _band_scene(k)
+    h, w = bands.shape[1:]
+    phi0 = O.rasterize_seeds([np.array([[4., 4.], [60., 4.], [60., 68.], [4., 68.]])], -1, w, h)
+    p = O.OracleParams(model="region", dt=15.0, sigma2=1.0, ts_reg=9, max_iters=60,
+                       conv_check_every=61)
+    ref = O.run_fixed(bands if k > 1 else bands[0], phi0, p, 60)
+    r = OC.COracleRun(bands, phi0, p, O.gaussian_weights)
+    r.advance(60)
+    assert r.iteration == 60
+    assert np.array_equal(r.phi, ref.phi)
+    if k == 1:
+        r1 = OC.COracleRun(bands[0], phi0, p, O.gaussian_weights)
+        r1.advance(60)
+        assert np.array_equal(r1.phi, r.phi)
+
+
+def test_c_oracle_thread_count_does_not_change_results():
+    bands = _band_scene(2, seed=3)
+    phi0 = O.rasterize_seeds([np.array([[4., 4.], [60., 4.], [60., 68.], [4., 68.]])], 1, 64, 72)
+    p = O.OracleParams(model="region", dt=15.0, sigma2=1.0, ts_reg=9, max_iters=30,
+                       conv_check_every=31)
+    out = []
+    for n in (1, 4):
+        OC.set_threads(n)
+        r = OC.COracleRun(bands, phi0, p, O.gaussian_weights)
+        r.advance(30)
+        out.append(r.phi.copy())
+    OC.set_threads(0)
+    assert np.array_equal(out[0], out[1])
