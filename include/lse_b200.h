@@ -172,6 +172,12 @@ int lse_run_set_profiling(lse_run* run, int enabled);
 int lse_run_kernel_times(lse_run* run, double* update_ms, long long* update_launches,
                          double* partition_ms, long long* partition_launches);
 
+/* Speculative fused iterations (single tiled region / zhang runs; the
+ * library's own execution strategy, invisible in the results): out[4] =
+ * {fused iterations launched, of which redone whole, pixels decided from the
+ * fix list, fused path enabled (0/1)}.  LSE_FUSED=0 at creation disables it. */
+int lse_run_spec_stats(lse_run* run, long long* out4);
+
 void lse_run_destroy(lse_run* run);
 
 /* ---- batched tiles -----------------------------------------

@@ -15,6 +15,7 @@
 #include <atomic>
 #include <climits>
 #include <cmath>
+#include <cstddef>
 #include <cstdio>
 #include <cstring>
 #include <string>
@@ -254,7 +255,9 @@ struct lse_run {
   bool prof = false;
   std::vector<cudaEvent_t> evpool;
   size_t evused = 0;
-  struct EvRec { cudaEvent_t e0, e1, e2; bool part; };
+  // e0..e1 an update (upd), e1..e2 a partition + finalize (part); a fused
+  // iteration records its pass as the update and finalize + fix as the rest
+  struct EvRec { cudaEvent_t e0, e1, e2; bool upd, part; };
   std::vector<EvRec> evrec;
   double t_update = 0, t_part = 0;
   long long n_update = 0, n_part = 0;
@@ -280,6 +283,11 @@ struct lse_run {
   TilePartial* strip_out = nullptr;
   bool strip_part = false, strip_ckpt = false;   // phases owed by the last update
   cudaEvent_t pev[2] = {nullptr, nullptr};       // profiling events of the pending update
+  // speculative fused iteration (k_update_fused): eligible runs, fix list
+  bool fused = false;
+  int2* d_fix = nullptr;
+  unsigned int fix_cap = 0;
+  long long fused_iters = 0;
 };
 
 namespace {
@@ -587,7 +595,7 @@ int launch_partition(lse_run* r, FastParams P) {
     if (fine_cta_parts(r) && !is_bands(r)) {
       PartRanges RF{{r->d_part, r->d_part, r->d_part}, {(int)n, 0, 0}};
       TRY(launch_pdl(k_finalize_run, 1, 64, r->st, RF, r->d_scal, PART ? 1 : 0, CKPT ? 1 : 0,
-                     (long long)P.iter));
+                     (long long)P.iter, 0));
       return LSE_OK;
     }
   } else {
@@ -608,7 +616,7 @@ int launch_partition(lse_run* r, FastParams P) {
     if (!is_bands(r) && !r->strip && n <= r->onestage_max) {
       // few partials (small images): a single-stage finalize, one launch less
       TRY(launch_pdl(k_finalize_run, 1, 64, r->st, R3, r->d_scal, PART ? 1 : 0, CKPT ? 1 : 0,
-                     (long long)P.iter));
+                     (long long)P.iter, 0));
       return LSE_OK;
     }
     if (!is_bands(r)) {
@@ -626,7 +634,7 @@ int launch_partition(lse_run* r, FastParams P) {
       k_reduce_to_one<<<1, 256, 0, r->st>>>(R1, r->strip_out, r->d_scal, 1);
     } else {
       TRY(launch_pdl(k_finalize_run, 1, 64, r->st, R1, r->d_scal, PART ? 1 : 0, CKPT ? 1 : 0,
-                     (long long)P.iter));
+                     (long long)P.iter, 0));
     }
     CKL();
   }
@@ -661,7 +669,13 @@ int launch_fast_R(lse_run* r, long long it, bool ckpt, int phase) {
     r->launched.emplace_back(it, r->cur);
     r->strip_part = MODEL == REGION || ckpt;
     r->strip_ckpt = ckpt;
-    if (phase == PH_UPDATE) return LSE_OK;
+    if (phase == PH_UPDATE) {
+      if (r->prof) r->evrec.push_back({r->pev[0], r->pev[1], r->pev[1], true, false});
+      return LSE_OK;
+    }
+  } else if (r->prof) {
+    r->pev[0] = r->pev[1] = next_event(r);       // partition phase alone
+    cudaEventRecord(r->pev[1], r->st);
   }
   P.bits_in = r->d_bits[r->cur];
   bool launched_part = false;
@@ -676,7 +690,7 @@ int launch_fast_R(lse_run* r, long long it, bool ckpt, int phase) {
   if (r->prof) {
     cudaEvent_t e2 = next_event(r);
     cudaEventRecord(e2, r->st);
-    r->evrec.push_back({r->pev[0], r->pev[1], e2, launched_part});
+    r->evrec.push_back({r->pev[0], r->pev[1], e2, phase != PH_PARTITION, launched_part});
   }
   return LSE_OK;
 }
@@ -696,6 +710,72 @@ int launch_fast(lse_run* r, long long it, bool ckpt, int phase = PH_BOTH) {
   // the mean-separation model differs only in its finalize coefficients
   if (two_mean(r->p.model)) return launch_fast_model<REGION>(r, it, ckpt, phase);
   return launch_fast_model<EDGE>(r, it, ckpt, phase);
+}
+
+// One speculative fused iteration (lse_fast.cuh, k_update_fused): the
+// partition of the current state b^{it-1} (its checkpoint when ckpt_prev)
+// and the update it-1 -> it in one pass, then the finalize of iteration it-1
+// (true coefficients of update it, prediction check) and k_spec_fix (fix list
+// or full redo).  Only after an update whose partition is still owed.
+template <int R>
+int launch_fused_R(lse_run* r, long long it, bool ckpt_prev) {
+  FastParams P = fast_params(r);
+  P.iter = it - 1;
+  set_check(P, it);
+  P.bits_in = r->d_bits[r->cur];
+  P.bits_out = r->d_bits[r->cur ^ 1];
+  P.fix = r->d_fix;
+  P.fix_cap = r->fix_cap;
+  P.fix_par = (int)(it & 1);
+  const long long n = r->nb_upd[0] + r->ni_upd;
+  const int g = fast_grid(n, kUpdateCtasPerSm);
+  P.work_base = take_work(r, n, g);
+  cudaEvent_t e0 = nullptr, e1 = nullptr;
+  if (r->prof) {
+    e0 = next_event(r);
+    e1 = next_event(r);
+    cudaEventRecord(e0, r->st);
+  }
+  if (ckpt_prev) TRY(launch_pdl(k_update_fused<R, true>, g, kThreads, r->st, P));
+  else TRY(launch_pdl(k_update_fused<R, false>, g, kThreads, r->st, P));
+  if (r->prof) cudaEventRecord(e1, r->st);
+  PartRanges R3{{r->d_part, r->d_part, r->d_part}, {(int)n, 0, 0}};
+  const int spec = 1 + P.fix_par;
+  if (n <= r->onestage_max) {
+    TRY(launch_pdl(k_finalize_run, 1, 64, r->st, R3, r->d_scal, 1, ckpt_prev ? 1 : 0, it - 1,
+                   spec));
+  } else {
+    TRY(launch_pdl(k_finalize_stage1, kFinSlices, 256, r->st, R3, r->d_part_fin,
+                   (const Scalars*)r->d_scal));
+    PartRanges R1{{r->d_part_fin, r->d_part_fin, r->d_part_fin}, {kFinSlices, 0, 0}};
+    TRY(launch_pdl(k_finalize_run, 1, 64, r->st, R1, r->d_scal, 1, ckpt_prev ? 1 : 0, it - 1,
+                   spec));
+  }
+  FastParams Q = P;                              // the redo pass has its own work counter
+  Q.work = &r->d_scal->work2;
+  Q.work_base = 0;
+  TRY(launch_pdl(k_spec_fix<R>, g, kThreads, r->st, Q));
+  if (r->prof) {
+    cudaEvent_t e2 = next_event(r);
+    cudaEventRecord(e2, r->st);
+    r->evrec.push_back({e0, e1, e2, true, true});
+  }
+  r->cur ^= 1;
+  r->mode = SRC_SMOOTH;
+  r->field_valid = false;
+  r->launched.emplace_back(it, r->cur);
+  r->fused_iters++;
+  return LSE_OK;
+}
+
+int launch_fused(lse_run* r, long long it, bool ckpt_prev) {
+  switch (r->R) {
+    case 1: return launch_fused_R<1>(r, it, ckpt_prev);
+    case 2: return launch_fused_R<2>(r, it, ckpt_prev);
+    case 3: return launch_fused_R<3>(r, it, ckpt_prev);
+    case 4: return launch_fused_R<4>(r, it, ckpt_prev);
+  }
+  return fail(LSE_ERR_ARG, "unsupported template radius");
 }
 
 // wait for the device, fold profiling events, detect convergence
@@ -718,9 +798,11 @@ int collect(lse_run* r) {
   if (r->prof) {
     for (auto& e : r->evrec) {
       float ms = 0.f;
-      cudaEventElapsedTime(&ms, e.e0, e.e1);
-      r->t_update += ms;
-      r->n_update++;
+      if (e.upd) {
+        cudaEventElapsedTime(&ms, e.e0, e.e1);
+        r->t_update += ms;
+        r->n_update++;
+      }
       if (e.part) {
         cudaEventElapsedTime(&ms, e.e1, e.e2);
         r->t_part += ms;
@@ -1356,8 +1438,28 @@ int create_impl(lse_run** out, const lse_params* p, long long height, long long 
     // changes it per run); LSE_SKIP_UNIFORM=0 makes every new run dense
     if (const char* sv = std::getenv("LSE_SKIP_UNIFORM")) r->skip_uniform = std::atoi(sv) != 0;
   }
+  // speculative fused iterations (one pass per iteration): single tiled runs
+  // of the region / zhang models with unsplit update units; LSE_FUSED=0 keeps
+  // the two-pass iteration (A/B); validation builds check the two-pass path
+  {
+    bool fz = !r->strip && !r->fine && r->split_parts == 1 && r->R >= 1 && r->R <= 4 &&
+              (p->model == LSE_MODEL_REGION || p->model == LSE_MODEL_ZHANG);
+#ifdef LSE_CHECK_BOUND
+    fz = false;
+#endif
+    if (const char* fv = std::getenv("LSE_FUSED")) fz = fz && std::atoi(fv) != 0;
+    r->fused = fz;
+    // fix list: pixels in the speculative band (a tiny fraction near the
+    // fronts); more than this and the iteration is redone instead
+    r->fix_cap = fz ? (unsigned)std::min<long long>(std::max<long long>(r->npx / 256, 4096),
+                                                    1LL << 22)
+                    : 0u;
+    if (const char* cv = std::getenv("LSE_FIX_CAP"))   // (tests: force the redo pass)
+      if (fz) r->fix_cap = (unsigned)std::max(0LL, std::atoll(cv));
+  }
   const long long nparts = std::max<long long>(
-      std::max<long long>(r->g.ntiles, r->ni_part + r->nb_part),
+      std::max<long long>(std::max<long long>(r->g.ntiles, r->ni_part + r->nb_part),
+                          r->fused ? r->nb_upd[0] + r->ni_upd : 0LL),
       r->fine ? fine_parts(r) : 0LL);
   auto cleanup = [&](int rc) {
     lse_run_destroy(r);
@@ -1378,6 +1480,7 @@ int create_impl(lse_run** out, const lse_params* p, long long height, long long 
       (rc = dalloc(&r->d_part_fin, kFinSlices)) ||
       (rc = dalloc(&r->d_part_init, (size_t)r->g.HR * ((r->g.pitch_w + 1023) / 1024))))
     return cleanup(rc);
+  if (r->fused && (rc = dalloc(&r->d_fix, r->fix_cap))) return cleanup(rc);
   if (p->model == LSE_MODEL_BANDS &&
       ((rc = dalloc(&r->d_bands32, (size_t)p->n_bands * r->g.data_pitch * r->H)) ||
        (rc = dalloc(&r->d_chg, nbits)) ||
@@ -1441,6 +1544,8 @@ int create_impl(lse_run** out, const lse_params* p, long long height, long long 
   s0.conv_window = p->conv_window;
   s0.eps_phi = (float)kEpsPhi;
   s0.eps_u = (float)edge_eps_u(p->dt);
+  s0.spec_delta = -1.0f;
+  s0.fix_cap = r->fix_cap;
   if (p->model == LSE_MODEL_EDGE) s0.A = 1.0f;   // vf = 1 * g + 0 in a batched launch
   if (cudaMemcpyAsync(r->d_scal, &s0, sizeof(s0), cudaMemcpyHostToDevice, r->st) != cudaSuccess)
     return cleanup(fail(LSE_ERR_CUDA, "scalar upload failed"));
@@ -1555,7 +1660,7 @@ int lse_strip_finalize(lse_run* r, const void* parts, int nparts, int absolute) 
   if (!r->strip_part) return LSE_OK;
   PartRanges R{{tp, tp, tp}, {nparts, 0, 0}};
   k_finalize_run<<<1, 64, 0, r->st>>>(R, r->d_scal, two_mean(r->p.model) ? 1 : 0,
-                                        r->strip_ckpt ? 1 : 0, r->iteration);
+                                        r->strip_ckpt ? 1 : 0, r->iteration, 0);
   CKL();
   r->strip_part = false;
   return LSE_OK;
@@ -1611,17 +1716,36 @@ int lse_run_advance(lse_run* r, long long n_steps, lse_status* st) {
   CK(cudaMemsetAsync(r->d_work, 0, sizeof(unsigned long long), r->st));
   r->work_next = 0;
   const long long it0 = r->iteration;
+  const long long cce = r->p.conv_check_every;
   bool pending = false;
+  // fused runs: the partition of the last update's output is owed to the next
+  // pass (a fused iteration) or to the trailing partition phase
+  bool owe = false;
+  long long owe_it = 0;
+  if (r->fused)
+    CK(cudaMemsetAsync(reinterpret_cast<char*>(r->d_scal) + offsetof(Scalars, fix_n), 0,
+                       sizeof(unsigned int) * 2, r->st));
   for (long long it = it0 + 1; it <= it0 + steps; ++it) {
     const bool reinit_now = r->p.reinit_period > 0 && it % r->p.reinit_period == 0;
     const bool reg_now = it % r->p.reg_period == 0;
     const bool ckpt = it % r->p.conv_check_every == 0;
     if (reinit_now && reg_now && r->mode != SRC_FIELD && fp32_ok(r)) {
-      TRY(launch_fast(r, it, ckpt));
+      if (r->fused) {
+        if (owe) TRY(launch_fused(r, it, owe_it % cce == 0));
+        else TRY(launch_fast(r, it, ckpt, PH_UPDATE));
+        owe = true;
+        owe_it = it;
+      } else {
+        TRY(launch_fast(r, it, ckpt));
+      }
       r->iteration = it;
       r->fast_iters++;
       pending = true;
     } else {
+      if (owe) {
+        TRY(launch_fast(r, owe_it, owe_it % cce == 0, PH_PARTITION));
+        owe = false;
+      }
       if (pending) {
         TRY(collect(r));
         pending = false;
@@ -1639,6 +1763,7 @@ int lse_run_advance(lse_run* r, long long n_steps, lse_status* st) {
       if (r->converged) break;
     }
   }
+  if (owe) TRY(launch_fast(r, owe_it, owe_it % cce == 0, PH_PARTITION));
   if (pending) TRY(collect(r));
   fill_status(r, st, -1);
   return LSE_OK;
@@ -1776,6 +1901,17 @@ int lse_run_end_timing(lse_run* r, double* ms) {
   float f = 0.f;
   CK(cudaEventElapsedTime(&f, r->t_begin, r->t_end));
   *ms = f;
+  return LSE_OK;
+}
+
+int lse_run_spec_stats(lse_run* r, long long* out4) {
+  if (!r || !out4) return fail(LSE_ERR_ARG, "null argument");
+  CK(cudaMemcpyAsync(r->h_scal, r->d_scal, sizeof(Scalars), cudaMemcpyDeviceToHost, r->st));
+  CK(cudaStreamSynchronize(r->st));
+  out4[0] = r->fused_iters;
+  out4[1] = (long long)r->h_scal->spec_redos;
+  out4[2] = (long long)r->h_scal->spec_fixes;
+  out4[3] = r->fused ? 1 : 0;
   return LSE_OK;
 }
 
@@ -2167,7 +2303,8 @@ void lse_run_destroy(lse_run* r) {
                   r->d_bands32, r->d_bands64, r->d_chg, r->d_bpart, r->d_pmax, r->d_lut64,
                   r->d_work, r->d_part_fin, r->d_part_init, r->d_data32, r->d_data64, r->d_bits[0], r->d_bits[1], r->d_P, r->d_M,
                   r->d_mask, r->d_part, r->d_scal, r->d_lut_t, r->d_lut_s, r->d_ctx,
-                  r->d_w64, r->d_keys, r->d_count, r->d_F[0], r->d_F[1], r->d_U, r->d_T};
+                  r->d_w64, r->d_keys, r->d_count, r->d_F[0], r->d_F[1], r->d_U, r->d_T,
+                  r->d_fix};
   for (void* q : ptrs)
     if (q) cudaFree(q);
   if (r->h_scal) cudaFreeHost(r->h_scal);

@@ -52,7 +52,18 @@ struct __align__(16) Scalars {
   long long conv_window;
   double dt;
   int model;
-  int pad_;
+  // speculative fused iteration (k_update<..., FUSED>): the update of
+  // iteration n runs with the coefficients of iteration n-1 while the same
+  // pass computes the partition that defines iteration n's own; every pixel
+  // with |u| - spec_delta * h <= spec_e0 goes to the fix list and is decided
+  // exactly once the true coefficients are known (k_spec_fix), or the whole
+  // update is redone when the coefficients moved more than spec_delta
+  int redo;                           // the last speculative update must be redone
+  float spec_delta, spec_e0;          // flag band of the next speculative update (delta < 0: none)
+  unsigned int fix_n[2];              // fix-list entries of the speculative update (by parity)
+  unsigned int fix_cap;               // fix-list capacity
+  unsigned long long work2;           // work counter of the redo pass
+  unsigned long long spec_redos, spec_fixes;   // statistics
 };
 
 // Per-tile partial (fixed tile geometry => deterministic, GPU-count independent

@@ -89,6 +89,11 @@ struct FastParams {
   long long tile_words, tile_data;
   CheckSlot* chk;            // validation builds: per-thread certification slots (or null)
   long long chk_cap;
+  // speculative fused iteration: pixels whose decision waits for the true
+  // coefficients, (x, row) pairs; entries counted in scal->fix_n[fix_par]
+  int2* fix;
+  unsigned int fix_cap;
+  int fix_par;
 };
 
 // exact-path frame of tile t (its context, state and first image row)
@@ -430,6 +435,35 @@ __device__ __forceinline__ void load_data_row(const FastParams& P, int i, int x0
   }
 }
 
+#ifndef LSE_FUSED_PREFETCH
+#define LSE_FUSED_PREFETCH 0
+#endif
+// codegen knobs of the fused loop (A/B builds)
+#ifndef LSE_LUT_EXPLICIT
+#define LSE_LUT_EXPLICIT 0
+#endif
+#ifndef LSE_TIE_PARAM
+#define LSE_TIE_PARAM 1
+#endif
+#if LSE_TIE_PARAM
+#define LSE_TIE_P P
+#else
+#define LSE_TIE_P Pn
+#endif
+#ifndef LSE_PAIR_MIN
+#define LSE_PAIR_MIN 1
+#endif
+__device__ __forceinline__ void prefetch_l1(const void* p) {
+  asm volatile("prefetch.global.L1 [%0];" ::"l"(p));
+}
+
+// three-input minimum (FMNMX3, sm_100+)
+__device__ __forceinline__ float fmin3(float a, float b, float c) {
+  float r;
+  asm("min.f32 %0, %1, %2, %3;" : "=f"(r) : "f"(a), "f"(b), "f"(c));
+  return r;
+}
+
 __device__ __forceinline__ float sqrt_approx(float x) {
   float y;
   asm("sqrt.approx.ftz.f32 %0, %1;" : "=f"(y) : "f"(x));
@@ -549,8 +583,14 @@ __device__ __forceinline__ void phi_rows2_int(const FastParams& P, const uint32_
   }
 #pragma unroll
   for (int j = 0; j < NT; ++j) {
+#if LSE_LUT_EXPLICIT
+    uint32_t tb;
+    asm("mov.u32 %0, _ZN3lse10g_pair_lutE;" : "=r"(tb));   // the table's shared address
+    const float2 t = lds_f32x2(tb + ((win8[j] >> m0) & PM8));
+#else
     const float2 t = *reinterpret_cast<const float2*>(
         reinterpret_cast<const char*>(g_pair_lut) + ((win8[j] >> m0) & PM8));
+#endif
 #pragma unroll
     for (int c = 0; c < NOUT; ++c) {
       const int d = j - c - R;
@@ -567,9 +607,10 @@ __device__ __forceinline__ void phi_rows2_int(const FastParams& P, const uint32_
 // fp32 values with exactly the loop's operations -- phi_rows2_int's packed
 // lanes are independent FMAs, so a row's values do not depend on which row
 // it was paired with -- and return the columns that need the fp64 decision.
-template <int R, int MODEL, int CPL, int SRC>
+template <int R, int MODEL, int CPL, int SRC, bool SPEC = false>
 __device__ __noinline__ uint32_t update_tie_cols(const FastParams& P, uint32_t lut_base, int r,
-                                                 int x0, int k, float A, float B, float eps_u) {
+                                                 int x0, int k, float A, float B, float eps_u,
+                                                 float delta = 0.f) {
   constexpr int NT = CPL + 2 * (R + 1);
   constexpr int NP = CPL + 2;
   const int y0 = r * 32;
@@ -592,12 +633,22 @@ __device__ __noinline__ uint32_t update_tie_cols(const FastParams& P, uint32_t l
     const float d = __ldg(drow + c);
     const float vf = (MODEL == REGION) ? __fmaf_rn(A, d, B) : d;
     const float u = __fmaf_rn(vf, h, pa[c + 1].y);
-    if (fabsf(u) <= eps_u) cols |= 1u << c;
+    // SPEC: the speculative band |u| - delta h <= e0 (eps_u holds e0), the
+    // fused loop's test on the same values
+    if ((SPEC ? __fmaf_rn(-delta, h, fabsf(u)) : fabsf(u)) <= eps_u) cols |= 1u << c;
   }
-  return cols ? cols : (1u << CPL) - 1u;         // (all columns if nothing matched)
+  // (all columns if nothing matched; SPEC callers flag row pairs, so a row
+  // may legitimately have no match there)
+  return (cols || SPEC) ? cols : (1u << CPL) - 1u;
 }
 
-template <int R>
+// a pixel whose speculative decision waits for the true coefficients
+__device__ __forceinline__ void spec_append(const FastParams& P, int i, int x) {
+  const unsigned q = atomicAdd(&P.scal->fix_n[P.fix_par], 1u);
+  if (q < P.fix_cap) P.fix[q] = make_int2(x, i);
+}
+
+template <int R, bool EXACT = false>
 __device__ __noinline__ uint32_t partition_tie_cols(const FastParams& P, uint32_t lut_base, int r,
                                                     int x0, int k, float eps_phi) {
   constexpr int NT = kColsPerThread + 2 * R;
@@ -613,20 +664,31 @@ __device__ __noinline__ uint32_t partition_tie_cols(const FastParams& P, uint32_
 #pragma unroll
   for (int c = 0; c < 8; ++c)
     if (fabsf(ph[c].x) <= eps_phi) cols |= 1u << c;
-  return cols ? cols : 0xffu;
+  return (cols || EXACT) ? cols : 0xffu;        // EXACT: row pairs flagged (fused pass)
 }
 
 constexpr int kRing2 = 8;                       // data rows buffered per warp (2-row steps)
 
 // Interior update block, two rows per step (see update_block_int for the
 // design); phi rows are kept as (row, row+1) pairs.
-template <int R, int MODEL, int CPL, int SRC>
+//
+// FUSED (the speculative fused iteration, single runs): the same pass also
+// yields the partition of its input state -- the centre values pp.y / pn.x
+// are phi^n itself -- as pw (phi >= 0) / mw (phi > 0) words, near ties
+// resolved exactly; the update's coefficients are a prediction, so instead of
+// the eps_u guard every pixel with |u| - delta h <= eps_u (eps_u then holds
+// the band's e0) goes to the fix list (spec_append), decided by k_spec_fix.
+template <int R, int MODEL, int CPL, int SRC, bool FUSED = false>
 __device__ __forceinline__ void update_block_int2(const FastParams& P, uint32_t lut_base,
                                                   float* ring, int r, int x0, float A, float B,
                                                   float eps_u,
                                                   const uint32_t (&prev)[CPL + 2 * (R + 1)],
                                                   const uint32_t (&cur)[CPL + 2 * (R + 1)],
-                                                  int tile) {
+                                                  int tile, float delta, uint32_t (&pw)[CPL],
+                                                  uint32_t (&mw)[CPL], const FastParams& Pn) {
+  // Pn: the launch parameters as seen by the noinline tie helpers (the CTA's
+  // shared copy: passing the kernel parameter block by reference to a noinline
+  // function makes every thread copy it to local memory first)
   constexpr int NT = CPL + 2 * (R + 1);
   constexpr int NP = CPL + 2;
   constexpr uint32_t kSlot = 32 * CPL * 4;
@@ -650,9 +712,13 @@ __device__ __forceinline__ void update_block_int2(const FastParams& P, uint32_t 
   }
   float2 pp[NP], pn[NP];
   uint32_t ow[CPL];
-  uint32_t fbrows = 0u;
+  uint32_t fbrows = 0u, pfrows = 0u;
 #pragma unroll
   for (int c = 0; c < CPL; ++c) ow[c] = 0u;
+  if (FUSED) {
+#pragma unroll
+    for (int c = 0; c < CPL; ++c) pw[c] = 0u;
+  }
   phi_rows2_int<R, NT, NP, SRC>(P, win4, 0, lut_base, pp);     // rows -1, 0
   const uint32_t* wrow = P.bits_in + (size_t)r * P.g.pitch_w + (x0 - (R + 1));
 #pragma unroll 2
@@ -691,7 +757,7 @@ __device__ __forceinline__ void update_block_int2(const FastParams& P, uint32_t 
         d1[4 * v] = q1.x; d1[4 * v + 1] = q1.y; d1[4 * v + 2] = q1.z; d1[4 * v + 3] = q1.w;
       }
     }
-    float umin0 = 3.0e38f, umin1 = 3.0e38f;
+    float umin0 = 3.0e38f, umin1 = 3.0e38f, pmin0 = 3.0e38f;
 #pragma unroll
     for (int c = 0; c < CPL; ++c) {
       // rows 2s (centre pp.y) and 2s+1 (centre pn.x); dy = phi(k+1) - phi(k-1)
@@ -705,15 +771,40 @@ __device__ __forceinline__ void update_block_int2(const FastParams& P, uint32_t 
       const float u1 = fmaf(vf1, h1, pn[c + 1].x);
       ow[c] = __funnelshift_l(__float_as_uint(u0), ow[c], 1);
       ow[c] = __funnelshift_l(__float_as_uint(u1), ow[c], 1);
-      umin0 = fminf(umin0, fabsf(u0));
-      umin1 = fminf(umin1, fabsf(u1));
-      LSE_CHECK_U(R, SRC, P, tile_ctx(P, tile), tile_bits(P, tile),
-                  y0 - tile_y0(P, tile) + 2 * s, x0 + c, u0, eps_u);
-      LSE_CHECK_U(R, SRC, P, tile_ctx(P, tile), tile_bits(P, tile),
-                  y0 - tile_y0(P, tile) + 2 * s + 1, x0 + c, u1, eps_u);
+      if (FUSED) {
+        pw[c] = __funnelshift_l(__float_as_uint(pp[c + 1].y), pw[c], 1);
+        pw[c] = __funnelshift_l(__float_as_uint(pn[c + 1].x), pw[c], 1);
+#if LSE_PAIR_MIN
+        // one minimum per row pair (three-input FMNMX): the pair's rows are
+        // then searched column by column (exact matches only)
+        umin0 = fmin3(umin0, fmaf(-delta, h0, fabsf(u0)), fmaf(-delta, h1, fabsf(u1)));
+        pmin0 = fmin3(pmin0, fabsf(pp[c + 1].y), fabsf(pn[c + 1].x));
+#else
+        umin0 = fminf(umin0, fmaf(-delta, h0, fabsf(u0)));
+        umin1 = fminf(umin1, fmaf(-delta, h1, fabsf(u1)));
+        pmin0 = fminf(pmin0, fminf(fabsf(pp[c + 1].y), fabsf(pn[c + 1].x)));
+#endif
+      } else {
+        umin0 = fminf(umin0, fabsf(u0));
+        umin1 = fminf(umin1, fabsf(u1));
+        LSE_CHECK_U(R, SRC, P, tile_ctx(P, tile), tile_bits(P, tile),
+                    y0 - tile_y0(P, tile) + 2 * s, x0 + c, u0, eps_u);
+        LSE_CHECK_U(R, SRC, P, tile_ctx(P, tile), tile_bits(P, tile),
+                    y0 - tile_y0(P, tile) + 2 * s + 1, x0 + c, u1, eps_u);
+      }
     }
-    if (umin0 <= eps_u) fbrows |= 1u << (2 * s);
-    if (umin1 <= eps_u) fbrows |= 2u << (2 * s);
+    if (FUSED) {
+#if LSE_PAIR_MIN
+      if (umin0 <= eps_u) fbrows |= 3u << (2 * s);
+#else
+      if (umin0 <= eps_u) fbrows |= 1u << (2 * s);
+      if (umin1 <= eps_u) fbrows |= 2u << (2 * s);
+#endif
+      if (pmin0 <= P.scal->eps_phi) pfrows |= 3u << (2 * s);
+    } else {
+      if (umin0 <= eps_u) fbrows |= 1u << (2 * s);
+      if (umin1 <= eps_u) fbrows |= 2u << (2 * s);
+    }
 #pragma unroll
     for (int c = 0; c < NP; ++c) pp[c] = pn[c];
   }
@@ -724,15 +815,45 @@ __device__ __forceinline__ void update_block_int2(const FastParams& P, uint32_t 
     const int k = __ffs(fbrows) - 1;
     fbrows &= fbrows - 1;
     const uint32_t bitk = 1u << k;
-    uint32_t cols = update_tie_cols<R, MODEL, CPL, SRC>(P, lut_base, r, x0, k, A, B, eps_u);
+    uint32_t cols =
+        update_tie_cols<R, MODEL, CPL, SRC, FUSED>(LSE_TIE_P, lut_base, r, x0, k, A, B, eps_u, delta);
     while (cols) {
       const int c = __ffs(cols) - 1;
       cols &= cols - 1;
+      if (FUSED) {
+        spec_append(P, y0 + k, x0 + c);           // decided by k_spec_fix
+        continue;
+      }
       const bool pos = exact_u_fast<R, SRC>(tile_ctx(P, tile), tile_bits(P, tile),
                                             y0 - tile_y0(P, tile) + k, x0 + c) > 0.0;
 #pragma unroll
       for (int q = 0; q < CPL; ++q)
         if (q == c) ow[q] = pos ? (ow[q] | bitk) : (ow[q] & ~bitk);
+    }
+  }
+  if (FUSED) {
+    // partition of the input state: bit k = phi_k >= +0 off ties, then the
+    // exact signs of the tie columns (as partition_block)
+#pragma unroll
+    for (int c = 0; c < CPL; ++c) mw[c] = pw[c] = ~__brev(pw[c]);
+    const float eps_phi = P.scal->eps_phi;
+    while (pfrows) {
+      const int k = __ffs(pfrows) - 1;
+      pfrows &= pfrows - 1;
+      const uint32_t bitk = 1u << k;
+      uint32_t cols = partition_tie_cols<R, true>(LSE_TIE_P, lut_base, r, x0, k, eps_phi);
+      while (cols) {
+        const int c = __ffs(cols) - 1;
+        cols &= cols - 1;
+        const double e = exact_phi_fast<R>(P.ctx, P.bits_in, y0 + k, x0 + c);
+#pragma unroll
+        for (int q = 0; q < CPL; ++q) {
+          if (q == c) {
+            pw[q] = e >= 0.0 ? (pw[q] | bitk) : (pw[q] & ~bitk);
+            mw[q] = e > 0.0 ? (mw[q] | bitk) : (mw[q] & ~bitk);
+          }
+        }
+      }
     }
   }
   uint32_t* dst = P.bits_out + (size_t)r * P.g.pitch_w + x0;
@@ -917,11 +1038,13 @@ __device__ __forceinline__ int grab_unit(const FastParams& P, int lane) {
 // Border rows k0 .. k0 + nrows - 1 of the lane block (r, x0): zero
 // padding / one-sided gradients (update_block's arithmetic on a row range).
 // ow[c] gets bit k for the rows of the range only.
-template <int R, int MODEL, int SRC, int CPL>
+// FUSED: eps_u holds the speculative band's e0; flagged pixels go to the fix
+// list instead of the exact path (see update_block_int2).
+template <int R, int MODEL, int SRC, int CPL, bool FUSED = false>
 __device__ __forceinline__ void update_rows_border(const FastParams& P, const float* s_lt,
                                                    const float* s_ls, int r, int x0, int k0,
                                                    int nrows, float A, float B, float eps_u,
-                                                   uint32_t (&ow)[CPL]) {
+                                                   uint32_t (&ow)[CPL], float delta = 0.f) {
   constexpr int NT = CPL + 2 * (R + 1);
   constexpr int NP = CPL + 2;
   const int H = P.g.H, W = P.g.W;
@@ -964,8 +1087,8 @@ __device__ __forceinline__ void update_rows_border(const FastParams& P, const fl
         const float vf = (MODEL == REGION) ? fmaf(A, dcur[c], B) : dcur[c];
         const float u = fmaf(vf, h, p0[c + 1]);
         if (u > 0.f) ow[c] |= bitk;
-        if (fabsf(u) <= eps_u) fb |= 1u << c;
-        LSE_CHECK_U(R, SRC, P, P.ctx, P.bits_in, y0 + k, x, u, eps_u);
+        if ((FUSED ? fmaf(-delta, h, fabsf(u)) : fabsf(u)) <= eps_u) fb |= 1u << c;
+        if (!FUSED) LSE_CHECK_U(R, SRC, P, P.ctx, P.bits_in, y0 + k, x, u, eps_u);
       }
       if (fb) fbrows |= bitk;
     }
@@ -981,6 +1104,10 @@ __device__ __forceinline__ void update_rows_border(const FastParams& P, const fl
 #pragma unroll 1
     for (int c = 0; c < CPL; ++c) {
       if (x0 + c >= W) break;
+      if (FUSED) {                               // (the whole flagged row: a superset)
+        spec_append(P, y0 + k, x0 + c);
+        continue;
+      }
       const bool pos = exact_u_fast<R, SRC>(P.ctx, P.bits_in, y0 + k, x0 + c) > 0.0;
 #pragma unroll
       for (int q = 0; q < CPL; ++q)
@@ -1060,32 +1187,16 @@ __device__ __noinline__ void border_update_unit(const FastParams& P, const float
 // the tile's scalars (stop, A, B, guards) are read per unit.
 // NS > 1: split-warp units of 256/NS columns (update_block_split) for small
 // images.
+// The unit loop of k_update (also the redo pass of k_spec_fix): the launch's
+// units are grabbed from P.work until exhausted.
 template <int R, int MODEL, int SRC, bool BATCH, int NS>
-__global__ void __launch_bounds__(kThreads, kUpdateCtasPerSm) k_update(FastParams P) {
+__device__ __forceinline__ void update_units(const FastParams& P, const FastParams& s_P,
+                                             const SharedLuts& luts, const float* s_lt,
+                                             const float* s_ls, float* s_ring) {
   constexpr int CPL = kUpdCols;
   constexpr int NT = CPL + 2 * (R + 1);
-  constexpr int NPAT = 1 << (2 * R + 1);
-  __shared__ float s_lt[NPAT];
-  __shared__ float s_ls[NPAT];
-  __shared__ __align__(16) float s_ring[(kThreads / 32) * kRing2 * 32 * CPL];
   LSE_TRACE_ENTRY
-  // the noinline border path reads the launch parameters from this shared
-  // copy: handing it the kernel parameter block itself would force a
-  // per-thread local-memory copy of the block (taking its address)
-  __shared__ FastParams s_P;
-  const SharedLuts luts{s_lt, s_ls, (uint32_t)__cvta_generic_to_shared(g_pair_lut)};
-  load_luts<R>(P, luts);                         // static data: before the dependency wait
-  if (threadIdx.x == 0) s_P = P;
-  __syncthreads();
-  pdl_wait();
-  pdl_launch_dependents();
   const Scalars* sc = P.scal;
-  if (!BATCH && stop_flag(sc)) return;
-  if (MODEL == REGION && blockIdx.x == 0) {      // sticky degenerate (engine.py:239-240)
-    for (int t = threadIdx.x; t < (BATCH ? P.ntiles : 1); t += blockDim.x)
-      if (P.scal[t].zero_vel && !P.scal[t].stop && P.scal[t].model != EDGE)
-        P.scal[t].degenerate = 1;
-  }
   float A = sc->A, B = sc->B, eps_u = sc->eps_u;
   const int lane = threadIdx.x & 31;
   const int nb = border_units(P.gu);
@@ -1196,10 +1307,37 @@ __global__ void __launch_bounds__(kThreads, kUpdateCtasPerSm) k_update(FastParam
       continue;
     }
     if (!act) continue;
+    uint32_t npw[CPL], nmw[CPL];                  // (partition words: fused pass only)
     update_block_int2<R, MODEL, CPL, SRC>(P, luts.lt2,
                                           s_ring + (threadIdx.x >> 5) * kRing2 * 32 * CPL, r, x0,
-                                          A, B, eps_u, prev, cur, tile);
+                                          A, B, eps_u, prev, cur, tile, 0.f, npw, nmw, s_P);
   }
+}
+
+template <int R, int MODEL, int SRC, bool BATCH, int NS>
+__global__ void __launch_bounds__(kThreads, kUpdateCtasPerSm) k_update(FastParams P) {
+  constexpr int CPL = kUpdCols;
+  constexpr int NPAT = 1 << (2 * R + 1);
+  __shared__ float s_lt[NPAT];
+  __shared__ float s_ls[NPAT];
+  __shared__ __align__(16) float s_ring[(kThreads / 32) * kRing2 * 32 * CPL];
+  // the noinline border path reads the launch parameters from this shared
+  // copy: handing it the kernel parameter block itself would force a
+  // per-thread local-memory copy of the block (taking its address)
+  __shared__ FastParams s_P;
+  const SharedLuts luts{s_lt, s_ls, (uint32_t)__cvta_generic_to_shared(g_pair_lut)};
+  load_luts<R>(P, luts);                         // static data: before the dependency wait
+  if (threadIdx.x == 0) s_P = P;
+  __syncthreads();
+  pdl_wait();
+  pdl_launch_dependents();
+  if (!BATCH && stop_flag(P.scal)) return;
+  if (MODEL == REGION && blockIdx.x == 0) {      // sticky degenerate (engine.py:239-240)
+    for (int t = threadIdx.x; t < (BATCH ? P.ntiles : 1); t += blockDim.x)
+      if (P.scal[t].zero_vel && !P.scal[t].stop && P.scal[t].model != EDGE)
+        P.scal[t].degenerate = 1;
+  }
+  update_units<R, MODEL, SRC, BATCH, NS>(P, s_P, luts, s_lt, s_ls, s_ring);
 }
 
 // ------------------------------------------------------------- finalize
@@ -1330,8 +1468,44 @@ __device__ void reduce_slice(const PartRanges& R3, int t0, int t1, TilePartial* 
   }
 }
 
+// Check of a speculative update (spec = 1 + parity of its fix list) against
+// the coefficients just computed, and the flag band of the next one.
+// Not flagged means |u_g| - delta*h > e0 (the kernels' fp32 test is exact
+// enough: fl(|u| - delta h) > e0 implies |u| - delta h > e0).  With vf_g =
+// A' I + B' the kernel's, vf_t = A I + B the true coefficient of I, and
+// |vf_g - vf_t| <= |A - A'| max|I| + |B - B'| + 2^-23 max|vf| (two FMA
+// roundings), |u_g - u_t| <= |vf_g - vf_t| h + 2^-23 |u_g| (1 + tiny): so
+// delta (1 - 2^-20) >= (that bound) (1 + 2^-20) and e0 (1 - 2^-20) >= eps_u of
+// the true coefficients give |u_t| > eps_u with sign(u_t) = sign(u_g), i.e.
+// the unflagged decisions are the ones the non-speculative update makes.
+__device__ __forceinline__ void spec_check(Scalars* sc, float A0, float B0, float delta0, float e00,
+                                           int spec) {
+  const double am = sc->img_absmax * (1.0 + 0x1p-20);
+  const double A = sc->A, B = sc->B, a0 = A0, b0 = B0;
+  const double D = (fabs(A - a0) * am + fabs(B - b0)) * (1.0 + 0x1p-40);
+  const double vfm = fmax(fabs(A) * am + fabs(B), fabs(a0) * am + fabs(b0));
+  if (spec) {
+    const unsigned nfix = sc->fix_n[spec - 1];
+    const bool ok = nfix <= sc->fix_cap &&
+                    (double)delta0 * (1.0 - 0x1p-20) >= (D + 0x1p-22 * vfm) * (1.0 + 0x1p-20) &&
+                    (double)e00 * (1.0 - 0x1p-20) >= (double)sc->eps_u;
+    sc->redo = ok ? 0 : 1;
+    if (ok) {
+      sc->spec_fixes += nfix;
+    } else {
+      sc->spec_redos += 1;
+      sc->work2 = 0;
+    }
+  }
+  // next band: 4x the last move of the coefficients plus a floor; none when
+  // they still move by more than 1/8 of the velocity scale (early iterations)
+  const double nd = 4.0 * D + 0x1p-14 * vfm;
+  sc->spec_delta = nd <= vfm * 0x1p-3 ? (float)(nd * (1.0 + 0x1p-20)) : -1.0f;
+  sc->spec_e0 = (float)((double)sc->eps_u * 1.25);
+}
+
 __device__ void finalize_cta(const PartRanges& R3, Scalars* sc, bool delta, bool region,
-                             bool ckpt, long long iter) {
+                             bool ckpt, long long iter, int spec = 0) {
   const int n = R3.n[0] + R3.n[1] + R3.n[2];
   __shared__ double f_ah[32], f_al[32], f_bh[32], f_bl[32];
   __shared__ long long f_na[32], f_nb[32];
@@ -1402,6 +1576,7 @@ __device__ void finalize_cta(const PartRanges& R3, Scalars* sc, bool delta, bool
       smm += f_mm[w];
     }
     if (region) {
+      const float A0 = sc->A, B0 = sc->B, delta0 = sc->spec_delta, e00 = sc->spec_e0;
       if (delta) {
         dd_add_dd(sc->sp_hi, sc->sp_lo, sah, sal);
         dd_add_dd(sc->sp_hi, sc->sp_lo, -sbh, -sbl);
@@ -1414,6 +1589,7 @@ __device__ void finalize_cta(const PartRanges& R3, Scalars* sc, bool delta, bool
         sc->n_pos = sna;
       }
       region_coeffs(sc);
+      spec_check(sc, A0, B0, delta0, e00, spec);
     }
     if (ckpt) {                                    // engine.py:228-236
       sc->n_ckpt += 1;
@@ -1823,6 +1999,211 @@ __global__ void __launch_bounds__(kThreads, kPartitionCtasPerSm) k_partition(Fas
       t.mism = d.mism;
       P.part[unit] = t;
     }
+  }
+}
+
+
+// ------------------------------------------- speculative fused iteration
+// One pass per iteration instead of update + partition: k_update_fused reads
+// b^n, rebuilds phi^n once and from it derives both
+//   * the partition of iteration n (P bits, the c+/c- deltas, the checkpoint
+//     mask) -- exactly what k_partition computes from the same b^n, and
+//   * b^{n+1} with the coefficients of iteration n-1 as the prediction of
+//     iteration n's (the partition that defines them is being computed in
+//     the same pass).
+// The finalize then derives the true coefficients and checks the prediction
+// (spec_check): if it held, only the pixels in the flag band were undecided
+// and k_spec_fix decides them exactly; otherwise k_spec_fix redoes the whole
+// update with the true coefficients.  Either way b^{n+1} is the state the
+// two-pass iteration produces, bit for bit.
+
+template <int R, bool CKPT>
+__device__ __noinline__ void border_fused_unit(const FastParams& P, const float* s_lt,
+                                               const float* s_ls, int unit, float A, float B,
+                                               float e0, float delta, LaneDelta& d) {
+  constexpr int CPL = kUpdCols;
+  const int lane = threadIdx.x & 31;
+  int r = 0, x0 = 0;
+  const bool act = border_lane(P.gu, unit, lane, P.g.W, r, x0);
+  const int items = P.gu.bitems;
+  uint32_t ow[CPL], pw[CPL], mw[CPL];
+#pragma unroll
+  for (int c = 0; c < CPL; ++c) { ow[c] = 0u; pw[c] = 0u; mw[c] = 0u; }
+  if (act) {
+    const int k0 = (lane / items) * items;
+    update_rows_border<R, REGION, SRC_SMOOTH, CPL, true>(P, s_lt, s_ls, r, x0, k0, items, A, B,
+                                                         e0, ow, delta);
+    partition_rows_border<R>(P, s_lt, s_ls, r, x0, k0, items, P.scal->eps_phi, pw, mw);
+  }
+  for (int o = items; o < 32; o <<= 1) {
+#pragma unroll
+    for (int c = 0; c < CPL; ++c) {
+      ow[c] |= __shfl_xor_sync(0xffffffffu, ow[c], o);
+      pw[c] |= __shfl_xor_sync(0xffffffffu, pw[c], o);
+      mw[c] |= __shfl_xor_sync(0xffffffffu, mw[c], o);
+    }
+  }
+  if (!act || lane >= items) return;
+  uint32_t* dst = P.bits_out + (size_t)r * P.g.pitch_w + x0;
+#pragma unroll
+  for (int q = 0; q < CPL / 4; ++q)
+    reinterpret_cast<uint4*>(dst)[q] = make_uint4(ow[4 * q], ow[4 * q + 1], ow[4 * q + 2], ow[4 * q + 3]);
+  partition_commit<true, CKPT, false>(P, r, x0, pw, mw, d);
+}
+
+// Single runs, region / zhang, smoothed state, unsplit units: the update's
+// work geometry (gu) for both halves, one partial per unit (part[unit]).
+template <int R, bool CKPT>
+__global__ void __launch_bounds__(kThreads, kUpdateCtasPerSm) k_update_fused(FastParams P) {
+  constexpr int CPL = kUpdCols;
+  constexpr int NT = CPL + 2 * (R + 1);
+  constexpr int NPAT = 1 << (2 * R + 1);
+  __shared__ float s_lt[NPAT];
+  __shared__ float s_ls[NPAT];
+  __shared__ __align__(16) float s_ring[(kThreads / 32) * kRing2 * 32 * CPL];
+  __shared__ FastParams s_P;                     // see k_update
+  const SharedLuts luts{s_lt, s_ls, (uint32_t)__cvta_generic_to_shared(g_pair_lut)};
+  load_luts<R>(P, luts);
+  if (threadIdx.x == 0) s_P = P;
+  __syncthreads();
+  pdl_wait();
+  pdl_launch_dependents();
+  const Scalars* sc = P.scal;
+  if (stop_flag(sc)) return;
+  const float A = sc->A, B = sc->B, e0 = sc->spec_e0, delta = sc->spec_delta;
+  const int lane = threadIdx.x & 31;
+  const int nb = border_units(P.gu);
+  const int nch = chunk_units(P.gu);
+  const int nunits = nb + interior_units(P.gu);
+  float* ring = s_ring + (threadIdx.x >> 5) * kRing2 * 32 * CPL;
+  int unit = grab_unit(P, lane);
+  for (;;) {
+    if (unit >= nunits) break;
+#if LSE_FUSED_PREFETCH
+    // the next unit is grabbed now and read at the end of this one: the
+    // atomic's round trip overlaps the unit (same grab count: one failing
+    // grab per warp)
+    unsigned long long g_next = 0;
+    if (lane == 0) g_next = atomicAdd(P.work, 1ull) - P.work_base;
+#endif
+    LaneDelta d{0.0, 0.0, 0, 0, 0ull};
+    if (unit < nb) {
+      border_fused_unit<R, CKPT>(s_P, s_lt, s_ls, unit, A, B, e0, delta, d);
+    } else {
+      const int iu = unit - nb;
+      int r = 0, x0 = 0;
+      bool act = true;
+      if (iu < nch) {
+        r = P.gu.r_lo + iu / P.gu.nci;
+        x0 = P.gu.xoff + (iu % P.gu.nci) * kUpdChunk + CPL * lane;
+      } else {
+        act = b1_lane(P.gu, iu - nch, lane, r, x0);
+      }
+      uint32_t prev[NT], cur[NT];
+      uint32_t a = ~0u, o = 0u;
+      if (act) {
+        const uint32_t* wp = P.bits_in + (size_t)(r - 1) * P.g.pitch_w + (x0 - (R + 1));
+#if LSE_FUSED_PREFETCH
+        // into L1 ahead of use: the word-row below (the window of rows
+        // 16..31) and the old partition words (the commit)
+        prefetch_l1(wp + 2 * (size_t)P.g.pitch_w);
+        prefetch_l1(wp + 2 * (size_t)P.g.pitch_w + NT - 1);
+        prefetch_l1(P.pbits + (size_t)r * P.g.pitch_w + x0);
+        if (CKPT) prefetch_l1(P.mbits + (size_t)r * P.g.pitch_w + x0);
+#endif
+#pragma unroll
+        for (int j = 0; j < NT; ++j) {
+          prev[j] = __ldg(wp + j);
+          cur[j] = __ldg(wp + P.g.pitch_w + j);
+          if (P.skip_uniform) {
+            const uint32_t nx = __ldg(wp + 2 * (size_t)P.g.pitch_w + j);
+            a &= prev[j] & cur[j] & nx;
+            o |= prev[j] | cur[j] | nx;
+          }
+        }
+      }
+      uint32_t pw[CPL], mw[CPL];
+      if (P.skip_uniform && __all_sync(0xffffffffu, !act || a == ~0u || o == 0u)) {
+        // uniform window: phi has the sign of b everywhere, b^{n+1} = b^n
+        if (act) {
+          uint32_t* dst = P.bits_out + (size_t)r * P.g.pitch_w + x0;
+#pragma unroll
+          for (int q = 0; q < CPL / 4; ++q)
+            reinterpret_cast<uint4*>(dst)[q] = make_uint4(cur[R + 1 + 4 * q], cur[R + 2 + 4 * q],
+                                                          cur[R + 3 + 4 * q], cur[R + 4 + 4 * q]);
+#pragma unroll
+          for (int c = 0; c < CPL; ++c) pw[c] = mw[c] = cur[R + 1 + c];
+          partition_commit<true, CKPT, false>(P, r, x0, pw, mw, d);
+        }
+      } else if (act) {
+        update_block_int2<R, REGION, CPL, SRC_SMOOTH, true>(P, luts.lt2, ring, r, x0, A, B, e0,
+                                                            prev, cur, 0, delta, pw, mw, s_P);
+        partition_commit<true, CKPT, false>(P, r, x0, pw, mw, d);
+      }
+    }
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) {
+      d.a_in += __shfl_xor_sync(0xffffffffu, d.a_in, o);
+      d.a_out += __shfl_xor_sync(0xffffffffu, d.a_out, o);
+      d.n_in += __shfl_xor_sync(0xffffffffu, d.n_in, o);
+      d.n_out += __shfl_xor_sync(0xffffffffu, d.n_out, o);
+      d.mism += __shfl_xor_sync(0xffffffffu, d.mism, o);
+    }
+    if (lane == 0) {
+      TilePartial t{};
+      t.a_hi = d.a_in;
+      t.b_hi = d.a_out;
+      t.n_a = d.n_in;
+      t.n_b = d.n_out;
+      t.mism = d.mism;
+      P.part[unit] = t;
+    }
+#if LSE_FUSED_PREFETCH
+    g_next = (unsigned long long)__shfl_sync(0xffffffffu, (long long)g_next, 0);
+    unit = g_next > 0x7fffffffull ? 0x7fffffff : (int)g_next;
+#else
+    unit = grab_unit(P, lane);
+#endif
+  }
+}
+
+// After the finalize of a speculative update: either redo it with the true
+// coefficients (scal->redo; its own work counter scal->work2, reset by the
+// finalize) or decide the fix list's pixels exactly (u in fp64 with the
+// reference's operation order, exact_u_fast) and patch their bits.
+template <int R>
+__global__ void __launch_bounds__(kThreads, kUpdateCtasPerSm) k_spec_fix(FastParams P) {
+  constexpr int CPL = kUpdCols;
+  constexpr int NPAT = 1 << (2 * R + 1);
+  __shared__ float s_lt[NPAT];
+  __shared__ float s_ls[NPAT];
+  __shared__ __align__(16) float s_ring[(kThreads / 32) * kRing2 * 32 * CPL];
+  __shared__ FastParams s_P;
+  const SharedLuts luts{s_lt, s_ls, (uint32_t)__cvta_generic_to_shared(g_pair_lut)};
+  load_luts<R>(P, luts);
+  if (threadIdx.x == 0) s_P = P;
+  __syncthreads();
+  pdl_wait();
+  pdl_launch_dependents();
+  Scalars* sc = P.scal;
+  if (stop_flag(sc)) return;
+  if (blockIdx.x == 0 && threadIdx.x == 0) {
+    if (sc->zero_vel && sc->model != EDGE) sc->degenerate = 1;   // sticky (engine.py:239-240)
+    sc->fix_n[P.fix_par ^ 1] = 0u;               // the next speculative update's list
+  }
+  if (__ldcg(&sc->redo)) {
+    update_units<R, REGION, SRC_SMOOTH, false, 1>(P, s_P, luts, s_lt, s_ls, s_ring);
+    return;
+  }
+  const unsigned n = min(__ldcg(&sc->fix_n[P.fix_par]), P.fix_cap);
+  const unsigned stride = gridDim.x * blockDim.x;
+  for (unsigned q = blockIdx.x * blockDim.x + threadIdx.x; q < n; q += stride) {
+    const int2 e = __ldcg(&P.fix[q]);
+    const bool pos = exact_u_fast<R, SRC_SMOOTH>(P.ctx, P.bits_in, e.y, e.x) > 0.0;
+    uint32_t* w = P.bits_out + (size_t)(e.y >> 5) * P.g.pitch_w + e.x;
+    const uint32_t bit = 1u << (e.y & 31);
+    if (pos) atomicOr(w, bit);
+    else atomicAnd(w, ~bit);
   }
 }
 

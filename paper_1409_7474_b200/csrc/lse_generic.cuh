@@ -511,12 +511,14 @@ __global__ void __launch_bounds__(64) k_finalize_tiles_direct(const TilePartial*
 }
 
 // per-iteration finalize of the fast path (DELTA partials); no-op once stopped
+// (spec = 1 + fix-list parity: the partials came from a speculative fused
+// pass, whose prediction is checked here -- spec_check)
 __global__ void __launch_bounds__(64) k_finalize_run(PartRanges R3, Scalars* sc, int region,
-                                                       int ckpt, long long iter) {
+                                                       int ckpt, long long iter, int spec) {
   pdl_wait();
   pdl_launch_dependents();
   if (stop_flag(sc)) return;
-  finalize_cta(R3, sc, true, region != 0, ckpt != 0, iter);
+  finalize_cta(R3, sc, true, region != 0, ckpt != 0, iter, spec);
 }
 
 // image statistics: min, max, max|.| (order-preserving integer atomics)

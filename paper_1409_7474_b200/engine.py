@@ -391,6 +391,14 @@ class EvolutionRun:
         """fp64 re-evaluations of near-tie pixels so far (diagnostics)."""
         return int(self._dev.status().exact_fallbacks)
 
+    def spec_stats(self) -> dict:
+        """Speculative fused iterations of this run (diagnostics; results are
+        the same with LSE_FUSED=0): launched, redone whole, fix-list pixels."""
+        out = (C.c_longlong * 4)()
+        N.check(N.lib.lse_run_spec_stats(self._dev.h, out))
+        return dict(fused=int(out[0]), redos=int(out[1]), fixes=int(out[2]),
+                    enabled=bool(out[3]))
+
     def path_counts(self) -> tuple[int, int]:
         st = self._dev.status()
         return int(st.fast_iterations), int(st.generic_iterations)
