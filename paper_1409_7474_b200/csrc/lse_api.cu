@@ -18,6 +18,7 @@
 #include <cstddef>
 #include <cstdio>
 #include <cstring>
+#include <mutex>
 #include <string>
 #include <vector>
 
@@ -74,11 +75,12 @@ bool pdl_enabled() {
 }
 
 template <typename... KArgs, typename... Args>
-int launch_pdl(void (*kern)(KArgs...), dim3 grid, dim3 block, cudaStream_t st, Args... args) {
+int launch_pdl_smem(void (*kern)(KArgs...), dim3 grid, dim3 block, size_t smem, cudaStream_t st,
+                    Args... args) {
   cudaLaunchConfig_t cfg{};
   cfg.gridDim = grid;
   cfg.blockDim = block;
-  cfg.dynamicSmemBytes = 0;
+  cfg.dynamicSmemBytes = smem;
   cfg.stream = st;
   cudaLaunchAttribute attr[1];
   attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
@@ -88,6 +90,27 @@ int launch_pdl(void (*kern)(KArgs...), dim3 grid, dim3 block, cudaStream_t st, A
   g_launches.fetch_add(1, std::memory_order_relaxed);
   const cudaError_t e = cudaLaunchKernelEx(&cfg, kern, args...);
   if (e != cudaSuccess) return fail(LSE_ERR_CUDA, std::string("launch: ") + cudaGetErrorString(e));
+  return LSE_OK;
+}
+
+template <typename... KArgs, typename... Args>
+int launch_pdl(void (*kern)(KArgs...), dim3 grid, dim3 block, cudaStream_t st, Args... args) {
+  return launch_pdl_smem(kern, grid, block, 0, st, args...);
+}
+
+// a kernel with dynamic shared memory: opt in to the size and to the carveout
+// that keeps kUpdateCtasPerSm CTAs resident (once per kernel)
+template <typename... KArgs>
+int prepare_smem(void (*kern)(KArgs...), size_t smem) {
+  static std::vector<const void*> done;
+  static std::mutex mu;
+  std::lock_guard<std::mutex> lock(mu);
+  const void* key = reinterpret_cast<const void*>(kern);
+  if (std::find(done.begin(), done.end(), key) != done.end()) return LSE_OK;
+  CK(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+  CK(cudaFuncSetAttribute(kern, cudaFuncAttributePreferredSharedMemoryCarveout,
+                          cudaSharedmemCarveoutMaxShared));
+  done.push_back(key);
   return LSE_OK;
 }
 
@@ -728,7 +751,7 @@ int launch_fused_R(lse_run* r, long long it, bool ckpt_prev) {
   P.fix_cap = r->fix_cap;
   P.fix_par = (int)(it & 1);
   const long long n = r->nb_upd[0] + r->ni_upd;
-  const int g = fast_grid(n, kUpdateCtasPerSm);
+  const int g = fast_grid(n, kFusedCtasPerSm);
   P.work_base = take_work(r, n, g);
   cudaEvent_t e0 = nullptr, e1 = nullptr;
   if (r->prof) {
@@ -736,8 +759,14 @@ int launch_fused_R(lse_run* r, long long it, bool ckpt_prev) {
     e1 = next_event(r);
     cudaEventRecord(e0, r->st);
   }
-  if (ckpt_prev) TRY(launch_pdl(k_update_fused<R, true>, g, kThreads, r->st, P));
-  else TRY(launch_pdl(k_update_fused<R, false>, g, kThreads, r->st, P));
+  constexpr size_t smem = fused_smem_bytes<R>();
+  if (ckpt_prev) {
+    TRY(prepare_smem(k_update_fused<R, true>, smem));
+    TRY(launch_pdl_smem(k_update_fused<R, true>, g, kThreads, smem, r->st, P));
+  } else {
+    TRY(prepare_smem(k_update_fused<R, false>, smem));
+    TRY(launch_pdl_smem(k_update_fused<R, false>, g, kThreads, smem, r->st, P));
+  }
   if (r->prof) cudaEventRecord(e1, r->st);
   PartRanges R3{{r->d_part, r->d_part, r->d_part}, {(int)n, 0, 0}};
   const int spec = 1 + P.fix_par;
@@ -754,7 +783,7 @@ int launch_fused_R(lse_run* r, long long it, bool ckpt_prev) {
   FastParams Q = P;                              // the redo pass has its own work counter
   Q.work = &r->d_scal->work2;
   Q.work_base = 0;
-  TRY(launch_pdl(k_spec_fix<R>, g, kThreads, r->st, Q));
+  TRY(launch_pdl(k_spec_fix<R>, fast_grid(n, kUpdateCtasPerSm), kThreads, r->st, Q));
   if (r->prof) {
     cudaEvent_t e2 = next_event(r);
     cudaEventRecord(e2, r->st);

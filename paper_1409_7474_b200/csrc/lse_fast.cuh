@@ -145,6 +145,13 @@ constexpr int kPartitionCtasPerSm = 4;   // partition occupancy (launch bound an
 #define LSE_UPDATE_CTAS 4
 #endif
 constexpr int kUpdateCtasPerSm = LSE_UPDATE_CTAS;   // update occupancy (launch bound and grid)
+#ifndef LSE_FUSED_CTAS
+#define LSE_FUSED_CTAS 3
+#endif
+// fused pass: 3 CTAs (12 warps) per SM at 168 registers measured faster than
+// 4 at 128 (C5 766 -> 775 Gpix-it/s: the spills of the tighter budget cost
+// more than the extra warps hide)
+constexpr int kFusedCtasPerSm = LSE_FUSED_CTAS;
 constexpr int kUpdCols = 8;      // update: columns per lane
 constexpr int kUpdChunk = 32 * kUpdCols;   // update: columns per warp chunk
 
@@ -435,9 +442,6 @@ __device__ __forceinline__ void load_data_row(const FastParams& P, int i, int x0
   }
 }
 
-#ifndef LSE_FUSED_PREFETCH
-#define LSE_FUSED_PREFETCH 0
-#endif
 // codegen knobs of the fused loop (A/B builds)
 #ifndef LSE_LUT_EXPLICIT
 #define LSE_LUT_EXPLICIT 0
@@ -453,9 +457,10 @@ __device__ __forceinline__ void load_data_row(const FastParams& P, int i, int x0
 #ifndef LSE_PAIR_MIN
 #define LSE_PAIR_MIN 1
 #endif
-__device__ __forceinline__ void prefetch_l1(const void* p) {
-  asm volatile("prefetch.global.L1 [%0];" ::"l"(p));
-}
+#ifndef LSE_STEP_UNROLL
+#define LSE_STEP_UNROLL 2
+#endif
+constexpr int kStepUnroll = LSE_STEP_UNROLL;
 
 // three-input minimum (FMNMX3, sm_100+)
 __device__ __forceinline__ float fmin3(float a, float b, float c) {
@@ -685,7 +690,8 @@ __device__ __forceinline__ void update_block_int2(const FastParams& P, uint32_t 
                                                   const uint32_t (&prev)[CPL + 2 * (R + 1)],
                                                   const uint32_t (&cur)[CPL + 2 * (R + 1)],
                                                   int tile, float delta, uint32_t (&pw)[CPL],
-                                                  uint32_t (&mw)[CPL], const FastParams& Pn) {
+                                                  uint32_t (&mw)[CPL], const FastParams& Pn,
+                                                  const uint32_t* wslot = nullptr) {
   // Pn: the launch parameters as seen by the noinline tie helpers (the CTA's
   // shared copy: passing the kernel parameter block by reference to a noinline
   // function makes every thread copy it to local memory first)
@@ -721,7 +727,7 @@ __device__ __forceinline__ void update_block_int2(const FastParams& P, uint32_t 
   }
   phi_rows2_int<R, NT, NP, SRC>(P, win4, 0, lut_base, pp);     // rows -1, 0
   const uint32_t* wrow = P.bits_in + (size_t)r * P.g.pitch_w + (x0 - (R + 1));
-#pragma unroll 2
+#pragma unroll kStepUnroll
   for (int s = 0; s < 16; ++s) {
     {
       if (2 * s + kRing2 - 2 < 32) {
@@ -736,9 +742,17 @@ __device__ __forceinline__ void update_block_int2(const FastParams& P, uint32_t 
       cp_async_commit();
     }
     if (s == 8) {                               // window base y0+16-R for rows >= 17
+      if (FUSED) {                              // staged in shared memory at the unit start
+        // (an asm load: a plain one lets the compiler re-derive the value from
+        // the global words it was built from -- the loads this avoids)
+        const uint32_t ws = (uint32_t)__cvta_generic_to_shared(wslot) + 4 * lane;
 #pragma unroll
-      for (int j = 0; j < NT; ++j)
-        win4[j] = __funnelshift_r(__ldg(wrow + j), __ldg(wrow + P.g.pitch_w + j), 16 - R) << 3;
+        for (int j = 0; j < NT; ++j) asm volatile("ld.shared.u32 %0, [%1];" : "=r"(win4[j]) : "r"(ws + 128 * j));
+      } else {
+#pragma unroll
+        for (int j = 0; j < NT; ++j)
+          win4[j] = __funnelshift_r(__ldg(wrow + j), __ldg(wrow + P.g.pitch_w + j), 16 - R) << 3;
+      }
     }
     const int kn = 2 * s + 1;                   // first phi row of this step's pair
     phi_rows2_int<R, NT, NP, SRC>(P, win4, s < 8 ? kn + 1 : kn - 16, lut_base, pn);
@@ -2053,17 +2067,32 @@ __device__ __noinline__ void border_fused_unit(const FastParams& P, const float*
 
 // Single runs, region / zhang, smoothed state, unsplit units: the update's
 // work geometry (gu) for both halves, one partial per unit (part[unit]).
+template <int R>
+constexpr int fused_smem_bytes() {
+  return (kThreads / 32) * (kRing2 * 32 * kUpdCols + (kUpdCols + 2 * (R + 1)) * 32) * 4;
+}
+
 template <int R, bool CKPT>
-__global__ void __launch_bounds__(kThreads, kUpdateCtasPerSm) k_update_fused(FastParams P) {
+__global__ void __launch_bounds__(kThreads, kFusedCtasPerSm) k_update_fused(FastParams P) {
   constexpr int CPL = kUpdCols;
   constexpr int NT = CPL + 2 * (R + 1);
   constexpr int NPAT = 1 << (2 * R + 1);
-  __shared__ float s_lt[NPAT];
+  // (the border code's zero-padded rows read only the weight-sum table)
   __shared__ float s_ls[NPAT];
-  __shared__ __align__(16) float s_ring[(kThreads / 32) * kRing2 * 32 * CPL];
+  // dynamic shared memory (fused_smem_bytes): the data rings, then per warp
+  // the window of rows 16..31 of its unit, built at the unit start (word j of
+  // lane l at [j][l]) so the mid-unit switch reads shared memory
+  extern __shared__ __align__(16) float s_dyn[];
+  float* s_ring = s_dyn;
+  auto s_win = reinterpret_cast<uint32_t (*)[NT][32]>(s_dyn + (kThreads / 32) * kRing2 * 32 * CPL);
   __shared__ FastParams s_P;                     // see k_update
-  const SharedLuts luts{s_lt, s_ls, (uint32_t)__cvta_generic_to_shared(g_pair_lut)};
-  load_luts<R>(P, luts);
+  const SharedLuts luts{nullptr, s_ls, (uint32_t)__cvta_generic_to_shared(g_pair_lut)};
+  {
+    for (int q = threadIdx.x; q < NPAT; q += blockDim.x) s_ls[q] = __ldg(&P.lut_s[q]);
+    for (int q = threadIdx.x; q < 2 * NPAT; q += blockDim.x)
+      g_pair_lut[q] = make_float2(__ldg(&P.lut_t[q & (NPAT - 1)]), __ldg(&P.lut_t[q >> 1]));
+  }
+  const float* s_lt = nullptr;
   if (threadIdx.x == 0) s_P = P;
   __syncthreads();
   pdl_wait();
@@ -2076,16 +2105,13 @@ __global__ void __launch_bounds__(kThreads, kUpdateCtasPerSm) k_update_fused(Fas
   const int nch = chunk_units(P.gu);
   const int nunits = nb + interior_units(P.gu);
   float* ring = s_ring + (threadIdx.x >> 5) * kRing2 * 32 * CPL;
-  int unit = grab_unit(P, lane);
+  uint32_t (&win_b)[NT][32] = s_win[threadIdx.x >> 5];
+  // (Software-pipelining the units -- grabbing the next one and loading its
+  // window before this one's commit -- measured slower: 775 -> 764 Gpix-it/s
+  // on C5, the extra live window words cost more than the latency they hid.)
   for (;;) {
+    const int unit = grab_unit(P, lane);
     if (unit >= nunits) break;
-#if LSE_FUSED_PREFETCH
-    // the next unit is grabbed now and read at the end of this one: the
-    // atomic's round trip overlaps the unit (same grab count: one failing
-    // grab per warp)
-    unsigned long long g_next = 0;
-    if (lane == 0) g_next = atomicAdd(P.work, 1ull) - P.work_base;
-#endif
     LaneDelta d{0.0, 0.0, 0, 0, 0ull};
     if (unit < nb) {
       border_fused_unit<R, CKPT>(s_P, s_lt, s_ls, unit, A, B, e0, delta, d);
@@ -2103,23 +2129,16 @@ __global__ void __launch_bounds__(kThreads, kUpdateCtasPerSm) k_update_fused(Fas
       uint32_t a = ~0u, o = 0u;
       if (act) {
         const uint32_t* wp = P.bits_in + (size_t)(r - 1) * P.g.pitch_w + (x0 - (R + 1));
-#if LSE_FUSED_PREFETCH
-        // into L1 ahead of use: the word-row below (the window of rows
-        // 16..31) and the old partition words (the commit)
-        prefetch_l1(wp + 2 * (size_t)P.g.pitch_w);
-        prefetch_l1(wp + 2 * (size_t)P.g.pitch_w + NT - 1);
-        prefetch_l1(P.pbits + (size_t)r * P.g.pitch_w + x0);
-        if (CKPT) prefetch_l1(P.mbits + (size_t)r * P.g.pitch_w + x0);
-#endif
 #pragma unroll
         for (int j = 0; j < NT; ++j) {
           prev[j] = __ldg(wp + j);
           cur[j] = __ldg(wp + P.g.pitch_w + j);
+          const uint32_t nx = __ldg(wp + 2 * (size_t)P.g.pitch_w + j);
           if (P.skip_uniform) {
-            const uint32_t nx = __ldg(wp + 2 * (size_t)P.g.pitch_w + j);
             a &= prev[j] & cur[j] & nx;
             o |= prev[j] | cur[j] | nx;
           }
+          win_b[j][lane] = __funnelshift_r(cur[j], nx, 16 - R) << 3;
         }
       }
       uint32_t pw[CPL], mw[CPL];
@@ -2137,7 +2156,8 @@ __global__ void __launch_bounds__(kThreads, kUpdateCtasPerSm) k_update_fused(Fas
         }
       } else if (act) {
         update_block_int2<R, REGION, CPL, SRC_SMOOTH, true>(P, luts.lt2, ring, r, x0, A, B, e0,
-                                                            prev, cur, 0, delta, pw, mw, s_P);
+                                                            prev, cur, 0, delta, pw, mw, s_P,
+                                                            &win_b[0][0]);
         partition_commit<true, CKPT, false>(P, r, x0, pw, mw, d);
       }
     }
@@ -2158,12 +2178,6 @@ __global__ void __launch_bounds__(kThreads, kUpdateCtasPerSm) k_update_fused(Fas
       t.mism = d.mism;
       P.part[unit] = t;
     }
-#if LSE_FUSED_PREFETCH
-    g_next = (unsigned long long)__shfl_sync(0xffffffffu, (long long)g_next, 0);
-    unit = g_next > 0x7fffffffull ? 0x7fffffff : (int)g_next;
-#else
-    unit = grab_unit(P, lane);
-#endif
   }
 }
 
