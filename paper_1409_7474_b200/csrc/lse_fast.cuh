@@ -1734,10 +1734,19 @@ struct LaneDelta {
 };
 
 // P / M bit bookkeeping of one lane block (8 words) + the partition deltas.
+__device__ __forceinline__ uint4 lds_u4(uint32_t addr) {
+  uint4 v;
+  asm volatile("ld.shared.v4.u32 {%0, %1, %2, %3}, [%4];"
+               : "=r"(v.x), "=r"(v.y), "=r"(v.z), "=r"(v.w) : "r"(addr));
+  return v;
+}
+
+// sold: shared address of this lane's old P words (and, +1024, old M words)
+// staged by cp.async at the unit start (fused pass), 0: read global memory
 template <bool PART, bool CKPT, bool MASKONLY>
 __device__ __forceinline__ void partition_commit(const FastParams& P, int r, int x0,
                                                  const uint32_t (&pw)[8], const uint32_t (&mw)[8],
-                                                 LaneDelta& d, int tile = 0) {
+                                                 LaneDelta& d, int tile = 0, uint32_t sold = 0u) {
   const int y0 = r * 32;
   const size_t base = (size_t)r * P.g.pitch_w + x0;
   // a row strip's halo word-rows are owned (and counted) by the neighbour
@@ -1748,8 +1757,8 @@ __device__ __forceinline__ void partition_commit(const FastParams& P, int r, int
     return;
   }
   if (PART) {
-    const uint4 o0 = reinterpret_cast<const uint4*>(P.pbits + base)[0];
-    const uint4 o1 = reinterpret_cast<const uint4*>(P.pbits + base)[1];
+    const uint4 o0 = sold ? lds_u4(sold) : reinterpret_cast<const uint4*>(P.pbits + base)[0];
+    const uint4 o1 = sold ? lds_u4(sold + 16) : reinterpret_cast<const uint4*>(P.pbits + base)[1];
     const uint32_t old[8] = {o0.x, o0.y, o0.z, o0.w, o1.x, o1.y, o1.z, o1.w};
     uint32_t any = 0u;
     if (P.chg) {
@@ -1784,8 +1793,8 @@ __device__ __forceinline__ void partition_commit(const FastParams& P, int r, int
     }
   }
   if (CKPT) {
-    const uint4 o0 = reinterpret_cast<const uint4*>(P.mbits + base)[0];
-    const uint4 o1 = reinterpret_cast<const uint4*>(P.mbits + base)[1];
+    const uint4 o0 = sold ? lds_u4(sold + 1024) : reinterpret_cast<const uint4*>(P.mbits + base)[0];
+    const uint4 o1 = sold ? lds_u4(sold + 1040) : reinterpret_cast<const uint4*>(P.mbits + base)[1];
     const uint32_t old[8] = {o0.x, o0.y, o0.z, o0.w, o1.x, o1.y, o1.z, o1.w};
 #pragma unroll
     for (int c = 0; c < 8; ++c) d.mism += own ? __popc(old[c] ^ mw[c]) : 0;
@@ -2069,7 +2078,8 @@ __device__ __noinline__ void border_fused_unit(const FastParams& P, const float*
 // work geometry (gu) for both halves, one partial per unit (part[unit]).
 template <int R>
 constexpr int fused_smem_bytes() {
-  return (kThreads / 32) * (kRing2 * 32 * kUpdCols + (kUpdCols + 2 * (R + 1)) * 32) * 4;
+  // per warp: data ring, window of rows 16..31, old P and M words (2 x 1 KB)
+  return (kThreads / 32) * ((kRing2 * 32 * kUpdCols + (kUpdCols + 2 * (R + 1)) * 32) * 4 + 2048);
 }
 
 template <int R, bool CKPT>
@@ -2085,6 +2095,10 @@ __global__ void __launch_bounds__(kThreads, kFusedCtasPerSm) k_update_fused(Fast
   extern __shared__ __align__(16) float s_dyn[];
   float* s_ring = s_dyn;
   auto s_win = reinterpret_cast<uint32_t (*)[NT][32]>(s_dyn + (kThreads / 32) * kRing2 * 32 * CPL);
+  // per warp: the old P / M words of the unit's block, staged at the unit start
+  const uint32_t s_old = (uint32_t)__cvta_generic_to_shared(s_dyn) +
+                         (kThreads / 32) * (kRing2 * 32 * CPL + NT * 32) * 4 +
+                         (threadIdx.x >> 5) * 2048 + (threadIdx.x & 31) * 32;
   __shared__ FastParams s_P;                     // see k_update
   const SharedLuts luts{nullptr, s_ls, (uint32_t)__cvta_generic_to_shared(g_pair_lut)};
   {
@@ -2106,12 +2120,17 @@ __global__ void __launch_bounds__(kThreads, kFusedCtasPerSm) k_update_fused(Fast
   const int nunits = nb + interior_units(P.gu);
   float* ring = s_ring + (threadIdx.x >> 5) * kRing2 * 32 * CPL;
   uint32_t (&win_b)[NT][32] = s_win[threadIdx.x >> 5];
-  // (Software-pipelining the units -- grabbing the next one and loading its
-  // window before this one's commit -- measured slower: 775 -> 764 Gpix-it/s
-  // on C5, the extra live window words cost more than the latency they hid.)
+  // (Also loading the next unit's window before this one's commit measured
+  // slower: 775 -> 764 Gpix-it/s on C5, the live window words cost more than
+  // the latency they hid.)
+  // The next unit is grabbed when this one starts and read at its end (the
+  // atomic's round trip overlaps the unit; same grab count: one failing grab
+  // per warp).
+  int unit = grab_unit(P, lane);
   for (;;) {
-    const int unit = grab_unit(P, lane);
     if (unit >= nunits) break;
+    unsigned long long g_next = 0;
+    if (lane == 0) g_next = atomicAdd(P.work, 1ull) - P.work_base;
     LaneDelta d{0.0, 0.0, 0, 0, 0ull};
     if (unit < nb) {
       border_fused_unit<R, CKPT>(s_P, s_lt, s_ls, unit, A, B, e0, delta, d);
@@ -2127,6 +2146,17 @@ __global__ void __launch_bounds__(kThreads, kFusedCtasPerSm) k_update_fused(Fast
       }
       uint32_t prev[NT], cur[NT];
       uint32_t a = ~0u, o = 0u;
+      if (act) {
+        // old P (and M) words of the block: in flight until the commit
+        const size_t wb = (size_t)r * P.g.pitch_w + x0;
+        cp_async16(s_old, P.pbits + wb);
+        cp_async16(s_old + 16, P.pbits + wb + 4);
+        if (CKPT) {
+          cp_async16(s_old + 1024, P.mbits + wb);
+          cp_async16(s_old + 1040, P.mbits + wb + 4);
+        }
+      }
+      cp_async_commit();
       if (act) {
         const uint32_t* wp = P.bits_in + (size_t)(r - 1) * P.g.pitch_w + (x0 - (R + 1));
 #pragma unroll
@@ -2152,13 +2182,15 @@ __global__ void __launch_bounds__(kThreads, kFusedCtasPerSm) k_update_fused(Fast
                                                           cur[R + 3 + 4 * q], cur[R + 4 + 4 * q]);
 #pragma unroll
           for (int c = 0; c < CPL; ++c) pw[c] = mw[c] = cur[R + 1 + c];
-          partition_commit<true, CKPT, false>(P, r, x0, pw, mw, d);
+          cp_async_wait<0>();
+          partition_commit<true, CKPT, false>(P, r, x0, pw, mw, d, 0, s_old);
         }
       } else if (act) {
+        // (its final cp.async wait covers the old words too)
         update_block_int2<R, REGION, CPL, SRC_SMOOTH, true>(P, luts.lt2, ring, r, x0, A, B, e0,
                                                             prev, cur, 0, delta, pw, mw, s_P,
                                                             &win_b[0][0]);
-        partition_commit<true, CKPT, false>(P, r, x0, pw, mw, d);
+        partition_commit<true, CKPT, false>(P, r, x0, pw, mw, d, 0, s_old);
       }
     }
 #pragma unroll
@@ -2178,6 +2210,8 @@ __global__ void __launch_bounds__(kThreads, kFusedCtasPerSm) k_update_fused(Fast
       t.mism = d.mism;
       P.part[unit] = t;
     }
+    g_next = (unsigned long long)__shfl_sync(0xffffffffu, (long long)g_next, 0);
+    unit = g_next > 0x7fffffffull ? 0x7fffffff : (int)g_next;
   }
 }
 
