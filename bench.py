@@ -701,6 +701,13 @@ def main_c5(args, ws, rank, local, dist):
                                        C.byref(n_part)))
     N.check(N.lib.lse_run_set_profiling(h, 0))
     fallbacks = st.exact_fallbacks
+    spec = (C.c_longlong * 4)()
+    N.check(N.lib.lse_run_spec_stats(h, spec))
+    spec_stats = {"fused_iterations": int(spec[0]), "redone": int(spec[1]),
+                  "fix_list_pixels": int(spec[2]), "enabled": bool(spec[3]),
+                  "note": "cumulative over the run's jobs (warm-up included): one-pass "
+                          "speculative iterations, of which redone whole (prediction outside "
+                          "its band), pixels decided from the fix list"}
     px_its = job_px_its * args.steps
     value = px_its / (t_ms / 1e3) / 1e9
 
@@ -822,7 +829,7 @@ def main_c5(args, ws, rank, local, dist):
             "roofline": roof, "cpu_baseline": cpu, "e2e": e2e, "e2e_dropin": dropin,
             "gpu_launches": int(launches),
             "uniform_skip": skip, "other_configs": others,
-            "clocks": clk, "exact_fallbacks": int(fallbacks),
+            "clocks": clk, "exact_fallbacks": int(fallbacks), "speculation": spec_stats,
             "scene_gen_s": round(jb.t_gen, 2),
         }
         print(json.dumps(line), flush=True)

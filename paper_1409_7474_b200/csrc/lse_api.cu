@@ -774,16 +774,18 @@ int launch_fused_R(lse_run* r, long long it, bool ckpt_prev) {
     TRY(launch_pdl(k_finalize_run, 1, 64, r->st, R3, r->d_scal, 1, ckpt_prev ? 1 : 0, it - 1,
                    spec));
   } else {
-    TRY(launch_pdl(k_finalize_stage1, kFinSlices, 256, r->st, R3, r->d_part_fin,
+    // (one partial per unit, ~131 k on C5: a wider first stage)
+    TRY(launch_pdl(k_finalize_stage1, kFusedFinSlices, 256, r->st, R3, r->d_part_fin,
                    (const Scalars*)r->d_scal));
-    PartRanges R1{{r->d_part_fin, r->d_part_fin, r->d_part_fin}, {kFinSlices, 0, 0}};
+    PartRanges R1{{r->d_part_fin, r->d_part_fin, r->d_part_fin}, {kFusedFinSlices, 0, 0}};
     TRY(launch_pdl(k_finalize_run, 1, 64, r->st, R1, r->d_scal, 1, ckpt_prev ? 1 : 0, it - 1,
                    spec));
   }
+  TRY(launch_pdl(k_spec_fix<R>, num_sms(), 256, r->st, P));
   FastParams Q = P;                              // the redo pass has its own work counter
   Q.work = &r->d_scal->work2;
   Q.work_base = 0;
-  TRY(launch_pdl(k_spec_fix<R>, fast_grid(n, kUpdateCtasPerSm), kThreads, r->st, Q));
+  TRY(launch_pdl(k_spec_redo<R>, fast_grid(n, kUpdateCtasPerSm), kThreads, r->st, Q));
   if (r->prof) {
     cudaEvent_t e2 = next_event(r);
     cudaEventRecord(e2, r->st);
@@ -1506,7 +1508,7 @@ int create_impl(lse_run** out, const lse_params* p, long long height, long long 
       (rc = dalloc(&r->d_lut_s, 512)) || (rc = dalloc(&r->d_ctx, 1)) ||
       (rc = dalloc(&r->d_w64, 32)) || (rc = dalloc(&r->d_keys, 3)) ||
       (rc = dalloc(&r->d_count, 1)) || (rc = dalloc(&r->d_work, 1)) ||
-      (rc = dalloc(&r->d_part_fin, kFinSlices)) ||
+      (rc = dalloc(&r->d_part_fin, std::max(kFinSlices, kFusedFinSlices))) ||
       (rc = dalloc(&r->d_part_init, (size_t)r->g.HR * ((r->g.pitch_w + 1023) / 1024))))
     return cleanup(rc);
   if (r->fused && (rc = dalloc(&r->d_fix, r->fix_cap))) return cleanup(rc);

@@ -59,6 +59,7 @@ struct __align__(16) Scalars {
   // exactly once the true coefficients are known (k_spec_fix), or the whole
   // update is redone when the coefficients moved more than spec_delta
   int redo;                           // the last speculative update must be redone
+  int fix_needed;                     // its coefficients moved: the fix list decides the band
   float spec_delta, spec_e0;          // flag band of the next speculative update (delta < 0: none)
   unsigned int fix_n[2];              // fix-list entries of the speculative update (by parity)
   unsigned int fix_cap;               // fix-list capacity

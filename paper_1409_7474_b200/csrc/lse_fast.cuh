@@ -261,6 +261,10 @@ __device__ __forceinline__ void gather_window(const ExactCtx* c, const uint32_t*
 template <int R, int NC>
 __device__ __forceinline__ double wt(const ExactCtx* c, const uint32_t (&val)[NC],
                                      const uint32_t (&valid)[NC], int rr, int cc) {
+  // (interior pixels take the branch-free table path of exact_u_fast /
+  // exact_phi_fast; here each table lookup sits behind a data-dependent
+  // branch.  Always computing the explicit sum instead measured far worse:
+  // the unrolled sums' registers spill the fused kernel's hot loop.)
   constexpr uint32_t PM = (1u << (2 * R + 1)) - 1u;
   if (R <= 4 && c->lut64 && ((valid[cc] >> (rr - R)) & PM) == PM)
     return __ldg(&c->lut64[(val[cc] >> (rr - R)) & PM]);   // the same value, tabulated
@@ -286,11 +290,60 @@ __device__ __forceinline__ double wphi(const ExactCtx* c, const uint32_t (&val)[
   return acc;
 }
 
+#ifndef LSE_EXACT_INTERIOR
+#define LSE_EXACT_INTERIOR 1
+#endif
+// Interior pixels (the whole window inside the image, R <= 4): every vertical
+// value is a table entry, so all of them are loaded at once -- no per-value
+// branch to serialise the loads (the general path above takes ~45 dependent
+// L2 round trips, ~10 us per evaluation) -- then combined in scipy's order.
+template <int R, int NC>
+__device__ __forceinline__ void interior_window(const ExactCtx* c, const uint32_t* bits, int r0,
+                                                int xc0, uint32_t (&val)[NC]) {
+  const int HR = (c->H + 31) >> 5;
+  const int wr = r0 >> 5, sh = r0 & 31;
+  const uint32_t* p = bits + (size_t)wr * c->pitch_w + xc0;
+  const bool two = wr + 1 < HR;
+#pragma unroll
+  for (int cc = 0; cc < NC; ++cc) {
+    const uint32_t lo = __ldg(p + cc);
+    const uint32_t hi = two ? __ldg(p + c->pitch_w + cc) : 0u;
+    val[cc] = __funnelshift_r(lo, hi, sh);
+  }
+}
+template <int R, int NC>
+__device__ __forceinline__ void lut_row(const double* lut, const uint32_t (&val)[NC], int rr,
+                                        double (&t)[NC]) {
+  constexpr uint32_t PM = (1u << (2 * R + 1)) - 1u;
+#pragma unroll
+  for (int cc = 0; cc < NC; ++cc) t[cc] = __ldg(&lut[(val[cc] >> (rr - R)) & PM]);
+}
+// wphi's sum over one row of vertical values (same order)
+template <int R, int NC>
+__device__ __forceinline__ double wphi_row(const double (&t)[NC], int cc, const double (&w)[R + 1]) {
+  double acc = dmul(t[cc], w[0]);
+#pragma unroll
+  for (int d = R; d >= 1; --d) acc = dadd(acc, dmul(dadd(t[cc - d], t[cc + d]), w[d]));
+  return acc;
+}
+
 // phi^{n+1} at (i, x) exactly (partition near-ties)
 template <int R>
 __device__ __noinline__ double exact_phi_fast(const ExactCtx* c, const uint32_t* bits, int i, int x,
                                               bool count = true) {
   constexpr int NR = 2 * R + 1, NC = 2 * R + 1;
+  if (LSE_EXACT_INTERIOR && R <= 4 && c->lut64 && i >= R && i <= c->H - 1 - R && x >= R &&
+      x <= c->W - 1 - R) {
+    double w[R + 1];
+#pragma unroll
+    for (int d = 0; d <= R; ++d) w[d] = c->w64[d];
+    uint32_t v[NC];
+    interior_window<R, NC>(c, bits, i - R, x - R, v);
+    double t[NC];
+    lut_row<R, NC>(c->lut64, v, R, t);
+    if (count) atomicAdd(&c->scal->fallbacks, 1ull);
+    return wphi_row<R, NC>(t, R, w);
+  }
   uint32_t val[NC], valid[NC];
   gather_window<NR, NC>(c, bits, i - R, x - R, val, valid);
   if (count) atomicAdd(&c->scal->fallbacks, 1ull);
@@ -308,6 +361,29 @@ __device__ __noinline__ double exact_u_fast(const ExactCtx* c, const uint32_t* b
   // the pixel's data value is loaded with the window (one round of latency
   // for both; the multi-band term reads its bands later)
   const double Iv = c->model != VECTOR ? data_exact(c, i, x) : 0.0;
+  if (LSE_EXACT_INTERIOR && SRC != SRC_SCALED && R <= 4 && c->lut64 && i >= R + 1 &&
+      i <= H - 2 - R && x >= R + 1 && x <= W - 2 - R) {
+    // interior: rows i-1, i, i+1 of the window (rr = R .. R+2), central differences
+    double w[R + 1];
+#pragma unroll
+    for (int d = 0; d <= R; ++d) w[d] = c->w64[d];
+    uint32_t v[NC];
+    interior_window<R, NC>(c, bits, i - 1 - R, x - 1 - R, v);
+    double tu[NC], tc[NC], td[NC];
+    lut_row<R, NC>(c->lut64, v, R, tu);
+    lut_row<R, NC>(c->lut64, v, R + 1, tc);
+    lut_row<R, NC>(c->lut64, v, R + 2, td);
+    const double pc = wphi_row<R, NC>(tc, R + 1, w);
+    const double fx = dmul(dsub(wphi_row<R, NC>(tc, R + 2, w), wphi_row<R, NC>(tc, R, w)), 0.5);
+    const double fy = dmul(dsub(wphi_row<R, NC>(td, R + 1, w), wphi_row<R, NC>(tu, R + 1, w)), 0.5);
+    const double h = np_hypot(fx, fy);
+    double v2;
+    if (c->model == EDGE) v2 = dmul(Iv, h);
+    else if (c->model == VECTOR) v2 = exact_v_at(c, i, x, h);
+    else v2 = exact_v_twomean(c->scal, Iv, h);
+    if (count) atomicAdd(&c->scal->fallbacks, 1ull);
+    return dadd(pc, dmul(c->dt, v2));
+  }
   uint32_t val[NC], valid[NC];
   gather_window<NR, NC>(c, bits, i - 1 - R, x - 1 - R, val, valid);
   auto ph = [&](int di, int dx) -> double {      // phi at (i + di, x + dx)
@@ -442,6 +518,11 @@ __device__ __forceinline__ void load_data_row(const FastParams& P, int i, int x0
   }
 }
 
+// fused pass: decide the guard band of the coefficients used exactly in the
+// pass (so an iteration whose coefficients did not move needs no fix list)
+#ifndef LSE_SPEC_INLINE
+#define LSE_SPEC_INLINE 1
+#endif
 // codegen knobs of the fused loop (A/B builds)
 #ifndef LSE_LUT_EXPLICIT
 #define LSE_LUT_EXPLICIT 0
@@ -615,7 +696,7 @@ __device__ __forceinline__ void phi_rows2_int(const FastParams& P, const uint32_
 template <int R, int MODEL, int CPL, int SRC, bool SPEC = false>
 __device__ __noinline__ uint32_t update_tie_cols(const FastParams& P, uint32_t lut_base, int r,
                                                  int x0, int k, float A, float B, float eps_u,
-                                                 float delta = 0.f) {
+                                                 float delta = 0.f, float eps_t = 0.f) {
   constexpr int NT = CPL + 2 * (R + 1);
   constexpr int NP = CPL + 2;
   const int y0 = r * 32;
@@ -639,8 +720,10 @@ __device__ __noinline__ uint32_t update_tie_cols(const FastParams& P, uint32_t l
     const float vf = (MODEL == REGION) ? __fmaf_rn(A, d, B) : d;
     const float u = __fmaf_rn(vf, h, pa[c + 1].y);
     // SPEC: the speculative band |u| - delta h <= e0 (eps_u holds e0), the
-    // fused loop's test on the same values
+    // fused loop's test on the same values; bits 16.. mark the band's columns
+    // within the guard eps_t of the coefficients used (decided exactly there)
     if ((SPEC ? __fmaf_rn(-delta, h, fabsf(u)) : fabsf(u)) <= eps_u) cols |= 1u << c;
+    if (SPEC && fabsf(u) <= eps_t) cols |= 1u << (16 + c);
   }
   // (all columns if nothing matched; SPEC callers flag row pairs, so a row
   // may legitimately have no match there)
@@ -691,7 +774,8 @@ __device__ __forceinline__ void update_block_int2(const FastParams& P, uint32_t 
                                                   const uint32_t (&cur)[CPL + 2 * (R + 1)],
                                                   int tile, float delta, uint32_t (&pw)[CPL],
                                                   uint32_t (&mw)[CPL], const FastParams& Pn,
-                                                  const uint32_t* wslot = nullptr) {
+                                                  const uint32_t* wslot = nullptr,
+                                                  float eps_t = 0.f) {
   // Pn: the launch parameters as seen by the noinline tie helpers (the CTA's
   // shared copy: passing the kernel parameter block by reference to a noinline
   // function makes every thread copy it to local memory first)
@@ -829,14 +913,19 @@ __device__ __forceinline__ void update_block_int2(const FastParams& P, uint32_t 
     const int k = __ffs(fbrows) - 1;
     fbrows &= fbrows - 1;
     const uint32_t bitk = 1u << k;
-    uint32_t cols =
-        update_tie_cols<R, MODEL, CPL, SRC, FUSED>(LSE_TIE_P, lut_base, r, x0, k, A, B, eps_u, delta);
+    uint32_t cols = update_tie_cols<R, MODEL, CPL, SRC, FUSED>(LSE_TIE_P, lut_base, r, x0, k, A,
+                                                               B, eps_u, delta, eps_t);
+    uint32_t exact_cols = cols >> 16;
+    cols &= 0xffffu;
     while (cols) {
       const int c = __ffs(cols) - 1;
       cols &= cols - 1;
       if (FUSED) {
-        spec_append(P, y0 + k, x0 + c);           // decided by k_spec_fix
-        continue;
+        // decided by k_spec_fix unless the coefficients turn out unchanged;
+        // the guard band of the ones used is decided exactly now (final if
+        // they are unchanged, as they are once the partition settles)
+        spec_append(P, y0 + k, x0 + c);
+        if (!LSE_SPEC_INLINE || !((exact_cols >> c) & 1u)) continue;
       }
       const bool pos = exact_u_fast<R, SRC>(tile_ctx(P, tile), tile_bits(P, tile),
                                             y0 - tile_y0(P, tile) + k, x0 + c) > 0.0;
@@ -1118,9 +1207,12 @@ __device__ __forceinline__ void update_rows_border(const FastParams& P, const fl
 #pragma unroll 1
     for (int c = 0; c < CPL; ++c) {
       if (x0 + c >= W) break;
-      if (FUSED) {                               // (the whole flagged row: a superset)
+      // fused pass: the whole flagged row goes to the fix list (a superset)
+      // and is also decided exactly with the coefficients used (final if
+      // they turn out unchanged)
+      if (FUSED) {
         spec_append(P, y0 + k, x0 + c);
-        continue;
+        if (!LSE_SPEC_INLINE) continue;
       }
       const bool pos = exact_u_fast<R, SRC>(P.ctx, P.bits_in, y0 + k, x0 + c) > 0.0;
 #pragma unroll
@@ -1492,8 +1584,17 @@ __device__ void reduce_slice(const PartRanges& R3, int t0, int t1, TilePartial* 
 // delta (1 - 2^-20) >= (that bound) (1 + 2^-20) and e0 (1 - 2^-20) >= eps_u of
 // the true coefficients give |u_t| > eps_u with sign(u_t) = sign(u_g), i.e.
 // the unflagged decisions are the ones the non-speculative update makes.
+// exact coefficients of an update (what the exact evaluators read)
+struct ExactCoefs {
+  double cp, cm, dc, peak, mid;
+  int zero;
+};
+__device__ __forceinline__ ExactCoefs exact_coefs(const Scalars* sc) {
+  return ExactCoefs{sc->c_pos, sc->c_neg, sc->dc, sc->peak, sc->mid, sc->zero_vel};
+}
+
 __device__ __forceinline__ void spec_check(Scalars* sc, float A0, float B0, float delta0, float e00,
-                                           int spec) {
+                                           int spec, const ExactCoefs& k0) {
   const double am = sc->img_absmax * (1.0 + 0x1p-20);
   const double A = sc->A, B = sc->B, a0 = A0, b0 = B0;
   const double D = (fabs(A - a0) * am + fabs(B - b0)) * (1.0 + 0x1p-40);
@@ -1504,8 +1605,16 @@ __device__ __forceinline__ void spec_check(Scalars* sc, float A0, float B0, floa
                     (double)delta0 * (1.0 - 0x1p-20) >= (D + 0x1p-22 * vfm) * (1.0 + 0x1p-20) &&
                     (double)e00 * (1.0 - 0x1p-20) >= (double)sc->eps_u;
     sc->redo = ok ? 0 : 1;
+    // coefficients bit-identical to the ones the pass used (the partition did
+    // not move): its decisions -- the guard band decided exactly in the pass
+    // -- are final and the fix list is not needed
+    const ExactCoefs k1 = exact_coefs(sc);
+    const bool same = LSE_SPEC_INLINE && (float)A == A0 && (float)B == B0 && k1.zero == k0.zero &&
+                      k1.cp == k0.cp && k1.cm == k0.cm && k1.dc == k0.dc && k1.peak == k0.peak &&
+                      k1.mid == k0.mid;
+    sc->fix_needed = same ? 0 : 1;
     if (ok) {
-      sc->spec_fixes += nfix;
+      if (!same) sc->spec_fixes += nfix;
     } else {
       sc->spec_redos += 1;
       sc->work2 = 0;
@@ -1591,6 +1700,7 @@ __device__ void finalize_cta(const PartRanges& R3, Scalars* sc, bool delta, bool
     }
     if (region) {
       const float A0 = sc->A, B0 = sc->B, delta0 = sc->spec_delta, e00 = sc->spec_e0;
+      const ExactCoefs k0 = exact_coefs(sc);
       if (delta) {
         dd_add_dd(sc->sp_hi, sc->sp_lo, sah, sal);
         dd_add_dd(sc->sp_hi, sc->sp_lo, -sbh, -sbl);
@@ -1603,7 +1713,7 @@ __device__ void finalize_cta(const PartRanges& R3, Scalars* sc, bool delta, bool
         sc->n_pos = sna;
       }
       region_coeffs(sc);
-      spec_check(sc, A0, B0, delta0, e00, spec);
+      spec_check(sc, A0, B0, delta0, e00, spec, k0);
     }
     if (ckpt) {                                    // engine.py:228-236
       sc->n_ckpt += 1;
@@ -2114,6 +2224,7 @@ __global__ void __launch_bounds__(kThreads, kFusedCtasPerSm) k_update_fused(Fast
   const Scalars* sc = P.scal;
   if (stop_flag(sc)) return;
   const float A = sc->A, B = sc->B, e0 = sc->spec_e0, delta = sc->spec_delta;
+  const float eps_t = sc->eps_u;
   const int lane = threadIdx.x & 31;
   const int nb = border_units(P.gu);
   const int nch = chunk_units(P.gu);
@@ -2189,7 +2300,7 @@ __global__ void __launch_bounds__(kThreads, kFusedCtasPerSm) k_update_fused(Fast
         // (its final cp.async wait covers the old words too)
         update_block_int2<R, REGION, CPL, SRC_SMOOTH, true>(P, luts.lt2, ring, r, x0, A, B, e0,
                                                             prev, cur, 0, delta, pw, mw, s_P,
-                                                            &win_b[0][0]);
+                                                            &win_b[0][0], eps_t);
         partition_commit<true, CKPT, false>(P, r, x0, pw, mw, d, 0, s_old);
       }
     }
@@ -2215,44 +2326,66 @@ __global__ void __launch_bounds__(kThreads, kFusedCtasPerSm) k_update_fused(Fast
   }
 }
 
-// After the finalize of a speculative update: either redo it with the true
-// coefficients (scal->redo; its own work counter scal->work2, reset by the
-// finalize) or decide the fix list's pixels exactly (u in fp64 with the
-// reference's operation order, exact_u_fast) and patch their bits.
+// After the finalize of a speculative update, two launches (both no-ops once
+// the run has stopped):
+//   k_spec_fix  -- small grid: the sticky degenerate flag, the next update's
+//                  fix-list counter, and -- unless the update is to be redone
+//                  -- the fix list's pixels decided exactly (u in fp64 in the
+//                  reference's operation order, exact_u_fast) and patched;
+//   k_spec_redo -- the update grid: returns at once unless scal->redo, else
+//                  redoes the whole update with the true coefficients (its own
+//                  work counter scal->work2, reset by the finalize).
 template <int R>
-__global__ void __launch_bounds__(kThreads, kUpdateCtasPerSm) k_spec_fix(FastParams P) {
+__global__ void __launch_bounds__(256) k_spec_fix(const FastParams P) {
+  pdl_wait();
+  pdl_launch_dependents();
+  Scalars* sc = P.scal;
+  if (stop_flag(sc)) return;
+  const bool skip = __ldcg(&sc->redo) != 0 || __ldcg(&sc->fix_needed) == 0;
+  const unsigned n = min(__ldcg(&sc->fix_n[P.fix_par]), P.fix_cap);
+  if (blockIdx.x == 0 && threadIdx.x == 0) {
+    if (sc->zero_vel && sc->model != EDGE) sc->degenerate = 1;   // sticky (engine.py:239-240)
+    sc->fix_n[P.fix_par ^ 1] = 0u;               // the next speculative update's list
+    if (!skip) sc->fallbacks += n;               // (counted once: no contended atomics)
+  }
+  if (skip) return;
+  const unsigned stride = gridDim.x * blockDim.x;
+  for (unsigned q = blockIdx.x * blockDim.x + threadIdx.x; q < n; q += stride) {
+    const int2 e = __ldcg(&P.fix[q]);
+    const bool pos = exact_u_fast<R, SRC_SMOOTH>(P.ctx, P.bits_in, e.y, e.x, false) > 0.0;
+    uint32_t* w = P.bits_out + (size_t)(e.y >> 5) * P.g.pitch_w + e.x;
+    const uint32_t bit = 1u << (e.y & 31);
+    if (pos) atomicOr(w, bit);
+    else atomicAnd(w, ~bit);
+  }
+}
+
+// the redo pass proper: a noinline body over the CTA's shared copy of the
+// parameters, so the (almost always) early-returning kernel never copies its
+// parameter block to local memory
+template <int R>
+__device__ __noinline__ void spec_redo_body(const FastParams& P, float* s_lt, float* s_ls,
+                                            float* s_ring) {
+  const SharedLuts luts{s_lt, s_ls, (uint32_t)__cvta_generic_to_shared(g_pair_lut)};
+  load_luts<R>(P, luts);
+  __syncthreads();
+  update_units<R, REGION, SRC_SMOOTH, false, 1>(P, P, luts, s_lt, s_ls, s_ring);
+}
+
+template <int R>
+__global__ void __launch_bounds__(kThreads, kUpdateCtasPerSm) k_spec_redo(const FastParams P) {
   constexpr int CPL = kUpdCols;
   constexpr int NPAT = 1 << (2 * R + 1);
   __shared__ float s_lt[NPAT];
   __shared__ float s_ls[NPAT];
   __shared__ __align__(16) float s_ring[(kThreads / 32) * kRing2 * 32 * CPL];
   __shared__ FastParams s_P;
-  const SharedLuts luts{s_lt, s_ls, (uint32_t)__cvta_generic_to_shared(g_pair_lut)};
-  load_luts<R>(P, luts);
-  if (threadIdx.x == 0) s_P = P;
-  __syncthreads();
   pdl_wait();
   pdl_launch_dependents();
-  Scalars* sc = P.scal;
-  if (stop_flag(sc)) return;
-  if (blockIdx.x == 0 && threadIdx.x == 0) {
-    if (sc->zero_vel && sc->model != EDGE) sc->degenerate = 1;   // sticky (engine.py:239-240)
-    sc->fix_n[P.fix_par ^ 1] = 0u;               // the next speculative update's list
-  }
-  if (__ldcg(&sc->redo)) {
-    update_units<R, REGION, SRC_SMOOTH, false, 1>(P, s_P, luts, s_lt, s_ls, s_ring);
-    return;
-  }
-  const unsigned n = min(__ldcg(&sc->fix_n[P.fix_par]), P.fix_cap);
-  const unsigned stride = gridDim.x * blockDim.x;
-  for (unsigned q = blockIdx.x * blockDim.x + threadIdx.x; q < n; q += stride) {
-    const int2 e = __ldcg(&P.fix[q]);
-    const bool pos = exact_u_fast<R, SRC_SMOOTH>(P.ctx, P.bits_in, e.y, e.x) > 0.0;
-    uint32_t* w = P.bits_out + (size_t)(e.y >> 5) * P.g.pitch_w + e.x;
-    const uint32_t bit = 1u << (e.y & 31);
-    if (pos) atomicOr(w, bit);
-    else atomicAnd(w, ~bit);
-  }
+  if (stop_flag(P.scal) || !__ldcg(&P.scal->redo)) return;
+  if (threadIdx.x == 0) s_P = P;
+  __syncthreads();
+  spec_redo_body<R>(s_P, s_lt, s_ls, s_ring);
 }
 
 }  // namespace lse

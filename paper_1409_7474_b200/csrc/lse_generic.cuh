@@ -437,6 +437,7 @@ __global__ void __launch_bounds__(1024) k_finalize(const TilePartial* part, int 
 
 // stage 1 of the fast path's finalize: CTA b reduces slice b of the partials
 constexpr int kFinSlices = 64;
+constexpr int kFusedFinSlices = 256;             // the fused pass's (one partial per unit)
 __global__ void __launch_bounds__(256) k_finalize_stage1(PartRanges R3, TilePartial* out,
                                                          const Scalars* sc) {
   pdl_wait();
