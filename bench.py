@@ -779,13 +779,19 @@ def main_c5(args, ws, rank, local, dist):
                           "EvolutionParams) -> ExtractionResult.mask (bool, 1 B/px); wall "
                           "clock incl. run creation and teardown, dense pass"}
 
-    # ---- roofline of one iteration (k_update + k_partition + finalize)
+    # ---- roofline of one iteration.  Fused runs: k_update_fused (the partition
+    # of b^n and the update b^n -> b^{n+1} in one pass) is the dominant kernel,
+    # the finalize / fix / redo launches are 'partition_ms'; two-pass runs
+    # (strips): k_update + k_partition (+ finalize)
     peak, peak_kind = measured_peaks()
     t_upd = upd_ms.value / max(1, n_upd.value)
     t_part = part_ms.value / max(1, n_part.value)
     t_iter = t_upd + t_part
-    canon = 12.0 * jb.npx_local       # this rank's pixels per launch pair
-    actual = (4.0 + 2.0 / 8.0 + 3.0 / 8.0) * jb.npx_local  # I + b in/out (update) + b, P in/out
+    fused = bool(spec[3])
+    canon = 12.0 * jb.npx_local       # this rank's pixels per iteration
+    # bytes actually moved per pixel-iteration: the fp32 data plane, b in and
+    # out, P read (fused: one pass); two-pass: + b and P again in the partition
+    actual = ((4.0 + 3.0 / 8.0) if fused else (4.0 + 2.0 / 8.0 + 3.0 / 8.0)) * jb.npx_local
     traffic = None
     tp = os.path.join(REPO, "profiles", "traffic_latest.json")
     if os.path.exists(tp):
@@ -796,7 +802,9 @@ def main_c5(args, ws, rank, local, dist):
                 traffic = float(td["bytes_per_iteration"])
         except Exception:
             traffic = None
-    roof = {"bound": "hbm", "kernel": "k_update + k_partition (+ finalize): one LSE iteration",
+    roof = {"bound": "hbm",
+            "kernel": ("k_update_fused + finalize + fix (one-pass speculative LSE iteration)"
+                       if fused else "k_update + k_partition (+ finalize): one LSE iteration"),
             "achieved": canon / (t_iter / 1e3) / 1e9 if t_iter > 0 else None,
             "peak": peak, "unit": "GB/s",
             "frac": (canon / (t_iter / 1e3) / 1e9) / peak if t_iter > 0 else None,
