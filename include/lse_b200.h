@@ -228,6 +228,15 @@ int lse_strip_prepare(lse_run* run, void* partial_out);
 int lse_strip_update(lse_run* run, int* partition_next);
 int lse_strip_partition(lse_run* run, void* partial_out);
 int lse_strip_finalize(lse_run* run, const void* partials, int n_partials, int absolute);
+/* One-pass iteration of a strip (the speculative fused pass):
+ * the partition of the current state -- owed by the last lse_strip_update or
+ * lse_strip_fused -- and the update of the next iteration in one launch
+ * sequence; partial_out receives this rank's partition partial.  The ranks
+ * exchange them, lse_strip_finalize(absolute = 0) checks the prediction and
+ * decides the undecided pixels (or redoes the update); only then exchange the
+ * halo rows.  LSE_ERR_UNSUPPORTED when the strip runs the two-pass iteration
+ * (lse_run_spec_stats out[3] == 0). */
+int lse_strip_fused(lse_run* run, void* partial_out);
 int lse_strip_sync(lse_run* run, lse_status* st);
 void* lse_run_stream(lse_run* run);
 void* lse_run_bits_row(lse_run* run, int word_row);

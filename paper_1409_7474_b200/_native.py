@@ -109,6 +109,7 @@ _SIGS = {
     "lse_strip_update": (_i, [_vp, C.POINTER(C.c_int)]),
     "lse_strip_partition": (_i, [_vp, _vp]),
     "lse_strip_finalize": (_i, [_vp, _vp, _i, _i]),
+    "lse_strip_fused": (_i, [_vp, _vp]),
     "lse_strip_sync": (_i, [_vp, C.POINTER(LseStatus)]),
     "lse_run_stream": (_vp, [_vp]),
     "lse_run_bits_row": (_vp, [_vp, _i]),

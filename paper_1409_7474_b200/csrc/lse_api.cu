@@ -308,6 +308,8 @@ struct lse_run {
   cudaEvent_t pev[2] = {nullptr, nullptr};       // profiling events of the pending update
   // speculative fused iteration (k_update_fused): eligible runs, fix list
   bool fused = false;
+  bool strip_fused = false;      // the partials owed to lse_strip_finalize came from a fused pass
+  FastParams strip_fp{};         // ... whose fix / redo launches follow that finalize
   int2* d_fix = nullptr;
   unsigned int fix_cap = 0;
   long long fused_iters = 0;
@@ -740,8 +742,20 @@ int launch_fast(lse_run* r, long long it, bool ckpt, int phase = PH_BOTH) {
 // and the update it-1 -> it in one pass, then the finalize of iteration it-1
 // (true coefficients of update it, prediction check) and k_spec_fix (fix list
 // or full redo).  Only after an update whose partition is still owed.
+// the fix-list decision and the redo pass after a fused pass's finalize
 template <int R>
-int launch_fused_R(lse_run* r, long long it, bool ckpt_prev) {
+int launch_spec_tail(lse_run* r, const FastParams& P) {
+  TRY(launch_pdl(k_spec_fix<R>, num_sms(), 256, r->st, P));
+  FastParams Q = P;                              // the redo pass has its own work counter
+  Q.work = &r->d_scal->work2;
+  Q.work_base = 0;
+  const long long n = r->nb_upd[0] + r->ni_upd;
+  TRY(launch_pdl(k_spec_redo<R>, fast_grid(n, kUpdateCtasPerSm), kThreads, r->st, Q));
+  return LSE_OK;
+}
+
+template <int R>
+int launch_fused_R(lse_run* r, long long it, bool ckpt_prev, TilePartial* strip_out = nullptr) {
   FastParams P = fast_params(r);
   P.iter = it - 1;
   set_check(P, it);
@@ -770,7 +784,18 @@ int launch_fused_R(lse_run* r, long long it, bool ckpt_prev) {
   if (r->prof) cudaEventRecord(e1, r->st);
   PartRanges R3{{r->d_part, r->d_part, r->d_part}, {(int)n, 0, 0}};
   const int spec = 1 + P.fix_par;
-  if (n <= r->onestage_max) {
+  if (strip_out) {
+    // row strips: this rank's partial of the partition of b^{it-1}; the ranks
+    // exchange them, then lse_strip_finalize checks the prediction and
+    // launches the fix / redo pass (launch_spec_tail)
+    TRY(launch_pdl(k_finalize_stage1, kFusedFinSlices, 256, r->st, R3, r->d_part_fin,
+                   (const Scalars*)r->d_scal));
+    PartRanges R1{{r->d_part_fin, r->d_part_fin, r->d_part_fin}, {kFusedFinSlices, 0, 0}};
+    k_reduce_to_one<<<1, 256, 0, r->st>>>(R1, strip_out, r->d_scal, 1);
+    CKL();
+    r->strip_fused = true;
+    r->strip_fp = P;
+  } else if (n <= r->onestage_max) {
     TRY(launch_pdl(k_finalize_run, 1, 64, r->st, R3, r->d_scal, 1, ckpt_prev ? 1 : 0, it - 1,
                    spec));
   } else {
@@ -781,11 +806,7 @@ int launch_fused_R(lse_run* r, long long it, bool ckpt_prev) {
     TRY(launch_pdl(k_finalize_run, 1, 64, r->st, R1, r->d_scal, 1, ckpt_prev ? 1 : 0, it - 1,
                    spec));
   }
-  TRY(launch_pdl(k_spec_fix<R>, num_sms(), 256, r->st, P));
-  FastParams Q = P;                              // the redo pass has its own work counter
-  Q.work = &r->d_scal->work2;
-  Q.work_base = 0;
-  TRY(launch_pdl(k_spec_redo<R>, fast_grid(n, kUpdateCtasPerSm), kThreads, r->st, Q));
+  if (!strip_out) TRY(launch_spec_tail<R>(r, P));
   if (r->prof) {
     cudaEvent_t e2 = next_event(r);
     cudaEventRecord(e2, r->st);
@@ -799,12 +820,22 @@ int launch_fused_R(lse_run* r, long long it, bool ckpt_prev) {
   return LSE_OK;
 }
 
-int launch_fused(lse_run* r, long long it, bool ckpt_prev) {
+int launch_fused(lse_run* r, long long it, bool ckpt_prev, TilePartial* strip_out = nullptr) {
   switch (r->R) {
-    case 1: return launch_fused_R<1>(r, it, ckpt_prev);
-    case 2: return launch_fused_R<2>(r, it, ckpt_prev);
-    case 3: return launch_fused_R<3>(r, it, ckpt_prev);
-    case 4: return launch_fused_R<4>(r, it, ckpt_prev);
+    case 1: return launch_fused_R<1>(r, it, ckpt_prev, strip_out);
+    case 2: return launch_fused_R<2>(r, it, ckpt_prev, strip_out);
+    case 3: return launch_fused_R<3>(r, it, ckpt_prev, strip_out);
+    case 4: return launch_fused_R<4>(r, it, ckpt_prev, strip_out);
+  }
+  return fail(LSE_ERR_ARG, "unsupported template radius");
+}
+
+int launch_spec_tail_any(lse_run* r, const FastParams& P) {
+  switch (r->R) {
+    case 1: return launch_spec_tail<1>(r, P);
+    case 2: return launch_spec_tail<2>(r, P);
+    case 3: return launch_spec_tail<3>(r, P);
+    case 4: return launch_spec_tail<4>(r, P);
   }
   return fail(LSE_ERR_ARG, "unsupported template radius");
 }
@@ -1473,7 +1504,7 @@ int create_impl(lse_run** out, const lse_params* p, long long height, long long 
   // of the region / zhang models with unsplit update units; LSE_FUSED=0 keeps
   // the two-pass iteration (A/B); validation builds check the two-pass path
   {
-    bool fz = !r->strip && !r->fine && r->split_parts == 1 && r->R >= 1 && r->R <= 4 &&
+    bool fz = !r->fine && r->split_parts == 1 && r->R >= 1 && r->R <= 4 &&
               (p->model == LSE_MODEL_REGION || p->model == LSE_MODEL_ZHANG);
 #ifdef LSE_CHECK_BOUND
     fz = false;
@@ -1645,6 +1676,10 @@ int lse_strip_prepare(lse_run* r, void* part_out) {
   TRY(upload_ctx(r));
   CK(cudaMemsetAsync(r->d_work, 0, sizeof(unsigned long long), r->st));
   r->work_next = 0;
+  r->strip_fused = false;
+  if (r->fused)
+    CK(cudaMemsetAsync(reinterpret_cast<char*>(r->d_scal) + offsetof(Scalars, fix_n), 0,
+                       sizeof(unsigned int) * 2, r->st));
   const dim3 gr((r->g.pitch_w + 1023) / 1024, r->g.HR);
   k_partition_init_bits<<<gr, 256, 0, r->st>>>(r->d_bits[r->cur], r->d_ctx, r->d_P,
                                                r->d_part_init, r->g, r->own_lo, r->own_hi);
@@ -1677,6 +1712,23 @@ int lse_strip_partition(lse_run* r, void* part_out) {
   return LSE_OK;
 }
 
+int lse_strip_fused(lse_run* r, void* part_out) {
+  if (!r || !r->strip || !part_out) return fail(LSE_ERR_ARG, "bad arguments");
+  if (!r->fused)
+    return fail(LSE_ERR_UNSUPPORTED, "this strip runs the two-pass iteration (lse_strip_update)");
+  if (!r->prepared || !r->strip_part || r->strip_fused)
+    return fail(LSE_ERR_ARG, "lse_strip_fused follows an update whose partition is owed");
+  if (r->mode == SRC_FIELD || !fp32_ok(r))
+    return fail(LSE_ERR_UNSUPPORTED, "row strips need a binary state on the fast path");
+  const long long it = r->iteration + 1;
+  TRY(launch_fused(r, it, r->strip_ckpt, (TilePartial*)part_out));
+  r->iteration = it;
+  r->fast_iters++;
+  r->strip_part = true;                          // b^{it}'s partition is owed now
+  r->strip_ckpt = it % r->p.conv_check_every == 0;
+  return LSE_OK;
+}
+
 int lse_strip_finalize(lse_run* r, const void* parts, int nparts, int absolute) {
   if (!r || !r->strip || !parts || nparts < 1) return fail(LSE_ERR_ARG, "bad arguments");
   const TilePartial* tp = (const TilePartial*)parts;
@@ -1688,8 +1740,19 @@ int lse_strip_finalize(lse_run* r, const void* parts, int nparts, int absolute) 
     r->prepared = true;
     return LSE_OK;
   }
-  if (!r->strip_part) return LSE_OK;
   PartRanges R{{tp, tp, tp}, {nparts, 0, 0}};
+  if (r->strip_fused) {
+    // the partition of iteration it-1 (fused pass): its coefficients check
+    // the speculative update it, then the fix list or the redo
+    const FastParams& P = r->strip_fp;
+    k_finalize_run<<<1, 64, 0, r->st>>>(R, r->d_scal, 1, (P.iter % r->p.conv_check_every) == 0,
+                                          P.iter, 1 + P.fix_par);
+    CKL();
+    TRY(launch_spec_tail_any(r, P));
+    r->strip_fused = false;
+    return LSE_OK;
+  }
+  if (!r->strip_part) return LSE_OK;
   k_finalize_run<<<1, 64, 0, r->st>>>(R, r->d_scal, two_mean(r->p.model) ? 1 : 0,
                                         r->strip_ckpt ? 1 : 0, r->iteration, 0);
   CKL();

@@ -206,10 +206,15 @@ class DistComm:
 class StripDriver:
     """Runs the phases of the local strips in lock step with the other ranks."""
 
-    def __init__(self, strips, comm):
+    def __init__(self, strips, comm, fused=None):
         self.strips = list(strips)
         self.comm = comm
         self.iteration = 0
+        # one-pass iterations when every strip runs them (the same on every
+        # rank: the strips' geometry decides; fused=False forces two passes)
+        ok = all(getattr(s, "supports_fused", False) for s in self.strips)
+        self.fused = ok if fused is None else (bool(fused) and ok)
+        self._owed = False
 
     def setup(self):
         """Global image range, initial partition sums, seed-count check."""
@@ -225,6 +230,7 @@ class StripDriver:
     def initialize(self):
         """Partition sums of the initial state, seed-count check (engine.py:202-216)."""
         self.iteration = 0
+        self._owed = False
         parts = [s.prepare() for s in self.strips]
         gathered = self.comm.allgather(parts)
         for s in self.strips:
@@ -242,17 +248,39 @@ class StripDriver:
             s.finalize(g, absolute=True)
 
     def step(self):
-        need = [s.update() for s in self.strips]
-        self.comm.exchange_halos()
-        if need[0]:
-            parts = [s.partition() for s in self.strips]
+        if self.fused and self._owed:
+            # partition of b^n + speculative update -> exchange partials ->
+            # check / fix / redo -> halo rows of the final b^{n+1}
+            parts = [s.fused() for s in self.strips]
             for s, g in zip(self.strips, self.comm.allgather(parts)):
                 s.finalize(g, absolute=False)
+            self.comm.exchange_halos()
+            self.iteration += 1
+            return
+        need = [s.update() for s in self.strips]
+        self.comm.exchange_halos()
+        if need[0] and self.fused:
+            self._owed = True           # taken by the next fused pass or flush()
+        elif need[0]:
+            self._partition()
         self.iteration += 1
+
+    def _partition(self):
+        parts = [s.partition() for s in self.strips]
+        for s, g in zip(self.strips, self.comm.allgather(parts)):
+            s.finalize(g, absolute=False)
+
+    def flush(self):
+        """The partition owed by the last update (convergence bookkeeping and
+        the coefficients of the next iteration)."""
+        if self._owed:
+            self._partition()
+            self._owed = False
 
     def advance(self, n):
         for _ in range(int(n)):
             self.step()
+        self.flush()
         return [s.sync() for s in self.strips]
 
 
@@ -352,6 +380,18 @@ class DeviceStrip:
 
     def partition(self):
         self.N.check(self.N.lib.lse_strip_partition(self.h, C.c_void_p(self._part.data_ptr())))
+        return self._part
+
+    @property
+    def supports_fused(self):
+        out = (C.c_longlong * 4)()
+        self.N.check(self.N.lib.lse_run_spec_stats(self.h, out))
+        return bool(out[3])
+
+    def fused(self):
+        """One-pass iteration: the owed partition + the next (speculative)
+        update; returns this rank's partition partial."""
+        self.N.check(self.N.lib.lse_strip_fused(self.h, C.c_void_p(self._part.data_ptr())))
         return self._part
 
     def finalize(self, gathered, absolute):

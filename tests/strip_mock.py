@@ -150,7 +150,23 @@ class MockStrip:
             q[6] = mism
         return part
 
+    # the one-pass protocol (lse_strip_fused): the partition of the current
+    # state now, the update once the gathered partials fixed the coefficients
+    # -- the device's speculative pass + fix / redo produce exactly that
+    supports_fused = True
+
+    def fused(self):
+        part = self.partition()
+        self._pending_update = True
+        return part
+
     def finalize(self, gathered, absolute):
+        self._finalize(gathered, absolute)
+        if getattr(self, "_pending_update", False) and not absolute:
+            self._pending_update = False
+            self.update()
+
+    def _finalize(self, gathered, absolute):
         if self.stop and not absolute:
             return
         a, b, na, nb, mism = _unpack(gathered)

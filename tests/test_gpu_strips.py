@@ -65,6 +65,38 @@ def test_c5_crop_strips(world):
     check(sc.image, seeds, params("region", **sc.params), 60, world)
 
 
+@pytest.mark.parametrize("world", [2, 3, 5])
+def test_c5_crop_strips_fused(world, monkeypatch):
+    """Unsplit units (as at full size): every strip runs the one-pass
+    iteration (lse_strip_fused: partition + speculative update -> partial
+    exchange -> check / fix / redo -> halos) and reproduces the single run."""
+    monkeypatch.setenv("LSE_SPLIT_PARTS", "1")
+    sc = scenes.config5_crop(1024, 60)
+    seeds = L.SeedSpec(polygons=sc.polygons, inside_sign=sc.inside_sign)
+    prm = params("region", **sc.params)
+    ref = single(sc.image, seeds, prm, 60)
+    drv, strips, st = run_local_strips(sc.image, seeds, prm, world, 60)
+    assert drv.fused
+    phi = np.concatenate([s.own_phi() for s in strips])
+    assert np.array_equal(phi, ref.state.phi), np.abs(phi - ref.state.phi).max()
+    for s in st:
+        assert s.iteration == ref.state.iteration
+
+
+def test_small_strips_fused_converge(monkeypatch):
+    """Border-only strips on the one-pass iteration, converging mid-run."""
+    monkeypatch.setenv("LSE_SPLIT_PARTS", "1")
+    img, seeds = scene()
+    prm = params("region", max_iters=300, conv_check_every=3, conv_window=2)
+    ref = single(img, seeds, prm, 300)
+    drv, strips, st = run_local_strips(img, seeds, prm, 3, 300)
+    assert drv.fused
+    phi = np.concatenate([s.own_phi() for s in strips])
+    assert np.array_equal(phi, ref.state.phi)
+    for s in st:
+        assert s.iteration == ref.state.iteration and bool(s.converged) == ref.converged
+
+
 def test_strip_degenerate_seed_is_global():
     img, _ = scene()
     seeds = L.SeedSpec(polygons=(square(0, 0, 70, 150),), inside_sign=1)

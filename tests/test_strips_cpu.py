@@ -67,11 +67,15 @@ def test_plan_strips_partition_word_rows(h, world):
         plan_strips(h, 10, hr + 1)
 
 
+@pytest.mark.parametrize("fused", [True, False])
 @pytest.mark.parametrize("model,world,kw", [
     ("region", 2, {}), ("region", 4, {}), ("edge", 3, {}), ("zhang", 2, {}),
     ("region", 3, {"conv_check_every": 3, "conv_window": 2, "max_iters": 80}),
 ])
-def test_local_strips_match_single_grid(model, world, kw):
+def test_local_strips_match_single_grid(model, world, kw, fused):
+    """Both protocols of the driver: update -> halo -> partition -> allgather ->
+    finalize, and the one-pass one (partition + next update -> allgather ->
+    finalize (+ fix / redo) -> halo, the owed partition flushed at the end)."""
     img, seeds = scene()
     kw.setdefault("max_iters", 25)
     prm = params(model, **kw)
@@ -79,7 +83,8 @@ def test_local_strips_match_single_grid(model, world, kw):
     ref = oracle_run(img, seeds, prm, iters)
     wins = plan_strips(img.shape[0], img.shape[1], world)
     strips = [MockStrip(strip_rows(img, w), w, seeds, prm) for w in wins]
-    drv = StripDriver(strips, LocalComm(strips))
+    drv = StripDriver(strips, LocalComm(strips), fused=fused)
+    assert drv.fused == fused
     drv.setup()
     st = drv.advance(iters)
     phi = np.concatenate([s.own_phi() for s in strips])
