@@ -138,3 +138,45 @@ def test_degenerate_and_dense(monkeypatch):
     a.advance(25)
     monkeypatch.setenv("LSE_FUSED", "0")
     same(a, make_run(img, seeds, prm, [25]))
+
+
+FUZZ_SHAPES = [(33, 31), (64, 257), (65, 264), (129, 70), (200, 520), (257, 263), (70, 1030),
+               (1030, 70), (300, 777)]
+
+
+@pytest.mark.parametrize("h,w", FUZZ_SHAPES)
+@pytest.mark.parametrize("model,ts,f64", [("region", 9, False), ("region", 5, True),
+                                          ("zhang", 7, False), ("region", 3, True)])
+def test_fused_fuzz_geometry(h, w, model, ts, f64, monkeypatch):
+    """Fused pass on every unit decomposition edge case (border-only images,
+    partial word-rows, right tails / B1 packs), fp32 and float64 inputs (the
+    exact data plane), random checkpoint cadence with convergence, chunked
+    advance: identical to the two-pass iteration in every field, and to the
+    oracle's trajectory."""
+    tiled_env(monkeypatch)
+    rng = np.random.default_rng(7 * h + 13 * w + ts)
+    img = np.clip(0.3 + 0.4 * (rng.random((h, w)) > 0.6) + 0.05 * rng.standard_normal((h, w)),
+                  0, 1)
+    if not f64:
+        img = img.astype(np.float32)
+    y0, x0 = rng.integers(0, max(1, h // 3)), rng.integers(0, max(1, w // 3))
+    y1, x1 = h - rng.integers(0, max(1, h // 3)), w - rng.integers(0, max(1, w // 3))
+    poly = np.array([[x0 + 0.2, y0 + 0.2], [x1 - 0.2, y0 + 0.2], [x1 - 0.2, y1 - 0.2],
+                     [x0 + 0.2, y1 - 0.2]])
+    sign = 1 if rng.random() > 0.5 else -1
+    if O.rasterize_seeds([poly], sign, w, h) is None:
+        pytest.skip("degenerate seed for this draw")
+    cce = int(rng.integers(2, 6))
+    prm = params(model, ts_reg=ts, max_iters=60, conv_check_every=cce, conv_window=2)
+    seeds = L.SeedSpec(polygons=(poly,), inside_sign=sign)
+    chunks = [int(c) for c in rng.integers(1, 9, size=12)]
+    fused = make_run(img, seeds, prm, chunks)
+    monkeypatch.setenv("LSE_FUSED", "0")
+    plain = make_run(img, seeds, prm, chunks)
+    same(fused, plain)
+    it = fused.state.iteration
+    phi0 = O.rasterize_seeds([poly], sign, w, h)
+    ref = O.run_fixed(np.asarray(img, dtype=np.float64), phi0,
+                      O.OracleParams(model=model, ts_reg=ts, max_iters=it,
+                                     conv_check_every=it + 1), it)
+    assert np.array_equal(fused.state.phi, ref.phi)
