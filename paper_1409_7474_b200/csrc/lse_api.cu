@@ -402,6 +402,7 @@ FastParams fast_params(lse_run* r) {
   P.own_hi = r->own_hi;
   P.chg = is_bands(r) ? r->d_chg : nullptr;
   P.ntiles = 1;
+  P.fix_cnt = r->d_scal->fix_n;                  // (device address: no dereference)
   P.tile_hr = r->g.HR;
   P.tile_h = r->H;
   P.tile_words = (long long)r->g.HR * r->g.pitch_w;
@@ -745,12 +746,12 @@ int launch_fast(lse_run* r, long long it, bool ckpt, int phase = PH_BOTH) {
 // the fix-list decision and the redo pass after a fused pass's finalize
 template <int R>
 int launch_spec_tail(lse_run* r, const FastParams& P) {
-  TRY(launch_pdl(k_spec_fix<R>, num_sms(), 256, r->st, P));
+  TRY(launch_pdl(k_spec_fix<R, false>, num_sms(), 256, r->st, P));
   FastParams Q = P;                              // the redo pass has its own work counter
   Q.work = &r->d_scal->work2;
   Q.work_base = 0;
   const long long n = r->nb_upd[0] + r->ni_upd;
-  TRY(launch_pdl(k_spec_redo<R>, fast_grid(n, kUpdateCtasPerSm), kThreads, r->st, Q));
+  TRY(launch_pdl(k_spec_redo<R, false>, fast_grid(n, kUpdateCtasPerSm), kThreads, r->st, Q));
   return LSE_OK;
 }
 
@@ -775,11 +776,11 @@ int launch_fused_R(lse_run* r, long long it, bool ckpt_prev, TilePartial* strip_
   }
   constexpr size_t smem = fused_smem_bytes<R>();
   if (ckpt_prev) {
-    TRY(prepare_smem(k_update_fused<R, true>, smem));
-    TRY(launch_pdl_smem(k_update_fused<R, true>, g, kThreads, smem, r->st, P));
+    TRY(prepare_smem(k_update_fused<R, true, false>, smem));
+    TRY(launch_pdl_smem(k_update_fused<R, true, false>, g, kThreads, smem, r->st, P));
   } else {
-    TRY(prepare_smem(k_update_fused<R, false>, smem));
-    TRY(launch_pdl_smem(k_update_fused<R, false>, g, kThreads, smem, r->st, P));
+    TRY(prepare_smem(k_update_fused<R, false, false>, smem));
+    TRY(launch_pdl_smem(k_update_fused<R, false, false>, g, kThreads, smem, r->st, P));
   }
   if (r->prof) cudaEventRecord(e1, r->st);
   PartRanges R3{{r->d_part, r->d_part, r->d_part}, {(int)n, 0, 0}};
@@ -1608,6 +1609,12 @@ int create_impl(lse_run** out, const lse_params* p, long long height, long long 
   s0.eps_u = (float)edge_eps_u(p->dt);
   s0.spec_delta = -1.0f;
   s0.fix_cap = r->fix_cap;
+  if (p->model == LSE_MODEL_EDGE) {
+    // a batched edge tile runs the fused pass with its exact coefficients:
+    // band = the guard band, decided exactly in the pass, no fix list
+    s0.spec_delta = 0.0f;
+    s0.spec_e0 = (float)(edge_eps_u(p->dt) * 1.25);
+  }
   if (p->model == LSE_MODEL_EDGE) s0.A = 1.0f;   // vf = 1 * g + 0 in a batched launch
   if (cudaMemcpyAsync(r->d_scal, &s0, sizeof(s0), cudaMemcpyHostToDevice, r->st) != cudaSuccess)
     return cleanup(fail(LSE_ERR_CUDA, "scalar upload failed"));
@@ -2061,6 +2068,10 @@ struct lse_batch {
   long long tile_words = 0, tile_data = 0, nb_upd = 0, ni_upd = 0, nb_part = 0, ni_part = 0;
   int tile_hr = 0;
   int cur = 0;
+  // speculative fused iterations (batches with region / zhang tiles)
+  bool fused = false;
+  int2* fix = nullptr;
+  unsigned int fix_cap = 0;
   // device-event timing of whole lse_batch_advance calls (bench support)
   bool timing = false;
   cudaEvent_t ev[2] = {nullptr, nullptr};
@@ -2104,6 +2115,9 @@ FastParams batch_params(lse_batch* b, int sel) {
   P.g.HR = b->T * b->tile_hr;
   P.own_lo = 0;
   P.own_hi = P.g.HR;
+  P.fix = b->fix;
+  P.fix_cap = b->fix_cap;
+  P.fix_cnt = b->scal->fix_n;                 // the batch's counters: tile 0's scalars
   return P;
 }
 
@@ -2113,8 +2127,9 @@ unsigned long long batch_take_work(lse_batch* b, long long units, int grid) {
   return base;
 }
 
+// phase: the batched plain update of iteration it (b^{it-1} -> b^{it})
 template <int R>
-int batch_iteration(lse_batch* b, long long it, bool ckpt, int src, bool any_region) {
+int batch_update(lse_batch* b, long long it, int src) {
   FastParams P = batch_params(b, b->cur);
   P.iter = it;
   set_check(P, it);
@@ -2135,7 +2150,17 @@ int batch_iteration(lse_batch* b, long long it, bool ckpt, int src, bool any_reg
 #endif
   }
   b->cur ^= 1;
+  return LSE_OK;
+}
+
+// phase: the batched partition / checkpoint pass over the current state
+// (iteration it) and the per-tile finalize
+template <int R>
+int batch_partition(lse_batch* b, long long it, bool ckpt, bool any_region) {
   if (!any_region && !ckpt) return LSE_OK;
+  FastParams P = batch_params(b, b->cur);
+  P.iter = it;
+  set_check(P, it);
   P.bits_in = b->bits[b->cur];
   const long long n = (long long)b->T * (b->nb_part + b->ni_part);
   const int g = fast_grid(n, kPartitionCtasPerSm);
@@ -2150,14 +2175,62 @@ int batch_iteration(lse_batch* b, long long it, bool ckpt, int src, bool any_reg
 #endif
   if (b->nb_part + b->ni_part <= b->runs[0]->onestage_max) {   // as a lone tile: one stage
     TRY(launch_pdl(k_finalize_tiles_direct, b->T, 64, b->st, (const TilePartial*)b->part, b->scal,
-                   (int)b->nb_part, (int)b->ni_part, b->T, ckpt ? 1 : 0, it));
+                   (int)b->nb_part, (int)b->ni_part, b->T, ckpt ? 1 : 0, it, 0));
     return LSE_OK;
   }
   TRY(launch_pdl(k_finalize_stage1_tiles, dim3(kFinSlices, b->T), 256, b->st,
                  (const TilePartial*)b->part, b->part_fin, (const Scalars*)b->scal,
                  (int)b->nb_part, (int)b->ni_part, b->T, ckpt ? 1 : 0));
   TRY(launch_pdl(k_finalize_run_tiles, b->T, 64, b->st, (const TilePartial*)b->part_fin,
-                 b->scal, ckpt ? 1 : 0, it));
+                 b->scal, ckpt ? 1 : 0, it, 0));
+  return LSE_OK;
+}
+
+template <int R>
+int batch_iteration(lse_batch* b, long long it, bool ckpt, int src, bool any_region) {
+  TRY(batch_update<R>(b, it, src));
+  return batch_partition<R>(b, it, ckpt, any_region);
+}
+
+// One speculative fused iteration of every tile (batched): the
+// partition of b^{it-1} (its checkpoint when ckpt_prev) and the update it-1 ->
+// it in one pass, the per-tile finalize with each region tile's prediction
+// check, the fix list, the redo of the tiles that need it.
+template <int R>
+int batch_fused(lse_batch* b, long long it, bool ckpt_prev) {
+  FastParams P = batch_params(b, b->cur);
+  P.iter = it - 1;
+  set_check(P, it);
+  P.fix_par = (int)(it & 1);
+  const long long nu = b->nb_upd + b->ni_upd;
+  const long long n = (long long)b->T * nu;
+  const int g = fast_grid(n, kFusedCtasPerSm);
+  P.work_base = batch_take_work(b, n, g);
+  constexpr size_t smem = fused_smem_bytes<R>();
+  if (ckpt_prev) {
+    TRY(prepare_smem(k_update_fused<R, true, true>, smem));
+    TRY(launch_pdl_smem(k_update_fused<R, true, true>, g, kThreads, smem, b->st, P));
+  } else {
+    TRY(prepare_smem(k_update_fused<R, false, true>, smem));
+    TRY(launch_pdl_smem(k_update_fused<R, false, true>, g, kThreads, smem, b->st, P));
+  }
+  const int spec = 1 + P.fix_par;
+  if (nu <= b->runs[0]->onestage_max) {
+    TRY(launch_pdl(k_finalize_tiles_direct, b->T, 64, b->st, (const TilePartial*)b->part, b->scal,
+                   (int)b->nb_upd, (int)b->ni_upd, b->T, ckpt_prev ? 1 : 0, it - 1, spec));
+  } else {
+    TRY(launch_pdl(k_finalize_stage1_tiles, dim3(kFinSlices, b->T), 256, b->st,
+                   (const TilePartial*)b->part, b->part_fin, (const Scalars*)b->scal,
+                   (int)b->nb_upd, (int)b->ni_upd, b->T, ckpt_prev ? 1 : 0));
+    TRY(launch_pdl(k_finalize_run_tiles, b->T, 64, b->st, (const TilePartial*)b->part_fin,
+                   b->scal, ckpt_prev ? 1 : 0, it - 1, spec));
+  }
+  TRY(launch_pdl(k_spec_fix<R, true>, num_sms(), 256, b->st, P));
+  FastParams Q = P;                              // the redo pass has its own work counter
+  Q.work = &b->scal->work2;
+  Q.work_base = 0;
+  TRY(launch_pdl(k_spec_redo<R, true>, fast_grid(n, kUpdateCtasPerSm), kThreads, b->st, Q));
+  b->cur ^= 1;
   return LSE_OK;
 }
 
@@ -2216,6 +2289,29 @@ int lse_batch_create(lse_batch** out, lse_run* const* runs, int n) {
     return cleanup(rc);
   if (cudaMallocHost((void**)&b->h_scal, n * sizeof(Scalars)) != cudaSuccess)
     return cleanup(fail(LSE_ERR_CUDA, "pinned alloc failed"));
+  {
+    // batched fused iterations are opt-in (LSE_FUSED_BATCH=1): on C4's
+    // 1024^2 tiles the border units -- ~30 % of the update's work -- pay the
+    // partition's zero-padded recomputation on top of the update's, and the
+    // fused pass measured 306 us vs 126 + 65 us for update + partition (64
+    // tiles); the next step is deriving the border partition from the
+    // update's own phi rows, as the interior units do
+    bool fz = true;
+#ifdef LSE_CHECK_BOUND
+    fz = false;
+#endif
+    const char* bv = std::getenv("LSE_FUSED_BATCH");
+    fz = fz && bv && std::atoi(bv) != 0;
+    if (const char* fv = std::getenv("LSE_FUSED")) fz = fz && std::atoi(fv) != 0;
+    b->fused = fz;
+    if (fz) {
+      const long long px = (long long)n * r0->H * r0->W;
+      b->fix_cap = (unsigned)std::min<long long>(std::max<long long>(px / 256, 4096), 1LL << 22);
+      if (const char* cv = std::getenv("LSE_FIX_CAP"))
+        b->fix_cap = (unsigned)std::max(0LL, std::atoll(cv));
+      if ((rc = dalloc(&b->fix, std::max<unsigned>(1u, b->fix_cap)))) return cleanup(rc);
+    }
+  }
   // static data planes and per-tile contexts (tile t at word-row t * tile_hr)
   std::vector<ExactCtx> ctx(n);
   for (int t = 0; t < n; ++t) {
@@ -2284,18 +2380,55 @@ int lse_batch_advance(lse_batch* b, long long n_steps, lse_status* statuses) {
     b->work_next = 0;
     bool any_region = false;
     for (auto* r : b->runs) any_region |= two_mean(r->p.model);
+    // speculative fused iterations when some tile has a partition to compute
+    // every iteration (edge-only batches keep the update-only iterations)
+    const bool fz = b->fused && any_region;
+    if (fz) {
+      // fresh fix-list counters, its capacity and the batch redo flag (tile
+      // 0's scalars hold the batch's list state)
+      CK(cudaMemsetAsync(reinterpret_cast<char*>(b->scal) + offsetof(Scalars, fix_n), 0,
+                         sizeof(unsigned int) * 2, b->st));
+      CK(cudaMemsetAsync(reinterpret_cast<char*>(b->scal) + offsetof(Scalars, redo_any), 0,
+                         sizeof(int), b->st));
+      CK(cudaMemcpyAsync(reinterpret_cast<char*>(b->scal) + offsetof(Scalars, fix_cap),
+                         &b->fix_cap, sizeof(unsigned int), cudaMemcpyHostToDevice, b->st));
+    }
+    const long long cce = r0->p.conv_check_every;
+    bool owe = false;                            // the partition of owe_it is owed (fused)
+    long long owe_it = 0;
     int src_mode = r0->mode;
     for (long long it = it0 + 1; it <= it0 + steps; ++it) {
-      const bool ckpt = it % r0->p.conv_check_every == 0;
+      const bool ckpt = it % cce == 0;
       int rc = LSE_ERR_ARG;
       switch (r0->R) {
-        case 1: rc = batch_iteration<1>(b, it, ckpt, src_mode, any_region); break;
-        case 2: rc = batch_iteration<2>(b, it, ckpt, src_mode, any_region); break;
-        case 3: rc = batch_iteration<3>(b, it, ckpt, src_mode, any_region); break;
-        case 4: rc = batch_iteration<4>(b, it, ckpt, src_mode, any_region); break;
+        case 1: rc = fz && owe ? batch_fused<1>(b, it, owe_it % cce == 0)
+                 : fz ? batch_update<1>(b, it, src_mode)
+                      : batch_iteration<1>(b, it, ckpt, src_mode, any_region); break;
+        case 2: rc = fz && owe ? batch_fused<2>(b, it, owe_it % cce == 0)
+                 : fz ? batch_update<2>(b, it, src_mode)
+                      : batch_iteration<2>(b, it, ckpt, src_mode, any_region); break;
+        case 3: rc = fz && owe ? batch_fused<3>(b, it, owe_it % cce == 0)
+                 : fz ? batch_update<3>(b, it, src_mode)
+                      : batch_iteration<3>(b, it, ckpt, src_mode, any_region); break;
+        case 4: rc = fz && owe ? batch_fused<4>(b, it, owe_it % cce == 0)
+                 : fz ? batch_update<4>(b, it, src_mode)
+                      : batch_iteration<4>(b, it, ckpt, src_mode, any_region); break;
       }
       TRY(rc);
+      owe = fz;
+      owe_it = it;
       src_mode = SRC_SMOOTH;
+    }
+    if (owe) {                                   // the partition of the last iteration
+      int rc = LSE_ERR_ARG;
+      const bool ck = owe_it % cce == 0;
+      switch (r0->R) {
+        case 1: rc = batch_partition<1>(b, owe_it, ck, any_region); break;
+        case 2: rc = batch_partition<2>(b, owe_it, ck, any_region); break;
+        case 3: rc = batch_partition<3>(b, owe_it, ck, any_region); break;
+        case 4: rc = batch_partition<4>(b, owe_it, ck, any_region); break;
+      }
+      TRY(rc);
     }
     // collect + scatter back into the runs
     unsigned long long work = 0;
@@ -2380,7 +2513,8 @@ void lse_batch_destroy(lse_batch* b) {
   for (cudaEvent_t e : b->ev)
     if (e) cudaEventDestroy(e);
   void* ptrs[] = {b->bits[0], b->bits[1], b->P, b->M, b->data32, b->data64, b->scal,
-                  b->ctx, b->part, b->part_fin, b->work, (void*)b->d_src, (void*)b->d_dst};
+                  b->ctx, b->part, b->part_fin, b->work, (void*)b->d_src, (void*)b->d_dst,
+                  (void*)b->fix};
   for (void* q : ptrs)
     if (q) cudaFree(q);
   if (b->h_scal) cudaFreeHost(b->h_scal);

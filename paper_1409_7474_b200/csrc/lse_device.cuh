@@ -60,6 +60,7 @@ struct __align__(16) Scalars {
   // update is redone when the coefficients moved more than spec_delta
   int redo;                           // the last speculative update must be redone
   int fix_needed;                     // its coefficients moved: the fix list decides the band
+  int redo_any;                       // batches (tile 0's copy): some tile's update is redone
   float spec_delta, spec_e0;          // flag band of the next speculative update (delta < 0: none)
   unsigned int fix_n[2];              // fix-list entries of the speculative update (by parity)
   unsigned int fix_cap;               // fix-list capacity

@@ -94,6 +94,9 @@ struct FastParams {
   int2* fix;
   unsigned int fix_cap;
   int fix_par;
+  unsigned int* fix_cnt;     // the fix-list counters (by parity): scal->fix_n of the run / tile 0
+  int fix_row0;              // row offset of this view in the list's frame (batched tile views)
+  int redo_only;             // batched redo pass: only the tiles whose scal->redo is set
 };
 
 // exact-path frame of tile t (its context, state and first image row)
@@ -731,9 +734,10 @@ __device__ __noinline__ uint32_t update_tie_cols(const FastParams& P, uint32_t l
 }
 
 // a pixel whose speculative decision waits for the true coefficients
+// (rows in the list's frame: the stacked rows of a batch)
 __device__ __forceinline__ void spec_append(const FastParams& P, int i, int x) {
-  const unsigned q = atomicAdd(&P.scal->fix_n[P.fix_par], 1u);
-  if (q < P.fix_cap) P.fix[q] = make_int2(x, i);
+  const unsigned q = atomicAdd(&P.fix_cnt[P.fix_par], 1u);
+  if (q < P.fix_cap) P.fix[q] = make_int2(x, i + P.fix_row0);
 }
 
 template <int R, bool EXACT = false>
@@ -924,7 +928,8 @@ __device__ __forceinline__ void update_block_int2(const FastParams& P, uint32_t 
         // decided by k_spec_fix unless the coefficients turn out unchanged;
         // the guard band of the ones used is decided exactly now (final if
         // they are unchanged, as they are once the partition settles)
-        spec_append(P, y0 + k, x0 + c);
+        // (batched edge tiles run with their exact coefficients: nothing to fix)
+        if (tile_ctx(P, tile)->model != EDGE) spec_append(P, y0 + k, x0 + c);
         if (!LSE_SPEC_INLINE || !((exact_cols >> c) & 1u)) continue;
       }
       const bool pos = exact_u_fast<R, SRC>(tile_ctx(P, tile), tile_bits(P, tile),
@@ -948,7 +953,8 @@ __device__ __forceinline__ void update_block_int2(const FastParams& P, uint32_t 
       while (cols) {
         const int c = __ffs(cols) - 1;
         cols &= cols - 1;
-        const double e = exact_phi_fast<R>(P.ctx, P.bits_in, y0 + k, x0 + c);
+        const double e = exact_phi_fast<R>(tile_ctx(P, tile), tile_bits(P, tile),
+                                           y0 - tile_y0(P, tile) + k, x0 + c);
 #pragma unroll
         for (int q = 0; q < CPL; ++q) {
           if (q == c) {
@@ -1211,7 +1217,7 @@ __device__ __forceinline__ void update_rows_border(const FastParams& P, const fl
       // and is also decided exactly with the coefficients used (final if
       // they turn out unchanged)
       if (FUSED) {
-        spec_append(P, y0 + k, x0 + c);
+        if (P.ctx->model != EDGE) spec_append(P, y0 + k, x0 + c);
         if (!LSE_SPEC_INLINE) continue;
       }
       const bool pos = exact_u_fast<R, SRC>(P.ctx, P.bits_in, y0 + k, x0 + c) > 0.0;
@@ -1272,6 +1278,7 @@ __device__ __forceinline__ void tile_view(FastParams& Q, int tile) {
   Q.ctx += tile;
   Q.g.H = Q.tile_h;
   Q.g.HR = Q.tile_hr;
+  Q.fix_row0 += tile * Q.tile_hr * 32;
 }
 
 template <int R, int MODEL, int SRC, bool BATCH>
@@ -1328,6 +1335,7 @@ __device__ __forceinline__ void update_units(const FastParams& P, const FastPara
         lu = nb + (iu - tile * ni);
       }
       const Scalars* st = P.scal + tile;
+      if (P.redo_only && !__ldcg(&st->redo)) continue;   // (its speculative update stands)
       stopped = stop_flag(st) != 0;
       A = st->A;
       B = st->B;
@@ -1593,15 +1601,17 @@ __device__ __forceinline__ ExactCoefs exact_coefs(const Scalars* sc) {
   return ExactCoefs{sc->c_pos, sc->c_neg, sc->dc, sc->peak, sc->mid, sc->zero_vel};
 }
 
+// base: the scalars holding the fix-list counters and the redo work counter
+// (the run's own; tile 0's for every tile of a batch)
 __device__ __forceinline__ void spec_check(Scalars* sc, float A0, float B0, float delta0, float e00,
-                                           int spec, const ExactCoefs& k0) {
+                                           int spec, const ExactCoefs& k0, Scalars* base) {
   const double am = sc->img_absmax * (1.0 + 0x1p-20);
   const double A = sc->A, B = sc->B, a0 = A0, b0 = B0;
   const double D = (fabs(A - a0) * am + fabs(B - b0)) * (1.0 + 0x1p-40);
   const double vfm = fmax(fabs(A) * am + fabs(B), fabs(a0) * am + fabs(b0));
   if (spec) {
-    const unsigned nfix = sc->fix_n[spec - 1];
-    const bool ok = nfix <= sc->fix_cap &&
+    const unsigned nfix = base->fix_n[spec - 1];
+    const bool ok = nfix <= base->fix_cap &&
                     (double)delta0 * (1.0 - 0x1p-20) >= (D + 0x1p-22 * vfm) * (1.0 + 0x1p-20) &&
                     (double)e00 * (1.0 - 0x1p-20) >= (double)sc->eps_u;
     sc->redo = ok ? 0 : 1;
@@ -1617,7 +1627,8 @@ __device__ __forceinline__ void spec_check(Scalars* sc, float A0, float B0, floa
       if (!same) sc->spec_fixes += nfix;
     } else {
       sc->spec_redos += 1;
-      sc->work2 = 0;
+      base->work2 = 0;
+      if (base != sc) atomicOr(&base->redo_any, 1);
     }
   }
   // next band: 4x the last move of the coefficients plus a floor; none when
@@ -1628,7 +1639,7 @@ __device__ __forceinline__ void spec_check(Scalars* sc, float A0, float B0, floa
 }
 
 __device__ void finalize_cta(const PartRanges& R3, Scalars* sc, bool delta, bool region,
-                             bool ckpt, long long iter, int spec = 0) {
+                             bool ckpt, long long iter, int spec = 0, Scalars* base = nullptr) {
   const int n = R3.n[0] + R3.n[1] + R3.n[2];
   __shared__ double f_ah[32], f_al[32], f_bh[32], f_bl[32];
   __shared__ long long f_na[32], f_nb[32];
@@ -1713,7 +1724,7 @@ __device__ void finalize_cta(const PartRanges& R3, Scalars* sc, bool delta, bool
         sc->n_pos = sna;
       }
       region_coeffs(sc);
-      spec_check(sc, A0, B0, delta0, e00, spec, k0);
+      spec_check(sc, A0, B0, delta0, e00, spec, k0, base ? base : sc);
     }
     if (ckpt) {                                    // engine.py:228-236
       sc->n_ckpt += 1;
@@ -1723,6 +1734,14 @@ __device__ void finalize_cta(const PartRanges& R3, Scalars* sc, bool delta, bool
         sc->stop = 1;
         sc->converged = 1;
         sc->converged_iter = iter;
+        // a batched tile converging after a speculative pass: the pass has
+        // written b^{iter+1}; the redo pass puts b^{iter} back (a stopped
+        // tile's units copy their state)
+        if (spec && base && base != sc) {
+          sc->redo = 1;
+          base->work2 = 0;
+          atomicOr(&base->redo_any, 1);
+        }
       }
     }
   }
@@ -2192,7 +2211,12 @@ constexpr int fused_smem_bytes() {
   return (kThreads / 32) * ((kRing2 * 32 * kUpdCols + (kUpdCols + 2 * (R + 1)) * 32) * 4 + 2048);
 }
 
-template <int R, bool CKPT>
+// BATCH: every unit of every tile ([all tiles' border][all tiles' interior],
+// the batched update's order), each with its tile's coefficients and band;
+// converged tiles keep their state; edge tiles run with their exact
+// coefficients (A = 1, B = 0, delta = 0: nothing to predict) and produce
+// partition words only for the checkpoint masks.
+template <int R, bool CKPT, bool BATCH>
 __global__ void __launch_bounds__(kThreads, kFusedCtasPerSm) k_update_fused(FastParams P) {
   constexpr int CPL = kUpdCols;
   constexpr int NT = CPL + 2 * (R + 1);
@@ -2222,13 +2246,16 @@ __global__ void __launch_bounds__(kThreads, kFusedCtasPerSm) k_update_fused(Fast
   pdl_wait();
   pdl_launch_dependents();
   const Scalars* sc = P.scal;
-  if (stop_flag(sc)) return;
-  const float A = sc->A, B = sc->B, e0 = sc->spec_e0, delta = sc->spec_delta;
-  const float eps_t = sc->eps_u;
+  if (!BATCH && stop_flag(sc)) return;
+  if (BATCH && blockIdx.x == 0 && threadIdx.x == 0) P.scal->redo_any = 0;   // (this iteration's)
+  float A = sc->A, B = sc->B, e0 = sc->spec_e0, delta = sc->spec_delta;
+  float eps_t = sc->eps_u;
   const int lane = threadIdx.x & 31;
   const int nb = border_units(P.gu);
   const int nch = chunk_units(P.gu);
-  const int nunits = nb + interior_units(P.gu);
+  const int ni = interior_units(P.gu);
+  const int T = BATCH ? P.ntiles : 1;
+  const int nunits = T * (nb + ni);
   float* ring = s_ring + (threadIdx.x >> 5) * kRing2 * 32 * CPL;
   uint32_t (&win_b)[NT][32] = s_win[threadIdx.x >> 5];
   // (Also loading the next unit's window before this one's commit measured
@@ -2243,10 +2270,37 @@ __global__ void __launch_bounds__(kThreads, kFusedCtasPerSm) k_update_fused(Fast
     unsigned long long g_next = 0;
     if (lane == 0) g_next = atomicAdd(P.work, 1ull) - P.work_base;
     LaneDelta d{0.0, 0.0, 0, 0, 0ull};
-    if (unit < nb) {
-      border_fused_unit<R, CKPT>(s_P, s_lt, s_ls, unit, A, B, e0, delta, d);
+    int tile = 0, lu = unit;
+    bool stopped = false, part_t = true;
+    if (BATCH) {
+      if (unit < T * nb) {
+        tile = unit / nb;
+        lu = unit - tile * nb;
+      } else {
+        const int iu = unit - T * nb;
+        tile = iu / ni;
+        lu = nb + (iu - tile * ni);
+      }
+      const Scalars* st = P.scal + tile;
+      stopped = stop_flag(st) != 0;
+      A = st->A;
+      B = st->B;
+      e0 = st->spec_e0;
+      delta = st->spec_delta;
+      eps_t = st->eps_u;
+      part_t = st->model != EDGE || CKPT;        // edge tiles: checkpoint masks only
+    }
+    if (lu < nb) {
+      if (!BATCH) {
+        border_fused_unit<R, CKPT>(s_P, s_lt, s_ls, lu, A, B, e0, delta, d);
+      } else {
+        FastParams Q = s_P;
+        tile_view(Q, tile);
+        if (stopped) border_update_body<R, REGION, SRC_SMOOTH>(Q, s_lt, s_ls, lu, A, B, e0, true);
+        else border_fused_unit<R, CKPT>(Q, s_lt, s_ls, lu, A, B, e0, delta, d);
+      }
     } else {
-      const int iu = unit - nb;
+      const int iu = lu - nb;
       int r = 0, x0 = 0;
       bool act = true;
       if (iu < nch) {
@@ -2255,6 +2309,7 @@ __global__ void __launch_bounds__(kThreads, kFusedCtasPerSm) k_update_fused(Fast
       } else {
         act = b1_lane(P.gu, iu - nch, lane, r, x0);
       }
+      if (BATCH) r += tile * P.tile_hr;           // row of the tile in the stacked arrays
       uint32_t prev[NT], cur[NT];
       uint32_t a = ~0u, o = 0u;
       if (act) {
@@ -2283,8 +2338,9 @@ __global__ void __launch_bounds__(kThreads, kFusedCtasPerSm) k_update_fused(Fast
         }
       }
       uint32_t pw[CPL], mw[CPL];
-      if (P.skip_uniform && __all_sync(0xffffffffu, !act || a == ~0u || o == 0u)) {
+      if (stopped || (P.skip_uniform && __all_sync(0xffffffffu, !act || a == ~0u || o == 0u))) {
         // uniform window: phi has the sign of b everywhere, b^{n+1} = b^n
+        // (a converged tile of a batch keeps its state the same way)
         if (act) {
           uint32_t* dst = P.bits_out + (size_t)r * P.g.pitch_w + x0;
 #pragma unroll
@@ -2294,14 +2350,18 @@ __global__ void __launch_bounds__(kThreads, kFusedCtasPerSm) k_update_fused(Fast
 #pragma unroll
           for (int c = 0; c < CPL; ++c) pw[c] = mw[c] = cur[R + 1 + c];
           cp_async_wait<0>();
-          partition_commit<true, CKPT, false>(P, r, x0, pw, mw, d, 0, s_old);
+          if (!stopped) {
+            if (part_t) partition_commit<true, CKPT, false>(P, r, x0, pw, mw, d, tile, s_old);
+            else partition_commit<false, CKPT, false>(P, r, x0, pw, mw, d, tile, s_old);
+          }
         }
       } else if (act) {
         // (its final cp.async wait covers the old words too)
         update_block_int2<R, REGION, CPL, SRC_SMOOTH, true>(P, luts.lt2, ring, r, x0, A, B, e0,
-                                                            prev, cur, 0, delta, pw, mw, s_P,
+                                                            prev, cur, tile, delta, pw, mw, s_P,
                                                             &win_b[0][0], eps_t);
-        partition_commit<true, CKPT, false>(P, r, x0, pw, mw, d, 0, s_old);
+        if (!BATCH || part_t) partition_commit<true, CKPT, false>(P, r, x0, pw, mw, d, tile, s_old);
+        else partition_commit<false, CKPT, false>(P, r, x0, pw, mw, d, tile, s_old);
       }
     }
 #pragma unroll
@@ -2335,24 +2395,38 @@ __global__ void __launch_bounds__(kThreads, kFusedCtasPerSm) k_update_fused(Fast
 //   k_spec_redo -- the update grid: returns at once unless scal->redo, else
 //                  redoes the whole update with the true coefficients (its own
 //                  work counter scal->work2, reset by the finalize).
-template <int R>
+template <int R, bool BATCH>
 __global__ void __launch_bounds__(256) k_spec_fix(const FastParams P) {
   pdl_wait();
   pdl_launch_dependents();
-  Scalars* sc = P.scal;
-  if (stop_flag(sc)) return;
-  const bool skip = __ldcg(&sc->redo) != 0 || __ldcg(&sc->fix_needed) == 0;
-  const unsigned n = min(__ldcg(&sc->fix_n[P.fix_par]), P.fix_cap);
-  if (blockIdx.x == 0 && threadIdx.x == 0) {
-    if (sc->zero_vel && sc->model != EDGE) sc->degenerate = 1;   // sticky (engine.py:239-240)
-    sc->fix_n[P.fix_par ^ 1] = 0u;               // the next speculative update's list
-    if (!skip) sc->fallbacks += n;               // (counted once: no contended atomics)
+  Scalars* sc = P.scal;                          // (tile 0 of a batch: the list's counters)
+  if (!BATCH && stop_flag(sc)) return;
+  const bool skip = !BATCH && (__ldcg(&sc->redo) != 0 || __ldcg(&sc->fix_needed) == 0);
+  const unsigned n = min(__ldcg(&P.fix_cnt[P.fix_par]), P.fix_cap);
+  if (blockIdx.x == 0) {
+    for (int t = threadIdx.x; t < (BATCH ? P.ntiles : 1); t += blockDim.x) {
+      Scalars* st = sc + t;                      // sticky degenerate (engine.py:239-240)
+      if (st->zero_vel && st->model != EDGE && !st->stop) st->degenerate = 1;
+    }
+    if (threadIdx.x == 0) {
+      P.fix_cnt[P.fix_par ^ 1] = 0u;             // the next speculative update's list
+      if (!BATCH && !skip) sc->fallbacks += n;   // (counted once: no contended atomics)
+    }
   }
   if (skip) return;
+  const int tile_rows = P.tile_hr * 32;
   const unsigned stride = gridDim.x * blockDim.x;
   for (unsigned q = blockIdx.x * blockDim.x + threadIdx.x; q < n; q += stride) {
     const int2 e = __ldcg(&P.fix[q]);
-    const bool pos = exact_u_fast<R, SRC_SMOOTH>(P.ctx, P.bits_in, e.y, e.x, false) > 0.0;
+    int t = 0, i = e.y;
+    if (BATCH) {
+      t = e.y / tile_rows;
+      i = e.y - t * tile_rows;
+      const Scalars* st = sc + t;
+      if (__ldcg(&st->stop) || __ldcg(&st->redo) || !__ldcg(&st->fix_needed)) continue;
+    }
+    const bool pos = exact_u_fast<R, SRC_SMOOTH>(P.ctx + t, P.bits_in + (size_t)t * P.tile_words, i,
+                                                 e.x, false) > 0.0;
     uint32_t* w = P.bits_out + (size_t)(e.y >> 5) * P.g.pitch_w + e.x;
     const uint32_t bit = 1u << (e.y & 31);
     if (pos) atomicOr(w, bit);
@@ -2363,16 +2437,18 @@ __global__ void __launch_bounds__(256) k_spec_fix(const FastParams P) {
 // the redo pass proper: a noinline body over the CTA's shared copy of the
 // parameters, so the (almost always) early-returning kernel never copies its
 // parameter block to local memory
-template <int R>
+template <int R, bool BATCH>
 __device__ __noinline__ void spec_redo_body(const FastParams& P, float* s_lt, float* s_ls,
                                             float* s_ring) {
   const SharedLuts luts{s_lt, s_ls, (uint32_t)__cvta_generic_to_shared(g_pair_lut)};
   load_luts<R>(P, luts);
   __syncthreads();
-  update_units<R, REGION, SRC_SMOOTH, false, 1>(P, P, luts, s_lt, s_ls, s_ring);
+  update_units<R, REGION, SRC_SMOOTH, BATCH, 1>(P, P, luts, s_lt, s_ls, s_ring);
 }
 
-template <int R>
+// BATCH: the tiles whose scal->redo is set (a failed prediction, or a tile
+// that converged in this iteration: its state goes back to b^{iter})
+template <int R, bool BATCH>
 __global__ void __launch_bounds__(kThreads, kUpdateCtasPerSm) k_spec_redo(const FastParams P) {
   constexpr int CPL = kUpdCols;
   constexpr int NPAT = 1 << (2 * R + 1);
@@ -2382,10 +2458,13 @@ __global__ void __launch_bounds__(kThreads, kUpdateCtasPerSm) k_spec_redo(const 
   __shared__ FastParams s_P;
   pdl_wait();
   pdl_launch_dependents();
-  if (stop_flag(P.scal) || !__ldcg(&P.scal->redo)) return;
-  if (threadIdx.x == 0) s_P = P;
+  if (BATCH ? !__ldcg(&P.scal->redo_any) : (stop_flag(P.scal) || !__ldcg(&P.scal->redo))) return;
+  if (threadIdx.x == 0) {
+    s_P = P;
+    s_P.redo_only = BATCH ? 1 : 0;
+  }
   __syncthreads();
-  spec_redo_body<R>(s_P, s_lt, s_ls, s_ring);
+  spec_redo_body<R, BATCH>(s_P, s_lt, s_ls, s_ring);
 }
 
 }  // namespace lse

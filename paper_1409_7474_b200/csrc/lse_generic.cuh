@@ -478,8 +478,10 @@ __global__ void __launch_bounds__(256) k_finalize_stage1_tiles(const TilePartial
   reduce_slice(R3, t0, t1, out + (size_t)t * gridDim.x + blockIdx.x);
 }
 
+// (spec = 1 + fix-list parity after a speculative fused pass: the tile's
+// prediction is checked; tile 0's scalars hold the batch's fix-list counters)
 __global__ void __launch_bounds__(64) k_finalize_run_tiles(const TilePartial* fin, Scalars* scal,
-                                                           int ckpt, long long iter) {
+                                                           int ckpt, long long iter, int spec) {
   pdl_wait();
   pdl_launch_dependents();
   const int t = blockIdx.x;
@@ -489,7 +491,7 @@ __global__ void __launch_bounds__(64) k_finalize_run_tiles(const TilePartial* fi
   if (!region && !ckpt) return;
   const TilePartial* f = fin + (size_t)t * kFinSlices;
   PartRanges R1{{f, f, f}, {kFinSlices, 0, 0}};
-  finalize_cta(R1, sc, true, region, ckpt != 0, iter);
+  finalize_cta(R1, sc, true, region, ckpt != 0, iter, spec, scal);
 }
 
 // batched tiles with few partials per tile: a single-stage finalize per tile
@@ -498,7 +500,8 @@ __global__ void __launch_bounds__(64) k_finalize_run_tiles(const TilePartial* fi
 // tile run alone, so the reduction order is the same
 __global__ void __launch_bounds__(64) k_finalize_tiles_direct(const TilePartial* part,
                                                               Scalars* scal, int nb, int ni,
-                                                              int T, int ckpt, long long iter) {
+                                                              int T, int ckpt, long long iter,
+                                                              int spec) {
   pdl_wait();
   pdl_launch_dependents();
   const int t = blockIdx.x;
@@ -508,7 +511,7 @@ __global__ void __launch_bounds__(64) k_finalize_tiles_direct(const TilePartial*
   if (!region && !ckpt) return;
   PartRanges R3{{part + (size_t)t * nb, part + (size_t)T * nb + (size_t)t * ni, part},
                 {nb, ni, 0}};
-  finalize_cta(R3, sc, true, region, ckpt != 0, iter);
+  finalize_cta(R3, sc, true, region, ckpt != 0, iter, spec, scal);
 }
 
 // per-iteration finalize of the fast path (DELTA partials); no-op once stopped

@@ -96,6 +96,45 @@ def test_two_stage_batched_finalize_matches_single_runs(monkeypatch):
         assert np.array_equal(a.mask(), b.mask())
 
 
+@pytest.mark.parametrize("h,stages", [(100, "one"), (96, "one"), (100, "two")])
+def test_fused_batch_matches_single_runs(h, stages, monkeypatch):
+    """The opt-in batched speculative pass (LSE_FUSED_BATCH=1): mixed region /
+    edge / zhang tiles converging at different iterations, chunked advance,
+    the one- and two-stage per-tile finalize -- every tile equals the tile
+    alone, bit for bit."""
+    imgs, seeds, prm = mixed_case(h)
+    monkeypatch.setenv("LSE_FINE_MAX_PX", "0")
+    if stages == "two":
+        monkeypatch.setenv("LSE_ONESTAGE_MAX_PARTS", "0")
+    single = [L.EvolutionRun(imgs[k], seeds[k], prm[k]) for k in range(len(imgs))]
+    for r in single:
+        r.advance(60)
+    monkeypatch.setenv("LSE_FUSED_BATCH", "1")
+    batch = [L.EvolutionRun(imgs[k], seeds[k], prm[k]) for k in range(len(imgs))]
+    tb = TileBatch(batch)
+    for n in (1, 9, 50):
+        tb.advance(n)
+    check_same(batch, single)
+
+
+def test_fused_batch_degenerate_and_forced_redo(monkeypatch):
+    """Opt-in batched speculative pass with a zero-capacity fix list (every
+    region tile redone) and a constant (degenerate) tile."""
+    imgs = [tile(0), np.full((100, 80), 0.5), tile(2)]
+    seeds = [L.SeedSpec(polygons=(square(6, 8, 70, 90),), inside_sign=-1)] * 3
+    prm = [params("region", max_iters=40)] * 3
+    monkeypatch.setenv("LSE_FINE_MAX_PX", "0")
+    single = [L.EvolutionRun(imgs[k], seeds[k], prm[k]) for k in range(3)]
+    for r in single:
+        r.advance(40)
+    monkeypatch.setenv("LSE_FUSED_BATCH", "1")
+    monkeypatch.setenv("LSE_FIX_CAP", "0")
+    batch = [L.EvolutionRun(imgs[k], seeds[k], prm[k]) for k in range(3)]
+    TileBatch(batch).advance(40)
+    check_same(batch, single)
+    assert batch[1].state.degenerate
+
+
 def test_chunked_batch_advance_and_degenerate_tile():
     imgs = [tile(0), np.full((100, 80), 0.5), tile(2)]          # tile 1: constant image
     seeds = [L.SeedSpec(polygons=(square(6, 8, 70, 90),), inside_sign=-1)] * 3
