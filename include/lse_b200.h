@@ -178,6 +178,12 @@ int lse_run_kernel_times(lse_run* run, double* update_ms, long long* update_laun
  * fix list, fused path enabled (0/1)}.  LSE_FUSED=0 at creation disables it. */
 int lse_run_spec_stats(lse_run* run, long long* out4);
 
+/* Multi-band runs: out[2] = {peak passes reused (a partition that moved no
+ * pixel leaves the band means, the data term D, max|D| and the coefficients
+ * bit-identical, so the pass over every pixel is not repeated), reuse
+ * enabled (0/1)}.  LSE_BAND_REUSE=0 at creation disables the reuse. */
+int lse_run_band_stats(lse_run* run, long long* out2);
+
 void lse_run_destroy(lse_run* run);
 
 /* ---- batched tiles -----------------------------------------

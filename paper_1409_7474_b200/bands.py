@@ -92,6 +92,14 @@ class BandEvolutionRun(EvolutionRun):
         self.wall_time = 0.0
         self.trace = [(0, self._dev.contours())] if trace else None
 
+    def band_stats(self) -> dict:
+        """Peak passes reused because the partition moved no pixel (the
+        means, D and max|D| are then bit-identical; LSE_BAND_REUSE=0 at
+        creation recomputes them every iteration)."""
+        out = (C.c_longlong * 2)()
+        N.check(N.lib.lse_run_band_stats(self._dev.h, out))
+        return dict(reused=int(out[0]), enabled=bool(out[1]))
+
 
 def run_bands(bands, seeds: SeedSpec, params: EvolutionParams):
     """`run` (engine.py:272-277) for a multi-band image."""

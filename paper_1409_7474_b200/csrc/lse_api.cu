@@ -1609,6 +1609,8 @@ int create_impl(lse_run** out, const lse_params* p, long long height, long long 
   s0.eps_u = (float)edge_eps_u(p->dt);
   s0.spec_delta = -1.0f;
   s0.fix_cap = r->fix_cap;
+  s0.band_reuse = 1;
+  if (const char* v = std::getenv("LSE_BAND_REUSE")) s0.band_reuse = std::atoi(v) != 0;
   if (p->model == LSE_MODEL_EDGE) {
     // a batched edge tile runs the fused pass with its exact coefficients:
     // band = the guard band, decided exactly in the pass, no fix list
@@ -2013,6 +2015,15 @@ int lse_run_spec_stats(lse_run* r, long long* out4) {
   out4[1] = (long long)r->h_scal->spec_redos;
   out4[2] = (long long)r->h_scal->spec_fixes;
   out4[3] = r->fused ? 1 : 0;
+  return LSE_OK;
+}
+
+int lse_run_band_stats(lse_run* r, long long* out2) {
+  if (!r || !out2) return fail(LSE_ERR_ARG, "null argument");
+  CK(cudaMemcpyAsync(r->h_scal, r->d_scal, sizeof(Scalars), cudaMemcpyDeviceToHost, r->st));
+  CK(cudaStreamSynchronize(r->st));
+  out2[0] = (long long)r->h_scal->band_reused;
+  out2[1] = r->h_scal->band_reuse;
   return LSE_OK;
 }
 

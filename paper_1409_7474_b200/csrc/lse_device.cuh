@@ -66,6 +66,14 @@ struct __align__(16) Scalars {
   unsigned int fix_cap;               // fix-list capacity
   unsigned long long work2;           // work counter of the redo pass
   unsigned long long spec_redos, spec_fixes;   // statistics
+  // multi-band runs: the data plane, peak and coefficients of the last peak
+  // pass are a function of the band means alone; when a partition changed
+  // no pixel the means are bit-identical and the peak pass is not repeated
+  int band_valid;                     // the last peak pass completed (plane + coefficients)
+  int band_same;                      // this pass: the means did not move (peak pass skipped)
+  int band_reuse;                     // reuse enabled (LSE_BAND_REUSE, default 1)
+  int band_any;                       // k_band_sums: some block of this pass saw a changed pixel
+  unsigned long long band_reused;     // statistics: peak passes skipped
 };
 
 // Per-tile partial (fixed tile geometry => deterministic, GPU-count independent

@@ -74,3 +74,34 @@ def test_band_runs_refuse_the_generic_path():
     seeds = L.SeedSpec(polygons=(square(5, 5, 30, 30),))
     with pytest.raises(RuntimeError):
         BandEvolutionRun(bands, seeds, params(reinit_period=2))
+
+
+def test_peak_pass_reuse_is_exact(monkeypatch):
+    """Once the partition stops moving (C3's checkerboard settles within ~40
+    iterations) the band means, D and max|D| are bit-identical and the peak
+    pass is reused; the trajectory equals the recomputed one and the oracle."""
+    sc = scenes.config3(512, 90)
+    prm = params(**sc.params)
+    r = BandEvolutionRun(sc.image, sc.extra["signs"], prm)
+    r.advance(90)
+    st = r.band_stats()
+    assert st["enabled"] and st["reused"] > 10
+    monkeypatch.setenv("LSE_BAND_REUSE", "0")
+    r0 = BandEvolutionRun(sc.image, sc.extra["signs"], prm)
+    r0.advance(90)
+    assert r0.band_stats() == dict(reused=0, enabled=False)
+    assert np.array_equal(r.state.phi, r0.state.phi)
+    ref = oracle(sc.image, sc.extra["signs"].astype(np.float64), prm, 90)
+    assert np.array_equal(r.state.phi, ref.phi)
+
+
+def test_peak_pass_reuse_with_checkpoints():
+    """Reuse across checkpoint / convergence bookkeeping: the convergence
+    iteration and the final state equal the oracle's."""
+    sc = scenes.config3(256, 200)
+    prm = params(**dict(sc.params, max_iters=200, conv_check_every=7, conv_window=3))
+    r = BandEvolutionRun(sc.image, sc.extra["signs"], prm)
+    r.advance(200)
+    ref = oracle(sc.image, sc.extra["signs"].astype(np.float64), prm, 200)
+    assert r.state.iteration == ref.iteration and r.converged == ref.converged
+    assert np.array_equal(r.state.phi, ref.phi)
