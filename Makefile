@@ -28,10 +28,17 @@ $(CHECK_LIB): $(SRC) $(HDR)
 	@mkdir -p $(dir $@)
 	$(NVCC) $(FLAGS) -DLSE_CHECK_BOUND -shared -o $@ $(SRC) 2> /dev/null
 
+# resident-kernel phase timing (prints per-phase SM cycles per advance call)
+RESTRACE_LIB := paper_1409_7474_b200/_lib/liblse_b200_restrace.so
+restrace: $(RESTRACE_LIB)
+$(RESTRACE_LIB): $(SRC) $(HDR)
+	@mkdir -p $(dir $@)
+	$(NVCC) $(FLAGS) -DLSE_RES_TRACE -shared -o $@ $(SRC) 2> /dev/null
+
 oracle:
 	$(MAKE) -C oracle
 
 clean:
-	rm -f $(LIB) $(TRACE_LIB) $(CHECK_LIB)
+	rm -f $(LIB) $(TRACE_LIB) $(CHECK_LIB) $(RESTRACE_LIB)
 
-.PHONY: all clean oracle trace check
+.PHONY: all clean oracle trace check restrace

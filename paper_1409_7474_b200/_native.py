@@ -96,6 +96,7 @@ _SIGS = {
     "lse_run_kernel_times": (_i, [_vp, _dp, _llp, _dp, _llp]),
     "lse_run_spec_stats": (_i, [_vp, _llp]),
     "lse_run_band_stats": (_i, [_vp, _llp]),
+    "lse_run_resident_stats": (_i, [_vp, _llp]),
     "lse_run_destroy": (None, [_vp]),
     "lse_batch_create": (_i, [C.POINTER(_vp), C.POINTER(_vp), _i]),
     "lse_batch_advance": (_i, [_vp, _ll, C.POINTER(LseStatus)]),

@@ -27,6 +27,7 @@
 #include "lse_fast.cuh"
 #include "lse_generic.cuh"
 #include "lse_fine.cuh"
+#include "lse_resident.cuh"
 #include "lse_contours.cuh"
 
 using namespace lse;
@@ -313,6 +314,13 @@ struct lse_run {
   int2* d_fix = nullptr;
   unsigned int fix_cap = 0;
   long long fused_iters = 0;
+  // resident kernel (lse_resident.cuh): whole advance() calls of small images
+  // in one launch -- one cluster (res_grid false) or a cooperative grid
+  bool resident = false, res_grid = false;
+  int res_ctas = 0, res_tasks = 0;
+  TilePartial* d_res_parts = nullptr;
+  unsigned int* d_sync = nullptr;
+  long long resident_calls = 0;
 };
 
 namespace {
@@ -895,6 +903,156 @@ bool fp32_ok(lse_run* r) {
   if (r->p.model == LSE_MODEL_ZHANG && !(std::fabs(r->p.nu) <= 1e6)) return false;
   if (r->mode == SRC_SCALED && !(r->scale >= 1e-3 && r->scale <= 1e6)) return false;
   return true;
+}
+
+// ------------------------------------------------------- resident kernel
+// (lse_resident.cuh) whole advance() calls of small single images in one
+// launch.  LSE_RESIDENT=0 keeps the per-iteration launches, 2 forces the
+// cooperative-grid barrier where one cluster would do (tests / A-B).
+template <int R, int MODEL, bool GRID>
+int resident_launch_k(lse_run* r, const FastParams& P, const ResidentArgs& A) {
+  auto kern = k_resident<R, MODEL, GRID>;
+  cudaLaunchConfig_t cfg{};
+  cfg.gridDim = dim3((unsigned)r->res_ctas);
+  cfg.blockDim = dim3(kResThreads);
+  cfg.dynamicSmemBytes = 0;
+  cfg.stream = r->st;
+  cudaLaunchAttribute at[1];
+  if (GRID) {
+    at[0].id = cudaLaunchAttributeCooperative;
+    at[0].val.cooperative = 1;
+  } else {
+    if (r->res_ctas > 8)
+      CK(cudaFuncSetAttribute(kern, cudaFuncAttributeNonPortableClusterSizeAllowed, 1));
+    at[0].id = cudaLaunchAttributeClusterDimension;
+    at[0].val.clusterDim.x = (unsigned)r->res_ctas;
+    at[0].val.clusterDim.y = 1;
+    at[0].val.clusterDim.z = 1;
+  }
+  cfg.attrs = at;
+  cfg.numAttrs = 1;
+  CK(cudaLaunchKernelEx(&cfg, kern, P, A));
+  CKL();
+  return LSE_OK;
+}
+
+template <int R, int MODEL>
+int resident_launch_rm(lse_run* r, const FastParams& P, const ResidentArgs& A) {
+  if (r->res_grid) return resident_launch_k<R, MODEL, true>(r, P, A);
+  return resident_launch_k<R, MODEL, false>(r, P, A);
+}
+
+template <int MODEL>
+int resident_launch_m(lse_run* r, const FastParams& P, const ResidentArgs& A) {
+  switch (r->R) {
+    case 1: return resident_launch_rm<1, MODEL>(r, P, A);
+    case 2: return resident_launch_rm<2, MODEL>(r, P, A);
+    case 3: return resident_launch_rm<3, MODEL>(r, P, A);
+    case 4: return resident_launch_rm<4, MODEL>(r, P, A);
+  }
+  return fail(LSE_ERR_ARG, "unsupported template radius");
+}
+
+// can this run's launch shape be resident on the device?  (decided once)
+template <bool GRID>
+int resident_capacity(int ctas) {
+  // occupancy of the widest instantiation stands for all (same launch bounds)
+  auto kern = k_resident<4, REGION, GRID>;
+  if (GRID) {
+    int per_sm = 0;
+    if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, kResThreads, 0) != cudaSuccess)
+      return 0;
+    return per_sm * num_sms();
+  }
+  if (ctas > 8 &&
+      cudaFuncSetAttribute(kern, cudaFuncAttributeNonPortableClusterSizeAllowed, 1) != cudaSuccess) {
+    cudaGetLastError();
+    return 0;
+  }
+  cudaLaunchConfig_t cfg{};
+  cfg.gridDim = dim3((unsigned)ctas);
+  cfg.blockDim = dim3(kResThreads);
+  cudaLaunchAttribute at[1];
+  at[0].id = cudaLaunchAttributeClusterDimension;
+  at[0].val.clusterDim.x = (unsigned)ctas;
+  at[0].val.clusterDim.y = 1;
+  at[0].val.clusterDim.z = 1;
+  cfg.attrs = at;
+  cfg.numAttrs = 1;
+  int nclusters = 0;
+  if (cudaOccupancyMaxActiveClusters(&nclusters, kern, &cfg) != cudaSuccess) {
+    cudaGetLastError();
+    return 0;
+  }
+  return nclusters > 0 ? ctas : 0;
+}
+
+void resident_setup(lse_run* r) {
+  r->resident = false;
+  int mode = 1;
+  if (const char* v = std::getenv("LSE_RESIDENT")) mode = std::atoi(v);
+#ifdef LSE_CHECK_BOUND
+  mode = 0;                                      // validation builds certify the per-iteration kernels
+#endif
+  if (mode == 0 || !r->fine || is_bands(r) || is_cv(r) || r->strip) return;
+  const int ncb = (r->W + kResCols - 1) / kResCols;
+  const long long tasks = (long long)r->g.HR * ncb;
+  const int ctas = (int)((tasks + kResWarps - 1) / kResWarps);
+  bool grid = mode == 2 || ctas > kResClusterMax;
+  if (!grid && resident_capacity<false>(ctas) < ctas) grid = true;
+  if (grid && resident_capacity<true>(ctas) < ctas) return;
+  r->resident = true;
+  r->res_grid = grid;
+  r->res_ctas = ctas;
+  r->res_tasks = (int)tasks;
+}
+
+// is the whole call [it0+1, it0+steps] on the fast binary-state path?
+bool fp32_ok(lse_run* r);
+bool resident_now(lse_run* r) {
+  return r->resident && r->p.reinit_period == 1 && r->p.reg_period == 1 &&
+         r->mode != SRC_FIELD && fp32_ok(r);
+}
+
+int launch_resident(lse_run* r, long long steps) {
+  if (!r->d_res_parts) {
+    TRY(dalloc(&r->d_res_parts, (size_t)r->res_ctas));
+    TRY(dalloc(&r->d_sync, 1));
+  }
+  FastParams P = fast_params(r);
+  ResidentArgs A{};
+  A.bits[0] = r->d_bits[0];
+  A.bits[1] = r->d_bits[1];
+  A.cur0 = r->cur;
+  A.scaled = r->mode == SRC_SCALED ? 1 : 0;
+  A.it0 = r->iteration;
+  A.steps = steps;
+  A.cce = r->p.conv_check_every;
+  A.ncb = (r->W + kResCols - 1) / kResCols;
+  A.ntasks = r->res_tasks;
+  A.parts = r->d_res_parts;
+  A.sync = r->d_sync;
+  if (r->res_grid) CK(cudaMemsetAsync(r->d_sync, 0, sizeof(unsigned int), r->st));
+  cudaEvent_t e0 = nullptr, e1 = nullptr;
+  if (r->prof) {
+    e0 = next_event(r);
+    e1 = next_event(r);
+    cudaEventRecord(e0, r->st);
+  }
+  if (two_mean(r->p.model)) TRY(resident_launch_m<REGION>(r, P, A));
+  else TRY(resident_launch_m<EDGE>(r, P, A));
+  if (r->prof) {
+    cudaEventRecord(e1, r->st);
+    r->evrec.push_back({e0, e1, e1, true, false});
+  }
+  for (long long k = 1; k <= steps; ++k) r->launched.emplace_back(A.it0 + k, A.cur0 ^ (int)(k & 1));
+  r->cur = A.cur0 ^ (int)(steps & 1);
+  r->mode = SRC_SMOOTH;
+  r->field_valid = false;
+  r->iteration = A.it0 + steps;
+  r->fast_iters += steps;
+  r->resident_calls++;
+  return LSE_OK;
 }
 
 // -signed_distance(f > 0) of a dense field (engine.py:161-165) into out (may
@@ -1520,6 +1678,7 @@ int create_impl(lse_run** out, const lse_params* p, long long height, long long 
     if (const char* cv = std::getenv("LSE_FIX_CAP"))   // (tests: force the redo pass)
       if (fz) r->fix_cap = (unsigned)std::max(0LL, std::atoll(cv));
   }
+  resident_setup(r);
   const long long nparts = std::max<long long>(
       std::max<long long>(std::max<long long>(r->g.ntiles, r->ni_part + r->nb_part),
                           r->fused ? r->nb_upd[0] + r->ni_upd : 0LL),
@@ -1828,6 +1987,13 @@ int lse_run_advance(lse_run* r, long long n_steps, lse_status* st) {
   if (r->fused)
     CK(cudaMemsetAsync(reinterpret_cast<char*>(r->d_scal) + offsetof(Scalars, fix_n), 0,
                        sizeof(unsigned int) * 2, r->st));
+  if (resident_now(r)) {
+    // small image: the whole call is one resident kernel (lse_resident.cuh)
+    TRY(launch_resident(r, steps));
+    TRY(collect(r));
+    fill_status(r, st, -1);
+    return LSE_OK;
+  }
   for (long long it = it0 + 1; it <= it0 + steps; ++it) {
     const bool reinit_now = r->p.reinit_period > 0 && it % r->p.reinit_period == 0;
     const bool reg_now = it % r->p.reg_period == 0;
@@ -2015,6 +2181,15 @@ int lse_run_spec_stats(lse_run* r, long long* out4) {
   out4[1] = (long long)r->h_scal->spec_redos;
   out4[2] = (long long)r->h_scal->spec_fixes;
   out4[3] = r->fused ? 1 : 0;
+  return LSE_OK;
+}
+
+int lse_run_resident_stats(lse_run* r, long long* out4) {
+  if (!r || !out4) return fail(LSE_ERR_ARG, "null argument");
+  out4[0] = r->resident ? 1 : 0;
+  out4[1] = r->res_grid ? 1 : 0;
+  out4[2] = r->res_ctas;
+  out4[3] = r->resident_calls;
   return LSE_OK;
 }
 
@@ -2543,7 +2718,7 @@ void lse_run_destroy(lse_run* r) {
                   r->d_work, r->d_part_fin, r->d_part_init, r->d_data32, r->d_data64, r->d_bits[0], r->d_bits[1], r->d_P, r->d_M,
                   r->d_mask, r->d_part, r->d_scal, r->d_lut_t, r->d_lut_s, r->d_ctx,
                   r->d_w64, r->d_keys, r->d_count, r->d_F[0], r->d_F[1], r->d_U, r->d_T,
-                  r->d_fix};
+                  r->d_fix, r->d_res_parts, r->d_sync};
   for (void* q : ptrs)
     if (q) cudaFree(q);
   if (r->h_scal) cudaFreeHost(r->h_scal);

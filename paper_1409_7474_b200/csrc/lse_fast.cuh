@@ -236,7 +236,14 @@ __device__ __noinline__ double exact_u(const ExactCtx* c, const uint32_t* bits, 
 // near-tie costs one round of L2 latency instead of hundreds of dependent
 // loads.  val/valid hold, per window column, the signs and the in-image mask
 // of window rows r0 .. r0+NR-1.
-template <int NR, int NC>
+// (CG: the state is rewritten inside the running kernel -- the resident
+// kernels of lse_resident.cuh -- so its words are read at L2, never through
+// the non-coherent path)
+template <bool CG>
+__device__ __forceinline__ uint32_t state_word(const uint32_t* p) {
+  return CG ? __ldcg(p) : __ldg(p);
+}
+template <int NR, int NC, bool CG = false>
 __device__ __forceinline__ void gather_window(const ExactCtx* c, const uint32_t* bits, int r0,
                                               int xc0, uint32_t (&val)[NC], uint32_t (&valid)[NC]) {
   const int H = c->H, W = c->W, HR = (H + 31) >> 5;
@@ -250,8 +257,8 @@ __device__ __forceinline__ void gather_window(const ExactCtx* c, const uint32_t*
     const int xc = xc0 + cc;
     uint32_t lo = 0u, hi = 0u;
     if (xc >= 0 && xc < W) {
-      if (wr >= 0 && wr < HR) lo = __ldg(&bits[(size_t)wr * c->pitch_w + xc]);
-      if (wr + 1 >= 0 && wr + 1 < HR) hi = __ldg(&bits[(size_t)(wr + 1) * c->pitch_w + xc]);
+      if (wr >= 0 && wr < HR) lo = state_word<CG>(&bits[(size_t)wr * c->pitch_w + xc]);
+      if (wr + 1 >= 0 && wr + 1 < HR) hi = state_word<CG>(&bits[(size_t)(wr + 1) * c->pitch_w + xc]);
       valid[cc] = rows_ok;
     } else {
       valid[cc] = 0u;
@@ -300,7 +307,7 @@ __device__ __forceinline__ double wphi(const ExactCtx* c, const uint32_t (&val)[
 // value is a table entry, so all of them are loaded at once -- no per-value
 // branch to serialise the loads (the general path above takes ~45 dependent
 // L2 round trips, ~10 us per evaluation) -- then combined in scipy's order.
-template <int R, int NC>
+template <int R, int NC, bool CG = false>
 __device__ __forceinline__ void interior_window(const ExactCtx* c, const uint32_t* bits, int r0,
                                                 int xc0, uint32_t (&val)[NC]) {
   const int HR = (c->H + 31) >> 5;
@@ -309,8 +316,8 @@ __device__ __forceinline__ void interior_window(const ExactCtx* c, const uint32_
   const bool two = wr + 1 < HR;
 #pragma unroll
   for (int cc = 0; cc < NC; ++cc) {
-    const uint32_t lo = __ldg(p + cc);
-    const uint32_t hi = two ? __ldg(p + c->pitch_w + cc) : 0u;
+    const uint32_t lo = state_word<CG>(p + cc);
+    const uint32_t hi = two ? state_word<CG>(p + c->pitch_w + cc) : 0u;
     val[cc] = __funnelshift_r(lo, hi, sh);
   }
 }
@@ -331,7 +338,7 @@ __device__ __forceinline__ double wphi_row(const double (&t)[NC], int cc, const 
 }
 
 // phi^{n+1} at (i, x) exactly (partition near-ties)
-template <int R>
+template <int R, bool CG = false>
 __device__ __noinline__ double exact_phi_fast(const ExactCtx* c, const uint32_t* bits, int i, int x,
                                               bool count = true) {
   constexpr int NR = 2 * R + 1, NC = 2 * R + 1;
@@ -341,14 +348,14 @@ __device__ __noinline__ double exact_phi_fast(const ExactCtx* c, const uint32_t*
 #pragma unroll
     for (int d = 0; d <= R; ++d) w[d] = c->w64[d];
     uint32_t v[NC];
-    interior_window<R, NC>(c, bits, i - R, x - R, v);
+    interior_window<R, NC, CG>(c, bits, i - R, x - R, v);
     double t[NC];
     lut_row<R, NC>(c->lut64, v, R, t);
     if (count) atomicAdd(&c->scal->fallbacks, 1ull);
     return wphi_row<R, NC>(t, R, w);
   }
   uint32_t val[NC], valid[NC];
-  gather_window<NR, NC>(c, bits, i - R, x - R, val, valid);
+  gather_window<NR, NC, CG>(c, bits, i - R, x - R, val, valid);
   if (count) atomicAdd(&c->scal->fallbacks, 1ull);
   return wphi<R, NC>(c, val, valid, R, R);
 }
@@ -356,7 +363,7 @@ __device__ __noinline__ double exact_phi_fast(const ExactCtx* c, const uint32_t*
 // u at (i, x) exactly (update near-ties): phi at the pixel and its four
 // neighbours (np.gradient one-sided at the image border), glibc hypot,
 // the model's velocity, u = phi + dt * v.
-template <int R, int SRC>
+template <int R, int SRC, bool CG = false>
 __device__ __noinline__ double exact_u_fast(const ExactCtx* c, const uint32_t* bits, int i, int x,
                                             bool count = true) {
   constexpr int NR = 2 * R + 3, NC = 2 * R + 3;
@@ -371,7 +378,7 @@ __device__ __noinline__ double exact_u_fast(const ExactCtx* c, const uint32_t* b
 #pragma unroll
     for (int d = 0; d <= R; ++d) w[d] = c->w64[d];
     uint32_t v[NC];
-    interior_window<R, NC>(c, bits, i - 1 - R, x - 1 - R, v);
+    interior_window<R, NC, CG>(c, bits, i - 1 - R, x - 1 - R, v);
     double tu[NC], tc[NC], td[NC];
     lut_row<R, NC>(c->lut64, v, R, tu);
     lut_row<R, NC>(c->lut64, v, R + 1, tc);
@@ -388,7 +395,7 @@ __device__ __noinline__ double exact_u_fast(const ExactCtx* c, const uint32_t* b
     return dadd(pc, dmul(c->dt, v2));
   }
   uint32_t val[NC], valid[NC];
-  gather_window<NR, NC>(c, bits, i - 1 - R, x - 1 - R, val, valid);
+  gather_window<NR, NC, CG>(c, bits, i - 1 - R, x - 1 - R, val, valid);
   auto ph = [&](int di, int dx) -> double {      // phi at (i + di, x + dx)
     if (SRC == SRC_SCALED) {
       const int cc = R + 1 + dx, rr = R + 1 + di;

@@ -399,6 +399,13 @@ class EvolutionRun:
         return dict(fused=int(out[0]), redos=int(out[1]), fixes=int(out[2]),
                     enabled=bool(out[3]))
 
+    def resident_stats(self) -> dict:
+        """Resident-kernel path of small images (diagnostics; results are the
+        same with LSE_RESIDENT=0): enabled, barrier kind, CTAs, calls served."""
+        out = (C.c_longlong * 4)()
+        N.check(N.lib.lse_run_resident_stats(self._dev.h, out))
+        return dict(enabled=bool(out[0]), grid=bool(out[1]), ctas=int(out[2]), calls=int(out[3]))
+
     def path_counts(self) -> tuple[int, int]:
         st = self._dev.status()
         return int(st.fast_iterations), int(st.generic_iterations)
