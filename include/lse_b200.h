@@ -187,11 +187,11 @@ int lse_run_band_stats(lse_run* run, long long* out2);
 /* Small single images (lse_resident.cuh): a whole lse_run_advance call runs as
  * one resident kernel -- iterations separated by cluster / grid barriers
  * instead of kernel launches (replaces the launch chain of engine.py:242-254's
- * loop; same results).  out[4] = {resident path enabled (0/1), barrier kind
+ * loop; same results).  out[5] = {resident path enabled (0/1), barrier kind
  * (0 one thread-block cluster, 1 cooperative grid), CTAs of the launch,
- * advance calls served}.  LSE_RESIDENT=0 at creation disables it, 2 forces
- * the grid barrier. */
-int lse_run_resident_stats(lse_run* run, long long* out4);
+ * advance calls served, tasks (32 rows x 8 columns) per warp}.
+ * LSE_RESIDENT=0 at creation disables it, 2 forces the grid barrier. */
+int lse_run_resident_stats(lse_run* run, long long* out5);
 
 void lse_run_destroy(lse_run* run);
 

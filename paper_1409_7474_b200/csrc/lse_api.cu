@@ -317,7 +317,7 @@ struct lse_run {
   // resident kernel (lse_resident.cuh): whole advance() calls of small images
   // in one launch -- one cluster (res_grid false) or a cooperative grid
   bool resident = false, res_grid = false;
-  int res_ctas = 0, res_tasks = 0;
+  int res_ctas = 0, res_tasks = 0, res_nt = 1;
   TilePartial* d_res_parts = nullptr;
   unsigned int* d_sync = nullptr;
   long long resident_calls = 0;
@@ -909,9 +909,9 @@ bool fp32_ok(lse_run* r) {
 // (lse_resident.cuh) whole advance() calls of small single images in one
 // launch.  LSE_RESIDENT=0 keeps the per-iteration launches, 2 forces the
 // cooperative-grid barrier where one cluster would do (tests / A-B).
-template <int R, int MODEL, bool GRID>
+template <int R, int MODEL, bool GRID, int NT>
 int resident_launch_k(lse_run* r, const FastParams& P, const ResidentArgs& A) {
-  auto kern = k_resident<R, MODEL, GRID>;
+  auto kern = k_resident<R, MODEL, GRID, NT>;
   cudaLaunchConfig_t cfg{};
   cfg.gridDim = dim3((unsigned)r->res_ctas);
   cfg.blockDim = dim3(kResThreads);
@@ -938,8 +938,13 @@ int resident_launch_k(lse_run* r, const FastParams& P, const ResidentArgs& A) {
 
 template <int R, int MODEL>
 int resident_launch_rm(lse_run* r, const FastParams& P, const ResidentArgs& A) {
-  if (r->res_grid) return resident_launch_k<R, MODEL, true>(r, P, A);
-  return resident_launch_k<R, MODEL, false>(r, P, A);
+  if (MODEL == EDGE && r->res_nt > 1) {          // (several tasks per warp: grid launches only)
+    constexpr int M2 = EDGE;
+    if (r->res_nt == 2) return resident_launch_k<R, M2, true, 2>(r, P, A);
+    return resident_launch_k<R, M2, true, 3>(r, P, A);
+  }
+  if (r->res_grid) return resident_launch_k<R, MODEL, true, 1>(r, P, A);
+  return resident_launch_k<R, MODEL, false, 1>(r, P, A);
 }
 
 template <int MODEL>
@@ -957,7 +962,7 @@ int resident_launch_m(lse_run* r, const FastParams& P, const ResidentArgs& A) {
 template <bool GRID>
 int resident_capacity(int ctas) {
   // occupancy of the widest instantiation stands for all (same launch bounds)
-  auto kern = k_resident<4, REGION, GRID>;
+  auto kern = k_resident<4, REGION, GRID, 1>;
   if (GRID) {
     int per_sm = 0;
     if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, kResThreads, 0) != cudaSuccess)
@@ -987,6 +992,8 @@ int resident_capacity(int ctas) {
   return nclusters > 0 ? ctas : 0;
 }
 
+constexpr int kResMaxTasksPerWarp = 3;           // edge runs (k_resident NT)
+
 void resident_setup(lse_run* r) {
   r->resident = false;
   int mode = 1;
@@ -994,17 +1001,33 @@ void resident_setup(lse_run* r) {
 #ifdef LSE_CHECK_BOUND
   mode = 0;                                      // validation builds certify the per-iteration kernels
 #endif
-  if (mode == 0 || !r->fine || is_bands(r) || is_cv(r) || r->strip) return;
+  const bool edge = r->p.model == LSE_MODEL_EDGE;
+  if (mode == 0 || is_bands(r) || is_cv(r) || r->strip || r->R < 1 || r->R > 4) return;
+  // region / zhang: one task per warp (phi stays in registers across the
+  // coefficient barrier) -- the per-pixel kernels' size range; edge: up to
+  // kResMaxTasksPerWarp tasks per warp of a full cooperative grid
+  if (!edge && !r->fine) return;
   const int ncb = (r->W + kResCols - 1) / kResCols;
   const long long tasks = (long long)r->g.HR * ncb;
-  const int ctas = (int)((tasks + kResWarps - 1) / kResWarps);
+  long long ctas = (tasks + kResWarps - 1) / kResWarps;
+  int nt = 1;
   bool grid = mode == 2 || ctas > kResClusterMax;
-  if (!grid && resident_capacity<false>(ctas) < ctas) grid = true;
-  if (grid && resident_capacity<true>(ctas) < ctas) return;
+  if (!grid && resident_capacity<false>((int)ctas) < ctas) grid = true;
+  if (grid) {
+    const int cap = resident_capacity<true>((int)ctas);
+    if (cap <= 0) return;
+    if (ctas > cap) {
+      if (!edge) return;
+      nt = (int)((ctas + cap - 1) / cap);
+      if (nt > kResMaxTasksPerWarp) return;
+      ctas = (ctas + nt - 1) / nt;               // balanced: every warp has nt or nt-1 tasks
+    }
+  }
   r->resident = true;
   r->res_grid = grid;
-  r->res_ctas = ctas;
+  r->res_ctas = (int)ctas;
   r->res_tasks = (int)tasks;
+  r->res_nt = nt;
 }
 
 // is the whole call [it0+1, it0+steps] on the fast binary-state path?
@@ -1017,7 +1040,7 @@ bool resident_now(lse_run* r) {
 int launch_resident(lse_run* r, long long steps) {
   if (!r->d_res_parts) {
     TRY(dalloc(&r->d_res_parts, (size_t)r->res_ctas));
-    TRY(dalloc(&r->d_sync, 1));
+    TRY(dalloc(&r->d_sync, 64));
   }
   FastParams P = fast_params(r);
   ResidentArgs A{};
@@ -1032,7 +1055,7 @@ int launch_resident(lse_run* r, long long steps) {
   A.ntasks = r->res_tasks;
   A.parts = r->d_res_parts;
   A.sync = r->d_sync;
-  if (r->res_grid) CK(cudaMemsetAsync(r->d_sync, 0, sizeof(unsigned int), r->st));
+  if (r->res_grid) CK(cudaMemsetAsync(r->d_sync, 0, 64 * sizeof(unsigned int), r->st));
   cudaEvent_t e0 = nullptr, e1 = nullptr;
   if (r->prof) {
     e0 = next_event(r);
@@ -2184,12 +2207,13 @@ int lse_run_spec_stats(lse_run* r, long long* out4) {
   return LSE_OK;
 }
 
-int lse_run_resident_stats(lse_run* r, long long* out4) {
-  if (!r || !out4) return fail(LSE_ERR_ARG, "null argument");
-  out4[0] = r->resident ? 1 : 0;
-  out4[1] = r->res_grid ? 1 : 0;
-  out4[2] = r->res_ctas;
-  out4[3] = r->resident_calls;
+int lse_run_resident_stats(lse_run* r, long long* out5) {
+  if (!r || !out5) return fail(LSE_ERR_ARG, "null argument");
+  out5[0] = r->resident ? 1 : 0;
+  out5[1] = r->res_grid ? 1 : 0;
+  out5[2] = r->res_ctas;
+  out5[3] = r->resident_calls;
+  out5[4] = r->res_nt;
   return LSE_OK;
 }
 

@@ -50,10 +50,14 @@ struct ResidentArgs {
   long long cce;           // conv_check_every
   int ntasks, ncb;         // warp tasks = HR * ncb, ncb = ceil(W / kResCols)
   TilePartial* parts;      // one partial per CTA
-  unsigned int* sync;      // grid barrier counter (zero at launch; GRID only)
+  unsigned int* sync;      // grid barrier arrival counter (zero at launch; GRID only)
 };
 
 // All CTAs of the launch: memory written before is visible (at L2) after.
+// (Grid barrier: every CTA polls the arrival counter itself.  Publishing the
+// epoch on a second line for the others to poll measured slower -- the
+// release costs the last arriver two more L2 round trips: C2 107 -> 98
+// Gpix-it/s.)
 template <bool GRID>
 __device__ __forceinline__ void res_sync(unsigned int* ctr, unsigned int& epoch) {
   if (GRID) {
@@ -132,8 +136,14 @@ __device__ __forceinline__ void res_checkpoint(Scalars* sc, unsigned long long m
 #define RES_T(k) do { } while (0)
 #endif
 
-template <int R, int MODEL, bool GRID>
+// NT: tasks per warp.  Region / zhang runs need the coefficients between the
+// partition and the update of an iteration, so a warp keeps phi and |grad phi|
+// of its task across the barrier: NT = 1.  Edge runs have constant
+// coefficients: a warp finishes one task (phi -> checkpoint words -> update)
+// before the next, so NT > 1 costs only the data registers (larger images).
+template <int R, int MODEL, bool GRID, int NT>
 __global__ void __launch_bounds__(kResThreads, 1) k_resident(FastParams P, ResidentArgs A) {
+  static_assert(MODEL == EDGE || NT == 1, "region runs keep one task per warp");
   constexpr int CW = kResCols;
   constexpr int NPAT = 1 << (2 * R + 1);
   constexpr int NC = CW + 2 * R + 2;             // window columns x0-R-1 .. x0+CW+R
@@ -166,25 +176,29 @@ __global__ void __launch_bounds__(kResThreads, 1) k_resident(FastParams P, Resid
   if (!GRID) res_sync<GRID>(A.sync, epoch);      // every CTA of the cluster is running (DSMEM)
 
   const int H = P.g.H, W = P.g.W, HR = P.g.HR, pitch_w = P.g.pitch_w;
-  const int task = blockIdx.x * kResWarps + warp;
-  const bool active = task < A.ntasks;
-  const int r = active ? task / A.ncb : 0;
-  const int x0 = active ? (task - r * A.ncb) * CW : 0;
-  const int i = r * 32 + lane;
-  const bool rowok = active && i < H;
-  float d[CW];                                   // this lane's data values, all iterations
+  // task t of this warp: consecutive warps of the launch take adjacent tasks
+  int tk_r[NT], tk_x0[NT];
+  bool tk_on[NT];
+  float d[NT][CW];                               // this lane's data values, all iterations
+  uint32_t pold[NT], mold[NT];                   // lane c: partition / checkpoint word of column x0+c
 #pragma unroll
-  for (int c = 0; c < CW; ++c)
-    d[c] = (rowok && x0 + c < W) ? __ldg(P.data32 + (size_t)i * P.g.data_pitch + x0 + c) : 0.f;
-  // lane c keeps the partition / checkpoint words of column x0 + c
-  const bool wlane = active && lane < CW && x0 + lane < W;
-  const size_t wofs = (size_t)r * pitch_w + x0 + lane;
-  uint32_t pold = 0u, mold = 0u;
-  if (wlane) {
-    pold = __ldcg(P.pbits + wofs);
-    mold = __ldcg(P.mbits + wofs);
+  for (int t = 0; t < NT; ++t) {
+    const int task = (t * (int)gridDim.x + (int)blockIdx.x) * kResWarps + warp;
+    tk_on[t] = task < A.ntasks;
+    tk_r[t] = tk_on[t] ? task / A.ncb : 0;
+    tk_x0[t] = tk_on[t] ? (task - tk_r[t] * A.ncb) * CW : 0;
+    const int i = tk_r[t] * 32 + lane;
+#pragma unroll
+    for (int c = 0; c < CW; ++c)
+      d[t][c] = (tk_on[t] && i < H && tk_x0[t] + c < W)
+                    ? __ldg(P.data32 + (size_t)i * P.g.data_pitch + tk_x0[t] + c) : 0.f;
+    pold[t] = mold[t] = 0u;
+    if (tk_on[t] && lane < CW && tk_x0[t] + lane < W) {
+      const size_t wofs = (size_t)tk_r[t] * pitch_w + tk_x0[t] + lane;
+      pold[t] = __ldcg(P.pbits + wofs);
+      mold[t] = __ldcg(P.mbits + wofs);
+    }
   }
-  const bool cols_in = x0 - R - 1 >= 0 && x0 + CW + R <= W - 1;
   const float eps_phi = s_sc.eps_phi;
   const int up = lane > R ? 1 : 0;
   const int sh = up ? lane - R - 1 : lane + 31 - R;
@@ -198,111 +212,166 @@ __global__ void __launch_bounds__(kResThreads, 1) k_resident(FastParams P, Resid
   for (long long n = A.it0;; ++n) {
     RES_T(7);
     const uint32_t* bits = A.bits[cur];
+    uint32_t* bits_next = A.bits[cur ^ 1];
     const bool first = n == A.it0;
     const bool scaled = first && A.scaled;
+    const bool more = n != it_end;               // an update n -> n+1 follows
+    // partition / checkpoint of b^n (owed by update n; not on entry)
+    const bool do_part = !first && MODEL == REGION;
+    const bool do_ckpt = !first && to_ckpt == 0;
+    if (!first) to_ckpt = to_ckpt == 0 ? A.cce - 1 : to_ckpt - 1;
+    double a_in = 0.0, a_out = 0.0;
+    int n_in = 0, n_out = 0, mism = 0;           // (a warp's pixels: 32-bit counts)
     float p0[CW], hh[CW];                        // phi^n and 2 |grad phi^n| at the lane's pixels
-    if (active) {
-      for (int q = lane; q < 3 * NC; q += 32) {
-        const int row = q / NC, col = q - row * NC;
-        const int wr = r - 1 + row, xc = x0 - R - 1 + col;
-        s_w[warp][row][col] = (wr >= 0 && wr < HR && xc >= 0 && xc < W)
-                                  ? __ldcg(bits + (size_t)wr * pitch_w + xc) : 0u;
-      }
-      __syncwarp();
-      RES_T(8);
-      // window of each column: 32 rows from i-R-1 (k_update_fine's frame)
-      uint32_t win[NC];
-#pragma unroll
-      for (int j = 0; j < NC; ++j) win[j] = __funnelshift_r(s_w[warp][up][j], s_w[warp][up + 1][j], sh);
-      __syncwarp();
-      RES_T(9);
-      float pm[CW], pn[CW];
-      float pc[CW + 2];                          // phi of row i at columns x0-1 .. x0+CW
-      if (scaled) {                              // phi = +-s (binary initial state)
-        auto ps = [&](int j, int m) { return ((win[j] >> (m + R)) & 1u) ? P.scale32 : -P.scale32; };
-#pragma unroll
-        for (int j0 = 0; j0 < CW + 2; ++j0) pc[j0] = ps(j0 + R, 1);
-#pragma unroll
-        for (int c = 0; c < CW; ++c) {
-          pm[c] = ps(c + R + 1, 0);
-          pn[c] = ps(c + R + 1, 2);
-        }
-      } else {
-        float t[NC];
-        auto row_in = [&](int row) { return cols_in && row - R >= 0 && row + R <= H - 1; };
-        {
-          const bool in = row_in(i);
-          const uint32_t v0 = in ? 0u : row_valid_mask<R>(i, H);
-          res_trow<R, NC>(win, x0 - R - 1, W, 1, in, v0, in ? 0.f : s_ls[v0], s_lt, s_ls, t);
-#pragma unroll
-          for (int j0 = 0; j0 < CW + 2; ++j0) pc[j0] = fine_hsum<R, NC>(P, t, j0);
-        }
-        RES_T(10);
-#pragma unroll
-        for (int c = 0; c < CW; ++c) {
-          pm[c] = __shfl_up_sync(0xffffffffu, pc[c + 1], 1);
-          pn[c] = __shfl_down_sync(0xffffffffu, pc[c + 1], 1);
-        }
-        RES_T(11);
-        if (lane == 0 || lane == 31) {           // the row outside this warp
-          const int m = lane == 0 ? 0 : 2, row = i - 1 + m;
-          const bool in = row_in(row);
-          const uint32_t v = in ? 0u : row_valid_mask<R>(row, H);
-          res_trow<R, NC>(win, x0 - R - 1, W, m, in, v, in ? 0.f : s_ls[v], s_lt, s_ls, t);
-#pragma unroll
-          for (int c = 0; c < CW; ++c) {
-            const float pe = fine_hsum<R, NC>(P, t, c + 1);
-            if (lane == 0) pm[c] = pe;
-            else pn[c] = pe;
-          }
-        }
-        RES_T(12);
-      }
-      // np.gradient: central differences, one-sided at the image border --
-      // branch-free: the missing neighbour is replaced by the centre and the
-      // difference doubled (2 (b - a) and (b - a) 1 are exact scalings)
-      const bool yt = i == 0, yb = i == H - 1 && !yt;
-      const float sy = (yt || yb) ? 2.f : 1.f;
+
+    // b^{n+1} of task (r, x0) from p0 / hh and the coefficients; near ties in fp64
+    auto update_task = [&](int t, int r, int x0, float Av, float Bv, float eps_u) {
+      const int i = r * 32 + lane;
+      float u[CW];
 #pragma unroll
       for (int c = 0; c < CW; ++c) {
-        const int x = x0 + c;
-        p0[c] = pc[c + 1];
-        const bool xl = x == 0, xr = x == W - 1 && !xl;
-        const float xa = xl ? p0[c] : pc[c], xb = xr ? p0[c] : pc[c + 2];
-        const float ya = yt ? p0[c] : pm[c], yb2 = yb ? p0[c] : pn[c];
-        const float dx = (xb - xa) * ((xl || xr) ? 2.f : 1.f);
-        const float dy = (yb2 - ya) * sy;
-        hh[c] = sqrt_approx(fmaf(dx, dx, dy * dy));
-        // pixels outside the image: phi = -1, |grad| = 0 (never positive,
-        // never a near tie), so the loops below need no validity tests
-        if (!(rowok && x < W)) {
+        const float vf = (MODEL == REGION) ? fmaf(Av, d[t][c], Bv) : d[t][c];   // carry dt/2
+        u[c] = fmaf(vf, hh[c], p0[c]);
+      }
+      float umin = fabsf(u[0]);
+#pragma unroll
+      for (int c = 1; c < CW; ++c) umin = fminf(umin, fabsf(u[c]));
+      uint32_t wnew = 0u;
+      if (!__any_sync(0xffffffffu, umin <= eps_u)) {
+#pragma unroll
+        for (int c = 0; c < CW; ++c) {
+          const uint32_t w = __ballot_sync(0xffffffffu, u[c] > 0.f);
+          if (lane == c) wnew = w;
+        }
+      } else {                                   // near ties: the reference's fp64 decision
+        uint32_t b8 = 0u, tie8 = 0u;             // bit c: column x0 + c
+#pragma unroll
+        for (int c = 0; c < CW; ++c) {
+          b8 |= (u[c] > 0.f) ? (1u << c) : 0u;
+          tie8 |= (fabsf(u[c]) <= eps_u) ? (1u << c) : 0u;
+        }
+#pragma unroll 1
+        for (int c = 0; c < CW; ++c)
+          if ((tie8 >> c) & 1u) {
+            const double e = scaled ? exact_u_fast<R, SRC_SCALED, true>(&s_ctx, bits, i, x0 + c)
+                                    : exact_u_fast<R, SRC_SMOOTH, true>(&s_ctx, bits, i, x0 + c);
+            b8 = (b8 & ~(1u << c)) | (e > 0.0 ? (1u << c) : 0u);
+          }
+#pragma unroll
+        for (int c = 0; c < CW; ++c) {
+          const uint32_t w = __ballot_sync(0xffffffffu, (b8 >> c) & 1u);
+          if (lane == c) wnew = w;
+        }
+      }
+      if (lane < CW && x0 + lane < W) bits_next[(size_t)r * pitch_w + x0 + lane] = wnew;
+    };
+
+#pragma unroll
+    for (int t = 0; t < NT; ++t) {
+      const int r = tk_r[t], x0 = tk_x0[t];
+      const int i = r * 32 + lane;
+      const bool rowok = tk_on[t] && i < H;
+      if (tk_on[t]) {
+        for (int q = lane; q < 3 * NC; q += 32) {
+          const int row = q / NC, col = q - row * NC;
+          const int wr = r - 1 + row, xc = x0 - R - 1 + col;
+          s_w[warp][row][col] = (wr >= 0 && wr < HR && xc >= 0 && xc < W)
+                                    ? __ldcg(bits + (size_t)wr * pitch_w + xc) : 0u;
+        }
+        __syncwarp();
+        RES_T(8);
+        // window of each column: 32 rows from i-R-1 (k_update_fine's frame)
+        uint32_t win[NC];
+#pragma unroll
+        for (int j = 0; j < NC; ++j) win[j] = __funnelshift_r(s_w[warp][up][j], s_w[warp][up + 1][j], sh);
+        __syncwarp();
+        RES_T(9);
+        float pm[CW], pn[CW];
+        float pc[CW + 2];                        // phi of row i at columns x0-1 .. x0+CW
+        if (scaled) {                            // phi = +-s (binary initial state)
+          auto ps = [&](int j, int m) { return ((win[j] >> (m + R)) & 1u) ? P.scale32 : -P.scale32; };
+#pragma unroll
+          for (int j0 = 0; j0 < CW + 2; ++j0) pc[j0] = ps(j0 + R, 1);
+#pragma unroll
+          for (int c = 0; c < CW; ++c) {
+            pm[c] = ps(c + R + 1, 0);
+            pn[c] = ps(c + R + 1, 2);
+          }
+        } else {
+          float tv[NC];
+          const bool cols_in = x0 - R - 1 >= 0 && x0 + CW + R <= W - 1;
+          auto row_in = [&](int row) { return cols_in && row - R >= 0 && row + R <= H - 1; };
+          {
+            const bool in = row_in(i);
+            const uint32_t v0 = in ? 0u : row_valid_mask<R>(i, H);
+            res_trow<R, NC>(win, x0 - R - 1, W, 1, in, v0, in ? 0.f : s_ls[v0], s_lt, s_ls, tv);
+#pragma unroll
+            for (int j0 = 0; j0 < CW + 2; ++j0) pc[j0] = fine_hsum<R, NC>(P, tv, j0);
+          }
+          RES_T(10);
+#pragma unroll
+          for (int c = 0; c < CW; ++c) {
+            pm[c] = __shfl_up_sync(0xffffffffu, pc[c + 1], 1);
+            pn[c] = __shfl_down_sync(0xffffffffu, pc[c + 1], 1);
+          }
+          RES_T(11);
+          // the row outside this warp, on its two edge lanes (spreading it over
+          // 2 CW lanes -- one horizontal sum each from the staged words, then
+          // shuffles back -- measured slower: C1 9.85 -> 9.5 Gpix-it/s)
+          if (lane == 0 || lane == 31) {
+            const int m = lane == 0 ? 0 : 2, row = i - 1 + m;
+            const bool in = row_in(row);
+            const uint32_t v = in ? 0u : row_valid_mask<R>(row, H);
+            res_trow<R, NC>(win, x0 - R - 1, W, m, in, v, in ? 0.f : s_ls[v], s_lt, s_ls, tv);
+#pragma unroll
+            for (int c = 0; c < CW; ++c) {
+              const float pe = fine_hsum<R, NC>(P, tv, c + 1);
+              if (lane == 0) pm[c] = pe;
+              else pn[c] = pe;
+            }
+          }
+          RES_T(12);
+        }
+        // np.gradient: central differences, one-sided at the image border --
+        // branch-free: the missing neighbour is replaced by the centre and the
+        // difference doubled (2 (b - a) and (b - a) 1 are exact scalings)
+        const bool yt = i == 0, yb = i == H - 1 && !yt;
+        const float sy = (yt || yb) ? 2.f : 1.f;
+#pragma unroll
+        for (int c = 0; c < CW; ++c) {
+          const int x = x0 + c;
+          p0[c] = pc[c + 1];
+          const bool xl = x == 0, xr = x == W - 1 && !xl;
+          const float xa = xl ? p0[c] : pc[c], xb = xr ? p0[c] : pc[c + 2];
+          const float ya = yt ? p0[c] : pm[c], yb2 = yb ? p0[c] : pn[c];
+          const float dx = (xb - xa) * ((xl || xr) ? 2.f : 1.f);
+          const float dy = (yb2 - ya) * sy;
+          hh[c] = sqrt_approx(fmaf(dx, dx, dy * dy));
+          // pixels outside the image: phi = -1, |grad| = 0 (never positive,
+          // never a near tie), so the loops below need no validity tests
+          if (!(rowok && x < W)) {
+            p0[c] = -1.f;
+            hh[c] = 0.f;
+          }
+        }
+      } else {
+#pragma unroll
+        for (int c = 0; c < CW; ++c) {
           p0[c] = -1.f;
           hh[c] = 0.f;
         }
       }
-    } else {
-#pragma unroll
-      for (int c = 0; c < CW; ++c) {
-        p0[c] = -1.f;
-        hh[c] = 0.f;
-      }
-    }
+      RES_T(0);
 
-    RES_T(0);
-    // ---- partition / checkpoint of b^n (owed by update n; not on entry)
-    const bool do_part = !first && MODEL == REGION;
-    const bool do_ckpt = !first && to_ckpt == 0;
-    if (!first) to_ckpt = to_ckpt == 0 ? A.cce - 1 : to_ckpt - 1;
-    if (do_part || do_ckpt) {
-      double a_in = 0.0, a_out = 0.0;
-      int n_in = 0, n_out = 0, mism = 0;         // (a warp's pixels: 32-bit counts)
-      if (active) {
+      if ((do_part || do_ckpt) && tk_on[t]) {
         // signs of phi^n; near ties (rare: one warp-wide test on the smallest
         // |phi| of the lane) take the exact fp64 sign
+        const bool wlane = lane < CW && x0 + lane < W;
+        const size_t wofs = (size_t)r * pitch_w + x0 + lane;
         float amin = fabsf(p0[0]);
 #pragma unroll
         for (int c = 1; c < CW; ++c) amin = fminf(amin, fabsf(p0[c]));
-        uint32_t pnew = pold, mnew = mold;
+        uint32_t pnew = pold[t], mnew = mold[t];
         uint32_t pb8 = 0u;                       // bit c: this lane's pixel of column c is in P
         if (!__any_sync(0xffffffffu, amin <= eps_phi)) {
 #pragma unroll
@@ -341,28 +410,35 @@ __global__ void __launch_bounds__(kResThreads, 1) k_resident(FastParams P, Resid
           }
         }
         // sums of I over the pixels that changed side (few columns change)
-        if (do_part && __any_sync(0xffffffffu, wlane && pnew != pold)) {
+        if (do_part && __any_sync(0xffffffffu, wlane && pnew != pold[t])) {
 #pragma unroll
           for (int c = 0; c < CW; ++c) {
-            const uint32_t chg = __shfl_sync(0xffffffffu, pnew ^ pold, c);
+            const uint32_t chg = __shfl_sync(0xffffffffu, pnew ^ pold[t], c);
             if ((chg >> lane) & 1u) {
-              const double I = s_ctx.data64 ? data_exact(&s_ctx, i, x0 + c) : (double)d[c];
+              const double I = s_ctx.data64 ? data_exact(&s_ctx, i, x0 + c) : (double)d[t][c];
               if ((pb8 >> c) & 1u) { a_in += I; n_in += 1; }
               else { a_out += I; n_out += 1; }
             }
           }
         }
         if (wlane) {
-          if (do_part && pnew != pold) P.pbits[wofs] = pnew;
+          if (do_part && pnew != pold[t]) P.pbits[wofs] = pnew;
           if (do_ckpt) {
-            mism = __popc(mold ^ mnew);
+            mism += __popc(mold[t] ^ mnew);
             P.mbits[wofs] = mnew;
-            mold = mnew;
+            mold[t] = mnew;
           }
-          pold = pnew;
+          pold[t] = pnew;
         }
       }
       RES_T(13);
+      // edge runs: constant coefficients, the update follows at once (on a
+      // checkpoint that turns out converged, b^{n+1} lands in the buffer that
+      // is then not adopted)
+      if (MODEL == EDGE && more && tk_on[t]) update_task(t, r, x0, 0.f, 0.f, s_sc.eps_u);
+    }
+
+    if (do_part || do_ckpt) {
       // warp totals (few pixels change side: most warps have none to add)
       if (__any_sync(0xffffffffu, n_in + n_out != 0)) {
 #pragma unroll
@@ -398,9 +474,9 @@ __global__ void __launch_bounds__(kResThreads, 1) k_resident(FastParams P, Resid
         }
         if (GRID) {
           if (lane == 0) {
-            TilePartial t{};
-            t.a_hi = ca; t.b_hi = cb; t.n_a = cna; t.n_b = cnb; t.mism = (unsigned long long)cmm;
-            A.parts[blockIdx.x] = t;
+            TilePartial tp{};
+            tp.a_hi = ca; tp.b_hi = cb; tp.n_a = cna; tp.n_b = cnb; tp.mism = (unsigned long long)cmm;
+            A.parts[blockIdx.x] = tp;
           }
         } else if (lane < (int)gridDim.x) {
           // one cluster: straight into slot [this CTA] of CTA `lane`'s shared memory
@@ -421,19 +497,19 @@ __global__ void __launch_bounds__(kResThreads, 1) k_resident(FastParams P, Resid
         unsigned long long mm = 0;
         if (GRID) {
           for (int q = lane; q < (int)gridDim.x; q += 32) {
-            const TilePartial* p = A.parts + q;
-            const double2 SA = __ldcg(reinterpret_cast<const double2*>(&p->a_hi));
-            const double2 SB = __ldcg(reinterpret_cast<const double2*>(&p->b_hi));
-            const longlong2 NN = __ldcg(reinterpret_cast<const longlong2*>(&p->n_a));
+            const TilePartial* pp = A.parts + q;
+            const double2 SA = __ldcg(reinterpret_cast<const double2*>(&pp->a_hi));
+            const double2 SB = __ldcg(reinterpret_cast<const double2*>(&pp->b_hi));
+            const longlong2 NN = __ldcg(reinterpret_cast<const longlong2*>(&pp->n_a));
             dd_add_dd(ah, al, SA.x, SA.y);
             dd_add_dd(bh, bl, SB.x, SB.y);
             na += NN.x;
             nb += NN.y;
-            mm += __ldcg(&p->mism);
+            mm += __ldcg(&pp->mism);
           }
         } else if (lane < (int)gridDim.x) {
-          const volatile ResPart* p = &s_parts[lane];
-          ah = p->a; bh = p->b; na = p->na; nb = p->nb; mm = p->mm;
+          const volatile ResPart* pp = &s_parts[lane];
+          ah = pp->a; bh = pp->b; na = pp->na; nb = pp->nb; mm = pp->mm;
         }
         RES_T(16);
         int np2 = 1;
@@ -441,10 +517,12 @@ __global__ void __launch_bounds__(kResThreads, 1) k_resident(FastParams P, Resid
 #pragma unroll
         for (int o = 16; o > 0; o >>= 1) {
           if (o < np2) {                         // (lanes beyond the CTA count hold zeros)
-            dd_shfl_add(ah, al, o);
-            dd_shfl_add(bh, bl, o);
-            na += __shfl_xor_sync(0xffffffffu, na, o);
-            nb += __shfl_xor_sync(0xffffffffu, nb, o);
+            if (MODEL == REGION) {
+              dd_shfl_add(ah, al, o);
+              dd_shfl_add(bh, bl, o);
+              na += __shfl_xor_sync(0xffffffffu, na, o);
+              nb += __shfl_xor_sync(0xffffffffu, nb, o);
+            }
             mm += __shfl_xor_sync(0xffffffffu, mm, o);
           }
         }
@@ -467,50 +545,14 @@ __global__ void __launch_bounds__(kResThreads, 1) k_resident(FastParams P, Resid
       RES_T(3);
       if (s_sc.stop) break;                      // converged at n: b^n stays the state
     }
-    if (n == it_end) break;
+    if (!more) break;
 
-    // ---- update n -> n+1
-    const float Av = s_sc.A, Bv = s_sc.B, eps_u = s_sc.eps_u;
-    if (MODEL == REGION && tid == 0 && s_sc.zero_vel && s_sc.model != EDGE)
-      s_sc.degenerate = 1;                       // sticky degenerate (engine.py:239-240)
-    if (active) {
-      float u[CW];
-#pragma unroll
-      for (int c = 0; c < CW; ++c) {
-        const float vf = (MODEL == REGION) ? fmaf(Av, d[c], Bv) : d[c];   // carry dt/2
-        u[c] = fmaf(vf, hh[c], p0[c]);
-      }
-      float umin = fabsf(u[0]);
-#pragma unroll
-      for (int c = 1; c < CW; ++c) umin = fminf(umin, fabsf(u[c]));
-      uint32_t wnew = 0u;
-      if (!__any_sync(0xffffffffu, umin <= eps_u)) {
-#pragma unroll
-        for (int c = 0; c < CW; ++c) {
-          const uint32_t w = __ballot_sync(0xffffffffu, u[c] > 0.f);
-          if (lane == c) wnew = w;
-        }
-      } else {                                   // near ties: the reference's fp64 decision
-        uint32_t b8 = 0u, tie8 = 0u;             // bit c: column x0 + c
-#pragma unroll
-        for (int c = 0; c < CW; ++c) {
-          b8 |= (u[c] > 0.f) ? (1u << c) : 0u;
-          tie8 |= (fabsf(u[c]) <= eps_u) ? (1u << c) : 0u;
-        }
-#pragma unroll 1
-        for (int c = 0; c < CW; ++c)
-          if ((tie8 >> c) & 1u) {
-            const double e = scaled ? exact_u_fast<R, SRC_SCALED, true>(&s_ctx, bits, i, x0 + c)
-                                    : exact_u_fast<R, SRC_SMOOTH, true>(&s_ctx, bits, i, x0 + c);
-            b8 = (b8 & ~(1u << c)) | (e > 0.0 ? (1u << c) : 0u);
-          }
-#pragma unroll
-        for (int c = 0; c < CW; ++c) {
-          const uint32_t w = __ballot_sync(0xffffffffu, (b8 >> c) & 1u);
-          if (lane == c) wnew = w;
-        }
-      }
-      if (wlane) A.bits[cur ^ 1][wofs] = wnew;
+    // ---- update n -> n+1 (region / zhang: with the coefficients just derived)
+    if (MODEL == REGION) {
+      const float Av = s_sc.A, Bv = s_sc.B, eps_u = s_sc.eps_u;
+      if (tid == 0 && s_sc.zero_vel && s_sc.model != EDGE)
+        s_sc.degenerate = 1;                     // sticky degenerate (engine.py:239-240)
+      if (tk_on[0]) update_task(0, tk_r[0], tk_x0[0], Av, Bv, eps_u);
     }
     RES_T(4);
     res_sync<GRID>(A.sync, epoch);
@@ -519,11 +561,11 @@ __global__ void __launch_bounds__(kResThreads, 1) k_resident(FastParams P, Resid
   }
 #ifdef LSE_RES_TRACE
   if (tid == 0 && blockIdx.x == 0)
-    printf("res trace (cycles, %lld its): phi %lld part %lld sync1 %lld finalize %lld update %lld "
+    printf("res trace (cycles, %lld its): phi+grad %lld cta %lld sync1 %lld finalize %lld update %lld "
            "sync2 %lld loop %lld fallbacks %llu\n", A.steps, tr[0], tr[1], tr[2], tr[3], tr[4], tr[5],
            tr[7], s_sc.fallbacks - fallbacks0);
   if (tid == 0 && blockIdx.x == 0)
-    printf("  phi: stage %lld win %lld hsum %lld shfl %lld outer %lld grad %lld | part: cols %lld tree %lld "
+    printf("  phi: stage %lld win %lld hsum %lld shfl %lld outer %lld grad %lld | part: cols(+edge update) %lld tree %lld "
            "bar %lld cta %lld | fin: load %lld tree %lld coef %lld bar %lld\n", tr[8], tr[9], tr[10],
            tr[11], tr[12], tr[0], tr[13], tr[14], tr[15], tr[1], tr[16], tr[17], tr[18], tr[3]);
 #endif

@@ -402,9 +402,10 @@ class EvolutionRun:
     def resident_stats(self) -> dict:
         """Resident-kernel path of small images (diagnostics; results are the
         same with LSE_RESIDENT=0): enabled, barrier kind, CTAs, calls served."""
-        out = (C.c_longlong * 4)()
+        out = (C.c_longlong * 5)()
         N.check(N.lib.lse_run_resident_stats(self._dev.h, out))
-        return dict(enabled=bool(out[0]), grid=bool(out[1]), ctas=int(out[2]), calls=int(out[3]))
+        return dict(enabled=bool(out[0]), grid=bool(out[1]), ctas=int(out[2]), calls=int(out[3]),
+                    tasks_per_warp=int(out[4]))
 
     def path_counts(self) -> tuple[int, int]:
         st = self._dev.status()

@@ -158,3 +158,36 @@ def test_degenerate_and_float32_image(monkeypatch):
         assert out[0].resident_stats()["calls"] == 2
         same(out[0], out[1])
         assert out[0].state.degenerate == degenerate
+
+
+def test_c2_golden_several_tasks_per_warp():
+    """BASELINE C2 (1024^2 edge, 500 iterations): 4096 warp tasks on a
+    cooperative grid, two per warp; the reference's phi (SHA-256)."""
+    from test_gpu_parity import params_from, sha
+    g = load_golden("traj_C2")
+    sc = scenes.config2()
+    r = L.EvolutionRun(sc.image, L.SeedSpec(polygons=sc.polygons, inside_sign=sc.inside_sign),
+                       params_from(g))
+    for n in (130, 1, sc.iters):
+        r.advance(n)
+    st = r.resident_stats()
+    assert st["enabled"] and st["grid"] and st["tasks_per_warp"] >= 2, st
+    assert r.state.iteration == sc.iters
+    assert sha(r.state.phi) == str(g[f"sha_{sc.iters}"])
+
+
+@pytest.mark.parametrize("shape", [(700, 900), (1100, 1300)])
+def test_edge_large_matches_launch_chain(shape, monkeypatch):
+    """Edge runs beyond the per-pixel size range (1, 2 and 3 tasks per warp),
+    convergence checkpoints included."""
+    h, w = shape
+    rng = np.random.default_rng(h + w)
+    img = np.full((h, w), 0.35)
+    img[h // 4: 3 * h // 4, w // 3: 2 * w // 3] = 0.7
+    img = np.clip(img + 0.03 * rng.standard_normal((h, w)), 0, 1)
+    seeds = L.SeedSpec(polygons=(square(40, 40, w - 50, h - 60),), inside_sign=-1)
+    prm = params("edge", max_iters=60, conv_check_every=6, conv_window=40)
+    res = make_run(img, seeds, prm, [25, 35])
+    assert res.resident_stats()["enabled"], res.resident_stats()
+    monkeypatch.setenv("LSE_RESIDENT", "0")
+    same(res, make_run(img, seeds, prm, [60]))
