@@ -155,10 +155,11 @@ double host_t64(unsigned p, int R, const double* w) {
   return acc;
 }
 
-const double kEpsPhi = 0x1p-16;
+// near-tie guards (lse_device.cuh: kGuard x the a-priori fp32 error bounds)
+const double kEpsPhi = kGuard * kErrPhi;
 
 double edge_eps_u(double dt) {
-  return 4.0 * (0x1p-18 + dt * (0x1p-16 + 1.5 * 0x1p-22 + 0x1p-21) + 0x1p-22 * (1.0 + 1.5 * dt));
+  return kGuard * (kErrPhi + dt * (kErrGrad + 1.5 * 0x1p-22 + 0x1p-21) + 0x1p-22 * (1.0 + 1.5 * dt));
 }
 
 }  // namespace
@@ -902,6 +903,8 @@ bool fp32_ok(lse_run* r) {
   if (two_mean(r->p.model) && !(r->img_absmax <= 1e6)) return false;
   if (r->p.model == LSE_MODEL_ZHANG && !(std::fabs(r->p.nu) <= 1e6)) return false;
   if (r->mode == SRC_SCALED && !(r->scale >= 1e-3 && r->scale <= 1e6)) return false;
+  // +-s in fp32: exact, or its rounding (s 2^-24) far inside the phi bound
+  if (r->mode == SRC_SCALED && (double)(float)r->scale != r->scale && !(r->scale <= 4.0)) return false;
   return true;
 }
 

@@ -27,6 +27,18 @@ enum Model : int { EDGE = 0, REGION = 1, ZHANG = 2, VECTOR = 3, CHAN_VESE = 4 };
 constexpr int kMaxBands = 4;
 enum Src : int { SRC_SMOOTH = 0, SRC_SCALED = 1, SRC_FIELD = 2 };
 
+// A-priori error bounds of the fp32 evaluation.  phi32 is a
+// (2R+1 <= 9)-term FMA chain over table values: table rounding <= 2^-23 (the
+// zero-padded form 2 S - L; 2^-25 for the exact-rounded interior values),
+// weight rounding <= 2^-24, nine FMA roundings <= 2^-25 each (|partial sums|
+// <= 1): |phi32 - phi| <= 5.1e-7 < 0.54 * 2^-20.  h = 2|grad phi| from four such
+// values (one-sided differences double them): <= 5.66 * 5.1e-7 + roundings
+// (differences, squares, sqrt.approx at 2^-23 relative) < 2^-18 + 2^-21.  The
+// guards are kGuard times these bounds.
+constexpr double kErrPhi = 0x1p-20;
+constexpr double kErrGrad = 0x1p-18;
+constexpr double kGuard = 4.0;
+
 // Per-run scalars shared by the kernels of one run (device resident).
 struct __align__(16) Scalars {
   double sp_hi, sp_lo, sn_hi, sn_lo;  // running sums of I over {phi>=0} / {phi<0} (double-double)

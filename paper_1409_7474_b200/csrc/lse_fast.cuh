@@ -1502,14 +1502,14 @@ __device__ inline void region_coeffs(Scalars* sc) {
       double eps_d = 0x1p-21 * (fabs(a) * sc->img_absmax + fabs(b) + 1.0);
       // |v / |grad phi|| <= 1 for the region model, <= |nu| for zhang
       const double vs = sc->model == ZHANG ? fmax(1.0, fabs(sc->nu)) : 1.0;
-      sc->eps_u = (float)(4.0 * (0x1p-18 + dt * vs * (0x1p-16 + 1.5 * eps_d + 0x1p-21) +
-                                 0x1p-22 * (1.0 + 1.5 * dt * vs)));
+      sc->eps_u = (float)(kGuard * (kErrPhi + dt * vs * (kErrGrad + 1.5 * eps_d + 0x1p-21) +
+                                    0x1p-22 * (1.0 + 1.5 * dt * vs)));
     }
   }
   if (sc->zero_vel) {
     sc->A = 0.f;
     sc->B = 0.f;
-    sc->eps_u = (float)(4.0 * (0x1p-18 + 0x1p-22));
+    sc->eps_u = (float)(kGuard * (kErrPhi + 0x1p-22));
   }
 }
 

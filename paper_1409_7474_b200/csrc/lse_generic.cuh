@@ -958,7 +958,7 @@ __global__ void __launch_bounds__(256) k_band_peak(const ExactCtx* __restrict__ 
     sc->zero_vel = 1;
     sc->A = 0.f;
     sc->B = 0.f;
-    sc->eps_u = (float)(4.0 * (0x1p-18 + 0x1p-22));
+    sc->eps_u = (float)(kGuard * (kErrPhi + 0x1p-22));
     sc->band_valid = 1;
     return;
   }
@@ -967,8 +967,8 @@ __global__ void __launch_bounds__(256) k_band_peak(const ExactCtx* __restrict__ 
   sc->B = 0.f;
   // |a| * max|D| = 1; the fp32 plane adds one rounding of D
   const double eps_d = 0x1p-21 * (2.0 + 1.0 + 1.0);
-  sc->eps_u = (float)(4.0 * (0x1p-18 + dt * (0x1p-16 + 1.5 * eps_d + 0x1p-21) +
-                             0x1p-22 * (1.0 + 1.5 * dt)));
+  sc->eps_u = (float)(kGuard * (kErrPhi + dt * (kErrGrad + 1.5 * eps_d + 0x1p-21) +
+                                0x1p-22 * (1.0 + 1.5 * dt)));
   sc->band_valid = 1;
 }
 

@@ -3,7 +3,7 @@ the BASELINE workloads every fp32 decision value of the fused kernels stays
 within its a-priori guard (|u32 - u64| < eps_u, |phi32 - phi64| < eps_phi),
 so no fp32 decision outside the guard band can differ from the reference's
 fp64 decision.  Small sizes here; the full-size runs are committed under
-profiles/ (r02_certify_*.json)."""
+profiles/ (r02r_certify_*.json: all five BASELINE configs at full size)."""
 import json
 import os
 import subprocess
