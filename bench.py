@@ -140,7 +140,7 @@ def small_config(name, ws):
          "C3": "C3: 4096^2 x 4 bands (fp32), vector region term, +-1 checkerboard of 64^2 "
                "cells, sigma 1 (9x9), dt 15, 1000 fixed iterations per step"}[name]
     return {"workload": d, "parallelism": f"replicas x{ws}" if ws > 1 else "single GPU",
-            "l2": "C1/C2 L2-resident (launch-latency bound); C3 inputs 268 MB > L2"
+            "l2": "C1/C2 L2-resident (one resident kernel per job: barrier / dependency-latency bound); C3 inputs 268 MB > L2"
             if name != "C3" else "inputs (268 MB of bands) larger than L2"}
 
 
@@ -354,7 +354,7 @@ class Dist:
 
 # ------------------------------------------------- the other BASELINE configs
 def small_job(name, steps):
-    """C1 / C2 (single small images: L2-resident, launch-latency bound) and C3
+    """C1 / C2 (single small images: L2-resident, one resident kernel per job) and C3
     (4096^2 x 4 bands): device time of the fixed-iteration evolution through
     the C ABI, inputs resident, dense pass.  Returns (Gpix-it/s, ms/job,
     px-its per job, launches per job)."""
@@ -493,7 +493,7 @@ def other_configs(steps, c4_tiles, cpu_seconds, with_cpu):
         out[name] = {"value": v, "unit": "Gpix-it/s", "ms_per_job": ms,
                      "launches_per_job": launches,
                      "workload": small_config(name, 1)["workload"],
-                     "bound": "launch latency / L2 (not HBM)"}
+                     "bound": "barrier + dependency latency of the resident kernel (k_resident: one launch per job; not HBM)"}
     if with_cpu:
         for name, thr in (("C1", 1), ("C2", 1), ("C3", 0), ("C4", 0)):
             if name in out:
