@@ -941,10 +941,9 @@ int resident_launch_k(lse_run* r, const FastParams& P, const ResidentArgs& A) {
 
 template <int R, int MODEL>
 int resident_launch_rm(lse_run* r, const FastParams& P, const ResidentArgs& A) {
-  if (MODEL == EDGE && r->res_nt > 1) {          // (several tasks per warp: grid launches only)
-    constexpr int M2 = EDGE;
-    if (r->res_nt == 2) return resident_launch_k<R, M2, true, 2>(r, P, A);
-    return resident_launch_k<R, M2, true, 3>(r, P, A);
+  if (r->res_nt > 1) {                           // (several tasks per warp: grid launches only)
+    if (r->res_nt == 2) return resident_launch_k<R, MODEL, true, 2>(r, P, A);
+    return resident_launch_k<R, MODEL, true, 3>(r, P, A);
   }
   if (r->res_grid) return resident_launch_k<R, MODEL, true, 1>(r, P, A);
   return resident_launch_k<R, MODEL, false, 1>(r, P, A);
@@ -995,21 +994,29 @@ int resident_capacity(int ctas) {
   return nclusters > 0 ? ctas : 0;
 }
 
-constexpr int kResMaxTasksPerWarp = 3;           // edge runs (k_resident NT)
+constexpr int kResMaxTasksPerWarp = 3;           // k_resident NT
 
 void resident_setup(lse_run* r) {
   r->resident = false;
   int mode = 1;
-  if (const char* v = std::getenv("LSE_RESIDENT")) mode = std::atoi(v);
+  if (const char* v = std::getenv("LSE_RESIDENT")) {
+    mode = std::atoi(v);
+  } else {
+    // a knob that selects a variant of the per-iteration kernels (tests, A/B)
+    // asks for those kernels
+    for (const char* k : {"LSE_FINE_MAX_PX", "LSE_SPLIT_PARTS", "LSE_BORDER_Q", "LSE_FUSED",
+                          "LSE_FIX_CAP", "LSE_ONESTAGE_MAX_PARTS"})
+      if (std::getenv(k)) mode = 0;
+  }
 #ifdef LSE_CHECK_BOUND
   mode = 0;                                      // validation builds certify the per-iteration kernels
 #endif
-  const bool edge = r->p.model == LSE_MODEL_EDGE;
   if (mode == 0 || is_bands(r) || is_cv(r) || r->strip || r->R < 1 || r->R > 4) return;
-  // region / zhang: one task per warp (phi stays in registers across the
-  // coefficient barrier) -- the per-pixel kernels' size range; edge: up to
-  // kResMaxTasksPerWarp tasks per warp of a full cooperative grid
-  if (!edge && !r->fine) return;
+  // up to kResMaxTasksPerWarp tasks per warp of a full cooperative grid
+  // (~1.8 Mpx); larger images run the tiled kernels.  LSE_RESIDENT_MAX_PX
+  // lowers the limit (A/B against the tiled / per-pixel kernels).
+  if (const char* v = std::getenv("LSE_RESIDENT_MAX_PX"))
+    if (r->npx > std::atoll(v)) return;
   const int ncb = (r->W + kResCols - 1) / kResCols;
   const long long tasks = (long long)r->g.HR * ncb;
   long long ctas = (tasks + kResWarps - 1) / kResWarps;
@@ -1020,7 +1027,6 @@ void resident_setup(lse_run* r) {
     const int cap = resident_capacity<true>((int)ctas);
     if (cap <= 0) return;
     if (ctas > cap) {
-      if (!edge) return;
       nt = (int)((ctas + cap - 1) / cap);
       if (nt > kResMaxTasksPerWarp) return;
       ctas = (ctas + nt - 1) / nt;               // balanced: every warp has nt or nt-1 tasks

@@ -136,14 +136,15 @@ __device__ __forceinline__ void res_checkpoint(Scalars* sc, unsigned long long m
 #define RES_T(k) do { } while (0)
 #endif
 
-// NT: tasks per warp.  Region / zhang runs need the coefficients between the
-// partition and the update of an iteration, so a warp keeps phi and |grad phi|
-// of its task across the barrier: NT = 1.  Edge runs have constant
-// coefficients: a warp finishes one task (phi -> checkpoint words -> update)
-// before the next, so NT > 1 costs only the data registers (larger images).
+// NT: tasks per warp (larger images on a full cooperative grid).  Edge runs
+// have constant coefficients: a warp finishes one task (phi -> checkpoint
+// words -> update) before the next.  Region / zhang runs need the coefficients
+// between the partition and the update of an iteration, so a warp keeps phi
+// and |grad phi| of all its tasks across the barrier (NT > 1: some of them in
+// local memory -- one store and one load per pixel and iteration, far cheaper
+// than rebuilding phi).
 template <int R, int MODEL, bool GRID, int NT>
 __global__ void __launch_bounds__(kResThreads, 1) k_resident(FastParams P, ResidentArgs A) {
-  static_assert(MODEL == EDGE || NT == 1, "region runs keep one task per warp");
   constexpr int CW = kResCols;
   constexpr int NPAT = 1 << (2 * R + 1);
   constexpr int NC = CW + 2 * R + 2;             // window columns x0-R-1 .. x0+CW+R
@@ -222,11 +223,13 @@ __global__ void __launch_bounds__(kResThreads, 1) k_resident(FastParams P, Resid
     if (!first) to_ckpt = to_ckpt == 0 ? A.cce - 1 : to_ckpt - 1;
     double a_in = 0.0, a_out = 0.0;
     int n_in = 0, n_out = 0, mism = 0;           // (a warp's pixels: 32-bit counts)
-    float p0[CW], hh[CW];                        // phi^n and 2 |grad phi^n| at the lane's pixels
+    float p0a[NT][CW], hha[NT][CW];              // phi^n and 2 |grad phi^n| at the lane's pixels
 
     // b^{n+1} of task (r, x0) from p0 / hh and the coefficients; near ties in fp64
     auto update_task = [&](int t, int r, int x0, float Av, float Bv, float eps_u) {
       const int i = r * 32 + lane;
+      const float (&p0)[CW] = p0a[t];
+      const float (&hh)[CW] = hha[t];
       float u[CW];
 #pragma unroll
       for (int c = 0; c < CW; ++c) {
@@ -271,6 +274,8 @@ __global__ void __launch_bounds__(kResThreads, 1) k_resident(FastParams P, Resid
       const int r = tk_r[t], x0 = tk_x0[t];
       const int i = r * 32 + lane;
       const bool rowok = tk_on[t] && i < H;
+      float (&p0)[CW] = p0a[t];
+      float (&hh)[CW] = hha[t];
       if (tk_on[t]) {
         for (int q = lane; q < 3 * NC; q += 32) {
           const int row = q / NC, col = q - row * NC;
@@ -552,7 +557,9 @@ __global__ void __launch_bounds__(kResThreads, 1) k_resident(FastParams P, Resid
       const float Av = s_sc.A, Bv = s_sc.B, eps_u = s_sc.eps_u;
       if (tid == 0 && s_sc.zero_vel && s_sc.model != EDGE)
         s_sc.degenerate = 1;                     // sticky degenerate (engine.py:239-240)
-      if (tk_on[0]) update_task(0, tk_r[0], tk_x0[0], Av, Bv, eps_u);
+#pragma unroll
+      for (int t = 0; t < NT; ++t)
+        if (tk_on[t]) update_task(t, tk_r[t], tk_x0[t], Av, Bv, eps_u);
     }
     RES_T(4);
     res_sync<GRID>(A.sync, epoch);

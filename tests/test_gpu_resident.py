@@ -177,17 +177,34 @@ def test_c2_golden_several_tasks_per_warp():
 
 
 @pytest.mark.parametrize("shape", [(700, 900), (1100, 1300)])
-def test_edge_large_matches_launch_chain(shape, monkeypatch):
-    """Edge runs beyond the per-pixel size range (1, 2 and 3 tasks per warp),
-    convergence checkpoints included."""
+@pytest.mark.parametrize("model", ["edge", "region", "zhang"])
+def test_large_matches_launch_chain(shape, model, monkeypatch):
+    """Runs beyond the per-pixel size range (2 and 3 tasks per warp on a full
+    cooperative grid; region runs keep phi of every task across the
+    coefficient barrier), convergence checkpoints included -- against the
+    tiled kernels (the speculative fused pass for region / zhang)."""
     h, w = shape
     rng = np.random.default_rng(h + w)
     img = np.full((h, w), 0.35)
     img[h // 4: 3 * h // 4, w // 3: 2 * w // 3] = 0.7
     img = np.clip(img + 0.03 * rng.standard_normal((h, w)), 0, 1)
     seeds = L.SeedSpec(polygons=(square(40, 40, w - 50, h - 60),), inside_sign=-1)
-    prm = params("edge", max_iters=60, conv_check_every=6, conv_window=40)
+    prm = params(model, max_iters=60, conv_check_every=6, conv_window=40)
     res = make_run(img, seeds, prm, [25, 35])
-    assert res.resident_stats()["enabled"], res.resident_stats()
+    st = res.resident_stats()
+    assert st["enabled"] and st["grid"] and st["tasks_per_warp"] >= 2, st
     monkeypatch.setenv("LSE_RESIDENT", "0")
     same(res, make_run(img, seeds, prm, [60]))
+
+
+def test_size_limit(monkeypatch):
+    """Beyond three tasks per warp of the grid (and above LSE_RESIDENT_MAX_PX)
+    the tiled kernels run."""
+    img = np.full((1700, 1500), 0.4)
+    img[300:900, 200:1000] = 0.8
+    seeds = L.SeedSpec(polygons=(square(50, 50, 1400, 1600),), inside_sign=-1)
+    r = L.EvolutionRun(img, seeds, params("region", max_iters=3))
+    assert not r.resident_stats()["enabled"]
+    monkeypatch.setenv("LSE_RESIDENT_MAX_PX", "10000")
+    small, sd = scene()
+    assert not L.EvolutionRun(small, sd, params("region", max_iters=3)).resident_stats()["enabled"]
