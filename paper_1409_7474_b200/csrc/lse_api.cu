@@ -784,6 +784,9 @@ int launch_fused_R(lse_run* r, long long it, bool ckpt_prev, TilePartial* strip_
     cudaEventRecord(e0, r->st);
   }
   constexpr size_t smem = fused_smem_bytes<R>();
+#ifdef LSE_UNIT_TRACE
+  P.trace = trace_begin(r, n, g, "fused", r->nb_upd[0]);
+#endif
   if (ckpt_prev) {
     TRY(prepare_smem(k_update_fused<R, true, false>, smem));
     TRY(launch_pdl_smem(k_update_fused<R, true, false>, g, kThreads, smem, r->st, P));
@@ -791,6 +794,9 @@ int launch_fused_R(lse_run* r, long long it, bool ckpt_prev, TilePartial* strip_
     TRY(prepare_smem(k_update_fused<R, false, false>, smem));
     TRY(launch_pdl_smem(k_update_fused<R, false, false>, g, kThreads, smem, r->st, P));
   }
+#ifdef LSE_UNIT_TRACE
+  trace_after(r, P.trace);
+#endif
   if (r->prof) cudaEventRecord(e1, r->st);
   PartRanges R3{{r->d_part, r->d_part, r->d_part}, {(int)n, 0, 0}};
   const int spec = 1 + P.fix_par;

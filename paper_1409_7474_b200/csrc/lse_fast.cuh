@@ -1176,6 +1176,12 @@ __device__ __forceinline__ void update_rows_border(const FastParams& P, const fl
   }
   float pm[NP], p0[NP], pn[NP], dcur[CPL], dnext[CPL];
   uint32_t fbrows = 0u;
+  // flagged pixels of the first 8 rows of the range (bit 8 (k - k0) + c): border
+  // ranges are at most 8 rows, so only those pixels take the fp64 evaluation
+  // (a whole flagged row cost 8 general-path evaluations of ~10 us each and
+  // made single border units the critical path of mid-size images)
+  static_assert(CPL <= 8, "column mask");
+  unsigned long long fbm = 0ull;
 #pragma unroll
   for (int c = 0; c < CPL; ++c) { ow[c] = 0u; dcur[c] = 0.f; dnext[c] = 0.f; }
   phi_row<R, SRC, false, NT, NP>(P, win, cm, 0, y0 + k0 - 1, s_lt, s_ls, pm);
@@ -1206,7 +1212,10 @@ __device__ __forceinline__ void update_rows_border(const FastParams& P, const fl
         if ((FUSED ? fmaf(-delta, h, fabsf(u)) : fabsf(u)) <= eps_u) fb |= 1u << c;
         if (!FUSED) LSE_CHECK_U(R, SRC, P, P.ctx, P.bits_in, y0 + k, x, u, eps_u);
       }
-      if (fb) fbrows |= bitk;
+      if (fb) {
+        fbrows |= bitk;
+        if (k - k0 < 8) fbm |= (unsigned long long)fb << (8 * (k - k0));
+      }
     }
 #pragma unroll
     for (int c = 0; c < NP; ++c) { pm[c] = p0[c]; p0[c] = pn[c]; }
@@ -1217,12 +1226,13 @@ __device__ __forceinline__ void update_rows_border(const FastParams& P, const fl
     const int k = __ffs(fbrows) - 1;
     fbrows &= fbrows - 1;
     const uint32_t bitk = 1u << k;
+    const uint32_t cols = (k - k0 < 8) ? (uint32_t)(fbm >> (8 * (k - k0))) & 0xffu : 0xffu;
 #pragma unroll 1
     for (int c = 0; c < CPL; ++c) {
       if (x0 + c >= W) break;
-      // fused pass: the whole flagged row goes to the fix list (a superset)
-      // and is also decided exactly with the coefficients used (final if
-      // they turn out unchanged)
+      if (!((cols >> c) & 1u)) continue;
+      // fused pass: a flagged pixel goes to the fix list and is also decided
+      // exactly with the coefficients used (final if they turn out unchanged)
       if (FUSED) {
         if (P.ctx->model != EDGE) spec_append(P, y0 + k, x0 + c);
         if (!LSE_SPEC_INLINE) continue;
@@ -1961,6 +1971,7 @@ __device__ __forceinline__ void partition_rows_border(const FastParams& P, const
   }
   float ph[8];
   uint32_t fbrows = 0u;
+  unsigned long long fbm = 0ull;                 // near-tie pixels (see update_rows_border)
 #pragma unroll
   for (int c = 0; c < 8; ++c) { pw[c] = 0u; mw[c] = 0u; }
 #pragma unroll 1
@@ -1969,15 +1980,18 @@ __device__ __forceinline__ void partition_rows_border(const FastParams& P, const
     if (i >= H) break;
     phi_row<R, SRC_SMOOTH, false, NT, 8>(P, win, cm, k - k0, i, s_lt, s_ls, ph);
     const uint32_t bitk = 1u << k;
-    bool tie = false;
+    uint32_t tie = 0u;
 #pragma unroll
     for (int c = 0; c < 8; ++c) {
       if (x0 + c >= W) continue;
       if (ph[c] > 0.f) pw[c] |= bitk;
-      tie |= fabsf(ph[c]) <= eps_phi;
+      if (fabsf(ph[c]) <= eps_phi) tie |= 1u << c;
       LSE_CHECK_PHI(R, P, P.ctx, P.bits_in, i, x0 + c, ph[c], eps_phi);
     }
-    if (tie) fbrows |= bitk;
+    if (tie) {
+      fbrows |= bitk;
+      if (k - k0 < 8) fbm |= (unsigned long long)tie << (8 * (k - k0));
+    }
   }
 #pragma unroll
   for (int c = 0; c < 8; ++c) mw[c] = pw[c];     // phi > 0 unless phi == 0 (tie path)
@@ -1985,9 +1999,11 @@ __device__ __forceinline__ void partition_rows_border(const FastParams& P, const
     const int k = __ffs(fbrows) - 1;
     fbrows &= fbrows - 1;
     const uint32_t bitk = 1u << k;
+    const uint32_t cols = (k - k0 < 8) ? (uint32_t)(fbm >> (8 * (k - k0))) & 0xffu : 0xffu;
 #pragma unroll 1
     for (int c = 0; c < 8; ++c) {
       if (x0 + c >= W) break;
+      if (!((cols >> c) & 1u)) continue;
       const double e = exact_phi_fast<R>(P.ctx, P.bits_in, y0 + k, x0 + c);
 #pragma unroll
       for (int q = 0; q < 8; ++q) {
@@ -2234,6 +2250,7 @@ __global__ void __launch_bounds__(kThreads, kFusedCtasPerSm) k_update_fused(Fast
   // the window of rows 16..31 of its unit, built at the unit start (word j of
   // lane l at [j][l]) so the mid-unit switch reads shared memory
   extern __shared__ __align__(16) float s_dyn[];
+  LSE_TRACE_ENTRY
   float* s_ring = s_dyn;
   auto s_win = reinterpret_cast<uint32_t (*)[NT][32]>(s_dyn + (kThreads / 32) * kRing2 * 32 * CPL);
   // per warp: the old P / M words of the unit's block, staged at the unit start
@@ -2272,7 +2289,9 @@ __global__ void __launch_bounds__(kThreads, kFusedCtasPerSm) k_update_fused(Fast
   // atomic's round trip overlaps the unit; same grab count: one failing grab
   // per warp).
   int unit = grab_unit(P, lane);
+  LSE_TRACE_DECL
   for (;;) {
+    LSE_TRACE_MARK(unit < nunits ? unit : -1);
     if (unit >= nunits) break;
     unsigned long long g_next = 0;
     if (lane == 0) g_next = atomicAdd(P.work, 1ull) - P.work_base;
