@@ -24,14 +24,15 @@
 //   * phi is rebuilt once per iteration (the two-pass path rebuilds it in the
 //     update and again in the partition);
 //   * the barrier is a cluster barrier when the tasks fit one cluster of <= 16
-//     CTAs (hardware barrier, ~0.3 us), else a grid barrier of a cooperative
-//     launch (one CTA per SM);
+//     CTAs (hardware barrier, ~0.3 us; the CTAs' partials go straight into
+//     every CTA's shared memory), else a grid barrier of a cooperative launch
+//     (one CTA per SM, up to three tasks per warp: images up to ~1.8 Mpx);
 //   * edge runs need one barrier per iteration (two on checkpoints).
 //
 // The arithmetic of every decision is the per-pixel kernels' (same LUT values,
 // FMA order, gradient, guards, exact evaluators), so the decisions are the
 // reference's; only the grouping of the c+/c- sums differs (per lane over its
-// columns, lanes by xor tree, warps in order, CTAs by a double-double tree).
+// columns, lanes and warps by xor trees, CTAs by a double-double tree).
 // engine.py:148-174 (one iteration), :222-240 (checkpoints), grid.py:102-118.
 #pragma once
 
