@@ -371,6 +371,12 @@ int run_flag(lse_run* r, int** out) {
   return LSE_OK;
 }
 
+// LSE_BORDER_Q: row parts per border lane group (a power of two, 1 .. 16)
+int parse_border_q(const char* v) {
+  const int q = std::atoi(v);
+  return q >= 16 ? 16 : q >= 8 ? 8 : q >= 4 ? 4 : q >= 2 ? 2 : 1;
+}
+
 // partials of the per-pixel partition: one per CTA of kFineCols columns up to
 // kFineCtaParts CTAs, else one per state word
 constexpr long long kFineCtaParts = 768;
@@ -1652,7 +1658,7 @@ int create_impl(lse_run** out, const lse_params* p, long long height, long long 
     // partials, so a batched tile and the same tile alone group them alike)
     int bqp = kBorderQ;
     if (const char* bv = std::getenv("LSE_BORDER_Q"))
-      bq = bqp = std::atoi(bv) >= 16 ? 16 : std::atoi(bv) >= 8 ? 8 : 4;
+      bq = bqp = parse_border_q(bv);
     r->gu = make_geo(H, W, R, 1 + R, 1 + R, R + 1, bq);   // update reaches R+1 rows/columns
     r->gp = make_geo(H, W, R, R, R, R, bqp);              // partition reaches R
     if (si && (!geo_restrict_rows(r->gu, si->own_lo, si->own_hi) ||
@@ -2488,8 +2494,7 @@ int lse_batch_create(lse_batch** out, lse_run* const* runs, int n) {
   b->tile_data = (long long)r0->g.HR * 32 * r0->g.data_pitch;
   b->gu = make_geo(r0->H, r0->W, r0->R, 1 + r0->R, 1 + r0->R, r0->R + 1, kBorderQ);
   if (const char* bv = std::getenv("LSE_BORDER_Q"))
-    b->gu = make_geo(r0->H, r0->W, r0->R, 1 + r0->R, 1 + r0->R, r0->R + 1,
-                     std::atoi(bv) >= 16 ? 16 : std::atoi(bv) >= 8 ? 8 : 4);
+    b->gu = make_geo(r0->H, r0->W, r0->R, 1 + r0->R, 1 + r0->R, r0->R + 1, parse_border_q(bv));
   b->nb_upd = border_units(b->gu);
   b->ni_upd = r0->ni_upd;
   b->nb_part = r0->nb_part;
