@@ -30,15 +30,22 @@ $(CHECK_LIB): $(SRC) $(HDR)
 
 # resident-kernel phase timing (prints per-phase SM cycles per advance call)
 RESTRACE_LIB := paper_1409_7474_b200/_lib/liblse_b200_restrace.so
-restrace: $(RESTRACE_LIB)
+restrace: $(RESTRACE_LIB) $(TMA_LIB)
 $(RESTRACE_LIB): $(SRC) $(HDR)
 	@mkdir -p $(dir $@)
 	$(NVCC) $(FLAGS) -DLSE_RES_TRACE -shared -o $@ $(SRC) 2> /dev/null
+
+# A/B build: TMA (bulk copy + mbarrier) data ring in the fused pass
+TMA_LIB := paper_1409_7474_b200/_lib/liblse_b200_tma.so
+tma: $(TMA_LIB)
+$(TMA_LIB): $(SRC) $(HDR)
+	@mkdir -p $(dir $@)
+	$(NVCC) $(FLAGS) -DLSE_TMA_RING=1 -shared -o $@ $(SRC) 2> paper_1409_7474_b200/_lib/ptxas_tma.log
 
 oracle:
 	$(MAKE) -C oracle
 
 clean:
-	rm -f $(LIB) $(TRACE_LIB) $(CHECK_LIB) $(RESTRACE_LIB)
+	rm -f $(LIB) $(TRACE_LIB) $(CHECK_LIB) $(RESTRACE_LIB) $(TMA_LIB)
 
-.PHONY: all clean oracle trace check restrace
+.PHONY: all clean oracle trace check restrace tma

@@ -600,6 +600,33 @@ __device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commi
 template <int N>
 __device__ __forceinline__ void cp_async_wait() { asm volatile("cp.async.wait_group %0;" ::"n"(N)); }
 
+// ---- TMA (bulk async copy + mbarrier) variant of the data ring, A/B builds
+// only (-DLSE_TMA_RING=1, `make tma`): one elected lane copies a whole 1 KB
+// row of a chunk unit per instruction and the warp waits on an mbarrier,
+// instead of two 16-byte cp.async per lane and row.  Measured slower (C5 673
+// vs 772 Gpix-it/s, same box: a convergence point, the elected-lane branch
+// and an mbarrier wait per 2-row step cost more than the 4 LDGSTS they
+// replace in this issue-bound loop), so the default build keeps the per-lane
+// ring, which also serves the lane-scattered B1 units.
+#ifndef LSE_TMA_RING
+#define LSE_TMA_RING 0
+#endif
+__device__ __forceinline__ void mbar_init(uint32_t bar, uint32_t count) {
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(bar), "r"(count) : "memory");
+}
+__device__ __forceinline__ void mbar_expect_tx(uint32_t bar, uint32_t bytes) {
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(bar), "r"(bytes) : "memory");
+}
+__device__ __forceinline__ void bulk_g2s(uint32_t dst, const void* src, uint32_t bytes, uint32_t bar) {
+  asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];"
+               ::"r"(dst), "l"(src), "r"(bytes), "r"(bar) : "memory");
+}
+__device__ __forceinline__ void mbar_wait(uint32_t bar, uint32_t parity) {
+  asm volatile("{\n\t.reg .pred p;\n\tWAIT_%=:\n\t"
+               "mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n\t"
+               "@!p bra WAIT_%=;\n\t}" ::"r"(bar), "r"(parity) : "memory");
+}
+
 template <int R, int NT, int NOUT, int SRC = SRC_SMOOTH>
 __device__ __forceinline__ void phi_row_int(const FastParams& P, const uint32_t (&win4)[NT],
                                             int m0, uint32_t lut_base, float (&out)[NOUT]) {
@@ -786,7 +813,7 @@ __device__ __forceinline__ void update_block_int2(const FastParams& P, uint32_t 
                                                   int tile, float delta, uint32_t (&pw)[CPL],
                                                   uint32_t (&mw)[CPL], const FastParams& Pn,
                                                   const uint32_t* wslot = nullptr,
-                                                  float eps_t = 0.f) {
+                                                  float eps_t = 0.f, uint32_t tma_bars = 0u) {
   // Pn: the launch parameters as seen by the noinline tie helpers (the CTA's
   // shared copy: passing the kernel parameter block by reference to a noinline
   // function makes every thread copy it to local memory first)
@@ -801,6 +828,24 @@ __device__ __forceinline__ void update_block_int2(const FastParams& P, uint32_t 
   const uint32_t ring_s = (uint32_t)__cvta_generic_to_shared(ring) + lane * CPL * 4;
   const size_t dpitch = P.g.data_pitch;
   const float* gsrc = P.data32 + (size_t)y0 * dpitch + x0;
+  // (A/B builds) chunk units: whole rows by bulk copies of one lane, signalled
+  // on the warp's four mbarriers (one per slot pair; 16 steps = 4 phases each,
+  // so every unit starts at parity 0)
+  const bool tma = LSE_TMA_RING && FUSED && tma_bars != 0u;
+  const uint32_t ring_w = ring_s - lane * CPL * 4;             // the warp's ring, lane 0's view
+  const float* grow = gsrc - lane * CPL;                        // the chunk's first column
+  if (tma) {
+    if (lane == 0) {
+#pragma unroll
+      for (int q = 0; q < kRing2 - 2; q += 2) {
+        const uint32_t bar = tma_bars + 8 * (q >> 1);
+        mbar_expect_tx(bar, 2 * kSlot);
+        bulk_g2s(ring_w + q * kSlot, grow + (size_t)q * dpitch, kSlot, bar);
+        bulk_g2s(ring_w + (q + 1) * kSlot, grow + (size_t)(q + 1) * dpitch, kSlot, bar);
+      }
+    }
+    gsrc += (kRing2 - 2) * dpitch;
+  } else {
 #pragma unroll
   for (int q = 0; q < kRing2 - 2; q += 2) {    // rows 0 .. 5 in flight, 2 per group
 #pragma unroll
@@ -810,6 +855,7 @@ __device__ __forceinline__ void update_block_int2(const FastParams& P, uint32_t 
     }
     cp_async_commit();
     gsrc += 2 * dpitch;
+  }
   }
   float2 pp[NP], pn[NP];
   uint32_t ow[CPL];
@@ -824,7 +870,19 @@ __device__ __forceinline__ void update_block_int2(const FastParams& P, uint32_t 
   const uint32_t* wrow = P.bits_in + (size_t)r * P.g.pitch_w + (x0 - (R + 1));
 #pragma unroll kStepUnroll
   for (int s = 0; s < 16; ++s) {
-    {
+    if (tma) {
+      if (2 * s + kRing2 - 2 < 32) {
+        __syncwarp();                             // every lane has read the slots being refilled
+        if (lane == 0) {
+          const int q = (2 * s + kRing2 - 2) & (kRing2 - 1);
+          const uint32_t bar = tma_bars + 8 * (q >> 1);
+          asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+          mbar_expect_tx(bar, 2 * kSlot);
+          bulk_g2s(ring_w + q * kSlot, grow + (size_t)(2 * s + kRing2 - 2) * dpitch, kSlot, bar);
+          bulk_g2s(ring_w + (q + 1) * kSlot, grow + (size_t)(2 * s + kRing2 - 1) * dpitch, kSlot, bar);
+        }
+      }
+    } else {
       if (2 * s + kRing2 - 2 < 32) {
         const uint32_t d0 = ring_s + ((2 * s + kRing2 - 2) & (kRing2 - 1)) * kSlot;
 #pragma unroll
@@ -851,7 +909,8 @@ __device__ __forceinline__ void update_block_int2(const FastParams& P, uint32_t 
     }
     const int kn = 2 * s + 1;                   // first phi row of this step's pair
     phi_rows2_int<R, NT, NP, SRC>(P, win4, s < 8 ? kn + 1 : kn - 16, lut_base, pn);
-    cp_async_wait<kRing2 / 2 - 1>();            // rows 2s, 2s+1 have landed
+    if (tma) mbar_wait(tma_bars + 8 * (s & 3), (s >> 2) & 1);
+    else cp_async_wait<kRing2 / 2 - 1>();        // rows 2s, 2s+1 have landed
     float d0[CPL], d1[CPL];
     {
       const uint32_t src0 = ring_s + ((2 * s) & (kRing2 - 1)) * kSlot;
@@ -2231,7 +2290,8 @@ __device__ __noinline__ void border_fused_unit(const FastParams& P, const float*
 template <int R>
 constexpr int fused_smem_bytes() {
   // per warp: data ring, window of rows 16..31, old P and M words (2 x 1 KB)
-  return (kThreads / 32) * ((kRing2 * 32 * kUpdCols + (kUpdCols + 2 * (R + 1)) * 32) * 4 + 2048);
+  return (kThreads / 32) * ((kRing2 * 32 * kUpdCols + (kUpdCols + 2 * (R + 1)) * 32) * 4 + 2048) +
+         (LSE_TMA_RING ? (kThreads / 32) * 32 : 0);             // (A/B builds: 4 mbarriers per warp)
 }
 
 // BATCH: every unit of every tile ([all tiles' border][all tiles' interior],
@@ -2259,6 +2319,16 @@ __global__ void __launch_bounds__(kThreads, kFusedCtasPerSm) k_update_fused(Fast
                          (threadIdx.x >> 5) * 2048 + (threadIdx.x & 31) * 32;
   __shared__ FastParams s_P;                     // see k_update
   const SharedLuts luts{nullptr, s_ls, (uint32_t)__cvta_generic_to_shared(g_pair_lut)};
+  // (A/B builds) the warp's mbarriers, after everything else in dynamic shared memory
+  const uint32_t s_bars = LSE_TMA_RING
+      ? (uint32_t)__cvta_generic_to_shared(s_dyn) +
+            (kThreads / 32) * ((kRing2 * 32 * CPL + NT * 32) * 4 + 2048) + (threadIdx.x >> 5) * 32
+      : 0u;
+  if (LSE_TMA_RING && (threadIdx.x & 31) == 0) {
+#pragma unroll
+    for (int q = 0; q < 4; ++q) mbar_init(s_bars + 8 * q, 1u);
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  }
   {
     for (int q = threadIdx.x; q < NPAT; q += blockDim.x) s_ls[q] = __ldg(&P.lut_s[q]);
     for (int q = threadIdx.x; q < 2 * NPAT; q += blockDim.x)
@@ -2385,7 +2455,8 @@ __global__ void __launch_bounds__(kThreads, kFusedCtasPerSm) k_update_fused(Fast
         // (its final cp.async wait covers the old words too)
         update_block_int2<R, REGION, CPL, SRC_SMOOTH, true>(P, luts.lt2, ring, r, x0, A, B, e0,
                                                             prev, cur, tile, delta, pw, mw, s_P,
-                                                            &win_b[0][0], eps_t);
+                                                            &win_b[0][0], eps_t,
+                                                            iu < nch ? s_bars : 0u);
         if (!BATCH || part_t) partition_commit<true, CKPT, false>(P, r, x0, pw, mw, d, tile, s_old);
         else partition_commit<false, CKPT, false>(P, r, x0, pw, mw, d, tile, s_old);
       }
