@@ -20,6 +20,7 @@
 #include <cstring>
 #include <mutex>
 #include <string>
+#include <thread>
 #include <vector>
 
 #include "lse_b200.h"
@@ -1356,6 +1357,100 @@ void fill_status(lse_run* r, lse_status* s, long long instab) {
   s->generic_iterations = r->generic_iters;
 }
 
+// Large pageable float32 images: staged through two cached pinned buffers, the
+// host-side copies spread over a few threads (a plain cudaMemcpy from pageable
+// memory is staged by the driver on one thread at ~10 GB/s: 0.36 s for a
+// 32768^2 image; this path reaches the PCIe rate).  Pinned sources and small
+// images take the direct copy.
+constexpr size_t kStageBytes = 64u << 20;
+constexpr int kStageThreads = 6;
+struct StageBufs {
+  void* buf[2] = {nullptr, nullptr};
+  cudaEvent_t ev[2] = {nullptr, nullptr};
+  std::mutex mu;
+};
+StageBufs g_stage;
+
+int h2d_rows_f32(lse_run* r, float* dst, size_t dpitch_b, const float* src, int H, int W) {
+  const size_t row_b = (size_t)W * sizeof(float);
+  cudaPointerAttributes at{};
+  const bool pageable = cudaPointerGetAttributes(&at, src) != cudaSuccess ||
+                        at.type == cudaMemoryTypeUnregistered;
+  cudaGetLastError();
+  if (!pageable || row_b * H < 4 * kStageBytes || row_b > kStageBytes) {
+    CK(cudaMemcpy2DAsync(dst, dpitch_b, src, row_b, row_b, H, cudaMemcpyHostToDevice, r->st));
+    return LSE_OK;
+  }
+  std::lock_guard<std::mutex> lock(g_stage.mu);
+  for (int k = 0; k < 2; ++k)
+    if (!g_stage.buf[k]) {
+      CK(cudaHostAlloc(&g_stage.buf[k], kStageBytes, cudaHostAllocDefault));
+      CK(cudaEventCreateWithFlags(&g_stage.ev[k], cudaEventDisableTiming));
+    }
+  const int rows_per = (int)(kStageBytes / row_b);
+  int k = 0;
+  for (int y = 0; y < H; y += rows_per, k ^= 1) {
+    const int n = std::min(rows_per, H - y);
+    CK(cudaEventSynchronize(g_stage.ev[k]));       // the copy that last used this buffer is done
+    char* b = static_cast<char*>(g_stage.buf[k]);
+    const char* s0 = reinterpret_cast<const char*>(src) + (size_t)y * row_b;
+    const size_t bytes = (size_t)n * row_b, per = (bytes / kStageThreads + 4095) & ~(size_t)4095;
+    std::thread th[kStageThreads];
+    int nt = 0;
+    for (size_t o = 0; o < bytes; o += per)
+      th[nt++] = std::thread([=] { std::memcpy(b + o, s0 + o, std::min(per, bytes - o)); });
+    for (int t = 0; t < nt; ++t) th[t].join();
+    CK(cudaMemcpy2DAsync(reinterpret_cast<char*>(dst) + (size_t)y * dpitch_b, dpitch_b, b, row_b,
+                         row_b, n, cudaMemcpyHostToDevice, r->st));
+    CK(cudaEventRecord(g_stage.ev[k], r->st));
+  }
+  return LSE_OK;
+}
+
+// Large results into pageable host memory (the 1 byte/pixel mask of a big
+// scene): the same two pinned buffers, the DMA of one chunk overlapping the
+// threaded host copy of the previous one.
+int d2h_bytes(lse_run* r, unsigned char* out, const unsigned char* d_src, size_t nbytes) {
+  cudaPointerAttributes at{};
+  const bool pageable = cudaPointerGetAttributes(&at, out) != cudaSuccess ||
+                        at.type == cudaMemoryTypeUnregistered;
+  cudaGetLastError();
+  if (!pageable || nbytes < 4 * kStageBytes) {
+    CK(cudaMemcpyAsync(out, d_src, nbytes, cudaMemcpyDeviceToHost, r->st));
+    return LSE_OK;
+  }
+  std::lock_guard<std::mutex> lock(g_stage.mu);
+  for (int k = 0; k < 2; ++k)
+    if (!g_stage.buf[k]) {
+      CK(cudaHostAlloc(&g_stage.buf[k], kStageBytes, cudaHostAllocDefault));
+      CK(cudaEventCreateWithFlags(&g_stage.ev[k], cudaEventDisableTiming));
+    }
+  auto drain = [&](int k, size_t o, size_t n) -> int {
+    CK(cudaEventSynchronize(g_stage.ev[k]));
+    const char* b = static_cast<const char*>(g_stage.buf[k]);
+    unsigned char* d0 = out + o;
+    const size_t per = (n / kStageThreads + 4095) & ~(size_t)4095;
+    std::thread th[kStageThreads];
+    int nt = 0;
+    for (size_t q = 0; q < n; q += per)
+      th[nt++] = std::thread([=] { std::memcpy(d0 + q, b + q, std::min(per, n - q)); });
+    for (int t = 0; t < nt; ++t) th[t].join();
+    return LSE_OK;
+  };
+  size_t prev_o = 0, prev_n = 0;
+  int k = 0;
+  for (size_t o = 0; o < nbytes; o += kStageBytes, k ^= 1) {
+    const size_t n = std::min(kStageBytes, nbytes - o);
+    CK(cudaMemcpyAsync(g_stage.buf[k], d_src + o, n, cudaMemcpyDeviceToHost, r->st));
+    CK(cudaEventRecord(g_stage.ev[k], r->st));
+    if (prev_n) TRY(drain(k ^ 1, prev_o, prev_n));
+    prev_o = o;
+    prev_n = n;
+  }
+  if (prev_n) TRY(drain(k ^ 1, prev_o, prev_n));
+  return LSE_OK;
+}
+
 int upload_image(lse_run* r, const void* image, int is_f32) {
   const int H = r->H, W = r->W;
   const long long pitch = r->g.data_pitch;
@@ -1364,8 +1459,7 @@ int upload_image(lse_run* r, const void* image, int is_f32) {
   TRY(run_flag(r, &d_flag));
   CK(cudaMemsetAsync(d_flag, 0, sizeof(int), r->st));
   if (is_f32 == LSE_IMAGE_F32) {
-    CK(cudaMemcpy2DAsync(r->d_data32, pitch * sizeof(float), image, W * sizeof(float),
-                         W * sizeof(float), H, cudaMemcpyHostToDevice, r->st));
+    TRY(h2d_rows_f32(r, r->d_data32, pitch * sizeof(float), static_cast<const float*>(image), H, W));
     r->fp32_exact = true;
   } else {
     TRY(dalloc(&tmp64, r->npx));
@@ -1440,6 +1534,10 @@ int upload_image(lse_run* r, const void* image, int is_f32) {
   CK(cudaStreamSynchronize(r->st));
   r->img_absmax = r->h_scal->img_absmax;
   if (tmp64) cudaFree(tmp64);
+  // (two-mean models: the statistics above are the image's; NaN / inf order
+  // above every finite key, so one of them makes max |I| non-finite)
+  if (two_mean(r->p.model) && !std::isfinite(r->img_absmax))
+    return fail(LSE_ERR_ARG, "grid contains non-finite values");
   r->h_ctx.data32 = r->d_data32;
   r->h_ctx.data64 = r->d_data64;
   r->prepared = false;
@@ -2140,7 +2238,7 @@ int lse_run_read_mask(lse_run* r, unsigned char* out, int inside_sign, int packe
     TRY(scratch(r, r->npx, &d_out));
     k_mask_u8<<<grid2(r->W, r->H), 128, 0, r->st>>>(r->d_mask, r->g, invert, d_out);
     CKL();
-    CK(cudaMemcpyAsync(out, d_out, r->npx, cudaMemcpyDeviceToHost, r->st));
+    TRY(d2h_bytes(r, out, d_out, (size_t)r->npx));
   }
   CK(cudaStreamSynchronize(r->st));
   return LSE_OK;

@@ -211,6 +211,8 @@ class _DeviceRun:
         if rc == N.LSE_ERR_DEGENERATE_SEED:
             from .grid import DegenerateSeedError
             raise DegenerateSeedError(N.lib.lse_last_error().decode())
+        if rc == N.LSE_ERR_ARG and b"non-finite" in N.lib.lse_last_error():
+            raise ValueError("grid contains non-finite values")
         N.check(rc)
         self.h = h
         self.shape = image.shape[:2]
@@ -291,7 +293,10 @@ class EvolutionRun:
     def __init__(self, image: np.ndarray, seeds: SeedSpec,
                  params: EvolutionParams, trace: bool = False):
         _require_device_model(params.model)
-        self.image = as_image(image)
+        # two-mean models: the device's image statistics pass rejects
+        # non-finite values (as_field's ValueError, grid.py:24-31)
+        self.image = as_image(image, check_finite=params.model not in (ModelKind.REGION,
+                                                                        ModelKind.ZHANG))
         self.seeds = seeds
         self.params = params
         self._reg_kernel = gaussian_kernel(params.sigma2, params.ts_reg)

@@ -232,3 +232,16 @@ def test_plain_c_caller_matches_python_api(tmp_path):
         h = ((h ^ int(q)) * 1099511628211) & 0xFFFFFFFFFFFFFFFF
     assert int(it) == res.iterations and bool(int(conv)) == res.converged
     assert int(hsh, 16) == h
+
+
+@pytest.mark.parametrize("dtype", [np.float32, np.float64])
+@pytest.mark.parametrize("bad", [np.nan, np.inf, -np.inf])
+def test_non_finite_image_rejected(dtype, bad):
+    """as_field's ValueError (grid.py:24-31); float32 region images are checked
+    by the device's image statistics pass instead of a host scan."""
+    img = np.full((70, 90), 0.4, dtype=dtype)
+    img[33, 57] = bad
+    seeds = L.SeedSpec(polygons=(square(5, 5, 60, 50),), inside_sign=-1)
+    for kind in (L.ModelKind.REGION, L.ModelKind.EDGE):
+        with pytest.raises(ValueError, match="non-finite"):
+            L.EvolutionRun(img, seeds, L.default_params(kind))
