@@ -323,6 +323,8 @@ struct lse_run {
   TilePartial* d_res_parts = nullptr;
   unsigned int* d_sync = nullptr;
   long long resident_calls = 0;
+  long long res_base_it = -1;    // first iteration base / buffer of the resident launches since collect
+  int res_base_cur = 0;
 };
 
 namespace {
@@ -904,7 +906,11 @@ int collect(lse_run* r) {
     r->iteration = s.converged_iter;
     for (auto& pr : r->launched)
       if (pr.first == s.converged_iter) r->cur = pr.second;
+    // resident launches alternate the two state buffers from their base
+    if (r->res_base_it >= 0)
+      r->cur = r->res_base_cur ^ (int)((s.converged_iter - r->res_base_it) & 1);
   }
+  r->res_base_it = -1;
   r->launched.clear();
   return LSE_OK;
 }
@@ -1090,7 +1096,10 @@ int launch_resident(lse_run* r, long long steps) {
     cudaEventRecord(e1, r->st);
     r->evrec.push_back({e0, e1, e1, true, false});
   }
-  for (long long k = 1; k <= steps; ++k) r->launched.emplace_back(A.it0 + k, A.cur0 ^ (int)(k & 1));
+  if (r->res_base_it < 0) {                      // (collect: the buffer of a converged iteration)
+    r->res_base_it = A.it0;
+    r->res_base_cur = A.cur0;
+  }
   r->cur = A.cur0 ^ (int)(steps & 1);
   r->mode = SRC_SMOOTH;
   r->field_valid = false;
@@ -2130,8 +2139,14 @@ int lse_run_advance(lse_run* r, long long n_steps, lse_status* st) {
     CK(cudaMemsetAsync(reinterpret_cast<char*>(r->d_scal) + offsetof(Scalars, fix_n), 0,
                        sizeof(unsigned int) * 2, r->st));
   if (resident_now(r)) {
-    // small image: the whole call is one resident kernel (lse_resident.cuh)
-    TRY(launch_resident(r, steps));
+    // small image: the whole call is one resident kernel (lse_resident.cuh);
+    // very long calls in launches of 2^20 iterations (the grid barrier counts
+    // arrivals in 32 bits; a launch after convergence returns at once)
+    for (long long done = 0; done < steps;) {
+      const long long n = std::min<long long>(steps - done, 1LL << 20);
+      TRY(launch_resident(r, n));
+      done += n;
+    }
     TRY(collect(r));
     fill_status(r, st, -1);
     return LSE_OK;
