@@ -2214,7 +2214,8 @@ int lse_run_read_phi(lse_run* r, double* out) {
     CKL();
     src = r->d_U;
   }
-  CK(cudaMemcpyAsync(out, src, r->npx * sizeof(double), cudaMemcpyDeviceToHost, r->st));
+  TRY(d2h_bytes(r, reinterpret_cast<unsigned char*>(out), reinterpret_cast<const unsigned char*>(src),
+                (size_t)r->npx * sizeof(double)));
   CK(cudaStreamSynchronize(r->st));
   return LSE_OK;
 }
