@@ -1380,8 +1380,7 @@ struct StageBufs {
 };
 StageBufs g_stage;
 
-int h2d_rows_f32(lse_run* r, float* dst, size_t dpitch_b, const float* src, int H, int W) {
-  const size_t row_b = (size_t)W * sizeof(float);
+int h2d_rows(lse_run* r, void* dst, size_t dpitch_b, const void* src, int H, size_t row_b) {
   cudaPointerAttributes at{};
   const bool pageable = cudaPointerGetAttributes(&at, src) != cudaSuccess ||
                         at.type == cudaMemoryTypeUnregistered;
@@ -1468,7 +1467,7 @@ int upload_image(lse_run* r, const void* image, int is_f32) {
   TRY(run_flag(r, &d_flag));
   CK(cudaMemsetAsync(d_flag, 0, sizeof(int), r->st));
   if (is_f32 == LSE_IMAGE_F32) {
-    TRY(h2d_rows_f32(r, r->d_data32, pitch * sizeof(float), static_cast<const float*>(image), H, W));
+    TRY(h2d_rows(r, r->d_data32, pitch * sizeof(float), image, H, (size_t)W * sizeof(float)));
     r->fp32_exact = true;
   } else {
     TRY(dalloc(&tmp64, r->npx));
@@ -1476,13 +1475,13 @@ int upload_image(lse_run* r, const void* image, int is_f32) {
       // 8-bit RGB, decoded to the loader's float64 luma on the device
       unsigned char* d8 = nullptr;
       TRY(dalloc(&d8, 3 * r->npx));
-      CK(cudaMemcpyAsync(d8, image, 3 * r->npx, cudaMemcpyHostToDevice, r->st));
+      TRY(h2d_rows(r, d8, 3 * (size_t)W, image, H, 3 * (size_t)W));
       k_luma<<<(unsigned)((r->npx + 255) / 256), 256, 0, r->st>>>(d8, tmp64, r->npx);
       CKL();
       CK(cudaStreamSynchronize(r->st));
       cudaFree(d8);
     } else {
-      CK(cudaMemcpyAsync(tmp64, image, r->npx * sizeof(double), cudaMemcpyHostToDevice, r->st));
+      TRY(h2d_rows(r, tmp64, (size_t)W * sizeof(double), image, H, (size_t)W * sizeof(double)));
     }
     k_to_f32<<<grid2(W, H), 128, 0, r->st>>>(tmp64, r->d_data32, H, W, pitch, d_flag);
     CKL();
